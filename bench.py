@@ -1,0 +1,416 @@
+"""Benchmark: BASELINE.json metric on config 1 (100k agents, 180 days).
+
+One bench "step" = one complete 180-day simulation of config 1 (households +
+workplaces + Poisson(5) random contacts, 100 seeds, no interventions), i.e.
+one pass of the hot path over every day: per-day edge generation, message
+pass, fused infection/progression update and the per-day record.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--mode csr|fused] [--workload config1|config0]
+
+`value` = agent-interactions/s (directed edges x days, the reference's own
+definition, runner.py:269,287) over all ranks, device-timed with CUDA events
+(max over ranks).  `e2e` = the same through the public API from pinned host
+buffers: initial state H2D + 180 days + time-series D2H, every step.
+`--impl reference` times the CPU oracle port of the reference engine on the
+same workload (bounded sample of days, all host cores), see DESIGN.md §6.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+HORIZON = 180
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--mode", choices=["csr", "fused", "auto"], default="auto")
+    ap.add_argument("--workload", choices=["config1", "config0"], default="config1")
+    ap.add_argument("--cpu-seconds", type=float, default=20.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def workload_spec(name):
+    from paper_2110_04421_b200.confignet import ConfigNetworkSpec
+    return ConfigNetworkSpec.config(1 if name == "config1" else 0)
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
+            int(os.environ.get("WORLD_SIZE", 1)))
+
+
+# ---------------------------------------------------------------------------
+# CPU reference arm: oracle port of Engine.step + the config-network
+# restatement, one replica per process, bounded number of days.
+def _cpu_worker(args):
+    workload, seed, seconds = args
+    sys.path.insert(0, str(ROOT))
+    from oracle import confignet_np, engine_np
+    from paper_2110_04421_b200.confignet import synthesize
+    from paper_2110_04421_b200.defaults import default_disease, default_progression
+    from paper_2110_04421_b200.graph import StepGraph
+    from paper_2110_04421_b200.interventions import InterventionConfig
+    from paper_2110_04421_b200.sim import initial_columns
+    spec = workload_spec(workload)
+    pop = synthesize(spec, 0)
+    cols = initial_columns(pop)
+    disease, table, iv = default_disease(), default_progression(), InterventionConfig()
+    # seeding (population.py:151-177) with the oracle's keyed draws
+    from oracle import rng_np
+    ids = pop.seeds
+    entry = engine_np.pick(table.rules[0], cols.age_band[ids], rng_np.uniforms(seed, 0, 3, ids))
+    cols.stage[ids] = entry
+    cols.infected_at[ids] = 0
+    nxt, d = engine_np.schedule(table, entry, cols.age_band[ids], rng_np.uniforms(seed, 0, 4, ids),
+                                rng_np.uniforms(seed, 0, 5, ids))
+    cols.next_stage[ids] = nxt
+    cols.next_transition_at[ids] = d
+    eng = engine_np.OracleEngine(cols, disease, table, iv, seed)
+    t0 = time.perf_counter()
+    edges = days = 0
+    while days < HORIZON and (time.perf_counter() - t0) < seconds:
+        src, dst, kind = confignet_np.realize(pop, seed, days, cols.stage == 10, canonical=False)
+        ev = eng.step(StepGraph(days, src, dst, kind))
+        edges += ev.n_edges
+        days += 1
+    return edges, days, time.perf_counter() - t0
+
+
+def run_reference(a):
+    rank, _, world = dist_env()
+    if rank != 0:
+        return
+    from concurrent.futures import ProcessPoolExecutor
+    cores = os.cpu_count() or 1
+    total_e = total_t = 0.0
+    days_done = []
+    t_all = time.perf_counter()
+    steps = []
+    for i in range(a.warmup + a.steps):
+        t0 = time.perf_counter()
+        with ProcessPoolExecutor(max_workers=cores) as pool:
+            res = list(pool.map(_cpu_worker, [(a.workload, 1000 * i + w, a.cpu_seconds / 2)
+                                              for w in range(cores)]))
+        wall = time.perf_counter() - t0
+        if i >= a.warmup:
+            e = sum(r[0] for r in res)
+            steps.append((e, wall))
+            days_done.append(sum(r[1] for r in res))
+        if time.perf_counter() - t_all > 240:
+            break
+    e = sum(s[0] for s in steps)
+    w = sum(s[1] for s in steps)
+    v = e / w
+    line = {
+        "impl": "reference", "metric": "agent-interactions/sec", "value": v,
+        "unit": "agent-interactions/s", "n_gpus": a.gpus, "steps": len(steps), "warmup": a.warmup,
+        "ms_per_step": 1000 * w / max(1, len(steps)), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{a.workload}: BASELINE.json configs[1], 100k agents, "
+                   "household+workplace+Poisson(5) random network, 100 seeds, no interventions",
+                   "parallelism": f"{cores} host processes x 1 replica each"},
+        "cpu_baseline": {"value": v, "unit": "agent-interactions/s", "cores": cores, "kind": "port",
+                         "sample": f"each step: {cores} replicas x first days of the 180-day sim, "
+                                   f"~{a.cpu_seconds / 2:.0f}s each (days simulated: {days_done})"},
+        "e2e": {"value": v, "unit": "agent-interactions/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline_single(workload, seconds):
+    e, days, t = _cpu_worker((workload, 12345, seconds))
+    return {"value": e / t, "unit": "agent-interactions/s", "cores": 1, "kind": "port",
+            "sample": f"oracle engine_np + confignet_np, 1 replica, days 0-{days - 1} of 180 "
+                      f"({e} directed edges in {t:.1f}s), single process"}
+
+
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    """NVML polling thread (2 ms period) over the timed region: SM clock and
+    the throttle reasons nvidia-smi reports as clocks_event_reasons."""
+
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
+
+    def __init__(self, index):
+        import threading
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
+        except Exception as e:  # noqa: BLE001
+            self.nv, self.err = None, str(e)
+            return
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for name, bit in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:  # noqa: BLE001
+                pass
+            self._stop.wait(0.002)
+
+    def stop(self):
+        if self.nv is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [f"nvml unavailable: {self.err}"]}
+        self._stop.set()
+        self.t.join(timeout=2)
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def run_ours(a):
+    import torch
+    from paper_2110_04421_b200 import _native as N
+    from paper_2110_04421_b200.confignet import synthesize
+    from paper_2110_04421_b200.defaults import default_disease, default_progression
+    from paper_2110_04421_b200.interventions import InterventionConfig
+    from paper_2110_04421_b200.keyed import replication_seed
+    from paper_2110_04421_b200.sim import ConfigSimulation
+
+    rank, local_rank, world = dist_env()
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    spec = workload_spec(a.workload)
+    disease, table, iv = default_disease(), default_progression(), InterventionConfig()
+    pop = synthesize(spec, 0)
+    n_sims = a.warmup + a.steps
+    modes = ["csr", "fused"] if a.mode == "auto" else [a.mode]
+
+    def make(mode, i):
+        seed = replication_seed(0, rank * 100_000 + i)
+        return ConfigSimulation(pop, disease, table, iv, seed, mode=mode, precision="f32",
+                                horizon=HORIZON)
+
+    # L2 flush buffer (> 126 MB L2), written between timed simulations
+    flush = torch.empty(384 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+
+    def time_mode(mode):
+        sims = [make(mode, i) for i in range(n_sims)]
+        for s in sims:
+            s.capture()
+        torch.cuda.synchronize()
+        for s in sims[:a.warmup]:
+            s.replay()
+        torch.cuda.synchronize()
+        starts = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
+        ends = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps)]
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        clk = ClockSampler(local_rank)
+        t0 = time.perf_counter()
+        for k, s in enumerate(sims[a.warmup:]):
+            flush.fill_(float(k))
+            starts[k].record()
+            s.replay()
+            ends[k].record()
+        torch.cuda.synchronize()
+        wall = time.perf_counter() - t0
+        if dist:
+            dist.barrier()
+        clocks = clk.stop()
+        ms = [st.elapsed_time(en) for st, en in zip(starts, ends)]
+        edges = sum(int(s.records()[:, N.REC["edges"]].sum()) for s in sims[a.warmup:])
+        return dict(mode=mode, ms=ms, edges=edges, wall=wall, clocks=clocks, sims=sims)
+
+    results = [time_mode(m) for m in modes]
+    best = min(results, key=lambda r: sum(r["ms"]) / max(1, r["edges"]))
+    ms_total = sum(best["ms"])
+    if dist:
+        t = torch.tensor([ms_total], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+        e = torch.tensor([best["edges"]], device="cuda", dtype=torch.float64)
+        dist.all_reduce(e)
+        edges_all = float(e.item())
+    else:
+        edges_all = float(best["edges"])
+    value = edges_all / (ms_total / 1000.0)
+
+    # --- per-kernel device times (instrumented, same inputs) -> roofline
+    prof = kernel_profile(best["sims"][a.warmup], best["mode"])
+    # --- end to end through the public API from pinned host buffers
+    e2e = end_to_end(make(best["mode"], 0), a)
+
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) \
+        if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    roof = prof["roofline"]
+    roof["peak"] = peak
+    roof["frac"] = roof["achieved"] / peak
+    roof["peak_source"] = "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s"
+
+    if rank != 0:
+        return
+    line = {
+        "metric": "agent-interactions/sec", "value": value, "unit": "agent-interactions/s",
+        "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": ms_total / a.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {
+            "workload": f"{a.workload} (BASELINE.json configs[1]): 100k agents, 180 days, "
+                        "households U{1..6} + workplaces U{10..50} x 8 colleague draws + "
+                        "Poisson(5) random contacts, 100 seeds, no interventions",
+            "mode": best["mode"], "step": "one full 180-day simulation (CUDA graph replay)",
+            "replicas": f"{a.steps} timed replications per GPU, distinct seeds",
+            "l2": "flushed between timed simulations (384 MB write)",
+            "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+        },
+        "wall_s_per_sim": ms_total / a.steps / 1000.0,
+        "undirected_contacts_per_s": value / 2,
+        "modes": {r["mode"]: {"ms_per_sim": sum(r["ms"]) / len(r["ms"]),
+                              "interactions_per_s": r["edges"] / (sum(r["ms"]) / 1000)}
+                  for r in results},
+        "kernels": prof["kernels"],
+        "roofline": roof,
+        "e2e": e2e,
+        "gpu_launches": prof["launches_per_sim"] * a.steps,
+        "clocks": best["clocks"],
+    }
+    if not a.no_cpu_baseline and world == 1:
+        line["cpu_baseline"] = cpu_baseline_single(a.workload, a.cpu_seconds)
+    print(json.dumps(line), flush=True)
+
+
+def kernel_profile(sim, mode):
+    """Per-kernel CUDA-event times over one full simulation (non-graph run with
+    events between the launches of every day)."""
+    import ctypes
+    import torch
+    from paper_2110_04421_b200 import _native as N
+    from paper_2110_04421_b200.engine import _u64
+    sim.reset()
+    torch.cuda.synchronize()
+    lib = sim._lib
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(sim.horizon)]
+    for day in evs:
+        for e in day:
+            e.record()           # materialise the cudaEvent_t
+    torch.cuda.synchronize()
+    for t in range(sim.horizon):
+        handles = (ctypes.c_void_p * 4)(*[e.cuda_event for e in evs[t]])
+        st = sim.state.struct()
+        N.check(lib.epi_sim_step_timed(
+            sim._ctx, ctypes.byref(st), t, _u64(sim.seed), 0 if mode == "csr" else 1, N.F32,
+            N.ptr(sim.codes[t & 1]), N.ptr(sim.codes[(t + 1) & 1]), N.ptr(sim.rec[t]),
+            N.ptr(sim.vax), ctypes.addressof(handles), N.stream_handle()))
+    torch.cuda.synchronize()
+    sim.clock = sim.horizon
+    gen = [evs[t][0].elapsed_time(evs[t][1]) for t in range(sim.horizon)]
+    pas = [evs[t][1].elapsed_time(evs[t][2]) for t in range(sim.horizon)]
+    rec = sim.records()
+    E = rec[:, N.REC["edges"]].astype(np.float64)
+    n = sim.n
+    total_ms = sum(gen) + sum(pas)
+    kernels = {}
+    if mode == "csr":
+        # K3 generator writes 4 B per edge + 4 B row length + reads 2 B code/agent
+        # K12 message pass + update: SURVEY §8(d) B_K1 = 4E + 10N (+16N state r/w)
+        b_gen = 4 * E + 6 * n
+        b_pass = 4 * E + 10 * n + 16 * n
+        kernels["k_net_realize"] = {"ms_per_launch": sum(gen) / len(gen),
+                                    "share": sum(gen) / total_ms,
+                                    "alg_GBps": float(np.sum(b_gen) / (sum(gen) / 1e3) / 1e9)}
+        kernels["k_pass_update"] = {"ms_per_launch": sum(pas) / len(pas),
+                                    "share": sum(pas) / total_ms,
+                                    "alg_GBps": float(np.sum(b_pass) / (sum(pas) / 1e3) / 1e9)}
+        dom = "k_pass_update" if sum(pas) >= sum(gen) else "k_net_realize"
+        byt = b_pass if dom == "k_pass_update" else b_gen
+        ms = pas if dom == "k_pass_update" else gen
+        launches = 2
+    else:
+        b = 16 * n + 2 * n + 2 * E       # state r/w + own code + gathered codes (L2)
+        kernels["k_fused_step"] = {"ms_per_launch": sum(pas) / len(pas), "share": 1.0,
+                                   "alg_GBps": float(np.sum(b) / (sum(pas) / 1e3) / 1e9)}
+        dom, byt, ms, launches = "k_fused_step", b, pas, 1
+    achieved = float(np.sum(byt) / (sum(ms) / 1e3) / 1e9)
+    return {"kernels": kernels, "launches_per_sim": launches * sim.horizon,
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "unit": "GB/s",
+                         "traffic": None,
+                         "bytes_model": "see DESIGN.md §5 (algorithmic bytes per launch)"}}
+
+
+def end_to_end(sim, a):
+    """Public API from pinned host memory: upload initial state, simulate 180
+    days, read the time series back — every step."""
+    import torch
+    from paper_2110_04421_b200.state import COLUMN_SPECS
+    host = sim.initial_host_columns()
+    pinned = {}
+    for name, dt, _ in COLUMN_SPECS:
+        arr = np.ascontiguousarray(getattr(host, name))
+        if arr.dtype == np.bool_:
+            arr = arr.view(np.uint8)
+        pinned[name] = torch.from_numpy(arr).pin_memory()
+    out = torch.empty((sim.horizon, 19), dtype=torch.int64).pin_memory()
+    sim.capture()
+    h2d = sum(int(t.numel() * t.element_size()) for t in pinned.values())
+    d2h = int(out.numel() * out.element_size())
+
+    def once():
+        for name, t in pinned.items():
+            sim.initial.t[name].copy_(t, non_blocking=True)
+        sim.replay()
+        out.copy_(sim.rec[:, :19], non_blocking=True)
+
+    for _ in range(a.warmup):
+        once()
+    torch.cuda.synchronize()
+    st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    st.record()
+    for _ in range(a.steps):
+        once()
+    en.record()
+    torch.cuda.synchronize()
+    ms = st.elapsed_time(en) / a.steps
+    edges = float(sim.records()[:, 19].sum())
+    return {"value": edges / (ms / 1000.0), "unit": "agent-interactions/s",
+            "ms_per_step": ms, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,258 @@
+/*
+ * epi_b200.h — C ABI of the B200-native DeepABM-COVID step (libepib200.so).
+ *
+ * Plain pointers and sizes only (no torch / C++ types).  Every device pointer
+ * is caller-owned CUDA memory; a context owns parameter tables and scratch.
+ * Calls are asynchronous on the given stream (`void*` = cudaStream_t, NULL =
+ * legacy default stream) unless documented otherwise.
+ *
+ * The reference has no FFI: its interface for this path is the Python object
+ * API.  Each entry point below names the reference function it replaces
+ * (paths relative to /root/reference/pkg/src/epivec/):
+ *
+ *   epi_uniforms          rng.uniforms                     rng.py:92-100
+ *   epi_graph_load        Engine.step validation + the
+ *                         canonical lexsort of gather      engine.py:124-133, 98
+ *   epi_gather            Engine.gather_exposure           engine.py:77-117
+ *   epi_step              Engine.step (all phases)         engine.py:121-347
+ *   epi_net_realize       GraphRealizer.realize            graphs.py:200-240
+ *   epi_sim_step          runner loop body realize+step    runner.py:145-152
+ *   epi_read_flags        check_invariants / errors        state.py:90-102
+ *
+ * Return codes: 0 ok; -1 bad argument (ConfigError); -2 invariant
+ * (InvariantViolation); -3 CUDA/NCCL error.  epi_last_error() gives the text.
+ */
+#ifndef EPI_B200_H
+#define EPI_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EPI_OK 0
+#define EPI_EARG (-1)
+#define EPI_EINVARIANT (-2)
+#define EPI_ECUDA (-3)
+
+#define EPI_MAX_T 127          /* day-weight table length - 1 (7-bit code)   */
+#define EPI_MAX_SPECS 16       /* distinct duration distributions            */
+#define EPI_MAX_TAUS 512       /* delay thresholds per distribution          */
+#define EPI_MAX_SLOTS 32       /* random-network slots / colleague draws     */
+
+/* Per-step record written by the device (int64 each), see DESIGN.md §4. */
+#define EPI_REC_STEP 0
+#define EPI_REC_STAGE0 1        /* 11 stage counts: 1..11                     */
+#define EPI_REC_CUM_INF 12
+#define EPI_REC_CUM_DEATHS 13
+#define EPI_REC_IN_CARE 14
+#define EPI_REC_NEW_INF 15
+#define EPI_REC_TESTS 16
+#define EPI_REC_DOSES 17
+#define EPI_REC_NOTIFY 18
+#define EPI_REC_EDGES 19
+#define EPI_REC_DEATHS 20
+#define EPI_REC_HOSP 21
+#define EPI_REC_ACTIVE 22
+#define EPI_REC_FLAGS 23        /* invariant bits, see EPI_FLAG_*            */
+#define EPI_REC_LEN 24
+
+#define EPI_FLAG_INDEX 1        /* graph references agent >= n_agents        */
+#define EPI_FLAG_SELFLOOP 2
+#define EPI_FLAG_KIND 4
+#define EPI_FLAG_STAGE_RANGE 8
+#define EPI_FLAG_NO_TIMESTAMP 16
+#define EPI_FLAG_NEG_HAZARD 32
+
+/* Precision of the message pass. */
+#define EPI_F32 0               /* factored per-source message, fp32 sums    */
+#define EPI_F64_CANONICAL 1     /* bitwise reference order (dst, src, kind)  */
+
+/* Model parameters, flattened from DiseaseParams / ProgressionTable /
+ * InterventionConfig (transmission.py:71-104, progression.py:99-216,
+ * interventions.py:84-204). */
+typedef struct epi_params {
+    double rate_scale;
+    double asymptomatic_factor;
+    double mean_daily_interactions;
+    double age_susceptibility[9];
+    double network_scale[3];
+    int32_t t_max;
+    int32_t sterilizing;
+    double day_weights[EPI_MAX_T + 1];
+    /* progression: per stage, up to 3 branches */
+    int32_t n_targets[11];
+    int32_t targets[11][3];
+    int32_t spec_of[11][3];
+    double cum[11][9][3];
+    int32_t n_specs;
+    int32_t tau_len[EPI_MAX_SPECS];
+    double tau[EPI_MAX_SPECS][EPI_MAX_TAUS];
+    /* interventions */
+    int32_t quarantine_enabled;
+    int32_t quarantine_duration;
+    double quarantine_dropout;
+    int32_t testing_enabled;
+    int32_t turnaround_min;
+    int32_t turnaround_max;
+    int32_t den_enabled;
+    double detection_prob;
+    double false_positive_prob;
+    double den_compliance;
+    int32_t den_lookback;
+    int32_t vaccination_enabled;
+    int32_t strategy;
+    int32_t elderly_band;
+    double dose1_efficacy;
+    double dose2_efficacy;
+    double dose2_topup;
+    int32_t dose1_latency;
+    int32_t dose2_latency;
+    int32_t dose_gap;
+    int32_t _pad0;
+    int64_t dose_budget;          /* rint(daily_rate * N)                  */
+    double start_trigger_count;   /* start_trigger * N (float64, as ref)   */
+} epi_params;
+
+/* Device SoA columns, same dtypes as AgentColumns (state.py:21-75). */
+typedef struct epi_state {
+    int64_t n_agents;
+    int8_t *age_band;
+    int8_t *stage;
+    int32_t *infected_at;
+    int32_t *next_transition_at;
+    int8_t *next_stage;
+    int32_t *quarantine_until;
+    int32_t *quarantine_started_at;
+    uint8_t *has_den_app;
+    int8_t *vaccine_status;
+    int32_t *dose1_at;
+    int32_t *dose2_at;
+    uint8_t *immune;
+    int32_t *immunity_check_at;
+    double *immunity_check_prob;
+    int8_t *immunity_check_dose;
+    int32_t *test_sample_at;
+    int32_t *test_result_at;
+    uint8_t *test_positive;
+    int32_t *den_test_due_at;
+} epi_state;
+
+/* Static config-network layout (paper_2110_04421_b200/confignet.py). */
+typedef struct epi_net {
+    int64_t n_agents;
+    const uint8_t *hh_off;
+    const uint8_t *hh_size;
+    const int32_t *wp_id;
+    const uint8_t *wp_local;
+    const int32_t *wp_base;
+    const int32_t *wp_size;
+    const int32_t *wp_members;
+    int32_t n_workplaces;
+    int32_t colleague_draws;
+    int32_t random_slots;
+    int32_t row_cap;              /* padded CSR row capacity              */
+    double poisson_cdf[EPI_MAX_SLOTS];
+} epi_net;
+
+typedef struct epi_ctx epi_ctx;
+
+/* Context: parameters + scratch for `n_agents` agents. */
+int epi_create(const epi_params *params, int64_t n_agents, epi_ctx **out);
+int epi_destroy(epi_ctx *ctx);
+int epi_set_params(epi_ctx *ctx, const epi_params *params);
+const char *epi_last_error(void);
+int epi_version(void);
+/* sizeof of the ABI structs (0 params, 1 state, 2 net) for binding checks */
+int64_t epi_struct_size(int32_t which);
+
+/* Keyed uniforms u(seed, step, purpose, ids[i], k) -> out[i] (device).
+ * ids == NULL means ids[i] = i.  Replaces rng.uniforms (rng.py:92-100). */
+int epi_uniforms(uint64_t seed, int32_t step, int32_t purpose, const int64_t *ids,
+                 int64_t n, int32_t k, double *out, void *stream);
+
+/* Graph-in mode: COO (src, dst, kind) device arrays -> canonical CSR kept in
+ * the context.  Index range / self-loop / kind are checked on the device and
+ * reported through epi_read_flags (engine.py:124-133). */
+int epi_graph_load(epi_ctx *ctx, const int32_t *src, const int32_t *dst,
+                   const int8_t *kind, int64_t n_edges, void *stream);
+
+/* Hazard per agent over the loaded graph at `step` (engine.py:77-117).
+ * precision EPI_F64_CANONICAL writes double[N] bitwise equal to the
+ * reference; EPI_F32 writes float[N]. */
+int epi_gather(epi_ctx *ctx, const epi_state *st, int32_t step, int32_t precision,
+               void *lambda_out, void *stream);
+
+/* One full Engine.step over the loaded graph (engine.py:121-151): gather
+ * (fp64 canonical), transmission, progression, enabled intervention phases,
+ * contact-log push, invariant flags.  `record` = device int64[EPI_REC_LEN],
+ * zeroed and filled.  `vax_open` = device int32 latch (engine.vaccination_open).
+ * `injected` = NULL or 12 nullable device double[N] arrays indexed by
+ * Purpose (1..11) that replace the keyed draws. */
+int epi_step(epi_ctx *ctx, const epi_state *st, int32_t step, uint64_t seed,
+             int64_t *record, int32_t *vax_open, const double *const *injected,
+             int32_t check_invariants, void *stream);
+
+/* Apply update phases (transmission..vaccination) with an externally supplied
+ * hazard (double[N]) — for injected-draw parity tests. */
+int epi_step_with_hazard(epi_ctx *ctx, const epi_state *st, int32_t step, uint64_t seed,
+                         const double *hazard, int64_t *record, int32_t *vax_open,
+                         const double *const *injected, void *stream);
+
+/* Host read of the invariant bits accumulated by the last graph_load/step
+ * (synchronises the stream), then clears them. */
+int epi_read_flags(epi_ctx *ctx, int32_t *flags_out, void *stream);
+
+/* ---- config networks (BASELINE.json configs 0-4) ---------------------- */
+
+/* Per-agent 16-bit source code for `step` from the state: days since
+ * infection (7 bits) | asymptomatic-like << 7 | random-slot count << 8 |
+ * dead << 15 (count uses `net`, may be NULL).  Output uint16[N]. */
+int epi_codes(epi_ctx *ctx, const epi_state *st, const epi_net *net, uint64_t graph_seed,
+              int32_t step, uint16_t *codes_out, void *stream);
+
+/* Materialise step `step`'s in-edges as a padded dst-major CSR:
+ * entries[b*row_cap + i] = src << 2 | kind, i < row_len[b].  sort_rows = 1
+ * puts every row in canonical (src, kind) order.  Replaces
+ * GraphRealizer.realize (graphs.py:200-240) for the config networks. */
+int epi_net_realize(const epi_net *net, uint64_t graph_seed, int32_t step,
+                    const uint16_t *codes, uint32_t *entries, int32_t *row_len,
+                    int32_t sort_rows, void *stream);
+
+/* Bind a config network to the context and allocate its per-step padded CSR
+ * (a ring of den_lookback slots when exposure notification is enabled). */
+int epi_net_attach(epi_ctx *ctx, const epi_net *net);
+
+/* Fast path: one simulated day on the attached network, state resident on
+ * the device.  mode 0 = generate the CSR, then the fused message-pass+update
+ * kernel; mode 1 = fused generate+gather+update (no CSR in memory; no DEN).
+ * codes_cur holds this step's codes (see epi_codes), codes_next receives the
+ * next step's.  `record` as epi_step. */
+int epi_sim_step(epi_ctx *ctx, const epi_state *st, int32_t step, uint64_t seed,
+                 int32_t mode, int32_t precision, const uint16_t *codes_cur,
+                 uint16_t *codes_next, int64_t *record, int32_t *vax_open, void *stream);
+
+/* epi_sim_step that also records 4 caller-created cudaEvent_t: before the
+ * generator, before the message pass, after it, after the intervention
+ * phases — per-kernel device times for the roofline (bench.py). */
+int epi_sim_step_timed(epi_ctx *ctx, const epi_state *st, int32_t step, uint64_t seed,
+                       int32_t mode, int32_t precision, const uint16_t *codes_cur,
+                       uint16_t *codes_next, int64_t *record, int32_t *vax_open,
+                       void *const *events4, void *stream);
+
+/* Device pointers of the CSR slot written for `step` (mode 0), for export. */
+int epi_net_csr(epi_ctx *ctx, int32_t step, uint32_t **entries, int32_t **row_len);
+
+/* Seed infections at step 0: entry stage + first transition for ids[0..n)
+ * (population.py:151-177 after the choice of ids). */
+int epi_seed_infections(epi_ctx *ctx, const epi_state *st, uint64_t seed,
+                        const int64_t *ids, int64_t n, void *stream);
+
+/* DEN app adoption u(seed, 0, DEN_APP, a) < adoption (runner.py:86-89). */
+int epi_assign_app(const epi_state *st, uint64_t seed, double adoption, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EPI_B200_H */

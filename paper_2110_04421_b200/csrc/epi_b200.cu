@@ -1,0 +1,608 @@
+// libepib200 — host side of the C ABI declared in include/epi_b200.h.
+//
+// A context owns: the device copy of epi_params, per-agent scratch (codes,
+// flags, vaccination buckets), the graph-in CSR (CUB radix sort of
+// dst<<32|src<<2|kind keys), the contact ring for exposure notification, and
+// the per-step padded CSR ring of an attached config network.
+#include <cub/device/device_radix_sort.cuh>
+
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "epi_kernels.cuh"
+
+using namespace epi;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CK(call)                                                                         \
+  do {                                                                                   \
+    cudaError_t e_ = (call);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      return fail(EPI_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_));        \
+  } while (0)
+
+#define CKL()                                                                            \
+  do {                                                                                   \
+    cudaError_t e_ = cudaGetLastError();                                                 \
+    if (e_ != cudaSuccess)                                                               \
+      return fail(EPI_ECUDA, std::string("kernel launch: ") + cudaGetErrorString(e_));   \
+  } while (0)
+
+inline cudaStream_t S(void* s) { return (cudaStream_t)s; }
+
+int g_sms = 0;
+int sm_count() {
+  if (!g_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_sms <= 0) g_sms = 148;
+  }
+  return g_sms;
+}
+inline int grid_for(int64_t n, int threads, int per_sm = 8) {
+  int64_t g = (n + threads - 1) / threads;
+  int64_t cap = (int64_t)sm_count() * per_sm;
+  if (g > cap) g = cap;
+  return (int)(g < 1 ? 1 : g);
+}
+
+template <class T>
+int dalloc(T** p, size_t count) {
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  if (count == 0) count = 1;
+  CK(cudaMalloc((void**)p, count * sizeof(T)));
+  return 0;
+}
+
+}  // namespace
+
+struct epi_ctx {
+  epi_params host{};
+  epi_params* P = nullptr;           // device copy
+  int64_t n = 0;
+  uint8_t* flags = nullptr;          // n rounded up to 4
+  uint8_t* bucket = nullptr;
+  unsigned long long* hist = nullptr;
+  long long* plan = nullptr;
+  int* tile_off = nullptr;
+  long long* scratch_rec = nullptr;  // record when the caller passes none
+  long long* gflags = nullptr;       // graph validation bits (epi_graph_load)
+  uint16_t* codes = nullptr;         // graph-in codes
+  // graph-in CSR
+  int64_t edge_cap = 0, n_edges = 0;
+  uint64_t *keys_in = nullptr, *keys_out = nullptr;
+  uint32_t* entries = nullptr;
+  int64_t* row_begin = nullptr;
+  int32_t* row_len = nullptr;
+  void* cub_tmp = nullptr;
+  size_t cub_bytes = 0;
+  const int32_t *g_src = nullptr, *g_dst = nullptr;   // current graph (device, caller-owned)
+  // contact ring (graph-in)
+  struct Slot { int32_t *src = nullptr, *dst = nullptr; int64_t cap = 0, n = 0; };
+  std::vector<Slot> ring;
+  int ring_head = 0, ring_count = 0;
+  // attached config network
+  bool has_net = false;
+  epi_net net{};
+  epi_net* net_dev = nullptr;
+  int net_slots = 0;
+  std::vector<uint32_t*> net_entries;
+  std::vector<int32_t*> net_rowlen;
+  std::vector<int32_t> net_slot_step;
+  Injected* inj_dev = nullptr;
+};
+
+namespace {
+
+int upload_params(epi_ctx* c, const epi_params* p) {
+  if (p->t_max < 1 || p->t_max > EPI_MAX_T) return fail(EPI_EARG, "t_max outside [1, 127]");
+  if (p->n_specs < 0 || p->n_specs > EPI_MAX_SPECS) return fail(EPI_EARG, "too many duration specs");
+  for (int i = 0; i < p->n_specs; ++i)
+    if (p->tau_len[i] < 0 || p->tau_len[i] > EPI_MAX_TAUS) return fail(EPI_EARG, "tau table too long");
+  c->host = *p;
+  if (!c->P) CK(cudaMalloc((void**)&c->P, sizeof(epi_params)));
+  CK(cudaMemcpy(c->P, p, sizeof(epi_params), cudaMemcpyHostToDevice));
+  return 0;
+}
+
+StepArgs make_args(epi_ctx* c, const epi_state* st, int step, uint64_t seed, long long* rec,
+                   const Injected* inj, bool with_flags) {
+  StepArgs A;
+  A.P = c->P;
+  A.st = *st;
+  A.step = step;
+  A.K = make_step_keys(seed, step);
+  A.inj = inj;
+  A.rec = rec;
+  A.flags = with_flags ? c->flags : nullptr;
+  return A;
+}
+
+int upload_injected(epi_ctx* c, const double* const* injected, const Injected** out, cudaStream_t s) {
+  *out = nullptr;
+  if (!injected) return 0;
+  Injected h;
+  for (int i = 0; i < 12; ++i) h.u[i] = injected[i];
+  if (!c->inj_dev) CK(cudaMalloc((void**)&c->inj_dev, sizeof(Injected)));
+  CK(cudaMemcpyAsync(c->inj_dev, &h, sizeof(Injected), cudaMemcpyHostToDevice, s));
+  *out = c->inj_dev;
+  return 0;
+}
+
+bool interventions_on(const epi_params& p) {
+  return p.testing_enabled || p.quarantine_enabled || p.den_enabled || p.vaccination_enabled;
+}
+
+// Phases 3-6 + finish, shared by the graph-in step and the config sim step.
+// `den_scan` launches the contact scan for this step (may be empty).
+template <class DenScan>
+int run_interventions(epi_ctx* c, const StepArgs& A, uint16_t* codes_next, const epi_net* net_dev,
+                      uint64_t rcount_next, int32_t* vax_open, cudaStream_t s, DenScan&& den_scan) {
+  const epi_params& p = c->host;
+  const int64_t n = c->n;
+  const int threads = 256;
+  const int grid = grid_for(n, threads);
+  if (p.testing_enabled) {
+    k_iv_tests<<<grid, threads, 0, s>>>(A);
+    CKL();
+  }
+  if (p.den_enabled) {
+    int rc = den_scan();
+    if (rc) return rc;
+  }
+  if (p.vaccination_enabled) CK(cudaMemsetAsync(c->hist, 0, NUM_BUCKETS * sizeof(unsigned long long), s));
+  if (p.den_enabled || p.quarantine_enabled || p.vaccination_enabled) {
+    k_iv_post<<<grid, threads, 0, s>>>(A, c->bucket, c->hist);
+    CKL();
+  }
+  if (p.vaccination_enabled) {
+    if (!vax_open) return fail(EPI_EARG, "vaccination enabled but no vax_open latch given");
+    k_vax_plan<<<1, 32, 0, s>>>(c->P, c->hist, A.rec, vax_open, c->plan);
+    CKL();
+    const int64_t tiles = (n + VAX_TILE - 1) / VAX_TILE;
+    k_vax_tilecount<<<(unsigned)tiles, VAX_TILE, 0, s>>>(c->bucket, n, c->plan, c->tile_off);
+    CKL();
+    k_vax_tilescan<<<1, 1024, 0, s>>>(c->tile_off, tiles);
+    CKL();
+    k_vax_apply<<<(unsigned)tiles, VAX_TILE, 0, s>>>(A, c->bucket, c->plan, c->tile_off);
+    CKL();
+  }
+  k_finish<<<grid, threads, 0, s>>>(A, codes_next, net_dev, rcount_next);
+  CKL();
+  return 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* epi_last_error(void) { return g_err.c_str(); }
+int epi_version(void) { return 1; }
+
+int64_t epi_struct_size(int32_t which) {
+  switch (which) {
+    case 0: return (int64_t)sizeof(epi_params);
+    case 1: return (int64_t)sizeof(epi_state);
+    case 2: return (int64_t)sizeof(epi_net);
+    default: return -1;
+  }
+}
+
+int epi_create(const epi_params* params, int64_t n_agents, epi_ctx** out) {
+  if (!params || !out) return fail(EPI_EARG, "null argument");
+  if (n_agents < 1 || n_agents >= (1ll << 30)) return fail(EPI_EARG, "n_agents must be in [1, 2^30)");
+  epi_ctx* c = new epi_ctx();
+  c->n = n_agents;
+  int rc = upload_params(c, params);
+  const int64_t n4 = (n_agents + 3) / 4 * 4;
+  const int64_t tiles = (n_agents + VAX_TILE - 1) / VAX_TILE;
+  if (!rc) rc = dalloc(&c->flags, n4);
+  if (!rc) rc = dalloc(&c->bucket, n_agents);
+  if (!rc) rc = dalloc(&c->hist, NUM_BUCKETS);
+  if (!rc) rc = dalloc(&c->plan, 4);
+  if (!rc) rc = dalloc(&c->tile_off, tiles);
+  if (!rc) rc = dalloc(&c->scratch_rec, EPI_REC_LEN);
+  if (!rc) rc = dalloc(&c->gflags, 1);
+  if (!rc) rc = dalloc(&c->codes, n_agents);
+  if (!rc) rc = dalloc(&c->row_begin, n_agents);
+  if (!rc) rc = dalloc(&c->row_len, n_agents);
+  if (!rc) {
+    if (cudaMemset(c->flags, 0, n4) != cudaSuccess || cudaMemset(c->gflags, 0, 8) != cudaSuccess)
+      rc = fail(EPI_ECUDA, "memset scratch");
+  }
+  if (rc) {
+    epi_destroy(c);
+    return rc;
+  }
+  *out = c;
+  return 0;
+}
+
+int epi_destroy(epi_ctx* c) {
+  if (!c) return 0;
+  cudaFree(c->P);
+  cudaFree(c->flags);
+  cudaFree(c->bucket);
+  cudaFree(c->hist);
+  cudaFree(c->plan);
+  cudaFree(c->tile_off);
+  cudaFree(c->scratch_rec);
+  cudaFree(c->gflags);
+  cudaFree(c->codes);
+  cudaFree(c->keys_in);
+  cudaFree(c->keys_out);
+  cudaFree(c->entries);
+  cudaFree(c->row_begin);
+  cudaFree(c->row_len);
+  cudaFree(c->cub_tmp);
+  cudaFree(c->net_dev);
+  cudaFree(c->inj_dev);
+  for (auto& s : c->ring) { cudaFree(s.src); cudaFree(s.dst); }
+  for (auto* p : c->net_entries) cudaFree(p);
+  for (auto* p : c->net_rowlen) cudaFree(p);
+  delete c;
+  return 0;
+}
+
+int epi_set_params(epi_ctx* c, const epi_params* p) {
+  if (!c || !p) return fail(EPI_EARG, "null argument");
+  return upload_params(c, p);
+}
+
+int epi_uniforms(uint64_t seed, int32_t step, int32_t purpose, const int64_t* ids, int64_t n,
+                 int32_t k, double* out, void* stream) {
+  if (n < 0 || (!out && n)) return fail(EPI_EARG, "bad output");
+  if (!n) return 0;
+  k_uniforms<<<grid_for(n, 256), 256, 0, S(stream)>>>(key_prefix(seed, step, purpose), ids, n, k, out);
+  CKL();
+  return 0;
+}
+
+int epi_graph_load(epi_ctx* c, const int32_t* src, const int32_t* dst, const int8_t* kind,
+                   int64_t E, void* stream) {
+  if (!c || E < 0) return fail(EPI_EARG, "bad argument");
+  cudaStream_t s = S(stream);
+  c->n_edges = E;
+  c->g_src = src;
+  c->g_dst = dst;
+  CK(cudaMemsetAsync(c->row_len, 0, c->n * sizeof(int32_t), s));
+  CK(cudaMemsetAsync(c->row_begin, 0, c->n * sizeof(int64_t), s));
+  if (E == 0) return 0;
+  if (E > c->edge_cap) {
+    int64_t cap = E + E / 4;
+    int rc = dalloc(&c->keys_in, cap);
+    if (!rc) rc = dalloc(&c->keys_out, cap);
+    if (!rc) rc = dalloc(&c->entries, cap);
+    if (rc) return rc;
+    c->edge_cap = cap;
+  }
+  k_coo_keys<<<grid_for(E, 256), 256, 0, s>>>(src, dst, kind, E, c->n, c->keys_in, c->gflags);
+  CKL();
+  int end_bit = 32;
+  while ((1ll << (end_bit - 32)) < c->n) ++end_bit;
+  size_t need = 0;
+  CK(cub::DeviceRadixSort::SortKeys(nullptr, need, c->keys_in, c->keys_out, (int)E, 0, end_bit, s));
+  if (need > c->cub_bytes) {
+    cudaFree(c->cub_tmp);
+    c->cub_tmp = nullptr;
+    CK(cudaMalloc(&c->cub_tmp, need));
+    c->cub_bytes = need;
+  }
+  CK(cub::DeviceRadixSort::SortKeys(c->cub_tmp, need, c->keys_in, c->keys_out, (int)E, 0, end_bit, s));
+  k_rows_from_sorted<<<grid_for(E, 256), 256, 0, s>>>(c->keys_out, E, c->row_begin, c->row_len, c->entries);
+  CKL();
+  k_rows_finish<<<grid_for(c->n, 256), 256, 0, s>>>(c->n, c->row_begin, c->row_len);
+  CKL();
+  return 0;
+}
+
+int epi_read_flags(epi_ctx* c, int32_t* flags_out, void* stream) {
+  if (!c || !flags_out) return fail(EPI_EARG, "null argument");
+  long long f = 0;
+  CK(cudaMemcpyAsync(&f, c->gflags, sizeof(long long), cudaMemcpyDeviceToHost, S(stream)));
+  CK(cudaStreamSynchronize(S(stream)));
+  CK(cudaMemsetAsync(c->gflags, 0, sizeof(long long), S(stream)));
+  *flags_out = (int32_t)f;
+  return 0;
+}
+
+int epi_gather(epi_ctx* c, const epi_state* st, int32_t step, int32_t precision, void* lam_out,
+               void* stream) {
+  if (!c || !st || !lam_out) return fail(EPI_EARG, "null argument");
+  if (st->n_agents != c->n) return fail(EPI_EARG, "state size differs from context");
+  cudaStream_t s = S(stream);
+  k_codes<<<grid_for(c->n, 256), 256, 0, s>>>(c->P, *st, step, nullptr, 0, c->codes);
+  CKL();
+  StepArgs A = make_args(c, st, step, 0, c->scratch_rec, nullptr, false);
+  CsrView g{c->entries, c->row_len, c->row_begin, 0};
+  const int grid = grid_for(c->n, 256);
+  if (precision == EPI_F64_CANONICAL)
+    k_pass<true, 0><<<grid, 256, 0, s>>>(A, g, c->codes, lam_out, c->host.rate_scale, 0, nullptr, nullptr, 0);
+  else
+    k_pass<false, 0><<<grid, 256, 0, s>>>(A, g, c->codes, lam_out, c->host.rate_scale, 0, nullptr, nullptr, 0);
+  CKL();
+  return 0;
+}
+
+static int push_ring(epi_ctx* c, cudaStream_t s) {
+  const int L = c->host.den_lookback;
+  if ((int)c->ring.size() != L) {
+    for (auto& sl : c->ring) { cudaFree(sl.src); cudaFree(sl.dst); }
+    c->ring.assign(L, epi_ctx::Slot{});
+    c->ring_head = 0;
+    c->ring_count = 0;
+  }
+  epi_ctx::Slot& sl = c->ring[c->ring_head];
+  if (c->n_edges > sl.cap) {
+    int rc = dalloc(&sl.src, c->n_edges);
+    if (!rc) rc = dalloc(&sl.dst, c->n_edges);
+    if (rc) return rc;
+    sl.cap = c->n_edges;
+  }
+  sl.n = c->n_edges;
+  if (sl.n) {
+    CK(cudaMemcpyAsync(sl.src, c->g_src, sl.n * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpyAsync(sl.dst, c->g_dst, sl.n * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+  }
+  c->ring_head = (c->ring_head + 1) % L;
+  if (c->ring_count < L) ++c->ring_count;
+  return 0;
+}
+
+static int step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t seed,
+                     const double* hazard, int64_t* record, int32_t* vax_open,
+                     const double* const* injected, void* stream) {
+  if (!c || !st) return fail(EPI_EARG, "null argument");
+  if (st->n_agents != c->n) return fail(EPI_EARG, "state size differs from context");
+  cudaStream_t s = S(stream);
+  long long* rec = record ? (long long*)record : c->scratch_rec;
+  CK(cudaMemsetAsync(rec, 0, EPI_REC_LEN * sizeof(long long), s));
+  const Injected* inj = nullptr;
+  int rc = upload_injected(c, injected, &inj, s);
+  if (rc) return rc;
+  const bool iv = interventions_on(c->host);
+  StepArgs A = make_args(c, st, step, seed, rec, inj, iv);
+  const int grid = grid_for(c->n, 256);
+  if (hazard) {
+    k_update_from_hazard<<<grid, 256, 0, s>>>(A, hazard, iv ? 0 : 1);
+  } else {
+    k_codes<<<grid, 256, 0, s>>>(c->P, *st, step, nullptr, 0, c->codes);
+    CKL();
+    CsrView g{c->entries, c->row_len, c->row_begin, 0};
+    k_pass<true, 1><<<grid, 256, 0, s>>>(A, g, c->codes, nullptr, c->host.rate_scale, iv ? 0 : 1,
+                                         nullptr, nullptr, 0);
+  }
+  CKL();
+  if (iv) {
+    rc = run_interventions(c, A, nullptr, nullptr, 0, vax_open, s, [&]() -> int {
+      for (int i = 0; i < c->ring_count; ++i) {
+        const epi_ctx::Slot& sl = c->ring[i];
+        if (!sl.n) continue;
+        k_den_scan_coo<<<grid_for(sl.n, 256), 256, 0, s>>>(sl.src, sl.dst, sl.n, c->flags);
+        CKL();
+      }
+      return 0;
+    });
+    if (rc) return rc;
+  }
+  if (c->host.den_enabled && !hazard) {
+    rc = push_ring(c, s);
+    if (rc) return rc;
+  }
+  return 0;
+}
+
+int epi_step(epi_ctx* c, const epi_state* st, int32_t step, uint64_t seed, int64_t* record,
+             int32_t* vax_open, const double* const* injected, int32_t check_invariants,
+             void* stream) {
+  (void)check_invariants;   // flags are always accumulated; the caller decides to read them
+  return step_impl(c, st, step, seed, nullptr, record, vax_open, injected, stream);
+}
+
+int epi_step_with_hazard(epi_ctx* c, const epi_state* st, int32_t step, uint64_t seed,
+                         const double* hazard, int64_t* record, int32_t* vax_open,
+                         const double* const* injected, void* stream) {
+  if (!hazard) return fail(EPI_EARG, "hazard is null");
+  return step_impl(c, st, step, seed, hazard, record, vax_open, injected, stream);
+}
+
+int epi_codes(epi_ctx* c, const epi_state* st, const epi_net* net, uint64_t graph_seed, int32_t step,
+              uint16_t* codes_out, void* stream) {
+  if (!c || !st || !codes_out) return fail(EPI_EARG, "null argument");
+  const epi_net* nd = nullptr;
+  if (net) {
+    if (!c->has_net) return fail(EPI_EARG, "epi_codes with a network needs epi_net_attach first");
+    nd = c->net_dev;
+  }
+  k_codes<<<grid_for(c->n, 256), 256, 0, S(stream)>>>(c->P, *st, step, nd,
+                                                      key_prefix(graph_seed, step, P_NET_RCOUNT), codes_out);
+  CKL();
+  return 0;
+}
+
+static int check_net(const epi_net* net) {
+  if (!net) return fail(EPI_EARG, "null network");
+  if (net->random_slots < 0 || net->random_slots > EPI_MAX_SLOTS) return fail(EPI_EARG, "random_slots > 32");
+  if (net->colleague_draws < 0 || net->colleague_draws > EPI_MAX_SLOTS) return fail(EPI_EARG, "colleague_draws > 32");
+  if (net->row_cap < 1 || net->row_cap > 4096) return fail(EPI_EARG, "bad row_cap");
+  return 0;
+}
+
+static size_t realize_smem(const epi_net* net) {
+  return EPI_MAX_SLOTS * sizeof(PermKeys) + (size_t)128 * (net->row_cap | 1) * sizeof(uint32_t);
+}
+
+static size_t g_realize_smem_set = 0;
+static int prepare_realize(const epi_net* net) {
+  const size_t smem = realize_smem(net);
+  if (smem > g_realize_smem_set) {
+    CK(cudaFuncSetAttribute(k_net_realize<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(cudaFuncSetAttribute(k_net_realize<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    g_realize_smem_set = smem;
+  }
+  return 0;
+}
+
+static int launch_realize(const epi_net* net, uint64_t g, int32_t step, const uint16_t* codes,
+                          uint32_t* entries, int32_t* row_len, int sort_rows, long long* rec,
+                          cudaStream_t s) {
+  const size_t smem = realize_smem(net);
+  if (smem > g_realize_smem_set) return fail(EPI_EARG, "realize smem not prepared");
+  NetKeys nk = make_net_keys(g, step);
+  const int grid = grid_for(net->n_agents, 128, 16);
+  if (sort_rows) {
+    k_net_realize<true><<<grid, 128, smem, s>>>(*net, nk, codes, entries, row_len, rec);
+  } else {
+    k_net_realize<false><<<grid, 128, smem, s>>>(*net, nk, codes, entries, row_len, rec);
+  }
+  CKL();
+  return 0;
+}
+
+int epi_net_realize(const epi_net* net, uint64_t graph_seed, int32_t step, const uint16_t* codes,
+                    uint32_t* entries, int32_t* row_len, int32_t sort_rows, void* stream) {
+  int rc = check_net(net);
+  if (rc) return rc;
+  if (!codes || !entries || !row_len) return fail(EPI_EARG, "null buffer");
+  rc = prepare_realize(net);
+  if (rc) return rc;
+  return launch_realize(net, graph_seed, step, codes, entries, row_len, sort_rows, nullptr, S(stream));
+}
+
+int epi_net_attach(epi_ctx* c, const epi_net* net) {
+  if (!c) return fail(EPI_EARG, "null ctx");
+  int rc = check_net(net);
+  if (rc) return rc;
+  if (net->n_agents != c->n) return fail(EPI_EARG, "network size differs from context");
+  rc = prepare_realize(net);
+  if (rc) return rc;
+  c->net = *net;
+  c->has_net = true;
+  if (!c->net_dev) CK(cudaMalloc((void**)&c->net_dev, sizeof(epi_net)));
+  CK(cudaMemcpy(c->net_dev, net, sizeof(epi_net), cudaMemcpyHostToDevice));
+  const int slots = c->host.den_enabled ? c->host.den_lookback + 1 : 1;
+  for (auto* p : c->net_entries) cudaFree(p);
+  for (auto* p : c->net_rowlen) cudaFree(p);
+  c->net_entries.assign(slots, nullptr);
+  c->net_rowlen.assign(slots, nullptr);
+  c->net_slot_step.assign(slots, -1);
+  c->net_slots = slots;
+  for (int i = 0; i < slots; ++i) {
+    rc = dalloc(&c->net_entries[i], (size_t)c->n * net->row_cap);
+    if (!rc) rc = dalloc(&c->net_rowlen[i], (size_t)c->n);
+    if (rc) return rc;
+  }
+  return 0;
+}
+
+int epi_net_csr(epi_ctx* c, int32_t step, uint32_t** entries, int32_t** row_len) {
+  if (!c || !c->has_net || !entries || !row_len) return fail(EPI_EARG, "no attached network");
+  const int slot = step % c->net_slots;
+  if (c->net_slot_step[slot] != step) return fail(EPI_EARG, "CSR for that step is not resident");
+  *entries = c->net_entries[slot];
+  *row_len = c->net_rowlen[slot];
+  return 0;
+}
+
+static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t seed, int32_t mode,
+                         int32_t precision, const uint16_t* codes_cur, uint16_t* codes_next,
+                         int64_t* record, int32_t* vax_open, void* const* ev, void* stream) {
+  if (!c || !st || !codes_cur || !codes_next) return fail(EPI_EARG, "null argument");
+  if (!c->has_net) return fail(EPI_EARG, "epi_sim_step needs epi_net_attach first");
+  if (st->n_agents != c->n) return fail(EPI_EARG, "state size differs from context");
+  const bool iv = interventions_on(c->host);
+  if (mode == 1 && c->host.den_enabled) return fail(EPI_EARG, "fused mode keeps no contact log; use mode 0 with DEN");
+  if (mode == 1 && precision != EPI_F32) return fail(EPI_EARG, "fused mode is fp32 only");
+  cudaStream_t s = S(stream);
+  long long* rec = record ? (long long*)record : c->scratch_rec;
+  CK(cudaMemsetAsync(rec, 0, EPI_REC_LEN * sizeof(long long), s));
+  StepArgs A = make_args(c, st, step, seed, rec, nullptr, iv);
+  const uint64_t rcount_next = key_prefix(seed, step + 1, P_NET_RCOUNT);
+  const int grid = grid_for(c->n, 256);
+  const int slot = step % c->net_slots;
+  if (ev) CK(cudaEventRecord((cudaEvent_t)ev[0], s));
+  if (mode == 0) {
+    uint32_t* entries = c->net_entries[slot];
+    int32_t* row_len = c->net_rowlen[slot];
+    int rc = launch_realize(&c->net, seed, step, codes_cur, entries, row_len,
+                            precision == EPI_F64_CANONICAL, nullptr, s);
+    if (rc) return rc;
+    c->net_slot_step[slot] = step;
+    if (ev) CK(cudaEventRecord((cudaEvent_t)ev[1], s));
+    CsrView g{entries, row_len, nullptr, c->net.row_cap};
+    if (precision == EPI_F64_CANONICAL)
+      k_pass<true, 1><<<grid, 256, 0, s>>>(A, g, codes_cur, nullptr, c->host.rate_scale, iv ? 0 : 1,
+                                           codes_next, c->net_dev, rcount_next);
+    else
+      k_pass<false, 1><<<grid, 256, 0, s>>>(A, g, codes_cur, nullptr, c->host.rate_scale, iv ? 0 : 1,
+                                            codes_next, c->net_dev, rcount_next);
+    CKL();
+  } else {
+    if (ev) CK(cudaEventRecord((cudaEvent_t)ev[1], s));
+    k_fused_step<<<grid, 256, 0, s>>>(A, c->net, make_net_keys(seed, step), codes_cur, c->host.rate_scale,
+                                      codes_next, c->net_dev, rcount_next, iv ? 0 : 1);
+    CKL();
+  }
+  if (ev) CK(cudaEventRecord((cudaEvent_t)ev[2], s));
+  if (iv) {
+    int rc = run_interventions(c, A, codes_next, c->net_dev, rcount_next, vax_open, s, [&]() -> int {
+      const int L = c->host.den_lookback;
+      for (int i = 0; i < c->net_slots; ++i) {
+        const int st_i = c->net_slot_step[i];
+        if (st_i < 0 || st_i >= step || st_i < step - L) continue;
+        k_den_scan_csr<<<grid_for(c->n, 256), 256, 0, s>>>(c->net_entries[i], c->net_rowlen[i],
+                                                             c->net.row_cap, c->n, c->flags);
+        CKL();
+      }
+      return 0;
+    });
+    if (rc) return rc;
+  }
+  if (ev) CK(cudaEventRecord((cudaEvent_t)ev[3], s));
+  return 0;
+}
+
+int epi_sim_step(epi_ctx* c, const epi_state* st, int32_t step, uint64_t seed, int32_t mode,
+                 int32_t precision, const uint16_t* codes_cur, uint16_t* codes_next, int64_t* record,
+                 int32_t* vax_open, void* stream) {
+  return sim_step_impl(c, st, step, seed, mode, precision, codes_cur, codes_next, record, vax_open,
+                       nullptr, stream);
+}
+
+int epi_sim_step_timed(epi_ctx* c, const epi_state* st, int32_t step, uint64_t seed, int32_t mode,
+                       int32_t precision, const uint16_t* codes_cur, uint16_t* codes_next,
+                       int64_t* record, int32_t* vax_open, void* const* events4, void* stream) {
+  if (!events4) return fail(EPI_EARG, "events4 is null");
+  return sim_step_impl(c, st, step, seed, mode, precision, codes_cur, codes_next, record, vax_open,
+                       events4, stream);
+}
+
+int epi_seed_infections(epi_ctx* c, const epi_state* st, uint64_t seed, const int64_t* ids, int64_t n,
+                        void* stream) {
+  if (!c || !st) return fail(EPI_EARG, "null argument");
+  if (n <= 0) return 0;
+  k_seed<<<grid_for(n, 256), 256, 0, S(stream)>>>(c->P, *st, make_step_keys(seed, 0), ids, n);
+  CKL();
+  return 0;
+}
+
+int epi_assign_app(const epi_state* st, uint64_t seed, double adoption, void* stream) {
+  if (!st) return fail(EPI_EARG, "null argument");
+  k_assign_app<<<grid_for(st->n_agents, 256), 256, 0, S(stream)>>>(*st, key_prefix(seed, 0, P_APP), adoption);
+  CKL();
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,779 @@
+// Step kernels: message pass (gather), fused transmission/progression update,
+// intervention phases, per-step record.  Host wrappers live in epi_b200.cu.
+#pragma once
+
+#include <cub/block/block_scan.cuh>
+
+#include "epi_common.cuh"
+#include "epi_confignet.cuh"
+
+namespace epi {
+
+constexpr int NUM_BUCKETS = 54;      // 3 groups x 9 age bands x 2 dose ranks
+constexpr uint8_t FL_SYMPTOMATIC = 1, FL_NOTIFIER = 2, FL_NOTIFIED = 4;
+constexpr uint8_t NO_BUCKET = 0xFF;
+
+// ---------------------------------------------------------------------------
+// Per-block accumulation of the EPI_REC_* record (integer atomics only, so
+// the totals are deterministic).
+struct RecAcc {
+  unsigned long long v[EPI_REC_LEN];
+};
+
+__device__ __forceinline__ void rec_init(RecAcc& s) {
+  for (int i = threadIdx.x; i < EPI_REC_LEN; i += blockDim.x) s.v[i] = 0;
+}
+// warp-aggregated add of `x` (all 32 lanes must call)
+__device__ __forceinline__ void rec_add(RecAcc& s, int slot, unsigned x) {
+  const unsigned t = __reduce_add_sync(0xFFFFFFFFu, x);
+  if (lane_id() == 0 && t) atomicAdd(&s.v[slot], (unsigned long long)t);
+}
+__device__ __forceinline__ void rec_or(RecAcc& s, int slot, unsigned x) {
+  const unsigned t = __reduce_or_sync(0xFFFFFFFFu, x);
+  if (lane_id() == 0 && t) atomicOr(&s.v[slot], (unsigned long long)t);
+}
+__device__ __forceinline__ void rec_flush(const RecAcc& s, long long* rec, int step = -1) {
+  if (step >= 0 && blockIdx.x == 0 && threadIdx.x == 0) rec[EPI_REC_STEP] = step;
+  for (int i = threadIdx.x; i < EPI_REC_LEN; i += blockDim.x) {
+    if (i == EPI_REC_FLAGS) {
+      if (s.v[i]) atomicOr((unsigned long long*)&rec[i], s.v[i]);
+    } else if (s.v[i]) {
+      atomicAdd((unsigned long long*)&rec[i], s.v[i]);
+    }
+  }
+}
+
+// Stage histogram + derived time-series columns (runner.py:101-116) and the
+// structural invariants of state.py:90-102, for one agent per lane.
+__device__ __forceinline__ void rec_agent(RecAcc& s, bool valid, int stage, int32_t infected_at) {
+#pragma unroll
+  for (int k = 0; k < 11; ++k) {
+    const unsigned b = __ballot_sync(0xFFFFFFFFu, valid && stage == k);
+    if (lane_id() == 0 && b) atomicAdd(&s.v[EPI_REC_STAGE0 + k], (unsigned long long)__popc(b));
+  }
+  rec_add(s, EPI_REC_CUM_INF, valid && infected_at != NEVER);
+  rec_add(s, EPI_REC_CUM_DEATHS, valid && stage == S_DEAD);
+  rec_add(s, EPI_REC_IN_CARE, valid && (stage == S_HOSP || stage == S_ICU));
+  unsigned fl = 0;
+  if (valid && (stage < 0 || stage > 10)) fl |= EPI_FLAG_STAGE_RANGE;
+  if (valid && stage != S_SUS && stage != S_VAC && infected_at == NEVER) fl |= EPI_FLAG_NO_TIMESTAMP;
+  rec_or(s, EPI_REC_FLAGS, fl);
+}
+
+// ---------------------------------------------------------------------------
+// Kernel arguments shared by the step kernels.
+struct StepArgs {
+  const epi_params* __restrict__ P;
+  epi_state st;
+  int step;
+  StepKeys K;
+  const Injected* inj;        // device pointer or null
+  long long* rec;             // EPI_REC_LEN
+  uint8_t* flags;             // per agent scratch
+};
+
+// Shared tables for the fp32 message: factor[t | asym<<7] = rate*A*w[t],
+// sfac[age] = S[age] / Ibar, bfac[kind] = B[kind].
+struct MsgTables {
+  float factor[256];
+  float sfac[16];
+  float bfac[4];
+};
+__device__ __forceinline__ void build_msg_tables(MsgTables& T, const epi_params* __restrict__ P,
+                                                 double rate) {
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) {
+    const int t = i & 0x7F;
+    float f = 0.f;
+    if (t >= 1 && t <= P->t_max)
+      f = (float)(rate * ((i & 0x80) ? P->asymptomatic_factor : 1.0) * P->day_weights[t]);
+    T.factor[i] = f;
+  }
+  for (int i = threadIdx.x; i < 9; i += blockDim.x)
+    T.sfac[i] = (float)(P->age_susceptibility[i] / P->mean_daily_interactions);
+  for (int i = threadIdx.x; i < 3; i += blockDim.x) T.bfac[i] = (float)P->network_scale[i];
+}
+
+// fp64 term with the reference's pinned factor order (engine.py:100-107,
+// transmission.py:131-134): ((((rate*S[age_d])*A)*B[k])/Ibar)*w[t].
+__device__ __forceinline__ double term_f64(const epi_params* __restrict__ P, double rate_s,
+                                           uint16_t code, int kind) {
+  double x = __dmul_rn(rate_s, (code & CODE_ASYM) ? P->asymptomatic_factor : 1.0);
+  x = __dmul_rn(x, P->network_scale[kind]);
+  x = __ddiv_rn(x, P->mean_daily_interactions);
+  return __dmul_rn(x, P->day_weights[code & CODE_T_MASK]);
+}
+
+__device__ __forceinline__ bool is_target(const epi_params* __restrict__ P, const epi_state& st,
+                                          int64_t a) {
+  return st.stage[a] == S_SUS && !(P->sterilizing && st.immune[a]);
+}
+
+// ---------------------------------------------------------------------------
+// Phases 1-2 for one agent (engine.py:153-200).  Returns event bits:
+// 1 new infection, 2 death, 4 hospitalisation, 8 newly symptomatic.
+__device__ __forceinline__ unsigned transmit_progress(const StepArgs& A, int64_t a, double lam) {
+  const epi_params* __restrict__ P = A.P;
+  const epi_state& st = A.st;
+  const int step = A.step;
+  unsigned ev = 0;
+  int stage = st.stage[a];
+  int32_t nta = st.next_transition_at[a];
+  int age = -1;
+  if (stage == S_SUS && !(P->sterilizing && st.immune[a])) {
+    const double p = 1.0 - exp(-lam);
+    if (draw(A.K, A.inj, P_INFECTION, a) < p) {
+      age = st.age_band[a];
+      int entry = P->targets[S_SUS][pick_branch(P, S_SUS, age, draw(A.K, A.inj, P_ENTRY, a))];
+      if (!P->sterilizing && st.immune[a]) entry = S_ASYM;
+      int nxt, delay;
+      schedule(P, entry, age, draw(A.K, A.inj, P_BRANCH, a), draw(A.K, A.inj, P_DELAY, a), nxt, delay);
+      st.stage[a] = (int8_t)entry;
+      st.infected_at[a] = step;
+      st.next_stage[a] = (int8_t)nxt;
+      nta = step + delay;
+      st.next_transition_at[a] = nta;
+      ev |= 1u;
+    }
+  }
+  if (nta == step) {
+    if (age < 0) age = st.age_band[a];
+    const int dest = st.next_stage[a];
+    st.stage[a] = (int8_t)dest;
+    if (dest == S_DEAD) ev |= 2u;
+    if (dest == S_HOSP) ev |= 4u;
+    if (dest == S_MILD || dest == S_SEV) ev |= 8u;
+    if (dest == S_REC || dest == S_DEAD) {
+      st.next_stage[a] = NEVER8;
+      st.next_transition_at[a] = NEVER;
+    } else {
+      int nxt, delay;
+      schedule(P, dest, age, draw(A.K, A.inj, P_BRANCH, a), draw(A.K, A.inj, P_DELAY, a), nxt, delay);
+      st.next_stage[a] = (int8_t)nxt;
+      st.next_transition_at[a] = step + delay;
+    }
+  }
+  return ev;
+}
+
+__device__ __forceinline__ void rec_events(RecAcc& s, unsigned ev) {
+  rec_add(s, EPI_REC_NEW_INF, ev & 1u);
+  rec_add(s, EPI_REC_DEATHS, (ev >> 1) & 1u);
+  rec_add(s, EPI_REC_HOSP, (ev >> 2) & 1u);
+}
+
+// Next-step source code of agent a (after every phase of `step`).
+__device__ __forceinline__ uint16_t next_code(const epi_params* __restrict__ P, const epi_state& st,
+                                              int64_t a, int next_step, const epi_net* net,
+                                              uint64_t rcount_prefix) {
+  const int stage = st.stage[a];
+  uint16_t c = source_code(P, stage, st.infected_at[a], st.quarantine_until[a], next_step);
+  if (stage == S_DEAD) {
+    c |= CODE_DEAD;
+  } else if (net != nullptr) {
+    c |= (uint16_t)(random_count(*net, rcount_prefix, a) << 8);
+  }
+  return c;
+}
+
+// ---------------------------------------------------------------------------
+// Codes from state (graph-in gather, and step 0 of a config simulation).
+__global__ void k_codes(const epi_params* __restrict__ P, epi_state st, int step, const epi_net* net,
+                        uint64_t rcount_prefix, uint16_t* __restrict__ codes) {
+  const int64_t n = st.n_agents;
+  for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < n;
+       a += (int64_t)gridDim.x * blockDim.x)
+    codes[a] = next_code(P, st, a, step, net, rcount_prefix);
+}
+
+// ---------------------------------------------------------------------------
+// Graph-in: COO -> sort keys (dst << 32 | src << 2 | kind) + validation.
+__global__ void k_coo_keys(const int32_t* __restrict__ src, const int32_t* __restrict__ dst,
+                           const int8_t* __restrict__ kind, int64_t E, int64_t n,
+                           uint64_t* __restrict__ keys, long long* flag_word) {
+  unsigned fl = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < E;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t s = src[i], d = dst[i];
+    const int k = kind[i];
+    if (s < 0 || d < 0 || s >= n || d >= n) fl |= EPI_FLAG_INDEX;
+    if (s == d) fl |= EPI_FLAG_SELFLOOP;
+    if (k < 0 || k > 2) fl |= EPI_FLAG_KIND;
+    const uint64_t ss = (uint64_t)(uint32_t)s & 0x3FFFFFFFull, dd = (uint64_t)(uint32_t)d & 0x7FFFFFFFull;
+    keys[i] = (dd << 32) | (ss << 2) | (uint64_t)(k & 3);
+  }
+  if (fl) atomicOr((unsigned long long*)flag_word, (unsigned long long)fl);
+}
+
+// Row bounds of the sorted keys; entries = low 32 bits (src << 2 | kind).
+__global__ void k_rows_from_sorted(const uint64_t* __restrict__ keys, int64_t E,
+                                   int64_t* __restrict__ row_begin, int32_t* __restrict__ row_len,
+                                   uint32_t* __restrict__ entries) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < E;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t k = keys[i];
+    const int64_t d = (int64_t)(k >> 32);
+    entries[i] = (uint32_t)k;
+    if (i == 0 || (int64_t)(keys[i - 1] >> 32) != d) row_begin[d] = i;
+    if (i == E - 1 || (int64_t)(keys[i + 1] >> 32) != d) {
+      // length = i + 1 - begin; begin may be written by another thread, so
+      // compute it by scanning back is avoided: store end, fix up later
+      row_len[d] = (int32_t)(i + 1);   // temporarily the row end
+    }
+  }
+}
+__global__ void k_rows_finish(int64_t n, const int64_t* __restrict__ row_begin,
+                              int32_t* __restrict__ row_len) {
+  for (int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; d < n;
+       d += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t end = row_len[d];
+    row_len[d] = end ? (int32_t)(end - row_begin[d]) : 0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Gather / fused gather + update over a CSR given either by explicit
+// row_begin (graph-in) or implicitly by row * cap (padded config CSR).
+struct CsrView {
+  const uint32_t* __restrict__ entries;
+  const int32_t* __restrict__ row_len;
+  const int64_t* __restrict__ row_begin;   // null: padded rows of `cap`
+  int cap;
+  __device__ __forceinline__ int64_t begin(int64_t r) const {
+    return row_begin ? row_begin[r] : r * (int64_t)cap;
+  }
+};
+
+// MODE 0: write hazard (gather_exposure); MODE 1: fused update (+ record if
+// `final_pass`, + next codes).
+template <bool F64, int MODE>
+__global__ void __launch_bounds__(256) k_pass(StepArgs A, CsrView g, const uint16_t* __restrict__ codes,
+                                              void* __restrict__ lam_out, double rate,
+                                              int final_pass, uint16_t* __restrict__ codes_next,
+                                              const epi_net* net, uint64_t rcount_next) {
+  __shared__ MsgTables T;
+  __shared__ float lam_tile[8][32];
+  __shared__ RecAcc racc;
+  if (!F64) build_msg_tables(T, A.P, rate);
+  rec_init(racc);
+  __syncthreads();
+  const epi_params* __restrict__ P = A.P;
+  const int64_t n = A.st.n_agents;
+  const int warp = threadIdx.x >> 5, lane = lane_id();
+  const int64_t n_tiles = (n + 31) / 32;
+  const int64_t warps_total = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t tile = blockIdx.x * (int64_t)(blockDim.x >> 5) + warp; tile < n_tiles;
+       tile += warps_total) {
+    const int64_t base = tile * 32;
+    const int64_t a = base + lane;
+    const bool valid = a < n;
+    double lam = 0.0;
+    unsigned edges = 0;
+    if (F64) {
+      // one lane per row, sequential in canonical order
+      if (valid) {
+        const int len = g.row_len[a];
+        edges = (unsigned)len;
+        if (is_target(P, A.st, a)) {
+          const double rate_s = __dmul_rn(rate, P->age_susceptibility[A.st.age_band[a]]);
+          const uint32_t* e = g.entries + g.begin(a);
+          double h = 0.0;
+          for (int i = 0; i < len; ++i) {
+            const uint32_t x = e[i];
+            const uint16_t c = codes[x >> 2];
+            if (c & CODE_T_MASK) h = __dadd_rn(h, term_f64(P, rate_s, c, (int)(x & 3)));
+          }
+          lam = h;
+        }
+      }
+    } else {
+      // 8 lanes per row, 4 rows per pass, tree sum in fp32
+      const int grp = lane >> 3, gl = lane & 7;
+#pragma unroll 1
+      for (int r4 = 0; r4 < 8; ++r4) {
+        const int64_t row = base + r4 * 4 + grp;
+        float acc = 0.f;
+        if (row < n) {
+          const int len = g.row_len[row];
+          const uint32_t* e = g.entries + g.begin(row);
+          for (int i = gl; i < len; i += 8) {
+            const uint32_t x = __ldg(e + i);
+            acc += T.factor[codes[x >> 2] & 0xFF] * T.bfac[x & 3];
+          }
+        }
+        acc += __shfl_xor_sync(0xFFFFFFFFu, acc, 4);
+        acc += __shfl_xor_sync(0xFFFFFFFFu, acc, 2);
+        acc += __shfl_xor_sync(0xFFFFFFFFu, acc, 1);
+        if (gl == 0) lam_tile[warp][r4 * 4 + grp] = acc;
+      }
+      __syncwarp();
+      if (valid) {
+        edges = (unsigned)g.row_len[a];
+        lam = is_target(P, A.st, a)
+                  ? (double)(lam_tile[warp][lane] * T.sfac[A.st.age_band[a]])
+                  : 0.0;
+      }
+      __syncwarp();
+    }
+    if (MODE == 0) {
+      if (valid) {
+        if (F64) ((double*)lam_out)[a] = lam;
+        else ((float*)lam_out)[a] = (float)lam;
+      }
+      rec_add(racc, EPI_REC_EDGES, edges);
+      continue;
+    }
+    // MODE 1: fused update for this lane's agent
+    unsigned ev = 0;
+    if (valid) ev = transmit_progress(A, a, lam);
+    if (valid && (ev & 8u) && A.flags) A.flags[a] = FL_SYMPTOMATIC;
+    rec_events(racc, ev);
+    rec_add(racc, EPI_REC_EDGES, edges);
+    if (final_pass) {
+      int stage = valid ? A.st.stage[a] : 0;
+      rec_agent(racc, valid, stage, valid ? A.st.infected_at[a] : 0);
+      if (valid && codes_next) codes_next[a] = next_code(P, A.st, a, A.step + 1, net, rcount_next);
+    }
+  }
+  __syncthreads();
+  rec_flush(racc, A.rec, A.step);
+}
+
+// Update from an externally supplied fp64 hazard (injected-draw parity).
+__global__ void k_update_from_hazard(StepArgs A, const double* __restrict__ hazard, int final_pass) {
+  __shared__ RecAcc racc;
+  rec_init(racc);
+  __syncthreads();
+  const int64_t n = A.st.n_agents;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n; base += stride) {
+    const int64_t a = base + threadIdx.x;
+    const bool valid = a < n;
+    unsigned ev = 0;
+    if (valid) {
+      const double lam = is_target(A.P, A.st, a) ? hazard[a] : 0.0;
+      if (lam < 0) atomicOr((unsigned long long*)&A.rec[EPI_REC_FLAGS], EPI_FLAG_NEG_HAZARD);
+      ev = transmit_progress(A, a, lam);
+      if ((ev & 8u) && A.flags) A.flags[a] = FL_SYMPTOMATIC;
+    }
+    rec_events(racc, ev);
+    if (final_pass) rec_agent(racc, valid, valid ? A.st.stage[a] : 0, valid ? A.st.infected_at[a] : 0);
+  }
+  __syncthreads();
+  rec_flush(racc, A.rec, A.step);
+}
+
+// ---------------------------------------------------------------------------
+// Config CSR generation: one lane per destination row, rows staged in shared
+// memory (odd stride: conflict-free) then written out coalesced, one row per
+// warp-wide store.  SORT puts each row in canonical (src, kind) order.
+template <bool SORT>
+__global__ void __launch_bounds__(128) k_net_realize(epi_net net, NetKeys nk, const uint16_t* __restrict__ codes,
+                                                     uint32_t* __restrict__ entries,
+                                                     int32_t* __restrict__ row_len, long long* rec) {
+  extern __shared__ uint32_t smem[];
+  PermKeys* rk = (PermKeys*)smem;
+  uint32_t* stage_buf = (uint32_t*)(rk + EPI_MAX_SLOTS);
+  __shared__ RecAcc racc;
+  for (int j = threadIdx.x; j < net.random_slots; j += blockDim.x) rk[j] = random_slot_keys(nk.rperm, j);
+  rec_init(racc);
+  __syncthreads();
+  const int cap = net.row_cap;
+  const int stride_w = cap | 1;
+  const int warp = threadIdx.x >> 5, lane = lane_id();
+  uint32_t* mine = stage_buf + (size_t)(warp * 32 + lane) * stride_w;
+  uint32_t* wbuf = stage_buf + (size_t)warp * 32 * stride_w;
+  const int64_t n = net.n_agents;
+  const int64_t n_tiles = (n + 31) / 32;
+  const int64_t warps_total = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t tile = blockIdx.x * (int64_t)(blockDim.x >> 5) + warp; tile < n_tiles;
+       tile += warps_total) {
+    const int64_t base = tile * 32;
+    const int64_t b = base + lane;
+    int cnt = 0;
+    if (b < n) {
+      const uint16_t cb = codes[b];
+      if (!code_dead(cb)) {
+        for_each_in_edge(net, nk, rk, codes, b, cb, [&](int64_t c, int kind, uint16_t) {
+          mine[cnt++] = ((uint32_t)c << 2) | (uint32_t)kind;
+        });
+      }
+      if (SORT) {
+        for (int i = 1; i < cnt; ++i) {
+          const uint32_t x = mine[i];
+          int j = i - 1;
+          while (j >= 0 && mine[j] > x) { mine[j + 1] = mine[j]; --j; }
+          mine[j + 1] = x;
+        }
+      }
+      row_len[b] = cnt;
+    }
+    rec_add(racc, EPI_REC_EDGES, (unsigned)cnt);
+    __syncwarp();
+    const int rows = (n - base) < 32 ? (int)(n - base) : 32;
+    for (int r = 0; r < rows; ++r) {
+      const int len = __shfl_sync(0xFFFFFFFFu, cnt, r);
+      uint32_t* dst = entries + (base + r) * (int64_t)cap;
+      const uint32_t* srcrow = wbuf + r * stride_w;
+      for (int i = lane; i < len; i += 32) dst[i] = srcrow[i];
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  if (rec) rec_flush(racc, rec);
+}
+
+// Fused generate + gather + update: the in-edges are enumerated and their
+// source codes consumed on the fly, so no CSR ever reaches memory (mode 1).
+__global__ void __launch_bounds__(256) k_fused_step(StepArgs A, epi_net net, NetKeys nk,
+                                                    const uint16_t* __restrict__ codes, double rate,
+                                                    uint16_t* __restrict__ codes_next,
+                                                    const epi_net* net_dev, uint64_t rcount_next,
+                                                    int final_pass) {
+  __shared__ MsgTables T;
+  __shared__ PermKeys rk[EPI_MAX_SLOTS];
+  __shared__ RecAcc racc;
+  build_msg_tables(T, A.P, rate);
+  for (int j = threadIdx.x; j < net.random_slots; j += blockDim.x) rk[j] = random_slot_keys(nk.rperm, j);
+  rec_init(racc);
+  __syncthreads();
+  const int64_t n = A.st.n_agents;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n; base += stride) {
+    const int64_t b = base + threadIdx.x;
+    const bool valid = b < n;
+    unsigned edges = 0;
+    double lam = 0.0;
+    if (valid) {
+      const uint16_t cb = codes[b];
+      if (!code_dead(cb)) {
+        float acc = 0.f;
+        for_each_in_edge(net, nk, rk, codes, b, cb, [&](int64_t, int kind, uint16_t cc) {
+          ++edges;
+          acc += T.factor[cc & 0xFF] * T.bfac[kind];
+        });
+        if (is_target(A.P, A.st, b)) lam = (double)(acc * T.sfac[A.st.age_band[b]]);
+      }
+    }
+    unsigned ev = 0;
+    if (valid) ev = transmit_progress(A, b, lam);
+    if (valid && (ev & 8u) && A.flags) A.flags[b] = FL_SYMPTOMATIC;
+    rec_events(racc, ev);
+    rec_add(racc, EPI_REC_EDGES, edges);
+    if (final_pass) {
+      rec_agent(racc, valid, valid ? A.st.stage[b] : 0, valid ? A.st.infected_at[b] : 0);
+      if (valid) codes_next[b] = next_code(A.P, A.st, b, A.step + 1, net_dev, rcount_next);
+    }
+  }
+  __syncthreads();
+  rec_flush(racc, A.rec, A.step);
+}
+
+// ---------------------------------------------------------------------------
+// Intervention phases (engine.py:202-347).
+
+// Phase 3 + 4a: test sampling, then delivery (engine.py:202-242).
+__global__ void k_iv_tests(StepArgs A) {
+  __shared__ RecAcc racc;
+  rec_init(racc);
+  __syncthreads();
+  const epi_params* __restrict__ P = A.P;
+  const epi_state& st = A.st;
+  const int step = A.step;
+  const int64_t n = st.n_agents;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n; base += stride) {
+    const int64_t a = base + threadIdx.x;
+    unsigned tested = 0;
+    if (a < n) {
+      uint8_t fl = A.flags[a];
+      bool cand = (fl & FL_SYMPTOMATIC) != 0;
+      if (st.den_test_due_at[a] == step) {
+        st.den_test_due_at[a] = NEVER;
+        cand = true;
+      }
+      const int stage = st.stage[a];
+      if (cand && st.test_result_at[a] == NEVER && stage != S_DEAD) {
+        const double up = draw(A.K, A.inj, P_TEST_POS, a);
+        const bool pos = active_stage(stage) ? (up < P->detection_prob) : (up < P->false_positive_prob);
+        const int span = P->turnaround_max - P->turnaround_min + 1;
+        const int turn = P->turnaround_min + (int)(draw(A.K, A.inj, P_TEST_TURN, a) * span);
+        st.test_sample_at[a] = step;
+        st.test_result_at[a] = step + turn;
+        st.test_positive[a] = pos;
+        tested = 1;
+      }
+      // delivery
+      if (st.test_result_at[a] == step) {
+        const bool pos = st.test_positive[a] != 0;
+        st.test_result_at[a] = NEVER;
+        st.test_positive[a] = 0;
+        if (pos) {
+          if (P->quarantine_enabled) {
+            st.quarantine_until[a] = step + P->quarantine_duration;
+            st.quarantine_started_at[a] = step;
+          }
+          if (P->den_enabled && st.has_den_app[a]) fl |= FL_NOTIFIER;
+        }
+      }
+      A.flags[a] = fl;
+    }
+    rec_add(racc, EPI_REC_TESTS, tested);
+  }
+  __syncthreads();
+  rec_flush(racc, A.rec, A.step);
+}
+
+// Contact scan over a COO ring slot: notified[dst] if src is a notifier
+// (ContactLog.contacts_of, interventions.py:160-178).
+__global__ void k_den_scan_coo(const int32_t* __restrict__ src, const int32_t* __restrict__ dst,
+                               int64_t E, uint8_t* __restrict__ flags) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < E;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    if (flags[src[i]] & FL_NOTIFIER) {
+      const int32_t d = dst[i];
+      if (!(flags[d] & FL_NOTIFIED)) atomicOr((unsigned*)(flags + (d & ~3)), (unsigned)FL_NOTIFIED << (8 * (d & 3)));
+    }
+  }
+}
+// Same over a padded config CSR slot; config graphs are symmetric, so the
+// contacts of notifier a are the sources listed in a's own row.
+__global__ void k_den_scan_csr(const uint32_t* __restrict__ entries, const int32_t* __restrict__ row_len,
+                               int cap, int64_t n, uint8_t* __restrict__ flags) {
+  for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < n;
+       a += (int64_t)gridDim.x * blockDim.x) {
+    if (!(flags[a] & FL_NOTIFIER)) continue;
+    const int len = row_len[a];
+    const uint32_t* e = entries + a * (int64_t)cap;
+    for (int i = 0; i < len; ++i) {
+      const int64_t c = e[i] >> 2;
+      if (!(flags[c] & FL_NOTIFIED))
+        atomicOr((unsigned*)(flags + (c & ~3ll)), (unsigned)FL_NOTIFIED << (8 * (c & 3)));
+    }
+  }
+}
+
+__device__ __forceinline__ void realize_immunity(const StepArgs& A, int64_t a, int dose) {
+  const epi_state& st = A.st;
+  const double u = draw(A.K, A.inj, P_VAX, a, dose);
+  if (u < st.immunity_check_prob[a] && st.stage[a] == S_SUS) {
+    st.immune[a] = 1;
+    if (A.P->sterilizing) st.stage[a] = S_VAC;
+  }
+  st.immunity_check_at[a] = NEVER;
+  st.immunity_check_prob[a] = 0.0;
+  st.immunity_check_dose[a] = 0;
+}
+
+// Phase 4b (DEN follow-ups), 5 (dropout), 6a (due immunity checks,
+// eligibility buckets, active count).  engine.py:244-310.
+__global__ void k_iv_post(StepArgs A, uint8_t* __restrict__ bucket, unsigned long long* __restrict__ hist) {
+  __shared__ RecAcc racc;
+  __shared__ unsigned long long h[NUM_BUCKETS];
+  rec_init(racc);
+  for (int i = threadIdx.x; i < NUM_BUCKETS; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  const epi_params* __restrict__ P = A.P;
+  const epi_state& st = A.st;
+  const int step = A.step;
+  const int64_t n = st.n_agents;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n; base += stride) {
+    const int64_t a = base + threadIdx.x;
+    unsigned notified = 0, active = 0;
+    if (a < n) {
+      const uint8_t fl = A.flags[a];
+      if (P->den_enabled && (fl & FL_NOTIFIED) && st.has_den_app[a] &&
+          st.quarantine_until[a] <= step && st.stage[a] != S_DEAD) {
+        notified = 1;
+        if (draw(A.K, A.inj, P_DEN, a) < P->den_compliance) st.den_test_due_at[a] = step + 1;
+      }
+      if (P->quarantine_enabled && st.quarantine_until[a] > step && st.quarantine_started_at[a] < step) {
+        if (draw(A.K, A.inj, P_QDROP, a) < P->quarantine_dropout) st.quarantine_until[a] = step;
+      }
+      if (P->vaccination_enabled) {
+        if (st.immunity_check_at[a] == step) {
+          const int dose = st.immunity_check_dose[a];
+          if (dose == 1 || dose == 2) realize_immunity(A, a, dose);
+        }
+        const int stage = st.stage[a];
+        active = active_stage(stage);
+        const bool blocked = stage == S_DEAD || stage == S_HOSP || stage == S_ICU;
+        const int vs = st.vaccine_status[a];
+        const bool d1 = vs == 0 && !blocked;
+        const int32_t d1at = st.dose1_at[a];
+        const bool d2 = vs == 1 && d1at != NEVER && step >= d1at + P->dose_gap && !blocked;
+        uint8_t bk = NO_BUCKET;
+        if (d1 || d2) {
+          const int age = st.age_band[a];
+          int group;
+          if (P->strategy == 0) group = d2 ? 0 : 1;
+          else if (P->strategy == 1) group = d2 ? 1 : 0;
+          else group = (age >= P->elderly_band) ? 0 : (d2 ? 2 : 1);
+          bk = (uint8_t)((group * 9 + (8 - age)) * 2 + (d2 ? 1 : 0));
+          atomicAdd(&h[bk], 1ull);
+        }
+        bucket[a] = bk;
+      }
+    }
+    rec_add(racc, EPI_REC_NOTIFY, notified);
+    rec_add(racc, EPI_REC_ACTIVE, active);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < NUM_BUCKETS; i += blockDim.x)
+    if (h[i]) atomicAdd(&hist[i], h[i]);
+  rec_flush(racc, A.rec, A.step);
+}
+
+// plan[0] = cut bucket (-1: nobody), plan[1] = remaining slots in the cut
+// bucket.  Trigger latch + budget (engine.py:286-310).
+__global__ void k_vax_plan(const epi_params* __restrict__ P, const unsigned long long* __restrict__ hist,
+                           long long* rec, int32_t* vax_open, long long* plan) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  int open = *vax_open;
+  if (!open && (double)rec[EPI_REC_ACTIVE] >= P->start_trigger_count) open = 1;
+  *vax_open = open;
+  plan[0] = -1;
+  plan[1] = 0;
+  const long long budget = P->dose_budget;
+  if (!open || budget <= 0) return;
+  long long cum = 0;
+  for (int b = 0; b < NUM_BUCKETS; ++b) {
+    const long long c = (long long)hist[b];
+    if (cum + c >= budget) {
+      plan[0] = b;
+      plan[1] = budget - cum;
+      rec[EPI_REC_DOSES] = budget;
+      return;
+    }
+    cum += c;
+  }
+  plan[0] = NUM_BUCKETS;       // everyone eligible gets a dose
+  plan[1] = 0;
+  rec[EPI_REC_DOSES] = cum;
+}
+
+constexpr int VAX_TILE = 1024;
+
+__global__ void k_vax_tilecount(const uint8_t* __restrict__ bucket, int64_t n, const long long* plan,
+                                int* __restrict__ tile_count) {
+  const long long cut = plan[0];
+  __shared__ int cnt;
+  if (threadIdx.x == 0) cnt = 0;
+  __syncthreads();
+  const int64_t a = blockIdx.x * (int64_t)VAX_TILE + threadIdx.x;
+  const int hit = (cut >= 0 && cut < NUM_BUCKETS && a < n && bucket[a] == (uint8_t)cut) ? 1 : 0;
+  const int w = __reduce_add_sync(0xFFFFFFFFu, hit);
+  if (lane_id() == 0 && w) atomicAdd(&cnt, w);
+  __syncthreads();
+  if (threadIdx.x == 0) tile_count[blockIdx.x] = cnt;
+}
+
+__global__ void k_vax_tilescan(int* __restrict__ tile_count, int64_t tiles) {
+  // single block exclusive scan (tiles <= a few 10k)
+  typedef cub::BlockScan<int, 1024> Scan;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int64_t base = 0; base < tiles; base += 1024) {
+    const int64_t i = base + threadIdx.x;
+    const int v = i < tiles ? tile_count[i] : 0;
+    int ex, total;
+    Scan(tmp).ExclusiveSum(v, ex, total);
+    if (i < tiles) tile_count[i] = ex + carry;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += total;
+    __syncthreads();
+  }
+}
+
+// Phase 6b: administer doses to the selected agents (engine.py:306-335).
+__global__ void __launch_bounds__(1024) k_vax_apply(StepArgs A, const uint8_t* __restrict__ bucket,
+                                                    const long long* plan, const int* __restrict__ tile_off) {
+  typedef cub::BlockScan<int, 1024> Scan;
+  __shared__ typename Scan::TempStorage tmp;
+  const long long cut = plan[0], rem = plan[1];
+  const epi_params* __restrict__ P = A.P;
+  const epi_state& st = A.st;
+  const int step = A.step;
+  const int64_t n = st.n_agents;
+  const int64_t a = blockIdx.x * (int64_t)VAX_TILE + threadIdx.x;
+  const uint8_t bk = a < n ? bucket[a] : NO_BUCKET;
+  const int in_cut = (cut >= 0 && cut < NUM_BUCKETS && bk == (uint8_t)cut) ? 1 : 0;
+  int rank;
+  Scan(tmp).ExclusiveSum(in_cut, rank);
+  if (cut < 0 || bk == NO_BUCKET) return;
+  bool take = (long long)bk < cut || (in_cut && (long long)(tile_off[blockIdx.x] + rank) < rem);
+  if (!take) return;
+  if ((bk & 1) == 0) {       // first dose
+    st.vaccine_status[a] = 1;
+    st.dose1_at[a] = step;
+    st.immunity_check_at[a] = step + P->dose1_latency;
+    st.immunity_check_prob[a] = P->dose1_efficacy;
+    st.immunity_check_dose[a] = 1;
+    if (P->dose1_latency == 0) realize_immunity(A, a, 1);
+  } else {                   // second dose
+    st.vaccine_status[a] = 2;
+    st.dose2_at[a] = step;
+    double prob = (st.immunity_check_at[a] != NEVER) ? P->dose2_efficacy : P->dose2_topup;
+    if (st.immune[a]) prob = 0.0;
+    st.immunity_check_at[a] = step + P->dose2_latency;
+    st.immunity_check_prob[a] = prob;
+    st.immunity_check_dose[a] = 2;
+    if (P->dose2_latency == 0) realize_immunity(A, a, 2);
+  }
+}
+
+// Last kernel of an intervention step: record + next codes + clear flags.
+__global__ void k_finish(StepArgs A, uint16_t* __restrict__ codes_next, const epi_net* net,
+                         uint64_t rcount_next) {
+  __shared__ RecAcc racc;
+  rec_init(racc);
+  __syncthreads();
+  const int64_t n = A.st.n_agents;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n; base += stride) {
+    const int64_t a = base + threadIdx.x;
+    const bool valid = a < n;
+    rec_agent(racc, valid, valid ? A.st.stage[a] : 0, valid ? A.st.infected_at[a] : 0);
+    if (valid) {
+      if (codes_next) codes_next[a] = next_code(A.P, A.st, a, A.step + 1, net, rcount_next);
+      if (A.flags) A.flags[a] = 0;
+    }
+  }
+  __syncthreads();
+  rec_flush(racc, A.rec, A.step);
+}
+
+// ---------------------------------------------------------------------------
+__global__ void k_uniforms(uint64_t prefix, const int64_t* __restrict__ ids, int64_t n, int k,
+                           double* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = keyed_u(prefix, (uint64_t)(ids ? ids[i] : i), (uint64_t)k);
+}
+
+// Seeding at step 0 (population.py:151-177 after the choice of ids).
+__global__ void k_seed(const epi_params* __restrict__ P, epi_state st, StepKeys K,
+                       const int64_t* __restrict__ ids, int64_t m) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = ids[i];
+    const int age = st.age_band[a];
+    const int entry = P->targets[S_SUS][pick_branch(P, S_SUS, age, keyed_u(K.p[P_ENTRY], a))];
+    int nxt, delay;
+    schedule(P, entry, age, keyed_u(K.p[P_BRANCH], a), keyed_u(K.p[P_DELAY], a), nxt, delay);
+    st.stage[a] = (int8_t)entry;
+    st.infected_at[a] = 0;
+    st.next_stage[a] = (int8_t)nxt;
+    st.next_transition_at[a] = delay;
+  }
+}
+
+__global__ void k_assign_app(epi_state st, uint64_t prefix, double adoption) {
+  for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < st.n_agents;
+       a += (int64_t)gridDim.x * blockDim.x)
+    st.has_den_app[a] = keyed_u(prefix, (uint64_t)a) < adoption;
+}
+
+}  // namespace epi

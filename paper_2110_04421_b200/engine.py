@@ -1,0 +1,239 @@
+"""Drop-in replacement for the reference `Engine` (engine.py:55-347).
+
+Same constructor, attributes (`cols`, `disease`, `table`, `iv`, `seed`,
+`clock`, `vaccination_open`, `contact_log`, `check`) and methods
+(`step(graph) -> StepEvents`, `gather_exposure(graph) -> float64[N]`); every
+phase runs on the GPU through libepib200:
+
+  step(graph):  graph -> device COO -> CUB sort into canonical CSR
+                -> fp64 message pass in (dst, src, kind) order (bitwise equal
+                   to the reference) fused with transmission + progression
+                -> intervention phase kernels -> per-step record.
+
+Compat mode (default) uploads the caller's `AgentColumns` before each call and
+writes the new state back afterwards, because reference callers read and
+even mutate `cols` between steps (runner.py:101-116, tests).  With
+`resident=True` the state stays on the device and `sync_to_host()` /
+`sync_to_device()` move it explicitly.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from .device import DeviceColumns, pack_params
+from .errors import InvariantViolation
+from .state import DYNAMIC_COLUMNS
+
+
+@dataclass
+class StepEvents:
+    """Per-step counts (engine.py:41-52)."""
+
+    step: int
+    n_edges: int = 0
+    new_infections: int = 0
+    deaths: int = 0
+    hospitalizations: int = 0
+    tests_administered: int = 0
+    doses_given: int = 0
+    notifications_sent: int = 0
+
+    @classmethod
+    def from_record(cls, rec) -> "StepEvents":
+        r = N.REC
+        return cls(int(rec[r["step"]]), int(rec[r["edges"]]), int(rec[r["new_inf"]]),
+                   int(rec[r["deaths"]]), int(rec[r["hosp"]]), int(rec[r["tests"]]),
+                   int(rec[r["doses"]]), int(rec[r["notify"]]))
+
+
+class DeviceContactLog:
+    """Stand-in for `ContactLog` (interventions.py:145-178): the edges live in
+    a device ring inside the native context; this object reports its size."""
+
+    def __init__(self, lookback: int):
+        self.lookback = lookback
+        self._n = 0
+
+    def _pushed(self):
+        self._n = min(self._n + 1, self.lookback)
+
+    def __len__(self):
+        return self._n
+
+
+class GpuEngine:
+    """Single-writer columnar engine for one replication, on one GPU."""
+
+    def __init__(self, cols, disease, table, interventions, seed: int,
+                 check_invariants: bool = True, resident: bool = False, device=None):
+        import torch
+        self._lib = N.lib()
+        self.cols = cols
+        self.disease = disease
+        self.table = table
+        self.iv = interventions
+        self.seed = seed
+        self.clock = 0
+        self.check = check_invariants
+        self.resident = resident
+        self.contact_log = DeviceContactLog(interventions.den.lookback) \
+            if interventions.den_enabled else None
+        self._sterilizing = int(interventions.vaccine.immunity_mode) == 0
+        self.n = cols.n_agents
+        self.device = torch.device(device or "cuda")
+        self._params = pack_params(disease, table, interventions, self.n)
+        ctx = N._p()
+        N.check(self._lib.epi_create(C_ref(self._params), self.n, C_ref(ctx)))
+        self._ctx = ctx
+        self.dev = DeviceColumns.from_host(cols, self.device)
+        self._vax = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self._rec = torch.zeros(N.REC_LEN, dtype=torch.int64, device=self.device)
+
+    def __del__(self):
+        ctx = getattr(self, "_ctx", None)
+        if ctx is not None and ctx.value:
+            self._lib.epi_destroy(ctx)
+            self._ctx = None
+
+    # -- state movement ---------------------------------------------------
+    def sync_to_device(self):
+        self.dev.upload(self.cols)
+
+    def sync_to_host(self):
+        self.dev.download(self.cols, DYNAMIC_COLUMNS)
+
+    @property
+    def vaccination_open(self) -> bool:
+        return bool(int(self._vax.item()))
+
+    @vaccination_open.setter
+    def vaccination_open(self, value: bool):
+        self._vax.fill_(int(bool(value)))
+
+    # -- graph upload + validation (engine.py:124-133) ----------------------
+    def _load(self, graph):
+        import torch
+        if graph.on_device:
+            src, dst, kind = graph.src, graph.dst, graph.kind
+        else:
+            src = torch.from_numpy(np.ascontiguousarray(graph.src, np.int32)).to(self.device)
+            dst = torch.from_numpy(np.ascontiguousarray(graph.dst, np.int32)).to(self.device)
+            kind = torch.from_numpy(np.ascontiguousarray(graph.kind, np.int8)).to(self.device)
+        self._graph_tensors = (src, dst, kind)      # keep alive while the ctx refers to them
+        s = N.stream_handle()
+        N.check(self._lib.epi_graph_load(self._ctx, N.ptr(src), N.ptr(dst), N.ptr(kind),
+                                         int(src.shape[0]), s))
+        flags = N._i32()
+        N.check(self._lib.epi_read_flags(self._ctx, C_ref(flags), s))
+        f = flags.value
+        if f & N.FLAG_INDEX:
+            h = graph.to_host()
+            top = max(int(np.max(h.src)), int(np.max(h.dst)))
+            raise InvariantViolation(f"graph references agent {top} >= n_agents {self.n}")
+        if f & N.FLAG_SELFLOOP:
+            raise InvariantViolation("graph contains a self-loop")
+        if f & N.FLAG_KIND:
+            raise InvariantViolation("graph contains an unknown network kind")
+
+    def gather_exposure(self, graph):
+        """Summed hazard per agent, float64[N], bitwise equal to the reference."""
+        import torch
+        if not self.resident:
+            self.sync_to_device()
+        self._load(graph)
+        out = torch.empty(self.n, dtype=torch.float64, device=self.device)
+        st = self.dev.struct()
+        N.check(self._lib.epi_gather(self._ctx, C_ref(st), int(self.clock), N.F64_CANONICAL,
+                                     N.ptr(out), N.stream_handle()))
+        return out.cpu().numpy()
+
+    def gather_exposure_f32(self, graph):
+        """fp32 fast-mode hazard (factored per-source message), float32[N]."""
+        import torch
+        if not self.resident:
+            self.sync_to_device()
+        self._load(graph)
+        out = torch.empty(self.n, dtype=torch.float32, device=self.device)
+        st = self.dev.struct()
+        N.check(self._lib.epi_gather(self._ctx, C_ref(st), int(self.clock), N.F32,
+                                     N.ptr(out), N.stream_handle()))
+        return out.cpu().numpy()
+
+    # -- the step (engine.py:121-151) -----------------------------------------
+    def step(self, graph, injected=None) -> StepEvents:
+        if graph.step != self.clock:
+            raise InvariantViolation(
+                f"graph built for step {graph.step}, engine clock is {self.clock}")
+        if not self.resident:
+            self.sync_to_device()
+        self._load(graph)
+        st = self.dev.struct()
+        inj = _injected_array(injected)
+        N.check(self._lib.epi_step(self._ctx, C_ref(st), int(self.clock), _u64(self.seed),
+                                   N.ptr(self._rec), N.ptr(self._vax), inj, int(self.check),
+                                   N.stream_handle()))
+        rec = self._rec.cpu().numpy()
+        if not self.resident:
+            self.sync_to_host()
+        if self.contact_log is not None:
+            self.contact_log._pushed()
+        if self.check:
+            _raise_for_flags(int(rec[N.REC["flags"]]), self.clock, self.n)
+        ev = StepEvents.from_record(rec)
+        self.clock += 1
+        return ev
+
+    def step_with_hazard(self, hazard, injected=None) -> StepEvents:
+        """Phases 1-6 with a caller-supplied float64 hazard (parity tests)."""
+        import torch
+        if not self.resident:
+            self.sync_to_device()
+        h = torch.as_tensor(np.ascontiguousarray(hazard, np.float64)).to(self.device)
+        st = self.dev.struct()
+        N.check(self._lib.epi_step_with_hazard(self._ctx, C_ref(st), int(self.clock),
+                                               _u64(self.seed), N.ptr(h), N.ptr(self._rec),
+                                               N.ptr(self._vax), _injected_array(injected),
+                                               N.stream_handle()))
+        rec = self._rec.cpu().numpy()
+        if not self.resident:
+            self.sync_to_host()
+        ev = StepEvents.from_record(rec)
+        self.clock += 1
+        return ev
+
+    def last_record(self) -> np.ndarray:
+        return self._rec.cpu().numpy()
+
+
+def _raise_for_flags(f: int, step: int, n: int) -> None:
+    if f & N.FLAG_NEG_HAZARD:
+        raise InvariantViolation("negative hazard out of gather")
+    if f & N.FLAG_STAGE_RANGE:
+        raise InvariantViolation(f"step {step}: stage out of range")
+    if f & N.FLAG_NO_TIMESTAMP:
+        raise InvariantViolation(f"step {step}: non-susceptible agent without infection timestamp")
+
+
+def _u64(x: int) -> int:
+    return int(x) & ((1 << 64) - 1)
+
+
+def _injected_array(injected):
+    """dict purpose -> device float64 tensor  ->  double*[12] (or None)."""
+    if not injected:
+        return None
+    arr = (N._p * 12)()
+    for k, t in injected.items():
+        arr[int(k)] = N.ptr(t)
+    _injected_array.keep = (arr, injected)
+    import ctypes
+    return ctypes.addressof(arr)
+
+
+def C_ref(x):
+    import ctypes
+    return ctypes.byref(x)

@@ -1,0 +1,115 @@
+"""GPU config-network generator and device simulation vs the CPU oracle."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import confignet_np, engine_np
+from paper_2110_04421_b200.confignet import ConfigNetworkSpec, synthesize
+from paper_2110_04421_b200.defaults import default_disease, default_progression
+from paper_2110_04421_b200.graph import StepGraph
+from paper_2110_04421_b200.interventions import (DenConfig, InterventionConfig, TestKind,
+                                                 VaccinePolicy)
+from paper_2110_04421_b200.sim import ConfigSimulation, initial_columns
+
+pytestmark = pytest.mark.gpu
+
+
+def _same_edges(g, ref):
+    src, dst, kind = ref
+    g = g.sorted_canonical()
+    assert np.array_equal(g.dst, dst)
+    assert np.array_equal(g.src, src)
+    assert np.array_equal(g.kind, kind)
+
+
+@pytest.mark.parametrize("cfg,n", [(0, 3000), (1, 5000), (1, 37)])
+def test_realize_bitwise_vs_oracle(cfg, n):
+    spec = ConfigNetworkSpec.config(cfg, n_agents=n, initial_infections=min(10, n))
+    sim = ConfigSimulation.create(spec, seed=123, precision="f64")
+    for day in range(3):
+        dead = sim.host_columns().stage == 10
+        _same_edges(sim.realize_graph(day), confignet_np.realize(sim.population, sim.seed, day, dead))
+        sim.step()
+
+
+def test_realize_with_dead_agents_bitwise():
+    spec = ConfigNetworkSpec.config(1, n_agents=4000)
+    pop = synthesize(spec, 9)
+    cols = initial_columns(pop)
+    rng = np.random.default_rng(0)
+    dead_ids = rng.choice(spec.n_agents, 400, replace=False)
+    cols.stage[dead_ids] = 10
+    cols.infected_at[dead_ids] = 0
+    from paper_2110_04421_b200.device import DeviceColumns
+    sim = ConfigSimulation(pop, default_disease(), default_progression(), InterventionConfig(), 9,
+                           initial=DeviceColumns.from_host(cols))
+    dead = cols.stage == 10
+    g = sim.realize_graph(0)
+    _same_edges(g, confignet_np.realize(pop, 9, 0, dead))
+    h = g.to_host()
+    assert not dead[h.src].any() and not dead[h.dst].any()
+    assert not np.any(h.src == h.dst)
+
+
+def test_edge_counts_and_symmetry_at_config1_scale():
+    spec = ConfigNetworkSpec.config(1)
+    sim = ConfigSimulation.create(spec, seed=1)
+    g = sim.realize_graph(0).to_host()
+    per_agent = g.n_edges / spec.n_agents
+    assert 20.5 < per_agent < 21.6, per_agent
+    fwd = np.sort(g.src.astype(np.int64) << 32 | g.dst)
+    bwd = np.sort(g.dst.astype(np.int64) << 32 | g.src)
+    assert np.array_equal(fwd, bwd)
+
+
+def _oracle_run(sim, horizon, iv):
+    cols = sim.initial_host_columns()
+    eng = engine_np.OracleEngine(cols, sim.disease, sim.table, iv, sim.seed)
+    rows = []
+    for t in range(horizon):
+        src, dst, kind = confignet_np.realize(sim.population, sim.seed, t, cols.stage == 10)
+        ev = eng.step(StepGraph(t, src, dst, kind))
+        rows.append(engine_np.series_row(cols, ev))
+    return cols, np.array(rows)
+
+
+@pytest.mark.parametrize("iv_name", ["none", "all"])
+def test_device_simulation_bitwise_vs_oracle(iv_name):
+    iv = InterventionConfig()
+    if iv_name == "all":
+        iv = InterventionConfig(quarantine_enabled=True, testing_enabled=True,
+                                test_kind=TestKind("cfg2", 0.05, 2, 2), den_enabled=True,
+                                den=DenConfig(0.5), vaccination_enabled=True,
+                                vaccine=VaccinePolicy(daily_rate=0.01, dose1_efficacy=0.5,
+                                                      dose2_efficacy=0.9, dose_gap=21,
+                                                      start_trigger=0.002))
+    spec = ConfigNetworkSpec.config(1, n_agents=3000, initial_infections=30)
+    horizon = 40
+    sim = ConfigSimulation.create(spec, seed=5, interventions=iv, mode="csr", precision="f64",
+                                  horizon=horizon)
+    sim.run()
+    cols_o, rows_o = _oracle_run(sim, horizon, iv)
+    got = sim.time_series()
+    assert np.array_equal(got, rows_o), np.argwhere(got != rows_o)[:5]
+    cols_g = sim.host_columns()
+    for c in ("stage", "infected_at", "next_stage", "next_transition_at", "quarantine_until",
+              "vaccine_status", "immune", "dose1_at", "test_result_at"):
+        assert np.array_equal(getattr(cols_g, c), getattr(cols_o, c)), c
+
+
+def test_fused_and_csr_f32_agree_and_graph_replay_is_identical():
+    spec = ConfigNetworkSpec.config(1, n_agents=20000, initial_infections=50)
+    a = ConfigSimulation.create(spec, seed=2, mode="csr", precision="f32", horizon=60)
+    b = ConfigSimulation.create(spec, seed=2, mode="fused", precision="f32", horizon=60)
+    a.run()
+    b.run()
+    ra, rb = a.records(), b.records()
+    # identical edge counts until the first deaths (>= 2 weeks after infection)
+    assert np.array_equal(ra[:10, 19], rb[:10, 19])
+    # same network and draws: only fp32 summation order differs
+    assert abs(int(ra[-1, 12]) - int(rb[-1, 12])) <= 0.02 * max(1, int(ra[-1, 12]))
+    b.capture()
+    b.replay()
+    assert np.array_equal(b.records(), rb)

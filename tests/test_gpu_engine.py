@@ -1,0 +1,152 @@
+"""GPU parity of the drop-in engine (graph-in mode) against the oracle and the
+reference-generated trajectories.  Bar: bitwise for every state column and
+event count; fp32 hazard within 1e-5 relative."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+from oracle import engine_np, rng_np
+from paper_2110_04421_b200 import _native as N
+from paper_2110_04421_b200.engine import GpuEngine
+from paper_2110_04421_b200.errors import InvariantViolation
+from paper_2110_04421_b200.graph import StepGraph
+from paper_2110_04421_b200.interventions import InterventionConfig
+from paper_2110_04421_b200.stages import NetworkKind, Stage
+from paper_2110_04421_b200.state import AgentColumns
+
+from golden_io import Trajectory, compare_state, load
+
+pytestmark = pytest.mark.gpu
+
+
+def test_device_uniforms_match_reference_vectors():
+    lib = N.lib()
+    z = load("rng.npz")
+    ids = torch.from_numpy(z["ids"]).cuda()
+    for name in z.files:
+        if not name.startswith("vec_"):
+            continue
+        s, t, p, k = (int(x) for x in name[4:].split("_"))
+        out = torch.empty(ids.numel(), dtype=torch.float64, device="cuda")
+        N.check(lib.epi_uniforms(s & (2**64 - 1), t, p, N.ptr(ids), ids.numel(), k, N.ptr(out),
+                                 N.stream_handle()))
+        assert np.array_equal(out.cpu().numpy(), z[name]), name
+    out = torch.empty(5, dtype=torch.float64, device="cuda")
+    for key, want in zip(z["keys"].tolist(), z["scalar"]):
+        s, t, p, a, k = key
+        one = torch.tensor([a], dtype=torch.int64, device="cuda")
+        N.check(lib.epi_uniforms(s, t, p, N.ptr(one), 1, k, N.ptr(out), N.stream_handle()))
+        assert out[0].item() == want
+
+
+@pytest.mark.parametrize("name", ["noiv", "alliv", "nonster", "stdvax"])
+def test_engine_replays_reference_trajectory_bitwise(name):
+    tr = Trajectory(name)
+    cols = tr.initial_cols()
+    eng = GpuEngine(cols, tr.disease, tr.table, tr.iv, tr.seed)
+    for step in range(tr.horizon):
+        g = tr.graph(step)
+        want_h = tr.hazard(step)
+        if want_h is not None:
+            got_h = eng.gather_exposure(g)
+            assert np.array_equal(got_h, want_h), f"hazard differs at step {step}"
+            h32 = eng.gather_exposure_f32(g).astype(np.float64)
+            nz = want_h > 0
+            assert np.all(np.abs(h32[nz] - want_h[nz]) <= 1e-5 * want_h[nz])
+            assert np.all(h32[~nz] == 0)
+        ev = eng.step(g)
+        got = [ev.n_edges, ev.new_infections, ev.deaths, ev.hospitalizations,
+               ev.tests_administered, ev.doses_given, ev.notifications_sent]
+        assert got == tr.events[step].tolist(), f"events differ at step {step}: {got}"
+        compare_state(cols, tr, step)
+    assert eng.vaccination_open == bool(tr.z["vaccination_open"])
+
+
+def test_engine_matches_oracle_on_random_graphs_with_injected_hazard():
+    tr = Trajectory("alliv")
+    rng = np.random.default_rng(3)
+    cols_g, cols_o = tr.initial_cols(), tr.initial_cols()
+    eng = GpuEngine(cols_g, tr.disease, tr.table, tr.iv, tr.seed)
+    ora = engine_np.OracleEngine(cols_o, tr.disease, tr.table, tr.iv, tr.seed)
+    for step in range(tr.horizon):
+        g = tr.graph(step)
+        perm = rng.permutation(g.n_edges)
+        shuffled = StepGraph(step, g.src[perm], g.dst[perm], g.kind[perm])
+        ev_g, ev_o = eng.step(shuffled), ora.step(g)
+        assert ev_g.new_infections == ev_o.new_infections
+        for c in ("stage", "infected_at", "next_stage", "next_transition_at",
+                  "quarantine_until", "vaccine_status", "immune", "den_test_due_at"):
+            assert np.array_equal(getattr(cols_g, c), getattr(cols_o, c)), (step, c)
+
+
+def test_injected_uniforms_drive_stage_and_timer_bitwise():
+    """Stage/timer update given the same injected uniforms and hazard."""
+    tr = Trajectory("noiv")
+    cols_g, cols_o = tr.initial_cols(), tr.initial_cols()
+    n = tr.n
+    eng = GpuEngine(cols_g, tr.disease, tr.table, tr.iv, seed=0)
+    rng = np.random.default_rng(11)
+    for step in range(20):
+        hz = rng.exponential(0.3, n) * (rng.random(n) < 0.5)
+        draws = {p: rng.integers(0, 2**53, n).astype(np.float64) * 2.0**-53 for p in (1, 3, 4, 5)}
+        inj = {p: torch.from_numpy(v).cuda() for p, v in draws.items()}
+        eng.step_with_hazard(hz, injected=inj)
+        # oracle phases 1-2 with the same draws
+        c = cols_o
+        target = engine_np.target_mask(c, True)
+        hit = np.flatnonzero(target & (draws[1] < 1.0 - np.exp(-np.where(target, hz, 0.0))))
+        entry = engine_np.pick(tr.table.rules[0], c.age_band[hit], draws[3][hit])
+        c.stage[hit] = entry
+        c.infected_at[hit] = step
+        nxt, d = engine_np.schedule(tr.table, entry, c.age_band[hit], draws[4][hit], draws[5][hit])
+        c.next_stage[hit] = nxt
+        c.next_transition_at[hit] = step + d
+        due = np.flatnonzero(c.next_transition_at == step)
+        dest = c.next_stage[due].copy()
+        c.stage[due] = dest
+        fin = (dest == 8) | (dest == 10)
+        c.next_stage[due[fin]] = -1
+        c.next_transition_at[due[fin]] = -1
+        rest = due[~fin]
+        nxt, d = engine_np.schedule(tr.table, c.stage[rest], c.age_band[rest], draws[4][rest], draws[5][rest])
+        c.next_stage[rest] = nxt
+        c.next_transition_at[rest] = step + d
+        for col in ("stage", "infected_at", "next_stage", "next_transition_at"):
+            assert np.array_equal(getattr(cols_g, col), getattr(cols_o, col)), (step, col)
+
+
+def test_hard_errors():
+    cols = AgentColumns.allocate(3)
+    eng = GpuEngine(cols, Trajectory("noiv").disease, Trajectory("noiv").table, InterventionConfig(), 0)
+    with pytest.raises(InvariantViolation, match="clock"):
+        eng.step(StepGraph.empty(5))
+    bad = StepGraph(0, np.array([0], np.int32), np.array([7], np.int32), np.zeros(1, np.int8))
+    with pytest.raises(InvariantViolation, match="n_agents"):
+        eng.step(bad)
+    loop = StepGraph(0, np.array([1], np.int32), np.array([1], np.int32), np.zeros(1, np.int8))
+    with pytest.raises(InvariantViolation, match="self-loop"):
+        eng.step(loop)
+    ev = eng.step(StepGraph.empty(0))
+    assert ev.n_edges == 0 and ev.new_infections == 0 and eng.clock == 1
+
+
+def test_star_graph_gather_equals_formula():
+    from paper_2110_04421_b200.disease import edge_hazard
+    tr = Trajectory("noiv")
+    n_leaves = 6
+    cols = AgentColumns.allocate(n_leaves + 1)
+    cols.stage[0] = int(Stage.MILD_SYMPTOMATIC)
+    cols.infected_at[0] = 0
+    cols.next_stage[0] = int(Stage.RECOVERED)
+    cols.next_transition_at[0] = 10_000
+    eng = GpuEngine(cols, tr.disease, tr.table, InterventionConfig(), 0)
+    eng.clock = 4
+    leaves = np.arange(1, n_leaves + 1, dtype=np.int32)
+    hub = np.zeros(n_leaves, dtype=np.int32)
+    g = StepGraph(4, np.concatenate([hub, leaves]), np.concatenate([leaves, hub]),
+                  np.full(2 * n_leaves, int(NetworkKind.RANDOM), np.int8))
+    h = eng.gather_exposure(g)
+    assert np.all(h[1:] == edge_hazard(4, False, 0, 2, tr.disease))
+    assert h[0] == 0.0
