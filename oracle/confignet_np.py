@@ -18,29 +18,47 @@ from . import rng_np
 
 P_RCOUNT, P_RPERM, P_WPERM, P_WSHIFT = 72, 73, 74, 75
 M32 = np.uint64(0xFFFFFFFF)
+GOLD32 = np.uint64(0x9E3779B1)
 
 
-def _bits(n):
-    """Domain bits k with 2^k >= n (k >= 1)."""
-    return max(1, int(n - 1).bit_length())
+def radix(n):
+    """b = smallest integer with b*b >= n, a = ceil(n / b) (vectorised)."""
+    n = np.asarray(n, dtype=np.int64)
+    b = np.ceil(np.sqrt(np.maximum(n, 1).astype(np.float64))).astype(np.int64)
+    b = np.where(b * b < n, b + 1, b)
+    b = np.where((b > 1) & ((b - 1) * (b - 1) >= n), b - 1, b)
+    a = (n + b - 1) // b
+    return a.astype(np.uint64), b.astype(np.uint64)
 
 
-def _round_fwd(x, mult, key, mask, s):
-    x = (((x ^ key) * mult) & M32) & mask
-    return x ^ (x >> s)
+def _f(v, k1, k2, rad):
+    h = ((v ^ k1) * GOLD32) & M32
+    h = h ^ (h >> np.uint64(15))
+    h = (h * k2) & M32
+    h = h ^ (h >> np.uint64(13))
+    return (h * rad) >> np.uint64(32)
 
 
-def walk_forward(n, mults, keys):
-    """Cycle-walked keyed bijection of [0, n), evaluated for every x."""
-    k = _bits(n)
-    mask, s = np.uint64((1 << k) - 1), np.uint64((k + 1) >> 1)
-    out = np.arange(n, dtype=np.uint64)
-    todo = np.arange(n)
+def feistel_forward(x, k1, k2, a, b):
+    """One application of the 3-round mixed-radix Feistel on [0, a*b)."""
+    L, R = x // b, x % b
+    L = (L + _f(R, k1[0], k2[0], a)) % a
+    R = (R + _f(L, k1[1], k2[1], b)) % b
+    L = (L + _f(R, k1[2], k2[2], a)) % a
+    return L * b + R
+
+
+def walk(x, n, k1, k2, a, b):
+    """Cycle-walk the Feistel bijection until the value is < n (elementwise)."""
+    out = np.asarray(x, dtype=np.uint64).copy()
+    n = np.broadcast_to(np.asarray(n, dtype=np.uint64), out.shape)
+    todo = np.arange(len(out))
     cur = out.copy()
     while len(todo):
-        for m, kk in zip(mults, keys):
-            cur = _round_fwd(cur, np.uint64(m), np.uint64(kk) & mask, mask, s)
-        done = cur < np.uint64(n)
+        cur = feistel_forward(cur, [k[todo] if np.ndim(k) else k for k in k1],
+                              [k[todo] if np.ndim(k) else k for k in k2],
+                              a[todo] if np.ndim(a) else a, b[todo] if np.ndim(b) else b)
+        done = cur < n[todo]
         out[todo[done]] = cur[done]
         todo, cur = todo[~done], cur[~done]
     return out.astype(np.int64)
@@ -48,37 +66,32 @@ def walk_forward(n, mults, keys):
 
 def random_perm_keys(seed, step, slot):
     hs = [int(rng_np.hashes(seed, step, P_RPERM, [slot], r)[0]) for r in range(3)]
-    return [(h & 0xFFFFFFFF) | 1 for h in hs], [h >> 32 for h in hs]
+    return ([np.uint64(h & 0xFFFFFFFF) for h in hs],
+            [np.uint64((h >> 32) | 1) for h in hs])
 
 
-_BITLEN = np.array([max(1, int(x).bit_length()) for x in range(256)], dtype=np.uint64)
+def random_permutation(n, seed, step, slot):
+    """pi_{step,slot} as an array: pi[x] for every x in [0, n)."""
+    k1, k2 = random_perm_keys(seed, step, slot)
+    a, b = radix(n)
+    return walk(np.arange(n, dtype=np.uint64), n, k1, k2, np.uint64(a), np.uint64(b))
 
 
 def workplace_sigma(pop, seed, step):
-    """For every member slot (base_w + position): the local index sigma_w(position).
-    Vectorised over all workplaces; per-element domain bits, masks and keys."""
+    """For every member slot (base_w + position): the local index sigma_w(position)."""
     m_w = pop.wp_size.astype(np.int64)
     W = len(m_w)
-    h = rng_np.hashes(seed, step, P_WPERM, np.arange(W), 0)
+    ha = rng_np.hashes(seed, step, P_WPERM, np.arange(W), 0)
+    hb = rng_np.hashes(seed, step, P_WPERM, np.arange(W), 1)
+    m16 = np.uint64(0xFFFF)
+    k1 = [ha & m16, (ha >> np.uint64(32)) & m16, hb & m16]
+    k2 = [((ha >> np.uint64(16)) & m16) | np.uint64(1), ((ha >> np.uint64(48)) & m16) | np.uint64(1),
+          ((hb >> np.uint64(16)) & m16) | np.uint64(1)]
     owner = np.repeat(np.arange(W), m_w)
     pos = (np.arange(len(owner)) - pop.wp_base[owner]).astype(np.uint64)
-    m_i = m_w[owner].astype(np.uint64)
-    k_i = _BITLEN[np.maximum(m_w[owner] - 1, 0)]
-    mask = (np.uint64(1) << k_i) - np.uint64(1)
-    sh = (k_i + np.uint64(1)) >> np.uint64(1)
-    mult = [((h[owner] >> np.uint64(16 * r)) & np.uint64(0xFF)) | np.uint64(1) for r in range(3)]
-    key = [((h[owner] >> np.uint64(16 * r + 8)) & np.uint64(0xFF)) & mask for r in range(3)]
-    out = pos.copy()
-    todo = np.arange(len(pos))
-    cur = pos.copy()
-    while len(todo):
-        for r in range(3):
-            cur = (((cur ^ key[r][todo]) * mult[r][todo]) & M32) & mask[todo]
-            cur = cur ^ (cur >> sh[todo])
-        done = cur < m_i[todo]
-        out[todo[done]] = cur[done]
-        todo, cur = todo[~done], cur[~done]
-    return out.astype(np.int64)
+    a, b = radix(m_w)
+    return walk(pos, m_w[owner], [k[owner] for k in k1], [k[owner] for k in k2],
+                a[owner], b[owner])
 
 
 def work_shifts_all(pop, seed, step, draws):
@@ -141,8 +154,7 @@ def realize(pop, seed, step, dead, canonical=True):
     if n >= 2:
         cnt = random_counts(seed, step, n, pop.poisson_table(), dead)
         for j in range(spec.random_slots):
-            mults, keys = random_perm_keys(seed, step, j)
-            pi = walk_forward(n, mults, keys)
+            pi = random_permutation(n, seed, step, j)
             inv = np.empty(n, dtype=np.int64)
             inv[pi] = ids
             ok = (j < cnt) & (pi != ids) & alive & alive[pi]

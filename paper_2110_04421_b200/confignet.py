@@ -18,13 +18,23 @@ Per step t with graph seed g (the replication seed), dead agents excluded:
   household  : complete graph on the alive members;
   workplace  : sigma_{t,W} = keyed bijection of [0, m); shifts
                r_{t,W,j} in [1, m-1], j < colleague_draws; the worker at
-               position p interacts with positions p + r_j and p - r_j;
+               position p interacts with positions p + r_j and p - r_j (mod m);
   random     : for slot j < random_slots, pi_{t,j} = keyed bijection of
                [0, N); agent a with j < n_{t,a} (n ~ Poisson(random_mean)
                truncated at random_slots) interacts with pi_{t,j}(a) unless it
                is a itself.  The owner of b finds its in-partner via
                pi^{-1}(b) and checks n of that agent.
 Every interaction is stored in both directions.
+
+Keyed bijection of [0, n): 3-round Feistel network on the mixed-radix domain
+[0, a*b), b = ceil(sqrt(n)), a = ceil(n/b), x = L*b + R,
+    L <- (L + F(R, k0)) mod a;  R <- (R + F(L, k1)) mod b;  L <- (L + F(R, k2)) mod a
+with F(v, k) = mulhi(mix32(v ^ k.x) * k.y, radix), cycle-walked back into
+[0, n) (a*b - n < b, so a walk is needed with probability < 1/sqrt(n)).
+Round keys: random slot j, round r: hash64(g, t, NET_RANDOM_PERM, j, r)
+(low 32 bits = k.x, high 32 bits | 1 = k.y); workplace W: 16-bit fields of
+hash64(g, t, NET_WORK_PERM, W, 0..1).  Shift r_j: 16-bit chunk (j & 3) of
+hash64(g, t, NET_WORK_SHIFT, W, j >> 2), scaled as 1 + (v * (m-1)) >> 16.
 """
 
 from __future__ import annotations

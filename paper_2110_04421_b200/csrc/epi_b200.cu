@@ -441,15 +441,20 @@ static int check_net(const epi_net* net) {
 }
 
 static size_t realize_smem(const epi_net* net) {
-  return EPI_MAX_SLOTS * sizeof(PermKeys) + (size_t)128 * (net->row_cap | 1) * sizeof(uint32_t);
+  return (size_t)128 * (net->row_cap | 1) * sizeof(uint32_t);
 }
+
+// the register-batched enumerator covers <= 16 random slots and <= 8 draws
+static bool batched(const epi_net* net) { return net->random_slots <= 16 && net->colleague_draws <= 8; }
 
 static size_t g_realize_smem_set = 0;
 static int prepare_realize(const epi_net* net) {
   const size_t smem = realize_smem(net);
   if (smem > g_realize_smem_set) {
-    CK(cudaFuncSetAttribute(k_net_realize<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    CK(cudaFuncSetAttribute(k_net_realize<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(cudaFuncSetAttribute(k_net_realize<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(cudaFuncSetAttribute(k_net_realize<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(cudaFuncSetAttribute(k_net_realize<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(cudaFuncSetAttribute(k_net_realize<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     g_realize_smem_set = smem;
   }
   return 0;
@@ -462,10 +467,13 @@ static int launch_realize(const epi_net* net, uint64_t g, int32_t step, const ui
   if (smem > g_realize_smem_set) return fail(EPI_EARG, "realize smem not prepared");
   NetKeys nk = make_net_keys(g, step);
   const int grid = grid_for(net->n_agents, 128, 16);
+  const bool batch = batched(net);
   if (sort_rows) {
-    k_net_realize<true><<<grid, 128, smem, s>>>(*net, nk, codes, entries, row_len, rec);
+    if (batch) k_net_realize<true, true><<<grid, 128, smem, s>>>(*net, nk, codes, entries, row_len, rec);
+    else k_net_realize<true, false><<<grid, 128, smem, s>>>(*net, nk, codes, entries, row_len, rec);
   } else {
-    k_net_realize<false><<<grid, 128, smem, s>>>(*net, nk, codes, entries, row_len, rec);
+    if (batch) k_net_realize<false, true><<<grid, 128, smem, s>>>(*net, nk, codes, entries, row_len, rec);
+    else k_net_realize<false, false><<<grid, 128, smem, s>>>(*net, nk, codes, entries, row_len, rec);
   }
   CKL();
   return 0;
@@ -551,8 +559,14 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
     CKL();
   } else {
     if (ev) CK(cudaEventRecord((cudaEvent_t)ev[1], s));
-    k_fused_step<<<grid, 256, 0, s>>>(A, c->net, make_net_keys(seed, step), codes_cur, c->host.rate_scale,
-                                      codes_next, c->net_dev, rcount_next, iv ? 0 : 1);
+    if (batched(&c->net))
+      k_fused_step<true><<<grid, 256, 0, s>>>(A, c->net, make_net_keys(seed, step), codes_cur,
+                                              c->host.rate_scale, codes_next, c->net_dev, rcount_next,
+                                              iv ? 0 : 1);
+    else
+      k_fused_step<false><<<grid, 256, 0, s>>>(A, c->net, make_net_keys(seed, step), codes_cur,
+                                               c->host.rate_scale, codes_next, c->net_dev, rcount_next,
+                                               iv ? 0 : 1);
     CKL();
   }
   if (ev) CK(cudaEventRecord((cudaEvent_t)ev[2], s));

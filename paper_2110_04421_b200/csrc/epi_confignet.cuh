@@ -19,53 +19,76 @@
 
 namespace epi {
 
+// Keyed bijection of [0, n): a 3-round Feistel network on the mixed-radix
+// domain [0, a*b), b = ceil(sqrt(n)), a = ceil(n / b), so a*b - n < b and the
+// cycle walk back into [0, n) almost never iterates (probability < 1/sqrt(n)
+// per evaluation) — no warp divergence from rejection loops.
+//   x = L*b + R;  L += F(R,k0) mod a;  R += F(L,k1) mod b;  L += F(R,k2) mod a
+// F(v, k) = mulhi(mix(v ^ k.x, k.y), radix): uniform in [0, radix).
 struct PermKeys {
-  uint32_t mult[3], inv[3], key[3];
+  uint32_t k1[3], k2[3];
+};
+struct Radix {
+  uint32_t n, a, b, magic;   // magic = floor((2^32 - 1) / b)
 };
 
-__host__ __device__ __forceinline__ uint32_t inv_odd32(uint32_t m) {
-  uint32_t x = m;                 // correct to 3 bits for odd m
-  x *= 2u - m * x;                // 6
-  x *= 2u - m * x;                // 12
-  x *= 2u - m * x;                // 24
-  x *= 2u - m * x;                // 48
+__host__ __device__ __forceinline__ uint32_t isqrt_ceil(uint32_t n) {
+  // smallest b with b*b >= n (n >= 1)
+  uint32_t b = (uint32_t)sqrt((double)n);
+  while ((uint64_t)b * b < n) ++b;
+  while (b > 1 && (uint64_t)(b - 1) * (b - 1) >= n) --b;
+  return b;
+}
+__host__ __device__ __forceinline__ Radix make_radix(uint32_t n) {
+  Radix r;
+  r.n = n;
+  r.b = isqrt_ceil(n < 1 ? 1 : n);
+  r.a = (n + r.b - 1) / r.b;
+  r.magic = 0xFFFFFFFFu / r.b;
+  return r;
+}
+__device__ __forceinline__ uint32_t feistel_f(uint32_t v, uint32_t k1, uint32_t k2, uint32_t radix) {
+  uint32_t h = (v ^ k1) * 0x9E3779B1u;
+  h ^= h >> 15;
+  h *= k2;
+  h ^= h >> 13;
+  return __umulhi(h, radix);
+}
+__device__ __forceinline__ void split(uint32_t x, const Radix& d, uint32_t& L, uint32_t& R) {
+  L = __umulhi(x, d.magic);          // floor(x/b) or one less (x < 2^31)
+  R = x - L * d.b;
+  if (R >= d.b) { R -= d.b; ++L; }
+}
+__device__ __forceinline__ uint32_t add_mod(uint32_t x, uint32_t y, uint32_t m) {
+  const uint32_t z = x + y;
+  return z >= m ? z - m : z;
+}
+__device__ __forceinline__ uint32_t sub_mod(uint32_t x, uint32_t y, uint32_t m) {
+  return x >= y ? x - y : x + m - y;
+}
+__device__ __forceinline__ uint32_t perm_fwd(uint32_t x, const PermKeys& K, const Radix& d) {
+  uint32_t L, R;
+  split(x, d, L, R);
+  L = add_mod(L, feistel_f(R, K.k1[0], K.k2[0], d.a), d.a);
+  R = add_mod(R, feistel_f(L, K.k1[1], K.k2[1], d.b), d.b);
+  L = add_mod(L, feistel_f(R, K.k1[2], K.k2[2], d.a), d.a);
+  return L * d.b + R;
+}
+__device__ __forceinline__ uint32_t perm_inv(uint32_t y, const PermKeys& K, const Radix& d) {
+  uint32_t L, R;
+  split(y, d, L, R);
+  L = sub_mod(L, feistel_f(R, K.k1[2], K.k2[2], d.a), d.a);
+  R = sub_mod(R, feistel_f(L, K.k1[1], K.k2[1], d.b), d.b);
+  L = sub_mod(L, feistel_f(R, K.k1[0], K.k2[0], d.a), d.a);
+  return L * d.b + R;
+}
+// Cycle walking restricts the bijection of [0, a*b) to [0, n).
+__device__ __forceinline__ uint32_t walk_fwd(uint32_t x, const PermKeys& K, const Radix& d) {
+  do { x = perm_fwd(x, K, d); } while (x >= d.n);
   return x;
 }
-
-__host__ __device__ __forceinline__ int domain_bits(uint32_t n) {
-  // smallest k >= 1 with 2^k >= n
-  uint32_t v = n > 1 ? n - 1 : 1;
-  int k = 0;
-  while (v) { ++k; v >>= 1; }
-  return k < 1 ? 1 : k;
-}
-
-// One application of the 3-round multiply / xorshift bijection of [0, 2^k).
-__device__ __forceinline__ uint32_t perm_fwd(uint32_t x, const PermKeys& K, uint32_t mask, int s) {
-#pragma unroll
-  for (int r = 0; r < 3; ++r) {
-    x = ((x ^ (K.key[r] & mask)) * K.mult[r]) & mask;
-    x ^= x >> s;
-  }
-  return x;
-}
-__device__ __forceinline__ uint32_t perm_inv(uint32_t y, const PermKeys& K, uint32_t mask, int s) {
-#pragma unroll
-  for (int r = 2; r >= 0; --r) {
-    y ^= y >> s;
-    y = ((y * K.inv[r]) & mask) ^ (K.key[r] & mask);
-  }
-  return y;
-}
-// Cycle walking restricts the bijection of [0, 2^k) to [0, n).
-__device__ __forceinline__ uint32_t walk_fwd(uint32_t x, const PermKeys& K, uint32_t n,
-                                             uint32_t mask, int s) {
-  do { x = perm_fwd(x, K, mask, s); } while (x >= n);
-  return x;
-}
-__device__ __forceinline__ uint32_t walk_inv(uint32_t y, const PermKeys& K, uint32_t n,
-                                             uint32_t mask, int s) {
-  do { y = perm_inv(y, K, mask, s); } while (y >= n);
+__device__ __forceinline__ uint32_t walk_inv(uint32_t y, const PermKeys& K, const Radix& d) {
+  do { y = perm_inv(y, K, d); } while (y >= d.n);
   return y;
 }
 
@@ -84,23 +107,34 @@ __device__ __forceinline__ PermKeys random_slot_keys(uint64_t rperm_prefix, int 
 #pragma unroll
   for (int r = 0; r < 3; ++r) {
     const uint64_t h = fold(hs, (uint64_t)r);
-    K.mult[r] = (uint32_t)h | 1u;
-    K.inv[r] = inv_odd32(K.mult[r]);
-    K.key[r] = (uint32_t)(h >> 32);
+    K.k1[r] = (uint32_t)h;
+    K.k2[r] = (uint32_t)(h >> 32) | 1u;
   }
   return K;
 }
 
 __device__ __forceinline__ PermKeys work_keys(uint64_t wperm_prefix, int w) {
   PermKeys K;
-  const uint64_t h = fold(fold(wperm_prefix, (uint64_t)w), 0);
-#pragma unroll
-  for (int r = 0; r < 3; ++r) {
-    K.mult[r] = (uint32_t)((h >> (16 * r)) & 0xFF) | 1u;
-    K.inv[r] = inv_odd32(K.mult[r]);
-    K.key[r] = (uint32_t)((h >> (16 * r + 8)) & 0xFF);
-  }
+  const uint64_t hw = fold(wperm_prefix, (uint64_t)w);
+  const uint64_t ha = fold(hw, 0), hb = fold(hw, 1);
+  K.k1[0] = (uint32_t)(ha & 0xFFFF);
+  K.k2[0] = (uint32_t)((ha >> 16) & 0xFFFF) | 1u;
+  K.k1[1] = (uint32_t)((ha >> 32) & 0xFFFF);
+  K.k2[1] = (uint32_t)((ha >> 48) & 0xFFFF) | 1u;
+  K.k1[2] = (uint32_t)(hb & 0xFFFF);
+  K.k2[2] = (uint32_t)((hb >> 16) & 0xFFFF) | 1u;
   return K;
+}
+
+// Shared-memory table of the workplace domains (m <= 255) + the agent
+// domain, built once per block.
+struct NetTables {
+  PermKeys rk[EPI_MAX_SLOTS];
+  Radix wrad[256];
+};
+__device__ __forceinline__ void build_net_tables(NetTables& T, const epi_net& net, uint64_t rperm) {
+  for (int j = threadIdx.x; j < net.random_slots; j += blockDim.x) T.rk[j] = random_slot_keys(rperm, j);
+  for (int m = threadIdx.x; m < 256; m += blockDim.x) T.wrad[m] = make_radix(m < 1 ? 1u : (uint32_t)m);
 }
 
 // Random-slot count n_{t,a} ~ Poisson(mean) truncated at `slots`.
@@ -112,14 +146,89 @@ __device__ __forceinline__ int random_count(const epi_net& net, uint64_t rcount_
 }
 
 // Enumerate the in-edges of destination b (alive); visit(src, kind, code_src).
-// Order: household members ascending, workplace slots (out, in), random slots
-// (out, in).  `rk` holds the random-slot keys of this step (shared memory).
+// The work of one row is split over `nl` cooperating lanes; lane `li` takes
+// household members i, colleague draws j and random slots j with
+// index % nl == li.  With nl == 1 the order is: household members ascending,
+// workplace slots (out, in), random slots (out, in).  `rk` holds the
+// random-slot keys of this step (shared memory).
 template <class Visit>
 __device__ __forceinline__ void for_each_in_edge(const epi_net& net, const NetKeys& nk,
                                                  const PermKeys* __restrict__ rk,
+                                                 const Radix* __restrict__ wrad,
                                                  const uint16_t* __restrict__ codes, int64_t b,
-                                                 uint16_t code_b, Visit&& visit) {
+                                                 uint16_t code_b, int li, int nl, Visit&& visit) {
   // household: contiguous range
+  {
+    const int off = net.hh_off[b];
+    const int sz = net.hh_size[b];
+    const int64_t start = b - off;
+    for (int i = li; i < sz; i += nl) {
+      const int64_t c = start + i;
+      if (c == b) continue;
+      const uint16_t cc = codes[c];
+      if (!code_dead(cc)) visit(c, 0, cc);
+    }
+  }
+  // workplace
+  const int w = li < net.colleague_draws ? net.wp_id[b] : -1;
+  if (w >= 0) {
+    const int m = net.wp_size[w];
+    if (m >= 2) {
+      const Radix d = wrad[m];
+      const PermKeys K = work_keys(nk.wperm, w);
+      const int base = net.wp_base[w];
+      const uint32_t p = walk_inv(net.wp_local[b], K, d);
+      const uint64_t hw = fold(nk.wshift, (uint64_t)w);
+      uint64_t hq = 0;
+      int q_have = -1;
+      for (int j = li; j < net.colleague_draws; j += nl) {
+        if ((j >> 2) != q_have) { q_have = j >> 2; hq = fold(hw, (uint64_t)q_have); }
+        const uint32_t v = (uint32_t)((hq >> (16 * (j & 3))) & 0xFFFF);
+        const uint32_t r = 1u + ((v * (uint32_t)(m - 1)) >> 16);
+        const int32_t co = net.wp_members[base + walk_fwd(add_mod(p, r, (uint32_t)m), K, d)];
+        const int32_t ci = net.wp_members[base + walk_fwd(sub_mod(p, r, (uint32_t)m), K, d)];
+        const uint16_t cco = codes[co];
+        const uint16_t cci = codes[ci];
+        if (!code_dead(cco)) visit((int64_t)co, 1, cco);
+        if (!code_dead(cci)) visit((int64_t)ci, 1, cci);
+      }
+    }
+  }
+  // random slots
+  const uint32_t n = (uint32_t)net.n_agents;
+  if (n >= 2) {
+    const Radix d = make_radix(n);
+    const int nb = code_count(code_b);
+    for (int j = li; j < net.random_slots; j += nl) {
+      const PermKeys& K = rk[j];
+      const uint32_t ci = walk_inv((uint32_t)b, K, d);
+      if (j < nb) {
+        const uint32_t c = walk_fwd((uint32_t)b, K, d);
+        if (c != (uint32_t)b) {
+          const uint16_t cc = codes[c];
+          if (!code_dead(cc)) visit((int64_t)c, 2, cc);
+        }
+      }
+      if (ci != (uint32_t)b) {
+        const uint16_t cc = codes[ci];
+        if (j < code_count(cc)) visit((int64_t)ci, 2, cc);
+      }
+    }
+  }
+}
+
+// Batched single-lane enumeration: every partner id of a section is computed
+// first (pure ALU: keyed bijections), then all their codes are loaded at once
+// (up to 2*JMAX independent gathers in flight per lane), then visited.  Same
+// visit order as for_each_in_edge(..., 0, 1, ...).  Requires
+// random_slots <= JMAX and colleague_draws <= DMAX.
+template <int JMAX, int DMAX, class Visit>
+__device__ __forceinline__ void for_each_in_edge_batched(const epi_net& net, const NetKeys& nk,
+                                                         const PermKeys* __restrict__ rk,
+                                                         const Radix* __restrict__ wrad,
+                                                         const uint16_t* __restrict__ codes,
+                                                         int64_t b, uint16_t code_b, Visit&& visit) {
+  // household: contiguous range, one cache line in practice
   {
     const int off = net.hh_off[b];
     const int sz = net.hh_size[b];
@@ -136,49 +245,76 @@ __device__ __forceinline__ void for_each_in_edge(const epi_net& net, const NetKe
   if (w >= 0) {
     const int m = net.wp_size[w];
     if (m >= 2) {
-      const int kb = domain_bits((uint32_t)m);
-      const uint32_t mask = (1u << kb) - 1u;
-      const int s = (kb + 1) >> 1;
+      const Radix d = wrad[m];
       const PermKeys K = work_keys(nk.wperm, w);
       const int base = net.wp_base[w];
-      const uint32_t p = walk_inv(net.wp_local[b], K, (uint32_t)m, mask, s);
+      const uint32_t p = walk_inv(net.wp_local[b], K, d);
+      const uint64_t hw = fold(nk.wshift, (uint64_t)w);
+      const int draws = net.colleague_draws;
+      int32_t mo[DMAX], mi[DMAX];
       uint64_t hq = 0;
-      for (int j = 0; j < net.colleague_draws; ++j) {
-        if ((j & 3) == 0) hq = fold(fold(nk.wshift, (uint64_t)w), (uint64_t)(j >> 2));
-        const uint32_t v = (uint32_t)((hq >> (16 * (j & 3))) & 0xFFFF);
-        const uint32_t r = 1u + ((v * (uint32_t)(m - 1)) >> 16);
-        const uint32_t po = (p + r) % (uint32_t)m;
-        const uint32_t pi = (p + (uint32_t)m - r) % (uint32_t)m;
-        const int32_t co = net.wp_members[base + walk_fwd(po, K, (uint32_t)m, mask, s)];
-        const uint16_t cco = codes[co];
-        if (!code_dead(cco)) visit((int64_t)co, 1, cco);
-        const int32_t ci = net.wp_members[base + walk_fwd(pi, K, (uint32_t)m, mask, s)];
-        const uint16_t cci = codes[ci];
-        if (!code_dead(cci)) visit((int64_t)ci, 1, cci);
+#pragma unroll
+      for (int j = 0; j < DMAX; ++j) {
+        if (j < draws) {
+          if ((j & 3) == 0) hq = fold(hw, (uint64_t)(j >> 2));
+          const uint32_t v = (uint32_t)((hq >> (16 * (j & 3))) & 0xFFFF);
+          const uint32_t r = 1u + ((v * (uint32_t)(m - 1)) >> 16);
+          mo[j] = base + (int32_t)walk_fwd(add_mod(p, r, (uint32_t)m), K, d);
+          mi[j] = base + (int32_t)walk_fwd(sub_mod(p, r, (uint32_t)m), K, d);
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < DMAX; ++j) {
+        if (j < draws) {
+          mo[j] = net.wp_members[mo[j]];
+          mi[j] = net.wp_members[mi[j]];
+        }
+      }
+      uint16_t co[DMAX], ci[DMAX];
+#pragma unroll
+      for (int j = 0; j < DMAX; ++j) {
+        if (j < draws) {
+          co[j] = codes[mo[j]];
+          ci[j] = codes[mi[j]];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < DMAX; ++j) {
+        if (j < draws) {
+          if (!code_dead(co[j])) visit((int64_t)mo[j], 1, co[j]);
+          if (!code_dead(ci[j])) visit((int64_t)mi[j], 1, ci[j]);
+        }
       }
     }
   }
   // random slots
   const uint32_t n = (uint32_t)net.n_agents;
-  if (n >= 2 && net.random_slots > 0) {
-    const int kb = domain_bits(n);
-    const uint32_t mask = (kb >= 32) ? 0xFFFFFFFFu : ((1u << kb) - 1u);
-    const int s = (kb + 1) >> 1;
+  if (n >= 2) {
+    const Radix d = make_radix(n);
     const int nb = code_count(code_b);
-    for (int j = 0; j < net.random_slots; ++j) {
-      const PermKeys& K = rk[j];
-      if (j < nb) {
-        const uint32_t c = walk_fwd((uint32_t)b, K, n, mask, s);
-        if (c != (uint32_t)b) {
-          const uint16_t cc = codes[c];
-          if (!code_dead(cc)) visit((int64_t)c, 2, cc);
-        }
+    const int slots = net.random_slots;
+    const uint32_t self = (uint32_t)b;
+    uint32_t pin[JMAX], pout[JMAX];
+#pragma unroll
+    for (int j = 0; j < JMAX; ++j) {
+      pin[j] = self;
+      pout[j] = self;
+      if (j < slots) {
+        const PermKeys& K = rk[j];
+        pin[j] = walk_inv(self, K, d);
+        if (j < nb) pout[j] = walk_fwd(self, K, d);
       }
-      const uint32_t c = walk_inv((uint32_t)b, K, n, mask, s);
-      if (c != (uint32_t)b) {
-        const uint16_t cc = codes[c];
-        if (j < code_count(cc)) visit((int64_t)c, 2, cc);
-      }
+    }
+    uint16_t cin[JMAX], cout[JMAX];
+#pragma unroll
+    for (int j = 0; j < JMAX; ++j) {
+      cin[j] = pin[j] != self ? codes[pin[j]] : (uint16_t)0;
+      cout[j] = pout[j] != self ? codes[pout[j]] : (uint16_t)CODE_DEAD;
+    }
+#pragma unroll
+    for (int j = 0; j < JMAX; ++j) {
+      if (!code_dead(cout[j])) visit((int64_t)pout[j], 2, cout[j]);
+      if (j < code_count(cin[j])) visit((int64_t)pin[j], 2, cin[j]);
     }
   }
 }

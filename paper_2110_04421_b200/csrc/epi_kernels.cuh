@@ -295,9 +295,16 @@ __global__ void __launch_bounds__(256) k_pass(StepArgs A, CsrView g, const uint1
         if (row < n) {
           const int len = g.row_len[row];
           const uint32_t* e = g.entries + g.begin(row);
-          for (int i = gl; i < len; i += 8) {
-            const uint32_t x = __ldg(e + i);
-            acc += T.factor[codes[x >> 2] & 0xFF] * T.bfac[x & 3];
+          // 8 lanes x 4 entries in flight per pass, then their 4 code gathers
+          for (int i0 = gl; i0 < len; i0 += 32) {
+            uint32_t x[4];
+            uint16_t c[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) x[q] = (i0 + 8 * q < len) ? __ldg(e + i0 + 8 * q) : 0xFFFFFFFFu;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) c[q] = (x[q] != 0xFFFFFFFFu) ? codes[x[q] >> 2] : (uint16_t)0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc += T.factor[c[q] & 0xFF] * T.bfac[x[q] & 3];
           }
         }
         acc += __shfl_xor_sync(0xFFFFFFFFu, acc, 4);
@@ -363,18 +370,18 @@ __global__ void k_update_from_hazard(StepArgs A, const double* __restrict__ haza
 }
 
 // ---------------------------------------------------------------------------
-// Config CSR generation: one lane per destination row, rows staged in shared
-// memory (odd stride: conflict-free) then written out coalesced, one row per
-// warp-wide store.  SORT puts each row in canonical (src, kind) order.
-template <bool SORT>
+// Config CSR generation (mode 0): one lane per destination row; each row is
+// staged in shared memory (odd stride: conflict-free), optionally sorted into
+// canonical (src, kind) order, and the warp's 32 rows are written out
+// coalesced, one warp-wide store per row.
+template <bool SORT, bool BATCH>
 __global__ void __launch_bounds__(128) k_net_realize(epi_net net, NetKeys nk, const uint16_t* __restrict__ codes,
                                                      uint32_t* __restrict__ entries,
                                                      int32_t* __restrict__ row_len, long long* rec) {
-  extern __shared__ uint32_t smem[];
-  PermKeys* rk = (PermKeys*)smem;
-  uint32_t* stage_buf = (uint32_t*)(rk + EPI_MAX_SLOTS);
+  extern __shared__ uint32_t stage_buf[];
+  __shared__ NetTables NT;
   __shared__ RecAcc racc;
-  for (int j = threadIdx.x; j < net.random_slots; j += blockDim.x) rk[j] = random_slot_keys(nk.rperm, j);
+  build_net_tables(NT, net, nk.rperm);
   rec_init(racc);
   __syncthreads();
   const int cap = net.row_cap;
@@ -393,9 +400,9 @@ __global__ void __launch_bounds__(128) k_net_realize(epi_net net, NetKeys nk, co
     if (b < n) {
       const uint16_t cb = codes[b];
       if (!code_dead(cb)) {
-        for_each_in_edge(net, nk, rk, codes, b, cb, [&](int64_t c, int kind, uint16_t) {
-          mine[cnt++] = ((uint32_t)c << 2) | (uint32_t)kind;
-        });
+        auto put = [&](int64_t c, int kind, uint16_t) { mine[cnt++] = ((uint32_t)c << 2) | (uint32_t)kind; };
+        if (BATCH) for_each_in_edge_batched<16, 8>(net, nk, NT.rk, NT.wrad, codes, b, cb, put);
+        else for_each_in_edge(net, nk, NT.rk, NT.wrad, codes, b, cb, 0, 1, put);
       }
       if (SORT) {
         for (int i = 1; i < cnt; ++i) {
@@ -422,18 +429,20 @@ __global__ void __launch_bounds__(128) k_net_realize(epi_net net, NetKeys nk, co
   if (rec) rec_flush(racc, rec);
 }
 
-// Fused generate + gather + update: the in-edges are enumerated and their
-// source codes consumed on the fly, so no CSR ever reaches memory (mode 1).
+// Fused generate + gather + update (mode 1): the in-edges are enumerated and
+// their source codes consumed on the fly, so no CSR ever reaches memory.  One
+// lane per agent; gathers are batched per section (for_each_in_edge_batched).
+template <bool BATCH>
 __global__ void __launch_bounds__(256) k_fused_step(StepArgs A, epi_net net, NetKeys nk,
                                                     const uint16_t* __restrict__ codes, double rate,
                                                     uint16_t* __restrict__ codes_next,
                                                     const epi_net* net_dev, uint64_t rcount_next,
                                                     int final_pass) {
   __shared__ MsgTables T;
-  __shared__ PermKeys rk[EPI_MAX_SLOTS];
+  __shared__ NetTables NT;
   __shared__ RecAcc racc;
   build_msg_tables(T, A.P, rate);
-  for (int j = threadIdx.x; j < net.random_slots; j += blockDim.x) rk[j] = random_slot_keys(nk.rperm, j);
+  build_net_tables(NT, net, nk.rperm);
   rec_init(racc);
   __syncthreads();
   const int64_t n = A.st.n_agents;
@@ -447,10 +456,12 @@ __global__ void __launch_bounds__(256) k_fused_step(StepArgs A, epi_net net, Net
       const uint16_t cb = codes[b];
       if (!code_dead(cb)) {
         float acc = 0.f;
-        for_each_in_edge(net, nk, rk, codes, b, cb, [&](int64_t, int kind, uint16_t cc) {
+        auto add = [&](int64_t, int kind, uint16_t cc) {
           ++edges;
           acc += T.factor[cc & 0xFF] * T.bfac[kind];
-        });
+        };
+        if (BATCH) for_each_in_edge_batched<16, 8>(net, nk, NT.rk, NT.wrad, codes, b, cb, add);
+        else for_each_in_edge(net, nk, NT.rk, NT.wrad, codes, b, cb, 0, 1, add);
         if (is_target(A.P, A.st, b)) lam = (double)(acc * T.sfac[A.st.age_band[b]]);
       }
     }
