@@ -32,11 +32,8 @@ def radix(n):
 
 
 def _f(v, k1, k2, rad):
-    h = ((v ^ k1) * GOLD32) & M32
-    h = h ^ (h >> np.uint64(15))
-    h = (h * k2) & M32
-    h = h ^ (h >> np.uint64(13))
-    return (h * rad) >> np.uint64(32)
+    h = ((v ^ k1) * k2) & M32
+    return ((h ^ (h >> np.uint64(15))) * rad) >> np.uint64(32)
 
 
 def feistel_forward(x, k1, k2, a, b):

@@ -559,12 +559,13 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
     CKL();
   } else {
     if (ev) CK(cudaEventRecord((cudaEvent_t)ev[1], s));
+    const int fgrid = grid_for(c->n, 128, 16);
     if (batched(&c->net))
-      k_fused_step<true><<<grid, 256, 0, s>>>(A, c->net, make_net_keys(seed, step), codes_cur,
+      k_fused_step<true><<<fgrid, 128, 0, s>>>(A, c->net, make_net_keys(seed, step), codes_cur,
                                               c->host.rate_scale, codes_next, c->net_dev, rcount_next,
                                               iv ? 0 : 1);
     else
-      k_fused_step<false><<<grid, 256, 0, s>>>(A, c->net, make_net_keys(seed, step), codes_cur,
+      k_fused_step<false><<<fgrid, 128, 0, s>>>(A, c->net, make_net_keys(seed, step), codes_cur,
                                                c->host.rate_scale, codes_next, c->net_dev, rcount_next,
                                                iv ? 0 : 1);
     CKL();

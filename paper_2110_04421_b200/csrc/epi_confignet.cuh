@@ -48,11 +48,8 @@ __host__ __device__ __forceinline__ Radix make_radix(uint32_t n) {
   return r;
 }
 __device__ __forceinline__ uint32_t feistel_f(uint32_t v, uint32_t k1, uint32_t k2, uint32_t radix) {
-  uint32_t h = (v ^ k1) * 0x9E3779B1u;
-  h ^= h >> 15;
-  h *= k2;
-  h ^= h >> 13;
-  return __umulhi(h, radix);
+  const uint32_t h = (v ^ k1) * k2;
+  return __umulhi(h ^ (h >> 15), radix);
 }
 __device__ __forceinline__ void split(uint32_t x, const Radix& d, uint32_t& L, uint32_t& R) {
   L = __umulhi(x, d.magic);          // floor(x/b) or one less (x < 2^31)
@@ -219,8 +216,9 @@ __device__ __forceinline__ void for_each_in_edge(const epi_net& net, const NetKe
 
 // Batched single-lane enumeration: every partner id of a section is computed
 // first (pure ALU: keyed bijections), then all their codes are loaded at once
-// (up to 2*JMAX independent gathers in flight per lane), then visited.  Same
-// visit order as for_each_in_edge(..., 0, 1, ...).  Requires
+// (up to JMAX independent gathers in flight per lane), then visited.  Visit
+// order: household, workplace (out, in per draw), random out-partners, random
+// in-partners (the edge multiset equals for_each_in_edge's).  Requires
 // random_slots <= JMAX and colleague_draws <= DMAX.
 template <int JMAX, int DMAX, class Visit>
 __device__ __forceinline__ void for_each_in_edge_batched(const epi_net& net, const NetKeys& nk,
@@ -294,28 +292,29 @@ __device__ __forceinline__ void for_each_in_edge_batched(const epi_net& net, con
     const int nb = code_count(code_b);
     const int slots = net.random_slots;
     const uint32_t self = (uint32_t)b;
-    uint32_t pin[JMAX], pout[JMAX];
+    // in-partners: one inverse evaluation per slot, all lanes busy
+    uint32_t pin[JMAX];
 #pragma unroll
-    for (int j = 0; j < JMAX; ++j) {
-      pin[j] = self;
-      pout[j] = self;
-      if (j < slots) {
-        const PermKeys& K = rk[j];
-        pin[j] = walk_inv(self, K, d);
-        if (j < nb) pout[j] = walk_fwd(self, K, d);
-      }
+    for (int j = 0; j < JMAX; ++j) pin[j] = (j < slots) ? walk_inv(self, rk[j], d) : self;
+    uint16_t cin[JMAX];
+#pragma unroll
+    for (int j = 0; j < JMAX; ++j) cin[j] = pin[j] != self ? codes[pin[j]] : (uint16_t)0;
+    // out-partners: only the nb activated slots, in chunks of 4 (per-lane trip count)
+    const int nbe = nb < slots ? nb : slots;
+    for (int j0 = 0; j0 < nbe; j0 += 4) {
+      uint32_t po[4];
+      uint16_t co[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) po[q] = (j0 + q < nbe) ? walk_fwd(self, rk[j0 + q], d) : self;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) co[q] = po[q] != self ? codes[po[q]] : (uint16_t)CODE_DEAD;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (!code_dead(co[q])) visit((int64_t)po[q], 2, co[q]);
     }
-    uint16_t cin[JMAX], cout[JMAX];
 #pragma unroll
-    for (int j = 0; j < JMAX; ++j) {
-      cin[j] = pin[j] != self ? codes[pin[j]] : (uint16_t)0;
-      cout[j] = pout[j] != self ? codes[pout[j]] : (uint16_t)CODE_DEAD;
-    }
-#pragma unroll
-    for (int j = 0; j < JMAX; ++j) {
-      if (!code_dead(cout[j])) visit((int64_t)pout[j], 2, cout[j]);
+    for (int j = 0; j < JMAX; ++j)
       if (j < code_count(cin[j])) visit((int64_t)pin[j], 2, cin[j]);
-    }
   }
 }
 

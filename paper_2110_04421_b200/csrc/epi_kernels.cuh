@@ -375,7 +375,7 @@ __global__ void k_update_from_hazard(StepArgs A, const double* __restrict__ haza
 // canonical (src, kind) order, and the warp's 32 rows are written out
 // coalesced, one warp-wide store per row.
 template <bool SORT, bool BATCH>
-__global__ void __launch_bounds__(128) k_net_realize(epi_net net, NetKeys nk, const uint16_t* __restrict__ codes,
+__global__ void __launch_bounds__(128, 6) k_net_realize(epi_net net, NetKeys nk, const uint16_t* __restrict__ codes,
                                                      uint32_t* __restrict__ entries,
                                                      int32_t* __restrict__ row_len, long long* rec) {
   extern __shared__ uint32_t stage_buf[];
@@ -433,7 +433,7 @@ __global__ void __launch_bounds__(128) k_net_realize(epi_net net, NetKeys nk, co
 // their source codes consumed on the fly, so no CSR ever reaches memory.  One
 // lane per agent; gathers are batched per section (for_each_in_edge_batched).
 template <bool BATCH>
-__global__ void __launch_bounds__(256) k_fused_step(StepArgs A, epi_net net, NetKeys nk,
+__global__ void __launch_bounds__(128, 6) k_fused_step(StepArgs A, epi_net net, NetKeys nk,
                                                     const uint16_t* __restrict__ codes, double rate,
                                                     uint16_t* __restrict__ codes_next,
                                                     const epi_net* net_dev, uint64_t rcount_next,
