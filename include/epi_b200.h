@@ -153,6 +153,7 @@ typedef struct epi_net {
     int32_t colleague_draws;
     int32_t random_slots;
     int32_t row_cap;              /* padded CSR row capacity              */
+    int64_t n_member_slots;       /* length of wp_members                 */
     double poisson_cdf[EPI_MAX_SLOTS];
 } epi_net;
 

@@ -61,7 +61,7 @@ class EpiNet(C.Structure):
         ("n_agents", _i64), ("hh_off", _p), ("hh_size", _p), ("wp_id", _p), ("wp_local", _p),
         ("wp_base", _p), ("wp_size", _p), ("wp_members", _p), ("n_workplaces", _i32),
         ("colleague_draws", _i32), ("random_slots", _i32), ("row_cap", _i32),
-        ("poisson_cdf", _d * MAX_SLOTS),
+        ("n_member_slots", _i64), ("poisson_cdf", _d * MAX_SLOTS),
     ]
 
 

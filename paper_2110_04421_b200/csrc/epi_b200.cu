@@ -101,6 +101,8 @@ struct epi_ctx {
   std::vector<uint32_t*> net_entries;
   std::vector<int32_t*> net_rowlen;
   std::vector<int32_t> net_slot_step;
+  WorkTables wt_host{};              // device arrays, rebuilt each day
+  WorkTables* wt_dev = nullptr;
   Injected* inj_dev = nullptr;
 };
 
@@ -249,6 +251,10 @@ int epi_destroy(epi_ctx* c) {
   cudaFree(c->cub_tmp);
   cudaFree(c->net_dev);
   cudaFree(c->inj_dev);
+  cudaFree(c->wt_host.member_at_pos);
+  cudaFree(c->wt_host.pos_of);
+  cudaFree(c->wt_host.shift);
+  cudaFree(c->wt_dev);
   for (auto& s : c->ring) { cudaFree(s.src); cudaFree(s.dst); }
   for (auto* p : c->net_entries) cudaFree(p);
   for (auto* p : c->net_rowlen) cudaFree(p);
@@ -462,18 +468,18 @@ static int prepare_realize(const epi_net* net) {
 
 static int launch_realize(const epi_net* net, uint64_t g, int32_t step, const uint16_t* codes,
                           uint32_t* entries, int32_t* row_len, int sort_rows, long long* rec,
-                          cudaStream_t s) {
+                          const WorkTables* wt, cudaStream_t s) {
   const size_t smem = realize_smem(net);
   if (smem > g_realize_smem_set) return fail(EPI_EARG, "realize smem not prepared");
   NetKeys nk = make_net_keys(g, step);
   const int grid = grid_for(net->n_agents, 128, 16);
   const bool batch = batched(net);
   if (sort_rows) {
-    if (batch) k_net_realize<true, true><<<grid, 128, smem, s>>>(*net, nk, codes, entries, row_len, rec);
-    else k_net_realize<true, false><<<grid, 128, smem, s>>>(*net, nk, codes, entries, row_len, rec);
+    if (batch) k_net_realize<true, true><<<grid, 128, smem, s>>>(*net, nk, codes, entries, row_len, rec, wt);
+    else k_net_realize<true, false><<<grid, 128, smem, s>>>(*net, nk, codes, entries, row_len, rec, wt);
   } else {
-    if (batch) k_net_realize<false, true><<<grid, 128, smem, s>>>(*net, nk, codes, entries, row_len, rec);
-    else k_net_realize<false, false><<<grid, 128, smem, s>>>(*net, nk, codes, entries, row_len, rec);
+    if (batch) k_net_realize<false, true><<<grid, 128, smem, s>>>(*net, nk, codes, entries, row_len, rec, wt);
+    else k_net_realize<false, false><<<grid, 128, smem, s>>>(*net, nk, codes, entries, row_len, rec, wt);
   }
   CKL();
   return 0;
@@ -486,7 +492,8 @@ int epi_net_realize(const epi_net* net, uint64_t graph_seed, int32_t step, const
   if (!codes || !entries || !row_len) return fail(EPI_EARG, "null buffer");
   rc = prepare_realize(net);
   if (rc) return rc;
-  return launch_realize(net, graph_seed, step, codes, entries, row_len, sort_rows, nullptr, S(stream));
+  return launch_realize(net, graph_seed, step, codes, entries, row_len, sort_rows, nullptr, nullptr,
+                        S(stream));
 }
 
 int epi_net_attach(epi_ctx* c, const epi_net* net) {
@@ -512,6 +519,12 @@ int epi_net_attach(epi_ctx* c, const epi_net* net) {
     if (!rc) rc = dalloc(&c->net_rowlen[i], (size_t)c->n);
     if (rc) return rc;
   }
+  rc = dalloc(&c->wt_host.member_at_pos, (size_t)net->n_member_slots);
+  if (!rc) rc = dalloc(&c->wt_host.pos_of, (size_t)net->n_member_slots);
+  if (!rc) rc = dalloc(&c->wt_host.shift, (size_t)net->n_workplaces * (net->colleague_draws + 1));
+  if (rc) return rc;
+  if (!c->wt_dev) CK(cudaMalloc((void**)&c->wt_dev, sizeof(WorkTables)));
+  CK(cudaMemcpy(c->wt_dev, &c->wt_host, sizeof(WorkTables), cudaMemcpyHostToDevice));
   return 0;
 }
 
@@ -541,11 +554,18 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
   const int grid = grid_for(c->n, 256);
   const int slot = step % c->net_slots;
   if (ev) CK(cudaEventRecord((cudaEvent_t)ev[0], s));
+  const NetKeys nk = make_net_keys(seed, step);
+  const bool use_wt = c->net.n_member_slots > 0 && c->net.colleague_draws > 0 && batched(&c->net);
+  if (use_wt) {
+    k_work_tables<<<grid_for(c->net.n_member_slots, 256), 256, 0, s>>>(c->net, nk, c->wt_host);
+    CKL();
+  }
+  const WorkTables* wt = use_wt ? c->wt_dev : nullptr;
   if (mode == 0) {
     uint32_t* entries = c->net_entries[slot];
     int32_t* row_len = c->net_rowlen[slot];
     int rc = launch_realize(&c->net, seed, step, codes_cur, entries, row_len,
-                            precision == EPI_F64_CANONICAL, nullptr, s);
+                            precision == EPI_F64_CANONICAL, nullptr, wt, s);
     if (rc) return rc;
     c->net_slot_step[slot] = step;
     if (ev) CK(cudaEventRecord((cudaEvent_t)ev[1], s));
@@ -561,13 +581,11 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
     if (ev) CK(cudaEventRecord((cudaEvent_t)ev[1], s));
     const int fgrid = grid_for(c->n, 128, 16);
     if (batched(&c->net))
-      k_fused_step<true><<<fgrid, 128, 0, s>>>(A, c->net, make_net_keys(seed, step), codes_cur,
-                                              c->host.rate_scale, codes_next, c->net_dev, rcount_next,
-                                              iv ? 0 : 1);
+      k_fused_step<true><<<fgrid, 128, 0, s>>>(A, c->net, nk, codes_cur, c->host.rate_scale, codes_next,
+                                               c->net_dev, rcount_next, iv ? 0 : 1, wt);
     else
-      k_fused_step<false><<<fgrid, 128, 0, s>>>(A, c->net, make_net_keys(seed, step), codes_cur,
-                                               c->host.rate_scale, codes_next, c->net_dev, rcount_next,
-                                               iv ? 0 : 1);
+      k_fused_step<false><<<fgrid, 128, 0, s>>>(A, c->net, nk, codes_cur, c->host.rate_scale, codes_next,
+                                                c->net_dev, rcount_next, iv ? 0 : 1, nullptr);
     CKL();
   }
   if (ev) CK(cudaEventRecord((cudaEvent_t)ev[2], s));

@@ -134,6 +134,24 @@ __device__ __forceinline__ void build_net_tables(NetTables& T, const epi_net& ne
   for (int m = threadIdx.x; m < 256; m += blockDim.x) T.wrad[m] = make_radix(m < 1 ? 1u : (uint32_t)m);
 }
 
+// Per-day workplace tables (a cache of sigma_{t,W} and the shifts): built by
+// k_work_tables with one bijection evaluation per member slot, then read by
+// every worker instead of 1 + 2*draws evaluations each.
+//   member_at_pos[base_W + q] = wp_members[base_W + sigma(q)]
+//   pos_of[base_W + l]        = sigma^{-1}(l)
+//   shift[W * draws + j]      = r_{t,W,j}
+struct WorkTables {
+  int32_t* member_at_pos;
+  uint8_t* pos_of;
+  uint8_t* shift;
+};
+
+__device__ __forceinline__ uint32_t work_shift(uint64_t wshift_prefix, int w, int j, int m) {
+  const uint64_t hq = fold(fold(wshift_prefix, (uint64_t)w), (uint64_t)(j >> 2));
+  const uint32_t v = (uint32_t)((hq >> (16 * (j & 3))) & 0xFFFF);
+  return 1u + ((v * (uint32_t)(m - 1)) >> 16);
+}
+
 // Random-slot count n_{t,a} ~ Poisson(mean) truncated at `slots`.
 __device__ __forceinline__ int random_count(const epi_net& net, uint64_t rcount_prefix, int64_t a) {
   const double u = keyed_u(rcount_prefix, (uint64_t)a, 0);
@@ -224,6 +242,7 @@ template <int JMAX, int DMAX, class Visit>
 __device__ __forceinline__ void for_each_in_edge_batched(const epi_net& net, const NetKeys& nk,
                                                          const PermKeys* __restrict__ rk,
                                                          const Radix* __restrict__ wrad,
+                                                         const WorkTables* wt,
                                                          const uint16_t* __restrict__ codes,
                                                          int64_t b, uint16_t code_b, Visit&& visit) {
   // household: contiguous range, one cache line in practice
@@ -243,29 +262,38 @@ __device__ __forceinline__ void for_each_in_edge_batched(const epi_net& net, con
   if (w >= 0) {
     const int m = net.wp_size[w];
     if (m >= 2) {
-      const Radix d = wrad[m];
-      const PermKeys K = work_keys(nk.wperm, w);
       const int base = net.wp_base[w];
-      const uint32_t p = walk_inv(net.wp_local[b], K, d);
-      const uint64_t hw = fold(nk.wshift, (uint64_t)w);
       const int draws = net.colleague_draws;
       int32_t mo[DMAX], mi[DMAX];
-      uint64_t hq = 0;
+      if (wt != nullptr) {
+        const uint32_t p = wt->pos_of[base + net.wp_local[b]];
+        const uint8_t* sh = wt->shift + (size_t)w * draws;
 #pragma unroll
-      for (int j = 0; j < DMAX; ++j) {
-        if (j < draws) {
-          if ((j & 3) == 0) hq = fold(hw, (uint64_t)(j >> 2));
-          const uint32_t v = (uint32_t)((hq >> (16 * (j & 3))) & 0xFFFF);
-          const uint32_t r = 1u + ((v * (uint32_t)(m - 1)) >> 16);
-          mo[j] = base + (int32_t)walk_fwd(add_mod(p, r, (uint32_t)m), K, d);
-          mi[j] = base + (int32_t)walk_fwd(sub_mod(p, r, (uint32_t)m), K, d);
+        for (int j = 0; j < DMAX; ++j) {
+          if (j < draws) {
+            const uint32_t r = sh[j];
+            mo[j] = wt->member_at_pos[base + add_mod(p, r, (uint32_t)m)];
+            mi[j] = wt->member_at_pos[base + sub_mod(p, r, (uint32_t)m)];
+          }
         }
-      }
+      } else {
+        const Radix d = wrad[m];
+        const PermKeys K = work_keys(nk.wperm, w);
+        const uint32_t p = walk_inv(net.wp_local[b], K, d);
 #pragma unroll
-      for (int j = 0; j < DMAX; ++j) {
-        if (j < draws) {
-          mo[j] = net.wp_members[mo[j]];
-          mi[j] = net.wp_members[mi[j]];
+        for (int j = 0; j < DMAX; ++j) {
+          if (j < draws) {
+            const uint32_t r = work_shift(nk.wshift, w, j, m);
+            mo[j] = base + (int32_t)walk_fwd(add_mod(p, r, (uint32_t)m), K, d);
+            mi[j] = base + (int32_t)walk_fwd(sub_mod(p, r, (uint32_t)m), K, d);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < DMAX; ++j) {
+          if (j < draws) {
+            mo[j] = net.wp_members[mo[j]];
+            mi[j] = net.wp_members[mi[j]];
+          }
         }
       }
       uint16_t co[DMAX], ci[DMAX];
@@ -294,8 +322,13 @@ __device__ __forceinline__ void for_each_in_edge_batched(const epi_net& net, con
     const uint32_t self = (uint32_t)b;
     // in-partners: one inverse evaluation per slot, all lanes busy
     uint32_t pin[JMAX];
+    // straight-line first application for every slot (16 independent chains
+    // the scheduler can interleave), then the rare cycle-walk fix-ups
 #pragma unroll
-    for (int j = 0; j < JMAX; ++j) pin[j] = (j < slots) ? walk_inv(self, rk[j], d) : self;
+    for (int j = 0; j < JMAX; ++j) pin[j] = (j < slots) ? perm_inv(self, rk[j], d) : self;
+#pragma unroll
+    for (int j = 0; j < JMAX; ++j)
+      if (pin[j] >= d.n) pin[j] = walk_inv(pin[j], rk[j], d);
     uint16_t cin[JMAX];
 #pragma unroll
     for (int j = 0; j < JMAX; ++j) cin[j] = pin[j] != self ? codes[pin[j]] : (uint16_t)0;
@@ -305,7 +338,10 @@ __device__ __forceinline__ void for_each_in_edge_batched(const epi_net& net, con
       uint32_t po[4];
       uint16_t co[4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) po[q] = (j0 + q < nbe) ? walk_fwd(self, rk[j0 + q], d) : self;
+      for (int q = 0; q < 4; ++q) po[q] = (j0 + q < nbe) ? perm_fwd(self, rk[j0 + q], d) : self;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (po[q] >= d.n) po[q] = walk_fwd(po[q], rk[j0 + q], d);
 #pragma unroll
       for (int q = 0; q < 4; ++q) co[q] = po[q] != self ? codes[po[q]] : (uint16_t)CODE_DEAD;
 #pragma unroll

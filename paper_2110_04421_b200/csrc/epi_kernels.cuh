@@ -377,7 +377,8 @@ __global__ void k_update_from_hazard(StepArgs A, const double* __restrict__ haza
 template <bool SORT, bool BATCH>
 __global__ void __launch_bounds__(128, 6) k_net_realize(epi_net net, NetKeys nk, const uint16_t* __restrict__ codes,
                                                      uint32_t* __restrict__ entries,
-                                                     int32_t* __restrict__ row_len, long long* rec) {
+                                                     int32_t* __restrict__ row_len, long long* rec,
+                                                     const WorkTables* wt) {
   extern __shared__ uint32_t stage_buf[];
   __shared__ NetTables NT;
   __shared__ RecAcc racc;
@@ -401,7 +402,7 @@ __global__ void __launch_bounds__(128, 6) k_net_realize(epi_net net, NetKeys nk,
       const uint16_t cb = codes[b];
       if (!code_dead(cb)) {
         auto put = [&](int64_t c, int kind, uint16_t) { mine[cnt++] = ((uint32_t)c << 2) | (uint32_t)kind; };
-        if (BATCH) for_each_in_edge_batched<16, 8>(net, nk, NT.rk, NT.wrad, codes, b, cb, put);
+        if (BATCH) for_each_in_edge_batched<16, 8>(net, nk, NT.rk, NT.wrad, wt, codes, b, cb, put);
         else for_each_in_edge(net, nk, NT.rk, NT.wrad, codes, b, cb, 0, 1, put);
       }
       if (SORT) {
@@ -437,7 +438,7 @@ __global__ void __launch_bounds__(128, 6) k_fused_step(StepArgs A, epi_net net, 
                                                     const uint16_t* __restrict__ codes, double rate,
                                                     uint16_t* __restrict__ codes_next,
                                                     const epi_net* net_dev, uint64_t rcount_next,
-                                                    int final_pass) {
+                                                    int final_pass, const WorkTables* wt) {
   __shared__ MsgTables T;
   __shared__ NetTables NT;
   __shared__ RecAcc racc;
@@ -460,7 +461,7 @@ __global__ void __launch_bounds__(128, 6) k_fused_step(StepArgs A, epi_net net, 
           ++edges;
           acc += T.factor[cc & 0xFF] * T.bfac[kind];
         };
-        if (BATCH) for_each_in_edge_batched<16, 8>(net, nk, NT.rk, NT.wrad, codes, b, cb, add);
+        if (BATCH) for_each_in_edge_batched<16, 8>(net, nk, NT.rk, NT.wrad, wt, codes, b, cb, add);
         else for_each_in_edge(net, nk, NT.rk, NT.wrad, codes, b, cb, 0, 1, add);
         if (is_target(A.P, A.st, b)) lam = (double)(acc * T.sfac[A.st.age_band[b]]);
       }
@@ -477,6 +478,32 @@ __global__ void __launch_bounds__(128, 6) k_fused_step(StepArgs A, epi_net net, 
   }
   __syncthreads();
   rec_flush(racc, A.rec, A.step);
+}
+
+// Per-day workplace tables: one thread per member slot.
+__global__ void k_work_tables(epi_net net, NetKeys nk, WorkTables wt) {
+  __shared__ Radix wrad[256];
+  for (int m = threadIdx.x; m < 256; m += blockDim.x) wrad[m] = make_radix(m < 1 ? 1u : (uint32_t)m);
+  __syncthreads();
+  const int draws = net.colleague_draws;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < net.n_member_slots;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t c = net.wp_members[i];
+    const int w = net.wp_id[c];
+    const int base = net.wp_base[w];
+    const int m = net.wp_size[w];
+    const uint32_t q = (uint32_t)(i - base);
+    if (m >= 2) {
+      const PermKeys K = work_keys(nk.wperm, w);
+      const uint32_t loc = walk_fwd(q, K, wrad[m]);
+      wt.member_at_pos[i] = net.wp_members[base + loc];
+      wt.pos_of[base + loc] = (uint8_t)q;
+      for (int j = (int)q; j < draws; j += m) wt.shift[(size_t)w * draws + j] = (uint8_t)work_shift(nk.wshift, w, j, m);
+    } else {
+      wt.member_at_pos[i] = c;
+      wt.pos_of[i] = 0;
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------

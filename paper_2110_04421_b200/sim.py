@@ -60,6 +60,7 @@ class DeviceNetwork:
         s.colleague_draws = spec.colleague_draws
         s.random_slots = spec.random_slots
         s.row_cap = spec.row_capacity
+        s.n_member_slots = len(pop.wp_members)
         tab = pop.poisson_table()
         s.poisson_cdf[:len(tab)] = tab.tolist()
         self.struct = s
