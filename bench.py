@@ -276,6 +276,12 @@ def run_ours(a):
     roof["peak"] = peak
     roof["frac"] = roof["achieved"] / peak
     roof["peak_source"] = "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s"
+    tfile = ROOT / "profiles" / "r01_traffic.json"
+    if tfile.exists():
+        tr = json.loads(tfile.read_text()).get(roof["kernel"])
+        if tr:
+            roof["traffic"] = tr["dram_bytes_read"] + tr["dram_bytes_write"]
+            roof["traffic_source"] = tr["source"]
 
     if rank != 0:
         return
