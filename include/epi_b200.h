@@ -163,6 +163,9 @@ typedef struct epi_ctx epi_ctx;
 int epi_create(const epi_params *params, int64_t n_agents, epi_ctx **out);
 int epi_destroy(epi_ctx *ctx);
 int epi_set_params(epi_ctx *ctx, const epi_params *params);
+/* Restrict the config-simulation kernels to the owned agent rows [lo, hi)
+ * (agent-range partition; state/code buffers stay globally indexed). */
+int epi_set_rows(epi_ctx *ctx, int64_t lo, int64_t hi);
 const char *epi_last_error(void);
 int epi_version(void);
 /* sizeof of the ABI structs (0 params, 1 state, 2 net) for binding checks */

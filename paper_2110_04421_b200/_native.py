@@ -69,6 +69,7 @@ _SIGS = {
     "epi_create": (_i32, [C.POINTER(EpiParams), _i64, C.POINTER(_p)]),
     "epi_destroy": (_i32, [_p]),
     "epi_set_params": (_i32, [_p, C.POINTER(EpiParams)]),
+    "epi_set_rows": (_i32, [_p, _i64, _i64]),
     "epi_last_error": (C.c_char_p, []),
     "epi_version": (_i32, []),
     "epi_struct_size": (_i64, [_i32]),

@@ -72,6 +72,7 @@ struct epi_ctx {
   epi_params host{};
   epi_params* P = nullptr;           // device copy
   int64_t n = 0;
+  int64_t lo = 0, hi = 0;            // owned rows (agent-range partition)
   uint8_t* flags = nullptr;          // n rounded up to 4
   uint8_t* bucket = nullptr;
   unsigned long long* hist = nullptr;
@@ -129,6 +130,8 @@ StepArgs make_args(epi_ctx* c, const epi_state* st, int step, uint64_t seed, lon
   A.inj = inj;
   A.rec = rec;
   A.flags = with_flags ? c->flags : nullptr;
+  A.lo = c->lo;
+  A.hi = c->hi;
   return A;
 }
 
@@ -207,6 +210,8 @@ int epi_create(const epi_params* params, int64_t n_agents, epi_ctx** out) {
   if (n_agents < 1 || n_agents >= (1ll << 30)) return fail(EPI_EARG, "n_agents must be in [1, 2^30)");
   epi_ctx* c = new epi_ctx();
   c->n = n_agents;
+  c->lo = 0;
+  c->hi = n_agents;
   int rc = upload_params(c, params);
   const int64_t n4 = (n_agents + 3) / 4 * 4;
   const int64_t tiles = (n_agents + VAX_TILE - 1) / VAX_TILE;
@@ -259,6 +264,13 @@ int epi_destroy(epi_ctx* c) {
   for (auto* p : c->net_entries) cudaFree(p);
   for (auto* p : c->net_rowlen) cudaFree(p);
   delete c;
+  return 0;
+}
+
+int epi_set_rows(epi_ctx* c, int64_t lo, int64_t hi) {
+  if (!c || lo < 0 || hi > c->n || lo >= hi) return fail(EPI_EARG, "row range outside [0, n_agents)");
+  c->lo = lo;
+  c->hi = hi;
   return 0;
 }
 
@@ -329,7 +341,7 @@ int epi_gather(epi_ctx* c, const epi_state* st, int32_t step, int32_t precision,
   if (!c || !st || !lam_out) return fail(EPI_EARG, "null argument");
   if (st->n_agents != c->n) return fail(EPI_EARG, "state size differs from context");
   cudaStream_t s = S(stream);
-  k_codes<<<grid_for(c->n, 256), 256, 0, s>>>(c->P, *st, step, nullptr, 0, c->codes);
+  k_codes<<<grid_for(c->n, 256), 256, 0, s>>>(c->P, *st, step, nullptr, 0, c->codes, 0, c->n);
   CKL();
   StepArgs A = make_args(c, st, step, 0, c->scratch_rec, nullptr, false);
   CsrView g{c->entries, c->row_len, c->row_begin, 0};
@@ -384,7 +396,7 @@ static int step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t see
   if (hazard) {
     k_update_from_hazard<<<grid, 256, 0, s>>>(A, hazard, iv ? 0 : 1);
   } else {
-    k_codes<<<grid, 256, 0, s>>>(c->P, *st, step, nullptr, 0, c->codes);
+    k_codes<<<grid, 256, 0, s>>>(c->P, *st, step, nullptr, 0, c->codes, 0, c->n);
     CKL();
     CsrView g{c->entries, c->row_len, c->row_begin, 0};
     k_pass<true, 1><<<grid, 256, 0, s>>>(A, g, c->codes, nullptr, c->host.rate_scale, iv ? 0 : 1,
@@ -432,8 +444,8 @@ int epi_codes(epi_ctx* c, const epi_state* st, const epi_net* net, uint64_t grap
     if (!c->has_net) return fail(EPI_EARG, "epi_codes with a network needs epi_net_attach first");
     nd = c->net_dev;
   }
-  k_codes<<<grid_for(c->n, 256), 256, 0, S(stream)>>>(c->P, *st, step, nd,
-                                                      key_prefix(graph_seed, step, P_NET_RCOUNT), codes_out);
+  k_codes<<<grid_for(c->hi - c->lo, 256), 256, 0, S(stream)>>>(
+      c->P, *st, step, nd, key_prefix(graph_seed, step, P_NET_RCOUNT), codes_out, c->lo, c->hi);
   CKL();
   return 0;
 }
@@ -468,18 +480,18 @@ static int prepare_realize(const epi_net* net) {
 
 static int launch_realize(const epi_net* net, uint64_t g, int32_t step, const uint16_t* codes,
                           uint32_t* entries, int32_t* row_len, int sort_rows, long long* rec,
-                          const WorkTables* wt, cudaStream_t s) {
+                          const WorkTables* wt, int64_t lo, int64_t hi, cudaStream_t s) {
   const size_t smem = realize_smem(net);
   if (smem > g_realize_smem_set) return fail(EPI_EARG, "realize smem not prepared");
   NetKeys nk = make_net_keys(g, step);
-  const int grid = grid_for(net->n_agents, 128, 16);
+  const int grid = grid_for(hi - lo, 128, 16);
   const bool batch = batched(net);
   if (sort_rows) {
-    if (batch) k_net_realize<true, true><<<grid, 128, smem, s>>>(*net, nk, codes, entries, row_len, rec, wt);
-    else k_net_realize<true, false><<<grid, 128, smem, s>>>(*net, nk, codes, entries, row_len, rec, wt);
+    if (batch) k_net_realize<true, true><<<grid, 128, smem, s>>>(*net, nk, codes, entries, row_len, rec, wt, lo, hi);
+    else k_net_realize<true, false><<<grid, 128, smem, s>>>(*net, nk, codes, entries, row_len, rec, wt, lo, hi);
   } else {
-    if (batch) k_net_realize<false, true><<<grid, 128, smem, s>>>(*net, nk, codes, entries, row_len, rec, wt);
-    else k_net_realize<false, false><<<grid, 128, smem, s>>>(*net, nk, codes, entries, row_len, rec, wt);
+    if (batch) k_net_realize<false, true><<<grid, 128, smem, s>>>(*net, nk, codes, entries, row_len, rec, wt, lo, hi);
+    else k_net_realize<false, false><<<grid, 128, smem, s>>>(*net, nk, codes, entries, row_len, rec, wt, lo, hi);
   }
   CKL();
   return 0;
@@ -493,7 +505,7 @@ int epi_net_realize(const epi_net* net, uint64_t graph_seed, int32_t step, const
   rc = prepare_realize(net);
   if (rc) return rc;
   return launch_realize(net, graph_seed, step, codes, entries, row_len, sort_rows, nullptr, nullptr,
-                        S(stream));
+                        0, net->n_agents, S(stream));
 }
 
 int epi_net_attach(epi_ctx* c, const epi_net* net) {
@@ -544,6 +556,9 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
   if (!c->has_net) return fail(EPI_EARG, "epi_sim_step needs epi_net_attach first");
   if (st->n_agents != c->n) return fail(EPI_EARG, "state size differs from context");
   const bool iv = interventions_on(c->host);
+  if ((c->lo != 0 || c->hi != c->n) && (c->host.den_enabled || c->host.vaccination_enabled))
+    return fail(EPI_EARG, "exposure notification and vaccination need the whole population "
+                          "(partitioned runs support quarantine and testing only)");
   if (mode == 1 && c->host.den_enabled) return fail(EPI_EARG, "fused mode keeps no contact log; use mode 0 with DEN");
   if (mode == 1 && precision != EPI_F32) return fail(EPI_EARG, "fused mode is fp32 only");
   cudaStream_t s = S(stream);
@@ -551,7 +566,7 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
   CK(cudaMemsetAsync(rec, 0, EPI_REC_LEN * sizeof(long long), s));
   StepArgs A = make_args(c, st, step, seed, rec, nullptr, iv);
   const uint64_t rcount_next = key_prefix(seed, step + 1, P_NET_RCOUNT);
-  const int grid = grid_for(c->n, 256);
+  const int grid = grid_for(c->hi - c->lo, 256);
   const int slot = step % c->net_slots;
   if (ev) CK(cudaEventRecord((cudaEvent_t)ev[0], s));
   const NetKeys nk = make_net_keys(seed, step);
@@ -565,7 +580,7 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
     uint32_t* entries = c->net_entries[slot];
     int32_t* row_len = c->net_rowlen[slot];
     int rc = launch_realize(&c->net, seed, step, codes_cur, entries, row_len,
-                            precision == EPI_F64_CANONICAL, nullptr, wt, s);
+                            precision == EPI_F64_CANONICAL, nullptr, wt, c->lo, c->hi, s);
     if (rc) return rc;
     c->net_slot_step[slot] = step;
     if (ev) CK(cudaEventRecord((cudaEvent_t)ev[1], s));
@@ -579,7 +594,7 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
     CKL();
   } else {
     if (ev) CK(cudaEventRecord((cudaEvent_t)ev[1], s));
-    const int fgrid = grid_for(c->n, 128, 16);
+    const int fgrid = grid_for(c->hi - c->lo, 128, 16);
     if (batched(&c->net))
       k_fused_step<true><<<fgrid, 128, 0, s>>>(A, c->net, nk, codes_cur, c->host.rate_scale, codes_next,
                                                c->net_dev, rcount_next, iv ? 0 : 1, wt);

@@ -70,6 +70,7 @@ struct StepArgs {
   const Injected* inj;        // device pointer or null
   long long* rec;             // EPI_REC_LEN
   uint8_t* flags;             // per agent scratch
+  int64_t lo, hi;             // owned agent rows [lo, hi) (partitioned runs)
 };
 
 // Shared tables for the fp32 message: factor[t | asym<<7] = rate*A*w[t],
@@ -178,9 +179,9 @@ __device__ __forceinline__ uint16_t next_code(const epi_params* __restrict__ P, 
 // ---------------------------------------------------------------------------
 // Codes from state (graph-in gather, and step 0 of a config simulation).
 __global__ void k_codes(const epi_params* __restrict__ P, epi_state st, int step, const epi_net* net,
-                        uint64_t rcount_prefix, uint16_t* __restrict__ codes) {
-  const int64_t n = st.n_agents;
-  for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < n;
+                        uint64_t rcount_prefix, uint16_t* __restrict__ codes, int64_t lo, int64_t hi) {
+  const int64_t n = hi;
+  for (int64_t a = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < n;
        a += (int64_t)gridDim.x * blockDim.x)
     codes[a] = next_code(P, st, a, step, net, rcount_prefix);
 }
@@ -257,13 +258,13 @@ __global__ void __launch_bounds__(256) k_pass(StepArgs A, CsrView g, const uint1
   rec_init(racc);
   __syncthreads();
   const epi_params* __restrict__ P = A.P;
-  const int64_t n = A.st.n_agents;
+  const int64_t n = A.hi;
   const int warp = threadIdx.x >> 5, lane = lane_id();
-  const int64_t n_tiles = (n + 31) / 32;
+  const int64_t n_tiles = (n - A.lo + 31) / 32;
   const int64_t warps_total = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t tile = blockIdx.x * (int64_t)(blockDim.x >> 5) + warp; tile < n_tiles;
        tile += warps_total) {
-    const int64_t base = tile * 32;
+    const int64_t base = A.lo + tile * 32;
     const int64_t a = base + lane;
     const bool valid = a < n;
     double lam = 0.0;
@@ -350,9 +351,9 @@ __global__ void k_update_from_hazard(StepArgs A, const double* __restrict__ haza
   __shared__ RecAcc racc;
   rec_init(racc);
   __syncthreads();
-  const int64_t n = A.st.n_agents;
+  const int64_t n = A.hi;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n; base += stride) {
+  for (int64_t base = A.lo + blockIdx.x * (int64_t)blockDim.x; base < n; base += stride) {
     const int64_t a = base + threadIdx.x;
     const bool valid = a < n;
     unsigned ev = 0;
@@ -378,7 +379,7 @@ template <bool SORT, bool BATCH>
 __global__ void __launch_bounds__(128, 6) k_net_realize(epi_net net, NetKeys nk, const uint16_t* __restrict__ codes,
                                                      uint32_t* __restrict__ entries,
                                                      int32_t* __restrict__ row_len, long long* rec,
-                                                     const WorkTables* wt) {
+                                                     const WorkTables* wt, int64_t lo, int64_t hi) {
   extern __shared__ uint32_t stage_buf[];
   __shared__ NetTables NT;
   __shared__ RecAcc racc;
@@ -390,12 +391,12 @@ __global__ void __launch_bounds__(128, 6) k_net_realize(epi_net net, NetKeys nk,
   const int warp = threadIdx.x >> 5, lane = lane_id();
   uint32_t* mine = stage_buf + (size_t)(warp * 32 + lane) * stride_w;
   uint32_t* wbuf = stage_buf + (size_t)warp * 32 * stride_w;
-  const int64_t n = net.n_agents;
-  const int64_t n_tiles = (n + 31) / 32;
+  const int64_t n = hi;
+  const int64_t n_tiles = (n - lo + 31) / 32;
   const int64_t warps_total = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t tile = blockIdx.x * (int64_t)(blockDim.x >> 5) + warp; tile < n_tiles;
        tile += warps_total) {
-    const int64_t base = tile * 32;
+    const int64_t base = lo + tile * 32;
     const int64_t b = base + lane;
     int cnt = 0;
     if (b < n) {
@@ -446,9 +447,9 @@ __global__ void __launch_bounds__(128, 6) k_fused_step(StepArgs A, epi_net net, 
   build_net_tables(NT, net, nk.rperm);
   rec_init(racc);
   __syncthreads();
-  const int64_t n = A.st.n_agents;
+  const int64_t n = A.hi;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n; base += stride) {
+  for (int64_t base = A.lo + blockIdx.x * (int64_t)blockDim.x; base < n; base += stride) {
     const int64_t b = base + threadIdx.x;
     const bool valid = b < n;
     unsigned edges = 0;
@@ -517,9 +518,9 @@ __global__ void k_iv_tests(StepArgs A) {
   const epi_params* __restrict__ P = A.P;
   const epi_state& st = A.st;
   const int step = A.step;
-  const int64_t n = st.n_agents;
+  const int64_t n = A.hi;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n; base += stride) {
+  for (int64_t base = A.lo + blockIdx.x * (int64_t)blockDim.x; base < n; base += stride) {
     const int64_t a = base + threadIdx.x;
     unsigned tested = 0;
     if (a < n) {
@@ -613,9 +614,9 @@ __global__ void k_iv_post(StepArgs A, uint8_t* __restrict__ bucket, unsigned lon
   const epi_params* __restrict__ P = A.P;
   const epi_state& st = A.st;
   const int step = A.step;
-  const int64_t n = st.n_agents;
+  const int64_t n = A.hi;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n; base += stride) {
+  for (int64_t base = A.lo + blockIdx.x * (int64_t)blockDim.x; base < n; base += stride) {
     const int64_t a = base + threadIdx.x;
     unsigned notified = 0, active = 0;
     if (a < n) {
@@ -768,9 +769,9 @@ __global__ void k_finish(StepArgs A, uint16_t* __restrict__ codes_next, const ep
   __shared__ RecAcc racc;
   rec_init(racc);
   __syncthreads();
-  const int64_t n = A.st.n_agents;
+  const int64_t n = A.hi;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t base = blockIdx.x * (int64_t)blockDim.x; base < n; base += stride) {
+  for (int64_t base = A.lo + blockIdx.x * (int64_t)blockDim.x; base < n; base += stride) {
     const int64_t a = base + threadIdx.x;
     const bool valid = a < n;
     rec_agent(racc, valid, valid ? A.st.stage[a] : 0, valid ? A.st.infected_at[a] : 0);

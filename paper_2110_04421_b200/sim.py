@@ -101,13 +101,21 @@ class ConfigSimulation:
         N.check(self._lib.epi_create(ctypes.byref(self._params), self.n, ctypes.byref(ctx)))
         self._ctx = ctx
         N.check(self._lib.epi_net_attach(self._ctx, ctypes.byref(self.net.struct)))
+        self._after_attach()
         self.state = DeviceColumns(self.n, self.device)
-        self.codes = [torch.zeros(self.n, dtype=torch.int16, device=self.device) for _ in range(2)]
+        self.codes = self._alloc_codes()
         self.rec = torch.zeros((horizon, N.REC_LEN), dtype=torch.int64, device=self.device)
         self.vax = torch.zeros(1, dtype=torch.int32, device=self.device)
         self.initial = initial if initial is not None else self._seeded_initial()
         self.reset()
         self._graph = None
+
+    def _alloc_codes(self):
+        import torch
+        return [torch.zeros(self.n, dtype=torch.int16, device=self.device) for _ in range(2)]
+
+    def _after_attach(self):
+        pass
 
     @classmethod
     def create(cls, spec: ConfigNetworkSpec, seed: int, disease=None, table=None,

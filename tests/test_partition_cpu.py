@@ -1,0 +1,72 @@
+"""Host-side logic of the agent-range partition, multi-process on CPU (gloo)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2110_04421_b200 import _native as N
+from paper_2110_04421_b200.errors import ConfigError
+from paper_2110_04421_b200.partition import NcclCodeExchange, PartitionPlan
+
+
+def test_plan_rows_cover_population_once():
+    for n, w in [(10, 1), (10, 3), (100_000, 8), (7, 7), (10_000_000, 8)]:
+        plan = PartitionPlan(n, w)
+        rows = [plan.rows(r) for r in range(w)]
+        assert rows[0][0] == 0 and rows[-1][1] == n
+        assert all(a[1] == b[0] for a, b in zip(rows, rows[1:]))
+        assert plan.padded >= n and plan.padded % w == 0
+    with pytest.raises(ConfigError):
+        PartitionPlan(3, 4)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, n, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    plan = PartitionPlan(n, world)
+    ex = NcclCodeExchange(plan, rank)
+    codes = torch.zeros(plan.padded, dtype=torch.int16)
+    lo, hi = plan.rows(rank)
+    codes[lo:hi] = torch.arange(lo, hi, dtype=torch.int16) * 3 + 1   # this rank's rows
+    ex.exchange(codes)
+    rec = torch.zeros((4, N.REC_LEN), dtype=torch.int64)
+    rec[:, N.REC["step"]] = torch.arange(4)
+    rec[:, N.REC["edges"]] = 10 * (rank + 1)
+    rec[:, N.REC["flags"]] = rank
+    ex.reduce_records(rec)
+    q.put((rank, codes.numpy().copy(), rec.numpy().copy()))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n", [10, 1001])
+def test_code_exchange_and_record_reduction_gloo_world2(n):
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, n, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=60) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = (np.arange(n, dtype=np.int16) * 3 + 1)
+    for rank, codes, rec in out:
+        assert np.array_equal(codes[:n], want)
+        assert np.array_equal(rec[:, N.REC["step"]], np.arange(4))
+        assert np.all(rec[:, N.REC["edges"]] == 30)
+        assert np.all(rec[:, N.REC["flags"]] == 1)
