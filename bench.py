@@ -42,7 +42,10 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--mode", choices=["csr", "fused", "auto"], default="auto")
-    ap.add_argument("--workload", choices=["config1", "config0"], default="config1")
+    ap.add_argument("--workload", choices=["config1", "config0", "config3", "config4"],
+                    default="config1")
+    ap.add_argument("--replicas", type=int, default=128, help="config4: replicas per GPU")
+    ap.add_argument("--streams", type=int, default=8, help="config4: concurrent streams")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
@@ -50,7 +53,7 @@ def parse():
 
 def workload_spec(name):
     from paper_2110_04421_b200.confignet import ConfigNetworkSpec
-    return ConfigNetworkSpec.config(1 if name == "config1" else 0)
+    return ConfigNetworkSpec.config({"config0": 0, "config1": 1, "config3": 3, "config4": 4}[name])
 
 
 def dist_env():
@@ -351,19 +354,19 @@ def kernel_profile(sim, mode):
         # K12 message pass + update: SURVEY §8(d) B_K1 = 4E + 10N (+16N state r/w)
         b_gen = 4 * E + 6 * n
         b_pass = 4 * E + 10 * n + 16 * n
-        kernels["k_work_tables+k_net_realize"] = {"ms_per_launch": sum(gen) / len(gen),
+        kernels["k_day_tables+k_net_realize"] = {"ms_per_launch": sum(gen) / len(gen),
                                     "share": sum(gen) / total_ms,
                                     "alg_GBps": float(np.sum(b_gen) / (sum(gen) / 1e3) / 1e9)}
         kernels["k_pass_update"] = {"ms_per_launch": sum(pas) / len(pas),
                                     "share": sum(pas) / total_ms,
                                     "alg_GBps": float(np.sum(b_pass) / (sum(pas) / 1e3) / 1e9)}
-        dom = "k_pass_update" if sum(pas) >= sum(gen) else "k_work_tables+k_net_realize"
+        dom = "k_pass_update" if sum(pas) >= sum(gen) else "k_day_tables+k_net_realize"
         byt = b_pass if dom == "k_pass_update" else b_gen
         ms = pas if dom == "k_pass_update" else gen
         launches = 3
     else:
         b = 16 * n + 2 * n + 2 * E       # state r/w + own code + gathered codes (L2)
-        kernels["k_work_tables"] = {"ms_per_launch": sum(gen) / len(gen), "share": sum(gen) / total_ms}
+        kernels["k_day_tables"] = {"ms_per_launch": sum(gen) / len(gen), "share": sum(gen) / total_ms}
         kernels["k_fused_step"] = {"ms_per_launch": sum(pas) / len(pas), "share": sum(pas) / total_ms,
                                    "alg_GBps": float(np.sum(b) / (sum(pas) / 1e3) / 1e9)}
         dom, byt, ms, launches = "k_fused_step", b, pas, 2
@@ -412,10 +415,160 @@ def end_to_end(sim, a):
             "ms_per_step": ms, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
 
 
+def run_config3(a):
+    """10M agents, agent-range partition over the ranks (NCCL code all-gather)."""
+    import torch
+    from paper_2110_04421_b200 import _native as N
+    from paper_2110_04421_b200.confignet import synthesize
+    from paper_2110_04421_b200.defaults import default_disease, default_progression
+    from paper_2110_04421_b200.interventions import InterventionConfig
+    from paper_2110_04421_b200.keyed import replication_seed
+    from paper_2110_04421_b200.partition import (NcclCodeExchange, PartitionedSimulation,
+                                                 PartitionPlan)
+    from paper_2110_04421_b200.sim import ConfigSimulation
+    rank, local_rank, world = dist_env()
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    spec = workload_spec("config3")
+    pop = synthesize(spec, 0)
+    d, t, iv = default_disease(), default_progression(), InterventionConfig()
+    seed = replication_seed(0, 0)
+    if world > 1:
+        plan = PartitionPlan(spec.n_agents, world)
+        sim = PartitionedSimulation(pop, d, t, iv, seed, plan, rank,
+                                    NcclCodeExchange(plan, rank), mode="fused", horizon=HORIZON)
+    else:
+        sim = ConfigSimulation(pop, d, t, iv, seed, mode="fused", horizon=HORIZON)
+    for _ in range(a.warmup):
+        sim.reset()
+        sim.run()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clk = ClockSampler(local_rank)
+    st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    st.record()
+    edges = 0
+    for _ in range(a.steps):
+        sim.reset()
+        sim.run()
+    en.record()
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    ms = st.elapsed_time(en)
+    rec = sim.rec.clone()
+    if dist:
+        NcclCodeExchange(plan, rank).reduce_records(rec)
+        tt = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    edges = float(rec[:, N.REC["edges"]].sum().item()) * a.steps
+    if rank == 0:
+        print(json.dumps({
+            "metric": "agent-interactions/sec", "value": edges / (ms / 1e3),
+            "unit": "agent-interactions/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "config3 (BASELINE.json configs[3]): 10M agents, config-1 "
+                       "networks, 180 days, fused mode", "parallelism": f"agent ranges x{world}, "
+                       "NCCL all-gather of 16-bit codes per day" if world > 1 else "1 GPU",
+                       "l2": "inputs (10M-agent state, 20 MB codes) exceed nothing; L2 not flushed "
+                       "between days"},
+            "wall_s_per_sim": ms / a.steps / 1e3, "clocks": clocks}), flush=True)
+
+
+def run_config4(a):
+    """Ensemble: R replicas per GPU of config 1, own seeds and rate scales,
+    CUDA graphs replayed on concurrent streams; no inter-GPU communication."""
+    import torch
+    from paper_2110_04421_b200 import _native as N
+    from paper_2110_04421_b200 import keyed
+    from paper_2110_04421_b200.confignet import synthesize
+    from paper_2110_04421_b200.defaults import default_disease, default_progression
+    from paper_2110_04421_b200.interventions import InterventionConfig
+    from paper_2110_04421_b200.sim import ConfigSimulation
+    rank, local_rank, world = dist_env()
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    spec = workload_spec("config4")
+    pop = synthesize(spec, 0)
+    d0, t, iv = default_disease(), default_progression(), InterventionConfig()
+    sims = []
+    for i in range(a.replicas):
+        r = rank * a.replicas + i
+        u = keyed.uniform(0, 0, keyed.Purpose.REPLICATION, r, k=1)
+        d = d0.with_rate(d0.rate_scale * (0.5 + u))
+        sims.append(ConfigSimulation(pop, d, t, iv, keyed.replication_seed(0, r), mode="fused",
+                                     horizon=HORIZON))
+    streams = [torch.cuda.Stream() for _ in range(a.streams)]
+    for s in sims:
+        s.capture()
+    torch.cuda.synchronize()
+
+    def sweep():
+        for i, s in enumerate(sims):
+            with torch.cuda.stream(streams[i % len(streams)]):
+                s._graph.replay()
+        for st_ in streams:
+            torch.cuda.current_stream().wait_stream(st_)
+    for _ in range(a.warmup):
+        sweep()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clk = ClockSampler(local_rank)
+    st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    st.record()
+    for _ in range(a.steps):
+        sweep()
+    en.record()
+    torch.cuda.synchronize()
+    clocks = clk.stop()
+    ms = st.elapsed_time(en)
+    recs = torch.stack([s.rec for s in sims])                     # [R, days, 24]
+    edges = float(recs[:, :, N.REC["edges"]].sum().item()) * a.steps
+    new_inf = recs[:, :, N.REC["new_inf"]].double()
+    if dist:
+        tt = torch.tensor([ms, edges], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt[:1], op=dist.ReduceOp.MAX)
+        dist.all_reduce(tt[1:])
+        ms, edges = float(tt[0]), float(tt[1])
+        allc = [torch.empty_like(new_inf) for _ in range(world)]
+        dist.all_gather(allc, new_inf)
+        new_inf = torch.cat(allc)
+    reps = a.replicas * world
+    if rank == 0:
+        mean = new_inf.mean(0).cpu().numpy()
+        std = new_inf.std(0).cpu().numpy()
+        print(json.dumps({
+            "metric": "agent-interactions/sec", "value": edges / (ms / 1e3),
+            "unit": "agent-interactions/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"config4 (BASELINE.json configs[4]): {reps} replicas of config 1 "
+                       "(shared static population, own seed, rate 3.3x[0.5,1.5]); one step = all "
+                       "replicas x 180 days", "parallelism": f"{a.replicas} replicas/GPU on "
+                       f"{a.streams} streams x {world} GPUs"},
+            "replica_steps_per_s": reps * HORIZON * a.steps / (ms / 1e3),
+            "daily_new_infections_mean": [round(float(x), 2) for x in mean],
+            "daily_new_infections_std": [round(float(x), 2) for x in std],
+            "clocks": clocks}), flush=True)
+
+
 def main():
     a = parse()
     if a.impl == "reference":
         run_reference(a)
+    elif a.workload == "config3":
+        run_config3(a)
+    elif a.workload == "config4":
+        run_config4(a)
     else:
         run_ours(a)
 

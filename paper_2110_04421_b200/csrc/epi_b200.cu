@@ -104,6 +104,7 @@ struct epi_ctx {
   std::vector<int32_t> net_slot_step;
   WorkTables wt_host{};              // device arrays, rebuilt each day
   WorkTables* wt_dev = nullptr;
+  int wt_whole = -1;                 // which variant wt_dev currently holds
   Injected* inj_dev = nullptr;
 };
 
@@ -259,6 +260,8 @@ int epi_destroy(epi_ctx* c) {
   cudaFree(c->wt_host.member_at_pos);
   cudaFree(c->wt_host.pos_of);
   cudaFree(c->wt_host.shift);
+  cudaFree(c->wt_host.rout);
+  cudaFree(c->wt_host.rin);
   cudaFree(c->wt_dev);
   for (auto& s : c->ring) { cudaFree(s.src); cudaFree(s.dst); }
   for (auto* p : c->net_entries) cudaFree(p);
@@ -534,9 +537,13 @@ int epi_net_attach(epi_ctx* c, const epi_net* net) {
   rc = dalloc(&c->wt_host.member_at_pos, (size_t)net->n_member_slots);
   if (!rc) rc = dalloc(&c->wt_host.pos_of, (size_t)net->n_member_slots);
   if (!rc) rc = dalloc(&c->wt_host.shift, (size_t)net->n_workplaces * (net->colleague_draws + 1));
+  if (!rc) rc = dalloc(&c->wt_host.rout, (size_t)c->n * RT_SLOTS);
+  if (!rc) rc = dalloc(&c->wt_host.rin, (size_t)c->n * RT_SLOTS);
   if (rc) return rc;
+  CK(cudaMemset(c->wt_host.rin, 0, (size_t)c->n * RT_SLOTS * sizeof(uint32_t)));
   if (!c->wt_dev) CK(cudaMalloc((void**)&c->wt_dev, sizeof(WorkTables)));
   CK(cudaMemcpy(c->wt_dev, &c->wt_host, sizeof(WorkTables), cudaMemcpyHostToDevice));
+  c->wt_whole = 1;
   return 0;
 }
 
@@ -570,9 +577,24 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
   const int slot = step % c->net_slots;
   if (ev) CK(cudaEventRecord((cudaEvent_t)ev[0], s));
   const NetKeys nk = make_net_keys(seed, step);
-  const bool use_wt = c->net.n_member_slots > 0 && c->net.colleague_draws > 0 && batched(&c->net);
+  // day tables: workplace sigma cache, and the random-slot scatter tables for
+  // whole-population runs (a partitioned rank cannot scatter into peers' rows)
+  const bool use_wt = batched(&c->net) &&
+                      ((c->net.n_member_slots > 0 && c->net.colleague_draws > 0) ||
+                       (c->net.random_slots == RT_SLOTS));
+  const bool whole = c->lo == 0 && c->hi == c->n && c->net.random_slots == RT_SLOTS;
   if (use_wt) {
-    k_work_tables<<<grid_for(c->net.n_member_slots, 256), 256, 0, s>>>(c->net, nk, c->wt_host);
+    WorkTables w = c->wt_host;
+    if (!whole) { w.rin = nullptr; w.rout = nullptr; }
+    if (c->wt_whole != (int)whole) {
+      CK(cudaMemcpyAsync(c->wt_dev, &w, sizeof(WorkTables), cudaMemcpyHostToDevice, s));
+      c->wt_whole = (int)whole;
+    }
+    if (whole && step == 0)
+      CK(cudaMemsetAsync(c->wt_host.rin, 0, (size_t)c->n * RT_SLOTS * sizeof(uint32_t), s));
+    const int64_t work = whole ? (c->hi - c->lo) : 0;
+    const int64_t total = c->net.n_member_slots > work ? c->net.n_member_slots : work;
+    k_day_tables<<<grid_for(total, 256), 256, 0, s>>>(c->net, nk, w, codes_cur, c->lo, c->hi);
     CKL();
   }
   const WorkTables* wt = use_wt ? c->wt_dev : nullptr;

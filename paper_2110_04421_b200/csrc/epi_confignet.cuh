@@ -144,7 +144,16 @@ struct WorkTables {
   int32_t* member_at_pos;
   uint8_t* pos_of;
   uint8_t* shift;
+  // Random-slot tables (whole-population runs only; RT_SLOTS per agent):
+  //   rout[a*16 + j] = pi_{t,j}(a) for j < n_{t,a}  (own out-partners)
+  //   rin [b*16 + j] = c + 1 where pi_{t,j}(c) = b, j < n_{t,c}, c != b; else 0.
+  // Filled by k_day_tables with n_{t,a} ~ 5 forward evaluations per agent
+  // (a conflict-free scatter: pi is a bijection); rin rows are cleared by
+  // their consumer after reading, so the next day's scatter starts from 0.
+  uint32_t* rout;
+  uint32_t* rin;
 };
+constexpr int RT_SLOTS = 16;
 
 __device__ __forceinline__ uint32_t work_shift(uint64_t wshift_prefix, int w, int j, int m) {
   const uint64_t hq = fold(fold(wshift_prefix, (uint64_t)w), (uint64_t)(j >> 2));
@@ -320,6 +329,38 @@ __device__ __forceinline__ void for_each_in_edge_batched(const epi_net& net, con
     const int nb = code_count(code_b);
     const int slots = net.random_slots;
     const uint32_t self = (uint32_t)b;
+    if (wt != nullptr && wt->rin != nullptr && JMAX == RT_SLOTS) {
+      // table path: in-partners and own out-partners were produced by
+      // k_day_tables; consume them and clear the in-row for tomorrow
+      uint4* rowin = (uint4*)(wt->rin + (size_t)b * RT_SLOTS);
+      const uint4* rowout = (const uint4*)(wt->rout + (size_t)b * RT_SLOTS);
+      uint32_t pin[RT_SLOTS], pout[RT_SLOTS];
+#pragma unroll
+      for (int q = 0; q < RT_SLOTS / 4; ++q) {
+        const uint4 v = rowin[q];
+        pin[4 * q] = v.x; pin[4 * q + 1] = v.y; pin[4 * q + 2] = v.z; pin[4 * q + 3] = v.w;
+      }
+      const int nbe = nb < slots ? nb : slots;
+#pragma unroll
+      for (int q = 0; q < RT_SLOTS / 4; ++q) {
+        uint4 v = make_uint4(self, self, self, self);
+        if (4 * q < nbe) v = rowout[q];
+        pout[4 * q] = v.x; pout[4 * q + 1] = v.y; pout[4 * q + 2] = v.z; pout[4 * q + 3] = v.w;
+      }
+      uint16_t cin[RT_SLOTS], cout[RT_SLOTS];
+#pragma unroll
+      for (int j = 0; j < RT_SLOTS; ++j) {
+        cin[j] = pin[j] ? codes[pin[j] - 1] : (uint16_t)0;
+        cout[j] = (j < nbe && pout[j] != self) ? codes[pout[j]] : (uint16_t)CODE_DEAD;
+      }
+#pragma unroll
+      for (int j = 0; j < RT_SLOTS; ++j)
+        if (!code_dead(cout[j])) visit((int64_t)pout[j], 2, cout[j]);
+#pragma unroll
+      for (int j = 0; j < RT_SLOTS; ++j)
+        if (pin[j]) visit((int64_t)(pin[j] - 1), 2, cin[j]);
+      return;
+    }
     // in-partners: one inverse evaluation per slot, all lanes busy
     uint32_t pin[JMAX];
     // straight-line first application for every slot (16 independent chains

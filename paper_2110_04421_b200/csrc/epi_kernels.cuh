@@ -370,6 +370,15 @@ __global__ void k_update_from_hazard(StepArgs A, const double* __restrict__ haza
   rec_flush(racc, A.rec, A.step);
 }
 
+__device__ __forceinline__ void clear_rin_row(const WorkTables* wt, int64_t b) {
+  if (wt != nullptr && wt->rin != nullptr) {
+    uint4* row = (uint4*)(wt->rin + (size_t)b * RT_SLOTS);
+#pragma unroll
+    for (int q = 0; q < RT_SLOTS / 4; ++q) row[q] = make_uint4(0, 0, 0, 0);
+  }
+}
+
+
 // ---------------------------------------------------------------------------
 // Config CSR generation (mode 0): one lane per destination row; each row is
 // staged in shared memory (odd stride: conflict-free), optionally sorted into
@@ -406,6 +415,7 @@ __global__ void __launch_bounds__(128, 6) k_net_realize(epi_net net, NetKeys nk,
         if (BATCH) for_each_in_edge_batched<16, 8>(net, nk, NT.rk, NT.wrad, wt, codes, b, cb, put);
         else for_each_in_edge(net, nk, NT.rk, NT.wrad, codes, b, cb, 0, 1, put);
       }
+      if (BATCH) clear_rin_row(wt, b);
       if (SORT) {
         for (int i = 1; i < cnt; ++i) {
           const uint32_t x = mine[i];
@@ -466,6 +476,7 @@ __global__ void __launch_bounds__(128, 6) k_fused_step(StepArgs A, epi_net net, 
         else for_each_in_edge(net, nk, NT.rk, NT.wrad, codes, b, cb, 0, 1, add);
         if (is_target(A.P, A.st, b)) lam = (double)(acc * T.sfac[A.st.age_band[b]]);
       }
+      if (BATCH) clear_rin_row(wt, b);
     }
     unsigned ev = 0;
     if (valid) ev = transmit_progress(A, b, lam);
@@ -481,28 +492,47 @@ __global__ void __launch_bounds__(128, 6) k_fused_step(StepArgs A, epi_net net, 
   rec_flush(racc, A.rec, A.step);
 }
 
-// Per-day workplace tables: one thread per member slot.
-__global__ void k_work_tables(epi_net net, NetKeys nk, WorkTables wt) {
-  __shared__ Radix wrad[256];
-  for (int m = threadIdx.x; m < 256; m += blockDim.x) wrad[m] = make_radix(m < 1 ? 1u : (uint32_t)m);
+// Per-day tables: workplace (one thread per member slot) and, for whole-
+// population runs, random slots (one thread per agent: ~n_{t,a} forward
+// bijection evaluations + a conflict-free scatter into the in-table).
+__global__ void k_day_tables(epi_net net, NetKeys nk, WorkTables wt, const uint16_t* __restrict__ codes,
+                             int64_t lo, int64_t hi) {
+  __shared__ NetTables NT;
+  build_net_tables(NT, net, nk.rperm);
   __syncthreads();
   const int draws = net.colleague_draws;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < net.n_member_slots;
+  const int64_t n_rows = wt.rin ? hi - lo : 0;
+  const int64_t total = net.n_member_slots > n_rows ? net.n_member_slots : n_rows;
+  const Radix dn = make_radix((uint32_t)net.n_agents);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t c = net.wp_members[i];
-    const int w = net.wp_id[c];
-    const int base = net.wp_base[w];
-    const int m = net.wp_size[w];
-    const uint32_t q = (uint32_t)(i - base);
-    if (m >= 2) {
-      const PermKeys K = work_keys(nk.wperm, w);
-      const uint32_t loc = walk_fwd(q, K, wrad[m]);
-      wt.member_at_pos[i] = net.wp_members[base + loc];
-      wt.pos_of[base + loc] = (uint8_t)q;
-      for (int j = (int)q; j < draws; j += m) wt.shift[(size_t)w * draws + j] = (uint8_t)work_shift(nk.wshift, w, j, m);
-    } else {
-      wt.member_at_pos[i] = c;
-      wt.pos_of[i] = 0;
+    if (i < net.n_member_slots && draws > 0) {
+      const int32_t c = net.wp_members[i];
+      const int w = net.wp_id[c];
+      const int base = net.wp_base[w];
+      const int m = net.wp_size[w];
+      const uint32_t q = (uint32_t)(i - base);
+      if (m >= 2) {
+        const PermKeys K = work_keys(nk.wperm, w);
+        const uint32_t loc = walk_fwd(q, K, NT.wrad[m]);
+        wt.member_at_pos[i] = net.wp_members[base + loc];
+        wt.pos_of[base + loc] = (uint8_t)q;
+        for (int j = (int)q; j < draws; j += m)
+          wt.shift[(size_t)w * draws + j] = (uint8_t)work_shift(nk.wshift, w, j, m);
+      } else {
+        wt.member_at_pos[i] = c;
+        wt.pos_of[i] = 0;
+      }
+    }
+    if (i < n_rows && net.n_agents >= 2) {
+      const uint32_t a = (uint32_t)(lo + i);
+      const int na = code_count(codes[a]);         // 0 for dead agents
+      const int nae = na < net.random_slots ? na : net.random_slots;
+      for (int j = 0; j < nae; ++j) {
+        const uint32_t y = walk_fwd(a, NT.rk[j], dn);
+        wt.rout[(size_t)a * RT_SLOTS + j] = y;
+        if (y != a) wt.rin[(size_t)y * RT_SLOTS + j] = a + 1;
+      }
     }
   }
 }
