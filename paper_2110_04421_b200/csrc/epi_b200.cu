@@ -260,6 +260,7 @@ int epi_destroy(epi_ctx* c) {
   cudaFree(c->wt_host.member_at_pos);
   cudaFree(c->wt_host.pos_of);
   cudaFree(c->wt_host.shift);
+  cudaFree(c->wt_host.wcode);
   cudaFree(c->wt_host.rout);
   cudaFree(c->wt_host.rin);
   cudaFree(c->wt_dev);
@@ -537,13 +538,14 @@ int epi_net_attach(epi_ctx* c, const epi_net* net) {
   rc = dalloc(&c->wt_host.member_at_pos, (size_t)net->n_member_slots);
   if (!rc) rc = dalloc(&c->wt_host.pos_of, (size_t)net->n_member_slots);
   if (!rc) rc = dalloc(&c->wt_host.shift, (size_t)net->n_workplaces * (net->colleague_draws + 1));
+  if (!rc) rc = dalloc(&c->wt_host.wcode, (size_t)net->n_member_slots);
   if (!rc) rc = dalloc(&c->wt_host.rout, (size_t)c->n * RT_SLOTS);
   if (!rc) rc = dalloc(&c->wt_host.rin, (size_t)c->n * RT_SLOTS);
   if (rc) return rc;
-  CK(cudaMemset(c->wt_host.rin, 0, (size_t)c->n * RT_SLOTS * sizeof(uint32_t)));
+  CK(cudaMemset(c->wt_host.rin, 0, (size_t)c->n * RT_SLOTS * sizeof(uint16_t)));
   if (!c->wt_dev) CK(cudaMalloc((void**)&c->wt_dev, sizeof(WorkTables)));
   CK(cudaMemcpy(c->wt_dev, &c->wt_host, sizeof(WorkTables), cudaMemcpyHostToDevice));
-  c->wt_whole = 1;
+  c->wt_whole = -1;
   return 0;
 }
 
@@ -577,25 +579,29 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
   const int slot = step % c->net_slots;
   if (ev) CK(cudaEventRecord((cudaEvent_t)ev[0], s));
   const NetKeys nk = make_net_keys(seed, step);
-  // day tables: workplace sigma cache, and the random-slot scatter tables for
-  // whole-population runs (a partitioned rank cannot scatter into peers' rows)
-  const bool use_wt = batched(&c->net) &&
-                      ((c->net.n_member_slots > 0 && c->net.colleague_draws > 0) ||
-                       (c->net.random_slots == RT_SLOTS));
-  const bool whole = c->lo == 0 && c->hi == c->n && c->net.random_slots == RT_SLOTS;
+  // day tables: workplace sigma cache (all modes); in fused mode also the
+  // push tables (workplace codes; random-slot codes for whole-population runs
+  // — a partitioned rank cannot scatter into its peers' rows)
+  const bool has_work = c->net.n_member_slots > 0 && c->net.colleague_draws > 0;
+  const bool push_rand = mode == 1 && c->lo == 0 && c->hi == c->n && c->net.n_agents >= 2;
+  const bool use_wt = (mode == 0 && has_work && batched(&c->net)) || mode == 1;
   if (use_wt) {
     WorkTables w = c->wt_host;
-    if (!whole) { w.rin = nullptr; w.rout = nullptr; }
-    if (c->wt_whole != (int)whole) {
+    if (mode == 0) w.wcode = nullptr;
+    if (!push_rand) { w.rin = nullptr; w.rout = nullptr; }
+    const int variant = (mode == 1 ? 2 : 0) | (push_rand ? 1 : 0);
+    if (c->wt_whole != variant) {
       CK(cudaMemcpyAsync(c->wt_dev, &w, sizeof(WorkTables), cudaMemcpyHostToDevice, s));
-      c->wt_whole = (int)whole;
+      c->wt_whole = variant;
     }
-    if (whole && step == 0)
-      CK(cudaMemsetAsync(c->wt_host.rin, 0, (size_t)c->n * RT_SLOTS * sizeof(uint32_t), s));
-    const int64_t work = whole ? (c->hi - c->lo) : 0;
-    const int64_t total = c->net.n_member_slots > work ? c->net.n_member_slots : work;
-    k_day_tables<<<grid_for(total, 256), 256, 0, s>>>(c->net, nk, w, codes_cur, c->lo, c->hi);
-    CKL();
+    if (push_rand && step == 0)
+      CK(cudaMemsetAsync(c->wt_host.rin, 0, (size_t)c->n * RT_SLOTS * sizeof(uint16_t), s));
+    const int64_t work = push_rand ? (c->hi - c->lo) : 0;
+    const int64_t total = (has_work ? c->net.n_member_slots : 0) > work ? c->net.n_member_slots : work;
+    if (total > 0) {
+      k_day_tables<<<grid_for(total, 256), 256, 0, s>>>(c->net, nk, w, codes_cur, c->lo, c->hi);
+      CKL();
+    }
   }
   const WorkTables* wt = use_wt ? c->wt_dev : nullptr;
   if (mode == 0) {
@@ -617,12 +623,8 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
   } else {
     if (ev) CK(cudaEventRecord((cudaEvent_t)ev[1], s));
     const int fgrid = grid_for(c->hi - c->lo, 128, 16);
-    if (batched(&c->net))
-      k_fused_step<true><<<fgrid, 128, 0, s>>>(A, c->net, nk, codes_cur, c->host.rate_scale, codes_next,
-                                               c->net_dev, rcount_next, iv ? 0 : 1, wt);
-    else
-      k_fused_step<false><<<fgrid, 128, 0, s>>>(A, c->net, nk, codes_cur, c->host.rate_scale, codes_next,
-                                                c->net_dev, rcount_next, iv ? 0 : 1, nullptr);
+    k_fused_step<<<fgrid, 128, 0, s>>>(A, c->net, nk, codes_cur, c->host.rate_scale, codes_next,
+                                       c->net_dev, rcount_next, iv ? 0 : 1, wt);
     CKL();
   }
   if (ev) CK(cudaEventRecord((cudaEvent_t)ev[2], s));

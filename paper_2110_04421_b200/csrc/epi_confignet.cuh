@@ -144,16 +144,19 @@ struct WorkTables {
   int32_t* member_at_pos;
   uint8_t* pos_of;
   uint8_t* shift;
-  // Random-slot tables (whole-population runs only; RT_SLOTS per agent):
-  //   rout[a*16 + j] = pi_{t,j}(a) for j < n_{t,a}  (own out-partners)
-  //   rin [b*16 + j] = c + 1 where pi_{t,j}(c) = b, j < n_{t,c}, c != b; else 0.
-  // Filled by k_day_tables with n_{t,a} ~ 5 forward evaluations per agent
-  // (a conflict-free scatter: pi is a bijection); rin rows are cleared by
-  // their consumer after reading, so the next day's scatter starts from 0.
-  uint32_t* rout;
-  uint32_t* rin;
+  // Fused mode only ("push" tables: the consumer reads contiguous rows
+  // instead of gathering random 2-byte codes):
+  //   wcode[base_W + q] = code of member_at_pos[base_W + q]
+  //   rout[a*16 + j] = code(pi_{t,j}(a)) | PRESENT   for j < n_{t,a}, pi(a) != a
+  //   rin [b*16 + j] = code(c) | PRESENT where pi_{t,j}(c) = b, j < n_{t,c}, c != b
+  // (whole-population runs only; the scatter into rin is conflict-free because
+  // pi is a bijection, and rin rows are cleared by their consumer).
+  uint16_t* wcode;
+  uint16_t* rout;
+  uint16_t* rin;
 };
 constexpr int RT_SLOTS = 16;
+constexpr uint16_t CODE_PRESENT = 0x4000;
 
 __device__ __forceinline__ uint32_t work_shift(uint64_t wshift_prefix, int w, int j, int m) {
   const uint64_t hq = fold(fold(wshift_prefix, (uint64_t)w), (uint64_t)(j >> 2));
@@ -329,38 +332,6 @@ __device__ __forceinline__ void for_each_in_edge_batched(const epi_net& net, con
     const int nb = code_count(code_b);
     const int slots = net.random_slots;
     const uint32_t self = (uint32_t)b;
-    if (wt != nullptr && wt->rin != nullptr && JMAX == RT_SLOTS) {
-      // table path: in-partners and own out-partners were produced by
-      // k_day_tables; consume them and clear the in-row for tomorrow
-      uint4* rowin = (uint4*)(wt->rin + (size_t)b * RT_SLOTS);
-      const uint4* rowout = (const uint4*)(wt->rout + (size_t)b * RT_SLOTS);
-      uint32_t pin[RT_SLOTS], pout[RT_SLOTS];
-#pragma unroll
-      for (int q = 0; q < RT_SLOTS / 4; ++q) {
-        const uint4 v = rowin[q];
-        pin[4 * q] = v.x; pin[4 * q + 1] = v.y; pin[4 * q + 2] = v.z; pin[4 * q + 3] = v.w;
-      }
-      const int nbe = nb < slots ? nb : slots;
-#pragma unroll
-      for (int q = 0; q < RT_SLOTS / 4; ++q) {
-        uint4 v = make_uint4(self, self, self, self);
-        if (4 * q < nbe) v = rowout[q];
-        pout[4 * q] = v.x; pout[4 * q + 1] = v.y; pout[4 * q + 2] = v.z; pout[4 * q + 3] = v.w;
-      }
-      uint16_t cin[RT_SLOTS], cout[RT_SLOTS];
-#pragma unroll
-      for (int j = 0; j < RT_SLOTS; ++j) {
-        cin[j] = pin[j] ? codes[pin[j] - 1] : (uint16_t)0;
-        cout[j] = (j < nbe && pout[j] != self) ? codes[pout[j]] : (uint16_t)CODE_DEAD;
-      }
-#pragma unroll
-      for (int j = 0; j < RT_SLOTS; ++j)
-        if (!code_dead(cout[j])) visit((int64_t)pout[j], 2, cout[j]);
-#pragma unroll
-      for (int j = 0; j < RT_SLOTS; ++j)
-        if (pin[j]) visit((int64_t)(pin[j] - 1), 2, cin[j]);
-      return;
-    }
     // in-partners: one inverse evaluation per slot, all lanes busy
     uint32_t pin[JMAX];
     // straight-line first application for every slot (16 independent chains
@@ -392,6 +363,107 @@ __device__ __forceinline__ void for_each_in_edge_batched(const epi_net& net, con
 #pragma unroll
     for (int j = 0; j < JMAX; ++j)
       if (j < code_count(cin[j])) visit((int64_t)pin[j], 2, cin[j]);
+  }
+}
+
+// Code-only enumeration for the fused kernel: visit(kind, code_src) for every
+// in-edge of alive b, reading the day's push tables (wt != null) where they
+// exist, else evaluating the bijections (partitioned ranks).  Same edge
+// multiset and the same visit order as for_each_in_edge_batched.
+template <class Visit>
+__device__ __forceinline__ void for_each_in_code(const epi_net& net, const NetKeys& nk,
+                                                 const PermKeys* __restrict__ rk,
+                                                 const Radix* __restrict__ wrad, const Radix& dn,
+                                                 const WorkTables* wt,
+                                                 const uint16_t* __restrict__ codes, int64_t b,
+                                                 uint16_t code_b, Visit&& visit) {
+  // household: contiguous ids -> contiguous codes
+  {
+    const int off = net.hh_off[b];
+    const int sz = net.hh_size[b];
+    const int64_t start = b - off;
+    for (int i = 0; i < sz; ++i) {
+      const int64_t c = start + i;
+      if (c == b) continue;
+      const uint16_t cc = codes[c];
+      if (!code_dead(cc)) visit(0, cc);
+    }
+  }
+  const int w = net.wp_id[b];
+  if (w >= 0) {
+    const int m = net.wp_size[w];
+    if (m >= 2) {
+      const int base = net.wp_base[w];
+      const int draws = net.colleague_draws;
+      if (wt != nullptr && wt->wcode != nullptr) {
+        const uint32_t p = wt->pos_of[base + net.wp_local[b]];
+        const uint8_t* sh = wt->shift + (size_t)w * draws;
+        const uint16_t* wc = wt->wcode + base;
+        for (int j = 0; j < draws; ++j) {
+          const uint32_t r = sh[j];
+          const uint16_t co = wc[add_mod(p, r, (uint32_t)m)];
+          const uint16_t ci = wc[sub_mod(p, r, (uint32_t)m)];
+          if (!code_dead(co)) visit(1, co);
+          if (!code_dead(ci)) visit(1, ci);
+        }
+      } else {
+        const Radix d = wrad[m];
+        const PermKeys K = work_keys(nk.wperm, w);
+        const uint32_t p = walk_inv(net.wp_local[b], K, d);
+        for (int j = 0; j < draws; ++j) {
+          const uint32_t r = work_shift(nk.wshift, w, j, m);
+          const uint16_t co = codes[net.wp_members[base + walk_fwd(add_mod(p, r, (uint32_t)m), K, d)]];
+          const uint16_t ci = codes[net.wp_members[base + walk_fwd(sub_mod(p, r, (uint32_t)m), K, d)]];
+          if (!code_dead(co)) visit(1, co);
+          if (!code_dead(ci)) visit(1, ci);
+        }
+      }
+    }
+  }
+  if (net.n_agents < 2) return;
+  if (wt != nullptr && wt->rin != nullptr) {
+    const uint4* ro = (const uint4*)(wt->rout + (size_t)b * RT_SLOTS);
+    const uint4* ri = (const uint4*)(wt->rin + (size_t)b * RT_SLOTS);
+    uint4 o[2] = {ro[0], ro[1]}, in[2] = {ri[0], ri[1]};
+    const uint16_t* ov = (const uint16_t*)o;
+    const uint16_t* iv = (const uint16_t*)in;
+#pragma unroll
+    for (int j = 0; j < RT_SLOTS; ++j)
+      if ((ov[j] & CODE_PRESENT) && !code_dead(ov[j])) visit(2, (uint16_t)(ov[j] & ~CODE_PRESENT));
+#pragma unroll
+    for (int j = 0; j < RT_SLOTS; ++j)
+      if (iv[j] & CODE_PRESENT) visit(2, (uint16_t)(iv[j] & ~CODE_PRESENT));
+    return;
+  }
+  // random section evaluated on the fly (no tables)
+  const uint32_t self = (uint32_t)b;
+  const int nb = code_count(code_b);
+  const int slots = net.random_slots;
+  const int nbe = nb < slots ? nb : slots;
+  for (int j0 = 0; j0 < nbe; j0 += 4) {
+    uint32_t po[4];
+    uint16_t co[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) po[q] = (j0 + q < nbe) ? walk_fwd(self, rk[j0 + q], dn) : self;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) co[q] = po[q] != self ? codes[po[q]] : (uint16_t)CODE_DEAD;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (!code_dead(co[q])) visit(2, co[q]);
+  }
+  for (int j0 = 0; j0 < slots; j0 += 8) {
+    uint32_t pi[8];
+    uint16_t ci[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) pi[q] = (j0 + q < slots) ? perm_inv(self, rk[j0 + q], dn) : self;
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (pi[q] >= dn.n) pi[q] = walk_inv(pi[q], rk[j0 + q], dn);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) ci[q] = pi[q] != self ? codes[pi[q]] : (uint16_t)0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (j0 + q < code_count(ci[q])) visit(2, ci[q]);
   }
 }
 

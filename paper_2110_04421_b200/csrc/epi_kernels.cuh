@@ -373,11 +373,10 @@ __global__ void k_update_from_hazard(StepArgs A, const double* __restrict__ haza
 __device__ __forceinline__ void clear_rin_row(const WorkTables* wt, int64_t b) {
   if (wt != nullptr && wt->rin != nullptr) {
     uint4* row = (uint4*)(wt->rin + (size_t)b * RT_SLOTS);
-#pragma unroll
-    for (int q = 0; q < RT_SLOTS / 4; ++q) row[q] = make_uint4(0, 0, 0, 0);
+    row[0] = make_uint4(0, 0, 0, 0);
+    row[1] = make_uint4(0, 0, 0, 0);
   }
 }
-
 
 // ---------------------------------------------------------------------------
 // Config CSR generation (mode 0): one lane per destination row; each row is
@@ -415,7 +414,6 @@ __global__ void __launch_bounds__(128, 6) k_net_realize(epi_net net, NetKeys nk,
         if (BATCH) for_each_in_edge_batched<16, 8>(net, nk, NT.rk, NT.wrad, wt, codes, b, cb, put);
         else for_each_in_edge(net, nk, NT.rk, NT.wrad, codes, b, cb, 0, 1, put);
       }
-      if (BATCH) clear_rin_row(wt, b);
       if (SORT) {
         for (int i = 1; i < cnt; ++i) {
           const uint32_t x = mine[i];
@@ -443,8 +441,8 @@ __global__ void __launch_bounds__(128, 6) k_net_realize(epi_net net, NetKeys nk,
 
 // Fused generate + gather + update (mode 1): the in-edges are enumerated and
 // their source codes consumed on the fly, so no CSR ever reaches memory.  One
-// lane per agent; gathers are batched per section (for_each_in_edge_batched).
-template <bool BATCH>
+// lane per agent; with the day's push tables the random and workplace codes
+// come from contiguous rows (for_each_in_code).
 __global__ void __launch_bounds__(128, 6) k_fused_step(StepArgs A, epi_net net, NetKeys nk,
                                                     const uint16_t* __restrict__ codes, double rate,
                                                     uint16_t* __restrict__ codes_next,
@@ -457,6 +455,7 @@ __global__ void __launch_bounds__(128, 6) k_fused_step(StepArgs A, epi_net net, 
   build_net_tables(NT, net, nk.rperm);
   rec_init(racc);
   __syncthreads();
+  const Radix dn = make_radix((uint32_t)net.n_agents);
   const int64_t n = A.hi;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t base = A.lo + blockIdx.x * (int64_t)blockDim.x; base < n; base += stride) {
@@ -468,15 +467,13 @@ __global__ void __launch_bounds__(128, 6) k_fused_step(StepArgs A, epi_net net, 
       const uint16_t cb = codes[b];
       if (!code_dead(cb)) {
         float acc = 0.f;
-        auto add = [&](int64_t, int kind, uint16_t cc) {
+        for_each_in_code(net, nk, NT.rk, NT.wrad, dn, wt, codes, b, cb, [&](int kind, uint16_t cc) {
           ++edges;
           acc += T.factor[cc & 0xFF] * T.bfac[kind];
-        };
-        if (BATCH) for_each_in_edge_batched<16, 8>(net, nk, NT.rk, NT.wrad, wt, codes, b, cb, add);
-        else for_each_in_edge(net, nk, NT.rk, NT.wrad, codes, b, cb, 0, 1, add);
+        });
         if (is_target(A.P, A.st, b)) lam = (double)(acc * T.sfac[A.st.age_band[b]]);
       }
-      if (BATCH) clear_rin_row(wt, b);
+      clear_rin_row(wt, b);
     }
     unsigned ev = 0;
     if (valid) ev = transmit_progress(A, b, lam);
@@ -492,9 +489,11 @@ __global__ void __launch_bounds__(128, 6) k_fused_step(StepArgs A, epi_net net, 
   rec_flush(racc, A.rec, A.step);
 }
 
-// Per-day tables: workplace (one thread per member slot) and, for whole-
-// population runs, random slots (one thread per agent: ~n_{t,a} forward
-// bijection evaluations + a conflict-free scatter into the in-table).
+// Per-day tables, one thread per member slot and (push tables) per agent:
+//  * workplace: member_at_pos / pos_of / shift (all modes) and wcode (fused);
+//  * random push tables (fused, whole population): agent a evaluates its
+//    n_{t,a} forward partners y = pi_j(a) and writes rout[a][j] = code(y) and
+//    rin[y][j] = code(a) (conflict-free scatter, pi is a bijection).
 __global__ void k_day_tables(epi_net net, NetKeys nk, WorkTables wt, const uint16_t* __restrict__ codes,
                              int64_t lo, int64_t hi) {
   __shared__ NetTables NT;
@@ -512,27 +511,42 @@ __global__ void k_day_tables(epi_net net, NetKeys nk, WorkTables wt, const uint1
       const int base = net.wp_base[w];
       const int m = net.wp_size[w];
       const uint32_t q = (uint32_t)(i - base);
+      int32_t who = c;
       if (m >= 2) {
         const PermKeys K = work_keys(nk.wperm, w);
         const uint32_t loc = walk_fwd(q, K, NT.wrad[m]);
-        wt.member_at_pos[i] = net.wp_members[base + loc];
+        who = net.wp_members[base + loc];
         wt.pos_of[base + loc] = (uint8_t)q;
         for (int j = (int)q; j < draws; j += m)
           wt.shift[(size_t)w * draws + j] = (uint8_t)work_shift(nk.wshift, w, j, m);
       } else {
-        wt.member_at_pos[i] = c;
         wt.pos_of[i] = 0;
       }
+      wt.member_at_pos[i] = who;
+      if (wt.wcode) wt.wcode[i] = codes[who];
     }
     if (i < n_rows && net.n_agents >= 2) {
       const uint32_t a = (uint32_t)(lo + i);
-      const int na = code_count(codes[a]);         // 0 for dead agents
-      const int nae = na < net.random_slots ? na : net.random_slots;
-      for (int j = 0; j < nae; ++j) {
-        const uint32_t y = walk_fwd(a, NT.rk[j], dn);
-        wt.rout[(size_t)a * RT_SLOTS + j] = y;
-        if (y != a) wt.rin[(size_t)y * RT_SLOTS + j] = a + 1;
+      const uint16_t ca = codes[a];
+      const int na = code_count(ca);                // 0 for dead agents
+      const int nae = na < RT_SLOTS ? na : RT_SLOTS;
+      uint16_t row[RT_SLOTS];
+#pragma unroll
+      for (int j = 0; j < RT_SLOTS; ++j) row[j] = 0;
+#pragma unroll
+      for (int j = 0; j < RT_SLOTS; ++j) {
+        if (j < nae) {
+          const uint32_t y = walk_fwd(a, NT.rk[j], dn);
+          if (y != a) {
+            row[j] = codes[y] | CODE_PRESENT;
+            wt.rin[(size_t)y * RT_SLOTS + j] = ca | CODE_PRESENT;
+          }
+        }
       }
+      uint4* out = (uint4*)(wt.rout + (size_t)a * RT_SLOTS);
+      const uint4* rv = (const uint4*)row;
+      out[0] = rv[0];
+      out[1] = rv[1];
     }
   }
 }
