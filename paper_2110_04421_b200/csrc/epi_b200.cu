@@ -102,6 +102,9 @@ struct epi_ctx {
   std::vector<uint32_t*> net_entries;
   std::vector<int32_t*> net_rowlen;
   std::vector<int32_t> net_slot_step;
+  MsgTables* msg_dev = nullptr;      // fp32 message tables (rate_scale baked in)
+  NetTables ntab{};                  // host copy (static radix tables)
+  NetTables* ntab_dev[2] = {nullptr, nullptr};   // per-day keys, by step parity
   WorkTables wt_host{};              // device arrays, rebuilt each day
   WorkTables* wt_dev = nullptr;
   int wt_whole = -1;                 // which variant wt_dev currently holds
@@ -118,6 +121,10 @@ int upload_params(epi_ctx* c, const epi_params* p) {
   c->host = *p;
   if (!c->P) CK(cudaMalloc((void**)&c->P, sizeof(epi_params)));
   CK(cudaMemcpy(c->P, p, sizeof(epi_params), cudaMemcpyHostToDevice));
+  MsgTables mt;
+  fill_msg_tables(mt, *p, p->rate_scale);
+  if (!c->msg_dev) CK(cudaMalloc((void**)&c->msg_dev, sizeof(MsgTables)));
+  CK(cudaMemcpy(c->msg_dev, &mt, sizeof(MsgTables), cudaMemcpyHostToDevice));
   return 0;
 }
 
@@ -257,6 +264,9 @@ int epi_destroy(epi_ctx* c) {
   cudaFree(c->cub_tmp);
   cudaFree(c->net_dev);
   cudaFree(c->inj_dev);
+  cudaFree(c->msg_dev);
+  cudaFree(c->ntab_dev[0]);
+  cudaFree(c->ntab_dev[1]);
   cudaFree(c->wt_host.member_at_pos);
   cudaFree(c->wt_host.pos_of);
   cudaFree(c->wt_host.shift);
@@ -351,9 +361,11 @@ int epi_gather(epi_ctx* c, const epi_state* st, int32_t step, int32_t precision,
   CsrView g{c->entries, c->row_len, c->row_begin, 0};
   const int grid = grid_for(c->n, 256);
   if (precision == EPI_F64_CANONICAL)
-    k_pass<true, 0><<<grid, 256, 0, s>>>(A, g, c->codes, lam_out, c->host.rate_scale, 0, nullptr, nullptr, 0);
+    k_pass<true, 0><<<grid, 256, 0, s>>>(A, g, c->codes, lam_out, c->host.rate_scale, 0, nullptr, nullptr, 0,
+                                         c->msg_dev);
   else
-    k_pass<false, 0><<<grid, 256, 0, s>>>(A, g, c->codes, lam_out, c->host.rate_scale, 0, nullptr, nullptr, 0);
+    k_pass<false, 0><<<grid, 256, 0, s>>>(A, g, c->codes, lam_out, c->host.rate_scale, 0, nullptr, nullptr, 0,
+                                          c->msg_dev);
   CKL();
   return 0;
 }
@@ -404,7 +416,7 @@ static int step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t see
     CKL();
     CsrView g{c->entries, c->row_len, c->row_begin, 0};
     k_pass<true, 1><<<grid, 256, 0, s>>>(A, g, c->codes, nullptr, c->host.rate_scale, iv ? 0 : 1,
-                                         nullptr, nullptr, 0);
+                                         nullptr, nullptr, 0, c->msg_dev);
   }
   CKL();
   if (iv) {
@@ -484,18 +496,28 @@ static int prepare_realize(const epi_net* net) {
 
 static int launch_realize(const epi_net* net, uint64_t g, int32_t step, const uint16_t* codes,
                           uint32_t* entries, int32_t* row_len, int sort_rows, long long* rec,
-                          const WorkTables* wt, int64_t lo, int64_t hi, cudaStream_t s) {
+                          const WorkTables* wt, int64_t lo, int64_t hi, cudaStream_t s,
+                          const NetTables* ntab_dev = nullptr) {
   const size_t smem = realize_smem(net);
   if (smem > g_realize_smem_set) return fail(EPI_EARG, "realize smem not prepared");
   NetKeys nk = make_net_keys(g, step);
+  static NetTables* scratch = nullptr;           // standalone epi_net_realize only
+  if (!ntab_dev) {
+    NetTables local;
+    fill_net_tables(local, *net, nk.rperm);
+    if (!scratch) CK(cudaMalloc((void**)&scratch, sizeof(NetTables)));
+    CK(cudaMemcpyAsync(scratch, &local, sizeof(NetTables), cudaMemcpyHostToDevice, s));
+    CK(cudaStreamSynchronize(s));
+    ntab_dev = scratch;
+  }
   const int grid = grid_for(hi - lo, 128, 16);
   const bool batch = batched(net);
   if (sort_rows) {
-    if (batch) k_net_realize<true, true><<<grid, 128, smem, s>>>(*net, nk, codes, entries, row_len, rec, wt, lo, hi);
-    else k_net_realize<true, false><<<grid, 128, smem, s>>>(*net, nk, codes, entries, row_len, rec, wt, lo, hi);
+    if (batch) k_net_realize<true, true><<<grid, 128, smem, s>>>(*net, nk, codes, entries, row_len, rec, wt, lo, hi, ntab_dev);
+    else k_net_realize<true, false><<<grid, 128, smem, s>>>(*net, nk, codes, entries, row_len, rec, wt, lo, hi, ntab_dev);
   } else {
-    if (batch) k_net_realize<false, true><<<grid, 128, smem, s>>>(*net, nk, codes, entries, row_len, rec, wt, lo, hi);
-    else k_net_realize<false, false><<<grid, 128, smem, s>>>(*net, nk, codes, entries, row_len, rec, wt, lo, hi);
+    if (batch) k_net_realize<false, true><<<grid, 128, smem, s>>>(*net, nk, codes, entries, row_len, rec, wt, lo, hi, ntab_dev);
+    else k_net_realize<false, false><<<grid, 128, smem, s>>>(*net, nk, codes, entries, row_len, rec, wt, lo, hi, ntab_dev);
   }
   CKL();
   return 0;
@@ -520,6 +542,11 @@ int epi_net_attach(epi_ctx* c, const epi_net* net) {
   rc = prepare_realize(net);
   if (rc) return rc;
   c->net = *net;
+  fill_net_tables(c->ntab, *net, 0);
+  for (int i = 0; i < 2; ++i) {
+    if (!c->ntab_dev[i]) CK(cudaMalloc((void**)&c->ntab_dev[i], sizeof(NetTables)));
+    CK(cudaMemcpy(c->ntab_dev[i], &c->ntab, sizeof(NetTables), cudaMemcpyHostToDevice));
+  }
   c->has_net = true;
   if (!c->net_dev) CK(cudaMalloc((void**)&c->net_dev, sizeof(epi_net)));
   CK(cudaMemcpy(c->net_dev, net, sizeof(epi_net), cudaMemcpyHostToDevice));
@@ -579,6 +606,12 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
   const int slot = step % c->net_slots;
   if (ev) CK(cudaEventRecord((cudaEvent_t)ev[0], s));
   const NetKeys nk = make_net_keys(seed, step);
+  NetTables* nt_today = c->ntab_dev[step & 1];
+  NetTables* nt_next = c->ntab_dev[(step + 1) & 1];
+  if (step == 0) {
+    k_day_keys<<<1, 32, 0, s>>>(nt_today, nk.rperm);
+    CKL();
+  }
   // day tables: workplace sigma cache (all modes); in fused mode also the
   // push tables (workplace codes; random-slot codes for whole-population runs
   // — a partitioned rank cannot scatter into its peers' rows)
@@ -596,35 +629,38 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
     }
     if (push_rand && step == 0)
       CK(cudaMemsetAsync(c->wt_host.rin, 0, (size_t)c->n * RT_SLOTS * sizeof(uint16_t), s));
-    const int64_t work = push_rand ? (c->hi - c->lo) : 0;
-    const int64_t total = (has_work ? c->net.n_member_slots : 0) > work ? c->net.n_member_slots : work;
-    if (total > 0) {
-      k_day_tables<<<grid_for(total, 256), 256, 0, s>>>(c->net, nk, w, codes_cur, c->lo, c->hi);
-      CKL();
-    }
+    const int wblocks = has_work ? grid_for(c->net.n_member_slots, 256, 4) : 0;
+    const int rblocks = push_rand ? grid_for(c->hi - c->lo, 256, 8) : 0;
+    k_day_tables<<<wblocks + rblocks > 0 ? wblocks + rblocks : 1, 256, 0, s>>>(
+        c->net, nk, w, codes_cur, c->lo, c->hi, wblocks, nt_today, nt_next,
+        key_prefix(seed, step + 1, P_NET_RPERM));
+    CKL();
+  } else {
+    k_day_keys<<<1, 32, 0, s>>>(nt_next, key_prefix(seed, step + 1, P_NET_RPERM));
+    CKL();
   }
   const WorkTables* wt = use_wt ? c->wt_dev : nullptr;
   if (mode == 0) {
     uint32_t* entries = c->net_entries[slot];
     int32_t* row_len = c->net_rowlen[slot];
     int rc = launch_realize(&c->net, seed, step, codes_cur, entries, row_len,
-                            precision == EPI_F64_CANONICAL, nullptr, wt, c->lo, c->hi, s);
+                            precision == EPI_F64_CANONICAL, nullptr, wt, c->lo, c->hi, s, nt_today);
     if (rc) return rc;
     c->net_slot_step[slot] = step;
     if (ev) CK(cudaEventRecord((cudaEvent_t)ev[1], s));
     CsrView g{entries, row_len, nullptr, c->net.row_cap};
     if (precision == EPI_F64_CANONICAL)
       k_pass<true, 1><<<grid, 256, 0, s>>>(A, g, codes_cur, nullptr, c->host.rate_scale, iv ? 0 : 1,
-                                           codes_next, c->net_dev, rcount_next);
+                                           codes_next, c->net_dev, rcount_next, c->msg_dev);
     else
       k_pass<false, 1><<<grid, 256, 0, s>>>(A, g, codes_cur, nullptr, c->host.rate_scale, iv ? 0 : 1,
-                                            codes_next, c->net_dev, rcount_next);
+                                            codes_next, c->net_dev, rcount_next, c->msg_dev);
     CKL();
   } else {
     if (ev) CK(cudaEventRecord((cudaEvent_t)ev[1], s));
     const int fgrid = grid_for(c->hi - c->lo, 128, 16);
     k_fused_step<<<fgrid, 128, 0, s>>>(A, c->net, nk, codes_cur, c->host.rate_scale, codes_next,
-                                       c->net_dev, rcount_next, iv ? 0 : 1, wt);
+                                       c->net_dev, rcount_next, iv ? 0 : 1, wt, c->msg_dev, nt_today);
     CKL();
   }
   if (ev) CK(cudaEventRecord((cudaEvent_t)ev[2], s));

@@ -98,7 +98,7 @@ inline NetKeys make_net_keys(uint64_t g, int step) {
                  key_prefix(g, step, P_NET_WPERM), key_prefix(g, step, P_NET_WSHIFT)};
 }
 
-__device__ __forceinline__ PermKeys random_slot_keys(uint64_t rperm_prefix, int slot) {
+__host__ __device__ __forceinline__ PermKeys random_slot_keys(uint64_t rperm_prefix, int slot) {
   PermKeys K;
   const uint64_t hs = fold(rperm_prefix, (uint64_t)slot);
 #pragma unroll
@@ -123,19 +123,26 @@ __device__ __forceinline__ PermKeys work_keys(uint64_t wperm_prefix, int w) {
   return K;
 }
 
-// Shared-memory table of the workplace domains (m <= 255) + the agent
-// domain, built once per block.
+// Per-day key/domain tables, computed once on the host per simulated day and
+// passed by value (kernel parameter); blocks copy them to shared memory.
 struct NetTables {
-  PermKeys rk[EPI_MAX_SLOTS];
-  Radix wrad[256];
+  PermKeys rk[EPI_MAX_SLOTS];   // random-slot Feistel keys of the day
+  Radix wrad[256];              // workplace domains, m <= 255 (static)
+  Radix dn;                     // agent domain [0, N)
 };
-__device__ __forceinline__ void build_net_tables(NetTables& T, const epi_net& net, uint64_t rperm) {
-  for (int j = threadIdx.x; j < net.random_slots; j += blockDim.x) T.rk[j] = random_slot_keys(rperm, j);
-  for (int m = threadIdx.x; m < 256; m += blockDim.x) T.wrad[m] = make_radix(m < 1 ? 1u : (uint32_t)m);
+inline void fill_net_tables(NetTables& T, const epi_net& net, uint64_t rperm) {
+  for (int j = 0; j < EPI_MAX_SLOTS; ++j) T.rk[j] = random_slot_keys(rperm, j);
+  for (int m = 0; m < 256; ++m) T.wrad[m] = make_radix(m < 1 ? 1u : (uint32_t)m);
+  T.dn = make_radix(net.n_agents < 1 ? 1u : (uint32_t)net.n_agents);
+}
+__device__ __forceinline__ void load_net_tables(NetTables& S, const NetTables* __restrict__ P) {
+  const uint32_t* src = (const uint32_t*)P;
+  uint32_t* dst = (uint32_t*)&S;
+  for (int i = threadIdx.x; i < (int)(sizeof(NetTables) / 4); i += blockDim.x) dst[i] = src[i];
 }
 
 // Per-day workplace tables (a cache of sigma_{t,W} and the shifts): built by
-// k_work_tables with one bijection evaluation per member slot, then read by
+// k_day_tables with one bijection evaluation per member slot, then read by
 // every worker instead of 1 + 2*draws evaluations each.
 //   member_at_pos[base_W + q] = wp_members[base_W + sigma(q)]
 //   pos_of[base_W + l]        = sigma^{-1}(l)

@@ -80,6 +80,23 @@ struct MsgTables {
   float sfac[16];
   float bfac[4];
 };
+inline void fill_msg_tables(MsgTables& T, const epi_params& P, double rate) {
+  for (int i = 0; i < 256; ++i) {
+    const int t = i & 0x7F;
+    float f = 0.f;
+    if (t >= 1 && t <= P.t_max)
+      f = (float)(rate * ((i & 0x80) ? P.asymptomatic_factor : 1.0) * P.day_weights[t]);
+    T.factor[i] = f;
+  }
+  for (int i = 0; i < 16; ++i)
+    T.sfac[i] = i < 9 ? (float)(P.age_susceptibility[i] / P.mean_daily_interactions) : 0.f;
+  for (int i = 0; i < 4; ++i) T.bfac[i] = i < 3 ? (float)P.network_scale[i] : 0.f;
+}
+__device__ __forceinline__ void load_msg_tables(MsgTables& S, const MsgTables* __restrict__ G) {
+  const uint32_t* src = (const uint32_t*)G;
+  uint32_t* dst = (uint32_t*)&S;
+  for (int i = threadIdx.x; i < (int)(sizeof(MsgTables) / 4); i += blockDim.x) dst[i] = src[i];
+}
 __device__ __forceinline__ void build_msg_tables(MsgTables& T, const epi_params* __restrict__ P,
                                                  double rate) {
   for (int i = threadIdx.x; i < 256; i += blockDim.x) {
@@ -250,11 +267,15 @@ template <bool F64, int MODE>
 __global__ void __launch_bounds__(256) k_pass(StepArgs A, CsrView g, const uint16_t* __restrict__ codes,
                                               void* __restrict__ lam_out, double rate,
                                               int final_pass, uint16_t* __restrict__ codes_next,
-                                              const epi_net* net, uint64_t rcount_next) {
+                                              const epi_net* net, uint64_t rcount_next,
+                                              const MsgTables* __restrict__ mt) {
   __shared__ MsgTables T;
   __shared__ float lam_tile[8][32];
   __shared__ RecAcc racc;
-  if (!F64) build_msg_tables(T, A.P, rate);
+  if (!F64) {
+    if (mt) load_msg_tables(T, mt);
+    else build_msg_tables(T, A.P, rate);
+  }
   rec_init(racc);
   __syncthreads();
   const epi_params* __restrict__ P = A.P;
@@ -370,6 +391,12 @@ __global__ void k_update_from_hazard(StepArgs A, const double* __restrict__ haza
   rec_flush(racc, A.rec, A.step);
 }
 
+// Day-0 keys (every later day's keys are written by the previous day's
+// k_day_tables).
+__global__ void k_day_keys(NetTables* __restrict__ NT, uint64_t rperm) {
+  if (threadIdx.x < EPI_MAX_SLOTS) NT->rk[threadIdx.x] = random_slot_keys(rperm, threadIdx.x);
+}
+
 __device__ __forceinline__ void clear_rin_row(const WorkTables* wt, int64_t b) {
   if (wt != nullptr && wt->rin != nullptr) {
     uint4* row = (uint4*)(wt->rin + (size_t)b * RT_SLOTS);
@@ -387,11 +414,12 @@ template <bool SORT, bool BATCH>
 __global__ void __launch_bounds__(128, 6) k_net_realize(epi_net net, NetKeys nk, const uint16_t* __restrict__ codes,
                                                      uint32_t* __restrict__ entries,
                                                      int32_t* __restrict__ row_len, long long* rec,
-                                                     const WorkTables* wt, int64_t lo, int64_t hi) {
+                                                     const WorkTables* wt, int64_t lo, int64_t hi,
+                                                     const NetTables* __restrict__ NTp) {
   extern __shared__ uint32_t stage_buf[];
   __shared__ NetTables NT;
   __shared__ RecAcc racc;
-  build_net_tables(NT, net, nk.rperm);
+  load_net_tables(NT, NTp);
   rec_init(racc);
   __syncthreads();
   const int cap = net.row_cap;
@@ -447,15 +475,17 @@ __global__ void __launch_bounds__(128, 6) k_fused_step(StepArgs A, epi_net net, 
                                                     const uint16_t* __restrict__ codes, double rate,
                                                     uint16_t* __restrict__ codes_next,
                                                     const epi_net* net_dev, uint64_t rcount_next,
-                                                    int final_pass, const WorkTables* wt) {
+                                                    int final_pass, const WorkTables* wt,
+                                                    const MsgTables* __restrict__ mt,
+                                                    const NetTables* __restrict__ NTp) {
   __shared__ MsgTables T;
   __shared__ NetTables NT;
   __shared__ RecAcc racc;
-  build_msg_tables(T, A.P, rate);
-  build_net_tables(NT, net, nk.rperm);
+  load_msg_tables(T, mt);
+  load_net_tables(NT, NTp);
   rec_init(racc);
   __syncthreads();
-  const Radix dn = make_radix((uint32_t)net.n_agents);
+  const Radix dn = NT.dn;
   const int64_t n = A.hi;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t base = A.lo + blockIdx.x * (int64_t)blockDim.x; base < n; base += stride) {
@@ -489,23 +519,29 @@ __global__ void __launch_bounds__(128, 6) k_fused_step(StepArgs A, epi_net net, 
   rec_flush(racc, A.rec, A.step);
 }
 
-// Per-day tables, one thread per member slot and (push tables) per agent:
-//  * workplace: member_at_pos / pos_of / shift (all modes) and wcode (fused);
-//  * random push tables (fused, whole population): agent a evaluates its
-//    n_{t,a} forward partners y = pi_j(a) and writes rout[a][j] = code(y) and
-//    rin[y][j] = code(a) (conflict-free scatter, pi is a bijection).
-__global__ void k_day_tables(epi_net net, NetKeys nk, WorkTables wt, const uint16_t* __restrict__ codes,
-                             int64_t lo, int64_t hi) {
+// Per-day tables.  Blocks [0, wblocks) own the workplace member slots (one
+// thread each: member_at_pos / pos_of / shift, and wcode in fused mode);
+// the remaining blocks own agent rows [lo, hi) for the random push tables:
+// each warp takes 32 agents, flattens their (agent, slot j < n_a) work items
+// with a warp prefix sum and evaluates them 32 at a time (no idle lanes),
+// writing rout[a][j] = code(pi_j(a)) and scattering rin[pi_j(a)][j] = code(a)
+// (conflict-free: pi_j is a bijection).
+__global__ void __launch_bounds__(256) k_day_tables(epi_net net, NetKeys nk, WorkTables wt,
+                                                    const uint16_t* __restrict__ codes, int64_t lo,
+                                                    int64_t hi, int wblocks, const NetTables* __restrict__ NTp,
+                                                    NetTables* __restrict__ NTnext, uint64_t rperm_next) {
   __shared__ NetTables NT;
-  build_net_tables(NT, net, nk.rperm);
+  __shared__ int excl_s[8][32];
+  load_net_tables(NT, NTp);
   __syncthreads();
+  // tomorrow's random-slot keys (the other buffer; nobody reads it today)
+  if (blockIdx.x == 0 && threadIdx.x < EPI_MAX_SLOTS)
+    NTnext->rk[threadIdx.x] = random_slot_keys(rperm_next, threadIdx.x);
   const int draws = net.colleague_draws;
-  const int64_t n_rows = wt.rin ? hi - lo : 0;
-  const int64_t total = net.n_member_slots > n_rows ? net.n_member_slots : n_rows;
-  const Radix dn = make_radix((uint32_t)net.n_agents);
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    if (i < net.n_member_slots && draws > 0) {
+  if ((int)blockIdx.x < wblocks) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < net.n_member_slots;
+         i += (int64_t)wblocks * blockDim.x) {
+      if (draws <= 0) break;
       const int32_t c = net.wp_members[i];
       const int w = net.wp_id[c];
       const int base = net.wp_base[w];
@@ -525,29 +561,51 @@ __global__ void k_day_tables(epi_net net, NetKeys nk, WorkTables wt, const uint1
       wt.member_at_pos[i] = who;
       if (wt.wcode) wt.wcode[i] = codes[who];
     }
-    if (i < n_rows && net.n_agents >= 2) {
-      const uint32_t a = (uint32_t)(lo + i);
-      const uint16_t ca = codes[a];
-      const int na = code_count(ca);                // 0 for dead agents
-      const int nae = na < RT_SLOTS ? na : RT_SLOTS;
-      uint16_t row[RT_SLOTS];
-#pragma unroll
-      for (int j = 0; j < RT_SLOTS; ++j) row[j] = 0;
-#pragma unroll
-      for (int j = 0; j < RT_SLOTS; ++j) {
-        if (j < nae) {
-          const uint32_t y = walk_fwd(a, NT.rk[j], dn);
-          if (y != a) {
-            row[j] = codes[y] | CODE_PRESENT;
-            wt.rin[(size_t)y * RT_SLOTS + j] = ca | CODE_PRESENT;
-          }
-        }
-      }
-      uint4* out = (uint4*)(wt.rout + (size_t)a * RT_SLOTS);
-      const uint4* rv = (const uint4*)row;
-      out[0] = rv[0];
-      out[1] = rv[1];
+    return;
+  }
+  if (wt.rin == nullptr || net.n_agents < 2) return;
+  const Radix dn = NT.dn;
+  const int warp = threadIdx.x >> 5, lane = lane_id();
+  const int64_t n_tiles = (hi - lo + 31) / 32;
+  const int64_t warps_total = (int64_t)(gridDim.x - wblocks) * (blockDim.x >> 5);
+  for (int64_t tile = (blockIdx.x - wblocks) * (int64_t)(blockDim.x >> 5) + warp; tile < n_tiles;
+       tile += warps_total) {
+    const int64_t base = lo + tile * 32;
+    const int64_t a = base + lane;
+    uint16_t ca = 0;
+    int na = 0;
+    if (a < hi) {
+      ca = codes[a];
+      na = code_count(ca);
+      na = na < RT_SLOTS ? na : RT_SLOTS;
+      uint4* row = (uint4*)(wt.rout + (size_t)a * RT_SLOTS);
+      row[0] = make_uint4(0, 0, 0, 0);
+      row[1] = make_uint4(0, 0, 0, 0);
     }
+    int incl = na;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+    excl_s[warp][lane] = incl - na;
+    __syncwarp();
+    for (int k = lane; k < total; k += 32) {
+      int l = 0;                                    // owner: last lane with excl <= k
+#pragma unroll
+      for (int step = 16; step >= 1; step >>= 1)
+        if (l + step < 32 && excl_s[warp][l + step] <= k) l += step;
+      const int j = k - excl_s[warp][l];
+      const uint32_t src = (uint32_t)(base + l);
+      const uint32_t y = walk_fwd(src, NT.rk[j], dn);
+      if (y != src) {
+        const uint16_t csrc = codes[src];
+        wt.rin[(size_t)y * RT_SLOTS + j] = csrc | CODE_PRESENT;
+        wt.rout[(size_t)src * RT_SLOTS + j] = codes[y] | CODE_PRESENT;
+      }
+    }
+    __syncwarp();
   }
 }
 
