@@ -350,10 +350,12 @@ def kernel_profile(sim, mode):
     total_ms = sum(gen) + sum(pas)
     kernels = {}
     if mode == "csr":
-        # K3 generator writes 4 B per edge + 4 B row length + reads 2 B code/agent
-        # K12 message pass + update: SURVEY §8(d) B_K1 = 4E + 10N (+16N state r/w)
-        b_gen = 4 * E + 6 * n
-        b_pass = 4 * E + 10 * n + 16 * n
+        # generator writes a 2 B pre-joined message per edge + 4 B row length
+        # and reads 2 B code/agent; message pass + update streams the 2 B
+        # messages: B_K1 = 2E + 10N (SURVEY §8(d) with 2-byte messages instead
+        # of 4-byte src ids, no code gathers) + 16N state r/w
+        b_gen = 2 * E + 6 * n
+        b_pass = 2 * E + 10 * n + 16 * n
         kernels["k_day_tables+k_net_realize"] = {"ms_per_launch": sum(gen) / len(gen),
                                     "share": sum(gen) / total_ms,
                                     "alg_GBps": float(np.sum(b_gen) / (sum(gen) / 1e3) / 1e9)}

@@ -100,6 +100,7 @@ struct epi_ctx {
   epi_net* net_dev = nullptr;
   int net_slots = 0;
   std::vector<uint32_t*> net_entries;
+  uint16_t* net_msgs = nullptr;      // fp32 csr mode: pre-joined messages (one slot)
   std::vector<int32_t*> net_rowlen;
   std::vector<int32_t> net_slot_step;
   MsgTables* msg_dev = nullptr;      // fp32 message tables (rate_scale baked in)
@@ -277,6 +278,7 @@ int epi_destroy(epi_ctx* c) {
   for (auto& s : c->ring) { cudaFree(s.src); cudaFree(s.dst); }
   for (auto* p : c->net_entries) cudaFree(p);
   for (auto* p : c->net_rowlen) cudaFree(p);
+  cudaFree(c->net_msgs);
   delete c;
   return 0;
 }
@@ -358,7 +360,7 @@ int epi_gather(epi_ctx* c, const epi_state* st, int32_t step, int32_t precision,
   k_codes<<<grid_for(c->n, 256), 256, 0, s>>>(c->P, *st, step, nullptr, 0, c->codes, 0, c->n);
   CKL();
   StepArgs A = make_args(c, st, step, 0, c->scratch_rec, nullptr, false);
-  CsrView g{c->entries, c->row_len, c->row_begin, 0};
+  CsrView g{c->entries, c->row_len, c->row_begin, 0, nullptr};
   const int grid = grid_for(c->n, 256);
   if (precision == EPI_F64_CANONICAL)
     k_pass<true, 0><<<grid, 256, 0, s>>>(A, g, c->codes, lam_out, c->host.rate_scale, 0, nullptr, nullptr, 0,
@@ -414,7 +416,7 @@ static int step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t see
   } else {
     k_codes<<<grid, 256, 0, s>>>(c->P, *st, step, nullptr, 0, c->codes, 0, c->n);
     CKL();
-    CsrView g{c->entries, c->row_len, c->row_begin, 0};
+    CsrView g{c->entries, c->row_len, c->row_begin, 0, nullptr};
     k_pass<true, 1><<<grid, 256, 0, s>>>(A, g, c->codes, nullptr, c->host.rate_scale, iv ? 0 : 1,
                                          nullptr, nullptr, 0, c->msg_dev);
   }
@@ -495,7 +497,7 @@ static int prepare_realize(const epi_net* net) {
 }
 
 static int launch_realize(const epi_net* net, uint64_t g, int32_t step, const uint16_t* codes,
-                          uint32_t* entries, int32_t* row_len, int sort_rows, long long* rec,
+                          uint32_t* entries, uint16_t* msgs, int32_t* row_len, int sort_rows, long long* rec,
                           const WorkTables* wt, int64_t lo, int64_t hi, cudaStream_t s,
                           const NetTables* ntab_dev = nullptr) {
   const size_t smem = realize_smem(net);
@@ -513,11 +515,11 @@ static int launch_realize(const epi_net* net, uint64_t g, int32_t step, const ui
   const int grid = grid_for(hi - lo, 128, 16);
   const bool batch = batched(net);
   if (sort_rows) {
-    if (batch) k_net_realize<true, true><<<grid, 128, smem, s>>>(*net, nk, codes, entries, row_len, rec, wt, lo, hi, ntab_dev);
-    else k_net_realize<true, false><<<grid, 128, smem, s>>>(*net, nk, codes, entries, row_len, rec, wt, lo, hi, ntab_dev);
+    if (batch) k_net_realize<true, true><<<grid, 128, smem, s>>>(*net, nk, codes, entries, msgs, row_len, rec, wt, lo, hi, ntab_dev);
+    else k_net_realize<true, false><<<grid, 128, smem, s>>>(*net, nk, codes, entries, msgs, row_len, rec, wt, lo, hi, ntab_dev);
   } else {
-    if (batch) k_net_realize<false, true><<<grid, 128, smem, s>>>(*net, nk, codes, entries, row_len, rec, wt, lo, hi, ntab_dev);
-    else k_net_realize<false, false><<<grid, 128, smem, s>>>(*net, nk, codes, entries, row_len, rec, wt, lo, hi, ntab_dev);
+    if (batch) k_net_realize<false, true><<<grid, 128, smem, s>>>(*net, nk, codes, entries, msgs, row_len, rec, wt, lo, hi, ntab_dev);
+    else k_net_realize<false, false><<<grid, 128, smem, s>>>(*net, nk, codes, entries, msgs, row_len, rec, wt, lo, hi, ntab_dev);
   }
   CKL();
   return 0;
@@ -530,7 +532,7 @@ int epi_net_realize(const epi_net* net, uint64_t graph_seed, int32_t step, const
   if (!codes || !entries || !row_len) return fail(EPI_EARG, "null buffer");
   rc = prepare_realize(net);
   if (rc) return rc;
-  return launch_realize(net, graph_seed, step, codes, entries, row_len, sort_rows, nullptr, nullptr,
+  return launch_realize(net, graph_seed, step, codes, entries, nullptr, row_len, sort_rows, nullptr, nullptr,
                         0, net->n_agents, S(stream));
 }
 
@@ -562,6 +564,8 @@ int epi_net_attach(epi_ctx* c, const epi_net* net) {
     if (!rc) rc = dalloc(&c->net_rowlen[i], (size_t)c->n);
     if (rc) return rc;
   }
+  rc = dalloc(&c->net_msgs, (size_t)c->n * net->row_cap + 4);
+  if (rc) return rc;
   rc = dalloc(&c->wt_host.member_at_pos, (size_t)net->n_member_slots);
   if (!rc) rc = dalloc(&c->wt_host.pos_of, (size_t)net->n_member_slots);
   if (!rc) rc = dalloc(&c->wt_host.shift, (size_t)net->n_workplaces * (net->colleague_draws + 1));
@@ -641,14 +645,18 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
   }
   const WorkTables* wt = use_wt ? c->wt_dev : nullptr;
   if (mode == 0) {
-    uint32_t* entries = c->net_entries[slot];
+    // fp32 without contact log: the generator writes pre-joined messages and
+    // the message pass streams them; otherwise ids (export, DEN, fp64 order)
+    const bool msg_only = precision == EPI_F32 && !c->host.den_enabled;
+    uint32_t* entries = msg_only ? nullptr : c->net_entries[slot];
+    uint16_t* msgs = msg_only ? c->net_msgs : nullptr;
     int32_t* row_len = c->net_rowlen[slot];
-    int rc = launch_realize(&c->net, seed, step, codes_cur, entries, row_len,
+    int rc = launch_realize(&c->net, seed, step, codes_cur, entries, msgs, row_len,
                             precision == EPI_F64_CANONICAL, nullptr, wt, c->lo, c->hi, s, nt_today);
     if (rc) return rc;
-    c->net_slot_step[slot] = step;
+    c->net_slot_step[slot] = msg_only ? -1 : step;
     if (ev) CK(cudaEventRecord((cudaEvent_t)ev[1], s));
-    CsrView g{entries, row_len, nullptr, c->net.row_cap};
+    CsrView g{entries, row_len, nullptr, c->net.row_cap, msgs};
     if (precision == EPI_F64_CANONICAL)
       k_pass<true, 1><<<grid, 256, 0, s>>>(A, g, codes_cur, nullptr, c->host.rate_scale, iv ? 0 : 1,
                                            codes_next, c->net_dev, rcount_next, c->msg_dev);

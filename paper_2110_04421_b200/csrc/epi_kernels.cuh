@@ -256,6 +256,10 @@ struct CsrView {
   const int32_t* __restrict__ row_len;
   const int64_t* __restrict__ row_begin;   // null: padded rows of `cap`
   int cap;
+  // Optional pre-joined messages (padded rows, same layout as entries):
+  // msg = (source code & 0xFF) | kind << 8, written by the generator, so the
+  // fp32 message pass streams 2 B per edge with no gathers.
+  const uint16_t* __restrict__ msgs;
   __device__ __forceinline__ int64_t begin(int64_t r) const {
     return row_begin ? row_begin[r] : r * (int64_t)cap;
   }
@@ -314,7 +318,19 @@ __global__ void __launch_bounds__(256) k_pass(StepArgs A, CsrView g, const uint1
       for (int r4 = 0; r4 < 8; ++r4) {
         const int64_t row = base + r4 * 4 + grp;
         float acc = 0.f;
-        if (row < n) {
+        if (row < n && g.msgs != nullptr) {
+          // streaming: lane gl reads 4 consecutive messages (8 B) per pass
+          const int len = g.row_len[row];
+          const uint16_t* mrow = g.msgs + row * (int64_t)g.cap;
+          for (int i0 = 4 * gl; i0 < len; i0 += 32) {
+            const uint2 v = *(const uint2*)(mrow + i0);
+            const uint16_t m4[4] = {(uint16_t)v.x, (uint16_t)(v.x >> 16), (uint16_t)v.y,
+                                    (uint16_t)(v.y >> 16)};
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              if (i0 + q < len) acc += T.factor[m4[q] & 0xFF] * T.bfac[m4[q] >> 8];
+          }
+        } else if (row < n) {
           const int len = g.row_len[row];
           const uint32_t* e = g.entries + g.begin(row);
           // 8 lanes x 4 entries in flight per pass, then their 4 code gathers
@@ -413,6 +429,7 @@ __device__ __forceinline__ void clear_rin_row(const WorkTables* wt, int64_t b) {
 template <bool SORT, bool BATCH>
 __global__ void __launch_bounds__(128, 6) k_net_realize(epi_net net, NetKeys nk, const uint16_t* __restrict__ codes,
                                                      uint32_t* __restrict__ entries,
+                                                     uint16_t* __restrict__ msgs,
                                                      int32_t* __restrict__ row_len, long long* rec,
                                                      const WorkTables* wt, int64_t lo, int64_t hi,
                                                      const NetTables* __restrict__ NTp) {
@@ -438,7 +455,12 @@ __global__ void __launch_bounds__(128, 6) k_net_realize(epi_net net, NetKeys nk,
     if (b < n) {
       const uint16_t cb = codes[b];
       if (!code_dead(cb)) {
-        auto put = [&](int64_t c, int kind, uint16_t) { mine[cnt++] = ((uint32_t)c << 2) | (uint32_t)kind; };
+        // the staging row holds either ids (src<<2|kind) or messages
+        // ((code & 0xFF) | kind<<8) when only messages are requested
+        auto put = [&](int64_t c, int kind, uint16_t cc) {
+          mine[cnt++] = entries ? (((uint32_t)c << 2) | (uint32_t)kind)
+                                : ((uint32_t)(cc & 0xFF) | ((uint32_t)kind << 8));
+        };
         if (BATCH) for_each_in_edge_batched<16, 8>(net, nk, NT.rk, NT.wrad, wt, codes, b, cb, put);
         else for_each_in_edge(net, nk, NT.rk, NT.wrad, codes, b, cb, 0, 1, put);
       }
@@ -457,9 +479,14 @@ __global__ void __launch_bounds__(128, 6) k_net_realize(epi_net net, NetKeys nk,
     const int rows = (n - base) < 32 ? (int)(n - base) : 32;
     for (int r = 0; r < rows; ++r) {
       const int len = __shfl_sync(0xFFFFFFFFu, cnt, r);
-      uint32_t* dst = entries + (base + r) * (int64_t)cap;
       const uint32_t* srcrow = wbuf + r * stride_w;
-      for (int i = lane; i < len; i += 32) dst[i] = srcrow[i];
+      if (entries) {
+        uint32_t* dst = entries + (base + r) * (int64_t)cap;
+        for (int i = lane; i < len; i += 32) dst[i] = srcrow[i];
+      } else {
+        uint16_t* dst = msgs + (base + r) * (int64_t)cap;
+        for (int i = lane; i < len; i += 32) dst[i] = (uint16_t)srcrow[i];
+      }
     }
     __syncwarp();
   }
