@@ -245,6 +245,17 @@ int epi_sim_step_timed(epi_ctx *ctx, const epi_state *st, int32_t step, uint64_t
                        uint16_t *codes_next, int64_t *record, int32_t *vax_open,
                        void *const *events4, void *stream);
 
+/* The north-star decomposition of one day, as separate launches:
+ *   (c) epi_net_generate: day tables + generator writing the pre-joined
+ *       16-bit message CSR of day `step` (ctx-owned, padded rows);
+ *   (a) epi_net_gather: the message pass alone, hazard float[N] out
+ *       (engine.py:77-117 on the config networks, fp32 fast mode);
+ *       `record` (nullable) receives the edge count. */
+int epi_net_generate(epi_ctx *ctx, int32_t step, uint64_t seed, const uint16_t *codes_cur,
+                     void *stream);
+int epi_net_gather(epi_ctx *ctx, const epi_state *st, int32_t step, const uint16_t *codes_cur,
+                   float *lambda_out, int64_t *record, void *stream);
+
 /* Device pointers of the CSR slot written for `step` (mode 0), for export. */
 int epi_net_csr(epi_ctx *ctx, int32_t step, uint32_t **entries, int32_t **row_len);
 

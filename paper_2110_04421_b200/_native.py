@@ -85,6 +85,8 @@ _SIGS = {
     "epi_sim_step": (_i32, [_p, C.POINTER(EpiState), _i32, _u64, _i32, _i32, _p, _p, _p, _p, _p]),
     "epi_sim_step_timed": (_i32, [_p, C.POINTER(EpiState), _i32, _u64, _i32, _i32, _p, _p, _p, _p,
                                   _p, _p]),
+    "epi_net_generate": (_i32, [_p, _i32, _u64, _p, _p]),
+    "epi_net_gather": (_i32, [_p, C.POINTER(EpiState), _i32, _p, _p, _p, _p]),
     "epi_net_csr": (_i32, [_p, _i32, C.POINTER(_p), C.POINTER(_p)]),
     "epi_seed_infections": (_i32, [_p, C.POINTER(EpiState), _u64, _p, _i64, _p]),
     "epi_assign_app": (_i32, [C.POINTER(EpiState), _u64, _d, _p]),

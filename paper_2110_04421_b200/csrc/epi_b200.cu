@@ -705,6 +705,46 @@ int epi_sim_step_timed(epi_ctx* c, const epi_state* st, int32_t step, uint64_t s
                        events4, stream);
 }
 
+int epi_net_generate(epi_ctx* c, int32_t step, uint64_t seed, const uint16_t* codes_cur, void* stream) {
+  if (!c || !c->has_net || !codes_cur) return fail(EPI_EARG, "needs an attached network and codes");
+  if (!batched(&c->net)) return fail(EPI_EARG, "epi_net_generate needs <= 16 slots and <= 8 draws");
+  cudaStream_t s = S(stream);
+  const NetKeys nk = make_net_keys(seed, step);
+  NetTables* nt = c->ntab_dev[step & 1];
+  k_day_keys<<<1, 32, 0, s>>>(nt, nk.rperm);
+  CKL();
+  const bool has_work = c->net.n_member_slots > 0 && c->net.colleague_draws > 0;
+  WorkTables w = c->wt_host;
+  w.wcode = nullptr;
+  w.rin = nullptr;
+  w.rout = nullptr;
+  if (c->wt_whole != 0) {
+    CK(cudaMemcpyAsync(c->wt_dev, &w, sizeof(WorkTables), cudaMemcpyHostToDevice, s));
+    c->wt_whole = 0;
+  }
+  if (has_work) {
+    k_day_tables<<<grid_for(c->net.n_member_slots, 256, 4), 256, 0, s>>>(
+        c->net, nk, w, codes_cur, c->lo, c->hi, grid_for(c->net.n_member_slots, 256, 4), nt,
+        c->ntab_dev[(step + 1) & 1], key_prefix(seed, step + 1, P_NET_RPERM));
+    CKL();
+  }
+  return launch_realize(&c->net, seed, step, codes_cur, nullptr, c->net_msgs, c->net_rowlen[0], 0,
+                        nullptr, has_work ? c->wt_dev : nullptr, c->lo, c->hi, s, nt);
+}
+
+int epi_net_gather(epi_ctx* c, const epi_state* st, int32_t step, const uint16_t* codes_cur,
+                   float* lambda_out, int64_t* record, void* stream) {
+  if (!c || !c->has_net || !st || !lambda_out) return fail(EPI_EARG, "null argument");
+  long long* rec = record ? (long long*)record : c->scratch_rec;
+  if (record) CK(cudaMemsetAsync(rec, 0, EPI_REC_LEN * sizeof(long long), S(stream)));
+  StepArgs A = make_args(c, st, step, 0, rec, nullptr, false);
+  CsrView g{nullptr, c->net_rowlen[0], nullptr, c->net.row_cap, c->net_msgs};
+  k_pass<false, 0><<<grid_for(c->hi - c->lo, 256), 256, 0, S(stream)>>>(
+      A, g, codes_cur, lambda_out, c->host.rate_scale, 0, nullptr, nullptr, 0, c->msg_dev);
+  CKL();
+  return 0;
+}
+
 int epi_seed_infections(epi_ctx* c, const epi_state* st, uint64_t seed, const int64_t* ids, int64_t n,
                         void* stream) {
   if (!c || !st) return fail(EPI_EARG, "null argument");

@@ -113,3 +113,21 @@ def test_fused_and_csr_f32_agree_and_graph_replay_is_identical():
     b.capture()
     b.replay()
     assert np.array_equal(b.records(), rb)
+
+
+def test_message_pass_alone_within_1e5_of_reference_hazard():
+    """North-star part (a) alone: generator -> 16-bit messages -> fp32 hazard,
+    vs the reference gather (oracle, fp64) on the same generated graph."""
+    from paper_2110_04421_b200 import roofline
+    sim = roofline.prepare(20_000, warm_days=25)
+    t = sim.clock
+    lam = torch.empty(sim.n, dtype=torch.float32, device="cuda")
+    roofline.gather(sim, lam)
+    cols = sim.host_columns()
+    src, dst, kind = confignet_np.realize(sim.population, sim.seed, t, cols.stage == 10)
+    ref = engine_np.hazard(cols, sim.disease, t, StepGraph(t, src, dst, kind), True)
+    got = lam.cpu().numpy().astype(np.float64)
+    nz = ref > 0
+    assert nz.sum() > 100
+    assert np.all(np.abs(got[nz] - ref[nz]) <= 1e-5 * ref[nz])
+    assert np.all(got[~nz] == 0)
