@@ -100,7 +100,8 @@ struct epi_ctx {
   epi_net* net_dev = nullptr;
   int net_slots = 0;
   std::vector<uint32_t*> net_entries;
-  uint16_t* net_msgs = nullptr;      // fp32 csr mode: pre-joined messages (one slot)
+  uint16_t* net_msgs = nullptr;      // fp32 csr mode: tile-packed pre-joined messages
+  uint16_t* net_toff = nullptr;      // per-tile row offsets (33 per tile of 32 rows)
   std::vector<int32_t*> net_rowlen;
   std::vector<int32_t> net_slot_step;
   MsgTables* msg_dev = nullptr;      // fp32 message tables (rate_scale baked in)
@@ -279,6 +280,7 @@ int epi_destroy(epi_ctx* c) {
   for (auto* p : c->net_entries) cudaFree(p);
   for (auto* p : c->net_rowlen) cudaFree(p);
   cudaFree(c->net_msgs);
+  cudaFree(c->net_toff);
   delete c;
   return 0;
 }
@@ -360,7 +362,7 @@ int epi_gather(epi_ctx* c, const epi_state* st, int32_t step, int32_t precision,
   k_codes<<<grid_for(c->n, 256), 256, 0, s>>>(c->P, *st, step, nullptr, 0, c->codes, 0, c->n);
   CKL();
   StepArgs A = make_args(c, st, step, 0, c->scratch_rec, nullptr, false);
-  CsrView g{c->entries, c->row_len, c->row_begin, 0, nullptr};
+  CsrView g{c->entries, c->row_len, c->row_begin, 0, nullptr, nullptr};
   const int grid = grid_for(c->n, 256);
   if (precision == EPI_F64_CANONICAL)
     k_pass<true, 0><<<grid, 256, 0, s>>>(A, g, c->codes, lam_out, c->host.rate_scale, 0, nullptr, nullptr, 0,
@@ -416,7 +418,7 @@ static int step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t see
   } else {
     k_codes<<<grid, 256, 0, s>>>(c->P, *st, step, nullptr, 0, c->codes, 0, c->n);
     CKL();
-    CsrView g{c->entries, c->row_len, c->row_begin, 0, nullptr};
+    CsrView g{c->entries, c->row_len, c->row_begin, 0, nullptr, nullptr};
     k_pass<true, 1><<<grid, 256, 0, s>>>(A, g, c->codes, nullptr, c->host.rate_scale, iv ? 0 : 1,
                                          nullptr, nullptr, 0, c->msg_dev);
   }
@@ -491,13 +493,17 @@ static int prepare_realize(const epi_net* net) {
     CK(cudaFuncSetAttribute(k_net_realize<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     CK(cudaFuncSetAttribute(k_net_realize<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     CK(cudaFuncSetAttribute(k_net_realize<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int psmem = 8 * 32 * net->row_cap * (int)sizeof(uint16_t);
+    CK(cudaFuncSetAttribute(k_pass<false, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, psmem));
+    CK(cudaFuncSetAttribute(k_pass<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, psmem));
     g_realize_smem_set = smem;
   }
   return 0;
 }
 
 static int launch_realize(const epi_net* net, uint64_t g, int32_t step, const uint16_t* codes,
-                          uint32_t* entries, uint16_t* msgs, int32_t* row_len, int sort_rows, long long* rec,
+                          uint32_t* entries, uint16_t* msgs, uint16_t* toff, int32_t* row_len, int sort_rows,
+                          long long* rec,
                           const WorkTables* wt, int64_t lo, int64_t hi, cudaStream_t s,
                           const NetTables* ntab_dev = nullptr) {
   const size_t smem = realize_smem(net);
@@ -515,11 +521,11 @@ static int launch_realize(const epi_net* net, uint64_t g, int32_t step, const ui
   const int grid = grid_for(hi - lo, 128, 16);
   const bool batch = batched(net);
   if (sort_rows) {
-    if (batch) k_net_realize<true, true><<<grid, 128, smem, s>>>(*net, nk, codes, entries, msgs, row_len, rec, wt, lo, hi, ntab_dev);
-    else k_net_realize<true, false><<<grid, 128, smem, s>>>(*net, nk, codes, entries, msgs, row_len, rec, wt, lo, hi, ntab_dev);
+    if (batch) k_net_realize<true, true><<<grid, 128, smem, s>>>(*net, nk, codes, entries, msgs, toff, row_len, rec, wt, lo, hi, ntab_dev);
+    else k_net_realize<true, false><<<grid, 128, smem, s>>>(*net, nk, codes, entries, msgs, toff, row_len, rec, wt, lo, hi, ntab_dev);
   } else {
-    if (batch) k_net_realize<false, true><<<grid, 128, smem, s>>>(*net, nk, codes, entries, msgs, row_len, rec, wt, lo, hi, ntab_dev);
-    else k_net_realize<false, false><<<grid, 128, smem, s>>>(*net, nk, codes, entries, msgs, row_len, rec, wt, lo, hi, ntab_dev);
+    if (batch) k_net_realize<false, true><<<grid, 128, smem, s>>>(*net, nk, codes, entries, msgs, toff, row_len, rec, wt, lo, hi, ntab_dev);
+    else k_net_realize<false, false><<<grid, 128, smem, s>>>(*net, nk, codes, entries, msgs, toff, row_len, rec, wt, lo, hi, ntab_dev);
   }
   CKL();
   return 0;
@@ -532,7 +538,8 @@ int epi_net_realize(const epi_net* net, uint64_t graph_seed, int32_t step, const
   if (!codes || !entries || !row_len) return fail(EPI_EARG, "null buffer");
   rc = prepare_realize(net);
   if (rc) return rc;
-  return launch_realize(net, graph_seed, step, codes, entries, nullptr, row_len, sort_rows, nullptr, nullptr,
+  return launch_realize(net, graph_seed, step, codes, entries, nullptr, nullptr, row_len, sort_rows, nullptr,
+                        nullptr,
                         0, net->n_agents, S(stream));
 }
 
@@ -564,7 +571,8 @@ int epi_net_attach(epi_ctx* c, const epi_net* net) {
     if (!rc) rc = dalloc(&c->net_rowlen[i], (size_t)c->n);
     if (rc) return rc;
   }
-  rc = dalloc(&c->net_msgs, (size_t)c->n * net->row_cap + 4);
+  rc = dalloc(&c->net_msgs, (size_t)((c->n + 31) / 32) * 32 * net->row_cap + 16);
+  if (!rc) rc = dalloc(&c->net_toff, (size_t)((c->n + 31) / 32) * 33);
   if (rc) return rc;
   rc = dalloc(&c->wt_host.member_at_pos, (size_t)net->n_member_slots);
   if (!rc) rc = dalloc(&c->wt_host.pos_of, (size_t)net->n_member_slots);
@@ -651,18 +659,19 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
     uint32_t* entries = msg_only ? nullptr : c->net_entries[slot];
     uint16_t* msgs = msg_only ? c->net_msgs : nullptr;
     int32_t* row_len = c->net_rowlen[slot];
-    int rc = launch_realize(&c->net, seed, step, codes_cur, entries, msgs, row_len,
+    int rc = launch_realize(&c->net, seed, step, codes_cur, entries, msgs, c->net_toff, row_len,
                             precision == EPI_F64_CANONICAL, nullptr, wt, c->lo, c->hi, s, nt_today);
     if (rc) return rc;
     c->net_slot_step[slot] = msg_only ? -1 : step;
     if (ev) CK(cudaEventRecord((cudaEvent_t)ev[1], s));
-    CsrView g{entries, row_len, nullptr, c->net.row_cap, msgs};
+    CsrView g{entries, row_len, nullptr, c->net.row_cap, msgs, c->net_toff};
+    const size_t msmem = msgs ? (size_t)8 * 32 * c->net.row_cap * sizeof(uint16_t) : 0;
     if (precision == EPI_F64_CANONICAL)
       k_pass<true, 1><<<grid, 256, 0, s>>>(A, g, codes_cur, nullptr, c->host.rate_scale, iv ? 0 : 1,
                                            codes_next, c->net_dev, rcount_next, c->msg_dev);
     else
-      k_pass<false, 1><<<grid, 256, 0, s>>>(A, g, codes_cur, nullptr, c->host.rate_scale, iv ? 0 : 1,
-                                            codes_next, c->net_dev, rcount_next, c->msg_dev);
+      k_pass<false, 1><<<grid, 256, msmem, s>>>(A, g, codes_cur, nullptr, c->host.rate_scale, iv ? 0 : 1,
+                                                codes_next, c->net_dev, rcount_next, c->msg_dev);
     CKL();
   } else {
     if (ev) CK(cudaEventRecord((cudaEvent_t)ev[1], s));
@@ -728,8 +737,8 @@ int epi_net_generate(epi_ctx* c, int32_t step, uint64_t seed, const uint16_t* co
         c->ntab_dev[(step + 1) & 1], key_prefix(seed, step + 1, P_NET_RPERM));
     CKL();
   }
-  return launch_realize(&c->net, seed, step, codes_cur, nullptr, c->net_msgs, c->net_rowlen[0], 0,
-                        nullptr, has_work ? c->wt_dev : nullptr, c->lo, c->hi, s, nt);
+  return launch_realize(&c->net, seed, step, codes_cur, nullptr, c->net_msgs, c->net_toff,
+                        c->net_rowlen[0], 0, nullptr, has_work ? c->wt_dev : nullptr, c->lo, c->hi, s, nt);
 }
 
 int epi_net_gather(epi_ctx* c, const epi_state* st, int32_t step, const uint16_t* codes_cur,
@@ -738,8 +747,9 @@ int epi_net_gather(epi_ctx* c, const epi_state* st, int32_t step, const uint16_t
   long long* rec = record ? (long long*)record : c->scratch_rec;
   if (record) CK(cudaMemsetAsync(rec, 0, EPI_REC_LEN * sizeof(long long), S(stream)));
   StepArgs A = make_args(c, st, step, 0, rec, nullptr, false);
-  CsrView g{nullptr, c->net_rowlen[0], nullptr, c->net.row_cap, c->net_msgs};
-  k_pass<false, 0><<<grid_for(c->hi - c->lo, 256), 256, 0, S(stream)>>>(
+  CsrView g{nullptr, c->net_rowlen[0], nullptr, c->net.row_cap, c->net_msgs, c->net_toff};
+  const size_t msmem = (size_t)8 * 32 * c->net.row_cap * sizeof(uint16_t);
+  k_pass<false, 0><<<grid_for(c->hi - c->lo, 256), 256, msmem, S(stream)>>>(
       A, g, codes_cur, lambda_out, c->host.rate_scale, 0, nullptr, nullptr, 0, c->msg_dev);
   CKL();
   return 0;

@@ -256,10 +256,13 @@ struct CsrView {
   const int32_t* __restrict__ row_len;
   const int64_t* __restrict__ row_begin;   // null: padded rows of `cap`
   int cap;
-  // Optional pre-joined messages (padded rows, same layout as entries):
-  // msg = (source code & 0xFF) | kind << 8, written by the generator, so the
-  // fp32 message pass streams 2 B per edge with no gathers.
+  // Optional pre-joined messages, tile-packed: msg = (source code & 0xFF) |
+  // kind << 8, written by the generator, so the fp32 message pass streams
+  // 2 B per edge with no gathers.  Tile k (32 rows from lo) owns the block
+  // msgs[k*32*cap ...]; its rows are packed back to back and
+  // tile_off[k*33 + r] is row r's start (tile_off[k*33 + 32] = total).
   const uint16_t* __restrict__ msgs;
+  const uint16_t* __restrict__ tile_off;
   __device__ __forceinline__ int64_t begin(int64_t r) const {
     return row_begin ? row_begin[r] : r * (int64_t)cap;
   }
@@ -276,6 +279,7 @@ __global__ void __launch_bounds__(256) k_pass(StepArgs A, CsrView g, const uint1
   __shared__ MsgTables T;
   __shared__ float lam_tile[8][32];
   __shared__ RecAcc racc;
+  extern __shared__ uint16_t msg_smem[];        // 8 warps x 32 rows x cap (msgs path)
   if (!F64) {
     if (mt) load_msg_tables(T, mt);
     else build_msg_tables(T, A.P, rate);
@@ -311,6 +315,30 @@ __global__ void __launch_bounds__(256) k_pass(StepArgs A, CsrView g, const uint1
           lam = h;
         }
       }
+    } else if (g.msgs != nullptr) {
+      // tile-packed messages: one coalesced copy of the tile's block into
+      // shared memory (16-byte vector loads), then one lane per row
+      const uint16_t* toff = g.tile_off + tile * 33;
+      const int my_lo = toff[lane];
+      const int total = toff[32];
+      const int nxt = __shfl_down_sync(0xFFFFFFFFu, my_lo, 1);
+      const int my_hi = lane < 31 ? nxt : total;
+      const uint4* blk = (const uint4*)(g.msgs + tile * (int64_t)(32 * g.cap));
+      uint4* sm = (uint4*)(msg_smem + (size_t)warp * 32 * g.cap);
+      const int nchunk = (total * 2 + 15) >> 4;
+      for (int c = lane; c < nchunk; c += 32) sm[c] = __ldg(blk + c);
+      __syncwarp();
+      const uint16_t* sm16 = (const uint16_t*)sm;
+      float acc = 0.f;
+      for (int i = my_lo; i < my_hi; ++i) {
+        const uint16_t m = sm16[i];
+        acc += T.factor[m & 0xFF] * T.bfac[m >> 8];
+      }
+      __syncwarp();
+      if (valid) {
+        edges = (unsigned)(my_hi - my_lo);
+        lam = is_target(P, A.st, a) ? (double)(acc * T.sfac[A.st.age_band[a]]) : 0.0;
+      }
     } else {
       // 8 lanes per row, 4 rows per pass, tree sum in fp32
       const int grp = lane >> 3, gl = lane & 7;
@@ -318,19 +346,7 @@ __global__ void __launch_bounds__(256) k_pass(StepArgs A, CsrView g, const uint1
       for (int r4 = 0; r4 < 8; ++r4) {
         const int64_t row = base + r4 * 4 + grp;
         float acc = 0.f;
-        if (row < n && g.msgs != nullptr) {
-          // streaming: lane gl reads 4 consecutive messages (8 B) per pass
-          const int len = g.row_len[row];
-          const uint16_t* mrow = g.msgs + row * (int64_t)g.cap;
-          for (int i0 = 4 * gl; i0 < len; i0 += 32) {
-            const uint2 v = *(const uint2*)(mrow + i0);
-            const uint16_t m4[4] = {(uint16_t)v.x, (uint16_t)(v.x >> 16), (uint16_t)v.y,
-                                    (uint16_t)(v.y >> 16)};
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-              if (i0 + q < len) acc += T.factor[m4[q] & 0xFF] * T.bfac[m4[q] >> 8];
-          }
-        } else if (row < n) {
+        if (row < n) {
           const int len = g.row_len[row];
           const uint32_t* e = g.entries + g.begin(row);
           // 8 lanes x 4 entries in flight per pass, then their 4 code gathers
@@ -430,6 +446,7 @@ template <bool SORT, bool BATCH>
 __global__ void __launch_bounds__(128, 6) k_net_realize(epi_net net, NetKeys nk, const uint16_t* __restrict__ codes,
                                                      uint32_t* __restrict__ entries,
                                                      uint16_t* __restrict__ msgs,
+                                                     uint16_t* __restrict__ tile_off,
                                                      int32_t* __restrict__ row_len, long long* rec,
                                                      const WorkTables* wt, int64_t lo, int64_t hi,
                                                      const NetTables* __restrict__ NTp) {
@@ -472,20 +489,36 @@ __global__ void __launch_bounds__(128, 6) k_net_realize(epi_net net, NetKeys nk,
           mine[j + 1] = x;
         }
       }
-      row_len[b] = cnt;
+      if (entries) row_len[b] = cnt;
     }
     rec_add(racc, EPI_REC_EDGES, (unsigned)cnt);
     __syncwarp();
     const int rows = (n - base) < 32 ? (int)(n - base) : 32;
-    for (int r = 0; r < rows; ++r) {
-      const int len = __shfl_sync(0xFFFFFFFFu, cnt, r);
-      const uint32_t* srcrow = wbuf + r * stride_w;
-      if (entries) {
+    if (entries) {
+      for (int r = 0; r < rows; ++r) {
+        const int len = __shfl_sync(0xFFFFFFFFu, cnt, r);
+        const uint32_t* srcrow = wbuf + r * stride_w;
         uint32_t* dst = entries + (base + r) * (int64_t)cap;
         for (int i = lane; i < len; i += 32) dst[i] = srcrow[i];
-      } else {
-        uint16_t* dst = msgs + (base + r) * (int64_t)cap;
-        for (int i = lane; i < len; i += 32) dst[i] = (uint16_t)srcrow[i];
+      }
+    } else {
+      // tile-packed messages: rows back to back + per-tile offsets
+      int incl = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      const int excl = incl - cnt;
+      uint16_t* toff = tile_off + tile * 33;
+      toff[lane] = (uint16_t)excl;
+      if (lane == 31) toff[32] = (uint16_t)incl;
+      uint16_t* blk = msgs + tile * (int64_t)(32 * cap);
+      for (int r = 0; r < rows; ++r) {
+        const int len = __shfl_sync(0xFFFFFFFFu, cnt, r);
+        const int off = __shfl_sync(0xFFFFFFFFu, excl, r);
+        const uint32_t* srcrow = wbuf + r * stride_w;
+        for (int i = lane; i < len; i += 32) blk[off + i] = (uint16_t)srcrow[i];
       }
     }
     __syncwarp();
