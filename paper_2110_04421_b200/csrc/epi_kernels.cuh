@@ -79,6 +79,7 @@ struct MsgTables {
   float factor[256];
   float sfac[16];
   float bfac[4];
+  float comb[3 * 256];      // factor[idx] * bfac[kind] at [kind << 8 | idx]
 };
 inline void fill_msg_tables(MsgTables& T, const epi_params& P, double rate) {
   for (int i = 0; i < 256; ++i) {
@@ -91,6 +92,8 @@ inline void fill_msg_tables(MsgTables& T, const epi_params& P, double rate) {
   for (int i = 0; i < 16; ++i)
     T.sfac[i] = i < 9 ? (float)(P.age_susceptibility[i] / P.mean_daily_interactions) : 0.f;
   for (int i = 0; i < 4; ++i) T.bfac[i] = i < 3 ? (float)P.network_scale[i] : 0.f;
+  for (int k = 0; k < 3; ++k)
+    for (int i = 0; i < 256; ++i) T.comb[k * 256 + i] = T.factor[i] * T.bfac[k];
 }
 __device__ __forceinline__ void load_msg_tables(MsgTables& S, const MsgTables* __restrict__ G) {
   const uint32_t* src = (const uint32_t*)G;
@@ -109,6 +112,8 @@ __device__ __forceinline__ void build_msg_tables(MsgTables& T, const epi_params*
   for (int i = threadIdx.x; i < 9; i += blockDim.x)
     T.sfac[i] = (float)(P->age_susceptibility[i] / P->mean_daily_interactions);
   for (int i = threadIdx.x; i < 3; i += blockDim.x) T.bfac[i] = (float)P->network_scale[i];
+  __syncthreads();
+  for (int i = threadIdx.x; i < 3 * 256; i += blockDim.x) T.comb[i] = T.factor[i & 255] * T.bfac[i >> 8];
 }
 
 // fp64 term with the reference's pinned factor order (engine.py:100-107,
@@ -318,26 +323,41 @@ __global__ void __launch_bounds__(256) k_pass(StepArgs A, CsrView g, const uint1
     } else if (g.msgs != nullptr) {
       // tile-packed messages: one coalesced copy of the tile's block into
       // shared memory (16-byte vector loads), then one lane per row
+      // every global load of the tile is issued up front (one round trip):
+      // offsets, a fixed-size speculative copy of the block (3 x 16 B per
+      // lane = 768 messages; longer tiles fetch the rest) and the state bytes
       const uint16_t* toff = g.tile_off + tile * 33;
-      const int my_lo = toff[lane];
-      const int total = toff[32];
-      const int nxt = __shfl_down_sync(0xFFFFFFFFu, my_lo, 1);
-      const int my_hi = lane < 31 ? nxt : total;
       const uint4* blk = (const uint4*)(g.msgs + tile * (int64_t)(32 * g.cap));
       uint4* sm = (uint4*)(msg_smem + (size_t)warp * 32 * g.cap);
+      const int cap_chunks = (32 * g.cap * 2) >> 4;
+      const int my_lo = toff[lane];
+      const int total = toff[32];
+      uint4 v[3];
+#pragma unroll
+      for (int q = 0; q < 3; ++q)
+        if (lane + 32 * q < cap_chunks) v[q] = __ldg(blk + lane + 32 * q);
+      int stage_a = S_DEAD, imm_a = 0, age_a = 0;
+      if (valid) {
+        stage_a = A.st.stage[a];
+        imm_a = A.st.immune[a];
+        age_a = A.st.age_band[a];
+      }
+#pragma unroll
+      for (int q = 0; q < 3; ++q)
+        if (lane + 32 * q < cap_chunks) sm[lane + 32 * q] = v[q];
       const int nchunk = (total * 2 + 15) >> 4;
-      for (int c = lane; c < nchunk; c += 32) sm[c] = __ldg(blk + c);
+      for (int c = 96 + lane; c < nchunk; c += 32) sm[c] = __ldg(blk + c);
+      const int nxt = __shfl_down_sync(0xFFFFFFFFu, my_lo, 1);
+      const int my_hi = lane < 31 ? nxt : total;
       __syncwarp();
       const uint16_t* sm16 = (const uint16_t*)sm;
       float acc = 0.f;
-      for (int i = my_lo; i < my_hi; ++i) {
-        const uint16_t m = sm16[i];
-        acc += T.factor[m & 0xFF] * T.bfac[m >> 8];
-      }
+      for (int i = my_lo; i < my_hi; ++i) acc += T.comb[sm16[i] & 0x3FF];
       __syncwarp();
       if (valid) {
         edges = (unsigned)(my_hi - my_lo);
-        lam = is_target(P, A.st, a) ? (double)(acc * T.sfac[A.st.age_band[a]]) : 0.0;
+        const bool target = stage_a == S_SUS && !(P->sterilizing && imm_a);
+        lam = target ? (double)(acc * T.sfac[age_a]) : 0.0;
       }
     } else {
       // 8 lanes per row, 4 rows per pass, tree sum in fp32
