@@ -79,7 +79,8 @@ struct MsgTables {
   float factor[256];
   float sfac[16];
   float bfac[4];
-  float comb[3 * 256];      // factor[idx] * bfac[kind] at [kind << 8 | idx]
+  float comb[4 * 256];      // factor[idx] * bfac[kind] at [idx << 2 | kind] (zero
+                            // weights of the 3 kinds in banks 0-2: no conflicts)
 };
 inline void fill_msg_tables(MsgTables& T, const epi_params& P, double rate) {
   for (int i = 0; i < 256; ++i) {
@@ -92,8 +93,8 @@ inline void fill_msg_tables(MsgTables& T, const epi_params& P, double rate) {
   for (int i = 0; i < 16; ++i)
     T.sfac[i] = i < 9 ? (float)(P.age_susceptibility[i] / P.mean_daily_interactions) : 0.f;
   for (int i = 0; i < 4; ++i) T.bfac[i] = i < 3 ? (float)P.network_scale[i] : 0.f;
-  for (int k = 0; k < 3; ++k)
-    for (int i = 0; i < 256; ++i) T.comb[k * 256 + i] = T.factor[i] * T.bfac[k];
+  for (int i = 0; i < 256; ++i)
+    for (int k = 0; k < 4; ++k) T.comb[(i << 2) | k] = T.factor[i] * T.bfac[k];
 }
 __device__ __forceinline__ void load_msg_tables(MsgTables& S, const MsgTables* __restrict__ G) {
   const uint32_t* src = (const uint32_t*)G;
@@ -113,7 +114,7 @@ __device__ __forceinline__ void build_msg_tables(MsgTables& T, const epi_params*
     T.sfac[i] = (float)(P->age_susceptibility[i] / P->mean_daily_interactions);
   for (int i = threadIdx.x; i < 3; i += blockDim.x) T.bfac[i] = (float)P->network_scale[i];
   __syncthreads();
-  for (int i = threadIdx.x; i < 3 * 256; i += blockDim.x) T.comb[i] = T.factor[i & 255] * T.bfac[i >> 8];
+  for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) T.comb[i] = T.factor[i >> 2] * T.bfac[i & 3];
 }
 
 // fp64 term with the reference's pinned factor order (engine.py:100-107,
@@ -261,8 +262,8 @@ struct CsrView {
   const int32_t* __restrict__ row_len;
   const int64_t* __restrict__ row_begin;   // null: padded rows of `cap`
   int cap;
-  // Optional pre-joined messages, tile-packed: msg = (source code & 0xFF) |
-  // kind << 8, written by the generator, so the fp32 message pass streams
+  // Optional pre-joined messages, tile-packed: msg = (source code & 0xFF) << 2
+  // | kind (an index into the fp32 weight table), written by the generator, so the fp32 message pass streams
   // 2 B per edge with no gathers.  Tile k (32 rows from lo) owns the block
   // msgs[k*32*cap ...]; its rows are packed back to back and
   // tile_off[k*33 + r] is row r's start (tile_off[k*33 + 32] = total).
@@ -350,9 +351,21 @@ __global__ void __launch_bounds__(256) k_pass(StepArgs A, CsrView g, const uint1
       const int nxt = __shfl_down_sync(0xFFFFFFFFu, my_lo, 1);
       const int my_hi = lane < 31 ? nxt : total;
       __syncwarp();
+      // one lane per row, messages read in 32-bit pairs, sequential sum
       const uint16_t* sm16 = (const uint16_t*)sm;
+      const uint32_t* sm32 = (const uint32_t*)sm;
       float acc = 0.f;
-      for (int i = my_lo; i < my_hi; ++i) acc += T.comb[sm16[i] & 0x3FF];
+      int i = my_lo;
+      if ((i & 1) && i < my_hi) {
+        acc += T.comb[sm16[i]];
+        ++i;
+      }
+      for (; i + 1 < my_hi; i += 2) {
+        const uint32_t w2 = sm32[i >> 1];
+        acc += T.comb[w2 & 0xFFFF];
+        acc += T.comb[w2 >> 16];
+      }
+      if (i < my_hi) acc += T.comb[sm16[i]];
       __syncwarp();
       if (valid) {
         edges = (unsigned)(my_hi - my_lo);
@@ -493,10 +506,11 @@ __global__ void __launch_bounds__(128, 6) k_net_realize(epi_net net, NetKeys nk,
       const uint16_t cb = codes[b];
       if (!code_dead(cb)) {
         // the staging row holds either ids (src<<2|kind) or messages
-        // ((code & 0xFF) | kind<<8) when only messages are requested
+        // ((code & 0xFF) << 2 | kind: the weight-table index) when only
+        // messages are requested
         auto put = [&](int64_t c, int kind, uint16_t cc) {
           mine[cnt++] = entries ? (((uint32_t)c << 2) | (uint32_t)kind)
-                                : ((uint32_t)(cc & 0xFF) | ((uint32_t)kind << 8));
+                                : (((uint32_t)(cc & 0xFF) << 2) | (uint32_t)kind);
         };
         if (BATCH) for_each_in_edge_batched<16, 8>(net, nk, NT.rk, NT.wrad, wt, codes, b, cb, put);
         else for_each_in_edge(net, nk, NT.rk, NT.wrad, codes, b, cb, 0, 1, put);
