@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--streams", type=int, default=8, help="config4: concurrent streams")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-message-pass", action="store_true",
+                    help="skip the 10M-agent message-pass roofline probe")
     return ap.parse_args()
 
 
@@ -315,6 +317,16 @@ def run_ours(a):
     }
     if not a.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline_single(a.workload, a.cpu_seconds)
+    if not a.no_message_pass and world == 1:
+        # north-star part (a) alone at BASELINE config-3 scale (10M agents):
+        # the HBM-bound kernel of the decomposition, streamed 16-bit messages
+        from paper_2110_04421_b200.roofline import message_pass_roofline
+        mp = message_pass_roofline(10_000_000, peak_gbps=peak)
+        tr = json.loads(tfile.read_text()).get("k_pass<F32,0> message pass (10M agents)") \
+            if tfile.exists() else None
+        mp["traffic"] = (tr["dram_bytes_read"] + tr["dram_bytes_write"]) if tr else None
+        mp["bound"] = "hbm"
+        line["roofline_message_pass_config3"] = mp
     print(json.dumps(line), flush=True)
 
 
