@@ -66,8 +66,8 @@ def message_pass_roofline(n_agents: int = 10_000_000, warm_days: int = 60, reps:
     ms = sorted(a.elapsed_time(b) for a, b in pairs)
     med = ms[len(ms) // 2]
     alg = 2 * edges + 11 * n_agents
-    out = {"kernel": "k_pass<F32,0>: message pass alone (16-bit pre-joined messages, "
-                     "8-byte vector loads, 8 lanes/row, fp32 tree sum)",
+    out = {"kernel": "k_pass<F32,0>: message pass alone (tile-packed 16-bit pre-joined "
+                     "messages, 16-byte global->smem copy, lane-per-row fp32 sum)",
            "n_agents": n_agents, "day": sim.clock, "edges": edges, "ms_median": med,
            "ms_min": ms[0], "alg_bytes": alg, "achieved": alg / (med / 1e3) / 1e9,
            "unit": "GB/s", "l2_flushed_between_reps": bool(flush_l2)}
