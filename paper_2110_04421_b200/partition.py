@@ -32,10 +32,15 @@ class PartitionPlan:
     def __post_init__(self):
         if self.world < 1 or self.n_agents < self.world:
             raise ConfigError(f"cannot split {self.n_agents} agents over {self.world} ranks")
+        if (self.world - 1) * self.chunk >= self.n_agents:
+            raise ConfigError(f"{self.n_agents} agents are too few for {self.world} ranks "
+                              "of 32-row tiles")
 
     @property
     def chunk(self) -> int:
-        return -(-self.n_agents // self.world)
+        # multiple of 32 rows: warp tiles line up with the unpartitioned run,
+        # so tile-local summation orders (and fp32 results) are identical
+        return -(-self.n_agents // (32 * self.world)) * 32
 
     @property
     def padded(self) -> int:

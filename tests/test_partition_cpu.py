@@ -15,14 +15,15 @@ from paper_2110_04421_b200.partition import NcclCodeExchange, PartitionPlan
 
 
 def test_plan_rows_cover_population_once():
-    for n, w in [(10, 1), (10, 3), (100_000, 8), (7, 7), (10_000_000, 8)]:
+    for n, w in [(10, 1), (200, 3), (100_000, 8), (6007, 5), (10_000_000, 8)]:
         plan = PartitionPlan(n, w)
         rows = [plan.rows(r) for r in range(w)]
         assert rows[0][0] == 0 and rows[-1][1] == n
         assert all(a[1] == b[0] for a, b in zip(rows, rows[1:]))
-        assert plan.padded >= n and plan.padded % w == 0
-    with pytest.raises(ConfigError):
-        PartitionPlan(3, 4)
+        assert plan.padded >= n and plan.padded % w == 0 and plan.chunk % 32 == 0
+    for n, w in [(3, 4), (7, 7), (40, 2)]:
+        with pytest.raises(ConfigError):
+            PartitionPlan(n, w)
 
 
 def _free_port():
@@ -51,7 +52,7 @@ def _worker(rank, world, port, n, q):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("n", [10, 1001])
+@pytest.mark.parametrize("n", [100, 1001])
 def test_code_exchange_and_record_reduction_gloo_world2(n):
     world = 2
     ctx = mp.get_context("spawn")
