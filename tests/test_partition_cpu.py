@@ -21,7 +21,7 @@ def test_plan_rows_cover_population_once():
         assert rows[0][0] == 0 and rows[-1][1] == n
         assert all(a[1] == b[0] for a, b in zip(rows, rows[1:]))
         assert plan.padded >= n and plan.padded % w == 0 and plan.chunk % 32 == 0
-    for n, w in [(3, 4), (7, 7), (40, 2)]:
+    for n, w in [(3, 4), (7, 7), (32, 2)]:
         with pytest.raises(ConfigError):
             PartitionPlan(n, w)
 
