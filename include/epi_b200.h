@@ -237,6 +237,13 @@ int epi_sim_step(epi_ctx *ctx, const epi_state *st, int32_t step, uint64_t seed,
                  int32_t mode, int32_t precision, const uint16_t *codes_cur,
                  uint16_t *codes_next, int64_t *record, int32_t *vax_open, void *stream);
 
+/* Days [first_step, first_step + n_days) in one call: codes0 / codes1 are
+ * the codes of even / odd days, records is int64[n_days][EPI_REC_LEN]
+ * (zeroed here).  Same kernels as epi_sim_step. */
+int epi_sim_run(epi_ctx *ctx, const epi_state *st, int32_t first_step, int32_t n_days,
+                uint64_t seed, int32_t mode, int32_t precision, uint16_t *codes0,
+                uint16_t *codes1, int64_t *records, int32_t *vax_open, void *stream);
+
 /* epi_sim_step that also records 4 caller-created cudaEvent_t: before the
  * generator, before the message pass, after it, after the intervention
  * phases — per-kernel device times for the roofline (bench.py). */

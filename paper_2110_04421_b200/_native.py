@@ -83,6 +83,7 @@ _SIGS = {
     "epi_net_realize": (_i32, [C.POINTER(EpiNet), _u64, _i32, _p, _p, _p, _i32, _p]),
     "epi_net_attach": (_i32, [_p, C.POINTER(EpiNet)]),
     "epi_sim_step": (_i32, [_p, C.POINTER(EpiState), _i32, _u64, _i32, _i32, _p, _p, _p, _p, _p]),
+    "epi_sim_run": (_i32, [_p, C.POINTER(EpiState), _i32, _i32, _u64, _i32, _i32, _p, _p, _p, _p, _p]),
     "epi_sim_step_timed": (_i32, [_p, C.POINTER(EpiState), _i32, _u64, _i32, _i32, _p, _p, _p, _p,
                                   _p, _p]),
     "epi_net_generate": (_i32, [_p, _i32, _u64, _p, _p]),

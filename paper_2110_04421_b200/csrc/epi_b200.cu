@@ -57,6 +57,23 @@ inline int grid_for(int64_t n, int threads, int per_sm = 8) {
   return (int)(g < 1 ? 1 : g);
 }
 
+// Launch with programmatic stream serialization (see pdl_wait/pdl_trigger).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, ((KArgs)args)...);
+}
+
 template <class T>
 int dalloc(T** p, size_t count) {
   if (*p) cudaFree(*p);
@@ -106,10 +123,11 @@ struct epi_ctx {
   std::vector<int32_t> net_slot_step;
   MsgTables* msg_dev = nullptr;      // fp32 message tables (rate_scale baked in)
   NetTables ntab{};                  // host copy (static radix tables)
-  NetTables* ntab_dev[2] = {nullptr, nullptr};   // per-day keys, by step parity
-  WorkTables wt_host{};              // device arrays, rebuilt each day
-  WorkTables* wt_dev = nullptr;
-  int wt_whole = -1;                 // which variant wt_dev currently holds
+  NetTables* ntab_dev[3] = {nullptr, nullptr, nullptr};   // per-day keys, by step % 3
+  WorkTables wt_host[2]{};           // day tables by step parity (member_at_pos shared)
+  WorkTables* wt_dev[2][3] = {};     // device structs per parity x variant
+                                     //   0 csr (ids), 1 fused partitioned, 2 fused whole
+  int merged_ready = -1;             // day whose tables the previous merged kernel built
   Injected* inj_dev = nullptr;
 };
 
@@ -267,15 +285,17 @@ int epi_destroy(epi_ctx* c) {
   cudaFree(c->net_dev);
   cudaFree(c->inj_dev);
   cudaFree(c->msg_dev);
-  cudaFree(c->ntab_dev[0]);
-  cudaFree(c->ntab_dev[1]);
-  cudaFree(c->wt_host.member_at_pos);
-  cudaFree(c->wt_host.pos_of);
-  cudaFree(c->wt_host.shift);
-  cudaFree(c->wt_host.wcode);
-  cudaFree(c->wt_host.rout);
-  cudaFree(c->wt_host.rin);
-  cudaFree(c->wt_dev);
+  for (auto* p : c->ntab_dev) cudaFree(p);
+  cudaFree(c->wt_host[0].member_at_pos);
+  for (auto& w : c->wt_host) {
+    cudaFree(w.pos_of);
+    cudaFree(w.shift);
+    cudaFree(w.wcode);
+    cudaFree(w.rout);
+    cudaFree(w.rin);
+  }
+  for (auto& row : c->wt_dev)
+    for (auto* p : row) cudaFree(p);
   for (auto& s : c->ring) { cudaFree(s.src); cudaFree(s.dst); }
   for (auto* p : c->net_entries) cudaFree(p);
   for (auto* p : c->net_rowlen) cudaFree(p);
@@ -520,13 +540,10 @@ static int launch_realize(const epi_net* net, uint64_t g, int32_t step, const ui
   }
   const int grid = grid_for(hi - lo, 128, 16);
   const bool batch = batched(net);
-  if (sort_rows) {
-    if (batch) k_net_realize<true, true><<<grid, 128, smem, s>>>(*net, nk, codes, entries, msgs, toff, row_len, rec, wt, lo, hi, ntab_dev);
-    else k_net_realize<true, false><<<grid, 128, smem, s>>>(*net, nk, codes, entries, msgs, toff, row_len, rec, wt, lo, hi, ntab_dev);
-  } else {
-    if (batch) k_net_realize<false, true><<<grid, 128, smem, s>>>(*net, nk, codes, entries, msgs, toff, row_len, rec, wt, lo, hi, ntab_dev);
-    else k_net_realize<false, false><<<grid, 128, smem, s>>>(*net, nk, codes, entries, msgs, toff, row_len, rec, wt, lo, hi, ntab_dev);
-  }
+  auto kern = sort_rows ? (batch ? k_net_realize<true, true> : k_net_realize<true, false>)
+                        : (batch ? k_net_realize<false, true> : k_net_realize<false, false>);
+  CK(launch_pdl(kern, dim3(grid), dim3(128), smem, s, *net, nk, codes, entries, msgs, toff, row_len, rec,
+                wt, lo, hi, ntab_dev));
   CKL();
   return 0;
 }
@@ -552,7 +569,7 @@ int epi_net_attach(epi_ctx* c, const epi_net* net) {
   if (rc) return rc;
   c->net = *net;
   fill_net_tables(c->ntab, *net, 0);
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < 3; ++i) {
     if (!c->ntab_dev[i]) CK(cudaMalloc((void**)&c->ntab_dev[i], sizeof(NetTables)));
     CK(cudaMemcpy(c->ntab_dev[i], &c->ntab, sizeof(NetTables), cudaMemcpyHostToDevice));
   }
@@ -574,17 +591,27 @@ int epi_net_attach(epi_ctx* c, const epi_net* net) {
   rc = dalloc(&c->net_msgs, (size_t)((c->n + 31) / 32) * 32 * net->row_cap + 16);
   if (!rc) rc = dalloc(&c->net_toff, (size_t)((c->n + 31) / 32) * 33);
   if (rc) return rc;
-  rc = dalloc(&c->wt_host.member_at_pos, (size_t)net->n_member_slots);
-  if (!rc) rc = dalloc(&c->wt_host.pos_of, (size_t)net->n_member_slots);
-  if (!rc) rc = dalloc(&c->wt_host.shift, (size_t)net->n_workplaces * (net->colleague_draws + 1));
-  if (!rc) rc = dalloc(&c->wt_host.wcode, (size_t)net->n_member_slots);
-  if (!rc) rc = dalloc(&c->wt_host.rout, (size_t)c->n * RT_SLOTS);
-  if (!rc) rc = dalloc(&c->wt_host.rin, (size_t)c->n * RT_SLOTS);
+  rc = dalloc(&c->wt_host[0].member_at_pos, (size_t)net->n_member_slots);
   if (rc) return rc;
-  CK(cudaMemset(c->wt_host.rin, 0, (size_t)c->n * RT_SLOTS * sizeof(uint16_t)));
-  if (!c->wt_dev) CK(cudaMalloc((void**)&c->wt_dev, sizeof(WorkTables)));
-  CK(cudaMemcpy(c->wt_dev, &c->wt_host, sizeof(WorkTables), cudaMemcpyHostToDevice));
-  c->wt_whole = -1;
+  for (int par = 0; par < 2; ++par) {
+    WorkTables& w = c->wt_host[par];
+    w.member_at_pos = c->wt_host[0].member_at_pos;
+    rc = dalloc(&w.pos_of, (size_t)net->n_member_slots);
+    if (!rc) rc = dalloc(&w.shift, (size_t)net->n_workplaces * (net->colleague_draws + 1));
+    if (!rc) rc = dalloc(&w.wcode, (size_t)net->n_member_slots);
+    if (!rc) rc = dalloc(&w.rout, (size_t)c->n * RT_SLOTS);
+    if (!rc) rc = dalloc(&w.rin, (size_t)c->n * RT_SLOTS);
+    if (rc) return rc;
+    CK(cudaMemset(w.rin, 0, (size_t)c->n * RT_SLOTS * sizeof(uint16_t)));
+    for (int var = 0; var < 3; ++var) {
+      WorkTables v = w;
+      if (var == 0) v.wcode = nullptr;
+      if (var < 2) { v.rin = nullptr; v.rout = nullptr; }
+      if (!c->wt_dev[par][var]) CK(cudaMalloc((void**)&c->wt_dev[par][var], sizeof(WorkTables)));
+      CK(cudaMemcpy(c->wt_dev[par][var], &v, sizeof(WorkTables), cudaMemcpyHostToDevice));
+    }
+  }
+  c->merged_ready = -1;
   return 0;
 }
 
@@ -599,7 +626,8 @@ int epi_net_csr(epi_ctx* c, int32_t step, uint32_t** entries, int32_t** row_len)
 
 static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t seed, int32_t mode,
                          int32_t precision, const uint16_t* codes_cur, uint16_t* codes_next,
-                         int64_t* record, int32_t* vax_open, void* const* ev, void* stream) {
+                         int64_t* record, int32_t* vax_open, void* const* ev, void* stream,
+                         bool zero_record = true) {
   if (!c || !st || !codes_cur || !codes_next) return fail(EPI_EARG, "null argument");
   if (!c->has_net) return fail(EPI_EARG, "epi_sim_step needs epi_net_attach first");
   if (st->n_agents != c->n) return fail(EPI_EARG, "state size differs from context");
@@ -611,47 +639,51 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
   if (mode == 1 && precision != EPI_F32) return fail(EPI_EARG, "fused mode is fp32 only");
   cudaStream_t s = S(stream);
   long long* rec = record ? (long long*)record : c->scratch_rec;
-  CK(cudaMemsetAsync(rec, 0, EPI_REC_LEN * sizeof(long long), s));
   StepArgs A = make_args(c, st, step, seed, rec, nullptr, iv);
   const uint64_t rcount_next = key_prefix(seed, step + 1, P_NET_RCOUNT);
   const int grid = grid_for(c->hi - c->lo, 256);
   const int slot = step % c->net_slots;
   if (ev) CK(cudaEventRecord((cudaEvent_t)ev[0], s));
   const NetKeys nk = make_net_keys(seed, step);
-  NetTables* nt_today = c->ntab_dev[step & 1];
-  NetTables* nt_next = c->ntab_dev[(step + 1) & 1];
-  if (step == 0) {
-    k_day_keys<<<1, 32, 0, s>>>(nt_today, nk.rperm);
-    CKL();
-  }
+  NetTables* nt_today = c->ntab_dev[step % 3];
+  NetTables* nt_next = c->ntab_dev[(step + 1) % 3];
+  const int par = step & 1;
   // day tables: workplace sigma cache (all modes); in fused mode also the
   // push tables (workplace codes; random-slot codes for whole-population runs
-  // — a partitioned rank cannot scatter into its peers' rows)
+  // — a partitioned rank cannot scatter into its peers' rows).  Fused runs
+  // without interventions are "merged": today's kernel builds tomorrow's
+  // tables in its epilogue, so after the first day there is one kernel per day.
   const bool has_work = c->net.n_member_slots > 0 && c->net.colleague_draws > 0;
-  const bool push_rand = mode == 1 && c->lo == 0 && c->hi == c->n && c->net.n_agents >= 2;
+  const bool push_rand = mode == 1 && c->lo == 0 && c->hi == c->n && c->net.n_agents >= 2 &&
+                         c->net.random_slots == RT_SLOTS && batched(&c->net);
+  const bool merged = push_rand && !iv;
   const bool use_wt = (mode == 0 && has_work && batched(&c->net)) || mode == 1;
-  if (use_wt) {
-    WorkTables w = c->wt_host;
-    if (mode == 0) w.wcode = nullptr;
-    if (!push_rand) { w.rin = nullptr; w.rout = nullptr; }
-    const int variant = (mode == 1 ? 2 : 0) | (push_rand ? 1 : 0);
-    if (c->wt_whole != variant) {
-      CK(cudaMemcpyAsync(c->wt_dev, &w, sizeof(WorkTables), cudaMemcpyHostToDevice, s));
-      c->wt_whole = variant;
-    }
-    if (push_rand && step == 0)
-      CK(cudaMemsetAsync(c->wt_host.rin, 0, (size_t)c->n * RT_SLOTS * sizeof(uint16_t), s));
-    const int wblocks = has_work ? grid_for(c->net.n_member_slots, 256, 4) : 0;
-    const int rblocks = push_rand ? grid_for(c->hi - c->lo, 256, 8) : 0;
-    k_day_tables<<<wblocks + rblocks > 0 ? wblocks + rblocks : 1, 256, 0, s>>>(
-        c->net, nk, w, codes_cur, c->lo, c->hi, wblocks, nt_today, nt_next,
-        key_prefix(seed, step + 1, P_NET_RPERM));
-    CKL();
+  const int variant = mode == 0 ? 0 : (push_rand ? 2 : 1);
+  long long* rec_zero = zero_record ? rec : nullptr;
+  if (merged && c->merged_ready == step) {
+    if (rec_zero) CK(cudaMemsetAsync(rec, 0, EPI_REC_LEN * sizeof(long long), s));
   } else {
-    k_day_keys<<<1, 32, 0, s>>>(nt_next, key_prefix(seed, step + 1, P_NET_RPERM));
-    CKL();
+    if (step == 0 || merged) {
+      k_day_keys<<<1, 32, 0, s>>>(nt_today, nk.rperm, nullptr);
+      CKL();
+    }
+    if (use_wt) {
+      if (push_rand && (step == 0 || merged))
+        CK(cudaMemsetAsync(c->wt_host[par].rin, 0, (size_t)c->n * RT_SLOTS * sizeof(uint16_t), s));
+      const int wblocks = has_work ? grid_for(c->net.n_member_slots, 256, 4) : 0;
+      const int rblocks = push_rand ? grid_for(c->hi - c->lo, 256, 8) : 0;
+      WorkTables w = c->wt_host[par];
+      if (variant == 0) w.wcode = nullptr;
+      if (variant < 2) { w.rin = nullptr; w.rout = nullptr; }
+      CK(launch_pdl(k_day_tables, dim3(wblocks + rblocks > 0 ? wblocks + rblocks : 1), dim3(256), 0, s,
+                    c->net, nk, w, codes_cur, c->lo, c->hi, wblocks, (const NetTables*)nt_today, nt_next,
+                    key_prefix(seed, step + 1, P_NET_RPERM), rec_zero));
+    } else {
+      CK(launch_pdl(k_day_keys, dim3(1), dim3(32), 0, s, nt_next, key_prefix(seed, step + 1, P_NET_RPERM),
+                    rec_zero));
+    }
   }
-  const WorkTables* wt = use_wt ? c->wt_dev : nullptr;
+  const WorkTables* wt = use_wt ? c->wt_dev[par][variant] : nullptr;
   if (mode == 0) {
     // fp32 without contact log: the generator writes pre-joined messages and
     // the message pass streams them; otherwise ids (export, DEN, fp64 order)
@@ -663,6 +695,7 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
                             precision == EPI_F64_CANONICAL, nullptr, wt, c->lo, c->hi, s, nt_today);
     if (rc) return rc;
     c->net_slot_step[slot] = msg_only ? -1 : step;
+    c->merged_ready = -1;
     if (ev) CK(cudaEventRecord((cudaEvent_t)ev[1], s));
     CsrView g{entries, row_len, nullptr, c->net.row_cap, msgs, c->net_toff};
     const size_t msmem = msgs ? (size_t)8 * 32 * c->net.row_cap * sizeof(uint16_t) : 0;
@@ -670,15 +703,25 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
       k_pass<true, 1><<<grid, 256, 0, s>>>(A, g, codes_cur, nullptr, c->host.rate_scale, iv ? 0 : 1,
                                            codes_next, c->net_dev, rcount_next, c->msg_dev);
     else
-      k_pass<false, 1><<<grid, 256, msmem, s>>>(A, g, codes_cur, nullptr, c->host.rate_scale, iv ? 0 : 1,
-                                                codes_next, c->net_dev, rcount_next, c->msg_dev);
+      CK(launch_pdl(k_pass<false, 1>, dim3(grid), dim3(256), msmem, s, A, g, codes_cur, (void*)nullptr,
+                    c->host.rate_scale, iv ? 0 : 1, codes_next, (const epi_net*)c->net_dev, rcount_next,
+                    (const MsgTables*)c->msg_dev));
     CKL();
   } else {
     if (ev) CK(cudaEventRecord((cudaEvent_t)ev[1], s));
     const int fgrid = grid_for(c->hi - c->lo, 128, 16);
-    k_fused_step<<<fgrid, 128, 0, s>>>(A, c->net, nk, codes_cur, c->host.rate_scale, codes_next,
-                                       c->net_dev, rcount_next, iv ? 0 : 1, wt, c->msg_dev, nt_today);
-    CKL();
+    NextTables nx{};
+    if (merged) {
+      nx.wt = c->wt_dev[par ^ 1][2];
+      nx.keys = nt_next;
+      nx.keys_out = c->ntab_dev[(step + 2) % 3];
+      nx.rperm_t2 = key_prefix(seed, step + 2, P_NET_RPERM);
+      nx.nk = make_net_keys(seed, step + 1);
+    }
+    CK(launch_pdl(k_fused_step, dim3(fgrid), dim3(128), 0, s, A, c->net, nk, codes_cur,
+                  c->host.rate_scale, codes_next, (const epi_net*)c->net_dev, rcount_next, iv ? 0 : 1, wt,
+                  (const MsgTables*)c->msg_dev, (const NetTables*)nt_today, nx));
+    c->merged_ready = merged ? step + 1 : -1;
   }
   if (ev) CK(cudaEventRecord((cudaEvent_t)ev[2], s));
   if (iv) {
@@ -706,6 +749,22 @@ int epi_sim_step(epi_ctx* c, const epi_state* st, int32_t step, uint64_t seed, i
                        nullptr, stream);
 }
 
+int epi_sim_run(epi_ctx* c, const epi_state* st, int32_t first_step, int32_t n_days, uint64_t seed,
+                int32_t mode, int32_t precision, uint16_t* codes0, uint16_t* codes1, int64_t* records,
+                int32_t* vax_open, void* stream) {
+  if (!c || !records || !codes0 || !codes1 || n_days < 0) return fail(EPI_EARG, "bad argument");
+  CK(cudaMemsetAsync(records, 0, (size_t)n_days * EPI_REC_LEN * sizeof(int64_t), S(stream)));
+  for (int d = 0; d < n_days; ++d) {
+    const int t = first_step + d;
+    uint16_t* cur = (t & 1) ? codes1 : codes0;
+    uint16_t* nxt = (t & 1) ? codes0 : codes1;
+    int rc = sim_step_impl(c, st, t, seed, mode, precision, cur, nxt, records + (size_t)d * EPI_REC_LEN,
+                           vax_open, nullptr, stream, false);
+    if (rc) return rc;
+  }
+  return 0;
+}
+
 int epi_sim_step_timed(epi_ctx* c, const epi_state* st, int32_t step, uint64_t seed, int32_t mode,
                        int32_t precision, const uint16_t* codes_cur, uint16_t* codes_next,
                        int64_t* record, int32_t* vax_open, void* const* events4, void* stream) {
@@ -719,26 +778,24 @@ int epi_net_generate(epi_ctx* c, int32_t step, uint64_t seed, const uint16_t* co
   if (!batched(&c->net)) return fail(EPI_EARG, "epi_net_generate needs <= 16 slots and <= 8 draws");
   cudaStream_t s = S(stream);
   const NetKeys nk = make_net_keys(seed, step);
-  NetTables* nt = c->ntab_dev[step & 1];
-  k_day_keys<<<1, 32, 0, s>>>(nt, nk.rperm);
+  NetTables* nt = c->ntab_dev[step % 3];
+  k_day_keys<<<1, 32, 0, s>>>(nt, nk.rperm, nullptr);
   CKL();
   const bool has_work = c->net.n_member_slots > 0 && c->net.colleague_draws > 0;
-  WorkTables w = c->wt_host;
+  WorkTables w = c->wt_host[step & 1];
   w.wcode = nullptr;
   w.rin = nullptr;
   w.rout = nullptr;
-  if (c->wt_whole != 0) {
-    CK(cudaMemcpyAsync(c->wt_dev, &w, sizeof(WorkTables), cudaMemcpyHostToDevice, s));
-    c->wt_whole = 0;
-  }
+  c->merged_ready = -1;
   if (has_work) {
     k_day_tables<<<grid_for(c->net.n_member_slots, 256, 4), 256, 0, s>>>(
         c->net, nk, w, codes_cur, c->lo, c->hi, grid_for(c->net.n_member_slots, 256, 4), nt,
-        c->ntab_dev[(step + 1) & 1], key_prefix(seed, step + 1, P_NET_RPERM));
+        c->ntab_dev[(step + 1) % 3], key_prefix(seed, step + 1, P_NET_RPERM), nullptr);
     CKL();
   }
   return launch_realize(&c->net, seed, step, codes_cur, nullptr, c->net_msgs, c->net_toff,
-                        c->net_rowlen[0], 0, nullptr, has_work ? c->wt_dev : nullptr, c->lo, c->hi, s, nt);
+                        c->net_rowlen[0], 0, nullptr, has_work ? c->wt_dev[step & 1][0] : nullptr, c->lo,
+                        c->hi, s, nt);
 }
 
 int epi_net_gather(epi_ctx* c, const epi_state* st, int32_t step, const uint16_t* codes_cur,

@@ -131,6 +131,17 @@ __device__ __forceinline__ uint16_t source_code(const epi_params* __restrict__ P
   return (uint16_t)t | (asym_like_stage(stage) ? CODE_ASYM : 0);
 }
 
+// ---- programmatic dependent launch ------------------------------------------
+// The per-day kernels are launched with programmatic stream serialization so
+// the next kernel's launch and shared-memory prologue overlap the current
+// kernel's tail.  Rule: a kernel's prologue reads only data finished at least
+// two launches earlier and writes nothing global; pdl_wait() (all prior grids
+// complete and visible) precedes every dependent read and every global write;
+// pdl_trigger() is issued only after pdl_wait(), which keeps the chain
+// transitive.  Without a programmatic predecessor both are no-ops.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
 // ---- warp helpers -----------------------------------------------------------
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 

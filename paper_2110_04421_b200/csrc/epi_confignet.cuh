@@ -152,14 +152,14 @@ struct WorkTables {
   uint8_t* pos_of;
   uint8_t* shift;
   // Fused mode only ("push" tables: the consumer reads contiguous rows
-  // instead of gathering random 2-byte codes):
-  //   wcode[base_W + q] = code of member_at_pos[base_W + q]
-  //   rout[a*16 + j] = code(pi_{t,j}(a)) | PRESENT   for j < n_{t,a}, pi(a) != a
+  // instead of evaluating bijections / gathering random 2-byte codes):
+  //   wcode[base_W + q] = code of the worker at position q
+  //   rout[a*16 + j] = pi_{t,j}(a) for j < n_{t,a}   (own out-partners)
   //   rin [b*16 + j] = code(c) | PRESENT where pi_{t,j}(c) = b, j < n_{t,c}, c != b
   // (whole-population runs only; the scatter into rin is conflict-free because
   // pi is a bijection, and rin rows are cleared by their consumer).
   uint16_t* wcode;
-  uint16_t* rout;
+  uint32_t* rout;
   uint16_t* rin;
 };
 constexpr int RT_SLOTS = 16;
@@ -429,14 +429,24 @@ __device__ __forceinline__ void for_each_in_code(const epi_net& net, const NetKe
   }
   if (net.n_agents < 2) return;
   if (wt != nullptr && wt->rin != nullptr) {
-    const uint4* ro = (const uint4*)(wt->rout + (size_t)b * RT_SLOTS);
+    const uint32_t self = (uint32_t)b;
+    const int nb = code_count(code_b);
+    const int nbe = nb < RT_SLOTS ? nb : RT_SLOTS;
     const uint4* ri = (const uint4*)(wt->rin + (size_t)b * RT_SLOTS);
-    uint4 o[2] = {ro[0], ro[1]}, in[2] = {ri[0], ri[1]};
-    const uint16_t* ov = (const uint16_t*)o;
-    const uint16_t* iv = (const uint16_t*)in;
+    const uint4 in[2] = {ri[0], ri[1]};
+    const uint4* ro = (const uint4*)(wt->rout + (size_t)b * RT_SLOTS);
+    for (int j0 = 0; j0 < nbe; j0 += 4) {
+      const uint4 o = ro[j0 >> 2];
+      const uint32_t po[4] = {o.x, o.y, o.z, o.w};
+      uint16_t co[4];
 #pragma unroll
-    for (int j = 0; j < RT_SLOTS; ++j)
-      if ((ov[j] & CODE_PRESENT) && !code_dead(ov[j])) visit(2, (uint16_t)(ov[j] & ~CODE_PRESENT));
+      for (int q = 0; q < 4; ++q)
+        co[q] = (j0 + q < nbe && po[q] != self) ? codes[po[q]] : (uint16_t)CODE_DEAD;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (!code_dead(co[q])) visit(2, co[q]);
+    }
+    const uint16_t* iv = (const uint16_t*)in;
 #pragma unroll
     for (int j = 0; j < RT_SLOTS; ++j)
       if (iv[j] & CODE_PRESENT) visit(2, (uint16_t)(iv[j] & ~CODE_PRESENT));

@@ -292,6 +292,8 @@ __global__ void __launch_bounds__(256) k_pass(StepArgs A, CsrView g, const uint1
   }
   rec_init(racc);
   __syncthreads();
+  pdl_wait();
+  pdl_trigger();
   const epi_params* __restrict__ P = A.P;
   const int64_t n = A.hi;
   const int warp = threadIdx.x >> 5, lane = lane_id();
@@ -458,8 +460,11 @@ __global__ void k_update_from_hazard(StepArgs A, const double* __restrict__ haza
 
 // Day-0 keys (every later day's keys are written by the previous day's
 // k_day_tables).
-__global__ void k_day_keys(NetTables* __restrict__ NT, uint64_t rperm) {
+__global__ void k_day_keys(NetTables* __restrict__ NT, uint64_t rperm, long long* rec) {
+  pdl_wait();
+  pdl_trigger();
   if (threadIdx.x < EPI_MAX_SLOTS) NT->rk[threadIdx.x] = random_slot_keys(rperm, threadIdx.x);
+  if (rec && threadIdx.x < EPI_REC_LEN) rec[threadIdx.x] = 0;   // the day's record
 }
 
 __device__ __forceinline__ void clear_rin_row(const WorkTables* wt, int64_t b) {
@@ -489,6 +494,8 @@ __global__ void __launch_bounds__(128, 6) k_net_realize(epi_net net, NetKeys nk,
   load_net_tables(NT, NTp);
   rec_init(racc);
   __syncthreads();
+  pdl_wait();
+  pdl_trigger();
   const int cap = net.row_cap;
   const int stride_w = cap | 1;
   const int warp = threadIdx.x >> 5, lane = lane_id();
@@ -565,21 +572,45 @@ __global__ void __launch_bounds__(128, 6) k_net_realize(epi_net net, NetKeys nk,
 // their source codes consumed on the fly, so no CSR ever reaches memory.  One
 // lane per agent; with the day's push tables the random and workplace codes
 // come from contiguous rows (for_each_in_code).
+// Tomorrow's push tables built in the epilogue of today's fused kernel
+// ("merged" mode: one kernel per simulated day).  Everything written here is
+// tomorrow's buffers; each agent scatters only its own next-day code.
+struct NextTables {
+  const WorkTables* wt;          // parity (t+1) buffers (device struct)
+  const NetTables* keys;         // day t+1 random-slot keys (read after pdl_wait)
+  NetTables* keys_out;           // day t+2 keys, written by block 0
+  uint64_t rperm_t2;             // NET_RANDOM_PERM prefix of day t+2
+  NetKeys nk;                    // prefixes of day t+1
+};
+
 __global__ void __launch_bounds__(128, 6) k_fused_step(StepArgs A, epi_net net, NetKeys nk,
                                                     const uint16_t* __restrict__ codes, double rate,
                                                     uint16_t* __restrict__ codes_next,
                                                     const epi_net* net_dev, uint64_t rcount_next,
                                                     int final_pass, const WorkTables* wt,
                                                     const MsgTables* __restrict__ mt,
-                                                    const NetTables* __restrict__ NTp) {
+                                                    const NetTables* __restrict__ NTp, NextTables nx) {
   __shared__ MsgTables T;
   __shared__ NetTables NT;
   __shared__ RecAcc racc;
+  __shared__ PermKeys rk_next[EPI_MAX_SLOTS];
+  __shared__ int excl_s[4][32];
+  __shared__ uint16_t cn_s[4][32];
   load_msg_tables(T, mt);
   load_net_tables(NT, NTp);
   rec_init(racc);
   __syncthreads();
+  pdl_wait();
+  pdl_trigger();
+  const bool merge = nx.wt != nullptr;
+  if (merge) {
+    for (int j = threadIdx.x; j < EPI_MAX_SLOTS; j += blockDim.x) rk_next[j] = nx.keys->rk[j];
+    if (blockIdx.x == 0 && threadIdx.x < EPI_MAX_SLOTS)
+      nx.keys_out->rk[threadIdx.x] = random_slot_keys(nx.rperm_t2, threadIdx.x);
+    __syncthreads();
+  }
   const Radix dn = NT.dn;
+  const int warp = threadIdx.x >> 5, lane = lane_id();
   const int64_t n = A.hi;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t base = A.lo + blockIdx.x * (int64_t)blockDim.x; base < n; base += stride) {
@@ -606,7 +637,54 @@ __global__ void __launch_bounds__(128, 6) k_fused_step(StepArgs A, epi_net net, 
     rec_add(racc, EPI_REC_EDGES, edges);
     if (final_pass) {
       rec_agent(racc, valid, valid ? A.st.stage[b] : 0, valid ? A.st.infected_at[b] : 0);
-      if (valid) codes_next[b] = next_code(A.P, A.st, b, A.step + 1, net_dev, rcount_next);
+      uint16_t cn = 0;
+      if (valid) {
+        cn = next_code(A.P, A.st, b, A.step + 1, net_dev, rcount_next);
+        codes_next[b] = cn;
+      }
+      if (merge) {
+        const WorkTables& W = *nx.wt;
+        // workplace: the worker's next-day position, its code at that position
+        const int w = valid ? net.wp_id[b] : -1;
+        if (w >= 0) {
+          const int m = net.wp_size[w];
+          if (m >= 2) {
+            const int wbase = net.wp_base[w];
+            const int loc = net.wp_local[b];
+            const uint32_t q = walk_inv((uint32_t)loc, work_keys(nx.nk.wperm, w), NT.wrad[m]);
+            W.pos_of[wbase + loc] = (uint8_t)q;
+            W.wcode[wbase + q] = cn;
+            for (int j = loc; j < net.colleague_draws; j += m)
+              W.shift[(size_t)w * net.colleague_draws + j] = (uint8_t)work_shift(nx.nk.wshift, w, j, m);
+          }
+        }
+        // random: flatten the warp's (agent, slot < n) items, 32 at a time
+        int na = valid ? code_count(cn) : 0;
+        na = na < RT_SLOTS ? na : RT_SLOTS;
+        int incl = na;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+          if (lane >= o) incl += v;
+        }
+        const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+        excl_s[warp][lane] = incl - na;
+        cn_s[warp][lane] = cn;
+        __syncwarp();
+        const int64_t wbase_agent = base + (threadIdx.x & ~31);
+        for (int k = lane; k < total; k += 32) {
+          int l = 0;
+#pragma unroll
+          for (int st = 16; st >= 1; st >>= 1)
+            if (l + st < 32 && excl_s[warp][l + st] <= k) l += st;
+          const int j = k - excl_s[warp][l];
+          const uint32_t src = (uint32_t)(wbase_agent + l);
+          const uint32_t y = walk_fwd(src, rk_next[j], dn);
+          W.rout[(size_t)src * RT_SLOTS + j] = y;
+          if (y != src) W.rin[(size_t)y * RT_SLOTS + j] = cn_s[warp][l] | CODE_PRESENT;
+        }
+        __syncwarp();
+      }
     }
   }
   __syncthreads();
@@ -623,14 +701,19 @@ __global__ void __launch_bounds__(128, 6) k_fused_step(StepArgs A, epi_net net, 
 __global__ void __launch_bounds__(256) k_day_tables(epi_net net, NetKeys nk, WorkTables wt,
                                                     const uint16_t* __restrict__ codes, int64_t lo,
                                                     int64_t hi, int wblocks, const NetTables* __restrict__ NTp,
-                                                    NetTables* __restrict__ NTnext, uint64_t rperm_next) {
+                                                    NetTables* __restrict__ NTnext, uint64_t rperm_next,
+                                                    long long* rec) {
   __shared__ NetTables NT;
   __shared__ int excl_s[8][32];
   load_net_tables(NT, NTp);
   __syncthreads();
-  // tomorrow's random-slot keys (the other buffer; nobody reads it today)
+  pdl_wait();
+  pdl_trigger();
+  // tomorrow's random-slot keys (the other buffer: yesterday's kernels, its
+  // last readers, are complete after pdl_wait) and today's zeroed record
   if (blockIdx.x == 0 && threadIdx.x < EPI_MAX_SLOTS)
     NTnext->rk[threadIdx.x] = random_slot_keys(rperm_next, threadIdx.x);
+  if (blockIdx.x == 0 && rec && threadIdx.x < EPI_REC_LEN) rec[threadIdx.x] = 0;
   const int draws = net.colleague_draws;
   if ((int)blockIdx.x < wblocks) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < net.n_member_slots;
@@ -672,9 +755,6 @@ __global__ void __launch_bounds__(256) k_day_tables(epi_net net, NetKeys nk, Wor
       ca = codes[a];
       na = code_count(ca);
       na = na < RT_SLOTS ? na : RT_SLOTS;
-      uint4* row = (uint4*)(wt.rout + (size_t)a * RT_SLOTS);
-      row[0] = make_uint4(0, 0, 0, 0);
-      row[1] = make_uint4(0, 0, 0, 0);
     }
     int incl = na;
 #pragma unroll
@@ -693,11 +773,8 @@ __global__ void __launch_bounds__(256) k_day_tables(epi_net net, NetKeys nk, Wor
       const int j = k - excl_s[warp][l];
       const uint32_t src = (uint32_t)(base + l);
       const uint32_t y = walk_fwd(src, NT.rk[j], dn);
-      if (y != src) {
-        const uint16_t csrc = codes[src];
-        wt.rin[(size_t)y * RT_SLOTS + j] = csrc | CODE_PRESENT;
-        wt.rout[(size_t)src * RT_SLOTS + j] = codes[y] | CODE_PRESENT;
-      }
+      wt.rout[(size_t)src * RT_SLOTS + j] = y;
+      if (y != src) wt.rin[(size_t)y * RT_SLOTS + j] = codes[src] | CODE_PRESENT;
     }
     __syncwarp();
   }

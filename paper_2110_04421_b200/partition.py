@@ -141,6 +141,11 @@ class PartitionedSimulation(ConfigSimulation):
         if isinstance(self.exchange, NcclCodeExchange):
             self.exchange.exchange(self.codes[(t + 1) & 1])
 
+    def run(self, days: int | None = None) -> None:
+        # one day at a time: the code exchange sits between days
+        for _ in range(self.horizon - self.clock if days is None else days):
+            self.step()
+
 
 def run_emulated(pop, disease, table, interventions, seed, world: int, days: int, **kw):
     """P ranks on one GPU, days in lockstep; returns (sims, summed records)."""

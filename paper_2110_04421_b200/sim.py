@@ -173,8 +173,19 @@ class ConfigSimulation:
         self.clock = t + 1
 
     def run(self, days: int | None = None) -> None:
-        for _ in range(self.horizon - self.clock if days is None else days):
-            self.step()
+        """Advance `days` (default: to the horizon) in one native call."""
+        d = self.horizon - self.clock if days is None else days
+        if d <= 0:
+            return
+        if self.clock + d > self.horizon:
+            raise ConfigError(f"horizon {self.horizon} exhausted")
+        st = self.state.struct()
+        t = self.clock
+        N.check(self._lib.epi_sim_run(
+            self._ctx, ctypes.byref(st), t, d, _u64(self.seed), 0 if self.mode == "csr" else 1,
+            N.F64_CANONICAL if self.precision == "f64" else N.F32, N.ptr(self.codes[0]),
+            N.ptr(self.codes[1]), N.ptr(self.rec[t]), N.ptr(self.vax), N.stream_handle()))
+        self.clock = t + d
 
     def capture(self):
         """Record reset + the whole horizon as one CUDA graph."""
