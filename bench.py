@@ -379,13 +379,15 @@ def kernel_profile(sim, mode):
         ms = pas if dom == "k_pass_update" else gen
         launches = 3
     else:
-        b = 16 * n + 2 * n + 2 * E       # state r/w + own code + gathered codes (L2)
-        kernels["k_day_tables"] = {"ms_per_launch": sum(gen) / len(gen), "share": sum(gen) / total_ms}
+        # merged fused kernel: state r/w 16 N + own code 2 N + push rows
+        # (rin 32 B + rout ids 64 B) + rin clear 32 B + next-day scatter ~16 B
+        b = (16 + 2 + 32 + 64 + 32 + 16) * n
+        kernels["day0_tables+keys"] = {"ms_per_launch": sum(gen) / len(gen), "share": sum(gen) / total_ms}
         kernels["k_fused_step"] = {"ms_per_launch": sum(pas) / len(pas), "share": sum(pas) / total_ms,
                                    "alg_GBps": float(np.sum(b) / (sum(pas) / 1e3) / 1e9)}
-        dom, byt, ms, launches = "k_fused_step", b, pas, 2
+        dom, byt, ms, launches = "k_fused_step", b * np.ones_like(E), pas, 1
     achieved = float(np.sum(byt) / (sum(ms) / 1e3) / 1e9)
-    return {"kernels": kernels, "launches_per_sim": launches * sim.horizon,
+    return {"kernels": kernels, "launches_per_sim": launches * sim.horizon + (2 if mode != "csr" else 0),
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "unit": "GB/s",
                          "traffic": None,
                          "bytes_model": "see DESIGN.md §5 (algorithmic bytes per launch)"}}
