@@ -274,6 +274,36 @@ int epi_seed_infections(epi_ctx *ctx, const epi_state *st, uint64_t seed,
 /* DEN app adoption u(seed, 0, DEN_APP, a) < adoption (runner.py:86-89). */
 int epi_assign_app(const epi_state *st, uint64_t seed, double adoption, void *stream);
 
+/* ---- reference-native networks ------------------
+ * Households from an arbitrary household_id, per-occupation Watts-Strogatz and
+ * configuration-model stub pairing as keyed parallel algorithms (specification
+ * in csrc/epi_refnet.cuh); replaces GraphRealizer (graphs.py:176-240). */
+typedef struct epi_refnet_desc {
+    int64_t n_agents;
+    const int32_t *hh_members;    /* agents grouped by household            */
+    const int32_t *hh_start;      /* per agent: first slot of its household */
+    const int32_t *hh_size;       /* per agent                              */
+    int32_t n_occ;
+    int32_t _pad;
+    const int32_t *occ_members;   /* agents grouped by occupation, ids asc  */
+    const int32_t *occ_start;     /* [n_occ + 1]                            */
+    const int32_t *occ_k;         /* round_to_even(mean interactions)       */
+    int64_t n_member_slots;
+    double rewire_beta;
+    const double *random_degree;  /* [N] target random degree               */
+    int64_t table_slots;          /* power of two >= 2 * (rewired + pairs)  */
+} epi_refnet_desc;
+
+typedef struct epi_refnet_t epi_refnet_t;
+
+int epi_refnet_create(const epi_refnet_desc *desc, epi_refnet_t **out);
+int epi_refnet_destroy(epi_refnet_t *net);
+/* Edges of step `step` given dead[N] (u8): writes COO into src/dst/kind
+ * (capacity entries) and *n_edges (host; synchronises the stream). */
+int epi_refnet_realize(epi_refnet_t *net, uint64_t seed, int32_t step, const uint8_t *dead,
+                       int32_t *src, int32_t *dst, int8_t *kind, int64_t capacity,
+                       int64_t *n_edges, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -33,6 +33,7 @@ def radix(n):
 
 def _f(v, k1, k2, rad):
     h = ((v ^ k1) * k2) & M32
+    h = ((h ^ (h >> np.uint64(16))) * np.uint64(0x7FEB352D)) & M32
     return ((h ^ (h >> np.uint64(15))) * rad) >> np.uint64(32)
 
 

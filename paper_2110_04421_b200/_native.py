@@ -65,6 +65,14 @@ class EpiNet(C.Structure):
     ]
 
 
+class EpiRefnetDesc(C.Structure):
+    _fields_ = [
+        ("n_agents", _i64), ("hh_members", _p), ("hh_start", _p), ("hh_size", _p),
+        ("n_occ", _i32), ("_pad", _i32), ("occ_members", _p), ("occ_start", _p), ("occ_k", _p),
+        ("n_member_slots", _i64), ("rewire_beta", _d), ("random_degree", _p), ("table_slots", _i64),
+    ]
+
+
 _SIGS = {
     "epi_create": (_i32, [C.POINTER(EpiParams), _i64, C.POINTER(_p)]),
     "epi_destroy": (_i32, [_p]),
@@ -88,6 +96,9 @@ _SIGS = {
                                   _p, _p]),
     "epi_net_generate": (_i32, [_p, _i32, _u64, _p, _p]),
     "epi_net_gather": (_i32, [_p, C.POINTER(EpiState), _i32, _p, _p, _p, _p]),
+    "epi_refnet_create": (_i32, [C.POINTER(EpiRefnetDesc), C.POINTER(_p)]),
+    "epi_refnet_destroy": (_i32, [_p]),
+    "epi_refnet_realize": (_i32, [_p, _u64, _i32, _p, _p, _p, _p, _i64, C.POINTER(_i64), _p]),
     "epi_net_csr": (_i32, [_p, _i32, C.POINTER(_p), C.POINTER(_p)]),
     "epi_seed_infections": (_i32, [_p, C.POINTER(EpiState), _u64, _p, _i64, _p]),
     "epi_assign_app": (_i32, [C.POINTER(EpiState), _u64, _d, _p]),
@@ -109,7 +120,7 @@ def load_library(path: os.PathLike | str | None = None) -> C.CDLL:
     for name, (res, args) in _SIGS.items():
         fn = getattr(lib, name)
         fn.restype, fn.argtypes = res, args
-    for which, cls in enumerate((EpiParams, EpiState, EpiNet)):
+    for which, cls in enumerate((EpiParams, EpiState, EpiNet, EpiRefnetDesc)):
         if lib.epi_struct_size(which) != C.sizeof(cls):
             raise DeviceError(f"ABI mismatch for {cls.__name__}: C {lib.epi_struct_size(which)} "
                               f"vs ctypes {C.sizeof(cls)}")

@@ -29,7 +29,8 @@ Every interaction is stored in both directions.
 Keyed bijection of [0, n): 3-round Feistel network on the mixed-radix domain
 [0, a*b), b = ceil(sqrt(n)), a = ceil(n/b), x = L*b + R,
     L <- (L + F(R, k0)) mod a;  R <- (R + F(L, k1)) mod b;  L <- (L + F(R, k2)) mod a
-with F(v, k) = mulhi(h ^ (h >> 15), radix), h = (v ^ k.x) * k.y mod 2^32,
+with F(v, k) = mulhi(g ^ (g >> 15), radix), g = (h ^ (h >> 16)) * 0x7FEB352D,
+h = (v ^ k.x) * k.y (all mod 2^32),
 cycle-walked back into
 [0, n) (a*b - n < b, so a walk is needed with probability < 1/sqrt(n)).
 Round keys: random slot j, round r: hash64(g, t, NET_RANDOM_PERM, j, r)

@@ -11,7 +11,10 @@
 #include <string>
 #include <vector>
 
+#include <cub/device/device_scan.cuh>
+
 #include "epi_kernels.cuh"
+#include "epi_refnet.cuh"
 
 using namespace epi;
 
@@ -229,6 +232,7 @@ int64_t epi_struct_size(int32_t which) {
     case 0: return (int64_t)sizeof(epi_params);
     case 1: return (int64_t)sizeof(epi_state);
     case 2: return (int64_t)sizeof(epi_net);
+    case 3: return (int64_t)sizeof(epi_refnet_desc);
     default: return -1;
   }
 }
@@ -825,6 +829,112 @@ int epi_assign_app(const epi_state* st, uint64_t seed, double adoption, void* st
   if (!st) return fail(EPI_EARG, "null argument");
   k_assign_app<<<grid_for(st->n_agents, 256), 256, 0, S(stream)>>>(*st, key_prefix(seed, 0, P_APP), adoption);
   CKL();
+  return 0;
+}
+
+struct epi_refnet_t {
+  RefNet net{};
+  RefScratch sc{};
+  int64_t n_member_slots = 0;
+  void* scan_tmp = nullptr;
+  size_t scan_bytes = 0;
+};
+
+int epi_refnet_create(const epi_refnet_desc* d, epi_refnet_t** out) {
+  if (!d || !out || d->n_agents < 1 || d->n_agents >= (1ll << 30) || d->n_occ < 0)
+    return fail(EPI_EARG, "bad reference-network descriptor");
+  if (d->table_slots < 2 || (d->table_slots & (d->table_slots - 1)))
+    return fail(EPI_EARG, "table_slots must be a power of two");
+  epi_refnet_t* r = new epi_refnet_t();
+  RefNet& n = r->net;
+  n.n_agents = d->n_agents;
+  n.hh_members = d->hh_members;
+  n.hh_start = d->hh_start;
+  n.hh_size = d->hh_size;
+  n.n_occ = d->n_occ;
+  n.occ_members = d->occ_members;
+  n.occ_start = d->occ_start;
+  n.occ_k = d->occ_k;
+  n.beta = d->rewire_beta;
+  n.random_degree = d->random_degree;
+  RefScratch& S = r->sc;
+  int rc = dalloc(&S.live_members, (size_t)d->n_member_slots + 1);
+  if (!rc) rc = dalloc(&S.occ_live, (size_t)d->n_occ + 1);
+  if (!rc) rc = dalloc(&S.stub_count, (size_t)d->n_agents + 1);
+  if (!rc) rc = dalloc(&S.stub_off, (size_t)d->n_agents + 1);
+  if (!rc) rc = dalloc(&S.table, (size_t)d->table_slots * 2);
+  if (!rc) rc = dalloc(&S.counter, 2);
+  S.table_slots = d->table_slots;
+  r->n_member_slots = d->n_member_slots;
+  if (!rc) {
+    size_t need = 0;
+    if (cub::DeviceScan::ExclusiveSum(nullptr, need, S.stub_count, S.stub_off, (int)(d->n_agents + 1)) !=
+        cudaSuccess)
+      rc = fail(EPI_ECUDA, "scan sizing");
+    else if (cudaMalloc(&r->scan_tmp, need + 16) != cudaSuccess)
+      rc = fail(EPI_ECUDA, "scan scratch");
+    r->scan_bytes = need + 16;
+  }
+  if (rc) {
+    epi_refnet_destroy(r);
+    return rc;
+  }
+  *out = r;
+  return 0;
+}
+
+int epi_refnet_destroy(epi_refnet_t* r) {
+  if (!r) return 0;
+  cudaFree(r->sc.live_members);
+  cudaFree(r->sc.occ_live);
+  cudaFree(r->sc.stub_count);
+  cudaFree(r->sc.stub_off);
+  cudaFree(r->sc.table);
+  cudaFree(r->sc.counter);
+  cudaFree(r->scan_tmp);
+  delete r;
+  return 0;
+}
+
+int epi_refnet_realize(epi_refnet_t* r, uint64_t seed, int32_t step, const uint8_t* dead, int32_t* src,
+                       int32_t* dst, int8_t* kind, int64_t capacity, int64_t* n_edges, void* stream) {
+  if (!r || !dead || !src || !dst || !kind || !n_edges) return fail(EPI_EARG, "null argument");
+  cudaStream_t s = S(stream);
+  RefScratch S = r->sc;
+  S.out_src = src;
+  S.out_dst = dst;
+  S.out_kind = kind;
+  S.capacity = capacity;
+  const int64_t n = r->net.n_agents;
+  CK(cudaMemsetAsync(S.counter, 0, 2 * sizeof(unsigned long long), s));
+  CK(cudaMemsetAsync(S.table, 0xFF, (size_t)S.table_slots * 2 * sizeof(unsigned long long), s));
+  k_ref_households<<<grid_for(n, 256), 256, 0, s>>>(r->net, dead, S);
+  CKL();
+  if (r->net.n_occ > 0) {
+    k_ref_occ_live<<<r->net.n_occ, 256, 0, s>>>(r->net, dead, S);
+    CKL();
+    const uint64_t ws = key_prefix(seed, step, P_REF_WS);
+    const dim3 g(8, r->net.n_occ);
+    k_ref_ws<0><<<g, 256, 0, s>>>(r->net, S, ws);
+    CKL();
+    k_ref_ws<1><<<g, 256, 0, s>>>(r->net, S, ws);
+    CKL();
+  }
+  k_ref_stub_count<<<grid_for(n, 256), 256, 0, s>>>(r->net, dead, S, key_prefix(seed, step, P_REF_STUB));
+  CKL();
+  size_t bytes = r->scan_bytes;
+  CK(cub::DeviceScan::ExclusiveSum(r->scan_tmp, bytes, S.stub_count, S.stub_off, (int)(n + 1), s));
+  const PermKeys K = random_slot_keys(key_prefix(seed, step, P_REF_PERM), 0);
+  k_ref_pairs<0><<<grid_for(n * 4, 256), 256, 0, s>>>(r->net, S, K);
+  CKL();
+  k_ref_pairs<1><<<grid_for(n * 4, 256), 256, 0, s>>>(r->net, S, K);
+  CKL();
+  unsigned long long h[2] = {0, 0};
+  CK(cudaMemcpyAsync(h, S.counter, sizeof(h), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  *n_edges = (int64_t)h[0];
+  if (h[1] & 1ull) return fail(EPI_EARG, "edge output capacity exceeded");
+  if (h[1] & 2ull) return fail(EPI_EARG, "dedupe hash table full");
   return 0;
 }
 

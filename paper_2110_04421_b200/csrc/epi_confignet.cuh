@@ -47,8 +47,13 @@ __host__ __device__ __forceinline__ Radix make_radix(uint32_t n) {
   r.magic = 0xFFFFFFFFu / r.b;
   return r;
 }
+// Round function: keyed multiply, then one xorshift-multiply-xorshift stage.
+// The plain multiplicative hash is nearly linear in v, which made pi(x+1) -
+// pi(x) take only a few thousand distinct values (adjacent agents got
+// partners that were adjacent too); the extra stage gives random-like spacing.
 __device__ __forceinline__ uint32_t feistel_f(uint32_t v, uint32_t k1, uint32_t k2, uint32_t radix) {
-  const uint32_t h = (v ^ k1) * k2;
+  uint32_t h = (v ^ k1) * k2;
+  h = (h ^ (h >> 16)) * 0x7FEB352Du;
   return __umulhi(h ^ (h >> 15), radix);
 }
 __device__ __forceinline__ void split(uint32_t x, const Radix& d, uint32_t& L, uint32_t& R) {

@@ -1,0 +1,248 @@
+// Reference-native networks on the device:
+// households from an arbitrary household_id, one Watts-Strogatz small-world
+// graph per occupation, and configuration-model stub pairing — the three
+// families of GraphRealizer.realize (graphs.py:54-75, 86-129, 138-168,
+// 200-240), re-defined as keyed parallel algorithms:
+//
+//  * households: complete graph on the alive members (exact, no randomness);
+//  * occupation j: ring lattice over its alive members in id order, k =
+//    min(round_to_even(mean_j), 2*floor((m-1)/2)); lattice edge e = (p, p+i),
+//    index e = (i-1)*m + p, is rewired iff u(e) < beta, to the position
+//    p + k/2 + 1 + floor(u'(e) * (m-k-1)) (uniform over p's non-neighbours;
+//    the reference instead rejects self/duplicates sequentially);
+//  * stub pairing: agent a gets floor(d_a) + [u(a) < frac(d_a)] stubs; stub q
+//    sits at position pi^{-1}(q) of a keyed Feistel permutation of [0, S);
+//    positions (2i, 2i+1) pair up; self pairs are dropped.
+// Duplicate undirected pairs (from rewiring or pairing) are resolved
+// deterministically: a pair survives only for its lowest edge / pair index
+// (atomicMin into an open-addressing hash table), matching the reference's
+// "keep first" rule (graphs.py:161-167) for stub pairs.
+#pragma once
+
+#include "epi_confignet.cuh"
+
+namespace epi {
+
+enum RefPurpose : int { P_REF_WS = 81, P_REF_STUB = 82, P_REF_PERM = 83 };
+
+struct RefNet {
+  int64_t n_agents;
+  const int32_t* hh_members;    // agents grouped by household
+  const int32_t* hh_start;      // per agent: first slot of its household
+  const int32_t* hh_size;       // per agent
+  int32_t n_occ;                // occupations 1..n_occ
+  const int32_t* occ_members;   // agents grouped by occupation, ascending ids
+  const int32_t* occ_start;     // [n_occ + 1]
+  const int32_t* occ_k;         // [n_occ] round_to_even(mean) (clipped per step)
+  double beta;
+  const double* random_degree;  // [N]
+};
+
+struct RefScratch {
+  int32_t* live_members;        // per occupation: its alive members, compacted
+  int32_t* occ_live;            // [n_occ]: alive count
+  int64_t* stub_count;          // [N + 1] (last = 0)
+  int64_t* stub_off;            // [N + 1] exclusive scan (device scan writes it)
+  unsigned long long* table;    // hash: (key, lowest index) per slot; all-ones = empty
+  int64_t table_slots;          // power of two
+  int32_t* out_src;
+  int32_t* out_dst;
+  int8_t* out_kind;
+  unsigned long long* counter;  // [0] = edges written, [1] = flags
+  int64_t capacity;
+};
+
+__device__ __forceinline__ double ref_u(uint64_t prefix, uint64_t idx, uint64_t k) {
+  return unit(fold(fold(prefix, idx), k));
+}
+
+// Warp-aggregated reservation of `n` output slots (n may differ per lane).
+__device__ __forceinline__ int64_t reserve(unsigned long long* counter, int n) {
+  const unsigned mask = __activemask();
+  int incl = n;
+  const int lane = lane_id();
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(mask, incl, o);
+    if (lane >= o && ((mask >> (lane - o)) & 1u)) incl += v;
+  }
+  const int leader = 31 - __clz(mask);
+  const int total = __shfl_sync(mask, incl, leader);
+  unsigned long long base = 0;
+  if (lane == leader && total) base = atomicAdd(counter, (unsigned long long)total);
+  base = __shfl_sync(mask, base, leader);
+  return (int64_t)base + incl - n;
+}
+
+__device__ __forceinline__ void emit2(const RefScratch& S, int64_t at, int32_t u, int32_t v, int8_t kind) {
+  if (at + 2 <= S.capacity) {
+    S.out_src[at] = u; S.out_dst[at] = v; S.out_kind[at] = kind;
+    S.out_src[at + 1] = v; S.out_dst[at + 1] = u; S.out_kind[at + 1] = kind;
+  } else {
+    atomicOr(&S.counter[1], 1ull);   // overflow flag
+  }
+}
+
+// Households: each alive agent b emits c -> b for its alive co-members.
+__global__ void k_ref_households(RefNet net, const uint8_t* __restrict__ dead, RefScratch S) {
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < net.n_agents;
+       b += (int64_t)gridDim.x * blockDim.x) {
+    int cnt = 0;
+    const int st = net.hh_start[b], sz = net.hh_size[b];
+    const bool alive = !dead[b];
+    if (alive)
+      for (int i = 0; i < sz; ++i) {
+        const int32_t c = net.hh_members[st + i];
+        cnt += (c != b && !dead[c]) ? 1 : 0;
+      }
+    const int64_t at = reserve(S.counter, cnt);
+    if (alive) {
+      int o = 0;
+      for (int i = 0; i < sz; ++i) {
+        const int32_t c = net.hh_members[st + i];
+        if (c != b && !dead[c]) {
+          if (at + o < S.capacity) {
+            S.out_src[at + o] = c; S.out_dst[at + o] = (int32_t)b; S.out_kind[at + o] = 0;
+          } else {
+            atomicOr(&S.counter[1], 1ull);
+          }
+          ++o;
+        }
+      }
+    }
+  }
+}
+
+// Alive positions inside every occupation (one block per occupation).
+__global__ void k_ref_occ_live(RefNet net, const uint8_t* __restrict__ dead, RefScratch S) {
+  typedef cub::BlockScan<int, 256> Scan;
+  __shared__ typename Scan::TempStorage tmp;
+  __shared__ int carry;
+  const int j = blockIdx.x;
+  const int lo = net.occ_start[j], hi = net.occ_start[j + 1];
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int b0 = lo; b0 < hi; b0 += 256) {
+    const int i = b0 + threadIdx.x;
+    const int alive = (i < hi && !dead[net.occ_members[i]]) ? 1 : 0;
+    int ex, total;
+    Scan(tmp).ExclusiveSum(alive, ex, total);
+    if (alive) S.live_members[lo + carry + ex] = net.occ_members[i];
+    __syncthreads();
+    if (threadIdx.x == 0) carry += total;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) S.occ_live[j] = carry;
+}
+
+__device__ __forceinline__ uint64_t hash_slot(uint64_t key, int64_t slots) {
+  return mix64(key ^ 0x5851F42D4C957F2Dull) & (uint64_t)(slots - 1);
+}
+// undirected pair + network kind (pairs only collide within one family)
+__device__ __forceinline__ uint64_t pair_key(uint32_t u, uint32_t v, int kind) {
+  const uint32_t a = u < v ? u : v, b = u < v ? v : u;
+  return ((uint64_t)kind << 62) | ((uint64_t)a << 31) | b;
+}
+__device__ __forceinline__ bool table_is_winner(const RefScratch& S, uint64_t key, uint64_t idx) {
+  uint64_t h = hash_slot(key, S.table_slots);
+  for (int64_t probe = 0; probe < S.table_slots; ++probe) {
+    const unsigned long long kk = S.table[2 * h];
+    if (kk == key) return S.table[2 * h + 1] == idx;
+    if (kk == ~0ull) return false;
+    h = (h + 1) & (uint64_t)(S.table_slots - 1);
+  }
+  return false;
+}
+// Insert key; keep the minimum index for it.  Returns the slot.
+__device__ __forceinline__ int64_t table_insert(const RefScratch& S, uint64_t key, uint64_t idx) {
+  uint64_t h = hash_slot(key, S.table_slots);
+  for (int64_t probe = 0; probe < S.table_slots; ++probe) {
+    unsigned long long* k = S.table + 2 * h;
+    const unsigned long long prev = atomicCAS(k, ~0ull, key);       // ~0 = empty
+    if (prev == ~0ull || prev == key) {
+      atomicMin(k + 1, (unsigned long long)idx);
+      return (int64_t)h;
+    }
+    h = (h + 1) & (uint64_t)(S.table_slots - 1);
+  }
+  atomicOr(&S.counter[1], 2ull);     // table full
+  return -1;
+}
+
+// Watts-Strogatz lattice edges of occupation j (one block per occupation;
+// threads over edge indices).  Pass 0 inserts rewired pairs, pass 1 emits.
+template <int PASS>
+__global__ void k_ref_ws(RefNet net, RefScratch S, uint64_t ws_prefix) {
+  const int j = blockIdx.y;
+  const int lo = net.occ_start[j];
+  const int m = S.occ_live[j];
+  const int kmax = 2 * ((m - 1) / 2);
+  const int k = net.occ_k[j] < kmax ? net.occ_k[j] : kmax;
+  if (m < 3 || k < 2) return;
+  const int half = k / 2;
+  const int64_t n_edges = (int64_t)half * m;
+  const int span = m - k - 1;                   // non-neighbours of a node
+  // alive members by position: members with live_pos >= 0 in id order
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_edges;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e / m) + 1, p = (int)(e % m);
+    const uint64_t idx = ((uint64_t)(j + 1) << 40) | (uint64_t)e;
+    const bool rewired = span > 0 && ref_u(ws_prefix, idx, 0) < net.beta;
+    int q = (p + i) % m;
+    if (rewired) q = (int)((p + half + 1 + (int)(ref_u(ws_prefix, idx, 1) * span)) % m);
+    const int32_t u = S.live_members[lo + p], v = S.live_members[lo + q];
+    if (!rewired) {
+      if (PASS == 1) emit2(S, reserve(S.counter, 2), u, v, 1);
+      continue;
+    }
+    const uint64_t key = pair_key((uint32_t)u, (uint32_t)v, 1);
+    if (PASS == 0) table_insert(S, key, idx);
+    else if (table_is_winner(S, key, idx)) emit2(S, reserve(S.counter, 2), u, v, 1);
+  }
+}
+
+// Stub counts of alive agents.
+__global__ void k_ref_stub_count(RefNet net, const uint8_t* __restrict__ dead, RefScratch S,
+                                 uint64_t stub_prefix) {
+  for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < net.n_agents;
+       a += (int64_t)gridDim.x * blockDim.x) {
+    int c = 0;
+    if (!dead[a]) {
+      const double d = net.random_degree[a];
+      const double fl = floor(d);
+      c = (int)fl + (ref_u(stub_prefix, (uint64_t)a, 0) < d - fl ? 1 : 0);
+    }
+    S.stub_count[a] = c;
+    if (a == 0) S.stub_count[net.n_agents] = 0;
+  }
+}
+
+__device__ __forceinline__ int32_t stub_owner(const RefScratch& S, int64_t n, int64_t q) {
+  int64_t a = 0, b = n;            // largest a with stub_off[a] <= q
+  while (b - a > 1) {
+    const int64_t mid = (a + b) >> 1;
+    if (S.stub_off[mid] <= q) a = mid; else b = mid;
+  }
+  return (int32_t)a;
+}
+
+// Stub pairs: positions (2i, 2i+1) of the keyed permutation of [0, S).
+template <int PASS>
+__global__ void k_ref_pairs(RefNet net, RefScratch S, PermKeys K) {
+  const int64_t n_stubs = S.stub_off[net.n_agents];
+  if (n_stubs < 2 || n_stubs >= (1ll << 31)) return;
+  const Radix d = make_radix((uint32_t)n_stubs);
+  const int64_t n_pairs = n_stubs / 2;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_pairs;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t s0 = walk_fwd((uint32_t)(2 * i), K, d);
+    const uint32_t s1 = walk_fwd((uint32_t)(2 * i + 1), K, d);
+    const int32_t u = stub_owner(S, net.n_agents, s0), v = stub_owner(S, net.n_agents, s1);
+    if (u == v) continue;
+    const uint64_t key = pair_key((uint32_t)u, (uint32_t)v, 2);
+    const uint64_t idx = (uint64_t)i;
+    if (PASS == 0) table_insert(S, key, idx);
+    else if (table_is_winner(S, key, idx)) emit2(S, reserve(S.counter, 2), u, v, 2);
+  }
+}
+
+}  // namespace epi

@@ -67,3 +67,23 @@ def default_disease():
 def default_progression():
     from .progression import ProgressionTable
     return ProgressionTable.from_dict(PROGRESSION)
+
+
+# Synthetic population spec (data/population_spec.json:4-22), used by the
+# reference-native scenarios (population.py:43-108).
+POPULATION = {
+    "n_agents": 10_000,
+    "age_distribution": [0.12, 0.13, 0.14, 0.13, 0.13, 0.13, 0.10, 0.07, 0.05],
+    "household_size_distribution": {"sizes": [1, 2, 3, 4, 5, 6],
+                                    "probabilities": [0.28, 0.34, 0.15, 0.13, 0.07, 0.03]},
+    "occupation_distribution": [0.09, 0.08, 0.07, 0.07, 0.06, 0.06, 0.05, 0.05, 0.05, 0.05,
+                                0.04, 0.04, 0.04, 0.04, 0.04, 0.03, 0.03, 0.03, 0.02, 0.02,
+                                0.02, 0.01, 0.01],
+    "occupation_eligible_age_bands": [2, 3, 4, 5, 6],
+    "random_degree_by_age": [2.0, 3.5, 4.5, 4.5, 4.5, 4.0, 3.5, 2.5, 2.0],
+    "networks": {
+        "occupation_mean_interactions": [10, 8, 12, 6, 8, 10, 8, 6, 14, 8, 6, 10, 4, 8, 12, 6, 8,
+                                         10, 4, 6, 8, 12, 6],
+        "rewire_beta": 0.1,
+    },
+}

@@ -31,7 +31,7 @@ def test_library_exports_every_declared_symbol():
 def test_struct_sizes_match():
     lib = N.load_library()
     import ctypes
-    for i, cls in enumerate((N.EpiParams, N.EpiState, N.EpiNet)):
+    for i, cls in enumerate((N.EpiParams, N.EpiState, N.EpiNet, N.EpiRefnetDesc)):
         assert lib.epi_struct_size(i) == ctypes.sizeof(cls)
 
 

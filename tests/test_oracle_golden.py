@@ -115,3 +115,20 @@ def test_oracle_replays_reference_trajectory(name):
         assert got == tr.events[step].tolist(), f"events differ at step {step}"
         compare_state(cols, tr, step)
     assert eng.vaccination_open == bool(tr.z["vaccination_open"])
+
+
+@pytest.mark.parametrize("name", ["noiv", "alliv"])
+def test_reference_realizer_restatement_reproduces_recorded_graphs(name):
+    """oracle/graphs_np restates GraphRealizer draw for draw (graphs.py:176-240)."""
+    from oracle.graphs_np import ReferenceRealizer
+    from paper_2110_04421_b200.defaults import POPULATION
+    tr = Trajectory(name)
+    z = tr.z
+    rr = ReferenceRealizer(tr.seed, z["init_household_id"], z["init_occupation"],
+                           z["init_random_degree"], POPULATION["networks"]["occupation_mean_interactions"],
+                           POPULATION["networks"]["rewire_beta"])
+    for step in range(min(tr.horizon, 12)):
+        dead = (z["init_stage"] if step == 0 else tr.state(step - 1, "stage")) == 10
+        s, d, k = rr.realize(step, dead)
+        g = tr.graph(step)
+        assert np.array_equal(s, g.src) and np.array_equal(d, g.dst) and np.array_equal(k, g.kind)
