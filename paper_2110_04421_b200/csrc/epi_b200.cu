@@ -935,6 +935,7 @@ int epi_refnet_realize(epi_refnet_t* r, uint64_t seed, int32_t step, const uint8
   *n_edges = (int64_t)h[0];
   if (h[1] & 1ull) return fail(EPI_EARG, "edge output capacity exceeded");
   if (h[1] & 2ull) return fail(EPI_EARG, "dedupe hash table full");
+  if (h[1] & 4ull) return fail(EPI_EARG, "more than 2^31 random-network stubs");
   return 0;
 }
 

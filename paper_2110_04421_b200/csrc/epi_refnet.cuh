@@ -56,20 +56,22 @@ __device__ __forceinline__ double ref_u(uint64_t prefix, uint64_t idx, uint64_t 
   return unit(fold(fold(prefix, idx), k));
 }
 
-// Warp-aggregated reservation of `n` output slots (n may differ per lane).
+// Warp-aggregated reservation of `n` output slots (n may differ per lane,
+// 0 for lanes with nothing to write).  Must be called by all 32 lanes: every
+// loop below runs whole warps (blockDim is a multiple of 32 and the trip
+// count is warp-uniform), with `valid` masking the tail.
 __device__ __forceinline__ int64_t reserve(unsigned long long* counter, int n) {
-  const unsigned mask = __activemask();
   int incl = n;
   const int lane = lane_id();
+#pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
-    const int v = __shfl_up_sync(mask, incl, o);
-    if (lane >= o && ((mask >> (lane - o)) & 1u)) incl += v;
+    const int v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    if (lane >= o) incl += v;
   }
-  const int leader = 31 - __clz(mask);
-  const int total = __shfl_sync(mask, incl, leader);
+  const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
   unsigned long long base = 0;
-  if (lane == leader && total) base = atomicAdd(counter, (unsigned long long)total);
-  base = __shfl_sync(mask, base, leader);
+  if (lane == 31 && total) base = atomicAdd(counter, (unsigned long long)total);
+  base = __shfl_sync(0xFFFFFFFFu, base, 31);
   return (int64_t)base + incl - n;
 }
 
@@ -84,29 +86,27 @@ __device__ __forceinline__ void emit2(const RefScratch& S, int64_t at, int32_t u
 
 // Households: each alive agent b emits c -> b for its alive co-members.
 __global__ void k_ref_households(RefNet net, const uint8_t* __restrict__ dead, RefScratch S) {
-  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < net.n_agents;
-       b += (int64_t)gridDim.x * blockDim.x) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t b0 = (int64_t)blockIdx.x * blockDim.x; b0 < net.n_agents; b0 += stride) {
+    const int64_t b = b0 + threadIdx.x;
+    const bool alive = b < net.n_agents && !dead[b];
+    const int st = alive ? net.hh_start[b] : 0, sz = alive ? net.hh_size[b] : 0;
     int cnt = 0;
-    const int st = net.hh_start[b], sz = net.hh_size[b];
-    const bool alive = !dead[b];
-    if (alive)
-      for (int i = 0; i < sz; ++i) {
-        const int32_t c = net.hh_members[st + i];
-        cnt += (c != b && !dead[c]) ? 1 : 0;
-      }
+    for (int i = 0; i < sz; ++i) {
+      const int32_t c = net.hh_members[st + i];
+      cnt += (c != b && !dead[c]) ? 1 : 0;
+    }
     const int64_t at = reserve(S.counter, cnt);
-    if (alive) {
-      int o = 0;
-      for (int i = 0; i < sz; ++i) {
-        const int32_t c = net.hh_members[st + i];
-        if (c != b && !dead[c]) {
-          if (at + o < S.capacity) {
-            S.out_src[at + o] = c; S.out_dst[at + o] = (int32_t)b; S.out_kind[at + o] = 0;
-          } else {
-            atomicOr(&S.counter[1], 1ull);
-          }
-          ++o;
+    int o = 0;
+    for (int i = 0; i < sz; ++i) {
+      const int32_t c = net.hh_members[st + i];
+      if (c != b && !dead[c]) {
+        if (at + o < S.capacity) {
+          S.out_src[at + o] = c; S.out_dst[at + o] = (int32_t)b; S.out_kind[at + o] = 0;
+        } else {
+          atomicOr(&S.counter[1], 1ull);
         }
+        ++o;
       }
     }
   }
@@ -181,22 +181,31 @@ __global__ void k_ref_ws(RefNet net, RefScratch S, uint64_t ws_prefix) {
   const int half = k / 2;
   const int64_t n_edges = (int64_t)half * m;
   const int span = m - k - 1;                   // non-neighbours of a node
-  // alive members by position: members with live_pos >= 0 in id order
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_edges;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int i = (int)(e / m) + 1, p = (int)(e % m);
-    const uint64_t idx = ((uint64_t)(j + 1) << 40) | (uint64_t)e;
-    const bool rewired = span > 0 && ref_u(ws_prefix, idx, 0) < net.beta;
-    int q = (p + i) % m;
-    if (rewired) q = (int)((p + half + 1 + (int)(ref_u(ws_prefix, idx, 1) * span)) % m);
-    const int32_t u = S.live_members[lo + p], v = S.live_members[lo + q];
-    if (!rewired) {
-      if (PASS == 1) emit2(S, reserve(S.counter, 2), u, v, 1);
-      continue;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t e0 = (int64_t)blockIdx.x * blockDim.x; e0 < n_edges; e0 += stride) {
+    const int64_t e = e0 + threadIdx.x;
+    bool emit = false;
+    int32_t u = 0, v = 0;
+    if (e < n_edges) {
+      const int i = (int)(e / m) + 1, p = (int)(e % m);
+      const uint64_t idx = ((uint64_t)(j + 1) << 40) | (uint64_t)e;
+      const bool rewired = span > 0 && ref_u(ws_prefix, idx, 0) < net.beta;
+      int q = (p + i) % m;
+      if (rewired) q = (int)((p + half + 1 + (int)(ref_u(ws_prefix, idx, 1) * span)) % m);
+      u = S.live_members[lo + p];
+      v = S.live_members[lo + q];
+      if (!rewired) {
+        emit = PASS == 1;
+      } else {
+        const uint64_t key = pair_key((uint32_t)u, (uint32_t)v, 1);
+        if (PASS == 0) table_insert(S, key, idx);
+        else emit = table_is_winner(S, key, idx);
+      }
     }
-    const uint64_t key = pair_key((uint32_t)u, (uint32_t)v, 1);
-    if (PASS == 0) table_insert(S, key, idx);
-    else if (table_is_winner(S, key, idx)) emit2(S, reserve(S.counter, 2), u, v, 1);
+    if (PASS == 1) {
+      const int64_t at = reserve(S.counter, emit ? 2 : 0);
+      if (emit) emit2(S, at, u, v, 1);
+    }
   }
 }
 
@@ -229,19 +238,33 @@ __device__ __forceinline__ int32_t stub_owner(const RefScratch& S, int64_t n, in
 template <int PASS>
 __global__ void k_ref_pairs(RefNet net, RefScratch S, PermKeys K) {
   const int64_t n_stubs = S.stub_off[net.n_agents];
-  if (n_stubs < 2 || n_stubs >= (1ll << 31)) return;
+  if (n_stubs >= (1ll << 31)) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(&S.counter[1], 4ull);
+    return;
+  }
+  if (n_stubs < 2) return;
   const Radix d = make_radix((uint32_t)n_stubs);
   const int64_t n_pairs = n_stubs / 2;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_pairs;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t s0 = walk_fwd((uint32_t)(2 * i), K, d);
-    const uint32_t s1 = walk_fwd((uint32_t)(2 * i + 1), K, d);
-    const int32_t u = stub_owner(S, net.n_agents, s0), v = stub_owner(S, net.n_agents, s1);
-    if (u == v) continue;
-    const uint64_t key = pair_key((uint32_t)u, (uint32_t)v, 2);
-    const uint64_t idx = (uint64_t)i;
-    if (PASS == 0) table_insert(S, key, idx);
-    else if (table_is_winner(S, key, idx)) emit2(S, reserve(S.counter, 2), u, v, 2);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < n_pairs; i0 += stride) {
+    const int64_t i = i0 + threadIdx.x;
+    bool emit = false;
+    int32_t u = 0, v = 0;
+    if (i < n_pairs) {
+      const uint32_t s0 = walk_fwd((uint32_t)(2 * i), K, d);
+      const uint32_t s1 = walk_fwd((uint32_t)(2 * i + 1), K, d);
+      u = stub_owner(S, net.n_agents, s0);
+      v = stub_owner(S, net.n_agents, s1);
+      if (u != v) {
+        const uint64_t key = pair_key((uint32_t)u, (uint32_t)v, 2);
+        if (PASS == 0) table_insert(S, key, (uint64_t)i);
+        else emit = table_is_winner(S, key, (uint64_t)i);
+      }
+    }
+    if (PASS == 1) {
+      const int64_t at = reserve(S.counter, emit ? 2 : 0);
+      if (emit) emit2(S, at, u, v, 2);
+    }
   }
 }
 
