@@ -322,7 +322,7 @@ def run_ours(a):
         # the HBM-bound kernel of the decomposition, streamed 16-bit messages
         from paper_2110_04421_b200.roofline import message_pass_roofline
         mp = message_pass_roofline(10_000_000, peak_gbps=peak)
-        tr = json.loads(tfile.read_text()).get("k_pass<F32,0> message pass (10M agents)") \
+        tr = json.loads(tfile.read_text()).get("k_msg_pass<0> message pass (10M agents)") \
             if tfile.exists() else None
         mp["traffic"] = (tr["dram_bytes_read"] + tr["dram_bytes_write"]) if tr else None
         mp["bound"] = "hbm"

@@ -14,6 +14,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include "epi_kernels.cuh"
+#include "epi_msgpass.cuh"
 #include "epi_refnet.cuh"
 
 using namespace epi;
@@ -125,6 +126,7 @@ struct epi_ctx {
   std::vector<int32_t*> net_rowlen;
   std::vector<int32_t> net_slot_step;
   MsgTables* msg_dev = nullptr;      // fp32 message tables (rate_scale baked in)
+  MsgComb* comb_dev = nullptr;       // fp64 weights of the pre-joined messages
   NetTables ntab{};                  // host copy (static radix tables)
   NetTables* ntab_dev[3] = {nullptr, nullptr, nullptr};   // per-day keys, by step % 3
   WorkTables wt_host[2]{};           // day tables by step parity (member_at_pos shared)
@@ -148,6 +150,10 @@ int upload_params(epi_ctx* c, const epi_params* p) {
   fill_msg_tables(mt, *p, p->rate_scale);
   if (!c->msg_dev) CK(cudaMalloc((void**)&c->msg_dev, sizeof(MsgTables)));
   CK(cudaMemcpy(c->msg_dev, &mt, sizeof(MsgTables), cudaMemcpyHostToDevice));
+  static MsgComb mc;   // 8 KB: not on the stack
+  fill_msg_comb(mc, *p, p->rate_scale);
+  if (!c->comb_dev) CK(cudaMalloc((void**)&c->comb_dev, sizeof(MsgComb)));
+  CK(cudaMemcpy(c->comb_dev, &mc, sizeof(MsgComb), cudaMemcpyHostToDevice));
   return 0;
 }
 
@@ -222,6 +228,23 @@ int run_interventions(epi_ctx* c, const StepArgs& A, uint16_t* codes_next, const
 
 }  // namespace
 
+// k_msg_pass: per-warp segment scratch
+static int msg_pass_smem(int) { return MP_SMEM; }
+
+// persistent grid: as many k_msg_pass blocks as fit on every SM at once
+template <int MODE>
+static int msg_pass_grid(int cap, int64_t rows) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_msg_pass<MODE>, MP_WARPS * 32,
+                                                    msg_pass_smem(cap)) != cudaSuccess || per_sm < 1)
+    per_sm = 1;
+  int64_t tiles = (rows + 31) / 32;
+  int64_t g = (int64_t)sm_count() * per_sm;
+  const int64_t need = (tiles + MP_WARPS - 1) / MP_WARPS;
+  if (g > need) g = need;
+  return (int)(g < 1 ? 1 : g);
+}
+
 extern "C" {
 
 const char* epi_last_error(void) { return g_err.c_str(); }
@@ -289,6 +312,7 @@ int epi_destroy(epi_ctx* c) {
   cudaFree(c->net_dev);
   cudaFree(c->inj_dev);
   cudaFree(c->msg_dev);
+  cudaFree(c->comb_dev);
   for (auto* p : c->ntab_dev) cudaFree(p);
   cudaFree(c->wt_host[0].member_at_pos);
   for (auto& w : c->wt_host) {
@@ -517,9 +541,9 @@ static int prepare_realize(const epi_net* net) {
     CK(cudaFuncSetAttribute(k_net_realize<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     CK(cudaFuncSetAttribute(k_net_realize<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     CK(cudaFuncSetAttribute(k_net_realize<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const int psmem = 8 * 32 * net->row_cap * (int)sizeof(uint16_t);
-    CK(cudaFuncSetAttribute(k_pass<false, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, psmem));
-    CK(cudaFuncSetAttribute(k_pass<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, psmem));
+    const int psmem = msg_pass_smem(net->row_cap);
+    CK(cudaFuncSetAttribute(k_msg_pass<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, psmem));
+    CK(cudaFuncSetAttribute(k_msg_pass<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, psmem));
     g_realize_smem_set = smem;
   }
   return 0;
@@ -592,9 +616,12 @@ int epi_net_attach(epi_ctx* c, const epi_net* net) {
     if (!rc) rc = dalloc(&c->net_rowlen[i], (size_t)c->n);
     if (rc) return rc;
   }
-  rc = dalloc(&c->net_msgs, (size_t)((c->n + 31) / 32) * 32 * net->row_cap + 16);
+  // zero-filled: every u16 of the buffer is always a valid weight-table offset
+  const size_t n_msgs = (size_t)((c->n + 31) / 32) * 32 * msg_cap(net->row_cap) + 16;
+  rc = dalloc(&c->net_msgs, n_msgs);
   if (!rc) rc = dalloc(&c->net_toff, (size_t)((c->n + 31) / 32) * 33);
   if (rc) return rc;
+  CK(cudaMemset(c->net_msgs, 0, n_msgs * sizeof(uint16_t)));
   rc = dalloc(&c->wt_host[0].member_at_pos, (size_t)net->n_member_slots);
   if (rc) return rc;
   for (int par = 0; par < 2; ++par) {
@@ -691,7 +718,7 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
   if (mode == 0) {
     // fp32 without contact log: the generator writes pre-joined messages and
     // the message pass streams them; otherwise ids (export, DEN, fp64 order)
-    const bool msg_only = precision == EPI_F32 && !c->host.den_enabled;
+    const bool msg_only = precision == EPI_F32 && !c->host.den_enabled && c->net.row_cap <= MP_MAX_CAP;
     uint32_t* entries = msg_only ? nullptr : c->net_entries[slot];
     uint16_t* msgs = msg_only ? c->net_msgs : nullptr;
     int32_t* row_len = c->net_rowlen[slot];
@@ -702,12 +729,16 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
     c->merged_ready = -1;
     if (ev) CK(cudaEventRecord((cudaEvent_t)ev[1], s));
     CsrView g{entries, row_len, nullptr, c->net.row_cap, msgs, c->net_toff};
-    const size_t msmem = msgs ? (size_t)8 * 32 * c->net.row_cap * sizeof(uint16_t) : 0;
     if (precision == EPI_F64_CANONICAL)
       k_pass<true, 1><<<grid, 256, 0, s>>>(A, g, codes_cur, nullptr, c->host.rate_scale, iv ? 0 : 1,
                                            codes_next, c->net_dev, rcount_next, c->msg_dev);
+    else if (msgs)
+      CK(launch_pdl(k_msg_pass<1>, dim3(msg_pass_grid<1>(c->net.row_cap, c->hi - c->lo)),
+                    dim3(MP_WARPS * 32), (size_t)msg_pass_smem(c->net.row_cap), s, A, g, (float*)nullptr,
+                    iv ? 0 : 1, codes_next, (const epi_net*)c->net_dev, rcount_next,
+                    (const MsgTables*)c->msg_dev, (const MsgComb*)c->comb_dev));
     else
-      CK(launch_pdl(k_pass<false, 1>, dim3(grid), dim3(256), msmem, s, A, g, codes_cur, (void*)nullptr,
+      CK(launch_pdl(k_pass<false, 1>, dim3(grid), dim3(256), (size_t)0, s, A, g, codes_cur, (void*)nullptr,
                     c->host.rate_scale, iv ? 0 : 1, codes_next, (const epi_net*)c->net_dev, rcount_next,
                     (const MsgTables*)c->msg_dev));
     CKL();
@@ -780,6 +811,7 @@ int epi_sim_step_timed(epi_ctx* c, const epi_state* st, int32_t step, uint64_t s
 int epi_net_generate(epi_ctx* c, int32_t step, uint64_t seed, const uint16_t* codes_cur, void* stream) {
   if (!c || !c->has_net || !codes_cur) return fail(EPI_EARG, "needs an attached network and codes");
   if (!batched(&c->net)) return fail(EPI_EARG, "epi_net_generate needs <= 16 slots and <= 8 draws");
+  if (c->net.row_cap > MP_MAX_CAP) return fail(EPI_EARG, "epi_net_generate needs row_cap <= 128");
   cudaStream_t s = S(stream);
   const NetKeys nk = make_net_keys(seed, step);
   NetTables* nt = c->ntab_dev[step % 3];
@@ -809,9 +841,10 @@ int epi_net_gather(epi_ctx* c, const epi_state* st, int32_t step, const uint16_t
   if (record) CK(cudaMemsetAsync(rec, 0, EPI_REC_LEN * sizeof(long long), S(stream)));
   StepArgs A = make_args(c, st, step, 0, rec, nullptr, false);
   CsrView g{nullptr, c->net_rowlen[0], nullptr, c->net.row_cap, c->net_msgs, c->net_toff};
-  const size_t msmem = (size_t)8 * 32 * c->net.row_cap * sizeof(uint16_t);
-  k_pass<false, 0><<<grid_for(c->hi - c->lo, 256), 256, msmem, S(stream)>>>(
-      A, g, codes_cur, lambda_out, c->host.rate_scale, 0, nullptr, nullptr, 0, c->msg_dev);
+  k_msg_pass<0><<<msg_pass_grid<0>(c->net.row_cap, c->hi - c->lo), MP_WARPS * 32,
+                  msg_pass_smem(c->net.row_cap), S(stream)>>>(A, g, lambda_out, 0, nullptr, nullptr, 0,
+                                                              (const MsgTables*)c->msg_dev,
+                                                              (const MsgComb*)c->comb_dev);
   CKL();
   return 0;
 }

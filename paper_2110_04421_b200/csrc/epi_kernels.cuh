@@ -79,8 +79,13 @@ struct MsgTables {
   float factor[256];
   float sfac[16];
   float bfac[4];
-  float comb[4 * 256];      // factor[idx] * bfac[kind] at [idx << 2 | kind] (zero
-                            // weights of the 3 kinds in banks 0-2: no conflicts)
+};
+// Weight of a pre-joined message (k_msg_pass): rate*A*w[t]*B[kind] (computed
+// in fp64, stored fp32) at [idx << 2 | kind], idx = source code & 0xFF; the
+// message itself is the byte offset of its weight, (idx << 2 | kind) << 2.
+// Message 0 (a non-infectious household source) weighs 0: it pads rows.
+struct MsgComb {
+  float w[4 * 256];
 };
 inline void fill_msg_tables(MsgTables& T, const epi_params& P, double rate) {
   for (int i = 0; i < 256; ++i) {
@@ -93,8 +98,17 @@ inline void fill_msg_tables(MsgTables& T, const epi_params& P, double rate) {
   for (int i = 0; i < 16; ++i)
     T.sfac[i] = i < 9 ? (float)(P.age_susceptibility[i] / P.mean_daily_interactions) : 0.f;
   for (int i = 0; i < 4; ++i) T.bfac[i] = i < 3 ? (float)P.network_scale[i] : 0.f;
-  for (int i = 0; i < 256; ++i)
-    for (int k = 0; k < 4; ++k) T.comb[(i << 2) | k] = T.factor[i] * T.bfac[k];
+}
+inline void fill_msg_comb(MsgComb& C, const epi_params& P, double rate) {
+  for (int i = 0; i < 256; ++i) {
+    const int t = i & 0x7F;
+    for (int k = 0; k < 4; ++k) {
+      double w = 0.0;
+      if (t >= 1 && t <= P.t_max && k < 3)
+        w = ((rate * ((i & 0x80) ? P.asymptomatic_factor : 1.0)) * P.network_scale[k]) * P.day_weights[t];
+      C.w[(i << 2) | k] = (float)w;
+    }
+  }
 }
 __device__ __forceinline__ void load_msg_tables(MsgTables& S, const MsgTables* __restrict__ G) {
   const uint32_t* src = (const uint32_t*)G;
@@ -113,8 +127,6 @@ __device__ __forceinline__ void build_msg_tables(MsgTables& T, const epi_params*
   for (int i = threadIdx.x; i < 9; i += blockDim.x)
     T.sfac[i] = (float)(P->age_susceptibility[i] / P->mean_daily_interactions);
   for (int i = threadIdx.x; i < 3; i += blockDim.x) T.bfac[i] = (float)P->network_scale[i];
-  __syncthreads();
-  for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) T.comb[i] = T.factor[i >> 2] * T.bfac[i & 3];
 }
 
 // fp64 term with the reference's pinned factor order (engine.py:100-107,
@@ -257,16 +269,21 @@ __global__ void k_rows_finish(int64_t n, const int64_t* __restrict__ row_begin,
 // ---------------------------------------------------------------------------
 // Gather / fused gather + update over a CSR given either by explicit
 // row_begin (graph-in) or implicitly by row * cap (padded config CSR).
+// Row capacity of the tile-packed message blocks (rows padded to 8).
+__host__ __device__ __forceinline__ int msg_cap(int cap) { return (cap + 7) & ~7; }
+
 struct CsrView {
   const uint32_t* __restrict__ entries;
   const int32_t* __restrict__ row_len;
   const int64_t* __restrict__ row_begin;   // null: padded rows of `cap`
   int cap;
-  // Optional pre-joined messages, tile-packed: msg = (source code & 0xFF) << 2
-  // | kind (an index into the fp32 weight table), written by the generator, so the fp32 message pass streams
+  // Optional pre-joined messages, tile-packed: msg = (source code & 0xFF) << 4
+  // | kind << 2 (a byte offset into the MsgComb table), written by the
+  // generator, so the fp32 message pass (k_msg_pass, epi_msgpass.cuh) streams
   // 2 B per edge with no gathers.  Tile k (32 rows from lo) owns the block
-  // msgs[k*32*cap ...]; its rows are packed back to back and
-  // tile_off[k*33 + r] is row r's start (tile_off[k*33 + 32] = total).
+  // msgs[k*32*msg_cap(cap) ...]; its rows are packed back to back, each
+  // padded to whole 8-message groups, and tile_off[k*33 + r] = row r's first
+  // group | pad << 12 (tile_off[k*33 + 32] = groups in the tile).
   const uint16_t* __restrict__ msgs;
   const uint16_t* __restrict__ tile_off;
   __device__ __forceinline__ int64_t begin(int64_t r) const {
@@ -285,7 +302,6 @@ __global__ void __launch_bounds__(256) k_pass(StepArgs A, CsrView g, const uint1
   __shared__ MsgTables T;
   __shared__ float lam_tile[8][32];
   __shared__ RecAcc racc;
-  extern __shared__ uint16_t msg_smem[];        // 8 warps x 32 rows x cap (msgs path)
   if (!F64) {
     if (mt) load_msg_tables(T, mt);
     else build_msg_tables(T, A.P, rate);
@@ -322,57 +338,6 @@ __global__ void __launch_bounds__(256) k_pass(StepArgs A, CsrView g, const uint1
           }
           lam = h;
         }
-      }
-    } else if (g.msgs != nullptr) {
-      // tile-packed messages: one coalesced copy of the tile's block into
-      // shared memory (16-byte vector loads), then one lane per row
-      // every global load of the tile is issued up front (one round trip):
-      // offsets, a fixed-size speculative copy of the block (3 x 16 B per
-      // lane = 768 messages; longer tiles fetch the rest) and the state bytes
-      const uint16_t* toff = g.tile_off + tile * 33;
-      const uint4* blk = (const uint4*)(g.msgs + tile * (int64_t)(32 * g.cap));
-      uint4* sm = (uint4*)(msg_smem + (size_t)warp * 32 * g.cap);
-      const int cap_chunks = (32 * g.cap * 2) >> 4;
-      const int my_lo = toff[lane];
-      const int total = toff[32];
-      uint4 v[3];
-#pragma unroll
-      for (int q = 0; q < 3; ++q)
-        if (lane + 32 * q < cap_chunks) v[q] = __ldg(blk + lane + 32 * q);
-      int stage_a = S_DEAD, imm_a = 0, age_a = 0;
-      if (valid) {
-        stage_a = A.st.stage[a];
-        imm_a = A.st.immune[a];
-        age_a = A.st.age_band[a];
-      }
-#pragma unroll
-      for (int q = 0; q < 3; ++q)
-        if (lane + 32 * q < cap_chunks) sm[lane + 32 * q] = v[q];
-      const int nchunk = (total * 2 + 15) >> 4;
-      for (int c = 96 + lane; c < nchunk; c += 32) sm[c] = __ldg(blk + c);
-      const int nxt = __shfl_down_sync(0xFFFFFFFFu, my_lo, 1);
-      const int my_hi = lane < 31 ? nxt : total;
-      __syncwarp();
-      // one lane per row, messages read in 32-bit pairs, sequential sum
-      const uint16_t* sm16 = (const uint16_t*)sm;
-      const uint32_t* sm32 = (const uint32_t*)sm;
-      float acc = 0.f;
-      int i = my_lo;
-      if ((i & 1) && i < my_hi) {
-        acc += T.comb[sm16[i]];
-        ++i;
-      }
-      for (; i + 1 < my_hi; i += 2) {
-        const uint32_t w2 = sm32[i >> 1];
-        acc += T.comb[w2 & 0xFFFF];
-        acc += T.comb[w2 >> 16];
-      }
-      if (i < my_hi) acc += T.comb[sm16[i]];
-      __syncwarp();
-      if (valid) {
-        edges = (unsigned)(my_hi - my_lo);
-        const bool target = stage_a == S_SUS && !(P->sterilizing && imm_a);
-        lam = target ? (double)(acc * T.sfac[age_a]) : 0.0;
       }
     } else {
       // 8 lanes per row, 4 rows per pass, tree sum in fp32
@@ -513,11 +478,11 @@ __global__ void __launch_bounds__(128, 6) k_net_realize(epi_net net, NetKeys nk,
       const uint16_t cb = codes[b];
       if (!code_dead(cb)) {
         // the staging row holds either ids (src<<2|kind) or messages
-        // ((code & 0xFF) << 2 | kind: the weight-table index) when only
-        // messages are requested
+        // ((code & 0xFF) << 4 | kind << 2: the byte offset of the weight in
+        // MsgComb) when only messages are requested
         auto put = [&](int64_t c, int kind, uint16_t cc) {
           mine[cnt++] = entries ? (((uint32_t)c << 2) | (uint32_t)kind)
-                                : (((uint32_t)(cc & 0xFF) << 2) | (uint32_t)kind);
+                                : (((uint32_t)(cc & 0xFF) << 4) | ((uint32_t)kind << 2));
         };
         if (BATCH) for_each_in_edge_batched<16, 8>(net, nk, NT.rk, NT.wrad, wt, codes, b, cb, put);
         else for_each_in_edge(net, nk, NT.rk, NT.wrad, codes, b, cb, 0, 1, put);
@@ -543,23 +508,27 @@ __global__ void __launch_bounds__(128, 6) k_net_realize(epi_net net, NetKeys nk,
         for (int i = lane; i < len; i += 32) dst[i] = srcrow[i];
       }
     } else {
-      // tile-packed messages: rows back to back + per-tile offsets
-      int incl = cnt;
+      // tile-packed messages: rows back to back, each padded with weight-0
+      // messages to whole 8-message groups; per row its first group and its
+      // pad count (toff = group | pad << 12), toff[32] = the tile's groups
+      const int ng = (cnt + 7) >> 3;
+      int incl = ng;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const int v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
         if (lane >= o) incl += v;
       }
-      const int excl = incl - cnt;
+      const int excl = incl - ng;
       uint16_t* toff = tile_off + tile * 33;
-      toff[lane] = (uint16_t)excl;
+      toff[lane] = (uint16_t)(excl | ((ng * 8 - cnt) << 12));
       if (lane == 31) toff[32] = (uint16_t)incl;
-      uint16_t* blk = msgs + tile * (int64_t)(32 * cap);
+      uint16_t* blk = msgs + tile * (int64_t)(32 * msg_cap(cap));
       for (int r = 0; r < rows; ++r) {
         const int len = __shfl_sync(0xFFFFFFFFu, cnt, r);
-        const int off = __shfl_sync(0xFFFFFFFFu, excl, r);
+        const int off = __shfl_sync(0xFFFFFFFFu, excl, r) << 3;
+        const int plen = (len + 7) & ~7;
         const uint32_t* srcrow = wbuf + r * stride_w;
-        for (int i = lane; i < len; i += 32) blk[off + i] = (uint16_t)srcrow[i];
+        for (int i = lane; i < plen; i += 32) blk[off + i] = i < len ? (uint16_t)srcrow[i] : (uint16_t)0;
       }
     }
     __syncwarp();

@@ -115,11 +115,27 @@ def test_fused_and_csr_f32_agree_and_graph_replay_is_identical():
     assert np.array_equal(b.records(), rb)
 
 
-def test_message_pass_alone_within_1e5_of_reference_hazard():
+# dense: households of 24-32 + 16 random slots -> tiles of ~2300 messages
+# (three 1024-message passes); sparse: singletons, no workplaces, few random
+# contacts -> many empty rows and empty tiles; ragged: N not a multiple of 32
+MESSAGE_PASS_SPECS = {   # name: (spec overrides, days simulated first)
+    "config1": (dict(n_agents=20_000, initial_infections=20), 25),
+    "dense": (dict(n_agents=6_000, household_sizes=(24, 32), household_probs=(0.5, 0.5),
+                   random_mean=14.0, initial_infections=20), 4),
+    "sparse": (dict(n_agents=9_001, household_sizes=(1,), household_probs=(1.0,), worker_bands=(),
+                    random_mean=0.3, initial_infections=400), 8),
+    "ragged": (dict(n_agents=1_237, initial_infections=30), 12),
+}
+
+
+@pytest.mark.parametrize("name", sorted(MESSAGE_PASS_SPECS))
+def test_message_pass_alone_within_1e5_of_reference_hazard(name):
     """North-star part (a) alone: generator -> 16-bit messages -> fp32 hazard,
     vs the reference gather (oracle, fp64) on the same generated graph."""
     from paper_2110_04421_b200 import roofline
-    sim = roofline.prepare(20_000, warm_days=25)
+    kw, days = MESSAGE_PASS_SPECS[name]
+    spec = ConfigNetworkSpec.config(1, **kw)
+    sim = roofline.prepare(spec.n_agents, warm_days=days, spec=spec)
     t = sim.clock
     lam = torch.empty(sim.n, dtype=torch.float32, device="cuda")
     roofline.gather(sim, lam)
@@ -128,6 +144,14 @@ def test_message_pass_alone_within_1e5_of_reference_hazard():
     ref = engine_np.hazard(cols, sim.disease, t, StepGraph(t, src, dst, kind), True)
     got = lam.cpu().numpy().astype(np.float64)
     nz = ref > 0
-    assert nz.sum() > 100
+    assert nz.sum() > 20
     assert np.all(np.abs(got[nz] - ref[nz]) <= 1e-5 * ref[nz])
     assert np.all(got[~nz] == 0)
+    # edge count of the pass = the restated graph's
+    rec = torch.zeros(24, dtype=torch.int64, device="cuda")
+    roofline.gather(sim, lam, rec)
+    assert int(rec[19]) == len(src)
+    # deterministic: a second pass is bitwise identical
+    again = torch.empty_like(lam)
+    roofline.gather(sim, again)
+    assert torch.equal(again, lam)
