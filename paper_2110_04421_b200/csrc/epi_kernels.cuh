@@ -14,50 +14,62 @@ constexpr uint8_t FL_SYMPTOMATIC = 1, FL_NOTIFIER = 2, FL_NOTIFIED = 4;
 constexpr uint8_t NO_BUCKET = 0xFF;
 
 // ---------------------------------------------------------------------------
-// Per-block accumulation of the EPI_REC_* record (integer atomics only, so
-// the totals are deterministic).
+// Per-block accumulation of the EPI_REC_* record.  Every warp owns a row of
+// 32-bit counters that only its own lanes update, with plain shared-memory
+// adds (no atomics, no contention between warps); rec_flush sums the rows
+// and adds the block total to the global record with integer atomics, so
+// the totals are deterministic.
+constexpr int REC_MAX_WARPS = 32;
 struct RecAcc {
-  unsigned long long v[EPI_REC_LEN];
+  unsigned v[REC_MAX_WARPS][EPI_REC_LEN];
 };
 
 __device__ __forceinline__ void rec_init(RecAcc& s) {
-  for (int i = threadIdx.x; i < EPI_REC_LEN; i += blockDim.x) s.v[i] = 0;
+  for (int i = threadIdx.x; i < REC_MAX_WARPS * EPI_REC_LEN; i += blockDim.x) (&s.v[0][0])[i] = 0u;
 }
 // warp-aggregated add of `x` (all 32 lanes must call)
 __device__ __forceinline__ void rec_add(RecAcc& s, int slot, unsigned x) {
   const unsigned t = __reduce_add_sync(0xFFFFFFFFu, x);
-  if (lane_id() == 0 && t) atomicAdd(&s.v[slot], (unsigned long long)t);
+  if (lane_id() == 0) s.v[threadIdx.x >> 5][slot] += t;
 }
 __device__ __forceinline__ void rec_or(RecAcc& s, int slot, unsigned x) {
   const unsigned t = __reduce_or_sync(0xFFFFFFFFu, x);
-  if (lane_id() == 0 && t) atomicOr(&s.v[slot], (unsigned long long)t);
+  if (lane_id() == 0) s.v[threadIdx.x >> 5][slot] |= t;
 }
+// all threads of the block must call
 __device__ __forceinline__ void rec_flush(const RecAcc& s, long long* rec, int step = -1) {
+  __syncthreads();
   if (step >= 0 && blockIdx.x == 0 && threadIdx.x == 0) rec[EPI_REC_STEP] = step;
+  const int nw = (blockDim.x + 31) >> 5;
   for (int i = threadIdx.x; i < EPI_REC_LEN; i += blockDim.x) {
+    unsigned long long t = 0;
     if (i == EPI_REC_FLAGS) {
-      if (s.v[i]) atomicOr((unsigned long long*)&rec[i], s.v[i]);
-    } else if (s.v[i]) {
-      atomicAdd((unsigned long long*)&rec[i], s.v[i]);
+      for (int w = 0; w < nw; ++w) t |= s.v[w][i];
+      if (t) atomicOr((unsigned long long*)&rec[i], t);
+    } else {
+      for (int w = 0; w < nw; ++w) t += s.v[w][i];
+      if (t) atomicAdd((unsigned long long*)&rec[i], t);
     }
   }
 }
 
 // Stage histogram + derived time-series columns (runner.py:101-116) and the
-// structural invariants of state.py:90-102, for one agent per lane.
+// structural invariants of state.py:90-102, for one agent per lane.  The
+// histogram is one match per warp: the lowest lane of each stage group adds
+// the group's size (distinct groups, distinct counters).
 __device__ __forceinline__ void rec_agent(RecAcc& s, bool valid, int stage, int32_t infected_at) {
-#pragma unroll
-  for (int k = 0; k < 11; ++k) {
-    const unsigned b = __ballot_sync(0xFFFFFFFFu, valid && stage == k);
-    if (lane_id() == 0 && b) atomicAdd(&s.v[EPI_REC_STAGE0 + k], (unsigned long long)__popc(b));
-  }
+  const bool in_range = stage >= 0 && stage <= 10;
+  const unsigned grp = __match_any_sync(0xFFFFFFFFu, valid && in_range ? stage : -1);
+  if (valid && in_range && lane_id() == __ffs(grp) - 1)
+    s.v[threadIdx.x >> 5][EPI_REC_STAGE0 + stage] += __popc(grp);
   rec_add(s, EPI_REC_CUM_INF, valid && infected_at != NEVER);
   rec_add(s, EPI_REC_CUM_DEATHS, valid && stage == S_DEAD);
   rec_add(s, EPI_REC_IN_CARE, valid && (stage == S_HOSP || stage == S_ICU));
   unsigned fl = 0;
-  if (valid && (stage < 0 || stage > 10)) fl |= EPI_FLAG_STAGE_RANGE;
+  if (valid && !in_range) fl |= EPI_FLAG_STAGE_RANGE;
   if (valid && stage != S_SUS && stage != S_VAC && infected_at == NEVER) fl |= EPI_FLAG_NO_TIMESTAMP;
   rec_or(s, EPI_REC_FLAGS, fl);
+  __syncwarp();
 }
 
 // ---------------------------------------------------------------------------
@@ -156,8 +168,9 @@ __device__ __forceinline__ unsigned transmit_progress(const StepArgs& A, int64_t
   int32_t nta = st.next_transition_at[a];
   int age = -1;
   if (stage == S_SUS && !(P->sterilizing && st.immune[a])) {
+    // lam == 0 gives p == 0 and u < p never holds: skip the draw
     const double p = 1.0 - exp(-lam);
-    if (draw(A.K, A.inj, P_INFECTION, a) < p) {
+    if (lam > 0.0 && draw(A.K, A.inj, P_INFECTION, a) < p) {
       age = st.age_band[a];
       int entry = P->targets[S_SUS][pick_branch(P, S_SUS, age, draw(A.K, A.inj, P_ENTRY, a))];
       if (!P->sterilizing && st.immune[a]) entry = S_ASYM;
