@@ -224,6 +224,16 @@ int epi_net_realize(const epi_net *net, uint64_t graph_seed, int32_t step,
                     const uint16_t *codes, uint32_t *entries, int32_t *row_len,
                     int32_t sort_rows, void *stream);
 
+/* L2 residency for the day's random gathers (no reference counterpart:
+ * device tuning).  `base`/`bytes` = the source-code buffers of a simulation;
+ * the step kernels launch with a persisting L2 access-policy window over it
+ * (hit ratio = persisting carve-out / window).  bytes = 0 clears it. */
+int epi_set_hot_window(epi_ctx *ctx, const void *base, int64_t bytes);
+
+/* Whole-population runs build the random-slot push tables (96 B/agent) only
+ * up to `max_agents` agents (-1 = while they fit in L2). */
+int epi_set_push_max(epi_ctx *ctx, int64_t max_agents);
+
 /* Bind a config network to the context and allocate its per-step padded CSR
  * (a ring of den_lookback slots when exposure notification is enabled). */
 int epi_net_attach(epi_ctx *ctx, const epi_net *net);

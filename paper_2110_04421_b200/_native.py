@@ -78,6 +78,8 @@ _SIGS = {
     "epi_destroy": (_i32, [_p]),
     "epi_set_params": (_i32, [_p, C.POINTER(EpiParams)]),
     "epi_set_rows": (_i32, [_p, _i64, _i64]),
+    "epi_set_hot_window": (_i32, [_p, _p, _i64]),
+    "epi_set_push_max": (_i32, [_p, _i64]),
     "epi_last_error": (C.c_char_p, []),
     "epi_version": (_i32, []),
     "epi_struct_size": (_i64, [_i32]),

@@ -61,21 +61,45 @@ inline int grid_for(int64_t n, int threads, int per_sm = 8) {
   return (int)(g < 1 ? 1 : g);
 }
 
-// Launch with programmatic stream serialization (see pdl_wait/pdl_trigger).
+// L2 residency window for the random gathers of a day (the source-code
+// buffers): lines inside it are persisting, so the streamed tables and
+// messages of a 10M-agent day cannot evict them (epi_set_hot_window).
+struct HotWindow {
+  const void* base = nullptr;
+  size_t bytes = 0;
+  float hit_ratio = 0.f;
+};
+
+// Launch with programmatic stream serialization (see pdl_wait/pdl_trigger)
+// and, if given, the L2 access-policy window (kept by graph capture).
 template <typename... KArgs, typename... Args>
-cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
-                       Args... args) {
+cudaError_t launch_pdl_w(const HotWindow* w, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                         cudaStream_t s, Args... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
   cfg.numAttrs = 1;
+  if (w != nullptr && w->bytes > 0) {
+    attr[1].id = cudaLaunchAttributeAccessPolicyWindow;
+    attr[1].val.accessPolicyWindow.base_ptr = const_cast<void*>(w->base);
+    attr[1].val.accessPolicyWindow.num_bytes = w->bytes;
+    attr[1].val.accessPolicyWindow.hitRatio = w->hit_ratio;
+    attr[1].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr[1].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    cfg.numAttrs = 2;
+  }
+  cfg.attrs = attr;
   return cudaLaunchKernelEx(&cfg, kernel, ((KArgs)args)...);
+}
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args... args) {
+  return launch_pdl_w(nullptr, kernel, grid, block, smem, s, args...);
 }
 
 template <class T>
@@ -90,6 +114,8 @@ int dalloc(T** p, size_t count) {
 }  // namespace
 
 struct epi_ctx {
+  HotWindow hot;                     // L2-persisting window (source codes)
+  int push_max = -1;                 // push tables up to this many agents (-1: by L2 size)
   epi_params host{};
   epi_params* P = nullptr;           // device copy
   int64_t n = 0;
@@ -227,6 +253,17 @@ int run_interventions(epi_ctx* c, const StepArgs& A, uint16_t* codes_next, const
 }
 
 }  // namespace
+
+// Push tables (rin/rout: 96 B per agent, scattered to by random rows) pay
+// off while they stay in L2; beyond that the scatter goes to DRAM as
+// partial-sector writes and evaluating the bijections is cheaper.
+static bool push_fits(const epi_ctx* c) {
+  if (c->push_max >= 0) return c->n <= c->push_max;
+  int dev = 0, l2 = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+  return (double)c->n * 96.0 <= (double)l2;
+}
 
 // k_msg_pass: per-warp segment scratch
 static int msg_pass_smem(int) { return MP_SMEM; }
@@ -540,6 +577,8 @@ static int prepare_realize(const epi_net* net) {
     CK(cudaFuncSetAttribute(k_net_realize<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     CK(cudaFuncSetAttribute(k_net_realize<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     CK(cudaFuncSetAttribute(k_net_realize<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(cudaFuncSetAttribute(k_net_realize<false, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)smem));
     CK(cudaFuncSetAttribute(k_net_realize<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int psmem = msg_pass_smem(net->row_cap);
     CK(cudaFuncSetAttribute(k_msg_pass<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, psmem));
@@ -553,7 +592,8 @@ static int launch_realize(const epi_net* net, uint64_t g, int32_t step, const ui
                           uint32_t* entries, uint16_t* msgs, uint16_t* toff, int32_t* row_len, int sort_rows,
                           long long* rec,
                           const WorkTables* wt, int64_t lo, int64_t hi, cudaStream_t s,
-                          const NetTables* ntab_dev = nullptr) {
+                          const NetTables* ntab_dev = nullptr, bool push = false,
+                          const HotWindow* hot = nullptr) {
   const size_t smem = realize_smem(net);
   if (smem > g_realize_smem_set) return fail(EPI_EARG, "realize smem not prepared");
   NetKeys nk = make_net_keys(g, step);
@@ -568,9 +608,11 @@ static int launch_realize(const epi_net* net, uint64_t g, int32_t step, const ui
   }
   const int grid = grid_for(hi - lo, 128, 16);
   const bool batch = batched(net);
-  auto kern = sort_rows ? (batch ? k_net_realize<true, true> : k_net_realize<true, false>)
-                        : (batch ? k_net_realize<false, true> : k_net_realize<false, false>);
-  CK(launch_pdl(kern, dim3(grid), dim3(128), smem, s, *net, nk, codes, entries, msgs, toff, row_len, rec,
+  // push: messages from the day's push tables (wt must hold rin/rout)
+  auto kern = push ? k_net_realize<false, true, true>
+              : sort_rows ? (batch ? k_net_realize<true, true> : k_net_realize<true, false>)
+                          : (batch ? k_net_realize<false, true> : k_net_realize<false, false>);
+  CK(launch_pdl_w(hot, kern, dim3(grid), dim3(128), smem, s, *net, nk, codes, entries, msgs, toff, row_len, rec,
                 wt, lo, hi, ntab_dev));
   CKL();
   return 0;
@@ -586,6 +628,32 @@ int epi_net_realize(const epi_net* net, uint64_t graph_seed, int32_t step, const
   return launch_realize(net, graph_seed, step, codes, entries, nullptr, nullptr, row_len, sort_rows, nullptr,
                         nullptr,
                         0, net->n_agents, S(stream));
+}
+
+int epi_set_hot_window(epi_ctx* c, const void* base, int64_t bytes) {
+  if (!c || bytes < 0 || (bytes > 0 && !base)) return fail(EPI_EARG, "bad hot window");
+  c->hot = HotWindow{};
+  if (bytes == 0) return 0;
+  int dev = 0, maxp = 0, maxw = 0;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, dev));
+  CK(cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, dev));
+  if (maxp <= 0 || maxw <= 0) return 0;               // no persisting L2: plain caching
+  const size_t win = (size_t)bytes < (size_t)maxw ? (size_t)bytes : (size_t)maxw;
+  size_t cur = 0;
+  CK(cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize));
+  const size_t want = win < (size_t)maxp ? win : (size_t)maxp;
+  if (cur < want) CK(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want));
+  c->hot.base = base;
+  c->hot.bytes = win;
+  c->hot.hit_ratio = (float)((double)want / (double)win);
+  return 0;
+}
+
+int epi_set_push_max(epi_ctx* c, int64_t max_agents) {
+  if (!c) return fail(EPI_EARG, "null ctx");
+  c->push_max = max_agents < 0 ? -1 : (int)(max_agents > 0x7FFFFFFF ? 0x7FFFFFFF : max_agents);
+  return 0;
 }
 
 int epi_net_attach(epi_ctx* c, const epi_net* net) {
@@ -685,11 +753,14 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
   // without interventions are "merged": today's kernel builds tomorrow's
   // tables in its epilogue, so after the first day there is one kernel per day.
   const bool has_work = c->net.n_member_slots > 0 && c->net.colleague_draws > 0;
-  const bool push_rand = mode == 1 && c->lo == 0 && c->hi == c->n && c->net.n_agents >= 2 &&
-                         c->net.random_slots == RT_SLOTS && batched(&c->net);
-  const bool merged = push_rand && !iv;
-  const bool use_wt = (mode == 0 && has_work && batched(&c->net)) || mode == 1;
-  const int variant = mode == 0 ? 0 : (push_rand ? 2 : 1);
+  // csr mode writes messages only in fp32 without a contact log
+  const bool msg_only = mode == 0 && precision == EPI_F32 && !c->host.den_enabled &&
+                        c->net.row_cap <= MP_MAX_CAP;
+  const bool push_rand = (mode == 1 || msg_only) && c->lo == 0 && c->hi == c->n && c->net.n_agents >= 2 &&
+                         c->net.random_slots == RT_SLOTS && batched(&c->net) && push_fits(c);
+  const bool merged = mode == 1 && push_rand && !iv;
+  const bool use_wt = (mode == 0 && (push_rand || (has_work && batched(&c->net)))) || mode == 1;
+  const int variant = push_rand ? 2 : (mode == 0 ? 0 : 1);
   long long* rec_zero = zero_record ? rec : nullptr;
   if (merged && c->merged_ready == step) {
     if (rec_zero) CK(cudaMemsetAsync(rec, 0, EPI_REC_LEN * sizeof(long long), s));
@@ -706,7 +777,7 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
       WorkTables w = c->wt_host[par];
       if (variant == 0) w.wcode = nullptr;
       if (variant < 2) { w.rin = nullptr; w.rout = nullptr; }
-      CK(launch_pdl(k_day_tables, dim3(wblocks + rblocks > 0 ? wblocks + rblocks : 1), dim3(256), 0, s,
+      CK(launch_pdl_w(&c->hot, k_day_tables, dim3(wblocks + rblocks > 0 ? wblocks + rblocks : 1), dim3(256), 0, s,
                     c->net, nk, w, codes_cur, c->lo, c->hi, wblocks, (const NetTables*)nt_today, nt_next,
                     key_prefix(seed, step + 1, P_NET_RPERM), rec_zero));
     } else {
@@ -718,12 +789,12 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
   if (mode == 0) {
     // fp32 without contact log: the generator writes pre-joined messages and
     // the message pass streams them; otherwise ids (export, DEN, fp64 order)
-    const bool msg_only = precision == EPI_F32 && !c->host.den_enabled && c->net.row_cap <= MP_MAX_CAP;
     uint32_t* entries = msg_only ? nullptr : c->net_entries[slot];
     uint16_t* msgs = msg_only ? c->net_msgs : nullptr;
     int32_t* row_len = c->net_rowlen[slot];
     int rc = launch_realize(&c->net, seed, step, codes_cur, entries, msgs, c->net_toff, row_len,
-                            precision == EPI_F64_CANONICAL, nullptr, wt, c->lo, c->hi, s, nt_today);
+                            precision == EPI_F64_CANONICAL, nullptr, wt, c->lo, c->hi, s, nt_today,
+                            msg_only && push_rand, &c->hot);
     if (rc) return rc;
     c->net_slot_step[slot] = msg_only ? -1 : step;
     c->merged_ready = -1;
@@ -733,7 +804,7 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
       k_pass<true, 1><<<grid, 256, 0, s>>>(A, g, codes_cur, nullptr, c->host.rate_scale, iv ? 0 : 1,
                                            codes_next, c->net_dev, rcount_next, c->msg_dev);
     else if (msgs)
-      CK(launch_pdl(k_msg_pass<1>, dim3(msg_pass_grid<1>(c->net.row_cap, c->hi - c->lo)),
+      CK(launch_pdl_w(&c->hot, k_msg_pass<1>, dim3(msg_pass_grid<1>(c->net.row_cap, c->hi - c->lo)),
                     dim3(MP_WARPS * 32), (size_t)msg_pass_smem(c->net.row_cap), s, A, g, (float*)nullptr,
                     iv ? 0 : 1, codes_next, (const epi_net*)c->net_dev, rcount_next,
                     (const MsgTables*)c->msg_dev, (const MsgComb*)c->comb_dev));
@@ -753,7 +824,7 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
       nx.rperm_t2 = key_prefix(seed, step + 2, P_NET_RPERM);
       nx.nk = make_net_keys(seed, step + 1);
     }
-    CK(launch_pdl(k_fused_step, dim3(fgrid), dim3(128), 0, s, A, c->net, nk, codes_cur,
+    CK(launch_pdl_w(&c->hot, k_fused_step, dim3(fgrid), dim3(128), 0, s, A, c->net, nk, codes_cur,
                   c->host.rate_scale, codes_next, (const epi_net*)c->net_dev, rcount_next, iv ? 0 : 1, wt,
                   (const MsgTables*)c->msg_dev, (const NetTables*)nt_today, nx));
     c->merged_ready = merged ? step + 1 : -1;

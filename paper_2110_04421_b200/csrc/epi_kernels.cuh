@@ -457,8 +457,12 @@ __device__ __forceinline__ void clear_rin_row(const WorkTables* wt, int64_t b) {
 // Config CSR generation (mode 0): one lane per destination row; each row is
 // staged in shared memory (odd stride: conflict-free), optionally sorted into
 // canonical (src, kind) order, and the warp's 32 rows are written out
-// coalesced, one warp-wide store per row.
-template <bool SORT, bool BATCH>
+// coalesced: id rows one warp-wide store per row, message tiles as 16-byte
+// groups (one 8-message group per lane and store).  With PUSH (message-only
+// runs over the whole population) the random in-edges come from the day's
+// push tables (rin/rout, built by k_day_tables) instead of the random-slot
+// bijections, and the rin rows consumed are cleared.
+template <bool SORT, bool BATCH, bool PUSH = false>
 __global__ void __launch_bounds__(128, 6) k_net_realize(epi_net net, NetKeys nk, const uint16_t* __restrict__ codes,
                                                      uint32_t* __restrict__ entries,
                                                      uint16_t* __restrict__ msgs,
@@ -469,6 +473,7 @@ __global__ void __launch_bounds__(128, 6) k_net_realize(epi_net net, NetKeys nk,
   extern __shared__ uint32_t stage_buf[];
   __shared__ NetTables NT;
   __shared__ RecAcc racc;
+  __shared__ int goff_s[4][33], len_s[4][32];   // message tiles: group offsets, row lengths
   load_net_tables(NT, NTp);
   rec_init(racc);
   __syncthreads();
@@ -497,9 +502,13 @@ __global__ void __launch_bounds__(128, 6) k_net_realize(epi_net net, NetKeys nk,
           mine[cnt++] = entries ? (((uint32_t)c << 2) | (uint32_t)kind)
                                 : (((uint32_t)(cc & 0xFF) << 4) | ((uint32_t)kind << 2));
         };
-        if (BATCH) for_each_in_edge_batched<16, 8>(net, nk, NT.rk, NT.wrad, wt, codes, b, cb, put);
+        if (PUSH)
+          for_each_in_code(net, nk, NT.rk, NT.wrad, NT.dn, wt, codes, b, cb,
+                           [&](int kind, uint16_t cc) { put(0, kind, cc); });
+        else if (BATCH) for_each_in_edge_batched<16, 8>(net, nk, NT.rk, NT.wrad, wt, codes, b, cb, put);
         else for_each_in_edge(net, nk, NT.rk, NT.wrad, codes, b, cb, 0, 1, put);
       }
+      if (PUSH) clear_rin_row(wt, b);
       if (SORT) {
         for (int i = 1; i < cnt; ++i) {
           const uint32_t x = mine[i];
@@ -535,13 +544,30 @@ __global__ void __launch_bounds__(128, 6) k_net_realize(epi_net net, NetKeys nk,
       uint16_t* toff = tile_off + tile * 33;
       toff[lane] = (uint16_t)(excl | ((ng * 8 - cnt) << 12));
       if (lane == 31) toff[32] = (uint16_t)incl;
-      uint16_t* blk = msgs + tile * (int64_t)(32 * msg_cap(cap));
-      for (int r = 0; r < rows; ++r) {
-        const int len = __shfl_sync(0xFFFFFFFFu, cnt, r);
-        const int off = __shfl_sync(0xFFFFFFFFu, excl, r) << 3;
-        const int plen = (len + 7) & ~7;
-        const uint32_t* srcrow = wbuf + r * stride_w;
-        for (int i = lane; i < plen; i += 32) blk[off + i] = i < len ? (uint16_t)srcrow[i] : (uint16_t)0;
+      goff_s[warp][lane] = excl;
+      len_s[warp][lane] = cnt;
+      if (lane == 31) goff_s[warp][32] = incl;
+      __syncwarp();
+      // one 16-byte group per lane: row r = the last row starting at or
+      // before the group (rows without groups share their successor's start)
+      uint4* blk = (uint4*)(msgs + tile * (int64_t)(32 * msg_cap(cap)));
+      const int groups = __shfl_sync(0xFFFFFFFFu, incl, 31);
+      for (int gi = lane; gi < groups; gi += 32) {
+        int r = 0;
+#pragma unroll
+        for (int st = 16; st >= 1; st >>= 1)
+          if (goff_s[warp][r + st] <= gi) r += st;
+        const int k = (gi - goff_s[warp][r]) << 3;
+        const int len = len_s[warp][r];
+        const uint32_t* src = wbuf + r * stride_w + k;
+        uint32_t w[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint32_t m0 = k + 2 * q < len ? src[2 * q] : 0u;
+          const uint32_t m1 = k + 2 * q + 1 < len ? src[2 * q + 1] : 0u;
+          w[q] = (m0 & 0xFFFFu) | (m1 << 16);
+        }
+        blk[gi] = make_uint4(w[0], w[1], w[2], w[3]);
       }
     }
     __syncwarp();

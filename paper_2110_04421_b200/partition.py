@@ -124,7 +124,7 @@ class PartitionedSimulation(ConfigSimulation):
 
     def _alloc_codes(self):
         import torch
-        return [torch.zeros(self._code_len, dtype=torch.int16, device=self.device) for _ in range(2)]
+        return torch.zeros((2, self._code_len), dtype=torch.int16, device=self.device)
 
     def _after_attach(self):
         lo, hi = self.plan.rows(self.rank)

@@ -79,7 +79,7 @@ def initial_columns(pop: ConfigPopulation) -> AgentColumns:
 class ConfigSimulation:
     def __init__(self, pop: ConfigPopulation, disease, table, interventions, seed: int,
                  mode: str = "csr", precision: str = "f32", horizon: int = 180,
-                 device=None, initial=None):
+                 device=None, initial=None, push_max: int | None = None):
         import torch
         if mode not in ("csr", "fused"):
             raise ConfigError(f"unknown mode {mode!r}")
@@ -102,8 +102,14 @@ class ConfigSimulation:
         self._ctx = ctx
         N.check(self._lib.epi_net_attach(self._ctx, ctypes.byref(self.net.struct)))
         self._after_attach()
+        if push_max is not None:
+            N.check(self._lib.epi_set_push_max(self._ctx, int(push_max)))
         self.state = DeviceColumns(self.n, self.device)
-        self.codes = self._alloc_codes()
+        self._codes_buf = self._alloc_codes()
+        self.codes = [self._codes_buf[0], self._codes_buf[1]]
+        # the random code gathers of every day stay L2-resident
+        N.check(self._lib.epi_set_hot_window(self._ctx, N.ptr(self._codes_buf),
+                                             self._codes_buf.numel() * 2))
         self.rec = torch.zeros((horizon, N.REC_LEN), dtype=torch.int64, device=self.device)
         self.vax = torch.zeros(1, dtype=torch.int32, device=self.device)
         self.initial = initial if initial is not None else self._seeded_initial()
@@ -111,8 +117,9 @@ class ConfigSimulation:
         self._graph = None
 
     def _alloc_codes(self):
+        """Both day parities in one buffer (one L2 window covers them)."""
         import torch
-        return [torch.zeros(self.n, dtype=torch.int16, device=self.device) for _ in range(2)]
+        return torch.zeros((2, self.n), dtype=torch.int16, device=self.device)
 
     def _after_attach(self):
         pass

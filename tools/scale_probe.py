@@ -1,6 +1,9 @@
-"""Per-day device time vs population size (fused and csr modes)."""
+"""Per-day device time vs population size (fused and csr modes).
+PUSH_MAX=<agents> overrides the push-table cut-off (epi_set_push_max);
+HOT_WINDOW=0 drops the L2-persisting window over the codes."""
 import ctypes
 import json
+import os
 import sys
 from pathlib import Path
 
@@ -20,7 +23,11 @@ def main():
         for mode in ("fused", "csr"):
             days = 40
             spec = ConfigNetworkSpec.config(1, n_agents=n, initial_infections=max(10, n // 100))
-            sim = ConfigSimulation.create(spec, seed=3, mode=mode, horizon=days)
+            pm = os.environ.get("PUSH_MAX")
+            sim = ConfigSimulation.create(spec, seed=3, mode=mode, horizon=days,
+                                          push_max=int(pm) if pm is not None else None)
+            if os.environ.get("HOT_WINDOW") == "0":
+                N.check(sim._lib.epi_set_hot_window(sim._ctx, None, 0))
             evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(days)]
             for d in evs:
                 for e in d:
@@ -38,7 +45,7 @@ def main():
             gen = np.mean([evs[t][0].elapsed_time(evs[t][1]) for t in range(5, days)])
             pas = np.mean([evs[t][1].elapsed_time(evs[t][2]) for t in range(5, days)])
             E = float(sim.records()[5:, 19].mean())
-            r = dict(n=n, mode=mode, gen_us=1e3 * gen, main_us=1e3 * pas, edges=E,
+            r = dict(n=n, mode=mode, push_max=pm, gen_us=1e3 * gen, main_us=1e3 * pas, edges=E,
                      edges_per_us=E / (1e3 * (gen + pas)))
             print(json.dumps(r), flush=True)
             out.append(r)
