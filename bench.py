@@ -42,7 +42,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--mode", choices=["csr", "fused", "auto"], default="auto")
-    ap.add_argument("--workload", choices=["config1", "config0", "config3", "config4"],
+    ap.add_argument("--workload", choices=["config1", "config0", "config3", "config4", "refnet"],
                     default="config1")
     ap.add_argument("--replicas", type=int, default=128, help="config4: replicas per GPU")
     ap.add_argument("--streams", type=int, default=8, help="config4: concurrent streams")
@@ -100,6 +100,46 @@ def _cpu_worker(args):
     return edges, days, time.perf_counter() - t0
 
 
+def _cpu_worker_refnet(args):
+    """The reference's own scenario (`epivec bench`) restated on the host: the
+    population mirror, the oracle engine (engine_np) and the oracle restatement
+    of the reference realizer (graphs_np), one replica, bounded steps."""
+    _, seed, seconds = args
+    sys.path.insert(0, str(ROOT))
+    from oracle import engine_np, graphs_np, rng_np
+    from paper_2110_04421_b200.defaults import default_disease, default_progression
+    from paper_2110_04421_b200.graph import StepGraph
+    from paper_2110_04421_b200.interventions import InterventionConfig
+    from paper_2110_04421_b200.keyed import replication_seed
+    from paper_2110_04421_b200.population import PopulationSpec, choose_seeds, synthesize
+    spec = PopulationSpec.default(REFNET_AGENTS)
+    rseed = replication_seed(seed, 0)
+    cols = synthesize(spec, rseed)
+    table = default_progression()
+    ids = choose_seeds(cols, REFNET_SEEDS, rseed)
+    entry = engine_np.pick(table.rules[0], cols.age_band[ids], rng_np.uniforms(rseed, 0, 3, ids))
+    cols.stage[ids] = entry
+    cols.infected_at[ids] = 0
+    nxt, d = engine_np.schedule(table, entry, cols.age_band[ids], rng_np.uniforms(rseed, 0, 4, ids),
+                                rng_np.uniforms(rseed, 0, 5, ids))
+    cols.next_stage[ids] = nxt
+    cols.next_transition_at[ids] = d
+    realizer = graphs_np.ReferenceRealizer(rseed, cols.household_id, cols.occupation, cols.random_degree,
+                                           spec.occupation_mean_interactions, spec.rewire_beta)
+    eng = engine_np.OracleEngine(cols, default_disease(), table, InterventionConfig(), rseed)
+    t0 = time.perf_counter()
+    edges = days = 0
+    while days < HORIZON and (time.perf_counter() - t0) < seconds:
+        src, dst, kind = realizer.realize(days, cols.stage == 10)
+        ev = eng.step(StepGraph(days, src, dst, kind))
+        edges += ev.n_edges
+        days += 1
+    return edges, days, time.perf_counter() - t0
+
+
+REFNET_AGENTS, REFNET_SEEDS = 100_000, 10   # epivec bench --agents 100000 (scenario.py:53)
+
+
 def run_reference(a):
     rank, _, world = dist_env()
     if rank != 0:
@@ -113,8 +153,9 @@ def run_reference(a):
     for i in range(a.warmup + a.steps):
         t0 = time.perf_counter()
         with ProcessPoolExecutor(max_workers=cores) as pool:
-            res = list(pool.map(_cpu_worker, [(a.workload, 1000 * i + w, a.cpu_seconds / 2)
-                                              for w in range(cores)]))
+            worker = _cpu_worker_refnet if a.workload == "refnet" else _cpu_worker
+            res = list(pool.map(worker, [(a.workload, 1000 * i + w, a.cpu_seconds / 2)
+                                         for w in range(cores)]))
         wall = time.perf_counter() - t0
         if i >= a.warmup:
             e = sum(r[0] for r in res)
@@ -130,7 +171,8 @@ def run_reference(a):
         "unit": "agent-interactions/s", "n_gpus": a.gpus, "steps": len(steps), "warmup": a.warmup,
         "ms_per_step": 1000 * w / max(1, len(steps)), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{a.workload}: BASELINE.json configs[1], 100k agents, "
+        "config": {"workload": REFNET_DESC if a.workload == "refnet" else
+                   f"{a.workload}: BASELINE.json configs[1], 100k agents, "
                    "household+workplace+Poisson(5) random network, 100 seeds, no interventions",
                    "parallelism": f"{cores} host processes x 1 replica each"},
         "cpu_baseline": {"value": v, "unit": "agent-interactions/s", "cores": cores, "kind": "port",
@@ -577,6 +619,88 @@ def run_config4(a):
             "clocks": clocks}), flush=True)
 
 
+REFNET_DESC = ("refnet: the reference's own benchmark scenario (epivec bench --agents 100000 --steps "
+               "180): default population_spec.json population (mirror of population.synthesize), "
+               "households + per-occupation Watts-Strogatz (beta 0.1) + stub-pairing random network "
+               "realized every step, 10 seeds, default disease/progression, fp64 canonical hazard")
+
+
+def run_refnet(a):
+    """The reference's own benchmark on the device: ReferenceNativeSimulation
+    (population mirror, device realizer, GpuEngine resident).  One step = one
+    180-step replication; interactions = directed edges gathered."""
+    import torch
+    from paper_2110_04421_b200.refsim import ReferenceNativeSimulation
+    rank, local_rank, world = dist_env()
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+
+    def make(i):
+        return ReferenceNativeSimulation(REFNET_AGENTS, base_seed=1000 * rank + i,
+                                         initial_infections=REFNET_SEEDS, horizon=HORIZON)
+    for i in range(a.warmup):
+        make(i).run()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clk = ClockSampler(local_rank)
+    total_ms = 0.0
+    edges = 0
+    e2e_ms = 0.0
+    h2d = 0
+    for i in range(a.steps):
+        # e2e: host population -> device (engine + realizer tables), seeding,
+        # 180 steps (per-step events read back), final state -> host
+        t0 = time.perf_counter()
+        sim = make(a.warmup + i)
+        st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        st.record()
+        sim.run()
+        en.record()
+        sim.engine.sync_to_host()
+        torch.cuda.synchronize()
+        t_all = time.perf_counter() - t0
+        total_ms += st.elapsed_time(en)
+        edges += sim.interactions
+        e2e_ms += 1e3 * (t_all - sim.host_setup_s)       # minus the host-only population draw
+        h2d = sum(t.numel() * t.element_size() for t in sim.engine.dev.t.values())
+    clocks = clk.stop()
+    ms = total_ms
+    if dist:
+        tt = torch.tensor([ms, edges, e2e_ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt[:1], op=dist.ReduceOp.MAX)
+        dist.all_reduce(tt[1:2])
+        dist.all_reduce(tt[2:], op=dist.ReduceOp.MAX)
+        ms, edges, e2e_ms = float(tt[0]), float(tt[1]), float(tt[2])
+    if rank != 0:
+        return
+    line = {
+        "metric": "agent-interactions/sec", "value": edges / (ms / 1e3),
+        "unit": "agent-interactions/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": REFNET_DESC, "step": "one 180-step replication (GpuRealizer + "
+                   "GpuEngine resident, host loop with per-step event readback)",
+                   "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                   "l2": "not flushed; every step regenerates the graphs (> L2 traffic per step)"},
+        "wall_s_per_sim": ms / a.steps / 1e3,
+        "e2e": {"value": edges / (e2e_ms / 1e3), "unit": "agent-interactions/s",
+                "ms_per_step": e2e_ms / a.steps, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": h2d + HORIZON * 8 * 24},
+        "clocks": clocks,
+    }
+    if not a.no_cpu_baseline and world == 1:
+        e, days, t = _cpu_worker_refnet(("refnet", 12345, a.cpu_seconds))
+        line["cpu_baseline"] = {"value": e / t, "unit": "agent-interactions/s", "cores": 1,
+                                "kind": "port", "sample": f"oracle engine_np + graphs_np reference "
+                                f"realizer, 1 replica, steps 0-{days - 1} of 180 ({e} directed "
+                                f"edges in {t:.1f}s), single process"}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     a = parse()
     if a.impl == "reference":
@@ -585,6 +709,8 @@ def main():
         run_config3(a)
     elif a.workload == "config4":
         run_config4(a)
+    elif a.workload == "refnet":
+        run_refnet(a)
     else:
         run_ours(a)
 

@@ -99,6 +99,24 @@ class GpuEngine:
             self._lib.epi_destroy(ctx)
             self._ctx = None
 
+    # -- initial state on the device (population.py:168-177, runner.py:86-89)
+    def seed_infections(self, ids) -> None:
+        """Entry stage + first transition of the chosen agents (sorted ids,
+        device int64 tensor), with the reference's keyed step-0 draws."""
+        st = self.dev.struct()
+        N.check(self._lib.epi_seed_infections(self._ctx, C_ref(st), _u64(self.seed), N.ptr(ids),
+                                              int(ids.numel()), N.stream_handle()))
+        if not self.resident:
+            self.sync_to_host()
+
+    def assign_app(self, adoption: float) -> None:
+        """has_den_app = u(seed, 0, DEN_APP, id) < adoption."""
+        st = self.dev.struct()
+        N.check(self._lib.epi_assign_app(C_ref(st), _u64(self.seed), float(adoption),
+                                         N.stream_handle()))
+        if not self.resident:
+            self.sync_to_host()
+
     # -- state movement ---------------------------------------------------
     def sync_to_device(self):
         self.dev.upload(self.cols)

@@ -1,0 +1,76 @@
+"""The reference's own scenario on the device: `epivec bench` / `run_replication`
+with the reference-native networks (runner.py:81-98,
+138-152, 268-289).
+
+    population  : host mirror of population.synthesize + the seeding choice
+                  (population.py), bitwise identical to the reference's;
+    seeding     : entry stage + first transition scheduled on the device
+                  (k_seed, the same keyed draws as population.py:168-177);
+    per step    : GpuRealizer.realize(step, dead) -> device StepGraph
+                  (households, per-occupation small world, stub pairing)
+                  -> GpuEngine.step (graph-in: canonical CSR, fp64 message
+                  pass bitwise equal to Engine.gather_exposure, phases).
+
+The agent state stays on the device (`resident`); interactions are the
+directed edges gathered, the reference's definition (runner.py:269, 287).
+"""
+
+from __future__ import annotations
+
+import time
+
+from .defaults import default_disease, default_progression
+from .engine import GpuEngine
+from .interventions import InterventionConfig
+from .keyed import replication_seed
+from .population import PopulationSpec, choose_seeds, synthesize
+from .refnet import GpuRealizer
+
+
+class ReferenceNativeSimulation:
+    """One replication of the reference's default scenario (scenario.py
+    defaults: disease, progression, population_spec.json) at `n_agents`."""
+
+    def __init__(self, n_agents: int = 100_000, base_seed: int = 0, replication: int = 0,
+                 initial_infections: int = 10, horizon: int = 180, disease=None, table=None,
+                 interventions=None, spec: PopulationSpec | None = None, device=None,
+                 seed: int | None = None):
+        import torch
+        self.spec = spec or PopulationSpec.default(n_agents)
+        # the replication seed (runner.py:77-78), or an explicit one
+        self.seed = replication_seed(base_seed, replication) if seed is None else int(seed)
+        self.horizon = horizon
+        self.iv = interventions or InterventionConfig()
+        t0 = time.perf_counter()
+        cols = synthesize(self.spec, self.seed)
+        ids = choose_seeds(cols, initial_infections, self.seed)
+        self.host_setup_s = time.perf_counter() - t0   # host-only population draw
+        self.cols = cols
+        self.engine = GpuEngine(cols, disease or default_disease(), table or default_progression(),
+                                self.iv, self.seed, check_invariants=False, resident=True,
+                                device=device)
+        self.engine.seed_infections(torch.from_numpy(ids).to(self.engine.device))
+        if self.iv.den_enabled:     # runner.py:86-89
+            self.engine.assign_app(self.iv.den.app_adoption)
+        self.realizer = GpuRealizer(self.seed, cols.household_id, cols.occupation, cols.random_degree,
+                                    self.spec.occupation_mean_interactions, self.spec.rewire_beta,
+                                    device=device)
+        self.interactions = 0
+
+    @property
+    def clock(self) -> int:
+        return self.engine.clock
+
+    def step(self):
+        """One reference step: realize the day's networks for the alive agents,
+        then Engine.step on them (runner.py:145-150)."""
+        dead = self.engine.dev.t["stage"] == 10
+        ev = self.engine.step(self.realizer.realize(self.engine.clock, dead))
+        self.interactions += ev.n_edges
+        return ev
+
+    def run(self, steps: int | None = None):
+        out = []
+        for _ in range(self.horizon - self.clock if steps is None else steps):
+            out.append(self.step())
+        return out

@@ -1,0 +1,59 @@
+"""The reference's own scenario on the device (refsim.py): population mirror
++ device seeding vs the reference's recorded initialize_run state, then the
+device step loop (device realizer + GpuEngine) vs the oracle engine on the
+restated realizer's graphs, bitwise."""
+
+import dataclasses
+
+import numpy as np
+import pytest
+
+from golden_io import Trajectory
+from oracle import engine_np, refnet_np
+from paper_2110_04421_b200.defaults import POPULATION
+from paper_2110_04421_b200.graph import StepGraph
+from paper_2110_04421_b200.state import COLUMN_SPECS
+
+pytestmark = pytest.mark.gpu
+
+MEANS = POPULATION["networks"]["occupation_mean_interactions"]
+BETA = POPULATION["networks"]["rewire_beta"]
+
+
+def _sim(tr):
+    from paper_2110_04421_b200.refsim import ReferenceNativeSimulation
+    z = tr.z
+    infected = int(np.sum(z["init_infected_at"] == 0))
+    return ReferenceNativeSimulation(len(z["init_age_band"]), seed=tr.seed, initial_infections=infected,
+                                     horizon=int(z["horizon"]), disease=tr.disease, table=tr.table,
+                                     interventions=tr.iv)
+
+
+@pytest.mark.parametrize("name", ["noiv", "alliv", "nonster"])
+def test_initial_state_equals_reference_initialize_run(name):
+    tr = Trajectory(name)
+    sim = _sim(tr)
+    sim.engine.sync_to_host()
+    for c, _, _ in COLUMN_SPECS:
+        assert np.array_equal(getattr(sim.cols, c), tr.z[f"init_{c}"]), c
+
+
+@pytest.mark.parametrize("name", ["noiv", "alliv"])
+def test_device_loop_bitwise_vs_oracle(name):
+    tr = Trajectory(name)
+    sim = _sim(tr)
+    sim.engine.vaccination_open = bool(tr.z["vaccination_open"])
+    cols_o = tr.initial_cols()
+    eo = engine_np.OracleEngine(cols_o, tr.disease, tr.table, tr.iv, tr.seed)
+    eo.vaccination_open = bool(tr.z["vaccination_open"])
+    hh, occ, deg = sim.cols.household_id, sim.cols.occupation, sim.cols.random_degree
+    for t in range(25):
+        s, d, k = refnet_np.realize(tr.seed, t, hh, occ, deg, MEANS, BETA, cols_o.stage == 10)
+        ev_o = eo.step(StepGraph(t, s, d, k))
+        ev_g = sim.step()
+        assert dataclasses.astuple(ev_g) == dataclasses.astuple(ev_o), t
+    sim.engine.sync_to_host()
+    for c in ("stage", "infected_at", "next_stage", "next_transition_at", "quarantine_until",
+              "vaccine_status", "immune"):
+        assert np.array_equal(getattr(sim.cols, c), getattr(cols_o, c)), c
+    assert sim.interactions > 0
