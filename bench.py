@@ -477,7 +477,7 @@ def run_config3(a):
     """10M agents, agent-range partition over the ranks (NCCL code all-gather)."""
     import torch
     from paper_2110_04421_b200 import _native as N
-    from paper_2110_04421_b200.confignet import synthesize
+    from paper_2110_04421_b200.confignet import DevicePopulation
     from paper_2110_04421_b200.defaults import default_disease, default_progression
     from paper_2110_04421_b200.interventions import InterventionConfig
     from paper_2110_04421_b200.keyed import replication_seed
@@ -491,7 +491,7 @@ def run_config3(a):
         import torch.distributed as dist
         dist.init_process_group("nccl")
     spec = workload_spec("config3")
-    pop = synthesize(spec, 0)
+    pop = DevicePopulation(spec, 0)        # row f3: built on the device
     d, t, iv = default_disease(), default_progression(), InterventionConfig()
     seed = replication_seed(0, 0)
     if world > 1:
@@ -544,7 +544,7 @@ def run_config4(a):
     import torch
     from paper_2110_04421_b200 import _native as N
     from paper_2110_04421_b200 import keyed
-    from paper_2110_04421_b200.confignet import synthesize
+    from paper_2110_04421_b200.confignet import DevicePopulation
     from paper_2110_04421_b200.defaults import default_disease, default_progression
     from paper_2110_04421_b200.interventions import InterventionConfig
     from paper_2110_04421_b200.sim import ConfigSimulation
@@ -555,7 +555,7 @@ def run_config4(a):
         import torch.distributed as dist
         dist.init_process_group("nccl")
     spec = workload_spec("config4")
-    pop = synthesize(spec, 0)
+    pop = DevicePopulation(spec, 0)        # row f3: built on the device, shared by the replicas
     d0, t, iv = default_disease(), default_progression(), InterventionConfig()
     sims = []
     for i in range(a.replicas):

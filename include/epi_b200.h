@@ -157,6 +157,37 @@ typedef struct epi_net {
     double poisson_cdf[EPI_MAX_SLOTS];
 } epi_net;
 
+/* Config-population synthesis on the device (row f3; host restatement:
+ * paper_2110_04421_b200/confignet.py::synthesize).  Cumulative tables are
+ * computed by the caller in fp64 (np.cumsum) so both sides compare against
+ * the same doubles. */
+typedef struct epi_pop_spec {
+    int64_t n_agents;
+    double age_cum[9];
+    int32_t n_sizes;              /* household size classes (<= 32)       */
+    int32_t hh_sizes[32];
+    double hh_cum[32];
+    uint32_t worker_mask;         /* bit b: age band b works (0: no workplaces) */
+    int32_t wp_min, wp_max;
+    int64_t n_seeds;
+} epi_pop_spec;
+
+/* Caller-owned device outputs.  wp_members/wp_base/wp_size hold the first
+ * counts[1] / counts[0] entries; capacities: N, N / wp_min + 2. */
+typedef struct epi_pop_out {
+    int8_t *age_band;
+    int32_t *household_id;
+    uint8_t *hh_off, *hh_size;
+    int32_t *wp_id;
+    uint8_t *wp_local;
+    int32_t *wp_members;
+    int32_t *wp_base, *wp_size;
+    int64_t *seeds;               /* [n_seeds], ascending ids             */
+    int64_t *counts;              /* device [2]: workplaces, members      */
+} epi_pop_out;
+
+int epi_pop_synthesize(const epi_pop_spec *spec, uint64_t seed, const epi_pop_out *out, void *stream);
+
 typedef struct epi_ctx epi_ctx;
 
 /* Context: parameters + scratch for `n_agents` agents. */

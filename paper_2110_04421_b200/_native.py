@@ -65,6 +65,17 @@ class EpiNet(C.Structure):
     ]
 
 
+class EpiPopSpec(C.Structure):
+    _fields_ = [("n_agents", _i64), ("age_cum", _d * 9), ("n_sizes", _i32), ("hh_sizes", _i32 * 32),
+                ("hh_cum", _d * 32), ("worker_mask", C.c_uint32), ("wp_min", _i32), ("wp_max", _i32),
+                ("n_seeds", _i64)]
+
+
+class EpiPopOut(C.Structure):
+    _fields_ = [(f, _p) for f in ("age_band", "household_id", "hh_off", "hh_size", "wp_id", "wp_local",
+                                  "wp_members", "wp_base", "wp_size", "seeds", "counts")]
+
+
 class EpiRefnetDesc(C.Structure):
     _fields_ = [
         ("n_agents", _i64), ("hh_members", _p), ("hh_start", _p), ("hh_size", _p),
@@ -79,6 +90,7 @@ _SIGS = {
     "epi_set_params": (_i32, [_p, C.POINTER(EpiParams)]),
     "epi_set_rows": (_i32, [_p, _i64, _i64]),
     "epi_set_hot_window": (_i32, [_p, _p, _i64]),
+    "epi_pop_synthesize": (_i32, [C.POINTER(EpiPopSpec), _u64, C.POINTER(EpiPopOut), _p]),
     "epi_set_push_max": (_i32, [_p, _i64]),
     "epi_last_error": (C.c_char_p, []),
     "epi_version": (_i32, []),

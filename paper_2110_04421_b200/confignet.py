@@ -227,3 +227,68 @@ def synthesize(spec: ConfigNetworkSpec, seed: int) -> ConfigPopulation:
         seeds = np.sort(np.lexsort((ids, h))[:spec.initial_infections]).astype(np.int64)
     return ConfigPopulation(spec, seed, age, household_id, hh_off, hh_size, wp_id,
                             wp_local, wbase, wp_size, members, seeds)
+
+
+class DevicePopulation:
+    """The same population as `synthesize`, built on the device
+    (csrc/epi_population.cuh, row f3): every array is a torch tensor with the
+    ConfigPopulation name and dtype.  `to_host()` gives the ConfigPopulation."""
+
+    def __init__(self, spec: ConfigNetworkSpec, seed: int, device=None):
+        import ctypes
+
+        import torch
+
+        from . import _native as N
+        self.spec, self.seed = spec, int(seed)
+        dev = torch.device(device or "cuda")
+        n = spec.n_agents
+        workers = bool(spec.worker_bands) and spec.colleague_draws > 0
+        max_w = n // spec.wp_min + 2
+
+        def e(k, dt):
+            return torch.empty(max(k, 1), dtype=dt, device=dev)
+        self.age_band, self.household_id = e(n, torch.int8), e(n, torch.int32)
+        self.hh_off, self.hh_size = e(n, torch.uint8), e(n, torch.uint8)
+        self.wp_id, self.wp_local = e(n, torch.int32), e(n, torch.uint8)
+        members, base, size = e(n, torch.int32), e(max_w, torch.int32), e(max_w, torch.int32)
+        self.seeds = e(spec.initial_infections, torch.int64)
+        counts = torch.zeros(2, dtype=torch.int64, device=dev)
+        sp = N.EpiPopSpec()
+        sp.n_agents = n
+        sp.age_cum[:] = np.cumsum(spec.age_probs).tolist()
+        sp.n_sizes = len(spec.household_sizes)
+        sp.hh_sizes[:sp.n_sizes] = [int(x) for x in spec.household_sizes]
+        sp.hh_cum[:sp.n_sizes] = np.cumsum(spec.household_probs).tolist()
+        sp.worker_mask = sum(1 << int(b) for b in spec.worker_bands) if workers else 0
+        sp.wp_min, sp.wp_max = spec.wp_min, spec.wp_max
+        sp.n_seeds = spec.initial_infections
+        out = N.EpiPopOut()
+        for f, t in (("age_band", self.age_band), ("household_id", self.household_id),
+                     ("hh_off", self.hh_off), ("hh_size", self.hh_size), ("wp_id", self.wp_id),
+                     ("wp_local", self.wp_local), ("wp_members", members), ("wp_base", base),
+                     ("wp_size", size), ("seeds", self.seeds), ("counts", counts)):
+            setattr(out, f, N.ptr(t))
+        N.check(N.lib().epi_pop_synthesize(ctypes.byref(sp), self.seed & ((1 << 64) - 1),
+                                           ctypes.byref(out), N.stream_handle()))
+        n_w, n_m = (int(x) for x in counts.cpu())
+        self.wp_members, self.wp_base, self.wp_size = members[:n_m], base[:n_w], size[:n_w]
+        self.seeds = self.seeds[:spec.initial_infections]
+
+    @property
+    def n_agents(self) -> int:
+        return self.spec.n_agents
+
+    @property
+    def n_workplaces(self) -> int:
+        return int(self.wp_base.numel())
+
+    def poisson_table(self) -> np.ndarray:
+        return poisson_cdf_table(self.spec.random_mean, self.spec.random_slots)
+
+    def to_host(self) -> ConfigPopulation:
+        def h(t):
+            return t.cpu().numpy()
+        return ConfigPopulation(self.spec, self.seed, h(self.age_band), h(self.household_id),
+                                h(self.hh_off), h(self.hh_size), h(self.wp_id), h(self.wp_local),
+                                h(self.wp_base), h(self.wp_size), h(self.wp_members), h(self.seeds))

@@ -15,6 +15,7 @@
 
 #include "epi_kernels.cuh"
 #include "epi_msgpass.cuh"
+#include "epi_population.cuh"
 #include "epi_refnet.cuh"
 
 using namespace epi;
@@ -628,6 +629,98 @@ int epi_net_realize(const epi_net* net, uint64_t graph_seed, int32_t step, const
   return launch_realize(net, graph_seed, step, codes, entries, nullptr, nullptr, row_len, sort_rows, nullptr,
                         nullptr,
                         0, net->n_agents, S(stream));
+}
+
+int epi_pop_synthesize(const epi_pop_spec* sp, uint64_t seed, const epi_pop_out* o, void* stream) {
+  if (!sp || !o) return fail(EPI_EARG, "null argument");
+  const int64_t n = sp->n_agents;
+  if (n < 1 || n >= (1ll << 30)) return fail(EPI_EARG, "n_agents outside [1, 2^30)");
+  if (sp->n_sizes < 1 || sp->n_sizes > 32) return fail(EPI_EARG, "household size classes outside [1, 32]");
+  if (sp->wp_min < 2 || sp->wp_max < sp->wp_min || sp->wp_max > 255) return fail(EPI_EARG, "bad workplace sizes");
+  if (sp->n_seeds < 0 || sp->n_seeds > n) return fail(EPI_EARG, "n_seeds outside [0, n_agents]");
+  cudaStream_t s = S(stream);
+  PopTables T{};
+  for (int i = 0; i < 9; ++i) T.cum_age[i] = sp->age_cum[i];
+  for (int i = 0; i < sp->n_sizes; ++i) {
+    T.cum_hh[i] = sp->hh_cum[i];
+    T.hh_sizes[i] = sp->hh_sizes[i];
+  }
+  T.n_sizes = sp->n_sizes;
+  T.worker_mask = sp->worker_mask;
+  const int64_t max_w = n / sp->wp_min + 2;
+  // scratch (one-time setup: plain allocations, freed at the end)
+  uint8_t* worker = nullptr;
+  int64_t *size_k = nullptr, *ends = nullptr, *nW = nullptr, *wsz = nullptr, *wend = nullptr;
+  uint64_t *seed_key = nullptr, *key_sorted = nullptr, *wkey = nullptr, *wkey_sorted = nullptr;
+  int32_t *ids = nullptr, *ids_sorted = nullptr, *workers = nullptr, *seed32 = nullptr;
+  void* tmp = nullptr;
+  auto cleanup = [&]() {
+    for (void* p : {(void*)worker, (void*)size_k, (void*)ends, (void*)nW, (void*)wsz, (void*)wend,
+                    (void*)seed_key, (void*)key_sorted, (void*)wkey, (void*)wkey_sorted, (void*)ids,
+                    (void*)ids_sorted, (void*)workers, (void*)seed32, tmp})
+      if (p) cudaFree(p);
+  };
+  int rc = 0;
+  rc = rc ? rc : dalloc(&worker, n);
+  rc = rc ? rc : dalloc(&size_k, n);
+  rc = rc ? rc : dalloc(&ends, n);
+  rc = rc ? rc : dalloc(&nW, 1);
+  rc = rc ? rc : dalloc(&wsz, max_w);
+  rc = rc ? rc : dalloc(&wend, max_w);
+  rc = rc ? rc : dalloc(&seed_key, n);
+  rc = rc ? rc : dalloc(&key_sorted, n);
+  rc = rc ? rc : dalloc(&wkey, n);
+  rc = rc ? rc : dalloc(&wkey_sorted, n);
+  rc = rc ? rc : dalloc(&ids, n);
+  rc = rc ? rc : dalloc(&ids_sorted, n);
+  rc = rc ? rc : dalloc(&workers, n);
+  rc = rc ? rc : dalloc(&seed32, sp->n_seeds > 0 ? sp->n_seeds : 1);
+  if (rc) { cleanup(); return rc; }
+  size_t tb = 0, t1 = 0;
+  cub::DeviceScan::InclusiveSum(nullptr, t1, size_k, ends, (int)n, s); tb = t1 > tb ? t1 : tb;
+  cub::DeviceScan::InclusiveSum(nullptr, t1, wsz, wend, (int)max_w, s); tb = t1 > tb ? t1 : tb;
+  cub::DeviceSelect::Flagged(nullptr, t1, ids, worker, workers, nW, (int)n, s); tb = t1 > tb ? t1 : tb;
+  cub::DeviceRadixSort::SortPairs(nullptr, t1, seed_key, key_sorted, ids, ids_sorted, (int)n, 0, 64, s);
+  tb = t1 > tb ? t1 : tb;
+  cub::DeviceRadixSort::SortKeys(nullptr, t1, ids_sorted, seed32, (int)(sp->n_seeds > 0 ? sp->n_seeds : 1), 0, 32,
+                                 s);
+  tb = t1 > tb ? t1 : tb;
+  if (cudaMalloc(&tmp, tb > 0 ? tb : 1) != cudaSuccess) { cleanup(); return fail(EPI_ECUDA, "temp alloc"); }
+  const int g = grid_for(n, 256);
+#define PCK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { cleanup(); return fail(EPI_ECUDA, cudaGetErrorString(e_)); } } while (0)
+  k_pop_agents<<<g, 256, 0, s>>>(T, n, key_prefix(seed, 0, P_POP_AGE), key_prefix(seed, 0, P_POP_HOUSEHOLD),
+                                 key_prefix(seed, 0, P_POP_SEEDS), o->age_band, worker, size_k, seed_key, ids);
+  PCK(cudaGetLastError());
+  PCK(cub::DeviceScan::InclusiveSum(tmp, tb, size_k, ends, (int)n, s));
+  k_pop_households<<<g, 256, 0, s>>>(n, ends, size_k, o->household_id, o->hh_off, o->hh_size);
+  PCK(cudaGetLastError());
+  // workplaces: stable sort of the workers by key (ties keep ascending ids)
+  PCK(cub::DeviceSelect::Flagged(tmp, tb, ids, worker, workers, nW, (int)n, s));
+  int64_t W = 0;
+  PCK(cudaMemcpyAsync(&W, nW, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  PCK(cudaStreamSynchronize(s));
+  k_pop_worker_keys<<<g, 256, 0, s>>>(workers, nW, key_prefix(seed, 0, P_POP_WORKPLACE), wkey, max_w, sp->wp_min,
+                                      sp->wp_max - sp->wp_min + 1, wsz);
+  PCK(cudaGetLastError());
+  if (W > 0) PCK(cub::DeviceRadixSort::SortPairs(tmp, tb, wkey, wkey_sorted, workers, o->wp_members, (int)W, 0, 64, s));
+  PCK(cub::DeviceScan::InclusiveSum(tmp, tb, wsz, wend, (int)max_w, s));
+  k_fill_i32<<<g, 256, 0, s>>>(o->wp_id, n, -1);
+  PCK(cudaMemsetAsync(o->wp_local, 0, (size_t)n, s));
+  k_pop_workplaces<<<g, 256, 0, s>>>(o->wp_members, nW, wend, wsz, max_w, o->wp_id, o->wp_local, o->wp_base,
+                                     o->wp_size, o->counts);
+  PCK(cudaGetLastError());
+  // seeds: the n_seeds smallest keys (ties: ascending id), then by id
+  if (sp->n_seeds > 0) {
+    PCK(cub::DeviceRadixSort::SortPairs(tmp, tb, seed_key, key_sorted, ids, ids_sorted, (int)n, 0, 64, s));
+    PCK(cub::DeviceRadixSort::SortKeys(tmp, tb, ids_sorted, seed32, (int)sp->n_seeds, 0, 32, s));
+    k_widen<<<grid_for(sp->n_seeds, 256), 256, 0, s>>>(seed32, sp->n_seeds, o->seeds);
+    PCK(cudaGetLastError());
+  }
+#undef PCK
+  const cudaError_t e = cudaStreamSynchronize(s);
+  cleanup();
+  if (e != cudaSuccess) return fail(EPI_ECUDA, cudaGetErrorString(e));
+  return 0;
 }
 
 int epi_set_hot_window(epi_ctx* c, const void* base, int64_t bytes) {

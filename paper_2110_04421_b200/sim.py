@@ -23,7 +23,7 @@ import ctypes
 import numpy as np
 
 from . import _native as N
-from .confignet import ConfigNetworkSpec, ConfigPopulation, synthesize
+from .confignet import ConfigNetworkSpec, ConfigPopulation, DevicePopulation, synthesize
 from .device import DeviceColumns, pack_params
 from .engine import _u64
 from .errors import ConfigError
@@ -35,12 +35,17 @@ SERIES_COLUMNS = slice(0, 19)
 
 
 class DeviceNetwork:
-    """Static config-network arrays on the device + the C `epi_net` view."""
+    """Static config-network arrays on the device + the C `epi_net` view
+    (from a host ConfigPopulation or a DevicePopulation)."""
 
     def __init__(self, pop: ConfigPopulation, device):
         import torch
+        if not _TORCH_DT:
+            _init_dtypes()
 
         def up(a, dt):
+            if torch.is_tensor(a):      # DevicePopulation: already on the device
+                return a.to(device=device, dtype=_TORCH_DT[np.dtype(dt)]).contiguous()
             return torch.from_numpy(np.ascontiguousarray(a, dtype=dt)).to(device)
         spec = pop.spec
         self.hh_off = up(pop.hh_off, np.uint8)
@@ -65,6 +70,15 @@ class DeviceNetwork:
         s.poisson_cdf[:len(tab)] = tab.tolist()
         self.struct = s
         self.row_cap = spec.row_capacity
+
+
+_TORCH_DT = {}
+
+
+def _init_dtypes():
+    import torch
+    _TORCH_DT.update({np.dtype(np.uint8): torch.uint8, np.dtype(np.int32): torch.int32,
+                      np.dtype(np.int8): torch.int8, np.dtype(np.int64): torch.int64})
 
 
 def initial_columns(pop: ConfigPopulation) -> AgentColumns:
@@ -128,7 +142,7 @@ class ConfigSimulation:
     def create(cls, spec: ConfigNetworkSpec, seed: int, disease=None, table=None,
                interventions=None, **kw) -> "ConfigSimulation":
         from .defaults import default_disease, default_progression
-        pop = synthesize(spec, seed)
+        pop = DevicePopulation(spec, seed) if kw.pop("on_device", False) else synthesize(spec, seed)
         return cls(pop, disease or default_disease(), table or default_progression(),
                    interventions or InterventionConfig(), seed, **kw)
 
@@ -141,8 +155,18 @@ class ConfigSimulation:
     # -- initial state ------------------------------------------------------
     def _seeded_initial(self) -> DeviceColumns:
         import torch
-        d = DeviceColumns.from_host(initial_columns(self.population), self.device)
-        ids = torch.from_numpy(self.population.seeds.astype(np.int64)).to(self.device)
+        pop = self.population
+        if isinstance(pop, DevicePopulation):
+            # initial_columns on the device
+            d = DeviceColumns(self.n, self.device)
+            d.t["age_band"].copy_(pop.age_band[:self.n])
+            d.t["household_id"].copy_(pop.household_id[:self.n])
+            d.t["occupation"].copy_((pop.wp_id[:self.n] >= 0).to(torch.int16))
+            d.t["random_degree"].fill_(pop.spec.random_mean)
+            ids = pop.seeds.to(self.device)
+        else:
+            d = DeviceColumns.from_host(initial_columns(pop), self.device)
+            ids = torch.from_numpy(pop.seeds.astype(np.int64)).to(self.device)
         st = d.struct()
         s = N.stream_handle()
         N.check(self._lib.epi_seed_infections(self._ctx, ctypes.byref(st), _u64(self.seed),
