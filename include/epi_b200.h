@@ -261,6 +261,22 @@ int epi_net_realize(const epi_net *net, uint64_t graph_seed, int32_t step,
  * (hit ratio = persisting carve-out / window).  bytes = 0 clears it. */
 int epi_set_hot_window(epi_ctx *ctx, const void *base, int64_t bytes);
 
+/* Cross-rank exchange of a partitioned run (agent ranges, SURVEY §8(e) and
+ * §8(f) row f2), called synchronously from inside epi_sim_step on `stream`;
+ * returns 0 on success.  Kinds:
+ *   EPI_X_GATHER_U8  all-gather: every rank's owned range [lo, hi) of the
+ *                    global-indexed byte array `buf` (count = N) to all
+ *                    ranks (the DEN notifier flags);
+ *   EPI_X_SUM_U64    all-reduce sum of `count` uint64 (the vaccination
+ *                    eligibility histogram + active count);
+ *   EPI_X_EXSCAN_I64 exclusive prefix sum over the ranks, in rank (= id)
+ *                    order, of `count` int64, in place (the cut-bucket offset). */
+#define EPI_X_GATHER_U8 1
+#define EPI_X_SUM_U64 2
+#define EPI_X_EXSCAN_I64 3
+typedef int (*epi_exchange_fn)(void *user, int32_t kind, void *buf, int64_t count, void *stream);
+int epi_set_exchange(epi_ctx *ctx, epi_exchange_fn fn, void *user);
+
 /* Whole-population runs build the random-slot push tables (96 B/agent) only
  * up to `max_agents` agents (-1 = while they fit in L2). */
 int epi_set_push_max(epi_ctx *ctx, int64_t max_agents);

@@ -65,6 +65,10 @@ class EpiNet(C.Structure):
     ]
 
 
+# epi_exchange_fn (include/epi_b200.h): (user, kind, buf, count, stream) -> int
+XFN = C.CFUNCTYPE(_i32, _p, _i32, _p, _i64, _p)
+
+
 class EpiPopSpec(C.Structure):
     _fields_ = [("n_agents", _i64), ("age_cum", _d * 9), ("n_sizes", _i32), ("hh_sizes", _i32 * 32),
                 ("hh_cum", _d * 32), ("worker_mask", C.c_uint32), ("wp_min", _i32), ("wp_max", _i32),
@@ -90,6 +94,7 @@ _SIGS = {
     "epi_set_params": (_i32, [_p, C.POINTER(EpiParams)]),
     "epi_set_rows": (_i32, [_p, _i64, _i64]),
     "epi_set_hot_window": (_i32, [_p, _p, _i64]),
+    "epi_set_exchange": (_i32, [_p, XFN, _p]),
     "epi_pop_synthesize": (_i32, [C.POINTER(EpiPopSpec), _u64, C.POINTER(EpiPopOut), _p]),
     "epi_set_push_max": (_i32, [_p, _i64]),
     "epi_last_error": (C.c_char_p, []),

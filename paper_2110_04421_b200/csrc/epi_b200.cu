@@ -116,6 +116,8 @@ int dalloc(T** p, size_t count) {
 
 struct epi_ctx {
   HotWindow hot;                     // L2-persisting window (source codes)
+  epi_exchange_fn xfn = nullptr;     // cross-rank exchange of a partitioned run
+  void* xuser = nullptr;
   int push_max = -1;                 // push tables up to this many agents (-1: by L2 size)
   epi_params host{};
   epi_params* P = nullptr;           // device copy
@@ -216,11 +218,23 @@ bool interventions_on(const epi_params& p) {
 
 // Phases 3-6 + finish, shared by the graph-in step and the config sim step.
 // `den_scan` launches the contact scan for this step (may be empty).
+static bool partitioned(const epi_ctx* c) { return c->lo != 0 || c->hi != c->n; }
+
+static int exchange(epi_ctx* c, int32_t kind, void* buf, int64_t count, cudaStream_t s) {
+  if (!c->xfn) return fail(EPI_EARG, "partitioned run without an exchange (epi_set_exchange)");
+  const int rc = c->xfn(c->xuser, kind, buf, count, (void*)s);
+  return rc ? fail(EPI_ECUDA, "exchange callback failed") : 0;
+}
+
+// `den_scan(pull)` launches the contact scan for this step (may be empty):
+// push from the notifiers' rows, or, in partitioned runs, pull into the
+// owned rows after the notifier flags were all-gathered.
 template <class DenScan>
 int run_interventions(epi_ctx* c, const StepArgs& A, uint16_t* codes_next, const epi_net* net_dev,
                       uint64_t rcount_next, int32_t* vax_open, cudaStream_t s, DenScan&& den_scan) {
   const epi_params& p = c->host;
   const int64_t n = c->n;
+  const bool part = partitioned(c);
   const int threads = 256;
   const int grid = grid_for(n, threads);
   if (p.testing_enabled) {
@@ -228,25 +242,50 @@ int run_interventions(epi_ctx* c, const StepArgs& A, uint16_t* codes_next, const
     CKL();
   }
   if (p.den_enabled) {
-    int rc = den_scan();
+    // every rank's notifiers (the owned bytes of `flags`) on every rank
+    if (part) {
+      int rc = exchange(c, EPI_X_GATHER_U8, c->flags, n, s);
+      if (rc) return rc;
+    }
+    int rc = den_scan(part);
     if (rc) return rc;
   }
-  if (p.vaccination_enabled) CK(cudaMemsetAsync(c->hist, 0, NUM_BUCKETS * sizeof(unsigned long long), s));
+  if (p.vaccination_enabled)
+    CK(cudaMemsetAsync(c->hist, 0, (NUM_BUCKETS + 2) * sizeof(unsigned long long), s));
   if (p.den_enabled || p.quarantine_enabled || p.vaccination_enabled) {
     k_iv_post<<<grid, threads, 0, s>>>(A, c->bucket, c->hist);
     CKL();
   }
   if (p.vaccination_enabled) {
     if (!vax_open) return fail(EPI_EARG, "vaccination enabled but no vax_open latch given");
-    k_vax_plan<<<1, 32, 0, s>>>(c->P, c->hist, A.rec, vax_open, c->plan);
+    if (part) {
+      // population histogram and active count: summed over the ranks
+      CK(cudaMemcpyAsync(c->hist + NUM_BUCKETS, A.rec + EPI_REC_ACTIVE, sizeof(long long),
+                         cudaMemcpyDeviceToDevice, s));
+      int rc = exchange(c, EPI_X_SUM_U64, c->hist, NUM_BUCKETS + 1, s);
+      if (rc) return rc;
+    }
+    k_vax_plan<<<1, 32, 0, s>>>(c->P, c->hist, A.rec, vax_open, c->plan, part ? 1 : 0, c->lo == 0 ? 1 : 0);
     CKL();
-    const int64_t tiles = (n + VAX_TILE - 1) / VAX_TILE;
-    k_vax_tilecount<<<(unsigned)tiles, VAX_TILE, 0, s>>>(c->bucket, n, c->plan, c->tile_off);
-    CKL();
-    k_vax_tilescan<<<1, 1024, 0, s>>>(c->tile_off, tiles);
-    CKL();
-    k_vax_apply<<<(unsigned)tiles, VAX_TILE, 0, s>>>(A, c->bucket, c->plan, c->tile_off);
-    CKL();
+    const int64_t tiles = (c->hi - c->lo + VAX_TILE - 1) / VAX_TILE;
+    if (tiles > 0) {
+      k_vax_tilecount<<<(unsigned)tiles, VAX_TILE, 0, s>>>(c->bucket, c->lo, c->hi, c->plan, c->tile_off);
+      CKL();
+      k_vax_tilescan<<<1, 1024, 0, s>>>(c->tile_off, tiles, c->plan + 2);
+      CKL();
+    } else {
+      CK(cudaMemsetAsync(c->plan + 2, 0, sizeof(long long), s));
+    }
+    // the cut bucket is served in id order across the ranks' contiguous ranges
+    if (part) {
+      int rc = exchange(c, EPI_X_EXSCAN_I64, c->plan + 2, 1, s);
+      if (rc) return rc;
+    }
+    if (tiles > 0) {
+      k_vax_apply<<<(unsigned)tiles, VAX_TILE, 0, s>>>(A, c->bucket, c->plan, c->tile_off,
+                                                       part ? (const long long*)(c->plan + 2) : nullptr);
+      CKL();
+    }
   }
   k_finish<<<grid, threads, 0, s>>>(A, codes_next, net_dev, rcount_next);
   CKL();
@@ -310,7 +349,7 @@ int epi_create(const epi_params* params, int64_t n_agents, epi_ctx** out) {
   const int64_t tiles = (n_agents + VAX_TILE - 1) / VAX_TILE;
   if (!rc) rc = dalloc(&c->flags, n4);
   if (!rc) rc = dalloc(&c->bucket, n_agents);
-  if (!rc) rc = dalloc(&c->hist, NUM_BUCKETS);
+  if (!rc) rc = dalloc(&c->hist, NUM_BUCKETS + 2);   // + population active count
   if (!rc) rc = dalloc(&c->plan, 4);
   if (!rc) rc = dalloc(&c->tile_off, tiles);
   if (!rc) rc = dalloc(&c->scratch_rec, EPI_REC_LEN);
@@ -510,7 +549,7 @@ static int step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t see
   }
   CKL();
   if (iv) {
-    rc = run_interventions(c, A, nullptr, nullptr, 0, vax_open, s, [&]() -> int {
+    rc = run_interventions(c, A, nullptr, nullptr, 0, vax_open, s, [&](bool) -> int {
       for (int i = 0; i < c->ring_count; ++i) {
         const epi_ctx::Slot& sl = c->ring[i];
         if (!sl.n) continue;
@@ -743,6 +782,13 @@ int epi_set_hot_window(epi_ctx* c, const void* base, int64_t bytes) {
   return 0;
 }
 
+int epi_set_exchange(epi_ctx* c, epi_exchange_fn fn, void* user) {
+  if (!c) return fail(EPI_EARG, "null ctx");
+  c->xfn = fn;
+  c->xuser = user;
+  return 0;
+}
+
 int epi_set_push_max(epi_ctx* c, int64_t max_agents) {
   if (!c) return fail(EPI_EARG, "null ctx");
   c->push_max = max_agents < 0 ? -1 : (int)(max_agents > 0x7FFFFFFF ? 0x7FFFFFFF : max_agents);
@@ -824,9 +870,9 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
   if (!c->has_net) return fail(EPI_EARG, "epi_sim_step needs epi_net_attach first");
   if (st->n_agents != c->n) return fail(EPI_EARG, "state size differs from context");
   const bool iv = interventions_on(c->host);
-  if ((c->lo != 0 || c->hi != c->n) && (c->host.den_enabled || c->host.vaccination_enabled))
-    return fail(EPI_EARG, "exposure notification and vaccination need the whole population "
-                          "(partitioned runs support quarantine and testing only)");
+  if (partitioned(c) && (c->host.den_enabled || c->host.vaccination_enabled) && !c->xfn)
+    return fail(EPI_EARG, "exposure notification and vaccination in a partitioned run need a "
+                          "cross-rank exchange (epi_set_exchange)");
   if (mode == 1 && c->host.den_enabled) return fail(EPI_EARG, "fused mode keeps no contact log; use mode 0 with DEN");
   if (mode == 1 && precision != EPI_F32) return fail(EPI_EARG, "fused mode is fp32 only");
   cudaStream_t s = S(stream);
@@ -924,13 +970,17 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
   }
   if (ev) CK(cudaEventRecord((cudaEvent_t)ev[2], s));
   if (iv) {
-    int rc = run_interventions(c, A, codes_next, c->net_dev, rcount_next, vax_open, s, [&]() -> int {
+    int rc = run_interventions(c, A, codes_next, c->net_dev, rcount_next, vax_open, s, [&](bool pull) -> int {
       const int L = c->host.den_lookback;
       for (int i = 0; i < c->net_slots; ++i) {
         const int st_i = c->net_slot_step[i];
         if (st_i < 0 || st_i >= step || st_i < step - L) continue;
-        k_den_scan_csr<<<grid_for(c->n, 256), 256, 0, s>>>(c->net_entries[i], c->net_rowlen[i],
-                                                             c->net.row_cap, c->n, c->flags);
+        if (pull)
+          k_den_pull_csr<<<grid_for(c->hi - c->lo, 256), 256, 0, s>>>(c->net_entries[i], c->net_rowlen[i],
+                                                                       c->net.row_cap, c->lo, c->hi, c->flags);
+        else
+          k_den_scan_csr<<<grid_for(c->n, 256), 256, 0, s>>>(c->net_entries[i], c->net_rowlen[i],
+                                                               c->net.row_cap, c->n, c->flags);
         CKL();
       }
       return 0;

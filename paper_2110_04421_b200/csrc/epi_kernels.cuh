@@ -855,6 +855,25 @@ __global__ void k_den_scan_coo(const int32_t* __restrict__ src, const int32_t* _
     }
   }
 }
+// Pull form for partitioned runs: agent a of the owned rows is notified if a
+// source in its own row is a notifier (the notifier flags of every rank were
+// all-gathered first).  Config graphs are symmetric, so this marks exactly
+// the agents the push scan below marks.
+__global__ void k_den_pull_csr(const uint32_t* __restrict__ entries, const int32_t* __restrict__ row_len,
+                               int cap, int64_t lo, int64_t hi, uint8_t* __restrict__ flags) {
+  for (int64_t a = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < hi;
+       a += (int64_t)gridDim.x * blockDim.x) {
+    const uint8_t fa = flags[a];
+    if (fa & FL_NOTIFIED) continue;
+    const int len = row_len[a];
+    const uint32_t* e = entries + a * (int64_t)cap;
+    for (int i = 0; i < len; ++i)
+      if (flags[e[i] >> 2] & FL_NOTIFIER) {
+        flags[a] = fa | FL_NOTIFIED;
+        break;
+      }
+  }
+}
 // Same over a padded config CSR slot; config graphs are symmetric, so the
 // contacts of notifier a are the sources listed in a's own row.
 __global__ void k_den_scan_csr(const uint32_t* __restrict__ entries, const int32_t* __restrict__ row_len,
@@ -945,12 +964,18 @@ __global__ void k_iv_post(StepArgs A, uint8_t* __restrict__ bucket, unsigned lon
 }
 
 // plan[0] = cut bucket (-1: nobody), plan[1] = remaining slots in the cut
-// bucket.  Trigger latch + budget (engine.py:286-310).
+// bucket.  Trigger latch + budget (engine.py:286-310).  `hist` is the
+// population's eligibility histogram; hist[NUM_BUCKETS] the population's
+// active count when `global_active` (partitioned runs: summed over ranks),
+// else the active count is this record's.  Only `write_doses` ranks record
+// the doses given (rank 0 of a partitioned run).
 __global__ void k_vax_plan(const epi_params* __restrict__ P, const unsigned long long* __restrict__ hist,
-                           long long* rec, int32_t* vax_open, long long* plan) {
+                           long long* rec, int32_t* vax_open, long long* plan, int global_active,
+                           int write_doses) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   int open = *vax_open;
-  if (!open && (double)rec[EPI_REC_ACTIVE] >= P->start_trigger_count) open = 1;
+  const double active = global_active ? (double)hist[NUM_BUCKETS] : (double)rec[EPI_REC_ACTIVE];
+  if (!open && active >= P->start_trigger_count) open = 1;
   *vax_open = open;
   plan[0] = -1;
   plan[1] = 0;
@@ -962,25 +987,26 @@ __global__ void k_vax_plan(const epi_params* __restrict__ P, const unsigned long
     if (cum + c >= budget) {
       plan[0] = b;
       plan[1] = budget - cum;
-      rec[EPI_REC_DOSES] = budget;
+      if (write_doses) rec[EPI_REC_DOSES] = budget;
       return;
     }
     cum += c;
   }
   plan[0] = NUM_BUCKETS;       // everyone eligible gets a dose
   plan[1] = 0;
-  rec[EPI_REC_DOSES] = cum;
+  if (write_doses) rec[EPI_REC_DOSES] = cum;
 }
 
 constexpr int VAX_TILE = 1024;
 
-__global__ void k_vax_tilecount(const uint8_t* __restrict__ bucket, int64_t n, const long long* plan,
+// Tiles of VAX_TILE agents over the owned rows [lo, n).
+__global__ void k_vax_tilecount(const uint8_t* __restrict__ bucket, int64_t lo, int64_t n, const long long* plan,
                                 int* __restrict__ tile_count) {
   const long long cut = plan[0];
   __shared__ int cnt;
   if (threadIdx.x == 0) cnt = 0;
   __syncthreads();
-  const int64_t a = blockIdx.x * (int64_t)VAX_TILE + threadIdx.x;
+  const int64_t a = lo + blockIdx.x * (int64_t)VAX_TILE + threadIdx.x;
   const int hit = (cut >= 0 && cut < NUM_BUCKETS && a < n && bucket[a] == (uint8_t)cut) ? 1 : 0;
   const int w = __reduce_add_sync(0xFFFFFFFFu, hit);
   if (lane_id() == 0 && w) atomicAdd(&cnt, w);
@@ -988,7 +1014,9 @@ __global__ void k_vax_tilecount(const uint8_t* __restrict__ bucket, int64_t n, c
   if (threadIdx.x == 0) tile_count[blockIdx.x] = cnt;
 }
 
-__global__ void k_vax_tilescan(int* __restrict__ tile_count, int64_t tiles) {
+// Exclusive scan of the tile counts; the total (this range's agents in the
+// cut bucket) goes to *total.
+__global__ void k_vax_tilescan(int* __restrict__ tile_count, int64_t tiles, long long* total) {
   // single block exclusive scan (tiles <= a few 10k)
   typedef cub::BlockScan<int, 1024> Scan;
   __shared__ typename Scan::TempStorage tmp;
@@ -1005,19 +1033,23 @@ __global__ void k_vax_tilescan(int* __restrict__ tile_count, int64_t tiles) {
     if (threadIdx.x == 0) carry += total;
     __syncthreads();
   }
+  if (threadIdx.x == 0) *total = carry;
 }
 
 // Phase 6b: administer doses to the selected agents (engine.py:306-335).
+// The cut bucket is served in id order: `offset` (nullable) = its agents on
+// lower-ranked (lower-id) partitions.
 __global__ void __launch_bounds__(1024) k_vax_apply(StepArgs A, const uint8_t* __restrict__ bucket,
-                                                    const long long* plan, const int* __restrict__ tile_off) {
+                                                    const long long* plan, const int* __restrict__ tile_off,
+                                                    const long long* offset) {
   typedef cub::BlockScan<int, 1024> Scan;
   __shared__ typename Scan::TempStorage tmp;
-  const long long cut = plan[0], rem = plan[1];
+  const long long cut = plan[0], rem = plan[1] - (offset ? *offset : 0);
   const epi_params* __restrict__ P = A.P;
   const epi_state& st = A.st;
   const int step = A.step;
-  const int64_t n = st.n_agents;
-  const int64_t a = blockIdx.x * (int64_t)VAX_TILE + threadIdx.x;
+  const int64_t n = A.hi;
+  const int64_t a = A.lo + blockIdx.x * (int64_t)VAX_TILE + threadIdx.x;
   const uint8_t bk = a < n ? bucket[a] : NO_BUCKET;
   const int in_cut = (cut >= 0 && cut < NUM_BUCKETS && bk == (uint8_t)cut) ? 1 : 0;
   int rank;

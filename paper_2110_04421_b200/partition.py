@@ -7,11 +7,26 @@ the only per-day exchange is one all-gather of the codes each rank just wrote
 for its rows (2 bytes/agent, N*2/P bytes sent per rank).  Day records are
 partial sums per rank, reduced once at the end.
 
+With exposure notification or vaccination a day
+also needs three in-step exchanges, which the native step requests through
+a callback (epi_set_exchange):
+  * the DEN notifier flags of every rank (all-gather of one byte per owned
+    agent), after which each rank pulls notifications into its own rows
+    (config graphs are symmetric);
+  * the vaccination eligibility histogram and active count (all-reduce of
+    55 integers), so every rank computes the same cut bucket and budget;
+  * the cut-bucket count of the lower-ranked (lower-id) ranges (exclusive
+    scan of one integer), so the cut bucket is served in global id order.
+
 The exchange is pluggable:
-  NcclCodeExchange   torch.distributed all_gather_into_tensor (NCCL over
-                     NVLink/NVSwitch on one 8xB200 node; gloo on CPU tests);
+  NcclCodeExchange   torch.distributed (NCCL over NVLink/NVSwitch on one
+                     8xB200 node; gloo on CPU tests);
   LocalCodeExchange  P emulated ranks in one process on one GPU (device
-                     copies), used to prove partition invariance bitwise.
+                     copies, days in lockstep), to prove partition invariance;
+  ThreadExchange     P emulated ranks in P host threads on one GPU (streams
+                     of their own, host barriers between the phases; no
+                     kernel ever waits on another rank's kernel), for the
+                     in-step exchanges of DEN and vaccination.
 """
 
 from __future__ import annotations
@@ -22,6 +37,21 @@ from dataclasses import dataclass
 from . import _native as N
 from .errors import ConfigError
 from .sim import ConfigSimulation
+
+_X_GATHER_U8, _X_SUM_U64, _X_EXSCAN_I64 = 1, 2, 3
+
+
+class _DevArray:
+    """Zero-copy view of a raw device pointer (__cuda_array_interface__)."""
+
+    def __init__(self, ptr, count, typestr):
+        self.__cuda_array_interface__ = {"shape": (int(count),), "typestr": typestr,
+                                         "data": (int(ptr), False), "version": 3}
+
+
+def _view(ptr, count, typestr):
+    import torch
+    return torch.as_tensor(_DevArray(ptr, count, typestr), device="cuda")
 
 
 @dataclass(frozen=True)
@@ -70,6 +100,40 @@ class NcclCodeExchange:
             for r, p in enumerate(parts):
                 codes[r * c:(r + 1) * c].copy_(p.to(codes.dtype))
 
+    # -- in-step exchanges (DEN, vaccination) --------------------------------
+    def gather_rows(self, t):
+        """Every rank's owned rows of the global-indexed tensor `t`, everywhere."""
+        import torch
+        import torch.distributed as dist
+        c = self.plan.chunk
+        lo, hi = self.plan.rows(self.rank)
+        mine = torch.zeros(c, dtype=t.dtype, device=t.device)
+        mine[:hi - lo] = t[lo:hi]
+        if t.is_cuda:
+            full = torch.empty(self.plan.padded, dtype=t.dtype, device=t.device)
+            dist.all_gather_into_tensor(full, mine, group=self.group)
+        else:   # gloo: widen
+            parts = [torch.empty(c, dtype=torch.int32) for _ in range(self.plan.world)]
+            dist.all_gather(parts, mine.to(torch.int32), group=self.group)
+            full = torch.cat(parts).to(t.dtype)
+        n = self.plan.n_agents
+        t[:n].copy_(full[:n])
+
+    def sum_(self, t):
+        import torch.distributed as dist
+        dist.all_reduce(t, group=self.group)
+
+    def exscan_(self, t):
+        """Exclusive prefix sum over the ranks (rank order), in place."""
+        import torch
+        import torch.distributed as dist
+        parts = [torch.empty_like(t) for _ in range(self.plan.world)]
+        dist.all_gather(parts, t.clone(), group=self.group)
+        acc = torch.zeros_like(t)
+        for r in range(self.rank):
+            acc += parts[r]
+        t.copy_(acc)
+
     def reduce_records(self, rec):
         """Sum the per-rank partial day records (step column kept)."""
         import torch.distributed as dist
@@ -110,17 +174,103 @@ class LocalCodeExchange:
         return out
 
 
+class ThreadExchange:
+    """P emulated ranks, one host thread and CUDA stream each, on one GPU.
+
+    Every exchange: the rank synchronises its stream, publishes its buffer,
+    waits at a host barrier, combines the published buffers into its own
+    (device copies on its stream), synchronises again and waits at a second
+    barrier, so no rank overwrites a buffer another rank is still reading."""
+
+    def __init__(self, plan: PartitionPlan):
+        import threading
+        self.plan = plan
+        self.barrier = threading.Barrier(plan.world)
+        self.posted = [None] * plan.world
+
+    def _post(self, rank, t):
+        import torch
+        torch.cuda.current_stream().synchronize()
+        self.posted[rank] = t
+        self.barrier.wait()
+
+    def _done(self):
+        import torch
+        torch.cuda.current_stream().synchronize()
+        self.barrier.wait()
+
+    def for_rank(self, rank):
+        ex = self
+
+        class _Rank:
+            def gather_rows(self, t):
+                ex._post(rank, t)
+                for q, other in enumerate(ex.posted):
+                    if q != rank:
+                        lo, hi = ex.plan.rows(q)
+                        t[lo:hi].copy_(other[lo:hi])
+                ex._done()
+
+            def sum_(self, t):
+                ex._post(rank, t.clone())
+                acc = ex.posted[0].clone()
+                for other in ex.posted[1:]:
+                    acc += other
+                t.copy_(acc)
+                ex._done()
+
+            def exscan_(self, t):
+                ex._post(rank, t.clone())
+                acc = torch_zeros_like(t)
+                for q in range(rank):
+                    acc += ex.posted[q]
+                t.copy_(acc)
+                ex._done()
+
+            def exchange(self, codes):
+                self.gather_rows(codes)
+        return _Rank()
+
+
+def torch_zeros_like(t):
+    import torch
+    return torch.zeros_like(t)
+
+
 class PartitionedSimulation(ConfigSimulation):
     """One rank of an agent-range partitioned config simulation."""
 
     def __init__(self, pop, disease, table, interventions, seed, plan: PartitionPlan, rank: int,
                  exchange=None, **kw):
-        if interventions.den_enabled or interventions.vaccination_enabled:
-            raise ConfigError("partitioned runs support quarantine/testing only "
-                              "(DEN and vaccination need global state; SURVEY §8(f) f2)")
+        needs_x = interventions.den_enabled or interventions.vaccination_enabled
+        if needs_x and not hasattr(exchange, "sum_"):
+            raise ConfigError("exposure notification and vaccination in a partitioned run need "
+                              "an in-step exchange (NcclCodeExchange or ThreadExchange)")
         self.plan, self.rank, self.exchange = plan, rank, exchange
         self._code_len = plan.padded
+        self._ready = False          # no exchange from inside the constructor's reset()
         super().__init__(pop, disease, table, interventions, seed, **kw)
+        self._ready = True
+        if needs_x:
+            self._hook = N.XFN(self._on_exchange)      # kept alive with the simulation
+            N.check(self._lib.epi_set_exchange(self._ctx, self._hook, None))
+
+    def _on_exchange(self, _user, kind, buf, count, _stream):
+        """Called by the native step (same thread, current stream)."""
+        try:
+            if kind == _X_GATHER_U8:
+                self.exchange.gather_rows(_view(buf, count, "|u1"))
+            elif kind == _X_SUM_U64:
+                self.exchange.sum_(_view(buf, count, "<i8"))    # non-negative counts
+            elif kind == _X_EXSCAN_I64:
+                self.exchange.exscan_(_view(buf, count, "<i8"))
+            else:
+                return 1
+            return 0
+        except Exception:  # noqa: BLE001 - reported through the C return code
+            import traceback
+            traceback.print_exc()
+            return 1
 
     def _alloc_codes(self):
         import torch
@@ -132,13 +282,13 @@ class PartitionedSimulation(ConfigSimulation):
 
     def reset(self) -> None:
         super().reset()
-        if isinstance(self.exchange, NcclCodeExchange):
+        if self._ready and self.exchange is not None and not isinstance(self.exchange, LocalCodeExchange):
             self.exchange.exchange(self.codes[0])
 
     def step(self) -> None:
         t = self.clock
         super().step()
-        if isinstance(self.exchange, NcclCodeExchange):
+        if self.exchange is not None and not isinstance(self.exchange, LocalCodeExchange):
             self.exchange.exchange(self.codes[(t + 1) & 1])
 
     def run(self, days: int | None = None) -> None:
@@ -159,4 +309,41 @@ def run_emulated(pop, disease, table, interventions, seed, world: int, days: int
         for s in sims:
             s.step()
         ex.exchange_all((t + 1) & 1)
+    return sims, LocalCodeExchange.reduce_records(sims)
+
+
+def run_threaded(pop, disease, table, interventions, seed, world: int, days: int, **kw):
+    """P ranks on one GPU in P host threads (own streams), with the in-step
+    exchanges of DEN and vaccination; returns (sims, summed records)."""
+    import threading
+
+    import torch
+    plan = PartitionPlan(pop.n_agents, world)
+    ex = ThreadExchange(plan)
+    sims = [None] * world
+    errors = []
+    build = threading.Lock()
+
+    def rank_main(r):
+        try:
+            stream = torch.cuda.Stream()
+            with torch.cuda.stream(stream):
+                with build:          # contexts and tables are built one at a time
+                    sims[r] = PartitionedSimulation(pop, disease, table, interventions, seed, plan, r,
+                                                    ex.for_rank(r), horizon=days, **kw)
+                ex.barrier.wait()
+                sims[r].reset()      # exchanges the day-0 codes
+                for _ in range(days):
+                    sims[r].step()
+                stream.synchronize()
+        except BaseException as e:  # noqa: BLE001
+            errors.append(e)
+            ex.barrier.abort()
+    threads = [threading.Thread(target=rank_main, args=(r,)) for r in range(world)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    if errors:
+        raise errors[0]
     return sims, LocalCodeExchange.reduce_records(sims)

@@ -36,3 +36,34 @@ def test_partitioned_equals_single(mode, precision, world):
         mine = s.host_columns()
         for c in ("stage", "infected_at", "next_transition_at", "quarantine_until", "test_result_at"):
             assert np.array_equal(getattr(mine, c)[lo:hi], getattr(full, c)[lo:hi]), (s.rank, c)
+
+
+@pytest.mark.parametrize("precision,world", [("f64", 2), ("f32", 3)])
+def test_partitioned_den_and_vaccination_equal_single(precision, world):
+    """Row f2: exposure notification and vaccination across agent ranges, the
+    in-step exchanges emulated by host threads; bitwise equal to P = 1."""
+    from paper_2110_04421_b200.interventions import DenConfig, VaccinePolicy
+    from paper_2110_04421_b200.partition import run_threaded
+    spec = ConfigNetworkSpec.config(1, n_agents=6007, initial_infections=60)
+    pop = synthesize(spec, 8)
+    iv = InterventionConfig(quarantine_enabled=True, testing_enabled=True,
+                            test_kind=TestKind("cfg2", 0.3, 1, 2), den_enabled=True,
+                            den=DenConfig(0.6), vaccination_enabled=True,
+                            vaccine=VaccinePolicy(daily_rate=0.02, dose1_efficacy=0.5,
+                                                  dose2_efficacy=0.9, dose_gap=7,
+                                                  start_trigger=0.002))
+    d, t = default_disease(), default_progression()
+    days = 40
+    ref = ConfigSimulation(pop, d, t, iv, 77, mode="csr", precision=precision, horizon=days)
+    ref.run()
+    r = ref.rec.cpu().numpy()
+    assert r[:, 17].sum() > 0 and r[:, 18].sum() > 0          # doses given, notifications sent
+    sims, rec = run_threaded(pop, d, t, iv, 77, world, days, mode="csr", precision=precision)
+    assert np.array_equal(rec.cpu().numpy(), r), np.argwhere(rec.cpu().numpy() != r)[:5]
+    full = ref.host_columns()
+    for s in sims:
+        lo, hi = s.plan.rows(s.rank)
+        mine = s.host_columns()
+        for c in ("stage", "infected_at", "next_transition_at", "quarantine_until", "vaccine_status",
+                  "dose1_at", "immune", "den_test_due_at"):
+            assert np.array_equal(getattr(mine, c)[lo:hi], getattr(full, c)[lo:hi]), (s.rank, c)

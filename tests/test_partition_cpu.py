@@ -48,7 +48,16 @@ def _worker(rank, world, port, n, q):
     rec[:, N.REC["edges"]] = 10 * (rank + 1)
     rec[:, N.REC["flags"]] = rank
     ex.reduce_records(rec)
-    q.put((rank, codes.numpy().copy(), rec.numpy().copy()))
+    # in-step exchanges of DEN / vaccination (row f2)
+    flags = torch.zeros(n, dtype=torch.uint8)
+    flags[lo:hi] = (torch.arange(lo, hi) % 7 == 0).to(torch.uint8) * (2 + rank)
+    ex.gather_rows(flags)
+    hist = torch.arange(55, dtype=torch.int64) * (rank + 1)
+    ex.sum_(hist)
+    cut = torch.tensor([5 + 10 * rank], dtype=torch.int64)
+    ex.exscan_(cut)
+    q.put((rank, codes.numpy().copy(), rec.numpy().copy(), flags.numpy().copy(), hist.numpy().copy(),
+           int(cut[0])))
     dist.destroy_process_group()
 
 
@@ -66,7 +75,16 @@ def test_code_exchange_and_record_reduction_gloo_world2(n):
         p.join(timeout=60)
         assert p.exitcode == 0
     want = (np.arange(n, dtype=np.int16) * 3 + 1)
-    for rank, codes, rec in out:
+    plan = PartitionPlan(n, world)
+    want_flags = np.zeros(n, np.uint8)
+    for r in range(world):
+        lo, hi = plan.rows(r)
+        ids = np.arange(lo, hi)
+        want_flags[lo:hi] = (ids % 7 == 0) * (2 + r)
+    for rank, codes, rec, flags, hist, cut in out:
+        assert np.array_equal(flags, want_flags)
+        assert np.array_equal(hist, np.arange(55) * 3)
+        assert cut == (0 if rank == 0 else 5)
         assert np.array_equal(codes[:n], want)
         assert np.array_equal(rec[:, N.REC["step"]], np.arange(4))
         assert np.all(rec[:, N.REC["edges"]] == 30)
