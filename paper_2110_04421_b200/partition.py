@@ -31,7 +31,6 @@ The exchange is pluggable:
 
 from __future__ import annotations
 
-import ctypes
 from dataclasses import dataclass
 
 from . import _native as N
