@@ -261,6 +261,15 @@ int epi_net_realize(const epi_net *net, uint64_t graph_seed, int32_t step,
  * (hit ratio = persisting carve-out / window).  bytes = 0 clears it. */
 int epi_set_hot_window(epi_ctx *ctx, const void *base, int64_t bytes);
 
+/* Infection decision of epi_step (graph-in, fp64 canonical): one aggregate
+ * draw against 1 - exp(-sum of hazards) (Engine, engine.py:153-175), or one
+ * Bernoulli per incident edge with keyed INFECTION_EDGE draws k = j over the
+ * nonzero contributions in (src, kind) order (the reference oracle's
+ * independent-edges mode, oracle.py:185-192; validation only). */
+#define EPI_INFECT_AGGREGATE 0
+#define EPI_INFECT_INDEPENDENT 1
+int epi_set_infection_mode(epi_ctx *ctx, int32_t mode);
+
 /* Cross-rank exchange of a partitioned run (agent ranges, SURVEY §8(e) and
  * §8(f) row f2), called synchronously from inside epi_sim_step on `stream`;
  * returns 0 on success.  Kinds:

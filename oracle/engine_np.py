@@ -24,7 +24,7 @@ INFECTIOUS = np.zeros(11, bool); INFECTIOUS[1:6] = True         # stages.py:63-6
 ASYM_LIKE = np.zeros(11, bool); ASYM_LIKE[1:4] = True           # stages.py:68-70
 ACTIVE = np.zeros(11, bool); ACTIVE[1:8] = True                 # stages.py:72-77
 
-P_INF, P_ENTRY, P_BRANCH, P_DELAY = 1, 3, 4, 5                  # rng.py:37-57
+P_INF, P_INF_EDGE, P_ENTRY, P_BRANCH, P_DELAY = 1, 2, 3, 4, 5      # rng.py:37-57
 P_TPOS, P_TTURN, P_QDROP, P_DEN, P_APP, P_VAX = 6, 7, 8, 9, 10, 11
 
 
@@ -81,6 +81,30 @@ def hazard(cols, disease, step, graph, sterilizing):
             out = np.bincount(d, weights=term, minlength=n)
     out[~target_mask(cols, sterilizing)] = 0.0
     return out
+
+
+def edge_terms(cols, disease, step, graph):
+    """Valid incident hazards in canonical (dst, src, kind) order, zero terms
+    dropped: the contributions of oracle.py:126-144, sorted as oracle.py:178."""
+    src = np.asarray(graph.src); dst = np.asarray(graph.dst); kind = np.asarray(graph.kind)
+    if not len(src):
+        e = np.empty(0, np.int64)
+        return e, e, e, np.empty(0)
+    t = step - cols.infected_at[src].astype(np.int64)
+    ok = (INFECTIOUS[cols.stage[src]] & (cols.quarantine_until[src] <= step)
+          & (t >= 1) & (t <= disease.t_max))
+    keep = np.flatnonzero(ok)
+    s, d, k, tt = src[keep], dst[keep], kind[keep], t[keep]
+    o = np.lexsort((k, s, d))
+    s, d, k, tt = s[o], d[o], k[o], tt[o]
+    a = np.where(ASYM_LIKE[cols.stage[s]], disease.asymptomatic_factor, 1.0)
+    term = disease.rate_scale * disease.age_susceptibility[cols.age_band[d]]
+    term = term * a
+    term = term * disease.network_scale[k]
+    term = term / disease.mean_daily_interactions
+    term = term * disease.day_weights[tt]
+    nz = term != 0.0
+    return d[nz].astype(np.int64), s[nz].astype(np.int64), k[nz].astype(np.int64), term[nz]
 
 
 def pick(rule, age_bands, u):
@@ -157,7 +181,11 @@ class ContactRing:
 class OracleEngine:
     """Restatement of `Engine` (engine.py:55-347) — same constructor shape."""
 
-    def __init__(self, cols, disease, table, interventions, seed, check_invariants=False):
+    def __init__(self, cols, disease, table, interventions, seed, check_invariants=False,
+                 infection_mode="aggregate"):
+        if infection_mode not in ("aggregate", "independent"):
+            raise ValueError(f"unknown infection mode {infection_mode!r}")
+        self.infection_mode = infection_mode
         self.cols, self.disease, self.table, self.iv = cols, disease, table, interventions
         self.seed = seed
         self.clock = 0
@@ -196,9 +224,12 @@ class OracleEngine:
     # engine.py:153-175
     def _transmit(self, graph, ev):
         c, t = self.cols, self.clock
-        lam = self.gather_exposure(graph)
-        p = 1.0 - np.exp(-lam)
-        hit = np.flatnonzero(target_mask(c, self.sterilizing) & (self.u(P_INF, self.everyone) < p))
+        if self.infection_mode == "independent":
+            hit = self._independent_hits(graph)
+        else:
+            lam = self.gather_exposure(graph)
+            p = 1.0 - np.exp(-lam)
+            hit = np.flatnonzero(target_mask(c, self.sterilizing) & (self.u(P_INF, self.everyone) < p))
         if not len(hit):
             return
         entry = pick(self.table.rules[S], c.age_band[hit], self.u(P_ENTRY, hit))
@@ -211,6 +242,19 @@ class OracleEngine:
         c.next_stage[hit] = nxt
         c.next_transition_at[hit] = t + delay
         ev.new_infections = len(hit)
+
+    # oracle.py:185-192 (independent-edges mode): contribution j of target d
+    # infects with its own draw u(seed, t, INFECTION_EDGE, d, k=j) < 1 - exp(-h_j)
+    def _independent_hits(self, graph):
+        c, t = self.cols, self.clock
+        d, _, _, term = edge_terms(c, self.disease, t, graph)
+        if not len(d):
+            return np.empty(0, dtype=np.int64)
+        first = np.searchsorted(d, d, side="left")
+        j = np.arange(len(d)) - first
+        u = rng_np.uniforms(self.seed, t, P_INF_EDGE, d, np.asarray(j, dtype=np.uint64))
+        hit = np.unique(d[u < 1.0 - np.exp(-term)])
+        return hit[target_mask(c, self.sterilizing)[hit]]
 
     # engine.py:177-200
     def _progress(self, ev):

@@ -95,6 +95,7 @@ _SIGS = {
     "epi_set_rows": (_i32, [_p, _i64, _i64]),
     "epi_set_hot_window": (_i32, [_p, _p, _i64]),
     "epi_set_exchange": (_i32, [_p, XFN, _p]),
+    "epi_set_infection_mode": (_i32, [_p, _i32]),
     "epi_pop_synthesize": (_i32, [C.POINTER(EpiPopSpec), _u64, C.POINTER(EpiPopOut), _p]),
     "epi_set_push_max": (_i32, [_p, _i64]),
     "epi_last_error": (C.c_char_p, []),

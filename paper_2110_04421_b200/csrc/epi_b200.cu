@@ -119,6 +119,7 @@ struct epi_ctx {
   epi_exchange_fn xfn = nullptr;     // cross-rank exchange of a partitioned run
   void* xuser = nullptr;
   int push_max = -1;                 // push tables up to this many agents (-1: by L2 size)
+  int indep = 0;                     // graph-in fp64: independent-edges infection draws
   epi_params host{};
   epi_params* P = nullptr;           // device copy
   int64_t n = 0;
@@ -198,6 +199,7 @@ StepArgs make_args(epi_ctx* c, const epi_state* st, int step, uint64_t seed, lon
   A.flags = with_flags ? c->flags : nullptr;
   A.lo = c->lo;
   A.hi = c->hi;
+  A.indep = c->indep;
   return A;
 }
 
@@ -779,6 +781,13 @@ int epi_set_hot_window(epi_ctx* c, const void* base, int64_t bytes) {
   c->hot.base = base;
   c->hot.bytes = win;
   c->hot.hit_ratio = (float)((double)want / (double)win);
+  return 0;
+}
+
+int epi_set_infection_mode(epi_ctx* c, int32_t mode) {
+  if (!c || (mode != EPI_INFECT_AGGREGATE && mode != EPI_INFECT_INDEPENDENT))
+    return fail(EPI_EARG, "infection mode must be EPI_INFECT_AGGREGATE or EPI_INFECT_INDEPENDENT");
+  c->indep = mode == EPI_INFECT_INDEPENDENT;
   return 0;
 }
 

@@ -26,7 +26,7 @@ enum StageId : int {
 
 // Purpose tags (rng.py:37-57 + config-network tags of keyed.py).
 enum PurposeId : int {
-  P_INFECTION = 1, P_ENTRY = 3, P_BRANCH = 4, P_DELAY = 5, P_TEST_POS = 6,
+  P_INFECTION = 1, P_INFECTION_EDGE = 2, P_ENTRY = 3, P_BRANCH = 4, P_DELAY = 5, P_TEST_POS = 6,
   P_TEST_TURN = 7, P_QDROP = 8, P_DEN = 9, P_APP = 10, P_VAX = 11,
   P_NET_RCOUNT = 72, P_NET_RPERM = 73, P_NET_WPERM = 74, P_NET_WSHIFT = 75
 };

@@ -83,6 +83,7 @@ struct StepArgs {
   long long* rec;             // EPI_REC_LEN
   uint8_t* flags;             // per agent scratch
   int64_t lo, hi;             // owned agent rows [lo, hi) (partitioned runs)
+  int indep;                  // independent-edges infection (oracle.py:185-192)
 };
 
 // Shared tables for the fp32 message: factor[t | asym<<7] = rate*A*w[t],
@@ -159,7 +160,10 @@ __device__ __forceinline__ bool is_target(const epi_params* __restrict__ P, cons
 // ---------------------------------------------------------------------------
 // Phases 1-2 for one agent (engine.py:153-200).  Returns event bits:
 // 1 new infection, 2 death, 4 hospitalisation, 8 newly symptomatic.
-__device__ __forceinline__ unsigned transmit_progress(const StepArgs& A, int64_t a, double lam) {
+// `forced` >= 0: the infection decision was already drawn per edge
+// (independent-edges mode) and replaces the aggregate draw.
+__device__ __forceinline__ unsigned transmit_progress(const StepArgs& A, int64_t a, double lam,
+                                                      int forced = -1) {
   const epi_params* __restrict__ P = A.P;
   const epi_state& st = A.st;
   const int step = A.step;
@@ -169,8 +173,14 @@ __device__ __forceinline__ unsigned transmit_progress(const StepArgs& A, int64_t
   int age = -1;
   if (stage == S_SUS && !(P->sterilizing && st.immune[a])) {
     // lam == 0 gives p == 0 and u < p never holds: skip the draw
-    const double p = 1.0 - exp(-lam);
-    if (lam > 0.0 && draw(A.K, A.inj, P_INFECTION, a) < p) {
+    bool infect;
+    if (forced >= 0) {
+      infect = forced != 0;
+    } else {
+      const double p = 1.0 - exp(-lam);
+      infect = lam > 0.0 && draw(A.K, A.inj, P_INFECTION, a) < p;
+    }
+    if (infect) {
       age = st.age_band[a];
       int entry = P->targets[S_SUS][pick_branch(P, S_SUS, age, draw(A.K, A.inj, P_ENTRY, a))];
       if (!P->sterilizing && st.immune[a]) entry = S_ASYM;
@@ -335,6 +345,7 @@ __global__ void __launch_bounds__(256) k_pass(StepArgs A, CsrView g, const uint1
     const bool valid = a < n;
     double lam = 0.0;
     unsigned edges = 0;
+    int forced = -1;
     if (F64) {
       // one lane per row, sequential in canonical order
       if (valid) {
@@ -343,13 +354,29 @@ __global__ void __launch_bounds__(256) k_pass(StepArgs A, CsrView g, const uint1
         if (is_target(P, A.st, a)) {
           const double rate_s = __dmul_rn(rate, P->age_susceptibility[A.st.age_band[a]]);
           const uint32_t* e = g.entries + g.begin(a);
-          double h = 0.0;
-          for (int i = 0; i < len; ++i) {
-            const uint32_t x = e[i];
-            const uint16_t c = codes[x >> 2];
-            if (c & CODE_T_MASK) h = __dadd_rn(h, term_f64(P, rate_s, c, (int)(x & 3)));
+          if (MODE == 1 && A.indep) {
+            // independent edges: contribution j (nonzero, canonical order) infects
+            // with u(INFECTION_EDGE, a, k=j) < 1 - exp(-h_j)
+            int j = 0;
+            forced = 0;
+            for (int i = 0; i < len; ++i) {
+              const uint32_t x = e[i];
+              const uint16_t c = codes[x >> 2];
+              if (!(c & CODE_T_MASK)) continue;
+              const double h = term_f64(P, rate_s, c, (int)(x & 3));
+              if (h == 0.0) continue;
+              if (keyed_u(A.K.p[P_INFECTION_EDGE], (uint64_t)a, (uint64_t)j) < 1.0 - exp(-h)) forced = 1;
+              ++j;
+            }
+          } else {
+            double h = 0.0;
+            for (int i = 0; i < len; ++i) {
+              const uint32_t x = e[i];
+              const uint16_t c = codes[x >> 2];
+              if (c & CODE_T_MASK) h = __dadd_rn(h, term_f64(P, rate_s, c, (int)(x & 3)));
+            }
+            lam = h;
           }
-          lam = h;
         }
       }
     } else {
@@ -398,7 +425,7 @@ __global__ void __launch_bounds__(256) k_pass(StepArgs A, CsrView g, const uint1
     }
     // MODE 1: fused update for this lane's agent
     unsigned ev = 0;
-    if (valid) ev = transmit_progress(A, a, lam);
+    if (valid) ev = transmit_progress(A, a, lam, forced);
     if (valid && (ev & 8u) && A.flags) A.flags[a] = FL_SYMPTOMATIC;
     rec_events(racc, ev);
     rec_add(racc, EPI_REC_EDGES, edges);

@@ -69,7 +69,8 @@ class GpuEngine:
     """Single-writer columnar engine for one replication, on one GPU."""
 
     def __init__(self, cols, disease, table, interventions, seed: int,
-                 check_invariants: bool = True, resident: bool = False, device=None):
+                 check_invariants: bool = True, resident: bool = False, device=None,
+                 infection_mode: str = "aggregate"):
         import torch
         self._lib = N.lib()
         self.cols = cols
@@ -89,6 +90,13 @@ class GpuEngine:
         ctx = N._p()
         N.check(self._lib.epi_create(C_ref(self._params), self.n, C_ref(ctx)))
         self._ctx = ctx
+        # "independent": the reference oracle's independent-edges mode
+        # (oracle.py:185-192), validation only
+        modes = {"aggregate": 0, "independent": 1}
+        if infection_mode not in modes:
+            from .errors import ConfigError
+            raise ConfigError(f"unknown infection mode {infection_mode!r}")
+        N.check(self._lib.epi_set_infection_mode(self._ctx, modes[infection_mode]))
         self.dev = DeviceColumns.from_host(cols, self.device)
         self._vax = torch.zeros(1, dtype=torch.int32, device=self.device)
         self._rec = torch.zeros(N.REC_LEN, dtype=torch.int64, device=self.device)

@@ -3,6 +3,7 @@
 Run in the build container only (needs /root/reference):
 
     PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py independent   (row f4 fixtures)
 
 Writes small .npz fixtures next to this script.  The GPU box never reads
 /root/reference; tests load these fixtures instead.
@@ -124,6 +125,40 @@ def trajectory_fixture(name, n, horizon, seed, interventions, infections=8, reco
         **init, **{f"state_{c}": np.stack(v) for c, v in states.items()}, **hz)
 
 
+def independent_fixture(name, n, horizon, seed, interventions, infections=8):
+    """The reference's naive oracle in independent-edges mode (oracle.py:185-192:
+    one Bernoulli per incident edge, keyed INFECTION_EDGE draws k = j over the
+    sorted contributions), on its own reference-realizer graphs."""
+    from epivec.oracle import OracleSim, agents_from_columns
+    pop = default_population_dict()
+    pop["n_agents"] = n
+    cfg = scenario_from_dict({"population": pop, "horizon": horizon, "replications": 1,
+                              "base_seed": seed, "initial_infections": infections,
+                              "interventions": interventions}, name=name)
+    rseed = replication_seed(cfg.base_seed, 0)
+    cols, realizer = initialize_run(cfg, rseed)
+    init = {f"init_{c}": getattr(cols, c).copy() for c in ALL_COLS}
+    sim = OracleSim(agents_from_columns(cols), cfg.disease, cfg.progression, cfg.interventions,
+                    rseed, mode=OracleSim.INDEPENDENT)
+    srcs, dsts, kinds, states = [], [], [], {c: [] for c in DYNAMIC_COLUMNS}
+    for step in range(horizon):
+        g = realizer.realize(step, sim.column("stage") == 10)
+        sim.step(g)
+        srcs.append(g.src); dsts.append(g.dst); kinds.append(g.kind)
+        for c in DYNAMIC_COLUMNS:
+            states[c].append(sim.column(c).astype(getattr(cols, c).dtype))
+    offs = np.concatenate(([0], np.cumsum([len(s) for s in srcs])))
+    np.savez_compressed(
+        OUT / f"traj_{name}.npz", seed=np.uint64(rseed), horizon=horizon,
+        edge_offsets=offs, src=np.concatenate(srcs), dst=np.concatenate(dsts),
+        kind=np.concatenate(kinds), events=np.zeros((horizon, 7), dtype=np.int64),
+        disease_json=json.dumps(default_disease_dict()),
+        table_json=json.dumps(default_progression_dict()),
+        iv_json=json.dumps(_iv_dict(cfg.interventions)),
+        vaccination_open=sim.vaccination_open,
+        **init, **{f"state_{c}": np.stack(v) for c, v in states.items()})
+
+
 ALL_IV = {
     "quarantine": {"enabled": True, "dropout_prob": 0.05},
     "testing": {"enabled": True, "kind": "rt-pcr"},
@@ -149,6 +184,10 @@ STD_IV = {
 
 
 if __name__ == "__main__":
+    if sys.argv[1:] == ["independent"]:
+        independent_fixture("indep_noiv", 800, 45, 21, {}, infections=20)
+        independent_fixture("indep_alliv", 300, 30, 4, ALL_IV, infections=8)
+        sys.exit(0)
     rng_fixture()
     progression_fixture()
     priority_fixture()

@@ -150,3 +150,17 @@ def test_star_graph_gather_equals_formula():
     h = eng.gather_exposure(g)
     assert np.all(h[1:] == edge_hazard(4, False, 0, 2, tr.disease))
     assert h[0] == 0.0
+
+
+@pytest.mark.parametrize("name", ["indep_noiv", "indep_alliv"])
+def test_engine_independent_edges_mode_replays_reference_oracle(name):
+    """Row f4: GpuEngine in the reference oracle's independent-edges mode
+    (oracle.py:185-192) replays the recorded reference trajectory bitwise."""
+    from golden_io import compare_state
+    from paper_2110_04421_b200.engine import GpuEngine
+    tr = Trajectory(name)
+    cols = tr.initial_cols()
+    eng = GpuEngine(cols, tr.disease, tr.table, tr.iv, tr.seed, infection_mode="independent")
+    for step in range(tr.horizon):
+        eng.step(tr.graph(step))
+        compare_state(cols, tr, step)

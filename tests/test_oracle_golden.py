@@ -132,3 +132,17 @@ def test_reference_realizer_restatement_reproduces_recorded_graphs(name):
         s, d, k = rr.realize(step, dead)
         g = tr.graph(step)
         assert np.array_equal(s, g.src) and np.array_equal(d, g.dst) and np.array_equal(k, g.kind)
+
+
+@pytest.mark.parametrize("name", ["indep_noiv", "indep_alliv"])
+def test_oracle_independent_edges_mode_replays_reference(name):
+    """Row f4: the reference's naive oracle in independent-edges mode
+    (oracle.py:185-192), recorded by make_golden.py, replayed bitwise."""
+    tr = Trajectory(name)
+    cols = tr.initial_cols()
+    eng = engine_np.OracleEngine(cols, tr.disease, tr.table, tr.iv, tr.seed,
+                                 infection_mode="independent")
+    for step in range(tr.horizon):
+        eng.step(tr.graph(step))
+        compare_state(cols, tr, step)
+    assert int(np.sum(cols.infected_at != -1)) > int(np.sum(tr.z["init_infected_at"] != -1))
