@@ -974,7 +974,7 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
     }
     CK(launch_pdl_w(&c->hot, k_fused_step, dim3(fgrid), dim3(128), 0, s, A, c->net, nk, codes_cur,
                   c->host.rate_scale, codes_next, (const epi_net*)c->net_dev, rcount_next, iv ? 0 : 1, wt,
-                  (const MsgTables*)c->msg_dev, (const NetTables*)nt_today, nx));
+                  (const MsgTables*)c->msg_dev, (const NetTables*)nt_today, nx, push_rand ? 1 : 0));
     c->merged_ready = merged ? step + 1 : -1;
   }
   if (ev) CK(cudaEventRecord((cudaEvent_t)ev[2], s));

@@ -624,7 +624,8 @@ __global__ void __launch_bounds__(128, 6) k_fused_step(StepArgs A, epi_net net, 
                                                     const epi_net* net_dev, uint64_t rcount_next,
                                                     int final_pass, const WorkTables* wt,
                                                     const MsgTables* __restrict__ mt,
-                                                    const NetTables* __restrict__ NTp, NextTables nx) {
+                                                    const NetTables* __restrict__ NTp, NextTables nx,
+                                                    int push) {
   __shared__ MsgTables T;
   __shared__ NetTables NT;
   __shared__ RecAcc racc;
@@ -632,7 +633,14 @@ __global__ void __launch_bounds__(128, 6) k_fused_step(StepArgs A, epi_net net, 
   __shared__ int excl_s[4][32];
   __shared__ uint16_t cn_s[4][32];
   load_msg_tables(T, mt);
-  load_net_tables(NT, NTp);
+  // with the day's push tables (random rows + workplace codes) only the agent
+  // domain is needed; the epilogue derives workplace domains on the fly
+  if (push) {
+    if (threadIdx.x < (int)(sizeof(Radix) / 4))
+      ((uint32_t*)&NT.dn)[threadIdx.x] = ((const uint32_t*)&NTp->dn)[threadIdx.x];
+  } else {
+    load_net_tables(NT, NTp);
+  }
   rec_init(racc);
   __syncthreads();
   pdl_wait();
@@ -656,12 +664,15 @@ __global__ void __launch_bounds__(128, 6) k_fused_step(StepArgs A, epi_net net, 
     if (valid) {
       const uint16_t cb = codes[b];
       if (!code_dead(cb)) {
-        float acc = 0.f;
+        // one sum per network kind (the kind is a constant at every visit),
+        // scaled by B[kind] once
+        float acc[3] = {0.f, 0.f, 0.f};
         for_each_in_code(net, nk, NT.rk, NT.wrad, dn, wt, codes, b, cb, [&](int kind, uint16_t cc) {
           ++edges;
-          acc += T.factor[cc & 0xFF] * T.bfac[kind];
+          acc[kind] += T.factor[cc & 0xFF];
         });
-        if (is_target(A.P, A.st, b)) lam = (double)(acc * T.sfac[A.st.age_band[b]]);
+        const float tot = acc[0] * T.bfac[0] + acc[1] * T.bfac[1] + acc[2] * T.bfac[2];
+        if (is_target(A.P, A.st, b)) lam = (double)(tot * T.sfac[A.st.age_band[b]]);
       }
       clear_rin_row(wt, b);
     }
@@ -686,7 +697,8 @@ __global__ void __launch_bounds__(128, 6) k_fused_step(StepArgs A, epi_net net, 
           if (m >= 2) {
             const int wbase = net.wp_base[w];
             const int loc = net.wp_local[b];
-            const uint32_t q = walk_inv((uint32_t)loc, work_keys(nx.nk.wperm, w), NT.wrad[m]);
+            const uint32_t q = walk_inv((uint32_t)loc, work_keys(nx.nk.wperm, w),
+                                        push ? make_radix((uint32_t)m) : NT.wrad[m]);
             W.pos_of[wbase + loc] = (uint8_t)q;
             W.wcode[wbase + q] = cn;
             for (int j = loc; j < net.colleague_draws; j += m)
