@@ -313,8 +313,18 @@ def run_ours(a):
     # --- per-kernel device times (instrumented, same inputs) -> roofline
     profs = {r["mode"]: kernel_profile(r["sims"][a.warmup], r["mode"]) for r in results}
     prof = profs[best["mode"]]
-    # --- end to end through the public API from pinned host buffers
+    # --- end to end through the public API from pinned host buffers (every
+    # rank; whole-job value = summed edges / max time over the ranks)
     e2e = end_to_end(make(best["mode"], 0), a)
+    if dist:
+        t = torch.tensor([e2e["ms_per_step"], e2e["edges_per_step"]], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t[:1], op=dist.ReduceOp.MAX)
+        dist.all_reduce(t[1:])
+        e2e["ms_per_step"], e2e["edges_per_step"] = float(t[0]), float(t[1])
+        e2e["value"] = e2e["edges_per_step"] / (e2e["ms_per_step"] / 1000.0)
+        e2e["h2d_bytes_per_step"] *= world
+        e2e["d2h_bytes_per_step"] *= world
+    e2e.pop("edges_per_step")
 
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) \
         if (ROOT / "MEASURED_PEAKS.json").exists() else {}
@@ -470,7 +480,8 @@ def end_to_end(sim, a):
     ms = st.elapsed_time(en) / a.steps
     edges = float(sim.records()[:, 19].sum())
     return {"value": edges / (ms / 1000.0), "unit": "agent-interactions/s",
-            "ms_per_step": ms, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h}
+            "ms_per_step": ms, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "edges_per_step": edges}
 
 
 def run_config3(a):
