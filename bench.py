@@ -358,6 +358,9 @@ def run_ours(a):
         },
         "wall_s_per_sim": ms_total / a.steps / 1000.0,
         "undirected_contacts_per_s": value / 2,
+        # end-to-end HBM GB/s = algorithmic bytes of all the
+        # day kernels / device time per simulation
+        "hbm_gbs_end_to_end": prof["alg_bytes_per_sim"] / (ms_total / a.steps / 1e3) / 1e9,
         "modes": {r["mode"]: {"ms_per_sim": sum(r["ms"]) / len(r["ms"]),
                               "interactions_per_s": r["edges"] / (sum(r["ms"]) / 1000)}
                   for r in results},
@@ -439,10 +442,12 @@ def kernel_profile(sim, mode):
                                    "alg_GBps": float(np.sum(b) / (sum(pas) / 1e3) / 1e9)}
         dom, byt, ms, launches = "k_fused_step", b * np.ones_like(E), pas, 1
     achieved = float(np.sum(byt) / (sum(ms) / 1e3) / 1e9)
+    sim_bytes = float(np.sum(b_gen) + np.sum(b_pass)) if mode == "csr" else float(np.sum(b * np.ones_like(E)))
     return {"kernels": kernels, "launches_per_sim": launches * sim.horizon + (2 if mode != "csr" else 0),
+            "alg_bytes_per_sim": sim_bytes,
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "unit": "GB/s",
                          "traffic": None,
-                         "bytes_model": "see DESIGN.md §5 (algorithmic bytes per launch)"}}
+                         "bytes_model": "see DESIGN.md §4 (algorithmic bytes per launch)"}}
 
 
 def end_to_end(sim, a):
