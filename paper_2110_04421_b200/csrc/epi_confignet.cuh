@@ -489,4 +489,99 @@ __device__ __forceinline__ void for_each_in_code(const epi_net& net, const NetKe
   }
 }
 
+// Push-table form of for_each_in_code for the fused day kernel, written so
+// that every load of a level is issued before any of them is consumed
+// (memory-level parallelism for the ~21 warps per SM of a 100k-agent day):
+//   level 1: household range, workplace id/slot, rin row, first rout row;
+//   level 2: household codes, workplace size/base/shifts, out-partner codes;
+//   level 3: the worker's position; level 4: the colleagues' codes.
+// The sums are accumulated per kind in exactly the visit order of
+// for_each_in_code (household, workplace out/in per draw, random out, random
+// in), so results are bitwise those of the generic enumerator.
+// Requires the day's push tables (wt->wcode, wt->rin) and <= 8 draws.
+__device__ __forceinline__ void push_kind_sums(const epi_net& net, const WorkTables* __restrict__ wt,
+                                               const uint16_t* __restrict__ codes, int64_t b, uint16_t code_b,
+                                               const float* __restrict__ factor, float acc[3],
+                                               unsigned& edges) {
+  constexpr int HH = 8, DR = 8;
+  // level 1
+  const int off = net.hh_off[b];
+  const int sz = net.hh_size[b];
+  const int w = net.wp_id[b];
+  const int loc = net.wp_local[b];
+  const uint4* ri = (const uint4*)(wt->rin + (size_t)b * RT_SLOTS);
+  const uint4 in0 = ri[0], in1 = ri[1];
+  const uint4* ro = (const uint4*)(wt->rout + (size_t)b * RT_SLOTS);
+  const uint32_t self = (uint32_t)b;
+  const int nb = code_count(code_b);
+  const int nbe = nb < RT_SLOTS ? nb : RT_SLOTS;
+  const uint4 o0 = nbe > 0 ? ro[0] : make_uint4(self, self, self, self);
+  // level 2
+  const int64_t start = b - off;
+  uint16_t hc[HH];
+#pragma unroll
+  for (int i = 0; i < HH; ++i) hc[i] = (i < sz && start + i != b) ? codes[start + i] : (uint16_t)CODE_DEAD;
+  const int draws = net.colleague_draws;
+  int m = 0, base = 0;
+  uint8_t sh[DR];
+  if (w >= 0) {
+    m = net.wp_size[w];
+    base = net.wp_base[w];
+    const uint8_t* shp = wt->shift + (size_t)w * draws;
+#pragma unroll
+    for (int j = 0; j < DR; ++j) sh[j] = j < draws ? shp[j] : (uint8_t)0;
+  }
+  const uint32_t po0[4] = {o0.x, o0.y, o0.z, o0.w};
+  uint16_t co0[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) co0[q] = (q < nbe && po0[q] != self) ? codes[po0[q]] : (uint16_t)CODE_DEAD;
+  // level 3
+  uint32_t p = 0;
+  if (w >= 0 && m >= 2) p = wt->pos_of[base + loc];
+  // level 4
+  uint16_t wo[DR], wi[DR];
+#pragma unroll
+  for (int j = 0; j < DR; ++j) {
+    wo[j] = wi[j] = (uint16_t)CODE_DEAD;
+    if (w >= 0 && m >= 2 && j < draws) {
+      const uint32_t r = sh[j];
+      wo[j] = wt->wcode[base + add_mod(p, r, (uint32_t)m)];
+      wi[j] = wt->wcode[base + sub_mod(p, r, (uint32_t)m)];
+    }
+  }
+  // accumulate in visit order
+#pragma unroll
+  for (int i = 0; i < HH; ++i)
+    if (!code_dead(hc[i])) { acc[0] += factor[hc[i] & 0xFF]; ++edges; }
+  for (int i = HH; i < sz; ++i) {            // households larger than HH (rare)
+    if (start + i == b) continue;
+    const uint16_t cc = codes[start + i];
+    if (!code_dead(cc)) { acc[0] += factor[cc & 0xFF]; ++edges; }
+  }
+#pragma unroll
+  for (int j = 0; j < DR; ++j) {
+    if (!code_dead(wo[j])) { acc[1] += factor[wo[j] & 0xFF]; ++edges; }
+    if (!code_dead(wi[j])) { acc[1] += factor[wi[j] & 0xFF]; ++edges; }
+  }
+  if (net.n_agents < 2) return;
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    if (!code_dead(co0[q])) { acc[2] += factor[co0[q] & 0xFF]; ++edges; }
+  for (int j0 = 4; j0 < nbe; j0 += 4) {       // more than 4 out-partners
+    const uint4 o = ro[j0 >> 2];
+    const uint32_t po[4] = {o.x, o.y, o.z, o.w};
+    uint16_t co[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) co[q] = (j0 + q < nbe && po[q] != self) ? codes[po[q]] : (uint16_t)CODE_DEAD;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (!code_dead(co[q])) { acc[2] += factor[co[q] & 0xFF]; ++edges; }
+  }
+  const uint4 inv[2] = {in0, in1};
+  const uint16_t* iv = (const uint16_t*)inv;
+#pragma unroll
+  for (int j = 0; j < RT_SLOTS; ++j)
+    if (iv[j] & CODE_PRESENT) { acc[2] += factor[iv[j] & 0xFF]; ++edges; }
+}
+
 }  // namespace epi

@@ -667,10 +667,13 @@ __global__ void __launch_bounds__(128, 6) k_fused_step(StepArgs A, epi_net net, 
         // one sum per network kind (the kind is a constant at every visit),
         // scaled by B[kind] once
         float acc[3] = {0.f, 0.f, 0.f};
-        for_each_in_code(net, nk, NT.rk, NT.wrad, dn, wt, codes, b, cb, [&](int kind, uint16_t cc) {
-          ++edges;
-          acc[kind] += T.factor[cc & 0xFF];
-        });
+        if (push)
+          push_kind_sums(net, wt, codes, b, cb, T.factor, acc, edges);
+        else
+          for_each_in_code(net, nk, NT.rk, NT.wrad, dn, wt, codes, b, cb, [&](int kind, uint16_t cc) {
+            ++edges;
+            acc[kind] += T.factor[cc & 0xFF];
+          });
         const float tot = acc[0] * T.bfac[0] + acc[1] * T.bfac[1] + acc[2] * T.bfac[2];
         if (is_target(A.P, A.st, b)) lam = (double)(tot * T.sfac[A.st.age_band[b]]);
       }
