@@ -160,18 +160,34 @@ __device__ __forceinline__ bool is_target(const epi_params* __restrict__ P, cons
 // ---------------------------------------------------------------------------
 // Phases 1-2 for one agent (engine.py:153-200).  Returns event bits:
 // 1 new infection, 2 death, 4 hospitalisation, 8 newly symptomatic.
+// The state fields of one agent that phases 1-2 and the next code read,
+// loaded once (the fused day kernel issues these loads before its gather).
+struct AgentHot {
+  int stage, immune, age, next_stage;
+  int32_t nta, infected_at, q_until;
+};
+__device__ __forceinline__ AgentHot load_hot(const epi_state& st, int64_t a) {
+  AgentHot h;
+  h.stage = st.stage[a];
+  h.immune = st.immune[a];
+  h.age = st.age_band[a];
+  h.next_stage = st.next_stage[a];
+  h.nta = st.next_transition_at[a];
+  h.infected_at = st.infected_at[a];
+  h.q_until = st.quarantine_until[a];
+  return h;
+}
+
+// Phases 1-2 on preloaded state (updated in place, and written through).
 // `forced` >= 0: the infection decision was already drawn per edge
 // (independent-edges mode) and replaces the aggregate draw.
-__device__ __forceinline__ unsigned transmit_progress(const StepArgs& A, int64_t a, double lam,
-                                                      int forced = -1) {
+__device__ __forceinline__ unsigned transmit_progress_hot(const StepArgs& A, int64_t a, double lam, int forced,
+                                                          AgentHot& h) {
   const epi_params* __restrict__ P = A.P;
   const epi_state& st = A.st;
   const int step = A.step;
   unsigned ev = 0;
-  int stage = st.stage[a];
-  int32_t nta = st.next_transition_at[a];
-  int age = -1;
-  if (stage == S_SUS && !(P->sterilizing && st.immune[a])) {
+  if (h.stage == S_SUS && !(P->sterilizing && h.immune)) {
     // lam == 0 gives p == 0 and u < p never holds: skip the draw
     bool infect;
     if (forced >= 0) {
@@ -181,43 +197,65 @@ __device__ __forceinline__ unsigned transmit_progress(const StepArgs& A, int64_t
       infect = lam > 0.0 && draw(A.K, A.inj, P_INFECTION, a) < p;
     }
     if (infect) {
-      age = st.age_band[a];
-      int entry = P->targets[S_SUS][pick_branch(P, S_SUS, age, draw(A.K, A.inj, P_ENTRY, a))];
-      if (!P->sterilizing && st.immune[a]) entry = S_ASYM;
+      int entry = P->targets[S_SUS][pick_branch(P, S_SUS, h.age, draw(A.K, A.inj, P_ENTRY, a))];
+      if (!P->sterilizing && h.immune) entry = S_ASYM;
       int nxt, delay;
-      schedule(P, entry, age, draw(A.K, A.inj, P_BRANCH, a), draw(A.K, A.inj, P_DELAY, a), nxt, delay);
+      schedule(P, entry, h.age, draw(A.K, A.inj, P_BRANCH, a), draw(A.K, A.inj, P_DELAY, a), nxt, delay);
+      h.stage = entry;
+      h.infected_at = step;
+      h.next_stage = nxt;
+      h.nta = step + delay;
       st.stage[a] = (int8_t)entry;
       st.infected_at[a] = step;
       st.next_stage[a] = (int8_t)nxt;
-      nta = step + delay;
-      st.next_transition_at[a] = nta;
+      st.next_transition_at[a] = h.nta;
       ev |= 1u;
     }
   }
-  if (nta == step) {
-    if (age < 0) age = st.age_band[a];
-    const int dest = st.next_stage[a];
+  if (h.nta == step) {
+    const int dest = h.next_stage;
+    h.stage = dest;
     st.stage[a] = (int8_t)dest;
     if (dest == S_DEAD) ev |= 2u;
     if (dest == S_HOSP) ev |= 4u;
     if (dest == S_MILD || dest == S_SEV) ev |= 8u;
     if (dest == S_REC || dest == S_DEAD) {
-      st.next_stage[a] = NEVER8;
-      st.next_transition_at[a] = NEVER;
+      h.next_stage = NEVER8;
+      h.nta = NEVER;
     } else {
       int nxt, delay;
-      schedule(P, dest, age, draw(A.K, A.inj, P_BRANCH, a), draw(A.K, A.inj, P_DELAY, a), nxt, delay);
-      st.next_stage[a] = (int8_t)nxt;
-      st.next_transition_at[a] = step + delay;
+      schedule(P, dest, h.age, draw(A.K, A.inj, P_BRANCH, a), draw(A.K, A.inj, P_DELAY, a), nxt, delay);
+      h.next_stage = nxt;
+      h.nta = step + delay;
     }
+    st.next_stage[a] = (int8_t)h.next_stage;
+    st.next_transition_at[a] = h.nta;
   }
   return ev;
+}
+
+__device__ __forceinline__ unsigned transmit_progress(const StepArgs& A, int64_t a, double lam,
+                                                      int forced = -1) {
+  AgentHot h = load_hot(A.st, a);
+  return transmit_progress_hot(A, a, lam, forced, h);
 }
 
 __device__ __forceinline__ void rec_events(RecAcc& s, unsigned ev) {
   rec_add(s, EPI_REC_NEW_INF, ev & 1u);
   rec_add(s, EPI_REC_DEATHS, (ev >> 1) & 1u);
   rec_add(s, EPI_REC_HOSP, (ev >> 2) & 1u);
+}
+
+// Next-step source code from preloaded (post-update) state.
+__device__ __forceinline__ uint16_t next_code_hot(const epi_params* __restrict__ P, const AgentHot& h, int64_t a,
+                                                  int next_step, const epi_net* net, uint64_t rcount_prefix) {
+  uint16_t c = source_code(P, h.stage, h.infected_at, h.q_until, next_step);
+  if (h.stage == S_DEAD) {
+    c |= CODE_DEAD;
+  } else if (net != nullptr) {
+    c |= (uint16_t)(random_count(*net, rcount_prefix, a) << 8);
+  }
+  return c;
 }
 
 // Next-step source code of agent a (after every phase of `step`).
@@ -661,6 +699,8 @@ __global__ void __launch_bounds__(128, 6) k_fused_step(StepArgs A, epi_net net, 
     const bool valid = b < n;
     unsigned edges = 0;
     double lam = 0.0;
+    AgentHot h{};
+    if (valid) h = load_hot(A.st, b);      // issued before the gather's loads
     if (valid) {
       const uint16_t cb = codes[b];
       if (!code_dead(cb)) {
@@ -675,20 +715,20 @@ __global__ void __launch_bounds__(128, 6) k_fused_step(StepArgs A, epi_net net, 
             acc[kind] += T.factor[cc & 0xFF];
           });
         const float tot = acc[0] * T.bfac[0] + acc[1] * T.bfac[1] + acc[2] * T.bfac[2];
-        if (is_target(A.P, A.st, b)) lam = (double)(tot * T.sfac[A.st.age_band[b]]);
+        if (h.stage == S_SUS && !(A.P->sterilizing && h.immune)) lam = (double)(tot * T.sfac[h.age]);
       }
       clear_rin_row(wt, b);
     }
     unsigned ev = 0;
-    if (valid) ev = transmit_progress(A, b, lam);
+    if (valid) ev = transmit_progress_hot(A, b, lam, -1, h);
     if (valid && (ev & 8u) && A.flags) A.flags[b] = FL_SYMPTOMATIC;
     rec_events(racc, ev);
     rec_add(racc, EPI_REC_EDGES, edges);
     if (final_pass) {
-      rec_agent(racc, valid, valid ? A.st.stage[b] : 0, valid ? A.st.infected_at[b] : 0);
+      rec_agent(racc, valid, valid ? h.stage : 0, valid ? h.infected_at : 0);
       uint16_t cn = 0;
       if (valid) {
-        cn = next_code(A.P, A.st, b, A.step + 1, net_dev, rcount_next);
+        cn = next_code_hot(A.P, h, b, A.step + 1, net_dev, rcount_next);
         codes_next[b] = cn;
       }
       if (merge) {
