@@ -156,7 +156,8 @@ struct epi_ctx {
   std::vector<int32_t*> net_rowlen;
   std::vector<int32_t> net_slot_step;
   MsgTables* msg_dev = nullptr;      // fp32 message tables (rate_scale baked in)
-  MsgComb* comb_dev = nullptr;       // fp64 weights of the pre-joined messages
+  MsgComb* comb_dev = nullptr;       // weights of the pre-joined messages
+  uint16_t* tau_lut = nullptr;       // bucket table of delay_steps
   NetTables ntab{};                  // host copy (static radix tables)
   NetTables* ntab_dev[3] = {nullptr, nullptr, nullptr};   // per-day keys, by step % 3
   WorkTables wt_host[2]{};           // day tables by step parity (member_at_pos shared)
@@ -180,10 +181,14 @@ int upload_params(epi_ctx* c, const epi_params* p) {
   fill_msg_tables(mt, *p, p->rate_scale);
   if (!c->msg_dev) CK(cudaMalloc((void**)&c->msg_dev, sizeof(MsgTables)));
   CK(cudaMemcpy(c->msg_dev, &mt, sizeof(MsgTables), cudaMemcpyHostToDevice));
-  static MsgComb mc;   // 8 KB: not on the stack
+  static MsgComb mc;   // 4 KB: not on the stack
   fill_msg_comb(mc, *p, p->rate_scale);
   if (!c->comb_dev) CK(cudaMalloc((void**)&c->comb_dev, sizeof(MsgComb)));
   CK(cudaMemcpy(c->comb_dev, &mc, sizeof(MsgComb), cudaMemcpyHostToDevice));
+  std::vector<uint16_t> lut((size_t)EPI_MAX_SPECS * TAU_LUT);
+  fill_tau_lut(lut.data(), *p);
+  if (!c->tau_lut) CK(cudaMalloc((void**)&c->tau_lut, lut.size() * sizeof(uint16_t)));
+  CK(cudaMemcpy(c->tau_lut, lut.data(), lut.size() * sizeof(uint16_t), cudaMemcpyHostToDevice));
   return 0;
 }
 
@@ -200,6 +205,7 @@ StepArgs make_args(epi_ctx* c, const epi_state* st, int step, uint64_t seed, lon
   A.lo = c->lo;
   A.hi = c->hi;
   A.indep = c->indep;
+  A.tau_lut = c->tau_lut;
   return A;
 }
 
@@ -392,6 +398,7 @@ int epi_destroy(epi_ctx* c) {
   cudaFree(c->inj_dev);
   cudaFree(c->msg_dev);
   cudaFree(c->comb_dev);
+  cudaFree(c->tau_lut);
   for (auto* p : c->ntab_dev) cudaFree(p);
   cudaFree(c->wt_host[0].member_at_pos);
   for (auto& w : c->wt_host) {

@@ -91,9 +91,22 @@ __device__ __forceinline__ int pick_branch(const epi_params* __restrict__ P, int
 }
 
 // delay = 1 + #(tau <= u): exact encoding of max(rint(ppf(u)), 1)
-__device__ __forceinline__ int delay_steps(const epi_params* __restrict__ P, int spec, double u) {
+//
+// With `lut` (TAU_LUT entries per spec: lut[k] = #(tau < k / TAU_LUT)) the
+// count starts at the bucket of u and steps over the few thresholds inside
+// the bucket: two dependent loads instead of a log2(len)-deep binary search.
+// Both give the same count: #(tau < floor(u*L)/L) <= #(tau <= u).
+constexpr int TAU_LUT = 1024;
+__device__ __forceinline__ int delay_steps(const epi_params* __restrict__ P, int spec, double u,
+                                           const uint16_t* __restrict__ lut = nullptr) {
   const double* tau = P->tau[spec];
-  int lo = 0, hi = P->tau_len[spec];
+  const int len = P->tau_len[spec];
+  if (lut != nullptr) {
+    int lo = lut[spec * TAU_LUT + (int)(u * TAU_LUT)];
+    while (lo < len && tau[lo] <= u) ++lo;
+    return 1 + lo;
+  }
+  int lo = 0, hi = len;
   while (lo < hi) {
     const int mid = (lo + hi) >> 1;
     if (tau[mid] <= u) lo = mid + 1; else hi = mid;
@@ -104,13 +117,26 @@ __device__ __forceinline__ int delay_steps(const epi_params* __restrict__ P, int
 // (next_stage, delay) out of `stage`; absorbing / entry stages give
 // (NEVER, NEVER) like progression.py:137-162.
 __device__ __forceinline__ void schedule(const epi_params* __restrict__ P, int stage, int age,
-                                         double ub, double ud, int& next, int& delay) {
+                                         double ub, double ud, int& next, int& delay,
+                                         const uint16_t* __restrict__ lut = nullptr) {
   if (stage == S_SUS || stage > 10 || stage < 0 || P->n_targets[stage] == 0) {
     next = NEVER; delay = NEVER; return;
   }
   const int j = pick_branch(P, stage, age, ub);
   next = P->targets[stage][j];
-  delay = delay_steps(P, P->spec_of[stage][j], ud);
+  delay = delay_steps(P, P->spec_of[stage][j], ud, lut);
+}
+
+// Host: the bucket table of delay_steps (spec-major, TAU_LUT per spec).
+inline void fill_tau_lut(uint16_t* lut, const epi_params& p) {
+  for (int s = 0; s < EPI_MAX_SPECS; ++s) {
+    int c = 0;
+    for (int k = 0; k < TAU_LUT; ++k) {
+      const double edge = (double)k / TAU_LUT;
+      while (s < p.n_specs && c < p.tau_len[s] && p.tau[s][c] < edge) ++c;
+      lut[s * TAU_LUT + k] = (uint16_t)c;
+    }
+  }
 }
 
 // ---- source codes ---------------------------------------------------------

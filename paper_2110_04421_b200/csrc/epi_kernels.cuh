@@ -84,6 +84,7 @@ struct StepArgs {
   uint8_t* flags;             // per agent scratch
   int64_t lo, hi;             // owned agent rows [lo, hi) (partitioned runs)
   int indep;                  // independent-edges infection (oracle.py:185-192)
+  const uint16_t* tau_lut;    // bucket table of delay_steps (or null: binary search)
 };
 
 // Shared tables for the fp32 message: factor[t | asym<<7] = rate*A*w[t],
@@ -200,7 +201,8 @@ __device__ __forceinline__ unsigned transmit_progress_hot(const StepArgs& A, int
       int entry = P->targets[S_SUS][pick_branch(P, S_SUS, h.age, draw(A.K, A.inj, P_ENTRY, a))];
       if (!P->sterilizing && h.immune) entry = S_ASYM;
       int nxt, delay;
-      schedule(P, entry, h.age, draw(A.K, A.inj, P_BRANCH, a), draw(A.K, A.inj, P_DELAY, a), nxt, delay);
+      schedule(P, entry, h.age, draw(A.K, A.inj, P_BRANCH, a), draw(A.K, A.inj, P_DELAY, a), nxt, delay,
+               A.tau_lut);
       h.stage = entry;
       h.infected_at = step;
       h.next_stage = nxt;
@@ -224,7 +226,8 @@ __device__ __forceinline__ unsigned transmit_progress_hot(const StepArgs& A, int
       h.nta = NEVER;
     } else {
       int nxt, delay;
-      schedule(P, dest, h.age, draw(A.K, A.inj, P_BRANCH, a), draw(A.K, A.inj, P_DELAY, a), nxt, delay);
+      schedule(P, dest, h.age, draw(A.K, A.inj, P_BRANCH, a), draw(A.K, A.inj, P_DELAY, a), nxt, delay,
+               A.tau_lut);
       h.next_stage = nxt;
       h.nta = step + delay;
     }
