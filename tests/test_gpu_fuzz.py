@@ -135,3 +135,37 @@ def test_generator_fuzz_bitwise(seed):
     g = sim.realize_graph(0).sorted_canonical()
     src, dst, kind = confignet_np.realize(pop, sim.seed, 0, dead)
     assert np.array_equal(g.dst, dst) and np.array_equal(g.src, src) and np.array_equal(g.kind, kind)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_message_pass_fuzz_within_1e5(seed):
+    """North-star part (a) on random network specs (row layouts from empty to
+    ~80 messages, ragged N, states reached by random numbers of fused days):
+    the fp32 message pass vs the oracle hazard on the restated graph."""
+    import torch
+    from paper_2110_04421_b200 import roofline
+    from paper_2110_04421_b200.graph import StepGraph
+    rng = np.random.default_rng(500 + seed)
+    hh = tuple(sorted(set(int(x) for x in rng.integers(1, 33, 3))))
+    probs = rng.dirichlet(np.ones(len(hh)))
+    spec = ConfigNetworkSpec(
+        n_agents=int(rng.choice([33, 500, 3001, 7777])),
+        household_sizes=hh, household_probs=tuple(float(p) for p in probs / probs.sum()),
+        worker_bands=tuple(int(b) for b in rng.choice(9, int(rng.integers(0, 9)), replace=False)),
+        wp_min=int(rng.integers(2, 20)), wp_max=int(rng.integers(20, 255)),
+        colleague_draws=int(rng.choice([0, 1, 4, 8])),
+        random_mean=float(rng.uniform(0, 12)), random_slots=int(rng.choice([0, 1, 8, 16])),
+        initial_infections=int(rng.integers(1, 30)))
+    sim = roofline.prepare(spec.n_agents, warm_days=int(rng.integers(1, 12)), spec=spec)
+    t = sim.clock
+    lam = torch.empty(spec.n_agents, dtype=torch.float32, device="cuda")
+    rec = torch.zeros(24, dtype=torch.int64, device="cuda")
+    roofline.gather(sim, lam, rec)
+    cols = sim.host_columns()
+    src, dst, kind = confignet_np.realize(sim.population, sim.seed, t, cols.stage == 10)
+    ref = engine_np.hazard(cols, sim.disease, t, StepGraph(t, src, dst, kind), True)
+    got = lam.cpu().numpy().astype(np.float64)
+    nz = ref > 0
+    assert np.all(np.abs(got[nz] - ref[nz]) <= 1e-5 * ref[nz])
+    assert np.all(got[~nz] == 0)
+    assert int(rec[19]) == len(src)
