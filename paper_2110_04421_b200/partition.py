@@ -290,6 +290,10 @@ class PartitionedSimulation(ConfigSimulation):
         if self.exchange is not None and not isinstance(self.exchange, LocalCodeExchange):
             self.exchange.exchange(self.codes[(t + 1) & 1])
 
+    def capture(self):
+        raise ConfigError("a partitioned simulation exchanges with its peers between and "
+                          "inside days; run it day by day (run()) instead of as a CUDA graph")
+
     def run(self, days: int | None = None) -> None:
         # one day at a time: the code exchange sits between days
         for _ in range(self.horizon - self.clock if days is None else days):
