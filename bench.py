@@ -33,6 +33,7 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 HORIZON = 180
+DOSE_GAP = [21]      # config2 second-dose delay (set from --dose-gap)
 
 
 def parse():
@@ -42,8 +43,10 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--mode", choices=["csr", "fused", "auto"], default="auto")
-    ap.add_argument("--workload", choices=["config1", "config0", "config3", "config4", "refnet"],
+    ap.add_argument("--workload", choices=["config1", "config0", "config2", "config3", "config4",
+                                           "refnet"],
                     default="config1")
+    ap.add_argument("--dose-gap", type=int, default=21, help="config2: second-dose delay (21 or 84)")
     ap.add_argument("--replicas", type=int, default=128, help="config4: replicas per GPU")
     ap.add_argument("--streams", type=int, default=8, help="config4: concurrent streams")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
@@ -55,7 +58,24 @@ def parse():
 
 def workload_spec(name):
     from paper_2110_04421_b200.confignet import ConfigNetworkSpec
-    return ConfigNetworkSpec.config({"config0": 0, "config1": 1, "config3": 3, "config4": 4}[name])
+    return ConfigNetworkSpec.config({"config0": 0, "config1": 1, "config2": 2, "config3": 3,
+                                     "config4": 4}[name])
+
+
+def workload_iv(name, dose_gap=21):
+    """BASELINE.json configs[2] (SURVEY §8(d) mapping): quarantine 14 days,
+    testing of symptomatic agents (detection 5 %, 2-day result delay), DEN with
+    app adoption 0.5, two-dose vaccination 1 %/day, efficacy 0.5 / 0.9, second
+    dose after `dose_gap` days; no interventions for the other configs."""
+    from paper_2110_04421_b200.interventions import (DenConfig, InterventionConfig, TestKind,
+                                                     VaccinePolicy)
+    if name != "config2":
+        return InterventionConfig()
+    return InterventionConfig(quarantine_enabled=True, testing_enabled=True,
+                              test_kind=TestKind("cfg2", 0.05, 2, 2), den_enabled=True,
+                              den=DenConfig(0.5), vaccination_enabled=True,
+                              vaccine=VaccinePolicy(daily_rate=0.01, dose1_efficacy=0.5,
+                                                    dose2_efficacy=0.9, dose_gap=dose_gap))
 
 
 def dist_env():
@@ -78,7 +98,8 @@ def _cpu_worker(args):
     spec = workload_spec(workload)
     pop = synthesize(spec, 0)
     cols = initial_columns(pop)
-    disease, table, iv = default_disease(), default_progression(), InterventionConfig()
+    disease, table = default_disease(), default_progression()
+    iv = workload_iv(workload) if workload != "config2" else workload_iv(workload, DOSE_GAP[0])
     # seeding (population.py:151-177) with the oracle's keyed draws
     from oracle import rng_np
     ids = pop.seeds
@@ -254,10 +275,12 @@ def run_ours(a):
         import torch.distributed as dist
         dist.init_process_group("nccl")
     spec = workload_spec(a.workload)
-    disease, table, iv = default_disease(), default_progression(), InterventionConfig()
+    disease, table, iv = default_disease(), default_progression(), workload_iv(a.workload, a.dose_gap)
     pop = synthesize(spec, 0)
     n_sims = a.warmup + a.steps
     modes = ["csr", "fused"] if a.mode == "auto" else [a.mode]
+    if iv.den_enabled:      # fused mode keeps no contact log
+        modes = ["csr"]
 
     def make(mode, i):
         seed = replication_seed(0, rank * 100_000 + i)
@@ -348,9 +371,12 @@ def run_ours(a):
         "ms_per_step": ms_total / a.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {
-            "workload": f"{a.workload} (BASELINE.json configs[1]): 100k agents, 180 days, "
-                        "households U{1..6} + workplaces U{10..50} x 8 colleague draws + "
-                        "Poisson(5) random contacts, 100 seeds, no interventions",
+            "workload": (f"config2 (BASELINE.json configs[2]): config 1 + quarantine 14 d, testing "
+                         f"(5 %, 2-day delay), DEN (app 0.5), vaccination 1 %/day, efficacy 0.5/0.9, "
+                         f"dose gap {a.dose_gap} d" if a.workload == "config2" else
+                         f"{a.workload} (BASELINE.json configs[1]): 100k agents, 180 days, "
+                         "households U{1..6} + workplaces U{10..50} x 8 colleague draws + "
+                         "Poisson(5) random contacts, 100 seeds, no interventions"),
             "mode": best["mode"], "step": "one full 180-day simulation (CUDA graph replay)",
             "replicas": f"{a.steps} timed replications per GPU, distinct seeds",
             "l2": "flushed between timed simulations (384 MB write)",
@@ -719,6 +745,7 @@ def run_refnet(a):
 
 def main():
     a = parse()
+    DOSE_GAP[0] = a.dose_gap
     if a.impl == "reference":
         run_reference(a)
     elif a.workload == "config3":

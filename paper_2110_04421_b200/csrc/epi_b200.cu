@@ -987,8 +987,29 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
   if (ev) CK(cudaEventRecord((cudaEvent_t)ev[2], s));
   if (iv) {
     int rc = run_interventions(c, A, codes_next, c->net_dev, rcount_next, vax_open, s, [&](bool pull) -> int {
+      // the window's slots (steps step-L .. step-1), scanned in one launch
       const int L = c->host.den_lookback;
+      DenRing R{};
+      R.cap = c->net.row_cap;
+      bool fits = true;
       for (int i = 0; i < c->net_slots; ++i) {
+        const int st_i = c->net_slot_step[i];
+        if (st_i < 0 || st_i >= step || st_i < step - L) continue;
+        if (R.n_slots == DEN_MAX_SLOTS) { fits = false; break; }
+        R.entries[R.n_slots] = c->net_entries[i];
+        R.row_len[R.n_slots] = c->net_rowlen[i];
+        ++R.n_slots;
+      }
+      if (fits) {
+        if (R.n_slots == 0) return 0;
+        if (pull)
+          k_den_pull_ring<<<grid_for(c->hi - c->lo, 256), 256, 0, s>>>(R, c->lo, c->hi, c->flags);
+        else
+          k_den_scan_ring<<<grid_for(c->n, 256), 256, 0, s>>>(R, c->n, c->flags);
+        CKL();
+        return 0;
+      }
+      for (int i = 0; i < c->net_slots; ++i) {      // very long lookbacks: one launch per slot
         const int st_i = c->net_slot_step[i];
         if (st_i < 0 || st_i >= step || st_i < step - L) continue;
         if (pull)

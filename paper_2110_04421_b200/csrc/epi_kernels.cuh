@@ -940,6 +940,52 @@ __global__ void k_den_scan_coo(const int32_t* __restrict__ src, const int32_t* _
     }
   }
 }
+// The contact-log slots of a day's DEN window, for one-launch scans.
+constexpr int DEN_MAX_SLOTS = 16;
+struct DenRing {
+  const uint32_t* entries[DEN_MAX_SLOTS];
+  const int32_t* row_len[DEN_MAX_SLOTS];
+  int n_slots, cap;
+};
+
+// Push scan over every slot of the window in one launch: each notifier marks
+// the sources of its own rows (config graphs are symmetric).  Same marks as
+// one k_den_scan_csr per slot.
+__global__ void k_den_scan_ring(DenRing R, int64_t n, uint8_t* __restrict__ flags) {
+  for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < n;
+       a += (int64_t)gridDim.x * blockDim.x) {
+    if (!(flags[a] & FL_NOTIFIER)) continue;
+    for (int k = 0; k < R.n_slots; ++k) {
+      const int len = R.row_len[k][a];
+      const uint32_t* e = R.entries[k] + a * (int64_t)R.cap;
+      for (int i = 0; i < len; ++i) {
+        const int64_t c = e[i] >> 2;
+        if (!(flags[c] & FL_NOTIFIED))
+          atomicOr((unsigned*)(flags + (c & ~3ll)), (unsigned)FL_NOTIFIED << (8 * (c & 3)));
+      }
+    }
+  }
+}
+// Pull form over every slot of the window (partitioned runs, see below).
+__global__ void k_den_pull_ring(DenRing R, int64_t lo, int64_t hi, uint8_t* __restrict__ flags) {
+  for (int64_t a = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < hi;
+       a += (int64_t)gridDim.x * blockDim.x) {
+    const uint8_t fa = flags[a];
+    if (fa & FL_NOTIFIED) continue;
+    bool hit = false;
+    for (int k = 0; k < R.n_slots && !hit; ++k) {
+      const int len = R.row_len[k][a];
+      const uint32_t* e = R.entries[k] + a * (int64_t)R.cap;
+      for (int i = 0; i < len; ++i)
+        if (flags[e[i] >> 2] & FL_NOTIFIER) {
+          hit = true;
+          break;
+        }
+    }
+    if (hit) flags[a] = fa | FL_NOTIFIED;
+  }
+}
+
 // Pull form for partitioned runs: agent a of the owned rows is notified if a
 // source in its own row is a notifier (the notifier flags of every rank were
 // all-gathered first).  Config graphs are symmetric, so this marks exactly
