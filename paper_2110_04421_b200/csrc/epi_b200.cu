@@ -161,7 +161,8 @@ struct epi_ctx {
   NetTables ntab{};                  // host copy (static radix tables)
   NetTables* ntab_dev[3] = {nullptr, nullptr, nullptr};   // per-day keys, by step % 3
   WorkTables wt_host[2]{};           // day tables by step parity (member_at_pos shared)
-  WorkTables* wt_dev[2][3] = {};     // device structs per parity x variant
+  WorkTables* wt_dev[2][4] = {};     // device structs per parity x variant (0 member tables,
+                                     // 1 + wcode, 2 + rin/rout, 3 + rin ids)
                                      //   0 csr (ids), 1 fused partitioned, 2 fused whole
   int merged_ready = -1;             // day whose tables the previous merged kernel built
   Injected* inj_dev = nullptr;
@@ -407,6 +408,7 @@ int epi_destroy(epi_ctx* c) {
     cudaFree(w.wcode);
     cudaFree(w.rout);
     cudaFree(w.rin);
+    cudaFree(w.rin_id);
   }
   for (auto& row : c->wt_dev)
     for (auto* p : row) cudaFree(p);
@@ -855,12 +857,14 @@ int epi_net_attach(epi_ctx* c, const epi_net* net) {
     if (!rc) rc = dalloc(&w.wcode, (size_t)net->n_member_slots);
     if (!rc) rc = dalloc(&w.rout, (size_t)c->n * RT_SLOTS);
     if (!rc) rc = dalloc(&w.rin, (size_t)c->n * RT_SLOTS);
+    if (!rc && c->host.den_enabled) rc = dalloc(&w.rin_id, (size_t)c->n * RT_SLOTS);
     if (rc) return rc;
     CK(cudaMemset(w.rin, 0, (size_t)c->n * RT_SLOTS * sizeof(uint16_t)));
-    for (int var = 0; var < 3; ++var) {
+    for (int var = 0; var < 4; ++var) {
       WorkTables v = w;
       if (var == 0) v.wcode = nullptr;
       if (var < 2) { v.rin = nullptr; v.rout = nullptr; }
+      if (var < 3) v.rin_id = nullptr;
       if (!c->wt_dev[par][var]) CK(cudaMalloc((void**)&c->wt_dev[par][var], sizeof(WorkTables)));
       CK(cudaMemcpy(c->wt_dev[par][var], &v, sizeof(WorkTables), cudaMemcpyHostToDevice));
     }
@@ -911,11 +915,14 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
   // csr mode writes messages only in fp32 without a contact log
   const bool msg_only = mode == 0 && precision == EPI_F32 && !c->host.den_enabled &&
                         c->net.row_cap <= MP_MAX_CAP;
-  const bool push_rand = (mode == 1 || msg_only) && c->lo == 0 && c->hi == c->n && c->net.n_agents >= 2 &&
-                         c->net.random_slots == RT_SLOTS && batched(&c->net) && push_fits(c);
+  // id generation (contact log, fp64 order) reads push tables with source ids
+  const bool id_push = mode == 0 && !msg_only && c->wt_host[par].rin_id != nullptr;
+  const bool push_rand = (mode == 1 || msg_only || id_push) && c->lo == 0 && c->hi == c->n &&
+                         c->net.n_agents >= 2 && c->net.random_slots == RT_SLOTS && batched(&c->net) &&
+                         push_fits(c);
   const bool merged = mode == 1 && push_rand && !iv;
   const bool use_wt = (mode == 0 && (push_rand || (has_work && batched(&c->net)))) || mode == 1;
-  const int variant = push_rand ? 2 : (mode == 0 ? 0 : 1);
+  const int variant = push_rand ? (id_push ? 3 : 2) : (mode == 0 ? 0 : 1);
   long long* rec_zero = zero_record ? rec : nullptr;
   if (merged && c->merged_ready == step) {
     if (rec_zero) CK(cudaMemsetAsync(rec, 0, EPI_REC_LEN * sizeof(long long), s));
@@ -932,6 +939,7 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
       WorkTables w = c->wt_host[par];
       if (variant == 0) w.wcode = nullptr;
       if (variant < 2) { w.rin = nullptr; w.rout = nullptr; }
+      if (variant < 3) w.rin_id = nullptr;
       CK(launch_pdl_w(&c->hot, k_day_tables, dim3(wblocks + rblocks > 0 ? wblocks + rblocks : 1), dim3(256), 0, s,
                     c->net, nk, w, codes_cur, c->lo, c->hi, wblocks, (const NetTables*)nt_today, nt_next,
                     key_prefix(seed, step + 1, P_NET_RPERM), rec_zero));

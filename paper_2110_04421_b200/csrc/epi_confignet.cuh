@@ -166,6 +166,7 @@ struct WorkTables {
   uint16_t* wcode;
   uint32_t* rout;
   uint16_t* rin;
+  uint32_t* rin_id;      // optional: the source ids of rin (id CSR generation, DEN)
 };
 constexpr int RT_SLOTS = 16;
 constexpr uint16_t CODE_PRESENT = 0x4000;
@@ -339,7 +340,31 @@ __device__ __forceinline__ void for_each_in_edge_batched(const epi_net& net, con
   }
   // random slots
   const uint32_t n = (uint32_t)net.n_agents;
-  if (n >= 2) {
+  if (n >= 2 && wt != nullptr && wt->rin != nullptr && wt->rin_id != nullptr) {
+    // from the day's push tables (ids + codes), same order as below
+    const uint32_t self = (uint32_t)b;
+    const int nb = code_count(code_b);
+    const int nbe = nb < RT_SLOTS ? nb : RT_SLOTS;
+    const uint4* ri = (const uint4*)(wt->rin + (size_t)b * RT_SLOTS);
+    const uint4 in[2] = {ri[0], ri[1]};
+    const uint4* ro = (const uint4*)(wt->rout + (size_t)b * RT_SLOTS);
+    for (int j0 = 0; j0 < nbe; j0 += 4) {
+      const uint4 o = ro[j0 >> 2];
+      const uint32_t po[4] = {o.x, o.y, o.z, o.w};
+      uint16_t co[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        co[q] = (j0 + q < nbe && po[q] != self) ? codes[po[q]] : (uint16_t)CODE_DEAD;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (!code_dead(co[q])) visit((int64_t)po[q], 2, co[q]);
+    }
+    const uint16_t* iv = (const uint16_t*)in;
+    const uint32_t* ids = wt->rin_id + (size_t)b * RT_SLOTS;
+#pragma unroll
+    for (int j = 0; j < RT_SLOTS; ++j)
+      if (iv[j] & CODE_PRESENT) visit((int64_t)ids[j], 2, (uint16_t)(iv[j] & ~CODE_PRESENT));
+  } else if (n >= 2) {
     const Radix d = make_radix(n);
     const int nb = code_count(code_b);
     const int slots = net.random_slots;

@@ -576,7 +576,7 @@ __global__ void __launch_bounds__(128, 6) k_net_realize(epi_net net, NetKeys nk,
         else if (BATCH) for_each_in_edge_batched<16, 8>(net, nk, NT.rk, NT.wrad, wt, codes, b, cb, put);
         else for_each_in_edge(net, nk, NT.rk, NT.wrad, codes, b, cb, 0, 1, put);
       }
-      if (PUSH) clear_rin_row(wt, b);
+      if (PUSH || BATCH) clear_rin_row(wt, b);    // consumed push rows (if any) start empty
       if (SORT) {
         for (int i = 1; i < cnt; ++i) {
           const uint32_t x = mine[i];
@@ -867,7 +867,10 @@ __global__ void __launch_bounds__(256) k_day_tables(epi_net net, NetKeys nk, Wor
       const uint32_t src = (uint32_t)(base + l);
       const uint32_t y = walk_fwd(src, NT.rk[j], dn);
       wt.rout[(size_t)src * RT_SLOTS + j] = y;
-      if (y != src) wt.rin[(size_t)y * RT_SLOTS + j] = codes[src] | CODE_PRESENT;
+      if (y != src) {
+        wt.rin[(size_t)y * RT_SLOTS + j] = codes[src] | CODE_PRESENT;
+        if (wt.rin_id) wt.rin_id[(size_t)y * RT_SLOTS + j] = src;
+      }
     }
     __syncwarp();
   }
@@ -950,18 +953,27 @@ struct DenRing {
 
 // Push scan over every slot of the window in one launch: each notifier marks
 // the sources of its own rows (config graphs are symmetric).  Same marks as
-// one k_den_scan_csr per slot.
+// one k_den_scan_csr per slot.  Notifiers are few and their window holds
+// ~lookback x 21 contacts, so a whole warp walks each notifier's rows (one
+// lane per contact) instead of one thread.
 __global__ void k_den_scan_ring(DenRing R, int64_t n, uint8_t* __restrict__ flags) {
-  for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < n;
-       a += (int64_t)gridDim.x * blockDim.x) {
-    if (!(flags[a] & FL_NOTIFIER)) continue;
-    for (int k = 0; k < R.n_slots; ++k) {
-      const int len = R.row_len[k][a];
-      const uint32_t* e = R.entries[k] + a * (int64_t)R.cap;
-      for (int i = 0; i < len; ++i) {
-        const int64_t c = e[i] >> 2;
-        if (!(flags[c] & FL_NOTIFIED))
-          atomicOr((unsigned*)(flags + (c & ~3ll)), (unsigned)FL_NOTIFIED << (8 * (c & 3)));
+  const int lane = lane_id();
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t base = (blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; base < n;
+       base += warps * 32) {
+    const int64_t a = base + lane;
+    unsigned m = __ballot_sync(0xFFFFFFFFu, a < n && (flags[a] & FL_NOTIFIER));
+    while (m) {
+      const int64_t an = base + __ffs(m) - 1;
+      m &= m - 1;
+      for (int k = 0; k < R.n_slots; ++k) {
+        const int len = R.row_len[k][an];
+        const uint32_t* e = R.entries[k] + an * (int64_t)R.cap;
+        for (int i = lane; i < len; i += 32) {
+          const int64_t c = e[i] >> 2;
+          if (!(flags[c] & FL_NOTIFIED))
+            atomicOr((unsigned*)(flags + (c & ~3ll)), (unsigned)FL_NOTIFIED << (8 * (c & 3)));
+        }
       }
     }
   }
