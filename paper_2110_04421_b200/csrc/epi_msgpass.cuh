@@ -113,6 +113,9 @@ __global__ void __launch_bounds__(MP_WARPS * 32, 3) k_msg_pass(StepArgs A, CsrVi
     const int a = lo_row + tile * 32 + lane;
     const bool valid = a < n;
     const uint4* blk = msgs + (size_t)tile * tile_words;
+    // MODE 1: the row's state, loaded before the sums so the loads overlap them
+    AgentHot h{};
+    if (MODE == 1 && valid) h = load_hot(A.st, a);
     // group sums
 #pragma unroll
     for (int q = 0; q < MP_STEPS; ++q)
@@ -138,15 +141,14 @@ __global__ void __launch_bounds__(MP_WARPS * 32, 3) k_msg_pass(StepArgs A, CsrVi
       }
     } else {
       double lam = 0.0;
-      if (valid && is_target(P, A.st, a)) lam = (double)(acc * T.sfac[A.st.age_band[a]]);
+      if (valid && h.stage == S_SUS && !(P->sterilizing && h.immune)) lam = (double)(acc * T.sfac[h.age]);
       unsigned ev = 0;
-      if (valid) ev = transmit_progress(A, a, lam);
+      if (valid) ev = transmit_progress_hot(A, a, lam, -1, h);
       if (valid && (ev & 8u) && A.flags) A.flags[a] = FL_SYMPTOMATIC;
       rec_events(racc, ev);
       if (final_pass) {
-        const int stg = valid ? A.st.stage[a] : 0;
-        rec_agent(racc, valid, stg, valid ? A.st.infected_at[a] : 0);
-        if (valid && codes_next) codes_next[a] = next_code(P, A.st, a, A.step + 1, net, rcount_next);
+        rec_agent(racc, valid, valid ? h.stage : 0, valid ? h.infected_at : 0);
+        if (valid && codes_next) codes_next[a] = next_code_hot(P, h, a, A.step + 1, net, rcount_next);
       }
     }
   };
