@@ -531,7 +531,7 @@ __device__ __forceinline__ void clear_rin_row(const WorkTables* wt, int64_t b) {
 // push tables (rin/rout, built by k_day_tables) instead of the random-slot
 // bijections, and the rin rows consumed are cleared.
 template <bool SORT, bool BATCH, bool PUSH = false>
-__global__ void __launch_bounds__(128, 6) k_net_realize(epi_net net, NetKeys nk, const uint16_t* __restrict__ codes,
+__global__ void __launch_bounds__(128, (BATCH && !PUSH) ? 5 : 6) k_net_realize(epi_net net, NetKeys nk, const uint16_t* __restrict__ codes,
                                                      uint32_t* __restrict__ entries,
                                                      uint16_t* __restrict__ msgs,
                                                      uint16_t* __restrict__ tile_off,
@@ -565,16 +565,21 @@ __global__ void __launch_bounds__(128, 6) k_net_realize(epi_net net, NetKeys nk,
       if (!code_dead(cb)) {
         // the staging row holds either ids (src<<2|kind) or messages
         // ((code & 0xFF) << 4 | kind << 2: the byte offset of the weight in
-        // MsgComb) when only messages are requested
-        auto put = [&](int64_t c, int kind, uint16_t cc) {
-          mine[cnt++] = entries ? (((uint32_t)c << 2) | (uint32_t)kind)
-                                : (((uint32_t)(cc & 0xFF) << 4) | ((uint32_t)kind << 2));
+        // MsgComb) when only messages are requested; one enumeration loop per
+        // form, so the per-edge store carries no test
+        auto run = [&](auto&& put) {
+          if (PUSH)
+            for_each_in_code(net, nk, NT.rk, NT.wrad, NT.dn, wt, codes, b, cb,
+                             [&](int kind, uint16_t cc) { put(0, kind, cc); });
+          else if (BATCH) for_each_in_edge_batched<16, 8>(net, nk, NT.rk, NT.wrad, wt, codes, b, cb, put);
+          else for_each_in_edge(net, nk, NT.rk, NT.wrad, codes, b, cb, 0, 1, put);
         };
-        if (PUSH)
-          for_each_in_code(net, nk, NT.rk, NT.wrad, NT.dn, wt, codes, b, cb,
-                           [&](int kind, uint16_t cc) { put(0, kind, cc); });
-        else if (BATCH) for_each_in_edge_batched<16, 8>(net, nk, NT.rk, NT.wrad, wt, codes, b, cb, put);
-        else for_each_in_edge(net, nk, NT.rk, NT.wrad, codes, b, cb, 0, 1, put);
+        if (entries)
+          run([&](int64_t c, int kind, uint16_t) { mine[cnt++] = ((uint32_t)c << 2) | (uint32_t)kind; });
+        else
+          run([&](int64_t, int kind, uint16_t cc) {
+            mine[cnt++] = ((uint32_t)(cc & 0xFF) << 4) | ((uint32_t)kind << 2);
+          });
       }
       if (PUSH || BATCH) clear_rin_row(wt, b);    // consumed push rows (if any) start empty
       if (SORT) {
