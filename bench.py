@@ -279,8 +279,6 @@ def run_ours(a):
     pop = synthesize(spec, 0)
     n_sims = a.warmup + a.steps
     modes = ["csr", "fused"] if a.mode == "auto" else [a.mode]
-    if iv.den_enabled:      # fused mode keeps no contact log
-        modes = ["csr"]
 
     def make(mode, i):
         seed = replication_seed(0, rank * 100_000 + i)

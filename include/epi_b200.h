@@ -279,10 +279,13 @@ int epi_set_infection_mode(epi_ctx *ctx, int32_t mode);
  *   EPI_X_SUM_U64    all-reduce sum of `count` uint64 (the vaccination
  *                    eligibility histogram + active count);
  *   EPI_X_EXSCAN_I64 exclusive prefix sum over the ranks, in rank (= id)
- *                    order, of `count` int64, in place (the cut-bucket offset). */
+ *                    order, of `count` int64, in place (the cut-bucket offset);
+ *   EPI_X_OR_U8      all-reduce bitwise OR of `count` bytes (the DEN
+ *                    notifications each rank pushed to anyone's contacts). */
 #define EPI_X_GATHER_U8 1
 #define EPI_X_SUM_U64 2
 #define EPI_X_EXSCAN_I64 3
+#define EPI_X_OR_U8 4
 typedef int (*epi_exchange_fn)(void *user, int32_t kind, void *buf, int64_t count, void *stream);
 int epi_set_exchange(epi_ctx *ctx, epi_exchange_fn fn, void *user);
 

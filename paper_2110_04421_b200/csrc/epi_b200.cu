@@ -120,6 +120,8 @@ struct epi_ctx {
   void* xuser = nullptr;
   int push_max = -1;                 // push tables up to this many agents (-1: by L2 size)
   int indep = 0;                     // graph-in fp64: independent-edges infection draws
+  int32_t* died_at = nullptr;        // DEN on config networks: death step per agent
+  uint8_t* den_mark = nullptr;       // DEN, partitioned: notifications pushed by this rank
   epi_params host{};
   epi_params* P = nullptr;           // device copy
   int64_t n = 0;
@@ -161,8 +163,8 @@ struct epi_ctx {
   NetTables ntab{};                  // host copy (static radix tables)
   NetTables* ntab_dev[3] = {nullptr, nullptr, nullptr};   // per-day keys, by step % 3
   WorkTables wt_host[2]{};           // day tables by step parity (member_at_pos shared)
-  WorkTables* wt_dev[2][4] = {};     // device structs per parity x variant (0 member tables,
-                                     // 1 + wcode, 2 + rin/rout, 3 + rin ids)
+  WorkTables* wt_dev[2][3] = {};     // device structs per parity x variant (0 member tables,
+                                     // 1 + wcode, 2 + rin/rout)
                                      //   0 csr (ids), 1 fused partitioned, 2 fused whole
   int merged_ready = -1;             // day whose tables the previous merged kernel built
   Injected* inj_dev = nullptr;
@@ -235,9 +237,7 @@ static int exchange(epi_ctx* c, int32_t kind, void* buf, int64_t count, cudaStre
   return rc ? fail(EPI_ECUDA, "exchange callback failed") : 0;
 }
 
-// `den_scan(pull)` launches the contact scan for this step (may be empty):
-// push from the notifiers' rows, or, in partitioned runs, pull into the
-// owned rows after the notifier flags were all-gathered.
+// `den_scan(partitioned)` marks this step's notified contacts (may be empty).
 template <class DenScan>
 int run_interventions(epi_ctx* c, const StepArgs& A, uint16_t* codes_next, const epi_net* net_dev,
                       uint64_t rcount_next, int32_t* vax_open, cudaStream_t s, DenScan&& den_scan) {
@@ -251,11 +251,6 @@ int run_interventions(epi_ctx* c, const StepArgs& A, uint16_t* codes_next, const
     CKL();
   }
   if (p.den_enabled) {
-    // every rank's notifiers (the owned bytes of `flags`) on every rank
-    if (part) {
-      int rc = exchange(c, EPI_X_GATHER_U8, c->flags, n, s);
-      if (rc) return rc;
-    }
     int rc = den_scan(part);
     if (rc) return rc;
   }
@@ -400,6 +395,8 @@ int epi_destroy(epi_ctx* c) {
   cudaFree(c->msg_dev);
   cudaFree(c->comb_dev);
   cudaFree(c->tau_lut);
+  cudaFree(c->died_at);
+  cudaFree(c->den_mark);
   for (auto* p : c->ntab_dev) cudaFree(p);
   cudaFree(c->wt_host[0].member_at_pos);
   for (auto& w : c->wt_host) {
@@ -408,7 +405,6 @@ int epi_destroy(epi_ctx* c) {
     cudaFree(w.wcode);
     cudaFree(w.rout);
     cudaFree(w.rin);
-    cudaFree(w.rin_id);
   }
   for (auto& row : c->wt_dev)
     for (auto* p : row) cudaFree(p);
@@ -600,8 +596,10 @@ int epi_codes(epi_ctx* c, const epi_state* st, const epi_net* net, uint64_t grap
     if (!c->has_net) return fail(EPI_EARG, "epi_codes with a network needs epi_net_attach first");
     nd = c->net_dev;
   }
-  k_codes<<<grid_for(c->hi - c->lo, 256), 256, 0, S(stream)>>>(
-      c->P, *st, step, nd, key_prefix(graph_seed, step, P_NET_RCOUNT), codes_out, c->lo, c->hi);
+  // a config simulation starting over: death steps restart from the state
+  int32_t* died = (net && step == 0) ? c->died_at : nullptr;
+  k_codes<<<grid_for(c->n, 256), 256, 0, S(stream)>>>(
+      c->P, *st, step, nd, key_prefix(graph_seed, step, P_NET_RCOUNT), codes_out, c->lo, c->hi, died, c->n);
   CKL();
   return 0;
 }
@@ -829,7 +827,17 @@ int epi_net_attach(epi_ctx* c, const epi_net* net) {
   c->has_net = true;
   if (!c->net_dev) CK(cudaMalloc((void**)&c->net_dev, sizeof(epi_net)));
   CK(cudaMemcpy(c->net_dev, net, sizeof(epi_net), cudaMemcpyHostToDevice));
-  const int slots = c->host.den_enabled ? c->host.den_lookback + 1 : 1;
+  // one CSR slot (id rows for fp64 order / export); DEN regenerates past
+  // days' contacts instead of keeping a contact log
+  const int slots = 1;
+  if (c->host.den_enabled) {
+    if (c->host.den_lookback > DEN_MAX_DAYS) return fail(EPI_EARG, "den.lookback > 16 on config networks");
+    rc = dalloc(&c->died_at, (size_t)c->n);
+    if (!rc) rc = dalloc(&c->den_mark, (size_t)c->n + 4);
+    if (rc) return rc;
+    k_fill_i32<<<grid_for(c->n, 256), 256>>>(c->died_at, c->n, INT32_MAX);
+    CKL();
+  }
   for (auto* p : c->net_entries) cudaFree(p);
   for (auto* p : c->net_rowlen) cudaFree(p);
   c->net_entries.assign(slots, nullptr);
@@ -857,14 +865,12 @@ int epi_net_attach(epi_ctx* c, const epi_net* net) {
     if (!rc) rc = dalloc(&w.wcode, (size_t)net->n_member_slots);
     if (!rc) rc = dalloc(&w.rout, (size_t)c->n * RT_SLOTS);
     if (!rc) rc = dalloc(&w.rin, (size_t)c->n * RT_SLOTS);
-    if (!rc && c->host.den_enabled) rc = dalloc(&w.rin_id, (size_t)c->n * RT_SLOTS);
     if (rc) return rc;
     CK(cudaMemset(w.rin, 0, (size_t)c->n * RT_SLOTS * sizeof(uint16_t)));
-    for (int var = 0; var < 4; ++var) {
+    for (int var = 0; var < 3; ++var) {
       WorkTables v = w;
       if (var == 0) v.wcode = nullptr;
       if (var < 2) { v.rin = nullptr; v.rout = nullptr; }
-      if (var < 3) v.rin_id = nullptr;
       if (!c->wt_dev[par][var]) CK(cudaMalloc((void**)&c->wt_dev[par][var], sizeof(WorkTables)));
       CK(cudaMemcpy(c->wt_dev[par][var], &v, sizeof(WorkTables), cudaMemcpyHostToDevice));
     }
@@ -893,7 +899,6 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
   if (partitioned(c) && (c->host.den_enabled || c->host.vaccination_enabled) && !c->xfn)
     return fail(EPI_EARG, "exposure notification and vaccination in a partitioned run need a "
                           "cross-rank exchange (epi_set_exchange)");
-  if (mode == 1 && c->host.den_enabled) return fail(EPI_EARG, "fused mode keeps no contact log; use mode 0 with DEN");
   if (mode == 1 && precision != EPI_F32) return fail(EPI_EARG, "fused mode is fp32 only");
   cudaStream_t s = S(stream);
   long long* rec = record ? (long long*)record : c->scratch_rec;
@@ -913,16 +918,12 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
   // tables in its epilogue, so after the first day there is one kernel per day.
   const bool has_work = c->net.n_member_slots > 0 && c->net.colleague_draws > 0;
   // csr mode writes messages only in fp32 without a contact log
-  const bool msg_only = mode == 0 && precision == EPI_F32 && !c->host.den_enabled &&
-                        c->net.row_cap <= MP_MAX_CAP;
-  // id generation (contact log, fp64 order) reads push tables with source ids
-  const bool id_push = mode == 0 && !msg_only && c->wt_host[par].rin_id != nullptr;
-  const bool push_rand = (mode == 1 || msg_only || id_push) && c->lo == 0 && c->hi == c->n &&
-                         c->net.n_agents >= 2 && c->net.random_slots == RT_SLOTS && batched(&c->net) &&
-                         push_fits(c);
+  const bool msg_only = mode == 0 && precision == EPI_F32 && c->net.row_cap <= MP_MAX_CAP;
+  const bool push_rand = (mode == 1 || msg_only) && c->lo == 0 && c->hi == c->n && c->net.n_agents >= 2 &&
+                         c->net.random_slots == RT_SLOTS && batched(&c->net) && push_fits(c);
   const bool merged = mode == 1 && push_rand && !iv;
   const bool use_wt = (mode == 0 && (push_rand || (has_work && batched(&c->net)))) || mode == 1;
-  const int variant = push_rand ? (id_push ? 3 : 2) : (mode == 0 ? 0 : 1);
+  const int variant = push_rand ? 2 : (mode == 0 ? 0 : 1);
   long long* rec_zero = zero_record ? rec : nullptr;
   if (merged && c->merged_ready == step) {
     if (rec_zero) CK(cudaMemsetAsync(rec, 0, EPI_REC_LEN * sizeof(long long), s));
@@ -939,7 +940,6 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
       WorkTables w = c->wt_host[par];
       if (variant == 0) w.wcode = nullptr;
       if (variant < 2) { w.rin = nullptr; w.rout = nullptr; }
-      if (variant < 3) w.rin_id = nullptr;
       CK(launch_pdl_w(&c->hot, k_day_tables, dim3(wblocks + rblocks > 0 ? wblocks + rblocks : 1), dim3(256), 0, s,
                     c->net, nk, w, codes_cur, c->lo, c->hi, wblocks, (const NetTables*)nt_today, nt_next,
                     key_prefix(seed, step + 1, P_NET_RPERM), rec_zero));
@@ -994,40 +994,32 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
   }
   if (ev) CK(cudaEventRecord((cudaEvent_t)ev[2], s));
   if (iv) {
-    int rc = run_interventions(c, A, codes_next, c->net_dev, rcount_next, vax_open, s, [&](bool pull) -> int {
-      // the window's slots (steps step-L .. step-1), scanned in one launch
-      const int L = c->host.den_lookback;
-      DenRing R{};
-      R.cap = c->net.row_cap;
-      bool fits = true;
-      for (int i = 0; i < c->net_slots; ++i) {
-        const int st_i = c->net_slot_step[i];
-        if (st_i < 0 || st_i >= step || st_i < step - L) continue;
-        if (R.n_slots == DEN_MAX_SLOTS) { fits = false; break; }
-        R.entries[R.n_slots] = c->net_entries[i];
-        R.row_len[R.n_slots] = c->net_rowlen[i];
-        ++R.n_slots;
-      }
-      if (fits) {
-        if (R.n_slots == 0) return 0;
-        if (pull)
-          k_den_pull_ring<<<grid_for(c->hi - c->lo, 256), 256, 0, s>>>(R, c->lo, c->hi, c->flags);
-        else
-          k_den_scan_ring<<<grid_for(c->n, 256), 256, 0, s>>>(R, c->n, c->flags);
+    if (c->host.den_enabled) {
+      // who died yesterday (the day's code vector is complete here)
+      k_died_update<<<grid_for(c->n, 256), 256, 0, s>>>(codes_cur, c->n, step, c->died_at);
+      CKL();
+    }
+    int rc = run_interventions(c, A, codes_next, c->net_dev, rcount_next, vax_open, s, [&](bool part) -> int {
+      // contacts of the notifiers over steps step-L .. step-1, regenerated
+      DenRegen D{};
+      D.first_day = step - c->host.den_lookback > 0 ? step - c->host.den_lookback : 0;
+      D.n_days = step - D.first_day;
+      if (D.n_days <= 0) return 0;
+      for (int d = 0; d < D.n_days; ++d) D.nk[d] = make_net_keys(seed, D.first_day + d);
+      const int g = grid_for((c->hi - c->lo + 31) / 32 * 32, 256);
+      if (!part) {
+        k_den_regen<<<g, 256, 0, s>>>(c->net, D, c->died_at, c->flags, c->flags, c->lo, c->hi);
         CKL();
         return 0;
       }
-      for (int i = 0; i < c->net_slots; ++i) {      // very long lookbacks: one launch per slot
-        const int st_i = c->net_slot_step[i];
-        if (st_i < 0 || st_i >= step || st_i < step - L) continue;
-        if (pull)
-          k_den_pull_csr<<<grid_for(c->hi - c->lo, 256), 256, 0, s>>>(c->net_entries[i], c->net_rowlen[i],
-                                                                       c->net.row_cap, c->lo, c->hi, c->flags);
-        else
-          k_den_scan_csr<<<grid_for(c->n, 256), 256, 0, s>>>(c->net_entries[i], c->net_rowlen[i],
-                                                               c->net.row_cap, c->n, c->flags);
-        CKL();
-      }
+      // partitioned: contacts may be anyone's; OR the ranks' marks together
+      CK(cudaMemsetAsync(c->den_mark, 0, (size_t)c->n, s));
+      k_den_regen<<<g, 256, 0, s>>>(c->net, D, c->died_at, c->flags, c->den_mark, c->lo, c->hi);
+      CKL();
+      int rc2 = exchange(c, EPI_X_OR_U8, c->den_mark, c->n, s);
+      if (rc2) return rc2;
+      k_den_merge<<<grid_for(c->hi - c->lo, 256), 256, 0, s>>>(c->den_mark, c->lo, c->hi, c->flags);
+      CKL();
       return 0;
     });
     if (rc) return rc;

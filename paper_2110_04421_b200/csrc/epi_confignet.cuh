@@ -166,7 +166,6 @@ struct WorkTables {
   uint16_t* wcode;
   uint32_t* rout;
   uint16_t* rin;
-  uint32_t* rin_id;      // optional: the source ids of rin (id CSR generation, DEN)
 };
 constexpr int RT_SLOTS = 16;
 constexpr uint16_t CODE_PRESENT = 0x4000;
@@ -190,13 +189,15 @@ __device__ __forceinline__ int random_count(const epi_net& net, uint64_t rcount_
 // household members i, colleague draws j and random slots j with
 // index % nl == li.  With nl == 1 the order is: household members ascending,
 // workplace slots (out, in), random slots (out, in).  `rk` holds the
-// random-slot keys of this step (shared memory).
-template <class Visit>
-__device__ __forceinline__ void for_each_in_edge(const epi_net& net, const NetKeys& nk,
-                                                 const PermKeys* __restrict__ rk,
-                                                 const Radix* __restrict__ wrad,
-                                                 const uint16_t* __restrict__ codes, int64_t b,
-                                                 uint16_t code_b, int li, int nl, Visit&& visit) {
+// random-slot keys of this step (shared memory).  `code_of(c)` gives agent
+// c's 16-bit code of the step (dead bit + random-slot count are all the
+// enumeration reads): the day's code vector, or a code rebuilt for a past
+// day (k_den_regen).
+template <class CodeOf, class Visit>
+__device__ __forceinline__ void for_each_in_edge_f(const epi_net& net, const NetKeys& nk,
+                                                   const PermKeys* __restrict__ rk,
+                                                   const Radix* __restrict__ wrad, CodeOf&& codes,
+                                                   int64_t b, uint16_t code_b, int li, int nl, Visit&& visit) {
   // household: contiguous range
   {
     const int off = net.hh_off[b];
@@ -205,7 +206,7 @@ __device__ __forceinline__ void for_each_in_edge(const epi_net& net, const NetKe
     for (int i = li; i < sz; i += nl) {
       const int64_t c = start + i;
       if (c == b) continue;
-      const uint16_t cc = codes[c];
+      const uint16_t cc = codes(c);
       if (!code_dead(cc)) visit(c, 0, cc);
     }
   }
@@ -227,8 +228,8 @@ __device__ __forceinline__ void for_each_in_edge(const epi_net& net, const NetKe
         const uint32_t r = 1u + ((v * (uint32_t)(m - 1)) >> 16);
         const int32_t co = net.wp_members[base + walk_fwd(add_mod(p, r, (uint32_t)m), K, d)];
         const int32_t ci = net.wp_members[base + walk_fwd(sub_mod(p, r, (uint32_t)m), K, d)];
-        const uint16_t cco = codes[co];
-        const uint16_t cci = codes[ci];
+        const uint16_t cco = codes(co);
+        const uint16_t cci = codes(ci);
         if (!code_dead(cco)) visit((int64_t)co, 1, cco);
         if (!code_dead(cci)) visit((int64_t)ci, 1, cci);
       }
@@ -245,16 +246,25 @@ __device__ __forceinline__ void for_each_in_edge(const epi_net& net, const NetKe
       if (j < nb) {
         const uint32_t c = walk_fwd((uint32_t)b, K, d);
         if (c != (uint32_t)b) {
-          const uint16_t cc = codes[c];
+          const uint16_t cc = codes(c);
           if (!code_dead(cc)) visit((int64_t)c, 2, cc);
         }
       }
       if (ci != (uint32_t)b) {
-        const uint16_t cc = codes[ci];
+        const uint16_t cc = codes(ci);
         if (j < code_count(cc)) visit((int64_t)ci, 2, cc);
       }
     }
   }
+}
+
+template <class Visit>
+__device__ __forceinline__ void for_each_in_edge(const epi_net& net, const NetKeys& nk,
+                                                 const PermKeys* __restrict__ rk,
+                                                 const Radix* __restrict__ wrad,
+                                                 const uint16_t* __restrict__ codes, int64_t b,
+                                                 uint16_t code_b, int li, int nl, Visit&& visit) {
+  for_each_in_edge_f(net, nk, rk, wrad, [&](int64_t c) { return codes[c]; }, b, code_b, li, nl, visit);
 }
 
 // Batched single-lane enumeration: every partner id of a section is computed
@@ -340,31 +350,7 @@ __device__ __forceinline__ void for_each_in_edge_batched(const epi_net& net, con
   }
   // random slots
   const uint32_t n = (uint32_t)net.n_agents;
-  if (n >= 2 && wt != nullptr && wt->rin != nullptr && wt->rin_id != nullptr) {
-    // from the day's push tables (ids + codes), same order as below
-    const uint32_t self = (uint32_t)b;
-    const int nb = code_count(code_b);
-    const int nbe = nb < RT_SLOTS ? nb : RT_SLOTS;
-    const uint4* ri = (const uint4*)(wt->rin + (size_t)b * RT_SLOTS);
-    const uint4 in[2] = {ri[0], ri[1]};
-    const uint4* ro = (const uint4*)(wt->rout + (size_t)b * RT_SLOTS);
-    for (int j0 = 0; j0 < nbe; j0 += 4) {
-      const uint4 o = ro[j0 >> 2];
-      const uint32_t po[4] = {o.x, o.y, o.z, o.w};
-      uint16_t co[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        co[q] = (j0 + q < nbe && po[q] != self) ? codes[po[q]] : (uint16_t)CODE_DEAD;
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (!code_dead(co[q])) visit((int64_t)po[q], 2, co[q]);
-    }
-    const uint16_t* iv = (const uint16_t*)in;
-    const uint32_t* ids = wt->rin_id + (size_t)b * RT_SLOTS;
-#pragma unroll
-    for (int j = 0; j < RT_SLOTS; ++j)
-      if (iv[j] & CODE_PRESENT) visit((int64_t)ids[j], 2, (uint16_t)(iv[j] & ~CODE_PRESENT));
-  } else if (n >= 2) {
+  if (n >= 2) {
     const Radix d = make_radix(n);
     const int nb = code_count(code_b);
     const int slots = net.random_slots;

@@ -277,12 +277,17 @@ __device__ __forceinline__ uint16_t next_code(const epi_params* __restrict__ P, 
 
 // ---------------------------------------------------------------------------
 // Codes from state (graph-in gather, and step 0 of a config simulation).
+// (With `died_at`: every agent's death step restarts — -1 if already dead.)
 __global__ void k_codes(const epi_params* __restrict__ P, epi_state st, int step, const epi_net* net,
-                        uint64_t rcount_prefix, uint16_t* __restrict__ codes, int64_t lo, int64_t hi) {
+                        uint64_t rcount_prefix, uint16_t* __restrict__ codes, int64_t lo, int64_t hi,
+                        int32_t* __restrict__ died_at = nullptr, int64_t n_all = 0) {
   const int64_t n = hi;
   for (int64_t a = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < n;
        a += (int64_t)gridDim.x * blockDim.x)
     codes[a] = next_code(P, st, a, step, net, rcount_prefix);
+  if (died_at)
+    for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < n_all; a += (int64_t)gridDim.x * blockDim.x)
+      died_at[a] = st.stage[a] == S_DEAD ? -1 : INT32_MAX;
 }
 
 // ---------------------------------------------------------------------------
@@ -872,10 +877,7 @@ __global__ void __launch_bounds__(256) k_day_tables(epi_net net, NetKeys nk, Wor
       const uint32_t src = (uint32_t)(base + l);
       const uint32_t y = walk_fwd(src, NT.rk[j], dn);
       wt.rout[(size_t)src * RT_SLOTS + j] = y;
-      if (y != src) {
-        wt.rin[(size_t)y * RT_SLOTS + j] = codes[src] | CODE_PRESENT;
-        if (wt.rin_id) wt.rin_id[(size_t)y * RT_SLOTS + j] = src;
-      }
+      if (y != src) wt.rin[(size_t)y * RT_SLOTS + j] = codes[src] | CODE_PRESENT;
     }
     __syncwarp();
   }
@@ -948,95 +950,70 @@ __global__ void k_den_scan_coo(const int32_t* __restrict__ src, const int32_t* _
     }
   }
 }
-// The contact-log slots of a day's DEN window, for one-launch scans.
-constexpr int DEN_MAX_SLOTS = 16;
-struct DenRing {
-  const uint32_t* entries[DEN_MAX_SLOTS];
-  const int32_t* row_len[DEN_MAX_SLOTS];
-  int n_slots, cap;
+// ---------------------------------------------------------------------------
+// Exposure notification without a contact log (config networks).  Every
+// day's graph is a pure function of (seed, day, who is dead that day), so a
+// notifier's contacts of the last `lookback` days are enumerated again
+// instead of being stored: for day s an agent is in the networks iff it had
+// not died before s (died_at[c] >= s), and its random-slot count is the keyed
+// draw of day s.  One warp per notifier and day (lanes split the household,
+// colleague draws and random slots), contacts marked NOTIFIED.  The marks
+// equal those of a scan over the stored edges of those days (ContactLog,
+// interventions.py:145-178), without the 4 B/edge/day log.
+constexpr int DEN_MAX_DAYS = 16;
+struct DenRegen {
+  NetKeys nk[DEN_MAX_DAYS];     // prefixes of days step - n_days .. step - 1
+  int first_day, n_days;
 };
 
-// Push scan over every slot of the window in one launch: each notifier marks
-// the sources of its own rows (config graphs are symmetric).  Same marks as
-// one k_den_scan_csr per slot.  Notifiers are few and their window holds
-// ~lookback x 21 contacts, so a whole warp walks each notifier's rows (one
-// lane per contact) instead of one thread.
-__global__ void k_den_scan_ring(DenRing R, int64_t n, uint8_t* __restrict__ flags) {
-  const int lane = lane_id();
+// died_at[c] = the step during which c died (-1: dead at the start), from
+// the day's (complete) code vector: dead in day t's codes and not yet known.
+__global__ void k_died_update(const uint16_t* __restrict__ codes, int64_t n, int step,
+                              int32_t* __restrict__ died_at) {
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < n; c += (int64_t)gridDim.x * blockDim.x)
+    if (code_dead(codes[c]) && died_at[c] == INT32_MAX) died_at[c] = step - 1;
+}
+
+__global__ void __launch_bounds__(256) k_den_regen(epi_net net, DenRegen D, const int32_t* __restrict__ died_at,
+                                                   const uint8_t* __restrict__ flags, uint8_t* __restrict__ mark,
+                                                   int64_t lo, int64_t hi) {
+  __shared__ Radix wrad[256];
+  __shared__ PermKeys rk[8][EPI_MAX_SLOTS];
+  for (int m = threadIdx.x; m < 256; m += blockDim.x) wrad[m] = make_radix(m < 1 ? 1u : (uint32_t)m);
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = lane_id();
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t base = (blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5)) * 32; base < n;
-       base += warps * 32) {
+  for (int64_t base = lo + (blockIdx.x * (int64_t)(blockDim.x >> 5) + warp) * 32; base < hi; base += warps * 32) {
     const int64_t a = base + lane;
-    unsigned m = __ballot_sync(0xFFFFFFFFu, a < n && (flags[a] & FL_NOTIFIER));
+    unsigned m = __ballot_sync(0xFFFFFFFFu, a < hi && (flags[a] & FL_NOTIFIER));
     while (m) {
       const int64_t an = base + __ffs(m) - 1;
       m &= m - 1;
-      for (int k = 0; k < R.n_slots; ++k) {
-        const int len = R.row_len[k][an];
-        const uint32_t* e = R.entries[k] + an * (int64_t)R.cap;
-        for (int i = lane; i < len; i += 32) {
-          const int64_t c = e[i] >> 2;
-          if (!(flags[c] & FL_NOTIFIED))
-            atomicOr((unsigned*)(flags + (c & ~3ll)), (unsigned)FL_NOTIFIED << (8 * (c & 3)));
-        }
+      for (int d = 0; d < D.n_days; ++d) {
+        const int day = D.first_day + d;
+        const NetKeys& nk = D.nk[d];
+        if (lane < net.random_slots) rk[warp][lane] = random_slot_keys(nk.rperm, lane);
+        __syncwarp();
+        auto code_of = [&](int64_t c) -> uint16_t {
+          if (died_at[c] < day) return CODE_DEAD;
+          return (uint16_t)(random_count(net, nk.rcount, c) << 8);
+        };
+        for_each_in_edge_f(net, nk, rk[warp], wrad, code_of, an, code_of(an), lane, 32,
+                           [&](int64_t c, int, uint16_t) {
+                             if (!(mark[c] & FL_NOTIFIED))
+                               atomicOr((unsigned*)(mark + (c & ~3ll)), (unsigned)FL_NOTIFIED << (8 * (c & 3)));
+                           });
+        __syncwarp();
       }
     }
-  }
-}
-// Pull form over every slot of the window (partitioned runs, see below).
-__global__ void k_den_pull_ring(DenRing R, int64_t lo, int64_t hi, uint8_t* __restrict__ flags) {
-  for (int64_t a = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < hi;
-       a += (int64_t)gridDim.x * blockDim.x) {
-    const uint8_t fa = flags[a];
-    if (fa & FL_NOTIFIED) continue;
-    bool hit = false;
-    for (int k = 0; k < R.n_slots && !hit; ++k) {
-      const int len = R.row_len[k][a];
-      const uint32_t* e = R.entries[k] + a * (int64_t)R.cap;
-      for (int i = 0; i < len; ++i)
-        if (flags[e[i] >> 2] & FL_NOTIFIER) {
-          hit = true;
-          break;
-        }
-    }
-    if (hit) flags[a] = fa | FL_NOTIFIED;
   }
 }
 
-// Pull form for partitioned runs: agent a of the owned rows is notified if a
-// source in its own row is a notifier (the notifier flags of every rank were
-// all-gathered first).  Config graphs are symmetric, so this marks exactly
-// the agents the push scan below marks.
-__global__ void k_den_pull_csr(const uint32_t* __restrict__ entries, const int32_t* __restrict__ row_len,
-                               int cap, int64_t lo, int64_t hi, uint8_t* __restrict__ flags) {
-  for (int64_t a = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < hi;
-       a += (int64_t)gridDim.x * blockDim.x) {
-    const uint8_t fa = flags[a];
-    if (fa & FL_NOTIFIED) continue;
-    const int len = row_len[a];
-    const uint32_t* e = entries + a * (int64_t)cap;
-    for (int i = 0; i < len; ++i)
-      if (flags[e[i] >> 2] & FL_NOTIFIER) {
-        flags[a] = fa | FL_NOTIFIED;
-        break;
-      }
-  }
-}
-// Same over a padded config CSR slot; config graphs are symmetric, so the
-// contacts of notifier a are the sources listed in a's own row.
-__global__ void k_den_scan_csr(const uint32_t* __restrict__ entries, const int32_t* __restrict__ row_len,
-                               int cap, int64_t n, uint8_t* __restrict__ flags) {
-  for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < n;
-       a += (int64_t)gridDim.x * blockDim.x) {
-    if (!(flags[a] & FL_NOTIFIER)) continue;
-    const int len = row_len[a];
-    const uint32_t* e = entries + a * (int64_t)cap;
-    for (int i = 0; i < len; ++i) {
-      const int64_t c = e[i] >> 2;
-      if (!(flags[c] & FL_NOTIFIED))
-        atomicOr((unsigned*)(flags + (c & ~3ll)), (unsigned)FL_NOTIFIED << (8 * (c & 3)));
-    }
-  }
+// Partitioned runs: the notifications pushed by every rank (OR-reduced into
+// `mark`) for the owned rows.
+__global__ void k_den_merge(const uint8_t* __restrict__ mark, int64_t lo, int64_t hi, uint8_t* __restrict__ flags) {
+  for (int64_t a = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < hi; a += (int64_t)gridDim.x * blockDim.x)
+    if (mark[a] & FL_NOTIFIED) flags[a] |= FL_NOTIFIED;
 }
 
 __device__ __forceinline__ void realize_immunity(const StepArgs& A, int64_t a, int dose) {

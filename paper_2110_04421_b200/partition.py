@@ -10,9 +10,9 @@ partial sums per rank, reduced once at the end.
 With exposure notification or vaccination a day
 also needs three in-step exchanges, which the native step requests through
 a callback (epi_set_exchange):
-  * the DEN notifier flags of every rank (all-gather of one byte per owned
-    agent), after which each rank pulls notifications into its own rows
-    (config graphs are symmetric);
+  * the DEN notifications: each rank regenerates the contacts of its own
+    notifiers over the lookback days and marks them, whoever owns them; the
+    marks are OR-reduced over the ranks (one byte per agent);
   * the vaccination eligibility histogram and active count (all-reduce of
     55 integers), so every rank computes the same cut bucket and budget;
   * the cut-bucket count of the lower-ranked (lower-id) ranges (exclusive
@@ -37,7 +37,7 @@ from . import _native as N
 from .errors import ConfigError
 from .sim import ConfigSimulation
 
-_X_GATHER_U8, _X_SUM_U64, _X_EXSCAN_I64 = 1, 2, 3
+_X_GATHER_U8, _X_SUM_U64, _X_EXSCAN_I64, _X_OR_U8 = 1, 2, 3, 4
 
 
 class _DevArray:
@@ -121,6 +121,18 @@ class NcclCodeExchange:
     def sum_(self, t):
         import torch.distributed as dist
         dist.all_reduce(t, group=self.group)
+
+    def or_(self, t):
+        """OR over the ranks of a byte array whose bytes are 0 or one common
+        flag bit (the DEN marks): equal to the MAX, in place."""
+        import torch
+        import torch.distributed as dist
+        if t.is_cuda:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+        else:   # gloo: widen
+            w = t.to(torch.int32)
+            dist.all_reduce(w, op=dist.ReduceOp.MAX, group=self.group)
+            t.copy_(w.to(t.dtype))
 
     def exscan_(self, t):
         """Exclusive prefix sum over the ranks (rank order), in place."""
@@ -218,6 +230,14 @@ class ThreadExchange:
                 t.copy_(acc)
                 ex._done()
 
+            def or_(self, t):
+                ex._post(rank, t.clone())
+                acc = ex.posted[0].clone()
+                for other in ex.posted[1:]:
+                    acc |= other
+                t.copy_(acc)
+                ex._done()
+
             def exscan_(self, t):
                 ex._post(rank, t.clone())
                 acc = torch_zeros_like(t)
@@ -263,6 +283,8 @@ class PartitionedSimulation(ConfigSimulation):
                 self.exchange.sum_(_view(buf, count, "<i8"))    # non-negative counts
             elif kind == _X_EXSCAN_I64:
                 self.exchange.exscan_(_view(buf, count, "<i8"))
+            elif kind == _X_OR_U8:
+                self.exchange.or_(_view(buf, count, "|u1"))
             else:
                 return 1
             return 0

@@ -99,8 +99,8 @@ class ConfigSimulation:
             raise ConfigError(f"unknown mode {mode!r}")
         if precision not in ("f32", "f64"):
             raise ConfigError(f"unknown precision {precision!r}")
-        if mode == "fused" and (precision == "f64" or interventions.den_enabled):
-            raise ConfigError("fused mode is fp32-only and keeps no contact log (DEN)")
+        if mode == "fused" and precision == "f64":
+            raise ConfigError("fused mode is fp32-only")
         self._lib = N.lib()
         self.population = pop
         self.disease, self.table, self.iv = disease, table, interventions

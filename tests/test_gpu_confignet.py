@@ -155,3 +155,22 @@ def test_message_pass_alone_within_1e5_of_reference_hazard(name):
     again = torch.empty_like(lam)
     roofline.gather(sim, again)
     assert torch.equal(again, lam)
+
+
+def test_fused_mode_runs_every_intervention():
+    """DEN needs no contact log (past days' contacts are regenerated), so the
+    fused day kernel runs config 2; same network as csr mode."""
+    iv = InterventionConfig(quarantine_enabled=True, testing_enabled=True,
+                            test_kind=TestKind("cfg2", 0.3, 1, 2), den_enabled=True, den=DenConfig(0.6),
+                            vaccination_enabled=True,
+                            vaccine=VaccinePolicy(daily_rate=0.02, dose1_efficacy=0.5, dose2_efficacy=0.9,
+                                                  dose_gap=7, start_trigger=0.002))
+    spec = ConfigNetworkSpec.config(1, n_agents=20000, initial_infections=60)
+    f = ConfigSimulation.create(spec, seed=6, mode="fused", interventions=iv, horizon=50)
+    c = ConfigSimulation.create(spec, seed=6, mode="csr", interventions=iv, horizon=50)
+    f.run()
+    c.run()
+    rf, rc = f.records(), c.records()
+    assert np.array_equal(rf[:10, 19], rc[:10, 19])
+    for r in (rf, rc):
+        assert r[:, 17].sum() > 0 and r[:, 18].sum() > 0 and r[:, 16].sum() > 0

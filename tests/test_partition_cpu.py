@@ -56,8 +56,11 @@ def _worker(rank, world, port, n, q):
     ex.sum_(hist)
     cut = torch.tensor([5 + 10 * rank], dtype=torch.int64)
     ex.exscan_(cut)
+    marks = torch.zeros(n, dtype=torch.uint8)
+    marks[rank::3] = 4                              # each rank notifies every third agent from its offset
+    ex.or_(marks)
     q.put((rank, codes.numpy().copy(), rec.numpy().copy(), flags.numpy().copy(), hist.numpy().copy(),
-           int(cut[0])))
+           int(cut[0]), marks.numpy().copy()))
     dist.destroy_process_group()
 
 
@@ -81,7 +84,11 @@ def test_code_exchange_and_record_reduction_gloo_world2(n):
         lo, hi = plan.rows(r)
         ids = np.arange(lo, hi)
         want_flags[lo:hi] = (ids % 7 == 0) * (2 + r)
-    for rank, codes, rec, flags, hist, cut in out:
+    want_marks = np.zeros(n, np.uint8)
+    for r in range(world):
+        want_marks[r::3] = 4
+    for rank, codes, rec, flags, hist, cut, marks in out:
+        assert np.array_equal(marks, want_marks)
         assert np.array_equal(flags, want_flags)
         assert np.array_equal(hist, np.arange(55) * 3)
         assert cut == (0 if rank == 0 else 5)
