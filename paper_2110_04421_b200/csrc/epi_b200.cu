@@ -122,6 +122,8 @@ struct epi_ctx {
   int indep = 0;                     // graph-in fp64: independent-edges infection draws
   int32_t* died_at = nullptr;        // DEN on config networks: death step per agent
   uint8_t* den_mark = nullptr;       // DEN, partitioned: notifications pushed by this rank
+  int32_t* den_list = nullptr;       // DEN: the day's notifiers (work list of k_den_regen)
+  int* den_count = nullptr;
   epi_params host{};
   epi_params* P = nullptr;           // device copy
   int64_t n = 0;
@@ -247,7 +249,10 @@ int run_interventions(epi_ctx* c, const StepArgs& A, uint16_t* codes_next, const
   const int threads = 256;
   const int grid = grid_for(n, threads);
   if (p.testing_enabled) {
-    k_iv_tests<<<grid, threads, 0, s>>>(A);
+    // config networks with DEN: the day's notifiers as a work list
+    const bool listed = p.den_enabled && c->den_list != nullptr && c->has_net;
+    if (listed) CK(cudaMemsetAsync(c->den_count, 0, sizeof(int), s));
+    k_iv_tests<<<grid, threads, 0, s>>>(A, listed ? c->den_list : nullptr, listed ? c->den_count : nullptr);
     CKL();
   }
   if (p.den_enabled) {
@@ -397,6 +402,8 @@ int epi_destroy(epi_ctx* c) {
   cudaFree(c->tau_lut);
   cudaFree(c->died_at);
   cudaFree(c->den_mark);
+  cudaFree(c->den_list);
+  cudaFree(c->den_count);
   for (auto* p : c->ntab_dev) cudaFree(p);
   cudaFree(c->wt_host[0].member_at_pos);
   for (auto& w : c->wt_host) {
@@ -834,6 +841,8 @@ int epi_net_attach(epi_ctx* c, const epi_net* net) {
     if (c->host.den_lookback > DEN_MAX_DAYS) return fail(EPI_EARG, "den.lookback > 16 on config networks");
     rc = dalloc(&c->died_at, (size_t)c->n);
     if (!rc) rc = dalloc(&c->den_mark, (size_t)c->n + 4);
+    if (!rc) rc = dalloc(&c->den_list, (size_t)c->n);
+    if (!rc) rc = dalloc(&c->den_count, 1);
     if (rc) return rc;
     k_fill_i32<<<grid_for(c->n, 256), 256>>>(c->died_at, c->n, INT32_MAX);
     CKL();
@@ -1006,15 +1015,16 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
       D.n_days = step - D.first_day;
       if (D.n_days <= 0) return 0;
       for (int d = 0; d < D.n_days; ++d) D.nk[d] = make_net_keys(seed, D.first_day + d);
-      const int g = grid_for((c->hi - c->lo + 31) / 32 * 32, 256);
+      if (!c->host.testing_enabled) return 0;           // no test results, no notifiers
+      const int g = sm_count() * 8;                    // persistent: items read on the device
       if (!part) {
-        k_den_regen<<<g, 256, 0, s>>>(c->net, D, c->died_at, c->flags, c->flags, c->lo, c->hi);
+        k_den_regen<<<g, 256, 0, s>>>(c->net, D, c->died_at, c->den_list, c->den_count, c->flags);
         CKL();
         return 0;
       }
       // partitioned: contacts may be anyone's; OR the ranks' marks together
       CK(cudaMemsetAsync(c->den_mark, 0, (size_t)c->n, s));
-      k_den_regen<<<g, 256, 0, s>>>(c->net, D, c->died_at, c->flags, c->den_mark, c->lo, c->hi);
+      k_den_regen<<<g, 256, 0, s>>>(c->net, D, c->died_at, c->den_list, c->den_count, c->den_mark);
       CKL();
       int rc2 = exchange(c, EPI_X_OR_U8, c->den_mark, c->n, s);
       if (rc2) return rc2;

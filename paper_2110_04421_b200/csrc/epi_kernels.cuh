@@ -887,7 +887,9 @@ __global__ void __launch_bounds__(256) k_day_tables(epi_net net, NetKeys nk, Wor
 // Intervention phases (engine.py:202-347).
 
 // Phase 3 + 4a: test sampling, then delivery (engine.py:202-242).
-__global__ void k_iv_tests(StepArgs A) {
+// Notifiers are also appended to `notif` (count in *n_notif) when given:
+// the work list of the DEN regeneration scan.
+__global__ void k_iv_tests(StepArgs A, int32_t* __restrict__ notif = nullptr, int* n_notif = nullptr) {
   __shared__ RecAcc racc;
   rec_init(racc);
   __syncthreads();
@@ -927,7 +929,10 @@ __global__ void k_iv_tests(StepArgs A) {
             st.quarantine_until[a] = step + P->quarantine_duration;
             st.quarantine_started_at[a] = step;
           }
-          if (P->den_enabled && st.has_den_app[a]) fl |= FL_NOTIFIER;
+          if (P->den_enabled && st.has_den_app[a]) {
+            fl |= FL_NOTIFIER;
+            if (notif) notif[atomicAdd(n_notif, 1)] = (int32_t)a;
+          }
         }
       }
       A.flags[a] = fl;
@@ -956,8 +961,9 @@ __global__ void k_den_scan_coo(const int32_t* __restrict__ src, const int32_t* _
 // notifier's contacts of the last `lookback` days are enumerated again
 // instead of being stored: for day s an agent is in the networks iff it had
 // not died before s (died_at[c] >= s), and its random-slot count is the keyed
-// draw of day s.  One warp per notifier and day (lanes split the household,
-// colleague draws and random slots), contacts marked NOTIFIED.  The marks
+// draw of day s.  One warp per (notifier, day) of the day's notifier list
+// (lanes split the household, colleague draws and random slots), contacts
+// marked NOTIFIED.  The marks
 // equal those of a scan over the stored edges of those days (ContactLog,
 // interventions.py:145-178), without the 4 B/edge/day log.
 constexpr int DEN_MAX_DAYS = 16;
@@ -975,37 +981,33 @@ __global__ void k_died_update(const uint16_t* __restrict__ codes, int64_t n, int
 }
 
 __global__ void __launch_bounds__(256) k_den_regen(epi_net net, DenRegen D, const int32_t* __restrict__ died_at,
-                                                   const uint8_t* __restrict__ flags, uint8_t* __restrict__ mark,
-                                                   int64_t lo, int64_t hi) {
+                                                   const int32_t* __restrict__ notif, const int* n_notif,
+                                                   uint8_t* __restrict__ mark) {
   __shared__ Radix wrad[256];
   __shared__ PermKeys rk[8][EPI_MAX_SLOTS];
   for (int m = threadIdx.x; m < 256; m += blockDim.x) wrad[m] = make_radix(m < 1 ? 1u : (uint32_t)m);
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = lane_id();
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t base = lo + (blockIdx.x * (int64_t)(blockDim.x >> 5) + warp) * 32; base < hi; base += warps * 32) {
-    const int64_t a = base + lane;
-    unsigned m = __ballot_sync(0xFFFFFFFFu, a < hi && (flags[a] & FL_NOTIFIER));
-    while (m) {
-      const int64_t an = base + __ffs(m) - 1;
-      m &= m - 1;
-      for (int d = 0; d < D.n_days; ++d) {
-        const int day = D.first_day + d;
-        const NetKeys& nk = D.nk[d];
-        if (lane < net.random_slots) rk[warp][lane] = random_slot_keys(nk.rperm, lane);
-        __syncwarp();
-        auto code_of = [&](int64_t c) -> uint16_t {
-          if (died_at[c] < day) return CODE_DEAD;
-          return (uint16_t)(random_count(net, nk.rcount, c) << 8);
-        };
-        for_each_in_edge_f(net, nk, rk[warp], wrad, code_of, an, code_of(an), lane, 32,
-                           [&](int64_t c, int, uint16_t) {
-                             if (!(mark[c] & FL_NOTIFIED))
-                               atomicOr((unsigned*)(mark + (c & ~3ll)), (unsigned)FL_NOTIFIED << (8 * (c & 3)));
-                           });
-        __syncwarp();
-      }
-    }
+  // one warp per (notifier, day)
+  const int64_t items = (int64_t)(*n_notif) * D.n_days;
+  for (int64_t it = blockIdx.x * (int64_t)(blockDim.x >> 5) + warp; it < items; it += warps) {
+    const int64_t an = notif[it / D.n_days];
+    const int d = (int)(it % D.n_days);
+    const int day = D.first_day + d;
+    const NetKeys& nk = D.nk[d];
+    if (lane < net.random_slots) rk[warp][lane] = random_slot_keys(nk.rperm, lane);
+    __syncwarp();
+    auto code_of = [&](int64_t c) -> uint16_t {
+      if (died_at[c] < day) return CODE_DEAD;
+      return (uint16_t)(random_count(net, nk.rcount, c) << 8);
+    };
+    for_each_in_edge_f(net, nk, rk[warp], wrad, code_of, an, code_of(an), lane, 32,
+                       [&](int64_t c, int, uint16_t) {
+                         if (!(mark[c] & FL_NOTIFIED))
+                           atomicOr((unsigned*)(mark + (c & ~3ll)), (unsigned)FL_NOTIFIED << (8 * (c & 3)));
+                       });
+    __syncwarp();
   }
 }
 
