@@ -141,7 +141,7 @@ class GpuEngine:
         self._vax.fill_(int(bool(value)))
 
     # -- graph upload + validation (engine.py:124-133) ----------------------
-    def _load(self, graph):
+    def _load(self, graph, check: bool = True):
         import torch
         if graph.on_device:
             src, dst, kind = graph.src, graph.dst, graph.kind
@@ -153,10 +153,19 @@ class GpuEngine:
         s = N.stream_handle()
         N.check(self._lib.epi_graph_load(self._ctx, N.ptr(src), N.ptr(dst), N.ptr(kind),
                                          int(src.shape[0]), s))
+        if check:
+            self.check_graph_flags(graph)
+
+    def check_graph_flags(self, graph=None):
+        """Raise for the validation flags the graph loads set (engine.py:124-133);
+        reads and clears the device flag word (a host sync)."""
+        s = N.stream_handle()
         flags = N._i32()
         N.check(self._lib.epi_read_flags(self._ctx, C_ref(flags), s))
         f = flags.value
         if f & N.FLAG_INDEX:
+            if graph is None:
+                raise InvariantViolation(f"a graph references an agent >= n_agents {self.n}")
             h = graph.to_host()
             top = max(int(np.max(h.src)), int(np.max(h.dst)))
             raise InvariantViolation(f"graph references agent {top} >= n_agents {self.n}")
@@ -212,6 +221,24 @@ class GpuEngine:
         ev = StepEvents.from_record(rec)
         self.clock += 1
         return ev
+
+    def advance(self, graph, record) -> None:
+        """`step` for device-resident pipelines: no host synchronisation.  The
+        day's record goes to the device int64[EPI_REC_LEN] tensor `record`
+        (StepEvents.from_record reads it later); graph validation flags
+        accumulate until `check_graph_flags()`."""
+        if graph.step != self.clock:
+            raise InvariantViolation(
+                f"graph built for step {graph.step}, engine clock is {self.clock}")
+        if not self.resident:
+            raise InvariantViolation("advance() needs resident=True")
+        self._load(graph, check=False)
+        st = self.dev.struct()
+        N.check(self._lib.epi_step(self._ctx, C_ref(st), int(self.clock), _u64(self.seed),
+                                   N.ptr(record), N.ptr(self._vax), None, 0, N.stream_handle()))
+        if self.contact_log is not None:
+            self.contact_log._pushed()
+        self.clock += 1
 
     def step_with_hazard(self, hazard, injected=None) -> StepEvents:
         """Phases 1-6 with a caller-supplied float64 hazard (parity tests)."""

@@ -106,8 +106,10 @@ class GpuRealizer:
             self._lib.epi_refnet_destroy(h)
             self._h = None
 
-    def realize(self, step: int, dead) -> StepGraph:
-        """Edges of `step` for the given dead mask (bool[N], numpy or torch)."""
+    def realize(self, step: int, dead, copy: bool = True) -> StepGraph:
+        """Edges of `step` for the given dead mask (bool[N], numpy or torch).
+        copy=False returns views of the realizer's buffers, valid until the
+        next call (a consumer that loads the graph at once)."""
         import torch
         if isinstance(dead, np.ndarray):
             dead_t = torch.from_numpy(np.ascontiguousarray(dead, dtype=np.uint8)).to(self.device)
@@ -118,4 +120,6 @@ class GpuRealizer:
                                              N.ptr(self._src), N.ptr(self._dst), N.ptr(self._kind),
                                              self.capacity, ctypes.byref(e), N.stream_handle()))
         m = int(e.value)
+        if not copy:
+            return StepGraph(step, self._src[:m], self._dst[:m], self._kind[:m])
         return StepGraph(step, self._src[:m].clone(), self._dst[:m].clone(), self._kind[:m].clone())

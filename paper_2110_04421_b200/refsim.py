@@ -19,8 +19,9 @@ from __future__ import annotations
 
 import time
 
+from . import _native as N
 from .defaults import default_disease, default_progression
-from .engine import GpuEngine
+from .engine import GpuEngine, StepEvents
 from .interventions import InterventionConfig
 from .keyed import replication_seed
 from .population import PopulationSpec, choose_seeds, synthesize
@@ -56,6 +57,7 @@ class ReferenceNativeSimulation:
                                     self.spec.occupation_mean_interactions, self.spec.rewire_beta,
                                     device=device)
         self.interactions = 0
+        self.records = torch.zeros((horizon, N.REC_LEN), dtype=torch.int64, device=self.engine.device)
 
     @property
     def clock(self) -> int:
@@ -70,7 +72,16 @@ class ReferenceNativeSimulation:
         return ev
 
     def run(self, steps: int | None = None):
-        out = []
-        for _ in range(self.horizon - self.clock if steps is None else steps):
-            out.append(self.step())
-        return out
+        """The remaining steps with the state and the records on the device:
+        one host synchronisation per step (the realized edge count the sort
+        needs); graph flags checked once at the end.  Returns the StepEvents."""
+        first = self.clock
+        last = self.horizon if steps is None else min(self.horizon, first + steps)
+        for t in range(first, last):
+            dead = self.engine.dev.t["stage"] == 10
+            self.engine.advance(self.realizer.realize(t, dead, copy=False), self.records[t])
+        self.engine.check_graph_flags()
+        rec = self.records[first:last].cpu().numpy()
+        events = [StepEvents.from_record(r) for r in rec]
+        self.interactions += sum(ev.n_edges for ev in events)
+        return events

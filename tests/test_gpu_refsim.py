@@ -57,3 +57,17 @@ def test_device_loop_bitwise_vs_oracle(name):
               "vaccine_status", "immune"):
         assert np.array_equal(getattr(sim.cols, c), getattr(cols_o, c)), c
     assert sim.interactions > 0
+
+
+def test_device_resident_run_equals_step_by_step():
+    """run() (records on the device, one sync per step) == step() events."""
+    import dataclasses as dc
+    tr = Trajectory("noiv")
+    a, b = _sim(tr), _sim(tr)
+    ev_a = [a.step() for _ in range(20)]
+    ev_b = b.run(20)
+    assert [dc.astuple(x) for x in ev_a] == [dc.astuple(x) for x in ev_b]
+    a.engine.sync_to_host()
+    b.engine.sync_to_host()
+    assert np.array_equal(a.cols.stage, b.cols.stage)
+    assert a.interactions == b.interactions
