@@ -573,8 +573,8 @@ def run_config3(a):
             "config": {"workload": "config3 (BASELINE.json configs[3]): 10M agents, config-1 "
                        "networks, 180 days, fused mode", "parallelism": f"agent ranges x{world}, "
                        "NCCL all-gather of 16-bit codes per day" if world > 1 else "1 GPU",
-                       "l2": "inputs (10M-agent state, 20 MB codes) exceed nothing; L2 not flushed "
-                       "between days"},
+                       "l2": "not flushed: every day touches the 10M-agent state (~160 MB hot, "
+                       "700 MB total) and tables, more than the 126 MB L2"},
             "wall_s_per_sim": ms / a.steps / 1e3, "clocks": clocks}), flush=True)
 
 
@@ -652,7 +652,9 @@ def run_config4(a):
             "config": {"workload": f"config4 (BASELINE.json configs[4]): {reps} replicas of config 1 "
                        "(shared static population, own seed, rate 3.3x[0.5,1.5]); one step = all "
                        "replicas x 180 days", "parallelism": f"{a.replicas} replicas/GPU on "
-                       f"{a.streams} streams x {world} GPUs"},
+                       f"{a.streams} streams x {world} GPUs",
+                       "l2": "not flushed: the replicas' states and push tables (~20 MB each) "
+                       "exceed the 126 MB L2 many times over"},
             "replica_steps_per_s": reps * HORIZON * a.steps / (ms / 1e3),
             "daily_new_infections_mean": [round(float(x), 2) for x in mean],
             "daily_new_infections_std": [round(float(x), 2) for x in std],
