@@ -602,8 +602,10 @@ def run_config4(a):
         r = rank * a.replicas + i
         u = keyed.uniform(0, 0, keyed.Purpose.REPLICATION, r, k=1)
         d = d0.with_rate(d0.rate_scale * (0.5 + u))
+        # concurrent replicas on 8 streams: per-day kernels (a persistent run
+        # needs the whole GPU resident for its grid barrier)
         sims.append(ConfigSimulation(pop, d, t, iv, keyed.replication_seed(0, r), mode="fused",
-                                     horizon=HORIZON))
+                                     horizon=HORIZON, persistent=False))
     streams = [torch.cuda.Stream() for _ in range(a.streams)]
     for s in sims:
         s.capture()

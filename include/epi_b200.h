@@ -313,6 +313,12 @@ int epi_sim_run(epi_ctx *ctx, const epi_state *st, int32_t first_step, int32_t n
                 uint64_t seed, int32_t mode, int32_t precision, uint16_t *codes0,
                 uint16_t *codes1, int64_t *records, int32_t *vax_open, void *stream);
 
+/* epi_sim_run sends the days of a merged fused run (mode 1, fp32, no
+ * interventions, whole population) to one persistent launch (k_fused_run:
+ * one resident thread per agent, a grid barrier per day); bitwise the same
+ * results as the per-day kernels.  on = 0 forces the per-day kernels. */
+int epi_set_persistent(epi_ctx *ctx, int32_t on);
+
 /* epi_sim_step that also records 4 caller-created cudaEvent_t: before the
  * generator, before the message pass, after it, after the intervention
  * phases — per-kernel device times for the roofline (bench.py). */

@@ -15,6 +15,7 @@
 
 #include "epi_kernels.cuh"
 #include "epi_msgpass.cuh"
+#include "epi_persistent.cuh"
 #include "epi_population.cuh"
 #include "epi_refnet.cuh"
 
@@ -170,6 +171,7 @@ struct epi_ctx {
                                      //   0 csr (ids), 1 fused partitioned, 2 fused whole
   int merged_ready = -1;             // day whose tables the previous merged kernel built
   Injected* inj_dev = nullptr;
+  int persistent = 1;                // epi_sim_run: one launch for the merged days
 };
 
 namespace {
@@ -1045,11 +1047,85 @@ int epi_sim_step(epi_ctx* c, const epi_state* st, int32_t step, uint64_t seed, i
                        nullptr, stream);
 }
 
+// Can the merged days of a run go to k_fused_run (one co-resident thread per
+// agent)?  Same conditions as the merged per-day path plus residency.
+static bool persistent_ok(epi_ctx* c, int32_t mode, int32_t precision) {
+  if (!c->persistent || mode != 1 || precision != EPI_F32 || interventions_on(c->host)) return false;
+  if (partitioned(c) || c->net.n_agents < 2 || c->net.random_slots != RT_SLOTS || !batched(&c->net) ||
+      !push_fits(c) || c->net.colleague_draws > 8)
+    return false;
+  static int per_sm = -1;
+  if (per_sm < 0 &&
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fused_run, RUN_THREADS, 0) != cudaSuccess)
+    per_sm = 0;
+  return (c->n + RUN_THREADS - 1) / RUN_THREADS <= (int64_t)per_sm * sm_count();
+}
+
+static int launch_run(epi_ctx* c, const epi_state* st, int32_t first, int32_t n_days, uint64_t seed,
+                      uint16_t* codes0, uint16_t* codes1, int64_t* records, cudaStream_t s) {
+  RunArgs R{};
+  R.P = c->P;
+  R.st = *st;
+  R.seed = seed;
+  R.first_step = first;
+  R.n_days = n_days;
+  R.records = (long long*)records;
+  R.codes[0] = codes0;
+  R.codes[1] = codes1;
+  R.wt[0] = c->wt_host[0];
+  R.wt[1] = c->wt_host[1];
+  R.ring_t2 = c->ntab_dev[(first + n_days + 1) % 3];
+  R.mt = (const MsgTables*)c->msg_dev;
+  R.tau_lut = c->tau_lut;
+  R.dn = c->ntab.dn;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)((c->n + RUN_THREADS - 1) / RUN_THREADS));
+  cfg.blockDim = dim3(RUN_THREADS);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeCooperative;     // every block resident: the grid barrier is safe
+  attr[0].val.cooperative = 1;
+  cfg.numAttrs = 1;
+  if (c->hot.bytes > 0) {
+    attr[1].id = cudaLaunchAttributeAccessPolicyWindow;
+    attr[1].val.accessPolicyWindow.base_ptr = const_cast<void*>(c->hot.base);
+    attr[1].val.accessPolicyWindow.num_bytes = c->hot.bytes;
+    attr[1].val.accessPolicyWindow.hitRatio = c->hot.hit_ratio;
+    attr[1].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr[1].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    cfg.numAttrs = 2;
+  }
+  cfg.attrs = attr;
+  CK(cudaLaunchKernelEx(&cfg, k_fused_run, R, c->net));
+  c->merged_ready = first + n_days;
+  return 0;
+}
+
+int epi_set_persistent(epi_ctx* c, int32_t on) {
+  if (!c) return fail(EPI_EARG, "null ctx");
+  c->persistent = on != 0;
+  return 0;
+}
+
 int epi_sim_run(epi_ctx* c, const epi_state* st, int32_t first_step, int32_t n_days, uint64_t seed,
                 int32_t mode, int32_t precision, uint16_t* codes0, uint16_t* codes1, int64_t* records,
                 int32_t* vax_open, void* stream) {
   if (!c || !records || !codes0 || !codes1 || n_days < 0) return fail(EPI_EARG, "bad argument");
   CK(cudaMemsetAsync(records, 0, (size_t)n_days * EPI_REC_LEN * sizeof(int64_t), S(stream)));
+  if (n_days >= 2 && c->has_net && st && st->n_agents == c->n && persistent_ok(c, mode, precision)) {
+    // the first day on the per-day path builds the day's tables (unless a
+    // previous merged day already did); every later day in one launch
+    int d0 = 0;
+    if (c->merged_ready != first_step) {
+      const int t = first_step;
+      int rc = sim_step_impl(c, st, t, seed, mode, precision, (t & 1) ? codes1 : codes0, (t & 1) ? codes0 : codes1,
+                             records, vax_open, nullptr, stream, false);
+      if (rc) return rc;
+      d0 = 1;
+    }
+    return launch_run(c, st, first_step + d0, n_days - d0, seed, codes0, codes1,
+                      records + (size_t)d0 * EPI_REC_LEN, S(stream));
+  }
   for (int d = 0; d < n_days; ++d) {
     const int t = first_step + d;
     uint16_t* cur = (t & 1) ? codes1 : codes0;

@@ -182,11 +182,12 @@ __device__ __forceinline__ AgentHot load_hot(const epi_state& st, int64_t a) {
 // Phases 1-2 on preloaded state (updated in place, and written through).
 // `forced` >= 0: the infection decision was already drawn per edge
 // (independent-edges mode) and replaces the aggregate draw.
-__device__ __forceinline__ unsigned transmit_progress_hot(const StepArgs& A, int64_t a, double lam, int forced,
-                                                          AgentHot& h) {
-  const epi_params* __restrict__ P = A.P;
-  const epi_state& st = A.st;
-  const int step = A.step;
+// The core takes the step's key prefixes explicitly (kernel parameter or, in
+// the persistent run, shared memory).
+__device__ __forceinline__ unsigned transmit_progress_core(const epi_params* __restrict__ P, const epi_state& st,
+                                                           const StepKeys& K, const Injected* inj, int step,
+                                                           const uint16_t* __restrict__ tau_lut, int64_t a,
+                                                           double lam, int forced, AgentHot& h) {
   unsigned ev = 0;
   if (h.stage == S_SUS && !(P->sterilizing && h.immune)) {
     // lam == 0 gives p == 0 and u < p never holds: skip the draw
@@ -195,14 +196,14 @@ __device__ __forceinline__ unsigned transmit_progress_hot(const StepArgs& A, int
       infect = forced != 0;
     } else {
       const double p = 1.0 - exp(-lam);
-      infect = lam > 0.0 && draw(A.K, A.inj, P_INFECTION, a) < p;
+      infect = lam > 0.0 && draw(K, inj, P_INFECTION, a) < p;
     }
     if (infect) {
-      int entry = P->targets[S_SUS][pick_branch(P, S_SUS, h.age, draw(A.K, A.inj, P_ENTRY, a))];
+      int entry = P->targets[S_SUS][pick_branch(P, S_SUS, h.age, draw(K, inj, P_ENTRY, a))];
       if (!P->sterilizing && h.immune) entry = S_ASYM;
       int nxt, delay;
-      schedule(P, entry, h.age, draw(A.K, A.inj, P_BRANCH, a), draw(A.K, A.inj, P_DELAY, a), nxt, delay,
-               A.tau_lut);
+      schedule(P, entry, h.age, draw(K, inj, P_BRANCH, a), draw(K, inj, P_DELAY, a), nxt, delay,
+               tau_lut);
       h.stage = entry;
       h.infected_at = step;
       h.next_stage = nxt;
@@ -226,8 +227,8 @@ __device__ __forceinline__ unsigned transmit_progress_hot(const StepArgs& A, int
       h.nta = NEVER;
     } else {
       int nxt, delay;
-      schedule(P, dest, h.age, draw(A.K, A.inj, P_BRANCH, a), draw(A.K, A.inj, P_DELAY, a), nxt, delay,
-               A.tau_lut);
+      schedule(P, dest, h.age, draw(K, inj, P_BRANCH, a), draw(K, inj, P_DELAY, a), nxt, delay,
+               tau_lut);
       h.next_stage = nxt;
       h.nta = step + delay;
     }
@@ -235,6 +236,11 @@ __device__ __forceinline__ unsigned transmit_progress_hot(const StepArgs& A, int
     st.next_transition_at[a] = h.nta;
   }
   return ev;
+}
+
+__device__ __forceinline__ unsigned transmit_progress_hot(const StepArgs& A, int64_t a, double lam, int forced,
+                                                          AgentHot& h) {
+  return transmit_progress_core(A.P, A.st, A.K, A.inj, A.step, A.tau_lut, a, lam, forced, h);
 }
 
 __device__ __forceinline__ unsigned transmit_progress(const StepArgs& A, int64_t a, double lam,

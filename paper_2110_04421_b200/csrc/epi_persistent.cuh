@@ -1,0 +1,280 @@
+// Persistent fused run: every day of a config-network simulation in ONE
+// launch (epi_sim_run, merged fused mode: no interventions, whole population,
+// push tables).  One thread per agent for the whole run and a grid barrier
+// between days, so what the per-day kernel (k_fused_step) reloads every day
+// stays in registers:
+//   - the agent's static network data (household range, workplace id, slot,
+//     size, base) and its state (AgentHot), written through on change only;
+//   - its own code and its workplace position of the day (computed by itself
+//     in the previous day's epilogue), which removes the two deepest levels
+//     of the per-day load chain (wp_id -> wp_size/base -> pos_of -> wcode);
+//   - the message tables; the day's key prefixes are computed on the device
+//     into shared memory while the block waits at the barrier.
+// Arithmetic, visit order and sums are those of k_fused_step with
+// push_kind_sums, so results are bitwise identical to the per-day path
+// (tests/test_gpu_persistent.py).
+//
+// Data written inside the kernel (codes, push tables) is read with plain
+// coherent loads, never through the read-only (.nc) path; the colleague
+// shifts are hashed in registers instead of read from the shift table.
+#pragma once
+
+#include <cooperative_groups.h>
+
+#include "epi_kernels.cuh"
+
+namespace epi {
+
+struct DayKeys {
+  StepKeys K;                     // purposes of day t
+  uint64_t wshift;                // P_NET_WSHIFT of day t (the colleague shifts, computed)
+  uint64_t rcount_next;           // P_NET_RCOUNT of t + 1 (tomorrow's codes)
+  uint64_t wperm_next, wshift_next;
+  PermKeys rk_next[RT_SLOTS];     // random-slot keys of t + 1 (tomorrow's push rows)
+};
+
+// one warp fills the keys of day t
+__device__ __forceinline__ void day_keys(DayKeys& D, uint64_t seed, int t, int lane) {
+  if (lane < 12) D.K.p[lane] = key_prefix(seed, t, lane);
+  else if (lane == 12) D.rcount_next = key_prefix(seed, t + 1, P_NET_RCOUNT);
+  else if (lane == 13) D.wperm_next = key_prefix(seed, t + 1, P_NET_WPERM);
+  else if (lane == 14) D.wshift_next = key_prefix(seed, t + 1, P_NET_WSHIFT);
+  else if (lane == 15) D.wshift = key_prefix(seed, t, P_NET_WSHIFT);
+  else if (lane >= 16) D.rk_next[lane - 16] = random_slot_keys(key_prefix(seed, t + 1, P_NET_RPERM), lane - 16);
+}
+
+struct RunArgs {
+  const epi_params* P;
+  epi_state st;
+  uint64_t seed;
+  int first_step, n_days;
+  long long* records;             // [n_days][EPI_REC_LEN], zeroed
+  uint16_t* codes[2];             // by day parity
+  WorkTables wt[2];               // push tables by day parity
+  NetTables* ring_t2;             // rk of day first+n_days+1 (keeps the merged chain resumable)
+  const MsgTables* mt;
+  const uint16_t* tau_lut;
+  Radix dn;
+};
+
+// sums of the day's rows into the day's record, rows zeroed for tomorrow
+__device__ __forceinline__ void rec_flush_day(RecAcc& s, long long* rec, int step) {
+  __syncthreads();
+  if (blockIdx.x == 0 && threadIdx.x == 0) rec[EPI_REC_STEP] = step;
+  const int nw = (blockDim.x + 31) >> 5;
+  for (int i = threadIdx.x; i < EPI_REC_LEN; i += blockDim.x) {
+    unsigned long long t = 0;
+    if (i == EPI_REC_FLAGS) {
+      for (int w = 0; w < nw; ++w) { t |= s.v[w][i]; s.v[w][i] = 0u; }
+      if (t) atomicOr((unsigned long long*)&rec[i], t);
+    } else {
+      for (int w = 0; w < nw; ++w) { t += s.v[w][i]; s.v[w][i] = 0u; }
+      if (t) atomicAdd((unsigned long long*)&rec[i], t);
+    }
+  }
+}
+
+constexpr int RUN_THREADS = 128;
+// loads of data written during the run: plain (coherent) global loads; the
+// grid barrier orders them after the writers' stores
+template <class T> __device__ __forceinline__ T LDM(const T* p) { return *p; }
+
+__global__ void __launch_bounds__(RUN_THREADS, 6) k_fused_run(RunArgs R, epi_net net) {
+  constexpr int HH = 8, DR = 8;
+  __shared__ MsgTables T;
+  __shared__ RecAcc racc;
+  __shared__ DayKeys dk[2];
+  __shared__ int excl_s[RUN_THREADS / 32][32];
+  __shared__ uint16_t cn_s[RUN_THREADS / 32][32];
+  load_msg_tables(T, R.mt);
+  rec_init(racc);
+  const int warp = threadIdx.x >> 5, lane = lane_id();
+  if (warp == 0) day_keys(dk[0], R.seed, R.first_step, lane);
+  const int64_t n = net.n_agents;
+  const int64_t b = blockIdx.x * (int64_t)RUN_THREADS + threadIdx.x;
+  const bool valid = b < n;
+  const uint32_t self = (uint32_t)b;
+  const int draws = net.colleague_draws;
+  // static network data and the agent's state, once
+  int off = 0, sz = 0, w = -1, loc = 0, m = 0, base = 0;
+  AgentHot h{};
+  uint16_t cb = CODE_DEAD;
+  uint32_t p = 0;
+  if (valid) {
+    off = net.hh_off[b];
+    sz = net.hh_size[b];
+    w = net.wp_id[b];
+    loc = net.wp_local[b];
+    h = load_hot(R.st, b);
+    cb = LDM(R.codes[R.first_step & 1] + b);
+    if (w >= 0) {
+      m = net.wp_size[w];
+      base = net.wp_base[w];
+      if (m >= 2) p = LDM(R.wt[R.first_step & 1].pos_of + base + loc);
+    }
+  }
+  const bool works = w >= 0 && m >= 2;
+  const int64_t start = b - off;
+  const Radix rm = make_radix(works ? (uint32_t)m : 1u);
+  __syncthreads();
+  for (int d = 0; d < R.n_days; ++d) {
+    const int t = R.first_step + d;
+    const int par = t & 1;
+    const DayKeys& D = dk[d & 1];
+    const uint16_t* codes = R.codes[par];
+    uint16_t* codes_next = R.codes[par ^ 1];
+    const WorkTables& W = R.wt[par];
+    const WorkTables& Wn = R.wt[par ^ 1];
+    unsigned edges = 0;
+    double lam = 0.0;
+    if (valid) {
+      // rows of the day (level 1)
+      const uint4* ri = (const uint4*)(W.rin + (size_t)b * RT_SLOTS);
+      const uint4 in0 = LDM(ri), in1 = LDM(ri + 1);
+      if (!code_dead(cb)) {
+        const uint4* ro = (const uint4*)(W.rout + (size_t)b * RT_SLOTS);
+        const int nb = code_count(cb);
+        const int nbe = nb < RT_SLOTS ? nb : RT_SLOTS;
+        const uint4 o0 = nbe > 0 ? LDM(ro) : make_uint4(self, self, self, self);
+        uint16_t hc[HH];
+#pragma unroll
+        for (int i = 0; i < HH; ++i)
+          hc[i] = (i < sz && start + i != b) ? LDM(codes + start + i) : (uint16_t)CODE_DEAD;
+        // the day's colleague shifts r_j (work_shift), four per hash
+        uint32_t sh[DR];
+        if (works) {
+          const uint64_t hw = fold(D.wshift, (uint64_t)w);
+#pragma unroll
+          for (int j4 = 0; j4 < DR; j4 += 4) {
+            const uint64_t hq = fold(hw, (uint64_t)(j4 >> 2));
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              sh[j4 + q] = 1u + ((((uint32_t)(hq >> (16 * q))) & 0xFFFFu) * (uint32_t)(m - 1) >> 16);
+          }
+        }
+        // level 2
+        const uint32_t po0[4] = {o0.x, o0.y, o0.z, o0.w};
+        uint16_t co0[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          co0[q] = (q < nbe && po0[q] != self) ? LDM(codes + po0[q]) : (uint16_t)CODE_DEAD;
+        uint16_t wo[DR], wi[DR];
+#pragma unroll
+        for (int j = 0; j < DR; ++j) {
+          wo[j] = wi[j] = (uint16_t)CODE_DEAD;
+          if (works && j < draws) {
+            const uint32_t r = sh[j];
+            wo[j] = LDM(W.wcode + base + add_mod(p, r, (uint32_t)m));
+            wi[j] = LDM(W.wcode + base + sub_mod(p, r, (uint32_t)m));
+          }
+        }
+        // per-kind sums in the visit order of for_each_in_code
+        float acc[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+        for (int i = 0; i < HH; ++i)
+          if (!code_dead(hc[i])) { acc[0] += T.factor[hc[i] & 0xFF]; ++edges; }
+        for (int i = HH; i < sz; ++i) {
+          if (start + i == b) continue;
+          const uint16_t cc = LDM(codes + start + i);
+          if (!code_dead(cc)) { acc[0] += T.factor[cc & 0xFF]; ++edges; }
+        }
+#pragma unroll
+        for (int j = 0; j < DR; ++j) {
+          if (!code_dead(wo[j])) { acc[1] += T.factor[wo[j] & 0xFF]; ++edges; }
+          if (!code_dead(wi[j])) { acc[1] += T.factor[wi[j] & 0xFF]; ++edges; }
+        }
+        if (n >= 2) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (!code_dead(co0[q])) { acc[2] += T.factor[co0[q] & 0xFF]; ++edges; }
+          for (int j0 = 4; j0 < nbe; j0 += 4) {
+            const uint4 o = LDM(ro + (j0 >> 2));
+            const uint32_t po[4] = {o.x, o.y, o.z, o.w};
+            uint16_t co[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              co[q] = (j0 + q < nbe && po[q] != self) ? LDM(codes + po[q]) : (uint16_t)CODE_DEAD;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              if (!code_dead(co[q])) { acc[2] += T.factor[co[q] & 0xFF]; ++edges; }
+          }
+          const uint4 inv[2] = {in0, in1};
+          const uint16_t* iv = (const uint16_t*)inv;
+#pragma unroll
+          for (int j = 0; j < RT_SLOTS; ++j)
+            if (iv[j] & CODE_PRESENT) { acc[2] += T.factor[iv[j] & 0xFF]; ++edges; }
+        }
+        const float tot = acc[0] * T.bfac[0] + acc[1] * T.bfac[1] + acc[2] * T.bfac[2];
+        if (h.stage == S_SUS && !(R.P->sterilizing && h.immune)) lam = (double)(tot * T.sfac[h.age]);
+      }
+      // the consumed row starts empty (it is written again two days on)
+      uint4* rw = (uint4*)(W.rin + (size_t)b * RT_SLOTS);
+      rw[0] = make_uint4(0, 0, 0, 0);
+      rw[1] = make_uint4(0, 0, 0, 0);
+    }
+    unsigned ev = 0;
+    if (valid) ev = transmit_progress_core(R.P, R.st, D.K, nullptr, t, R.tau_lut, b, lam, -1, h);
+    rec_events(racc, ev);
+    rec_add(racc, EPI_REC_EDGES, edges);
+    rec_agent(racc, valid, valid ? h.stage : 0, valid ? h.infected_at : 0);
+    // tomorrow's code
+    uint16_t cn = 0;
+    if (valid) {
+      cn = source_code(R.P, h.stage, h.infected_at, h.q_until, t + 1);
+      if (h.stage == S_DEAD) cn |= CODE_DEAD;
+      else cn |= (uint16_t)(random_count(net, D.rcount_next, b) << 8);
+      codes_next[b] = cn;
+    }
+    // tomorrow's push tables: the worker's position and its code there
+    if (valid && works) {
+      const uint32_t q = walk_inv((uint32_t)loc, work_keys(D.wperm_next, w), rm);
+      Wn.wcode[base + q] = cn;
+      p = q;
+      if (d + 1 == R.n_days) {         // position and shift tables for the per-day path
+        Wn.pos_of[base + loc] = (uint8_t)q;
+        for (int j = loc; j < draws; j += m)
+          Wn.shift[(size_t)w * draws + j] = (uint8_t)work_shift(D.wshift_next, w, j, m);
+      }
+    }
+    // random: flatten the warp's (agent, slot < n) items, 32 at a time
+    {
+      int na = valid ? code_count(cn) : 0;
+      na = na < RT_SLOTS ? na : RT_SLOTS;
+      int incl = na;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+      excl_s[warp][lane] = incl - na;
+      cn_s[warp][lane] = cn;
+      __syncwarp();
+      const int64_t wbase_agent = b - lane;
+      for (int k = lane; k < total; k += 32) {
+        int l = 0;
+#pragma unroll
+        for (int st = 16; st >= 1; st >>= 1)
+          if (l + st < 32 && excl_s[warp][l + st] <= k) l += st;
+        const int j = k - excl_s[warp][l];
+        const uint32_t src = (uint32_t)(wbase_agent + l);
+        const uint32_t y = walk_fwd(src, D.rk_next[j], R.dn);
+        Wn.rout[(size_t)src * RT_SLOTS + j] = y;
+        if (y != src) Wn.rin[(size_t)y * RT_SLOTS + j] = cn_s[warp][l] | CODE_PRESENT;
+      }
+    }
+    cb = cn;
+    rec_flush_day(racc, R.records + (size_t)d * EPI_REC_LEN, t);
+    if (d + 1 < R.n_days) {
+      if (warp == 0) day_keys(dk[(d + 1) & 1], R.seed, t + 1, lane);
+      cooperative_groups::this_grid().sync();
+    }
+  }
+  // the merged chain resumes at first + n_days: its kernel reads the
+  // random-slot keys of the day after from the ring
+  if (blockIdx.x == 0 && threadIdx.x < RT_SLOTS && R.ring_t2 != nullptr)
+    R.ring_t2->rk[threadIdx.x] =
+        random_slot_keys(key_prefix(R.seed, R.first_step + R.n_days + 1, P_NET_RPERM), threadIdx.x);
+}
+
+}  // namespace epi

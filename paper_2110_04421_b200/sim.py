@@ -93,7 +93,7 @@ def initial_columns(pop: ConfigPopulation) -> AgentColumns:
 class ConfigSimulation:
     def __init__(self, pop: ConfigPopulation, disease, table, interventions, seed: int,
                  mode: str = "csr", precision: str = "f32", horizon: int = 180,
-                 device=None, initial=None, push_max: int | None = None):
+                 device=None, initial=None, push_max: int | None = None, persistent: bool = True):
         import torch
         if mode not in ("csr", "fused"):
             raise ConfigError(f"unknown mode {mode!r}")
@@ -118,6 +118,8 @@ class ConfigSimulation:
         self._after_attach()
         if push_max is not None:
             N.check(self._lib.epi_set_push_max(self._ctx, int(push_max)))
+        # run(): merged fused days in one persistent launch (else one kernel per day)
+        N.check(self._lib.epi_set_persistent(self._ctx, int(bool(persistent))))
         self.state = DeviceColumns(self.n, self.device)
         self._codes_buf = self._alloc_codes()
         self.codes = [self._codes_buf[0], self._codes_buf[1]]
