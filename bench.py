@@ -376,6 +376,7 @@ def run_ours(a):
                          "households U{1..6} + workplaces U{10..50} x 8 colleague draws + "
                          "Poisson(5) random contacts, 100 seeds, no interventions"),
             "mode": best["mode"], "step": "one full 180-day simulation (CUDA graph replay)",
+            "kernel_path": prof.get("path", "one kernel sequence per day"),
             "replicas": f"{a.steps} timed replications per GPU, distinct seeds",
             "l2": "flushed between timed simulations (384 MB write)",
             "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
@@ -411,11 +412,14 @@ def run_ours(a):
 
 def kernel_profile(sim, mode):
     """Per-kernel CUDA-event times over one full simulation (non-graph run with
-    events between the launches of every day)."""
+    events between the launches of every day; a persistent run: events around
+    day 0 and around the one k_fused_run launch of the other days)."""
     import ctypes
     import torch
     from paper_2110_04421_b200 import _native as N
     from paper_2110_04421_b200.engine import _u64
+    if mode == "fused" and sim.uses_persistent_run():
+        return persistent_profile(sim)
     sim.reset()
     torch.cuda.synchronize()
     lib = sim._lib
@@ -472,6 +476,41 @@ def kernel_profile(sim, mode):
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "unit": "GB/s",
                          "traffic": None,
                          "bytes_model": "see DESIGN.md §4 (algorithmic bytes per launch)"}}
+
+
+def persistent_profile(sim):
+    """Day 0 (day tables + k_fused_step) and k_fused_run (days 1..179, one
+    launch), CUDA events on the launching stream."""
+    import torch
+    from paper_2110_04421_b200 import _native as N
+    sim.reset()
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    ev[0].record()
+    sim.run(1)
+    ev[1].record()
+    sim.run()
+    ev[2].record()
+    torch.cuda.synchronize()
+    day0, run = ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2])
+    n, days = sim.n, sim.horizon - 1
+    # per agent-day, state in registers: own code write 2 + push rows read
+    # (rin 32 + rout 64) + rin clear 32 + next-day scatter ~16 = 146 B
+    b_day = 146 * n
+    b_day0 = (16 + 2 + 32 + 64 + 32 + 16) * n + (32 + 10 + 1) * n      # + day-0 tables
+    total = day0 + run
+    kernels = {"day0_tables+k_fused_step": {"ms_per_launch": day0, "share": day0 / total},
+               "k_fused_run": {"ms_per_launch": run, "share": run / total, "days_per_launch": days,
+                               "us_per_day": run * 1e3 / days,
+                               "alg_GBps": b_day * days / (run / 1e3) / 1e9}}
+    achieved = b_day * days / (run / 1e3) / 1e9
+    # ours per simulation: k_codes (reset), k_day_keys + k_day_tables + k_fused_step (day 0), k_fused_run
+    return {"kernels": kernels, "launches_per_sim": 5,
+            "path": "day 0: day tables + k_fused_step; days 1-179: one persistent k_fused_run launch",
+            "alg_bytes_per_sim": float(b_day * days + b_day0),
+            "roofline": {"bound": "hbm", "kernel": "k_fused_run", "achieved": achieved, "unit": "GB/s",
+                         "traffic": None, "days_per_launch": days,
+                         "bytes_model": "146 B per agent-day (DESIGN.md §4), x 179 days per launch"}}
 
 
 def end_to_end(sim, a):

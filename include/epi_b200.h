@@ -318,6 +318,8 @@ int epi_sim_run(epi_ctx *ctx, const epi_state *st, int32_t first_step, int32_t n
  * one resident thread per agent, a grid barrier per day); bitwise the same
  * results as the per-day kernels.  on = 0 forces the per-day kernels. */
 int epi_set_persistent(epi_ctx *ctx, int32_t on);
+/* 1 if epi_sim_run(mode, precision) of >= 2 days would use k_fused_run. */
+int epi_run_persistent(epi_ctx *ctx, int32_t mode, int32_t precision);
 
 /* epi_sim_step that also records 4 caller-created cudaEvent_t: before the
  * generator, before the message pass, after it, after the intervention

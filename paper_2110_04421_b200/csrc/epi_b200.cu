@@ -1047,6 +1047,15 @@ int epi_sim_step(epi_ctx* c, const epi_state* st, int32_t step, uint64_t seed, i
                        nullptr, stream);
 }
 
+// k_fused_run grid: blocks of <= RUN_THREADS agents, rounded up to a
+// multiple of the SM count (equal work per SM; the kernel splits the agents
+// evenly over the blocks)
+static int64_t run_grid(int64_t n) {
+  const int64_t sms = sm_count();
+  const int64_t g = (n + RUN_THREADS - 1) / RUN_THREADS;
+  return (g + sms - 1) / sms * sms;
+}
+
 // Can the merged days of a run go to k_fused_run (one co-resident thread per
 // agent)?  Same conditions as the merged per-day path plus residency.
 static bool persistent_ok(epi_ctx* c, int32_t mode, int32_t precision) {
@@ -1058,7 +1067,7 @@ static bool persistent_ok(epi_ctx* c, int32_t mode, int32_t precision) {
   if (per_sm < 0 &&
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fused_run, RUN_THREADS, 0) != cudaSuccess)
     per_sm = 0;
-  return (c->n + RUN_THREADS - 1) / RUN_THREADS <= (int64_t)per_sm * sm_count();
+  return run_grid(c->n) <= (int64_t)per_sm * sm_count();
 }
 
 static int launch_run(epi_ctx* c, const epi_state* st, int32_t first, int32_t n_days, uint64_t seed,
@@ -1079,7 +1088,7 @@ static int launch_run(epi_ctx* c, const epi_state* st, int32_t first, int32_t n_
   R.tau_lut = c->tau_lut;
   R.dn = c->ntab.dn;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)((c->n + RUN_THREADS - 1) / RUN_THREADS));
+  cfg.gridDim = dim3((unsigned)run_grid(c->n));
   cfg.blockDim = dim3(RUN_THREADS);
   cfg.stream = s;
   cudaLaunchAttribute attr[2];
@@ -1099,6 +1108,11 @@ static int launch_run(epi_ctx* c, const epi_state* st, int32_t first, int32_t n_
   CK(cudaLaunchKernelEx(&cfg, k_fused_run, R, c->net));
   c->merged_ready = first + n_days;
   return 0;
+}
+
+int epi_run_persistent(epi_ctx* c, int32_t mode, int32_t precision) {
+  if (!c) return fail(EPI_EARG, "null ctx");
+  return c->has_net && persistent_ok(c, mode, precision) ? 1 : 0;
 }
 
 int epi_set_persistent(epi_ctx* c, int32_t on) {

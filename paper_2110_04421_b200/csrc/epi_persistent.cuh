@@ -91,8 +91,13 @@ __global__ void __launch_bounds__(RUN_THREADS, 6) k_fused_run(RunArgs R, epi_net
   const int warp = threadIdx.x >> 5, lane = lane_id();
   if (warp == 0) day_keys(dk[0], R.seed, R.first_step, lane);
   const int64_t n = net.n_agents;
-  const int64_t b = blockIdx.x * (int64_t)RUN_THREADS + threadIdx.x;
-  const bool valid = b < n;
+  // equal contiguous agent ranges per block (the grid is a multiple of the
+  // SM count, so every SM carries the same number of agents each day)
+  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t blo = blockIdx.x * per;
+  const int64_t bhi = blo + per < n ? blo + per : n;
+  const int64_t b = blo + threadIdx.x;
+  const bool valid = b < bhi;
   const uint32_t self = (uint32_t)b;
   const int draws = net.colleague_draws;
   // static network data and the agent's state, once

@@ -220,6 +220,13 @@ class ConfigSimulation:
             N.ptr(self.codes[1]), N.ptr(self.rec[t]), N.ptr(self.vax), N.stream_handle()))
         self.clock = t + d
 
+    def uses_persistent_run(self) -> bool:
+        """Whether run() sends its days after the first to k_fused_run."""
+        r = self._lib.epi_run_persistent(self._ctx, 0 if self.mode == "csr" else 1,
+                                         N.F64_CANONICAL if self.precision == "f64" else N.F32)
+        N.check(min(r, 0))
+        return r == 1
+
     def capture(self):
         """Record reset + the whole horizon as one CUDA graph."""
         import torch
