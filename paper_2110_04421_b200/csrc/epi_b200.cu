@@ -172,6 +172,7 @@ struct epi_ctx {
   int merged_ready = -1;             // day whose tables the previous merged kernel built
   Injected* inj_dev = nullptr;
   int persistent = 1;                // epi_sim_run: one launch for the merged days
+  unsigned* run_barrier = nullptr;   // arrival counter of k_fused_run's grid barrier
 };
 
 namespace {
@@ -406,6 +407,7 @@ int epi_destroy(epi_ctx* c) {
   cudaFree(c->den_mark);
   cudaFree(c->den_list);
   cudaFree(c->den_count);
+  cudaFree(c->run_barrier);
   for (auto* p : c->ntab_dev) cudaFree(p);
   cudaFree(c->wt_host[0].member_at_pos);
   for (auto& w : c->wt_host) {
@@ -1047,13 +1049,11 @@ int epi_sim_step(epi_ctx* c, const epi_state* st, int32_t step, uint64_t seed, i
                        nullptr, stream);
 }
 
-// k_fused_run grid: blocks of <= RUN_THREADS agents, rounded up to a
-// multiple of the SM count (equal work per SM; the kernel splits the agents
-// evenly over the blocks)
-static int64_t run_grid(int64_t n) {
+// k_fused_run: one block per SM, threads = the SM's agents rounded up to a warp
+static int64_t run_threads(int64_t n) {
   const int64_t sms = sm_count();
-  const int64_t g = (n + RUN_THREADS - 1) / RUN_THREADS;
-  return (g + sms - 1) / sms * sms;
+  const int64_t per = (n + sms - 1) / sms;
+  return (per + 31) / 32 * 32;
 }
 
 // Can the merged days of a run go to k_fused_run (one co-resident thread per
@@ -1065,13 +1065,15 @@ static bool persistent_ok(epi_ctx* c, int32_t mode, int32_t precision) {
     return false;
   static int per_sm = -1;
   if (per_sm < 0 &&
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fused_run, RUN_THREADS, 0) != cudaSuccess)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fused_run, RUN_MAX_THREADS, 0) != cudaSuccess)
     per_sm = 0;
-  return run_grid(c->n) <= (int64_t)per_sm * sm_count();
+  return per_sm >= 1 && run_threads(c->n) <= RUN_MAX_THREADS;
 }
 
 static int launch_run(epi_ctx* c, const epi_state* st, int32_t first, int32_t n_days, uint64_t seed,
                       uint16_t* codes0, uint16_t* codes1, int64_t* records, cudaStream_t s) {
+  if (!c->run_barrier) CK(cudaMalloc((void**)&c->run_barrier, sizeof(unsigned)));
+  CK(cudaMemsetAsync(c->run_barrier, 0, sizeof(unsigned), s));
   RunArgs R{};
   R.P = c->P;
   R.st = *st;
@@ -1087,9 +1089,10 @@ static int launch_run(epi_ctx* c, const epi_state* st, int32_t first, int32_t n_
   R.mt = (const MsgTables*)c->msg_dev;
   R.tau_lut = c->tau_lut;
   R.dn = c->ntab.dn;
+  R.barrier = c->run_barrier;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)run_grid(c->n));
-  cfg.blockDim = dim3(RUN_THREADS);
+  cfg.gridDim = dim3((unsigned)sm_count());
+  cfg.blockDim = dim3((unsigned)run_threads(c->n));
   cfg.stream = s;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeCooperative;     // every block resident: the grid barrier is safe

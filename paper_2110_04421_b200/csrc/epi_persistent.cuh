@@ -19,8 +19,6 @@
 // shifts are hashed in registers instead of read from the shift table.
 #pragma once
 
-#include <cooperative_groups.h>
-
 #include "epi_kernels.cuh"
 
 namespace epi {
@@ -55,7 +53,25 @@ struct RunArgs {
   const MsgTables* mt;
   const uint16_t* tau_lut;
   Radix dn;
+  unsigned* barrier;              // zeroed arrival counter
 };
+
+// Grid barrier between days: one arrival per block (acq_rel atomic on one
+// counter), thread 0 polls it with acquire loads; bar.sync extends the order
+// to the block.  One block per SM keeps the arrivals at 148 (1.2 us per
+// barrier measured, tools/micro/grid_barrier.cu; cg::grid.sync with 6 blocks
+// per SM: 1.9 us).
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned v;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(v) : "l"(bar) : "memory");
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+    } while (v < target);
+  }
+  __syncthreads();
+}
 
 // sums of the day's rows into the day's record, rows zeroed for tomorrow
 __device__ __forceinline__ void rec_flush_day(RecAcc& s, long long* rec, int step) {
@@ -74,25 +90,25 @@ __device__ __forceinline__ void rec_flush_day(RecAcc& s, long long* rec, int ste
   }
 }
 
-constexpr int RUN_THREADS = 128;
+// one block per SM, up to 768 threads (one agent each)
+constexpr int RUN_MAX_THREADS = 704;
 // loads of data written during the run: plain (coherent) global loads; the
 // grid barrier orders them after the writers' stores
 template <class T> __device__ __forceinline__ T LDM(const T* p) { return *p; }
 
-__global__ void __launch_bounds__(RUN_THREADS, 6) k_fused_run(RunArgs R, epi_net net) {
+__global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_fused_run(RunArgs R, epi_net net) {
   constexpr int HH = 8, DR = 8;
   __shared__ MsgTables T;
   __shared__ RecAcc racc;
   __shared__ DayKeys dk[2];
-  __shared__ int excl_s[RUN_THREADS / 32][32];
-  __shared__ uint16_t cn_s[RUN_THREADS / 32][32];
+  __shared__ int excl_s[RUN_MAX_THREADS / 32][32];
+  __shared__ uint16_t cn_s[RUN_MAX_THREADS / 32][32];
   load_msg_tables(T, R.mt);
   rec_init(racc);
   const int warp = threadIdx.x >> 5, lane = lane_id();
   if (warp == 0) day_keys(dk[0], R.seed, R.first_step, lane);
   const int64_t n = net.n_agents;
-  // equal contiguous agent ranges per block (the grid is a multiple of the
-  // SM count, so every SM carries the same number of agents each day)
+  // equal contiguous agent ranges per block (one block per SM)
   const int64_t per = (n + gridDim.x - 1) / gridDim.x;
   const int64_t blo = blockIdx.x * per;
   const int64_t bhi = blo + per < n ? blo + per : n;
@@ -272,7 +288,7 @@ __global__ void __launch_bounds__(RUN_THREADS, 6) k_fused_run(RunArgs R, epi_net
     rec_flush_day(racc, R.records + (size_t)d * EPI_REC_LEN, t);
     if (d + 1 < R.n_days) {
       if (warp == 0) day_keys(dk[(d + 1) & 1], R.seed, t + 1, lane);
-      cooperative_groups::this_grid().sync();
+      grid_barrier(R.barrier, (unsigned)(d + 1) * gridDim.x);
     }
   }
   // the merged chain resumes at first + n_days: its kernel reads the
