@@ -56,26 +56,27 @@ struct RunArgs {
   unsigned* barrier;              // zeroed arrival counter
 };
 
-// Grid barrier between days: one arrival per block (acq_rel atomic on one
-// counter), thread 0 polls it with acquire loads; bar.sync extends the order
-// to the block.  One block per SM keeps the arrivals at 148 (1.2 us per
-// barrier measured, tools/micro/grid_barrier.cu; cg::grid.sync with 6 blocks
-// per SM: 1.9 us).
-__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned target) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned v;
-    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(v) : "l"(bar) : "memory");
-    do {
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
-    } while (v < target);
-  }
-  __syncthreads();
+// Grid barrier between days, split: arrive, then the block's record flush
+// and tomorrow's keys while the other blocks finish, then wait.  One arrival
+// per block (acq_rel atomic on one counter) after a bar.sync, so every store
+// of the block's day precedes it; thread 0 polls with acquire loads and the
+// closing bar.sync extends the order to the block.  One block per SM keeps
+// the arrivals at 148 (1.2 us per barrier, tools/micro/grid_barrier.cu;
+// cg::grid.sync with 6 blocks per SM: 1.9 us).
+__device__ __forceinline__ void barrier_arrive(unsigned* bar) {
+  unsigned v;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(v) : "l"(bar) : "memory");
+}
+__device__ __forceinline__ void barrier_wait(const unsigned* bar, unsigned target) {
+  unsigned v;
+  do {
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+  } while (v < target);
 }
 
 // sums of the day's rows into the day's record, rows zeroed for tomorrow
-__device__ __forceinline__ void rec_flush_day(RecAcc& s, long long* rec, int step) {
-  __syncthreads();
+// (after a bar.sync; the next adds come after the closing bar.sync)
+__device__ __forceinline__ void rec_flush_rows(RecAcc& s, long long* rec, int step) {
   if (blockIdx.x == 0 && threadIdx.x == 0) rec[EPI_REC_STEP] = step;
   const int nw = (blockDim.x + 31) >> 5;
   for (int i = threadIdx.x; i < EPI_REC_LEN; i += blockDim.x) {
@@ -103,6 +104,7 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_fused_run(RunArgs R, epi
   __shared__ DayKeys dk[2];
   __shared__ int excl_s[RUN_MAX_THREADS / 32][32];
   __shared__ uint16_t cn_s[RUN_MAX_THREADS / 32][32];
+  __shared__ uint8_t own_s[RUN_MAX_THREADS / 32][32 * RT_SLOTS];
   load_msg_tables(T, R.mt);
   rec_init(racc);
   const int warp = threadIdx.x >> 5, lane = lane_id();
@@ -268,15 +270,14 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_fused_run(RunArgs R, epi
         if (lane >= o) incl += v;
       }
       const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
-      excl_s[warp][lane] = incl - na;
+      const int excl = incl - na;
+      excl_s[warp][lane] = excl;
       cn_s[warp][lane] = cn;
+      for (int i = 0; i < na; ++i) own_s[warp][excl + i] = (uint8_t)lane;   // item -> its agent's lane
       __syncwarp();
       const int64_t wbase_agent = b - lane;
       for (int k = lane; k < total; k += 32) {
-        int l = 0;
-#pragma unroll
-        for (int st = 16; st >= 1; st >>= 1)
-          if (l + st < 32 && excl_s[warp][l + st] <= k) l += st;
+        const int l = own_s[warp][k];
         const int j = k - excl_s[warp][l];
         const uint32_t src = (uint32_t)(wbase_agent + l);
         const uint32_t y = walk_fwd(src, D.rk_next[j], R.dn);
@@ -285,11 +286,15 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_fused_run(RunArgs R, epi
       }
     }
     cb = cn;
-    rec_flush_day(racc, R.records + (size_t)d * EPI_REC_LEN, t);
-    if (d + 1 < R.n_days) {
-      if (warp == 0) day_keys(dk[(d + 1) & 1], R.seed, t + 1, lane);
-      grid_barrier(R.barrier, (unsigned)(d + 1) * gridDim.x);
+    __syncthreads();                       // the block's day is complete
+    const bool more = d + 1 < R.n_days;
+    if (more && threadIdx.x == 0) barrier_arrive(R.barrier);
+    if (warp == 0) {
+      rec_flush_rows(racc, R.records + (size_t)d * EPI_REC_LEN, t);
+      if (more) day_keys(dk[(d + 1) & 1], R.seed, t + 1, lane);
+      if (more && lane == 0) barrier_wait(R.barrier, (unsigned)(d + 1) * gridDim.x);
     }
+    __syncthreads();
   }
   // the merged chain resumes at first + n_days: its kernel reads the
   // random-slot keys of the day after from the ring
