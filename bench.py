@@ -439,10 +439,13 @@ def kernel_profile(sim, mode):
     sim.clock = sim.horizon
     gen = [evs[t][0].elapsed_time(evs[t][1]) for t in range(sim.horizon)]
     pas = [evs[t][1].elapsed_time(evs[t][2]) for t in range(sim.horizon)]
+    ivt = [evs[t][2].elapsed_time(evs[t][3]) for t in range(sim.horizon)]
     rec = sim.records()
     E = rec[:, N.REC["edges"]].astype(np.float64)
     n = sim.n
-    total_ms = sum(gen) + sum(pas)
+    iv = sim.iv
+    has_iv = iv.testing_enabled or iv.quarantine_enabled or iv.den_enabled or iv.vaccination_enabled
+    total_ms = sum(gen) + sum(pas) + (sum(ivt) if has_iv else 0.0)
     kernels = {}
     if mode == "csr":
         # generator writes a 2 B pre-joined message per edge + 4 B row length
@@ -457,6 +460,9 @@ def kernel_profile(sim, mode):
         kernels["k_pass_update"] = {"ms_per_launch": sum(pas) / len(pas),
                                     "share": sum(pas) / total_ms,
                                     "alg_GBps": float(np.sum(b_pass) / (sum(pas) / 1e3) / 1e9)}
+        if has_iv:
+            kernels["interventions (per-phase kernels)"] = {"ms_per_launch": sum(ivt) / len(ivt),
+                                                            "share": sum(ivt) / total_ms}
         dom = "k_pass_update" if sum(pas) >= sum(gen) else "k_day_tables+k_net_realize"
         byt = b_pass if dom == "k_pass_update" else b_gen
         ms = pas if dom == "k_pass_update" else gen
@@ -467,11 +473,23 @@ def kernel_profile(sim, mode):
         b = (16 + 2 + 32 + 64 + 32 + 16) * n
         kernels["day0_tables+keys"] = {"ms_per_launch": sum(gen) / len(gen), "share": sum(gen) / total_ms}
         kernels["k_fused_step"] = {"ms_per_launch": sum(pas) / len(pas), "share": sum(pas) / total_ms,
-                                   "alg_GBps": float(np.sum(b) / (sum(pas) / 1e3) / 1e9)}
+                                   "alg_GBps": float(b * len(pas) / (sum(pas) / 1e3) / 1e9)}
         dom, byt, ms, launches = "k_fused_step", b * np.ones_like(E), pas, 1
+        extra = 2
+        if has_iv:
+            # fused intervention day: k_fused_step (+ testing), k_den_regen,
+            # k_iv_post_chunks, k_finish_iv (+ doses, death days, tomorrow's
+            # push tables); day 0 also k_day_keys + k_day_tables (+ k_died_update)
+            den = iv.den_enabled and iv.testing_enabled
+            post = iv.den_enabled or iv.quarantine_enabled or iv.vaccination_enabled
+            kernels["interventions: k_den_regen + k_iv_post_chunks + k_finish_iv"] = {
+                "ms_per_launch": sum(ivt) / len(ivt), "share": sum(ivt) / total_ms}
+            launches = 2 + (1 if post else 0) + (1 if den else 0)
+            extra = 1 + 2 + (1 if iv.den_enabled else 0) - (1 if den else 0)
     achieved = float(np.sum(byt) / (sum(ms) / 1e3) / 1e9)
     sim_bytes = float(np.sum(b_gen) + np.sum(b_pass)) if mode == "csr" else float(np.sum(b * np.ones_like(E)))
-    return {"kernels": kernels, "launches_per_sim": launches * sim.horizon + (2 if mode != "csr" else 0),
+    return {"kernels": kernels,
+            "launches_per_sim": launches * sim.horizon + (extra if mode != "csr" else 0),
             "alg_bytes_per_sim": sim_bytes,
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "unit": "GB/s",
                          "traffic": None,

@@ -318,6 +318,11 @@ int epi_sim_run(epi_ctx *ctx, const epi_state *st, int32_t first_step, int32_t n
  * one resident thread per agent, a grid barrier per day); bitwise the same
  * results as the per-day kernels.  on = 0 forces the per-day kernels. */
 int epi_set_persistent(epi_ctx *ctx, int32_t on);
+/* Fused-mode intervention days on the whole population in 4 launches
+ * (testing inside the day kernel; plan + doses + tomorrow's push tables in
+ * k_iv_post_chunks / k_finish_iv); bitwise the same as the per-phase kernels
+ * (on = 0). */
+int epi_set_iv_fusion(epi_ctx *ctx, int32_t on);
 /* 1 if epi_sim_run(mode, precision) of >= 2 days would use k_fused_run. */
 int epi_run_persistent(epi_ctx *ctx, int32_t mode, int32_t precision);
 

@@ -99,6 +99,7 @@ _SIGS = {
     "epi_pop_synthesize": (_i32, [C.POINTER(EpiPopSpec), _u64, C.POINTER(EpiPopOut), _p]),
     "epi_set_push_max": (_i32, [_p, _i64]),
     "epi_set_persistent": (_i32, [_p, _i32]),
+    "epi_set_iv_fusion": (_i32, [_p, _i32]),
     "epi_run_persistent": (_i32, [_p, _i32, _i32]),
     "epi_last_error": (C.c_char_p, []),
     "epi_version": (_i32, []),

@@ -172,6 +172,9 @@ struct epi_ctx {
   int merged_ready = -1;             // day whose tables the previous merged kernel built
   Injected* inj_dev = nullptr;
   int persistent = 1;                // epi_sim_run: one launch for the merged days
+  int iv_fusion = 1;                 // intervention days in 4 launches (k_iv_post_chunks, k_finish_iv)
+  unsigned* iv_tile_hist = nullptr;  // [chunks][NUM_BUCKETS]
+  unsigned long long* iv_hist = nullptr;   // [2][NUM_BUCKETS] eligibility histogram by day parity
   unsigned* run_barrier = nullptr;   // arrival counter of k_fused_run's grid barrier
 };
 
@@ -408,6 +411,8 @@ int epi_destroy(epi_ctx* c) {
   cudaFree(c->den_list);
   cudaFree(c->den_count);
   cudaFree(c->run_barrier);
+  cudaFree(c->iv_tile_hist);
+  cudaFree(c->iv_hist);
   for (auto* p : c->ntab_dev) cudaFree(p);
   cudaFree(c->wt_host[0].member_at_pos);
   for (auto& w : c->wt_host) {
@@ -901,6 +906,102 @@ int epi_net_csr(epi_ctx* c, int32_t step, uint32_t** entries, int32_t** row_len)
   return 0;
 }
 
+// Chunks of k_iv_post_chunks / k_finish_iv: a multiple of 256 agents each, at
+// most 8 blocks per SM.
+static void iv_chunks(int64_t n, int64_t* chunk, int* blocks) {
+  const int64_t g0 = grid_for(n, 256);
+  int64_t ch = (n + g0 - 1) / g0;
+  ch = (ch + 255) / 256 * 256;
+  *chunk = ch < 256 ? 256 : ch;
+  *blocks = (int)((n + *chunk - 1) / *chunk);
+}
+
+// One intervention day on the whole population with the push tables:
+// k_fused_step (+ testing) -> [k_den_regen] -> [k_iv_post_chunks] ->
+// k_finish_iv (+ doses, death days, tomorrow's push tables).  The day's
+// tables come from yesterday's k_finish_iv (merged_ready) or are built here.
+static int iv_fused_day(epi_ctx* c, const StepArgs& A, int32_t step, uint64_t seed, const uint16_t* codes_cur,
+                        uint16_t* codes_next, long long* rec, bool zero_record, int32_t* vax_open, void* const* ev,
+                        cudaStream_t s) {
+  const epi_params& p = c->host;
+  if (p.vaccination_enabled && !vax_open) return fail(EPI_EARG, "vaccination enabled but no vax_open latch given");
+  const NetKeys nk = make_net_keys(seed, step);
+  NetTables* nt_today = c->ntab_dev[step % 3];
+  NetTables* nt_next = c->ntab_dev[(step + 1) % 3];
+  const int par = step & 1;
+  const uint64_t rcount_next = key_prefix(seed, step + 1, P_NET_RCOUNT);
+  int64_t chunk;
+  int blocks;
+  iv_chunks(c->n, &chunk, &blocks);
+  int rc = 0;
+  if (!c->iv_hist) rc = dalloc(&c->iv_hist, (size_t)2 * NUM_BUCKETS);
+  if (!rc && !c->iv_tile_hist) rc = dalloc(&c->iv_tile_hist, (size_t)blocks * NUM_BUCKETS);
+  if (rc) return rc;
+  const bool listed = p.den_enabled && p.testing_enabled && c->den_list != nullptr;
+  const bool first = c->merged_ready != step;
+  if (ev) CK(cudaEventRecord((cudaEvent_t)ev[0], s));
+  if (first) {
+    // the day's tables from scratch; the day-to-day counters to zero
+    k_day_keys<<<1, 32, 0, s>>>(nt_today, nk.rperm, nullptr);
+    CKL();
+    CK(cudaMemsetAsync(c->wt_host[par].rin, 0, (size_t)c->n * RT_SLOTS * sizeof(uint16_t), s));
+    const bool has_work = c->net.n_member_slots > 0 && c->net.colleague_draws > 0;
+    const int wblocks = has_work ? grid_for(c->net.n_member_slots, 256, 4) : 0;
+    const int rblocks = grid_for(c->n, 256, 8);
+    CK(launch_pdl_w(&c->hot, k_day_tables, dim3(wblocks + rblocks), dim3(256), 0, s, c->net, nk, c->wt_host[par],
+                    codes_cur, (int64_t)0, c->n, wblocks, (const NetTables*)nt_today, nt_next,
+                    key_prefix(seed, step + 1, P_NET_RPERM), zero_record ? rec : (long long*)nullptr));
+    CK(cudaMemsetAsync(c->iv_hist, 0, (size_t)2 * NUM_BUCKETS * sizeof(unsigned long long), s));
+    if (listed) CK(cudaMemsetAsync(c->den_count, 0, sizeof(int), s));
+    if (p.den_enabled) {
+      // deaths of yesterday (later days: recorded by k_finish_iv)
+      k_died_update<<<grid_for(c->n, 256), 256, 0, s>>>(codes_cur, c->n, step, c->died_at);
+      CKL();
+    }
+  } else if (zero_record) {
+    CK(cudaMemsetAsync(rec, 0, EPI_REC_LEN * sizeof(long long), s));
+  }
+  if (ev) CK(cudaEventRecord((cudaEvent_t)ev[1], s));
+  const int fgrid = grid_for(c->n, 128, 16);
+  DayTests tests{p.testing_enabled ? 1 : 0, listed ? c->den_list : nullptr, listed ? c->den_count : nullptr};
+  CK(launch_pdl_w(&c->hot, k_fused_step, dim3(fgrid), dim3(128), 0, s, A, c->net, nk, codes_cur,
+                  c->host.rate_scale, codes_next, (const epi_net*)c->net_dev, rcount_next, 0,
+                  (const WorkTables*)c->wt_dev[par][2], (const MsgTables*)c->msg_dev, (const NetTables*)nt_today,
+                  NextTables{}, 1, tests));
+  if (ev) CK(cudaEventRecord((cudaEvent_t)ev[2], s));
+  if (p.den_enabled && p.testing_enabled) {
+    // contacts of the notifiers over steps step-L .. step-1, regenerated
+    DenRegen D{};
+    D.first_day = step - p.den_lookback > 0 ? step - p.den_lookback : 0;
+    D.n_days = step - D.first_day;
+    if (D.n_days > 0) {
+      for (int d = 0; d < D.n_days; ++d) D.nk[d] = make_net_keys(seed, D.first_day + d);
+      // one warp per (notifier, day) item, read on the device: one block per SM
+      k_den_regen<<<sm_count(), 256, 0, s>>>(c->net, D, c->died_at, c->den_list, c->den_count, c->flags,
+                                             (const Radix*)c->ntab_dev[0]->wrad);
+      CKL();
+    }
+  }
+  IvPlan V{c->iv_hist, c->iv_tile_hist, vax_open, chunk, p.vaccination_enabled ? 1 : 0};
+  if (p.den_enabled || p.quarantine_enabled || p.vaccination_enabled) {
+    k_iv_post_chunks<<<blocks, 256, 0, s>>>(A, c->bucket, V);
+    CKL();
+  }
+  NextTables nx{};
+  nx.wt = c->wt_dev[par ^ 1][2];
+  nx.keys = nt_next;
+  nx.keys_out = c->ntab_dev[(step + 2) % 3];
+  nx.rperm_t2 = key_prefix(seed, step + 2, P_NET_RPERM);
+  nx.nk = make_net_keys(seed, step + 1);
+  k_finish_iv<<<blocks, 256, 0, s>>>(A, codes_next, (const epi_net*)c->net_dev, rcount_next, c->bucket, V,
+                                      p.den_enabled ? c->died_at : nullptr, listed ? c->den_count : nullptr, c->net,
+                                      nx, c->ntab.dn);
+  CKL();
+  c->merged_ready = step + 1;
+  if (ev) CK(cudaEventRecord((cudaEvent_t)ev[3], s));
+  return 0;
+}
+
 static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t seed, int32_t mode,
                          int32_t precision, const uint16_t* codes_cur, uint16_t* codes_next,
                          int64_t* record, int32_t* vax_open, void* const* ev, void* stream,
@@ -935,6 +1036,8 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
   const bool push_rand = (mode == 1 || msg_only) && c->lo == 0 && c->hi == c->n && c->net.n_agents >= 2 &&
                          c->net.random_slots == RT_SLOTS && batched(&c->net) && push_fits(c);
   const bool merged = mode == 1 && push_rand && !iv;
+  if (mode == 1 && push_rand && iv && c->iv_fusion)
+    return iv_fused_day(c, A, step, seed, codes_cur, codes_next, rec, zero_record, vax_open, ev, s);
   const bool use_wt = (mode == 0 && (push_rand || (has_work && batched(&c->net)))) || mode == 1;
   const int variant = push_rand ? 2 : (mode == 0 ? 0 : 1);
   long long* rec_zero = zero_record ? rec : nullptr;
@@ -1002,7 +1105,7 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
     }
     CK(launch_pdl_w(&c->hot, k_fused_step, dim3(fgrid), dim3(128), 0, s, A, c->net, nk, codes_cur,
                   c->host.rate_scale, codes_next, (const epi_net*)c->net_dev, rcount_next, iv ? 0 : 1, wt,
-                  (const MsgTables*)c->msg_dev, (const NetTables*)nt_today, nx, push_rand ? 1 : 0));
+                  (const MsgTables*)c->msg_dev, (const NetTables*)nt_today, nx, push_rand ? 1 : 0, DayTests{}));
     c->merged_ready = merged ? step + 1 : -1;
   }
   if (ev) CK(cudaEventRecord((cudaEvent_t)ev[2], s));
@@ -1022,13 +1125,15 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
       if (!c->host.testing_enabled) return 0;           // no test results, no notifiers
       const int g = sm_count() * 8;                    // persistent: items read on the device
       if (!part) {
-        k_den_regen<<<g, 256, 0, s>>>(c->net, D, c->died_at, c->den_list, c->den_count, c->flags);
+        k_den_regen<<<g, 256, 0, s>>>(c->net, D, c->died_at, c->den_list, c->den_count, c->flags,
+                                      (const Radix*)c->ntab_dev[0]->wrad);
         CKL();
         return 0;
       }
       // partitioned: contacts may be anyone's; OR the ranks' marks together
       CK(cudaMemsetAsync(c->den_mark, 0, (size_t)c->n, s));
-      k_den_regen<<<g, 256, 0, s>>>(c->net, D, c->died_at, c->den_list, c->den_count, c->den_mark);
+      k_den_regen<<<g, 256, 0, s>>>(c->net, D, c->died_at, c->den_list, c->den_count, c->den_mark,
+                                    (const Radix*)c->ntab_dev[0]->wrad);
       CKL();
       int rc2 = exchange(c, EPI_X_OR_U8, c->den_mark, c->n, s);
       if (rc2) return rc2;
@@ -1116,6 +1221,13 @@ static int launch_run(epi_ctx* c, const epi_state* st, int32_t first, int32_t n_
 int epi_run_persistent(epi_ctx* c, int32_t mode, int32_t precision) {
   if (!c) return fail(EPI_EARG, "null ctx");
   return c->has_net && persistent_ok(c, mode, precision) ? 1 : 0;
+}
+
+int epi_set_iv_fusion(epi_ctx* c, int32_t on) {
+  if (!c) return fail(EPI_EARG, "null ctx");
+  c->iv_fusion = on != 0;
+  c->merged_ready = -1;
+  return 0;
 }
 
 int epi_set_persistent(epi_ctx* c, int32_t on) {

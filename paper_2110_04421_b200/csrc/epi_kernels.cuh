@@ -2,6 +2,7 @@
 // intervention phases, per-step record.  Host wrappers live in epi_b200.cu.
 #pragma once
 
+#include <cub/block/block_reduce.cuh>
 #include <cub/block/block_scan.cuh>
 
 #include "epi_common.cuh"
@@ -675,6 +676,113 @@ struct NextTables {
   NetKeys nk;                    // prefixes of day t+1
 };
 
+// Phase 3 + 4a for agent a (engine.py:202-242): test sampling, then
+// delivery.  `fl` is the agent's flags byte (in/out); returns 1 if sampled.
+__device__ __forceinline__ unsigned test_agent(const StepArgs& A, int64_t a, int stage, uint8_t& fl,
+                                               int32_t* __restrict__ notif, int* n_notif) {
+  const epi_params* __restrict__ P = A.P;
+  const epi_state& st = A.st;
+  const int step = A.step;
+  unsigned tested = 0;
+  bool cand = (fl & FL_SYMPTOMATIC) != 0;
+  if (st.den_test_due_at[a] == step) {
+    st.den_test_due_at[a] = NEVER;
+    cand = true;
+  }
+  if (cand && st.test_result_at[a] == NEVER && stage != S_DEAD) {
+    const double up = draw(A.K, A.inj, P_TEST_POS, a);
+    const bool pos = active_stage(stage) ? (up < P->detection_prob) : (up < P->false_positive_prob);
+    const int span = P->turnaround_max - P->turnaround_min + 1;
+    const int turn = P->turnaround_min + (int)(draw(A.K, A.inj, P_TEST_TURN, a) * span);
+    st.test_sample_at[a] = step;
+    st.test_result_at[a] = step + turn;
+    st.test_positive[a] = pos;
+    tested = 1;
+  }
+  // delivery
+  if (st.test_result_at[a] == step) {
+    const bool pos = st.test_positive[a] != 0;
+    st.test_result_at[a] = NEVER;
+    st.test_positive[a] = 0;
+    if (pos) {
+      if (P->quarantine_enabled) {
+        st.quarantine_until[a] = step + P->quarantine_duration;
+        st.quarantine_started_at[a] = step;
+      }
+      if (P->den_enabled && st.has_den_app[a]) {
+        fl |= FL_NOTIFIER;
+        if (notif) notif[atomicAdd(n_notif, 1)] = (int32_t)a;
+      }
+    }
+  }
+  return tested;
+}
+
+// Tomorrow's push tables from agent b's next-day code cn.  All 32 lanes of
+// the warp call; the warp's lanes hold consecutive agents from wbase_agent.
+//   workplace: the worker's next-day position q, wcode[q] = cn, the shifts;
+//   random   : the warp's (agent, slot < n) items flattened 32 at a time:
+//              rout[a][j] = pi_j(a), rin[pi_j(a)][j] = cn | PRESENT.
+__device__ __forceinline__ void push_next_day(const epi_net& net, const NextTables& nx, bool valid, int64_t b,
+                                              uint16_t cn, const PermKeys* rk_next, const Radix& dn,
+                                              int* excl_w, uint16_t* cn_w, int64_t wbase_agent, int lane) {
+  const WorkTables& W = *nx.wt;
+  const int w = valid ? net.wp_id[b] : -1;
+  if (w >= 0) {
+    const int m = net.wp_size[w];
+    if (m >= 2) {
+      const int wbase = net.wp_base[w];
+      const int loc = net.wp_local[b];
+      const uint32_t q = walk_inv((uint32_t)loc, work_keys(nx.nk.wperm, w), make_radix((uint32_t)m));
+      W.pos_of[wbase + loc] = (uint8_t)q;
+      W.wcode[wbase + q] = cn;
+      for (int j = loc; j < net.colleague_draws; j += m)
+        W.shift[(size_t)w * net.colleague_draws + j] = (uint8_t)work_shift(nx.nk.wshift, w, j, m);
+    }
+  }
+  int na = valid ? code_count(cn) : 0;
+  na = na < RT_SLOTS ? na : RT_SLOTS;
+  int incl = na;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+  excl_w[lane] = incl - na;
+  cn_w[lane] = cn;
+  __syncwarp();
+  for (int k = lane; k < total; k += 32) {
+    int l = 0;
+#pragma unroll
+    for (int st = 16; st >= 1; st >>= 1)
+      if (l + st < 32 && excl_w[l + st] <= k) l += st;
+    const int j = k - excl_w[l];
+    const uint32_t src = (uint32_t)(wbase_agent + l);
+    const uint32_t y = walk_fwd(src, rk_next[j], dn);
+    W.rout[(size_t)src * RT_SLOTS + j] = y;
+    if (y != src) W.rin[(size_t)y * RT_SLOTS + j] = cn_w[l] | CODE_PRESENT;
+  }
+  __syncwarp();
+}
+
+// tomorrow's random-slot keys into shared memory; block 0 writes those of
+// the day after into the ring (all threads call; ends with a bar.sync)
+__device__ __forceinline__ void load_next_keys(const NextTables& nx, PermKeys* rk_next) {
+  for (int j = threadIdx.x; j < EPI_MAX_SLOTS; j += blockDim.x) rk_next[j] = nx.keys->rk[j];
+  if (blockIdx.x == 0 && threadIdx.x < EPI_MAX_SLOTS)
+    nx.keys_out->rk[threadIdx.x] = random_slot_keys(nx.rperm_t2, threadIdx.x);
+  __syncthreads();
+}
+
+// Testing fused into the day kernel (intervention days on the whole
+// population): the notifier work list of the DEN scan.
+struct DayTests {
+  int on;
+  int32_t* notif;
+  int* n_notif;
+};
+
 __global__ void __launch_bounds__(128, 6) k_fused_step(StepArgs A, epi_net net, NetKeys nk,
                                                     const uint16_t* __restrict__ codes, double rate,
                                                     uint16_t* __restrict__ codes_next,
@@ -682,7 +790,7 @@ __global__ void __launch_bounds__(128, 6) k_fused_step(StepArgs A, epi_net net, 
                                                     int final_pass, const WorkTables* wt,
                                                     const MsgTables* __restrict__ mt,
                                                     const NetTables* __restrict__ NTp, NextTables nx,
-                                                    int push) {
+                                                    int push, DayTests tests) {
   __shared__ MsgTables T;
   __shared__ NetTables NT;
   __shared__ RecAcc racc;
@@ -703,12 +811,7 @@ __global__ void __launch_bounds__(128, 6) k_fused_step(StepArgs A, epi_net net, 
   pdl_wait();
   pdl_trigger();
   const bool merge = nx.wt != nullptr;
-  if (merge) {
-    for (int j = threadIdx.x; j < EPI_MAX_SLOTS; j += blockDim.x) rk_next[j] = nx.keys->rk[j];
-    if (blockIdx.x == 0 && threadIdx.x < EPI_MAX_SLOTS)
-      nx.keys_out->rk[threadIdx.x] = random_slot_keys(nx.rperm_t2, threadIdx.x);
-    __syncthreads();
-  }
+  if (merge) load_next_keys(nx, rk_next);
   const Radix dn = NT.dn;
   const int warp = threadIdx.x >> 5, lane = lane_id();
   const int64_t n = A.hi;
@@ -740,7 +843,18 @@ __global__ void __launch_bounds__(128, 6) k_fused_step(StepArgs A, epi_net net, 
     }
     unsigned ev = 0;
     if (valid) ev = transmit_progress_hot(A, b, lam, -1, h);
-    if (valid && (ev & 8u) && A.flags) A.flags[b] = FL_SYMPTOMATIC;
+    if (tests.on) {
+      // phase 3 + 4a on the agent's own state (k_iv_tests, fused)
+      unsigned tested = 0;
+      if (valid) {
+        uint8_t fl = (ev & 8u) ? FL_SYMPTOMATIC : A.flags[b];
+        tested = test_agent(A, b, h.stage, fl, tests.notif, tests.n_notif);
+        A.flags[b] = fl;
+      }
+      rec_add(racc, EPI_REC_TESTS, tested);
+    } else if (valid && (ev & 8u) && A.flags) {
+      A.flags[b] = FL_SYMPTOMATIC;
+    }
     rec_events(racc, ev);
     rec_add(racc, EPI_REC_EDGES, edges);
     if (final_pass) {
@@ -750,50 +864,9 @@ __global__ void __launch_bounds__(128, 6) k_fused_step(StepArgs A, epi_net net, 
         cn = next_code_hot(A.P, h, b, A.step + 1, net_dev, rcount_next);
         codes_next[b] = cn;
       }
-      if (merge) {
-        const WorkTables& W = *nx.wt;
-        // workplace: the worker's next-day position, its code at that position
-        const int w = valid ? net.wp_id[b] : -1;
-        if (w >= 0) {
-          const int m = net.wp_size[w];
-          if (m >= 2) {
-            const int wbase = net.wp_base[w];
-            const int loc = net.wp_local[b];
-            const uint32_t q = walk_inv((uint32_t)loc, work_keys(nx.nk.wperm, w),
-                                        push ? make_radix((uint32_t)m) : NT.wrad[m]);
-            W.pos_of[wbase + loc] = (uint8_t)q;
-            W.wcode[wbase + q] = cn;
-            for (int j = loc; j < net.colleague_draws; j += m)
-              W.shift[(size_t)w * net.colleague_draws + j] = (uint8_t)work_shift(nx.nk.wshift, w, j, m);
-          }
-        }
-        // random: flatten the warp's (agent, slot < n) items, 32 at a time
-        int na = valid ? code_count(cn) : 0;
-        na = na < RT_SLOTS ? na : RT_SLOTS;
-        int incl = na;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-          if (lane >= o) incl += v;
-        }
-        const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
-        excl_s[warp][lane] = incl - na;
-        cn_s[warp][lane] = cn;
-        __syncwarp();
-        const int64_t wbase_agent = base + (threadIdx.x & ~31);
-        for (int k = lane; k < total; k += 32) {
-          int l = 0;
-#pragma unroll
-          for (int st = 16; st >= 1; st >>= 1)
-            if (l + st < 32 && excl_s[warp][l + st] <= k) l += st;
-          const int j = k - excl_s[warp][l];
-          const uint32_t src = (uint32_t)(wbase_agent + l);
-          const uint32_t y = walk_fwd(src, rk_next[j], dn);
-          W.rout[(size_t)src * RT_SLOTS + j] = y;
-          if (y != src) W.rin[(size_t)y * RT_SLOTS + j] = cn_s[warp][l] | CODE_PRESENT;
-        }
-        __syncwarp();
-      }
+      if (merge)
+        push_next_day(net, nx, valid, b, cn, rk_next, dn, excl_s[warp], cn_s[warp], base + (threadIdx.x & ~31),
+                      lane);
     }
   }
   __syncthreads();
@@ -895,13 +968,12 @@ __global__ void __launch_bounds__(256) k_day_tables(epi_net net, NetKeys nk, Wor
 // Phase 3 + 4a: test sampling, then delivery (engine.py:202-242).
 // Notifiers are also appended to `notif` (count in *n_notif) when given:
 // the work list of the DEN regeneration scan.
+// Notifiers are also appended to `notif` (count in *n_notif) when given:
+// the work list of the DEN regeneration scan.
 __global__ void k_iv_tests(StepArgs A, int32_t* __restrict__ notif = nullptr, int* n_notif = nullptr) {
   __shared__ RecAcc racc;
   rec_init(racc);
   __syncthreads();
-  const epi_params* __restrict__ P = A.P;
-  const epi_state& st = A.st;
-  const int step = A.step;
   const int64_t n = A.hi;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t base = A.lo + blockIdx.x * (int64_t)blockDim.x; base < n; base += stride) {
@@ -909,38 +981,7 @@ __global__ void k_iv_tests(StepArgs A, int32_t* __restrict__ notif = nullptr, in
     unsigned tested = 0;
     if (a < n) {
       uint8_t fl = A.flags[a];
-      bool cand = (fl & FL_SYMPTOMATIC) != 0;
-      if (st.den_test_due_at[a] == step) {
-        st.den_test_due_at[a] = NEVER;
-        cand = true;
-      }
-      const int stage = st.stage[a];
-      if (cand && st.test_result_at[a] == NEVER && stage != S_DEAD) {
-        const double up = draw(A.K, A.inj, P_TEST_POS, a);
-        const bool pos = active_stage(stage) ? (up < P->detection_prob) : (up < P->false_positive_prob);
-        const int span = P->turnaround_max - P->turnaround_min + 1;
-        const int turn = P->turnaround_min + (int)(draw(A.K, A.inj, P_TEST_TURN, a) * span);
-        st.test_sample_at[a] = step;
-        st.test_result_at[a] = step + turn;
-        st.test_positive[a] = pos;
-        tested = 1;
-      }
-      // delivery
-      if (st.test_result_at[a] == step) {
-        const bool pos = st.test_positive[a] != 0;
-        st.test_result_at[a] = NEVER;
-        st.test_positive[a] = 0;
-        if (pos) {
-          if (P->quarantine_enabled) {
-            st.quarantine_until[a] = step + P->quarantine_duration;
-            st.quarantine_started_at[a] = step;
-          }
-          if (P->den_enabled && st.has_den_app[a]) {
-            fl |= FL_NOTIFIER;
-            if (notif) notif[atomicAdd(n_notif, 1)] = (int32_t)a;
-          }
-        }
-      }
+      tested = test_agent(A, a, A.st.stage[a], fl, notif, n_notif);
       A.flags[a] = fl;
     }
     rec_add(racc, EPI_REC_TESTS, tested);
@@ -988,10 +1029,10 @@ __global__ void k_died_update(const uint16_t* __restrict__ codes, int64_t n, int
 
 __global__ void __launch_bounds__(256) k_den_regen(epi_net net, DenRegen D, const int32_t* __restrict__ died_at,
                                                    const int32_t* __restrict__ notif, const int* n_notif,
-                                                   uint8_t* __restrict__ mark) {
+                                                   uint8_t* __restrict__ mark, const Radix* __restrict__ wrad_g) {
   __shared__ Radix wrad[256];
   __shared__ PermKeys rk[8][EPI_MAX_SLOTS];
-  for (int m = threadIdx.x; m < 256; m += blockDim.x) wrad[m] = make_radix(m < 1 ? 1u : (uint32_t)m);
+  for (int m = threadIdx.x; m < 256; m += blockDim.x) wrad[m] = wrad_g[m];     // static workplace domains
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = lane_id();
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -1038,61 +1079,64 @@ __device__ __forceinline__ void realize_immunity(const StepArgs& A, int64_t a, i
 
 // Phase 4b (DEN follow-ups), 5 (dropout), 6a (due immunity checks,
 // eligibility buckets, active count).  engine.py:244-310.
-__global__ void k_iv_post(StepArgs A, uint8_t* __restrict__ bucket, unsigned long long* __restrict__ hist) {
-  __shared__ RecAcc racc;
-  __shared__ unsigned long long h[NUM_BUCKETS];
-  rec_init(racc);
-  for (int i = threadIdx.x; i < NUM_BUCKETS; i += blockDim.x) h[i] = 0;
-  __syncthreads();
+__device__ __forceinline__ void iv_post_agent(const StepArgs& A, int64_t a, uint8_t* __restrict__ bucket,
+                                              unsigned* h, unsigned& notified, unsigned& active) {
   const epi_params* __restrict__ P = A.P;
   const epi_state& st = A.st;
   const int step = A.step;
+  const uint8_t fl = A.flags[a];
+  if (P->den_enabled && (fl & FL_NOTIFIED) && st.has_den_app[a] &&
+      st.quarantine_until[a] <= step && st.stage[a] != S_DEAD) {
+    notified = 1;
+    if (draw(A.K, A.inj, P_DEN, a) < P->den_compliance) st.den_test_due_at[a] = step + 1;
+  }
+  if (P->quarantine_enabled && st.quarantine_until[a] > step && st.quarantine_started_at[a] < step) {
+    if (draw(A.K, A.inj, P_QDROP, a) < P->quarantine_dropout) st.quarantine_until[a] = step;
+  }
+  if (P->vaccination_enabled) {
+    if (st.immunity_check_at[a] == step) {
+      const int dose = st.immunity_check_dose[a];
+      if (dose == 1 || dose == 2) realize_immunity(A, a, dose);
+    }
+    const int stage = st.stage[a];
+    active = active_stage(stage);
+    const bool blocked = stage == S_DEAD || stage == S_HOSP || stage == S_ICU;
+    const int vs = st.vaccine_status[a];
+    const bool d1 = vs == 0 && !blocked;
+    const int32_t d1at = st.dose1_at[a];
+    const bool d2 = vs == 1 && d1at != NEVER && step >= d1at + P->dose_gap && !blocked;
+    uint8_t bk = NO_BUCKET;
+    if (d1 || d2) {
+      const int age = st.age_band[a];
+      int group;
+      if (P->strategy == 0) group = d2 ? 0 : 1;
+      else if (P->strategy == 1) group = d2 ? 1 : 0;
+      else group = (age >= P->elderly_band) ? 0 : (d2 ? 2 : 1);
+      bk = (uint8_t)((group * 9 + (8 - age)) * 2 + (d2 ? 1 : 0));
+      atomicAdd(&h[bk], 1u);
+    }
+    bucket[a] = bk;
+  }
+}
+
+__global__ void k_iv_post(StepArgs A, uint8_t* __restrict__ bucket, unsigned long long* __restrict__ hist) {
+  __shared__ RecAcc racc;
+  __shared__ unsigned h[NUM_BUCKETS];
+  rec_init(racc);
+  for (int i = threadIdx.x; i < NUM_BUCKETS; i += blockDim.x) h[i] = 0;
+  __syncthreads();
   const int64_t n = A.hi;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t base = A.lo + blockIdx.x * (int64_t)blockDim.x; base < n; base += stride) {
     const int64_t a = base + threadIdx.x;
     unsigned notified = 0, active = 0;
-    if (a < n) {
-      const uint8_t fl = A.flags[a];
-      if (P->den_enabled && (fl & FL_NOTIFIED) && st.has_den_app[a] &&
-          st.quarantine_until[a] <= step && st.stage[a] != S_DEAD) {
-        notified = 1;
-        if (draw(A.K, A.inj, P_DEN, a) < P->den_compliance) st.den_test_due_at[a] = step + 1;
-      }
-      if (P->quarantine_enabled && st.quarantine_until[a] > step && st.quarantine_started_at[a] < step) {
-        if (draw(A.K, A.inj, P_QDROP, a) < P->quarantine_dropout) st.quarantine_until[a] = step;
-      }
-      if (P->vaccination_enabled) {
-        if (st.immunity_check_at[a] == step) {
-          const int dose = st.immunity_check_dose[a];
-          if (dose == 1 || dose == 2) realize_immunity(A, a, dose);
-        }
-        const int stage = st.stage[a];
-        active = active_stage(stage);
-        const bool blocked = stage == S_DEAD || stage == S_HOSP || stage == S_ICU;
-        const int vs = st.vaccine_status[a];
-        const bool d1 = vs == 0 && !blocked;
-        const int32_t d1at = st.dose1_at[a];
-        const bool d2 = vs == 1 && d1at != NEVER && step >= d1at + P->dose_gap && !blocked;
-        uint8_t bk = NO_BUCKET;
-        if (d1 || d2) {
-          const int age = st.age_band[a];
-          int group;
-          if (P->strategy == 0) group = d2 ? 0 : 1;
-          else if (P->strategy == 1) group = d2 ? 1 : 0;
-          else group = (age >= P->elderly_band) ? 0 : (d2 ? 2 : 1);
-          bk = (uint8_t)((group * 9 + (8 - age)) * 2 + (d2 ? 1 : 0));
-          atomicAdd(&h[bk], 1ull);
-        }
-        bucket[a] = bk;
-      }
-    }
+    if (a < n) iv_post_agent(A, a, bucket, h, notified, active);
     rec_add(racc, EPI_REC_NOTIFY, notified);
     rec_add(racc, EPI_REC_ACTIVE, active);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < NUM_BUCKETS; i += blockDim.x)
-    if (h[i]) atomicAdd(&hist[i], h[i]);
+    if (h[i]) atomicAdd(&hist[i], (unsigned long long)h[i]);
   rec_flush(racc, A.rec, A.step);
 }
 
@@ -1102,12 +1146,11 @@ __global__ void k_iv_post(StepArgs A, uint8_t* __restrict__ bucket, unsigned lon
 // active count when `global_active` (partitioned runs: summed over ranks),
 // else the active count is this record's.  Only `write_doses` ranks record
 // the doses given (rank 0 of a partitioned run).
-__global__ void k_vax_plan(const epi_params* __restrict__ P, const unsigned long long* __restrict__ hist,
-                           long long* rec, int32_t* vax_open, long long* plan, int global_active,
-                           int write_doses) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+__device__ __forceinline__ void vax_plan(const epi_params* __restrict__ P, const unsigned long long* hist,
+                                         long long* rec, int32_t* vax_open, long long* plan, int global_active,
+                                         int write_doses) {
   int open = *vax_open;
-  const double active = global_active ? (double)hist[NUM_BUCKETS] : (double)rec[EPI_REC_ACTIVE];
+  const double active = global_active ? (double)__ldcg(hist + NUM_BUCKETS) : (double)__ldcg(rec + EPI_REC_ACTIVE);
   if (!open && active >= P->start_trigger_count) open = 1;
   *vax_open = open;
   plan[0] = -1;
@@ -1116,7 +1159,7 @@ __global__ void k_vax_plan(const epi_params* __restrict__ P, const unsigned long
   if (!open || budget <= 0) return;
   long long cum = 0;
   for (int b = 0; b < NUM_BUCKETS; ++b) {
-    const long long c = (long long)hist[b];
+    const long long c = (long long)__ldcg(hist + b);
     if (cum + c >= budget) {
       plan[0] = b;
       plan[1] = budget - cum;
@@ -1128,6 +1171,37 @@ __global__ void k_vax_plan(const epi_params* __restrict__ P, const unsigned long
   plan[0] = NUM_BUCKETS;       // everyone eligible gets a dose
   plan[1] = 0;
   if (write_doses) rec[EPI_REC_DOSES] = cum;
+}
+
+__global__ void k_vax_plan(const epi_params* __restrict__ P, const unsigned long long* __restrict__ hist,
+                           long long* rec, int32_t* vax_open, long long* plan, int global_active,
+                           int write_doses) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  vax_plan(P, hist, rec, vax_open, plan, global_active, write_doses);
+}
+
+// Phase 6b for one selected agent (engine.py:306-335): bucket bit 0 = dose rank.
+__device__ __forceinline__ void give_dose(const StepArgs& A, int64_t a, uint8_t bk) {
+  const epi_params* __restrict__ P = A.P;
+  const epi_state& st = A.st;
+  const int step = A.step;
+  if ((bk & 1) == 0) {       // first dose
+    st.vaccine_status[a] = 1;
+    st.dose1_at[a] = step;
+    st.immunity_check_at[a] = step + P->dose1_latency;
+    st.immunity_check_prob[a] = P->dose1_efficacy;
+    st.immunity_check_dose[a] = 1;
+    if (P->dose1_latency == 0) realize_immunity(A, a, 1);
+  } else {                   // second dose
+    st.vaccine_status[a] = 2;
+    st.dose2_at[a] = step;
+    double prob = (st.immunity_check_at[a] != NEVER) ? P->dose2_efficacy : P->dose2_topup;
+    if (st.immune[a]) prob = 0.0;
+    st.immunity_check_at[a] = step + P->dose2_latency;
+    st.immunity_check_prob[a] = prob;
+    st.immunity_check_dose[a] = 2;
+    if (P->dose2_latency == 0) realize_immunity(A, a, 2);
+  }
 }
 
 constexpr int VAX_TILE = 1024;
@@ -1178,9 +1252,6 @@ __global__ void __launch_bounds__(1024) k_vax_apply(StepArgs A, const uint8_t* _
   typedef cub::BlockScan<int, 1024> Scan;
   __shared__ typename Scan::TempStorage tmp;
   const long long cut = plan[0], rem = plan[1] - (offset ? *offset : 0);
-  const epi_params* __restrict__ P = A.P;
-  const epi_state& st = A.st;
-  const int step = A.step;
   const int64_t n = A.hi;
   const int64_t a = A.lo + blockIdx.x * (int64_t)VAX_TILE + threadIdx.x;
   const uint8_t bk = a < n ? bucket[a] : NO_BUCKET;
@@ -1188,25 +1259,8 @@ __global__ void __launch_bounds__(1024) k_vax_apply(StepArgs A, const uint8_t* _
   int rank;
   Scan(tmp).ExclusiveSum(in_cut, rank);
   if (cut < 0 || bk == NO_BUCKET) return;
-  bool take = (long long)bk < cut || (in_cut && (long long)(tile_off[blockIdx.x] + rank) < rem);
-  if (!take) return;
-  if ((bk & 1) == 0) {       // first dose
-    st.vaccine_status[a] = 1;
-    st.dose1_at[a] = step;
-    st.immunity_check_at[a] = step + P->dose1_latency;
-    st.immunity_check_prob[a] = P->dose1_efficacy;
-    st.immunity_check_dose[a] = 1;
-    if (P->dose1_latency == 0) realize_immunity(A, a, 1);
-  } else {                   // second dose
-    st.vaccine_status[a] = 2;
-    st.dose2_at[a] = step;
-    double prob = (st.immunity_check_at[a] != NEVER) ? P->dose2_efficacy : P->dose2_topup;
-    if (st.immune[a]) prob = 0.0;
-    st.immunity_check_at[a] = step + P->dose2_latency;
-    st.immunity_check_prob[a] = prob;
-    st.immunity_check_dose[a] = 2;
-    if (P->dose2_latency == 0) realize_immunity(A, a, 2);
-  }
+  const bool take = (long long)bk < cut || (in_cut && (long long)(tile_off[blockIdx.x] + rank) < rem);
+  if (take) give_dose(A, a, bk);
 }
 
 // Last kernel of an intervention step: record + next codes + clear flags.
@@ -1225,6 +1279,158 @@ __global__ void k_finish(StepArgs A, uint16_t* __restrict__ codes_next, const ep
       if (codes_next) codes_next[a] = next_code(A.P, A.st, a, A.step + 1, net, rcount_next);
       if (A.flags) A.flags[a] = 0;
     }
+  }
+  __syncthreads();
+  rec_flush(racc, A.rec, A.step);
+}
+
+// ---------------------------------------------------------------------------
+// Intervention day on the whole population in three launches after the fused
+// day kernel (which also runs the testing phase): [k_den_regen] ->
+// k_iv_post_chunks -> k_finish_iv.  Both walk the same contiguous chunks (one
+// per block, a multiple of 256 agents), so a chunk is the vaccination tile:
+//   k_iv_post_chunks: phases 4b/5/6a per agent; the chunk's 54-bucket
+//     eligibility histogram to tile_hist[block] and into the day's histogram;
+//   k_finish_iv: every block derives the vaccination plan (trigger latch, cut
+//     bucket, remaining budget: k_vax_plan) from the day's histogram and its
+//     chunk's offset in the cut bucket from the earlier chunks' counts
+//     (k_vax_tilecount + k_vax_tilescan), gives the doses in id order
+//     (k_vax_apply), records the day each agent died (k_died_update, one day
+//     early), the record, next codes, cleared flags, and tomorrow's push
+//     tables (the merged fused epilogue) — so no k_day_tables.
+// The day's histogram is parity-buffered: k_finish_iv zeroes tomorrow's.
+// Same per-agent operations as the per-phase kernels: bitwise the same run.
+struct IvPlan {
+  unsigned long long* hist;     // [2][NUM_BUCKETS] by day parity
+  unsigned* tile_hist;          // [blocks][NUM_BUCKETS]
+  int32_t* vax_open;
+  int64_t chunk;
+  int vax;
+};
+
+__global__ void __launch_bounds__(256) k_iv_post_chunks(StepArgs A, uint8_t* __restrict__ bucket, IvPlan V) {
+  __shared__ RecAcc racc;
+  __shared__ unsigned h[NUM_BUCKETS];
+  rec_init(racc);
+  for (int i = threadIdx.x; i < NUM_BUCKETS; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  const int64_t lo = A.lo + blockIdx.x * V.chunk;
+  const int64_t hi = lo + V.chunk < A.hi ? lo + V.chunk : A.hi;
+  for (int64_t base = lo; base < hi; base += blockDim.x) {
+    const int64_t a = base + threadIdx.x;
+    unsigned notified = 0, active = 0;
+    if (a < hi) iv_post_agent(A, a, bucket, h, notified, active);
+    rec_add(racc, EPI_REC_NOTIFY, notified);
+    rec_add(racc, EPI_REC_ACTIVE, active);
+  }
+  __syncthreads();
+  if (V.vax) {
+    unsigned long long* hist = V.hist + (A.step & 1) * NUM_BUCKETS;
+    for (int i = threadIdx.x; i < NUM_BUCKETS; i += blockDim.x) {
+      V.tile_hist[(size_t)blockIdx.x * NUM_BUCKETS + i] = h[i];
+      if (h[i]) atomicAdd(&hist[i], (unsigned long long)h[i]);
+    }
+  }
+  rec_flush(racc, A.rec, A.step);
+}
+
+__global__ void __launch_bounds__(256) k_finish_iv(StepArgs A, uint16_t* __restrict__ codes_next,
+                                                   const epi_net* net_dev, uint64_t rcount_next,
+                                                   const uint8_t* __restrict__ bucket, IvPlan V,
+                                                   int32_t* __restrict__ died_at, int* den_count, epi_net net,
+                                                   NextTables nx, Radix dn) {
+  typedef cub::BlockScan<int, 256> Scan;
+  typedef cub::BlockReduce<int, 256> Reduce;
+  __shared__ union {
+    typename Scan::TempStorage scan;
+    typename Reduce::TempStorage reduce;
+  } tmp;
+  __shared__ RecAcc racc;
+  __shared__ PermKeys rk_next[EPI_MAX_SLOTS];
+  __shared__ int excl_s[8][32];
+  __shared__ uint16_t cn_s[8][32];
+  __shared__ unsigned long long h_s[NUM_BUCKETS];
+  __shared__ long long plan_s[2];
+  __shared__ int off_s;
+  rec_init(racc);
+  const int warp = threadIdx.x >> 5, lane = lane_id();
+  long long cut = -1, rem = 0;
+  int carry = 0;
+  if (V.vax) {
+    // the day's plan, derived by every block from the complete histogram
+    const unsigned long long* hist = V.hist + (A.step & 1) * NUM_BUCKETS;
+    for (int i = threadIdx.x; i < NUM_BUCKETS; i += blockDim.x) h_s[i] = hist[i];
+    if (blockIdx.x == 0)     // tomorrow's histogram starts empty
+      for (int i = threadIdx.x; i < NUM_BUCKETS; i += blockDim.x) V.hist[((A.step + 1) & 1) * NUM_BUCKETS + i] = 0;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const epi_params* __restrict__ P = A.P;
+      int open = *V.vax_open;
+      if (!open && (double)A.rec[EPI_REC_ACTIVE] >= P->start_trigger_count) open = 1;
+      long long c = -1, r = 0, doses = -1;
+      if (open && P->dose_budget > 0) {
+        long long cum = 0;
+        c = NUM_BUCKETS;                // everyone eligible gets a dose
+        doses = -2;
+        for (int b = 0; b < NUM_BUCKETS; ++b) {
+          const long long hb = (long long)h_s[b];
+          if (cum + hb >= P->dose_budget) { c = b; r = P->dose_budget - cum; doses = P->dose_budget; break; }
+          cum += hb;
+        }
+        if (doses == -2) doses = cum;
+      }
+      if (blockIdx.x == 0) {     // the latch only ever closes -> opens: a late reader derives the same
+        *V.vax_open = open;
+        if (doses >= 0) A.rec[EPI_REC_DOSES] = doses;
+      }
+      plan_s[0] = c;
+      plan_s[1] = r;
+    }
+    __syncthreads();
+    cut = plan_s[0];
+    rem = plan_s[1];
+    // this chunk's offset in the cut bucket: the earlier chunks' counts
+    int part = 0;
+    if (cut >= 0 && cut < NUM_BUCKETS)
+      for (int t = threadIdx.x; t < (int)blockIdx.x; t += blockDim.x)
+        part += (int)V.tile_hist[(size_t)t * NUM_BUCKETS + cut];
+    const int tot = Reduce(tmp.reduce).Sum(part);
+    if (threadIdx.x == 0) off_s = tot;
+    __syncthreads();
+    carry = off_s;
+  }
+  load_next_keys(nx, rk_next);
+  if (den_count && blockIdx.x == 0 && threadIdx.x == 0) *den_count = 0;   // tomorrow's notifier list
+  const bool in_scan = cut >= 0 && cut < NUM_BUCKETS;
+  const int64_t lo = A.lo + blockIdx.x * V.chunk;
+  const int64_t hi = lo + V.chunk < A.hi ? lo + V.chunk : A.hi;
+  for (int64_t base = lo; base < hi; base += blockDim.x) {
+    const int64_t a = base + threadIdx.x;
+    const bool valid = a < hi;
+    if (V.vax) {
+      const uint8_t bk = valid ? bucket[a] : NO_BUCKET;
+      const int in_cut = (in_scan && bk == (uint8_t)cut) ? 1 : 0;
+      int rank, total;
+      Scan(tmp.scan).ExclusiveSum(in_cut, rank, total);
+      if (cut >= 0 && bk != NO_BUCKET &&
+          ((long long)bk < cut || (in_cut && (long long)(carry + rank) < rem)))
+        give_dose(A, a, bk);
+      carry += total;
+      __syncthreads();
+    }
+    int stage = 0;
+    int32_t inf = 0;
+    uint16_t cn = 0;
+    if (valid) {
+      stage = A.st.stage[a];
+      inf = A.st.infected_at[a];
+      if (died_at && stage == S_DEAD && died_at[a] == INT32_MAX) died_at[a] = A.step;
+      cn = next_code(A.P, A.st, a, A.step + 1, net_dev, rcount_next);
+      codes_next[a] = cn;
+      A.flags[a] = 0;
+    }
+    rec_agent(racc, valid, stage, inf);
+    push_next_day(net, nx, valid, a, cn, rk_next, dn, excl_s[warp], cn_s[warp], base + (threadIdx.x & ~31), lane);
   }
   __syncthreads();
   rec_flush(racc, A.rec, A.step);

@@ -93,7 +93,8 @@ def initial_columns(pop: ConfigPopulation) -> AgentColumns:
 class ConfigSimulation:
     def __init__(self, pop: ConfigPopulation, disease, table, interventions, seed: int,
                  mode: str = "csr", precision: str = "f32", horizon: int = 180,
-                 device=None, initial=None, push_max: int | None = None, persistent: bool = True):
+                 device=None, initial=None, push_max: int | None = None, persistent: bool = True,
+                 iv_fusion: bool = True):
         import torch
         if mode not in ("csr", "fused"):
             raise ConfigError(f"unknown mode {mode!r}")
@@ -120,6 +121,8 @@ class ConfigSimulation:
             N.check(self._lib.epi_set_push_max(self._ctx, int(push_max)))
         # run(): merged fused days in one persistent launch (else one kernel per day)
         N.check(self._lib.epi_set_persistent(self._ctx, int(bool(persistent))))
+        # fused-mode intervention days in 4 launches (else one kernel per phase)
+        N.check(self._lib.epi_set_iv_fusion(self._ctx, int(bool(iv_fusion))))
         self.state = DeviceColumns(self.n, self.device)
         self._codes_buf = self._alloc_codes()
         self.codes = [self._codes_buf[0], self._codes_buf[1]]

@@ -63,3 +63,55 @@ def test_persistent_graph_replay_equals_run():
     a.replay()                                    # reset inside the graph: same result twice
     b.run()
     _same(a, b)
+
+
+def _iv(gap=7, den=True, vax=True, quarantine=True, testing=True):
+    from paper_2110_04421_b200.interventions import DenConfig, TestKind, VaccinePolicy
+    return InterventionConfig(quarantine_enabled=quarantine, testing_enabled=testing,
+                              test_kind=TestKind("cfg2", 0.3, 1, 2), den_enabled=den, den=DenConfig(0.6),
+                              vaccination_enabled=vax,
+                              vaccine=VaccinePolicy(daily_rate=0.02, dose1_efficacy=0.5, dose2_efficacy=0.9,
+                                                    dose_gap=gap, start_trigger=0.002))
+
+
+IV_COLS = COLS + ("quarantine_until", "vaccine_status", "dose1_at", "dose2_at", "immune", "den_test_due_at",
+                  "test_result_at", "immunity_check_at")
+
+
+@pytest.mark.parametrize("n,kw", [(20_000, {}), (100_000, {"gap": 21}), (7_777, {"vax": False}),
+                                  (9_001, {"den": False}), (5_003, {"den": False, "vax": False})])
+def test_fused_intervention_day_equals_per_phase_kernels(n, kw):
+    """k_fused_step(+tests) -> k_den_regen -> k_iv_post_plan -> k_finish_iv
+    against the per-phase kernels: bitwise records and state."""
+    spec = ConfigNetworkSpec.config(1, n_agents=n, initial_infections=max(20, n // 300))
+    pop = synthesize(spec, 3)
+    d, t = default_disease(), default_progression()
+    iv = _iv(**kw)
+    a = ConfigSimulation(pop, d, t, iv, 17, mode="fused", horizon=60, iv_fusion=True)
+    b = ConfigSimulation(pop, d, t, iv, 17, mode="fused", horizon=60, iv_fusion=False)
+    a.run(25); b.run(25)
+    a.step(); b.step()
+    a.run(); b.run()
+    ra, rb = a.rec.cpu().numpy(), b.rec.cpu().numpy()
+    assert np.array_equal(ra, rb), np.argwhere(ra != rb)[:5]
+    if kw.get("vax", True):
+        assert ra[:, 17].sum() > 0
+    if kw.get("den", True):
+        assert ra[:, 18].sum() > 0
+    assert ra[:, 16].sum() > 0
+    ha, hb = a.host_columns(), b.host_columns()
+    for c in IV_COLS:
+        assert np.array_equal(getattr(ha, c), getattr(hb, c)), c
+    assert torch.equal(a._codes_buf, b._codes_buf)
+    assert int(a.vax.item()) == int(b.vax.item())
+
+
+def test_fused_intervention_day_graph_replay():
+    spec = ConfigNetworkSpec.config(1, n_agents=30_000, initial_infections=100)
+    pop = synthesize(spec, 4)
+    d, t = default_disease(), default_progression()
+    a = ConfigSimulation(pop, d, t, _iv(), 23, mode="fused", horizon=80)
+    b = ConfigSimulation(pop, d, t, _iv(), 23, mode="fused", horizon=80, iv_fusion=False)
+    a.capture(); a.replay(); a.replay()
+    b.run()
+    assert np.array_equal(a.rec.cpu().numpy(), b.rec.cpu().numpy())
