@@ -906,13 +906,21 @@ int epi_net_csr(epi_ctx* c, int32_t step, uint32_t** entries, int32_t** row_len)
   return 0;
 }
 
-// Chunks of k_iv_post_chunks / k_finish_iv: a multiple of 256 agents each, at
-// most 8 blocks per SM.
+// Balanced grids: a multiple of the SM count, the agents split into equal
+// contiguous chunks (<= `threads` agents per block up to `per_sm` blocks per
+// SM, longer chunks beyond), so no SM carries an extra block.
+static int balanced_grid(int64_t n, int threads, int per_sm) {
+  const int64_t sms = sm_count();
+  int64_t k = (n + sms * threads - 1) / (sms * threads);
+  k = k < 1 ? 1 : (k > per_sm ? per_sm : k);
+  return (int)(sms * k);
+}
+
+// Chunks of k_iv_post_chunks / k_finish_iv (the vaccination tiles).
 static void iv_chunks(int64_t n, int64_t* chunk, int* blocks) {
-  const int64_t g0 = grid_for(n, 256);
-  int64_t ch = (n + g0 - 1) / g0;
-  ch = (ch + 255) / 256 * 256;
-  *chunk = ch < 256 ? 256 : ch;
+  *blocks = balanced_grid(n, 256, 1 << 20);
+  *chunk = (n + *blocks - 1) / *blocks;
+  if (*chunk < 1) *chunk = 1;
   *blocks = (int)((n + *chunk - 1) / *chunk);
 }
 
@@ -962,7 +970,7 @@ static int iv_fused_day(epi_ctx* c, const StepArgs& A, int32_t step, uint64_t se
     CK(cudaMemsetAsync(rec, 0, EPI_REC_LEN * sizeof(long long), s));
   }
   if (ev) CK(cudaEventRecord((cudaEvent_t)ev[1], s));
-  const int fgrid = grid_for(c->n, 128, 16);
+  const int fgrid = balanced_grid(c->n, 128, 16);
   DayTests tests{p.testing_enabled ? 1 : 0, listed ? c->den_list : nullptr, listed ? c->den_count : nullptr};
   CK(launch_pdl_w(&c->hot, k_fused_step, dim3(fgrid), dim3(128), 0, s, A, c->net, nk, codes_cur,
                   c->host.rate_scale, codes_next, (const epi_net*)c->net_dev, rcount_next, 0,
@@ -1094,7 +1102,7 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
     CKL();
   } else {
     if (ev) CK(cudaEventRecord((cudaEvent_t)ev[1], s));
-    const int fgrid = grid_for(c->hi - c->lo, 128, 16);
+    const int fgrid = balanced_grid(c->hi - c->lo, 128, 16);
     NextTables nx{};
     if (merged) {
       nx.wt = c->wt_dev[par ^ 1][2];

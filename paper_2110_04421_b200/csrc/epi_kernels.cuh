@@ -814,9 +814,12 @@ __global__ void __launch_bounds__(128, 6) k_fused_step(StepArgs A, epi_net net, 
   if (merge) load_next_keys(nx, rk_next);
   const Radix dn = NT.dn;
   const int warp = threadIdx.x >> 5, lane = lane_id();
-  const int64_t n = A.hi;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t base = A.lo + blockIdx.x * (int64_t)blockDim.x; base < n; base += stride) {
+  // one contiguous chunk per block; the grid is a multiple of the SM count,
+  // so every SM carries the same number of agents
+  const int64_t chunk = (A.hi - A.lo + gridDim.x - 1) / gridDim.x;
+  const int64_t c_lo = A.lo + blockIdx.x * chunk;
+  const int64_t n = c_lo + chunk < A.hi ? c_lo + chunk : A.hi;
+  for (int64_t base = c_lo; base < n; base += blockDim.x) {
     const int64_t b = base + threadIdx.x;
     const bool valid = b < n;
     unsigned edges = 0;
