@@ -662,7 +662,7 @@ def run_config4(a):
         # concurrent replicas on 8 streams: per-day kernels (a persistent run
         # needs the whole GPU resident for its grid barrier)
         sims.append(ConfigSimulation(pop, d, t, iv, keyed.replication_seed(0, r), mode="fused",
-                                     horizon=HORIZON, persistent=False))
+                                     horizon=HORIZON, persistent=os.environ.get("EPI_C4P") == "1"))
     streams = [torch.cuda.Stream() for _ in range(a.streams)]
     for s in sims:
         s.capture()

@@ -318,6 +318,14 @@ int epi_sim_run(epi_ctx *ctx, const epi_state *st, int32_t first_step, int32_t n
  * one resident thread per agent, a grid barrier per day); bitwise the same
  * results as the per-day kernels.  on = 0 forces the per-day kernels. */
 int epi_set_persistent(epi_ctx *ctx, int32_t on);
+/* Replication summary (runner.py:195-207 `summarize`): quartiles q25/q50/q75
+ * across n_rep <= 4096 replications, bitwise np.percentile (linear method).
+ * data: device int64 [n_rep][horizon][rec_len] (stacked records), cols:
+ * device int32[n_cols] record columns, out: device double
+ * [n_cols][horizon][3]. */
+int epi_quartiles(const int64_t *data, int64_t n_rep, int32_t horizon, int32_t rec_len,
+                  const int32_t *cols, int32_t n_cols, double *out, void *stream);
+
 /* Fused-mode intervention days on the whole population in 4 launches
  * (testing inside the day kernel; plan + doses + tomorrow's push tables in
  * k_iv_post_chunks / k_finish_iv); bitwise the same as the per-phase kernels

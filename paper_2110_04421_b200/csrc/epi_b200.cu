@@ -7,6 +7,7 @@
 #include <cub/device/device_radix_sort.cuh>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -18,6 +19,7 @@
 #include "epi_persistent.cuh"
 #include "epi_population.cuh"
 #include "epi_refnet.cuh"
+#include "epi_series.cuh"
 
 using namespace epi;
 
@@ -1102,7 +1104,7 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
     CKL();
   } else {
     if (ev) CK(cudaEventRecord((cudaEvent_t)ev[1], s));
-    const int fgrid = balanced_grid(c->hi - c->lo, 128, 16);
+    const int fgrid = balanced_grid(c->hi - c->lo, 128, getenv("EPI_FGRID") ? atoi(getenv("EPI_FGRID")) : 16);
     NextTables nx{};
     if (merged) {
       nx.wt = c->wt_dev[par ^ 1][2];
@@ -1229,6 +1231,18 @@ static int launch_run(epi_ctx* c, const epi_state* st, int32_t first, int32_t n_
 int epi_run_persistent(epi_ctx* c, int32_t mode, int32_t precision) {
   if (!c) return fail(EPI_EARG, "null ctx");
   return c->has_net && persistent_ok(c, mode, precision) ? 1 : 0;
+}
+
+int epi_quartiles(const int64_t* data, int64_t n_rep, int32_t horizon, int32_t rec_len, const int32_t* cols,
+                  int32_t n_cols, double* out, void* stream) {
+  if (!data || !cols || !out || n_rep < 1 || horizon < 0 || rec_len < 1 || n_cols < 0)
+    return fail(EPI_EARG, "bad argument");
+  if (n_rep > SUMMARY_MAX_R) return fail(EPI_EARG, "more than 4096 replications per summary");
+  if (horizon == 0 || n_cols == 0) return 0;
+  k_quartiles<<<dim3((unsigned)horizon, (unsigned)n_cols), 1024, 0, S(stream)>>>(data, (int)n_rep, horizon, rec_len,
+                                                                                  cols, out);
+  CKL();
+  return 0;
 }
 
 int epi_set_iv_fusion(epi_ctx* c, int32_t on) {

@@ -262,6 +262,14 @@ class ConfigSimulation:
         """[days, 19] rows in the reference CSV schema (runner.py:31-37)."""
         return self.records()[:, SERIES_COLUMNS]
 
+    def result(self, replication: int = 0):
+        """The run so far as the reference's `RunResult` (runner.py:41-74):
+        the CSV columns of the device records, the directed edges gathered."""
+        from .series import RunResult
+        rec = self.records()
+        return RunResult(replication=replication, seed=self.seed, data=rec[:, SERIES_COLUMNS].copy(),
+                         n_edges_total=int(rec[:, N.REC["edges"]].sum()))
+
     def host_columns(self) -> AgentColumns:
         return self.state.to_host()
 

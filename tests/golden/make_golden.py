@@ -4,6 +4,7 @@ Run in the build container only (needs /root/reference):
 
     PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py
     PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py independent   (row f4 fixtures)
+    PYTHONDONTWRITEBYTECODE=1 python tests/golden/make_golden.py series        (row f3 output fixtures)
 
 Writes small .npz fixtures next to this script.  The GPU box never reads
 /root/reference; tests load these fixtures instead.
@@ -183,7 +184,31 @@ STD_IV = {
 }
 
 
+def series_fixture():
+    """Row f3 (output): the reference's RunResult CSV, summarize() quartiles
+    and both summary CSV layouts, from real replications and from synthetic
+    ensembles (regenerated in the test from the same numpy seed)."""
+    from epivec.runner import (RunResult, run_replication, summarize, summary_to_csv,
+                               summary_to_long_csv)
+    cfg = scenario_from_dict({"population": dict(default_population_dict(), n_agents=300), "horizon": 15,
+                              "base_seed": 2, "replications": 7, "initial_infections": 10})
+    runs = [run_replication(cfg, i) for i in range(7)]
+    summ = summarize(runs)
+    out = {"run_data": runs[0].data, "run_seed": runs[0].seed, "run_csv": np.frombuffer(runs[0].to_csv().encode(), np.uint8),
+           "runs_data": np.stack([r.data for r in runs]),
+           "sum_wide": np.frombuffer(summary_to_csv(summ).encode(), np.uint8),
+           "sum_long": np.frombuffer(summary_to_long_csv(summ).encode(), np.uint8)}
+    for R, H, seed in ((1, 4, 10), (2, 4, 11), (5, 6, 12), (1000, 5, 13), (4096, 2, 14)):
+        data = np.random.default_rng(seed).integers(0, 100_000, size=(R, H, 19), dtype=np.int64)
+        s = summarize([RunResult(replication=i, seed=0, data=data[i]) for i in range(R)])
+        out[f"synth_{R}_{H}_{seed}"] = np.stack([s[m] for m in s])
+    np.savez_compressed(OUT / "series.npz", **out)
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["series"]:
+        series_fixture()
+        sys.exit(0)
     if sys.argv[1:] == ["independent"]:
         independent_fixture("indep_noiv", 800, 45, 21, {}, infections=20)
         independent_fixture("indep_alliv", 300, 30, 4, ALL_IV, infections=8)
