@@ -500,6 +500,19 @@ __device__ __forceinline__ void for_each_in_code(const epi_net& net, const NetKe
   }
 }
 
+// One source of a per-kind sum, branch-free: acc += factor[c & 0xFF] for every
+// slot.  A dead or absent source has code byte 0 and factor[0] = 0, and
+// acc + 0.0f == acc (acc >= +0), so the sums are bitwise those of skipping
+// it; `edges` counts the alive (resp. present) ones.
+__device__ __forceinline__ void add_src(float& acc, unsigned& edges, const float* __restrict__ factor, uint16_t c) {
+  acc += factor[c & 0xFF];
+  edges += ((unsigned)c >> 15) ^ 1u;
+}
+__device__ __forceinline__ void add_rin(float& acc, unsigned& edges, const float* __restrict__ factor, uint16_t c) {
+  acc += factor[c & 0xFF];
+  edges += ((unsigned)c >> 14) & 1u;
+}
+
 // Push-table form of for_each_in_code for the fused day kernel, written so
 // that every load of a level is issued before any of them is consumed
 // (memory-level parallelism for the ~21 warps per SM of a 100k-agent day):
@@ -562,22 +575,19 @@ __device__ __forceinline__ void push_kind_sums(const epi_net& net, const WorkTab
   }
   // accumulate in visit order
 #pragma unroll
-  for (int i = 0; i < HH; ++i)
-    if (!code_dead(hc[i])) { acc[0] += factor[hc[i] & 0xFF]; ++edges; }
+  for (int i = 0; i < HH; ++i) add_src(acc[0], edges, factor, hc[i]);
   for (int i = HH; i < sz; ++i) {            // households larger than HH (rare)
     if (start + i == b) continue;
-    const uint16_t cc = codes[start + i];
-    if (!code_dead(cc)) { acc[0] += factor[cc & 0xFF]; ++edges; }
+    add_src(acc[0], edges, factor, codes[start + i]);
   }
 #pragma unroll
   for (int j = 0; j < DR; ++j) {
-    if (!code_dead(wo[j])) { acc[1] += factor[wo[j] & 0xFF]; ++edges; }
-    if (!code_dead(wi[j])) { acc[1] += factor[wi[j] & 0xFF]; ++edges; }
+    add_src(acc[1], edges, factor, wo[j]);
+    add_src(acc[1], edges, factor, wi[j]);
   }
   if (net.n_agents < 2) return;
 #pragma unroll
-  for (int q = 0; q < 4; ++q)
-    if (!code_dead(co0[q])) { acc[2] += factor[co0[q] & 0xFF]; ++edges; }
+  for (int q = 0; q < 4; ++q) add_src(acc[2], edges, factor, co0[q]);
   for (int j0 = 4; j0 < nbe; j0 += 4) {       // more than 4 out-partners
     const uint4 o = ro[j0 >> 2];
     const uint32_t po[4] = {o.x, o.y, o.z, o.w};
@@ -585,14 +595,12 @@ __device__ __forceinline__ void push_kind_sums(const epi_net& net, const WorkTab
 #pragma unroll
     for (int q = 0; q < 4; ++q) co[q] = (j0 + q < nbe && po[q] != self) ? codes[po[q]] : (uint16_t)CODE_DEAD;
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
-      if (!code_dead(co[q])) { acc[2] += factor[co[q] & 0xFF]; ++edges; }
+    for (int q = 0; q < 4; ++q) add_src(acc[2], edges, factor, co[q]);
   }
   const uint4 inv[2] = {in0, in1};
   const uint16_t* iv = (const uint16_t*)inv;
 #pragma unroll
-  for (int j = 0; j < RT_SLOTS; ++j)
-    if (iv[j] & CODE_PRESENT) { acc[2] += factor[iv[j] & 0xFF]; ++edges; }
+  for (int j = 0; j < RT_SLOTS; ++j) add_rin(acc[2], edges, factor, iv[j]);
 }
 
 }  // namespace epi

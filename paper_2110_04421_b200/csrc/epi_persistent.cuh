@@ -194,22 +194,19 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_fused_run(RunArgs R, epi
         // per-kind sums in the visit order of for_each_in_code
         float acc[3] = {0.f, 0.f, 0.f};
 #pragma unroll
-        for (int i = 0; i < HH; ++i)
-          if (!code_dead(hc[i])) { acc[0] += T.factor[hc[i] & 0xFF]; ++edges; }
+        for (int i = 0; i < HH; ++i) add_src(acc[0], edges, T.factor, hc[i]);
         for (int i = HH; i < sz; ++i) {
           if (start + i == b) continue;
-          const uint16_t cc = LDM(codes + start + i);
-          if (!code_dead(cc)) { acc[0] += T.factor[cc & 0xFF]; ++edges; }
+          add_src(acc[0], edges, T.factor, LDM(codes + start + i));
         }
 #pragma unroll
         for (int j = 0; j < DR; ++j) {
-          if (!code_dead(wo[j])) { acc[1] += T.factor[wo[j] & 0xFF]; ++edges; }
-          if (!code_dead(wi[j])) { acc[1] += T.factor[wi[j] & 0xFF]; ++edges; }
+          add_src(acc[1], edges, T.factor, wo[j]);
+          add_src(acc[1], edges, T.factor, wi[j]);
         }
         if (n >= 2) {
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
-            if (!code_dead(co0[q])) { acc[2] += T.factor[co0[q] & 0xFF]; ++edges; }
+          for (int q = 0; q < 4; ++q) add_src(acc[2], edges, T.factor, co0[q]);
           for (int j0 = 4; j0 < nbe; j0 += 4) {
             const uint4 o = LDM(ro + (j0 >> 2));
             const uint32_t po[4] = {o.x, o.y, o.z, o.w};
@@ -218,14 +215,12 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_fused_run(RunArgs R, epi
             for (int q = 0; q < 4; ++q)
               co[q] = (j0 + q < nbe && po[q] != self) ? LDM(codes + po[q]) : (uint16_t)CODE_DEAD;
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
-              if (!code_dead(co[q])) { acc[2] += T.factor[co[q] & 0xFF]; ++edges; }
+            for (int q = 0; q < 4; ++q) add_src(acc[2], edges, T.factor, co[q]);
           }
           const uint4 inv[2] = {in0, in1};
           const uint16_t* iv = (const uint16_t*)inv;
 #pragma unroll
-          for (int j = 0; j < RT_SLOTS; ++j)
-            if (iv[j] & CODE_PRESENT) { acc[2] += T.factor[iv[j] & 0xFF]; ++edges; }
+          for (int j = 0; j < RT_SLOTS; ++j) add_rin(acc[2], edges, T.factor, iv[j]);
         }
         const float tot = acc[0] * T.bfac[0] + acc[1] * T.bfac[1] + acc[2] * T.bfac[2];
         if (h.stage == S_SUS && !(R.P->sterilizing && h.immune)) lam = (double)(tot * T.sfac[h.age]);
