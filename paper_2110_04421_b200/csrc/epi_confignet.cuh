@@ -513,6 +513,73 @@ __device__ __forceinline__ void add_rin(float& acc, unsigned& edges, const float
   edges += ((unsigned)c >> 14) & 1u;
 }
 
+// Branch-free per-kind sums of for_each_in_code without push rows (the
+// fused day kernel of partitioned ranks and of runs too large for the push
+// tables): the same visit order, every slot added (absent ones as code 0).
+// Needs the day's workplace code table (wt->wcode).
+__device__ __forceinline__ void code_kind_sums(const epi_net& net, const PermKeys* __restrict__ rk,
+                                               const Radix& dn, const WorkTables* __restrict__ wt,
+                                               const uint16_t* __restrict__ codes, int64_t b, uint16_t code_b,
+                                               const float* __restrict__ factor, float acc[3], unsigned& edges) {
+  {
+    const int off = net.hh_off[b];
+    const int sz = net.hh_size[b];
+    const int64_t start = b - off;
+    for (int i = 0; i < sz; ++i) {
+      const int64_t c = start + i;
+      add_src(acc[0], edges, factor, c == b ? (uint16_t)CODE_DEAD : codes[c]);
+    }
+  }
+  const int w = net.wp_id[b];
+  if (w >= 0) {
+    const int m = net.wp_size[w];
+    if (m >= 2) {
+      const int base = net.wp_base[w];
+      const int draws = net.colleague_draws;
+      const uint32_t p = wt->pos_of[base + net.wp_local[b]];
+      const uint8_t* sh = wt->shift + (size_t)w * draws;
+      const uint16_t* wc = wt->wcode + base;
+      for (int j = 0; j < draws; ++j) {
+        const uint32_t r = sh[j];
+        add_src(acc[1], edges, factor, wc[add_mod(p, r, (uint32_t)m)]);
+        add_src(acc[1], edges, factor, wc[sub_mod(p, r, (uint32_t)m)]);
+      }
+    }
+  }
+  if (net.n_agents < 2) return;
+  const uint32_t self = (uint32_t)b;
+  const int nb = code_count(code_b);
+  const int slots = net.random_slots;
+  const int nbe = nb < slots ? nb : slots;
+  for (int j0 = 0; j0 < nbe; j0 += 4) {
+    uint32_t po[4];
+    uint16_t co[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) po[q] = (j0 + q < nbe) ? walk_fwd(self, rk[j0 + q], dn) : self;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) co[q] = po[q] != self ? codes[po[q]] : (uint16_t)CODE_DEAD;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) add_src(acc[2], edges, factor, co[q]);
+  }
+  for (int j0 = 0; j0 < slots; j0 += 8) {
+    uint32_t pi[8];
+    uint16_t ci[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) pi[q] = (j0 + q < slots) ? perm_inv(self, rk[j0 + q], dn) : self;
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (pi[q] >= dn.n) pi[q] = walk_inv(pi[q], rk[j0 + q], dn);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) ci[q] = pi[q] != self ? codes[pi[q]] : (uint16_t)0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const bool in = j0 + q < code_count(ci[q]);
+      acc[2] += in ? factor[ci[q] & 0xFF] : 0.f;
+      edges += in ? 1u : 0u;
+    }
+  }
+}
+
 // Push-table form of for_each_in_code for the fused day kernel, written so
 // that every load of a level is issued before any of them is consumed
 // (memory-level parallelism for the ~21 warps per SM of a 100k-agent day):

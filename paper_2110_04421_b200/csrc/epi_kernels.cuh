@@ -835,10 +835,7 @@ __global__ void __launch_bounds__(128, 6) k_fused_step(StepArgs A, epi_net net, 
         if (push)
           push_kind_sums(net, wt, codes, b, cb, T.factor, acc, edges);
         else
-          for_each_in_code(net, nk, NT.rk, NT.wrad, dn, wt, codes, b, cb, [&](int kind, uint16_t cc) {
-            ++edges;
-            acc[kind] += T.factor[cc & 0xFF];
-          });
+          code_kind_sums(net, NT.rk, dn, wt, codes, b, cb, T.factor, acc, edges);
         const float tot = acc[0] * T.bfac[0] + acc[1] * T.bfac[1] + acc[2] * T.bfac[2];
         if (h.stage == S_SUS && !(A.P->sterilizing && h.immune)) lam = (double)(tot * T.sfac[h.age]);
       }
