@@ -725,7 +725,8 @@ __device__ __forceinline__ unsigned test_agent(const StepArgs& A, int64_t a, int
 //              rout[a][j] = pi_j(a), rin[pi_j(a)][j] = cn | PRESENT.
 __device__ __forceinline__ void push_next_day(const epi_net& net, const NextTables& nx, bool valid, int64_t b,
                                               uint16_t cn, const PermKeys* rk_next, const Radix& dn,
-                                              int* excl_w, uint16_t* cn_w, int64_t wbase_agent, int lane) {
+                                              int* excl_w, uint16_t* cn_w, uint8_t* own_w, int64_t wbase_agent,
+                                              int lane) {
   const WorkTables& W = *nx.wt;
   const int w = valid ? net.wp_id[b] : -1;
   if (w >= 0) {
@@ -749,14 +750,13 @@ __device__ __forceinline__ void push_next_day(const epi_net& net, const NextTabl
     if (lane >= o) incl += v;
   }
   const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
-  excl_w[lane] = incl - na;
+  const int excl = incl - na;
+  excl_w[lane] = excl;
   cn_w[lane] = cn;
+  for (int i = 0; i < na; ++i) own_w[excl + i] = (uint8_t)lane;   // item -> its agent's lane
   __syncwarp();
   for (int k = lane; k < total; k += 32) {
-    int l = 0;
-#pragma unroll
-    for (int st = 16; st >= 1; st >>= 1)
-      if (l + st < 32 && excl_w[l + st] <= k) l += st;
+    const int l = own_w[k];
     const int j = k - excl_w[l];
     const uint32_t src = (uint32_t)(wbase_agent + l);
     const uint32_t y = walk_fwd(src, rk_next[j], dn);
@@ -797,6 +797,7 @@ __global__ void __launch_bounds__(128, 6) k_fused_step(StepArgs A, epi_net net, 
   __shared__ PermKeys rk_next[EPI_MAX_SLOTS];
   __shared__ int excl_s[4][32];
   __shared__ uint16_t cn_s[4][32];
+  __shared__ uint8_t own_s[4][32 * RT_SLOTS];
   load_msg_tables(T, mt);
   // with the day's push tables (random rows + workplace codes) only the agent
   // domain is needed; the epilogue derives workplace domains on the fly
@@ -865,8 +866,8 @@ __global__ void __launch_bounds__(128, 6) k_fused_step(StepArgs A, epi_net net, 
         codes_next[b] = cn;
       }
       if (merge)
-        push_next_day(net, nx, valid, b, cn, rk_next, dn, excl_s[warp], cn_s[warp], base + (threadIdx.x & ~31),
-                      lane);
+        push_next_day(net, nx, valid, b, cn, rk_next, dn, excl_s[warp], cn_s[warp], own_s[warp],
+                      base + (threadIdx.x & ~31), lane);
     }
   }
   __syncthreads();
@@ -1349,6 +1350,7 @@ __global__ void __launch_bounds__(256) k_finish_iv(StepArgs A, uint16_t* __restr
   __shared__ PermKeys rk_next[EPI_MAX_SLOTS];
   __shared__ int excl_s[8][32];
   __shared__ uint16_t cn_s[8][32];
+  __shared__ uint8_t own_s[8][32 * RT_SLOTS];
   __shared__ unsigned long long h_s[NUM_BUCKETS];
   __shared__ long long plan_s[2];
   __shared__ int off_s;
@@ -1430,7 +1432,8 @@ __global__ void __launch_bounds__(256) k_finish_iv(StepArgs A, uint16_t* __restr
       A.flags[a] = 0;
     }
     rec_agent(racc, valid, stage, inf);
-    push_next_day(net, nx, valid, a, cn, rk_next, dn, excl_s[warp], cn_s[warp], base + (threadIdx.x & ~31), lane);
+    push_next_day(net, nx, valid, a, cn, rk_next, dn, excl_s[warp], cn_s[warp], own_s[warp],
+                  base + (threadIdx.x & ~31), lane);
   }
   __syncthreads();
   rec_flush(racc, A.rec, A.step);
