@@ -659,10 +659,12 @@ def run_config4(a):
         r = rank * a.replicas + i
         u = keyed.uniform(0, 0, keyed.Purpose.REPLICATION, r, k=1)
         d = d0.with_rate(d0.rate_scale * (0.5 + u))
-        # concurrent replicas on 8 streams: per-day kernels (a persistent run
-        # needs the whole GPU resident for its grid barrier)
+        # concurrent replicas on 8 streams: per-day kernels on one block per
+        # SM each (a persistent run needs the whole GPU resident for its grid
+        # barrier; measured: 1 block/SM 63.8 k replica-steps/s, 16: 59.4 k,
+        # persistent replicas one after another: 61.1 k)
         sims.append(ConfigSimulation(pop, d, t, iv, keyed.replication_seed(0, r), mode="fused",
-                                     horizon=HORIZON, persistent=os.environ.get("EPI_C4P") == "1"))
+                                     horizon=HORIZON, persistent=False, day_blocks_per_sm=1))
     streams = [torch.cuda.Stream() for _ in range(a.streams)]
     for s in sims:
         s.capture()

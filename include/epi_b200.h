@@ -331,6 +331,10 @@ int epi_quartiles(const int64_t *data, int64_t n_rep, int32_t horizon, int32_t r
  * k_iv_post_chunks / k_finish_iv); bitwise the same as the per-phase kernels
  * (on = 0). */
 int epi_set_iv_fusion(epi_ctx *ctx, int32_t on);
+/* Grid of the per-day fused kernel: at most blocks_per_sm blocks per SM
+ * (0 = default 16).  Replicas run concurrently on several streams fill the
+ * GPU better with 1 (config 4). */
+int epi_set_day_grid(epi_ctx *ctx, int32_t blocks_per_sm);
 /* 1 if epi_sim_run(mode, precision) of >= 2 days would use k_fused_run. */
 int epi_run_persistent(epi_ctx *ctx, int32_t mode, int32_t precision);
 

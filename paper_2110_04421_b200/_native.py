@@ -100,6 +100,7 @@ _SIGS = {
     "epi_set_push_max": (_i32, [_p, _i64]),
     "epi_set_persistent": (_i32, [_p, _i32]),
     "epi_set_iv_fusion": (_i32, [_p, _i32]),
+    "epi_set_day_grid": (_i32, [_p, _i32]),
     "epi_quartiles": (_i32, [_p, _i64, _i32, _i32, _p, _i32, _p, _p]),
     "epi_run_persistent": (_i32, [_p, _i32, _i32]),
     "epi_last_error": (C.c_char_p, []),

@@ -175,6 +175,7 @@ struct epi_ctx {
   Injected* inj_dev = nullptr;
   int persistent = 1;                // epi_sim_run: one launch for the merged days
   int iv_fusion = 1;                 // intervention days in 4 launches (k_iv_post_chunks, k_finish_iv)
+  int day_blocks_per_sm = 16;        // k_fused_step grid cap (concurrent replicas: 1)
   unsigned* iv_tile_hist = nullptr;  // [chunks][NUM_BUCKETS]
   unsigned long long* iv_hist = nullptr;   // [2][NUM_BUCKETS] eligibility histogram by day parity
   unsigned* run_barrier = nullptr;   // arrival counter of k_fused_run's grid barrier
@@ -972,7 +973,7 @@ static int iv_fused_day(epi_ctx* c, const StepArgs& A, int32_t step, uint64_t se
     CK(cudaMemsetAsync(rec, 0, EPI_REC_LEN * sizeof(long long), s));
   }
   if (ev) CK(cudaEventRecord((cudaEvent_t)ev[1], s));
-  const int fgrid = balanced_grid(c->n, 128, 16);
+  const int fgrid = balanced_grid(c->n, 128, c->day_blocks_per_sm);
   DayTests tests{p.testing_enabled ? 1 : 0, listed ? c->den_list : nullptr, listed ? c->den_count : nullptr};
   CK(launch_pdl_w(&c->hot, k_fused_step, dim3(fgrid), dim3(128), 0, s, A, c->net, nk, codes_cur,
                   c->host.rate_scale, codes_next, (const epi_net*)c->net_dev, rcount_next, 0,
@@ -1104,7 +1105,7 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
     CKL();
   } else {
     if (ev) CK(cudaEventRecord((cudaEvent_t)ev[1], s));
-    const int fgrid = balanced_grid(c->hi - c->lo, 128, getenv("EPI_FGRID") ? atoi(getenv("EPI_FGRID")) : 16);
+    const int fgrid = balanced_grid(c->hi - c->lo, 128, c->day_blocks_per_sm);
     NextTables nx{};
     if (merged) {
       nx.wt = c->wt_dev[par ^ 1][2];
@@ -1242,6 +1243,12 @@ int epi_quartiles(const int64_t* data, int64_t n_rep, int32_t horizon, int32_t r
   k_quartiles<<<dim3((unsigned)horizon, (unsigned)n_cols), 1024, 0, S(stream)>>>(data, (int)n_rep, horizon, rec_len,
                                                                                   cols, out);
   CKL();
+  return 0;
+}
+
+int epi_set_day_grid(epi_ctx* c, int32_t blocks_per_sm) {
+  if (!c || blocks_per_sm < 0) return fail(EPI_EARG, "bad argument");
+  c->day_blocks_per_sm = blocks_per_sm == 0 ? 16 : blocks_per_sm;
   return 0;
 }
 

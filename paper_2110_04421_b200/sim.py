@@ -94,7 +94,7 @@ class ConfigSimulation:
     def __init__(self, pop: ConfigPopulation, disease, table, interventions, seed: int,
                  mode: str = "csr", precision: str = "f32", horizon: int = 180,
                  device=None, initial=None, push_max: int | None = None, persistent: bool = True,
-                 iv_fusion: bool = True):
+                 iv_fusion: bool = True, day_blocks_per_sm: int = 0):
         import torch
         if mode not in ("csr", "fused"):
             raise ConfigError(f"unknown mode {mode!r}")
@@ -123,6 +123,8 @@ class ConfigSimulation:
         N.check(self._lib.epi_set_persistent(self._ctx, int(bool(persistent))))
         # fused-mode intervention days in 4 launches (else one kernel per phase)
         N.check(self._lib.epi_set_iv_fusion(self._ctx, int(bool(iv_fusion))))
+        # per-day kernel grid cap (0 = default; 1 for replicas on concurrent streams)
+        N.check(self._lib.epi_set_day_grid(self._ctx, int(day_blocks_per_sm)))
         self.state = DeviceColumns(self.n, self.device)
         self._codes_buf = self._alloc_codes()
         self.codes = [self._codes_buf[0], self._codes_buf[1]]
