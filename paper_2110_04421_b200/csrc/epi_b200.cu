@@ -988,15 +988,14 @@ static int iv_fused_day(epi_ctx* c, const StepArgs& A, int32_t step, uint64_t se
     if (D.n_days > 0) {
       for (int d = 0; d < D.n_days; ++d) D.nk[d] = make_net_keys(seed, D.first_day + d);
       // one warp per (notifier, day) item, read on the device: one block per SM
-      k_den_regen<<<sm_count(), 256, 0, s>>>(c->net, D, c->died_at, c->den_list, c->den_count, c->flags,
-                                             (const Radix*)c->ntab_dev[0]->wrad);
-      CKL();
+      CK(launch_pdl_w(&c->hot, k_den_regen, dim3(sm_count()), dim3(256), 0, s, c->net, D, (const int32_t*)c->died_at,
+                      (const int32_t*)c->den_list, (const int*)c->den_count, c->flags,
+                      (const Radix*)c->ntab_dev[0]->wrad));
     }
   }
   IvPlan V{c->iv_hist, c->iv_tile_hist, vax_open, chunk, p.vaccination_enabled ? 1 : 0};
   if (p.den_enabled || p.quarantine_enabled || p.vaccination_enabled) {
-    k_iv_post_chunks<<<blocks, 256, 0, s>>>(A, c->bucket, V);
-    CKL();
+    CK(launch_pdl_w(&c->hot, k_iv_post_chunks, dim3(blocks), dim3(256), 0, s, A, c->bucket, V));
   }
   NextTables nx{};
   nx.wt = c->wt_dev[par ^ 1][2];
@@ -1004,10 +1003,9 @@ static int iv_fused_day(epi_ctx* c, const StepArgs& A, int32_t step, uint64_t se
   nx.keys_out = c->ntab_dev[(step + 2) % 3];
   nx.rperm_t2 = key_prefix(seed, step + 2, P_NET_RPERM);
   nx.nk = make_net_keys(seed, step + 1);
-  k_finish_iv<<<blocks, 256, 0, s>>>(A, codes_next, (const epi_net*)c->net_dev, rcount_next, c->bucket, V,
-                                      p.den_enabled ? c->died_at : nullptr, listed ? c->den_count : nullptr, c->net,
-                                      nx, c->ntab.dn);
-  CKL();
+  CK(launch_pdl_w(&c->hot, k_finish_iv, dim3(blocks), dim3(256), 0, s, A, codes_next, (const epi_net*)c->net_dev,
+                  rcount_next, (const uint8_t*)c->bucket, V, p.den_enabled ? c->died_at : (int32_t*)nullptr,
+                  listed ? c->den_count : (int*)nullptr, c->net, nx, c->ntab.dn));
   c->merged_ready = step + 1;
   if (ev) CK(cudaEventRecord((cudaEvent_t)ev[3], s));
   return 0;

@@ -1035,6 +1035,8 @@ __global__ void __launch_bounds__(256) k_den_regen(epi_net net, DenRegen D, cons
   __shared__ PermKeys rk[8][EPI_MAX_SLOTS];
   for (int m = threadIdx.x; m < 256; m += blockDim.x) wrad[m] = wrad_g[m];     // static workplace domains
   __syncthreads();
+  pdl_wait();
+  pdl_trigger();
   const int warp = threadIdx.x >> 5, lane = lane_id();
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   // one warp per (notifier, day)
@@ -1315,6 +1317,8 @@ __global__ void __launch_bounds__(256) k_iv_post_chunks(StepArgs A, uint8_t* __r
   rec_init(racc);
   for (int i = threadIdx.x; i < NUM_BUCKETS; i += blockDim.x) h[i] = 0;
   __syncthreads();
+  pdl_wait();
+  pdl_trigger();
   const int64_t lo = A.lo + blockIdx.x * V.chunk;
   const int64_t hi = lo + V.chunk < A.hi ? lo + V.chunk : A.hi;
   for (int64_t base = lo; base < hi; base += blockDim.x) {
@@ -1355,6 +1359,13 @@ __global__ void __launch_bounds__(256) k_finish_iv(StepArgs A, uint16_t* __restr
   __shared__ long long plan_s[2];
   __shared__ int off_s;
   rec_init(racc);
+  // prologue (overlaps the previous kernel): tomorrow's random-slot keys
+  // (written by yesterday's k_finish_iv)
+  for (int j = threadIdx.x; j < EPI_MAX_SLOTS; j += blockDim.x) rk_next[j] = nx.keys->rk[j];
+  pdl_wait();
+  pdl_trigger();
+  if (blockIdx.x == 0 && threadIdx.x < EPI_MAX_SLOTS)
+    nx.keys_out->rk[threadIdx.x] = random_slot_keys(nx.rperm_t2, threadIdx.x);
   const int warp = threadIdx.x >> 5, lane = lane_id();
   long long cut = -1, rem = 0;
   int carry = 0;
@@ -1401,7 +1412,7 @@ __global__ void __launch_bounds__(256) k_finish_iv(StepArgs A, uint16_t* __restr
     __syncthreads();
     carry = off_s;
   }
-  load_next_keys(nx, rk_next);
+  __syncthreads();
   if (den_count && blockIdx.x == 0 && threadIdx.x == 0) *den_count = 0;   // tomorrow's notifier list
   const bool in_scan = cut >= 0 && cut < NUM_BUCKETS;
   const int64_t lo = A.lo + blockIdx.x * V.chunk;
