@@ -1178,9 +1178,12 @@ static bool persistent_ok(epi_ctx* c, int32_t mode, int32_t precision) {
       !push_fits(c) || c->net.colleague_draws > 8)
     return false;
   static int per_sm = -1;
-  if (per_sm < 0 &&
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fused_run, RUN_MAX_THREADS, 0) != cudaSuccess)
-    per_sm = 0;
+  if (per_sm < 0) {
+    const size_t dyn = run_smem_bytes(RUN_MAX_DAYS);
+    if (cudaFuncSetAttribute(k_fused_run, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fused_run, RUN_MAX_THREADS, dyn) != cudaSuccess)
+      per_sm = 0;
+  }
   return per_sm >= 1 && run_threads(c->n) <= RUN_MAX_THREADS;
 }
 
@@ -1207,6 +1210,7 @@ static int launch_run(epi_ctx* c, const epi_state* st, int32_t first, int32_t n_
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)sm_count());
   cfg.blockDim = dim3((unsigned)run_threads(c->n));
+  cfg.dynamicSmemBytes = run_smem_bytes(n_days);
   cfg.stream = s;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeCooperative;     // every block resident: the grid barrier is safe
@@ -1279,8 +1283,22 @@ int epi_sim_run(epi_ctx* c, const epi_state* st, int32_t first_step, int32_t n_d
       if (rc) return rc;
       d0 = 1;
     }
-    return launch_run(c, st, first_step + d0, n_days - d0, seed, codes0, codes1,
-                      records + (size_t)d0 * EPI_REC_LEN, S(stream));
+    // launches of <= RUN_MAX_DAYS days (their keys live in shared memory)
+    for (int d = d0; d < n_days; d += RUN_MAX_DAYS) {
+      const int nd = n_days - d < RUN_MAX_DAYS ? n_days - d : RUN_MAX_DAYS;
+      if (nd == 1) {
+        const int t = first_step + d;
+        int rc = sim_step_impl(c, st, t, seed, mode, precision, (t & 1) ? codes1 : codes0,
+                               (t & 1) ? codes0 : codes1, records + (size_t)d * EPI_REC_LEN, vax_open, nullptr,
+                               stream, false);
+        if (rc) return rc;
+        continue;
+      }
+      int rc = launch_run(c, st, first_step + d, nd, seed, codes0, codes1, records + (size_t)d * EPI_REC_LEN,
+                          S(stream));
+      if (rc) return rc;
+    }
+    return 0;
   }
   for (int d = 0; d < n_days; ++d) {
     const int t = first_step + d;

@@ -56,40 +56,47 @@ struct RunArgs {
   unsigned* barrier;              // zeroed arrival counter
 };
 
-// Grid barrier between days, split: arrive, then the block's record flush
-// and tomorrow's keys while the other blocks finish, then wait.  One arrival
-// per block (acq_rel atomic on one counter) after a bar.sync, so every store
-// of the block's day precedes it; thread 0 polls with acquire loads and the
-// closing bar.sync extends the order to the block.  One block per SM keeps
-// the arrivals at 148 (1.2 us per barrier, tools/micro/grid_barrier.cu;
+// Grid barrier between days: one arrival per block (acq_rel atomic on one
+// counter) after a bar.sync, so every store of the block's day precedes it;
+// thread 0 polls with acquire loads and the closing bar.sync extends the
+// order to the block.  Nothing else sits between arrive and wait: the day's
+// keys are computed for every day up front and the record is flushed the next
+// day, so the last block to arrive releases the grid at once.  One block per
+// SM keeps the arrivals at 148 (1.2 us per barrier, tools/micro/grid_barrier.cu;
 // cg::grid.sync with 6 blocks per SM: 1.9 us).
-__device__ __forceinline__ void barrier_arrive(unsigned* bar) {
-  unsigned v;
-  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(v) : "l"(bar) : "memory");
-}
-__device__ __forceinline__ void barrier_wait(const unsigned* bar, unsigned target) {
-  unsigned v;
-  do {
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
-  } while (v < target);
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned v;
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(v) : "l"(bar) : "memory");
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+    } while (v < target);
+  }
+  __syncthreads();
 }
 
-// sums of the day's rows into the day's record, rows zeroed for tomorrow
-// (after a bar.sync; the next adds come after the closing bar.sync)
-__device__ __forceinline__ void rec_flush_rows(RecAcc& s, long long* rec, int step) {
-  if (blockIdx.x == 0 && threadIdx.x == 0) rec[EPI_REC_STEP] = step;
+// The record rows of a finished day (all warps past a bar.sync) into the
+// day's record, spread over the warps: warp w reduces columns w, w + nw, ...
+// over the rows and zeroes them (their next adds come two days later).
+__device__ __forceinline__ void rec_flush_spread(RecAcc& s, long long* rec, int step, int warp, int lane) {
   const int nw = (blockDim.x + 31) >> 5;
-  for (int i = threadIdx.x; i < EPI_REC_LEN; i += blockDim.x) {
-    unsigned long long t = 0;
-    if (i == EPI_REC_FLAGS) {
-      for (int w = 0; w < nw; ++w) { t |= s.v[w][i]; s.v[w][i] = 0u; }
-      if (t) atomicOr((unsigned long long*)&rec[i], t);
+  if (blockIdx.x == 0 && threadIdx.x == 0) rec[EPI_REC_STEP] = step;
+  for (int c = warp; c < EPI_REC_LEN; c += nw) {
+    const unsigned v = lane < nw ? s.v[lane][c] : 0u;
+    if (lane < nw) s.v[lane][c] = 0u;
+    if (c == EPI_REC_FLAGS) {
+      const unsigned o = __reduce_or_sync(0xFFFFFFFFu, v);
+      if (lane == 0 && o) atomicOr((unsigned long long*)&rec[c], (unsigned long long)o);
     } else {
-      for (int w = 0; w < nw; ++w) { t += s.v[w][i]; s.v[w][i] = 0u; }
-      if (t) atomicAdd((unsigned long long*)&rec[i], t);
+      const unsigned t = __reduce_add_sync(0xFFFFFFFFu, v);
+      if (lane == 0 && t) atomicAdd((unsigned long long*)&rec[c], (unsigned long long)t);
     }
   }
 }
+
+constexpr int RUN_MAX_DAYS = 360;          // day keys of a launch in shared memory
+inline size_t run_smem_bytes(int days) { return (size_t)days * sizeof(DayKeys); }
 
 // one block per SM, up to 768 threads (one agent each)
 constexpr int RUN_MAX_THREADS = 704;
@@ -100,15 +107,18 @@ template <class T> __device__ __forceinline__ T LDM(const T* p) { return *p; }
 __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_fused_run(RunArgs R, epi_net net) {
   constexpr int HH = 8, DR = 8;
   __shared__ MsgTables T;
-  __shared__ RecAcc racc;
-  __shared__ DayKeys dk[2];
+  __shared__ RecAcc racc[2];               // record rows by day parity
   __shared__ int excl_s[RUN_MAX_THREADS / 32][32];
   __shared__ uint16_t cn_s[RUN_MAX_THREADS / 32][32];
   __shared__ uint8_t own_s[RUN_MAX_THREADS / 32][32 * RT_SLOTS];
+  extern __shared__ DayKeys dk[];          // [n_days]
   load_msg_tables(T, R.mt);
-  rec_init(racc);
+  rec_init(racc[0]);
+  rec_init(racc[1]);
   const int warp = threadIdx.x >> 5, lane = lane_id();
-  if (warp == 0) day_keys(dk[0], R.seed, R.first_step, lane);
+  // every day's key prefixes up front: (day, lane) tasks over the block
+  for (int i = threadIdx.x; i < R.n_days * 32; i += blockDim.x)
+    day_keys(dk[i >> 5], R.seed, R.first_step + (i >> 5), i & 31);
   const int64_t n = net.n_agents;
   // equal contiguous agent ranges per block (one block per SM)
   const int64_t per = (n + gridDim.x - 1) / gridDim.x;
@@ -143,7 +153,10 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_fused_run(RunArgs R, epi
   for (int d = 0; d < R.n_days; ++d) {
     const int t = R.first_step + d;
     const int par = t & 1;
-    const DayKeys& D = dk[d & 1];
+    const DayKeys& D = dk[d];
+    RecAcc& rc = racc[d & 1];
+    // yesterday's record rows (complete since the barrier)
+    if (d > 0) rec_flush_spread(racc[(d - 1) & 1], R.records + (size_t)(d - 1) * EPI_REC_LEN, t - 1, warp, lane);
     const uint16_t* codes = R.codes[par];
     uint16_t* codes_next = R.codes[par ^ 1];
     const WorkTables& W = R.wt[par];
@@ -232,9 +245,9 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_fused_run(RunArgs R, epi
     }
     unsigned ev = 0;
     if (valid) ev = transmit_progress_core(R.P, R.st, D.K, nullptr, t, R.tau_lut, b, lam, -1, h);
-    rec_events(racc, ev);
-    rec_add(racc, EPI_REC_EDGES, edges);
-    rec_agent(racc, valid, valid ? h.stage : 0, valid ? h.infected_at : 0);
+    rec_events(rc, ev);
+    rec_add(rc, EPI_REC_EDGES, edges);
+    rec_agent(rc, valid, valid ? h.stage : 0, valid ? h.infected_at : 0);
     // tomorrow's code
     uint16_t cn = 0;
     if (valid) {
@@ -281,16 +294,11 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_fused_run(RunArgs R, epi
       }
     }
     cb = cn;
-    __syncthreads();                       // the block's day is complete
-    const bool more = d + 1 < R.n_days;
-    if (more && threadIdx.x == 0) barrier_arrive(R.barrier);
-    if (warp == 0) {
-      rec_flush_rows(racc, R.records + (size_t)d * EPI_REC_LEN, t);
-      if (more) day_keys(dk[(d + 1) & 1], R.seed, t + 1, lane);
-      if (more && lane == 0) barrier_wait(R.barrier, (unsigned)(d + 1) * gridDim.x);
-    }
-    __syncthreads();
+    if (d + 1 < R.n_days) grid_barrier(R.barrier, (unsigned)(d + 1) * gridDim.x);
   }
+  __syncthreads();
+  rec_flush_spread(racc[(R.n_days - 1) & 1], R.records + (size_t)(R.n_days - 1) * EPI_REC_LEN,
+                   R.first_step + R.n_days - 1, warp, lane);
   // the merged chain resumes at first + n_days: its kernel reads the
   // random-slot keys of the day after from the ring
   if (blockIdx.x == 0 && threadIdx.x < RT_SLOTS && R.ring_t2 != nullptr)
