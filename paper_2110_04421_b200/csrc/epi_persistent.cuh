@@ -77,22 +77,20 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned target) {
 }
 
 // The record rows of a finished day (all warps past a bar.sync) into the
-// day's record, spread over the warps: warp w reduces columns w, w + nw, ...
-// over the rows and zeroes them (their next adds come two days later).
-__device__ __forceinline__ void rec_flush_spread(RecAcc& s, long long* rec, int step, int warp, int lane) {
-  const int nw = (blockDim.x + 31) >> 5;
-  if (blockIdx.x == 0 && threadIdx.x == 0) rec[EPI_REC_STEP] = step;
-  for (int c = warp; c < EPI_REC_LEN; c += nw) {
-    const unsigned v = lane < nw ? s.v[lane][c] : 0u;
-    if (lane < nw) s.v[lane][c] = 0u;
-    if (c == EPI_REC_FLAGS) {
-      const unsigned o = __reduce_or_sync(0xFFFFFFFFu, v);
-      if (lane == 0 && o) atomicOr((unsigned long long*)&rec[c], (unsigned long long)o);
-    } else {
-      const unsigned t = __reduce_add_sync(0xFFFFFFFFu, v);
-      if (lane == 0 && t) atomicAdd((unsigned long long*)&rec[c], (unsigned long long)t);
-    }
+// day's record, by one warp: lane c sums column c over the warps' rows and
+// zeroes them (their next adds come two days later).
+__device__ __forceinline__ void rec_flush_warp(RecAcc& s, long long* rec, int step, int nw, int lane) {
+  if (blockIdx.x == 0 && lane == 0) rec[EPI_REC_STEP] = step;
+  if (lane >= EPI_REC_LEN || lane == EPI_REC_STEP) return;
+  unsigned long long t = 0;
+  for (int w = 0; w < nw; ++w) {
+    const unsigned v = s.v[w][lane];
+    s.v[w][lane] = 0u;
+    t = lane == EPI_REC_FLAGS ? (t | v) : (t + v);
   }
+  if (!t) return;
+  if (lane == EPI_REC_FLAGS) atomicOr((unsigned long long*)&rec[lane], t);
+  else atomicAdd((unsigned long long*)&rec[lane], t);
 }
 
 constexpr int RUN_MAX_DAYS = 360;          // day keys of a launch in shared memory
@@ -116,6 +114,7 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_fused_run(RunArgs R, epi
   rec_init(racc[0]);
   rec_init(racc[1]);
   const int warp = threadIdx.x >> 5, lane = lane_id();
+  const int nwarps = (blockDim.x + 31) >> 5;
   // every day's key prefixes up front: (day, lane) tasks over the block
   for (int i = threadIdx.x; i < R.n_days * 32; i += blockDim.x)
     day_keys(dk[i >> 5], R.seed, R.first_step + (i >> 5), i & 31);
@@ -155,8 +154,10 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_fused_run(RunArgs R, epi
     const int par = t & 1;
     const DayKeys& D = dk[d];
     RecAcc& rc = racc[d & 1];
-    // yesterday's record rows (complete since the barrier)
-    if (d > 0) rec_flush_spread(racc[(d - 1) & 1], R.records + (size_t)(d - 1) * EPI_REC_LEN, t - 1, warp, lane);
+    // yesterday's record rows (complete since the barrier), by the block's
+    // last warp (the one with the fewest agents)
+    if (d > 0 && warp == nwarps - 1)
+      rec_flush_warp(racc[(d - 1) & 1], R.records + (size_t)(d - 1) * EPI_REC_LEN, t - 1, nwarps, lane);
     const uint16_t* codes = R.codes[par];
     uint16_t* codes_next = R.codes[par ^ 1];
     const WorkTables& W = R.wt[par];
@@ -297,8 +298,9 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_fused_run(RunArgs R, epi
     if (d + 1 < R.n_days) grid_barrier(R.barrier, (unsigned)(d + 1) * gridDim.x);
   }
   __syncthreads();
-  rec_flush_spread(racc[(R.n_days - 1) & 1], R.records + (size_t)(R.n_days - 1) * EPI_REC_LEN,
-                   R.first_step + R.n_days - 1, warp, lane);
+  if (warp == nwarps - 1)
+    rec_flush_warp(racc[(R.n_days - 1) & 1], R.records + (size_t)(R.n_days - 1) * EPI_REC_LEN,
+                   R.first_step + R.n_days - 1, nwarps, lane);
   // the merged chain resumes at first + n_days: its kernel reads the
   // random-slot keys of the day after from the ring
   if (blockIdx.x == 0 && threadIdx.x < RT_SLOTS && R.ring_t2 != nullptr)
