@@ -1178,13 +1178,10 @@ static bool persistent_ok(epi_ctx* c, int32_t mode, int32_t precision) {
       !push_fits(c) || c->net.colleague_draws > 8)
     return false;
   static int per_sm = -1;
-  if (per_sm < 0) {
-    const size_t dyn = run_smem_bytes(RUN_MAX_DAYS);
-    if (cudaFuncSetAttribute(k_fused_run, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn) != cudaSuccess ||
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fused_run, RUN_MAX_THREADS, dyn) != cudaSuccess)
-      per_sm = 0;
-  }
-  return per_sm >= 1 && run_threads(c->n) <= RUN_MAX_THREADS;
+  if (per_sm < 0 &&
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fused_run, RUN_MAX_THREADS, 0) != cudaSuccess)
+    per_sm = 0;
+  return per_sm >= 1 && run_threads(c->n) <= RUN_MAX_AGENTS;
 }
 
 static int launch_run(epi_ctx* c, const epi_state* st, int32_t first, int32_t n_days, uint64_t seed,
@@ -1209,8 +1206,7 @@ static int launch_run(epi_ctx* c, const epi_state* st, int32_t first, int32_t n_
   R.barrier = c->run_barrier;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)sm_count());
-  cfg.blockDim = dim3((unsigned)run_threads(c->n));
-  cfg.dynamicSmemBytes = run_smem_bytes(n_days);
+  cfg.blockDim = dim3((unsigned)run_threads(c->n) + 32);     // + the service warp
   cfg.stream = s;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeCooperative;     // every block resident: the grid barrier is safe
@@ -1283,7 +1279,7 @@ int epi_sim_run(epi_ctx* c, const epi_state* st, int32_t first_step, int32_t n_d
       if (rc) return rc;
       d0 = 1;
     }
-    // launches of <= RUN_MAX_DAYS days (their keys live in shared memory)
+    // launches of <= RUN_MAX_DAYS days
     for (int d = d0; d < n_days; d += RUN_MAX_DAYS) {
       const int nd = n_days - d < RUN_MAX_DAYS ? n_days - d : RUN_MAX_DAYS;
       if (nd == 1) {

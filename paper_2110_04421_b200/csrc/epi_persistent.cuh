@@ -59,9 +59,10 @@ struct RunArgs {
 // Grid barrier between days: one arrival per block (acq_rel atomic on one
 // counter) after a bar.sync, so every store of the block's day precedes it;
 // thread 0 polls with acquire loads and the closing bar.sync extends the
-// order to the block.  Nothing else sits between arrive and wait: the day's
-// keys are computed for every day up front and the record is flushed the next
-// day, so the last block to arrive releases the grid at once.  One block per
+// order to the block.  Nothing else sits between arrive and wait: the
+// service warp computes the next day's keys and flushes the previous day's
+// record while the agent warps work, so the last block to arrive releases the
+// grid at once.  One block per
 // SM keeps the arrivals at 148 (1.2 us per barrier, tools/micro/grid_barrier.cu;
 // cg::grid.sync with 6 blocks per SM: 1.9 us).
 __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned target) {
@@ -93,11 +94,13 @@ __device__ __forceinline__ void rec_flush_warp(RecAcc& s, long long* rec, int st
   else atomicAdd((unsigned long long*)&rec[lane], t);
 }
 
-constexpr int RUN_MAX_DAYS = 360;          // day keys of a launch in shared memory
-inline size_t run_smem_bytes(int days) { return (size_t)days * sizeof(DayKeys); }
+constexpr int RUN_MAX_DAYS = 1 << 20;      // days per launch (no per-day state)
 
-// one block per SM, up to 768 threads (one agent each)
-constexpr int RUN_MAX_THREADS = 704;
+// one block per SM: up to 704 agent threads (one agent each) + one service
+// warp that flushes yesterday's record and computes tomorrow's keys while
+// the agent warps work
+constexpr int RUN_MAX_AGENTS = 704;
+constexpr int RUN_MAX_THREADS = RUN_MAX_AGENTS + 32;
 // loads of data written during the run: plain (coherent) global loads; the
 // grid barrier orders them after the writers' stores
 template <class T> __device__ __forceinline__ T LDM(const T* p) { return *p; }
@@ -109,22 +112,21 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_fused_run(RunArgs R, epi
   __shared__ int excl_s[RUN_MAX_THREADS / 32][32];
   __shared__ uint16_t cn_s[RUN_MAX_THREADS / 32][32];
   __shared__ uint8_t own_s[RUN_MAX_THREADS / 32][32 * RT_SLOTS];
-  extern __shared__ DayKeys dk[];          // [n_days]
+  __shared__ DayKeys dk[2];                // keys by day parity
   load_msg_tables(T, R.mt);
   rec_init(racc[0]);
   rec_init(racc[1]);
   const int warp = threadIdx.x >> 5, lane = lane_id();
-  const int nwarps = (blockDim.x + 31) >> 5;
-  // every day's key prefixes up front: (day, lane) tasks over the block
-  for (int i = threadIdx.x; i < R.n_days * 32; i += blockDim.x)
-    day_keys(dk[i >> 5], R.seed, R.first_step + (i >> 5), i & 31);
+  const int nwa = (int)(blockDim.x >> 5) - 1;     // agent warps; warp nwa is the service warp
+  const bool service = warp == nwa;
+  if (warp == 0) day_keys(dk[0], R.seed, R.first_step, lane);
   const int64_t n = net.n_agents;
   // equal contiguous agent ranges per block (one block per SM)
   const int64_t per = (n + gridDim.x - 1) / gridDim.x;
   const int64_t blo = blockIdx.x * per;
   const int64_t bhi = blo + per < n ? blo + per : n;
   const int64_t b = blo + threadIdx.x;
-  const bool valid = b < bhi;
+  const bool valid = !service && b < bhi;
   const uint32_t self = (uint32_t)b;
   const int draws = net.colleague_draws;
   // static network data and the agent's state, once
@@ -152,12 +154,13 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_fused_run(RunArgs R, epi
   for (int d = 0; d < R.n_days; ++d) {
     const int t = R.first_step + d;
     const int par = t & 1;
-    const DayKeys& D = dk[d];
+    const DayKeys& D = dk[d & 1];
     RecAcc& rc = racc[d & 1];
-    // yesterday's record rows (complete since the barrier), by the block's
-    // last warp (the one with the fewest agents)
-    if (d > 0 && warp == nwarps - 1)
-      rec_flush_warp(racc[(d - 1) & 1], R.records + (size_t)(d - 1) * EPI_REC_LEN, t - 1, nwarps, lane);
+    if (service) {
+      // yesterday's record rows (complete since the barrier); tomorrow's keys
+      if (d > 0) rec_flush_warp(racc[(d - 1) & 1], R.records + (size_t)(d - 1) * EPI_REC_LEN, t - 1, nwa, lane);
+      if (d + 1 < R.n_days) day_keys(dk[(d + 1) & 1], R.seed, t + 1, lane);
+    } else {
     const uint16_t* codes = R.codes[par];
     uint16_t* codes_next = R.codes[par ^ 1];
     const WorkTables& W = R.wt[par];
@@ -295,12 +298,13 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_fused_run(RunArgs R, epi
       }
     }
     cb = cn;
+    }
     if (d + 1 < R.n_days) grid_barrier(R.barrier, (unsigned)(d + 1) * gridDim.x);
   }
   __syncthreads();
-  if (warp == nwarps - 1)
+  if (service)
     rec_flush_warp(racc[(R.n_days - 1) & 1], R.records + (size_t)(R.n_days - 1) * EPI_REC_LEN,
-                   R.first_step + R.n_days - 1, nwarps, lane);
+                   R.first_step + R.n_days - 1, nwa, lane);
   // the merged chain resumes at first + n_days: its kernel reads the
   // random-slot keys of the day after from the ring
   if (blockIdx.x == 0 && threadIdx.x < RT_SLOTS && R.ring_t2 != nullptr)
