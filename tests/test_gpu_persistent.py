@@ -38,6 +38,7 @@ def _same(a, b):
 @pytest.mark.parametrize("cfg,n,seeds", [(1, 100_000, 100), (0, 10_000, 10), (1, 6007, 300), (1, 129, 20)])
 def test_persistent_run_equals_per_day(cfg, n, seeds):
     a, b = _pair(cfg, n, seeds, 21, 180)
+    assert a.uses_persistent_run() and not b.uses_persistent_run()
     a.run()
     b.run()
     r = a.rec.cpu().numpy()
@@ -47,6 +48,7 @@ def test_persistent_run_equals_per_day(cfg, n, seeds):
 
 def test_persistent_split_runs_and_steps():
     a, b = _pair(1, 20_011, 200, 5, 120)
+    assert a.uses_persistent_run()
     for chunk in (1, 37, 2, 0, 50):
         a.run(chunk)
         b.run(chunk)
@@ -58,6 +60,7 @@ def test_persistent_split_runs_and_steps():
 
 def test_persistent_graph_replay_equals_run():
     a, b = _pair(1, 30_000, 60, 9, 90)
+    assert a.uses_persistent_run()
     a.capture()
     a.replay()
     a.replay()                                    # reset inside the graph: same result twice
@@ -115,3 +118,15 @@ def test_fused_intervention_day_graph_replay():
     a.capture(); a.replay(); a.replay()
     b.run()
     assert np.array_equal(a.rec.cpu().numpy(), b.rec.cpu().numpy())
+
+
+def test_persistent_only_where_one_wave_fits():
+    """Above 148 x 704 agents (one agent per thread, one block per SM) the
+    run falls back to one kernel per day."""
+    spec = ConfigNetworkSpec.config(1, n_agents=150_000, initial_infections=50)
+    pop = synthesize(spec, 5)
+    sim = ConfigSimulation(pop, default_disease(), default_progression(), InterventionConfig(), 1,
+                           mode="fused", horizon=5)
+    assert not sim.uses_persistent_run()
+    sim.run()
+    assert sim.records()[:, 19].sum() > 0
