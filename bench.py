@@ -49,6 +49,9 @@ def parse():
     ap.add_argument("--dose-gap", type=int, default=21, help="config2: second-dose delay (21 or 84)")
     ap.add_argument("--replicas", type=int, default=128, help="config4: replicas per GPU")
     ap.add_argument("--streams", type=int, default=8, help="config4: concurrent streams")
+    ap.add_argument("--replica-mode", default="persistent", choices=["concurrent", "persistent"],
+                    help="config4: one persistent run per replica, one after another on one "
+                         "stream (default), or per-day kernels of replicas on concurrent streams")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-message-pass", action="store_true",
@@ -637,7 +640,10 @@ def run_config3(a):
 
 def run_config4(a):
     """Ensemble: R replicas per GPU of config 1, own seeds and rate scales,
-    CUDA graphs replayed on concurrent streams; no inter-GPU communication."""
+    one CUDA graph per replica; no inter-GPU communication.  Default: each
+    replica one persistent run (k_fused_run holds the whole GPU), replicas one
+    after another on one stream; --replica-mode concurrent: per-day kernels on
+    one block per SM, replicas on --streams concurrent streams."""
     import torch
     from paper_2110_04421_b200 import _native as N
     from paper_2110_04421_b200 import keyed
@@ -659,13 +665,14 @@ def run_config4(a):
         r = rank * a.replicas + i
         u = keyed.uniform(0, 0, keyed.Purpose.REPLICATION, r, k=1)
         d = d0.with_rate(d0.rate_scale * (0.5 + u))
-        # concurrent replicas on 8 streams: per-day kernels on one block per
-        # SM each (a persistent run needs the whole GPU resident for its grid
-        # barrier; measured: 1 block/SM 63.8 k replica-steps/s, 16: 59.4 k,
-        # persistent replicas one after another: 61.1 k)
+        # measured (replica-steps/s): persistent one after another 66.1 k;
+        # concurrent on 8 streams with one block per SM 63.0 k (16 blocks
+        # per SM: 59.4 k)
         sims.append(ConfigSimulation(pop, d, t, iv, keyed.replication_seed(0, r), mode="fused",
-                                     horizon=HORIZON, persistent=False, day_blocks_per_sm=1))
-    streams = [torch.cuda.Stream() for _ in range(a.streams)]
+                                     horizon=HORIZON, persistent=a.replica_mode == "persistent",
+                                     day_blocks_per_sm=1))
+    n_streams = 1 if a.replica_mode == "persistent" else a.streams   # cooperative runs serialise anyway
+    streams = [torch.cuda.Stream() for _ in range(n_streams)]
     for s in sims:
         s.capture()
     torch.cuda.synchronize()
@@ -702,6 +709,10 @@ def run_config4(a):
         dist.all_gather(allc, new_inf)
         new_inf = torch.cat(allc)
     reps = a.replicas * world
+    # replication quartiles of the daily infection curve on the device
+    # (row f3 output: epi_quartiles, bitwise the reference's summarize)
+    from paper_2110_04421_b200.series import summarize_device
+    quart = summarize_device(recs, ["new_infections"])["new_infections"] if world == 1 else None
     if rank == 0:
         mean = new_inf.mean(0).cpu().numpy()
         std = new_inf.std(0).cpu().numpy()
@@ -712,13 +723,15 @@ def run_config4(a):
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": f"config4 (BASELINE.json configs[4]): {reps} replicas of config 1 "
                        "(shared static population, own seed, rate 3.3x[0.5,1.5]); one step = all "
-                       "replicas x 180 days", "parallelism": f"{a.replicas} replicas/GPU on "
-                       f"{a.streams} streams x {world} GPUs",
+                       "replicas x 180 days", "parallelism": f"{a.replicas} replicas/GPU ({a.replica_mode}) on "
+                       f"{n_streams} stream(s) x {world} GPUs",
                        "l2": "not flushed: the replicas' states and push tables (~20 MB each) "
                        "exceed the 126 MB L2 many times over"},
             "replica_steps_per_s": reps * HORIZON * a.steps / (ms / 1e3),
             "daily_new_infections_mean": [round(float(x), 2) for x in mean],
             "daily_new_infections_std": [round(float(x), 2) for x in std],
+            "daily_new_infections_quartiles": (None if quart is None else
+                                               [[round(float(v), 2) for v in row] for row in quart]),
             "clocks": clocks}), flush=True)
 
 
