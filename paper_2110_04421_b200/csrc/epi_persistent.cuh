@@ -1,15 +1,17 @@
 // Persistent fused run: every day of a config-network simulation in ONE
 // launch (epi_sim_run, merged fused mode: no interventions, whole population,
-// push tables).  One thread per agent for the whole run and a grid barrier
-// between days, so what the per-day kernel (k_fused_step) reloads every day
-// stays in registers:
+// push tables).  One block per SM, one thread per agent for the whole run and
+// a grid barrier between days, so what the per-day kernel (k_fused_step)
+// reloads every day stays in registers:
 //   - the agent's static network data (household range, workplace id, slot,
 //     size, base) and its state (AgentHot), written through on change only;
 //   - its own code and its workplace position of the day (computed by itself
 //     in the previous day's epilogue), which removes the two deepest levels
 //     of the per-day load chain (wp_id -> wp_size/base -> pos_of -> wcode);
-//   - the message tables; the day's key prefixes are computed on the device
-//     into shared memory while the block waits at the barrier.
+//   - the message tables.
+// A service warp per block computes the next day's key prefixes and flushes
+// the previous day's record while the agent warps work, so nothing sits
+// between the barrier's arrive and wait.
 // Arithmetic, visit order and sums are those of k_fused_step with
 // push_kind_sums, so results are bitwise identical to the per-day path
 // (tests/test_gpu_persistent.py).
@@ -59,12 +61,10 @@ struct RunArgs {
 // Grid barrier between days: one arrival per block (acq_rel atomic on one
 // counter) after a bar.sync, so every store of the block's day precedes it;
 // thread 0 polls with acquire loads and the closing bar.sync extends the
-// order to the block.  Nothing else sits between arrive and wait: the
-// service warp computes the next day's keys and flushes the previous day's
-// record while the agent warps work, so the last block to arrive releases the
-// grid at once.  One block per
-// SM keeps the arrivals at 148 (1.2 us per barrier, tools/micro/grid_barrier.cu;
-// cg::grid.sync with 6 blocks per SM: 1.9 us).
+// order to the block.  The last block to arrive releases the grid at once
+// (measured 1.3 us from its arrival).  One block per SM keeps the arrivals at
+// 148 (1.2 us per barrier, tools/micro/grid_barrier.cu; cg::grid.sync with 6
+// blocks per SM: 1.9 us).
 __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned target) {
   __syncthreads();
   if (threadIdx.x == 0) {
