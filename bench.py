@@ -515,23 +515,32 @@ def persistent_profile(sim):
     torch.cuda.synchronize()
     day0, run = ev[0].elapsed_time(ev[1]), ev[1].elapsed_time(ev[2])
     n, days = sim.n, sim.horizon - 1
+    iv = sim.iv
+    has_iv = iv.testing_enabled or iv.quarantine_enabled or iv.den_enabled or iv.vaccination_enabled
     # per agent-day, state in registers: own code write 2 + push rows read
-    # (rin 32 + rout 64) + rin clear 32 + next-day scatter ~16 = 146 B
-    b_day = 146 * n
+    # (rin 32 + rout 64) + rin clear 32 + next-day scatter ~16 = 146 B; on
+    # intervention days + the agent's state reloaded (16) and the
+    # intervention columns read and written (testing, DEN, dropout, doses,
+    # buckets: ~44) = 206 B
+    b_day = (206 if has_iv else 146) * n
     b_day0 = (16 + 2 + 32 + 64 + 32 + 16) * n + (32 + 10 + 1) * n      # + day-0 tables
     total = day0 + run
-    kernels = {"day0_tables+k_fused_step": {"ms_per_launch": day0, "share": day0 / total},
-               "k_fused_run": {"ms_per_launch": run, "share": run / total, "days_per_launch": days,
-                               "us_per_day": run * 1e3 / days,
-                               "alg_GBps": b_day * days / (run / 1e3) / 1e9}}
+    name = "k_iv_run" if has_iv else "k_fused_run"
+    d0name = "day0_tables+k_fused_step" + ("+intervention kernels" if has_iv else "")
+    kernels = {d0name: {"ms_per_launch": day0, "share": day0 / total},
+               name: {"ms_per_launch": run, "share": run / total, "days_per_launch": days,
+                      "us_per_day": run * 1e3 / days, "alg_GBps": b_day * days / (run / 1e3) / 1e9}}
     achieved = b_day * days / (run / 1e3) / 1e9
-    # ours per simulation: k_codes (reset), k_day_keys + k_day_tables + k_fused_step (day 0), k_fused_run
-    return {"kernels": kernels, "launches_per_sim": 5,
-            "path": "day 0: day tables + k_fused_step; days 1-179: one persistent k_fused_run launch",
+    # ours per simulation: k_codes (reset), k_day_keys + k_day_tables + k_fused_step (day 0), the run;
+    # intervention day 0 also k_died_update, k_iv_post_chunks, k_finish_iv
+    launches = 5 + (3 if has_iv else 0)
+    return {"kernels": kernels, "launches_per_sim": launches,
+            "path": f"day 0: day tables + k_fused_step{' + intervention kernels' if has_iv else ''}; "
+                    f"days 1-179: one persistent {name} launch",
             "alg_bytes_per_sim": float(b_day * days + b_day0),
-            "roofline": {"bound": "hbm", "kernel": "k_fused_run", "achieved": achieved, "unit": "GB/s",
+            "roofline": {"bound": "hbm", "kernel": name, "achieved": achieved, "unit": "GB/s",
                          "traffic": None, "days_per_launch": days,
-                         "bytes_model": "146 B per agent-day (DESIGN.md §4), x 179 days per launch"}}
+                         "bytes_model": f"{b_day // n} B per agent-day (DESIGN.md §4), x 179 days per launch"}}
 
 
 def end_to_end(sim, a):

@@ -17,6 +17,7 @@
 #include "epi_kernels.cuh"
 #include "epi_msgpass.cuh"
 #include "epi_persistent.cuh"
+#include "epi_persistent_iv.cuh"
 #include "epi_population.cuh"
 #include "epi_refnet.cuh"
 #include "epi_series.cuh"
@@ -178,6 +179,7 @@ struct epi_ctx {
   int day_blocks_per_sm = 16;        // k_fused_step grid cap (concurrent replicas: 1)
   unsigned* iv_tile_hist = nullptr;  // [chunks][NUM_BUCKETS]
   unsigned long long* iv_hist = nullptr;   // [2][NUM_BUCKETS] eligibility histogram by day parity
+  unsigned long long* ivr_hist = nullptr;  // k_iv_run: [2][NUM_BUCKETS + 1] (+ active count)
   unsigned* run_barrier = nullptr;   // arrival counter of k_fused_run's grid barrier
 };
 
@@ -416,6 +418,7 @@ int epi_destroy(epi_ctx* c) {
   cudaFree(c->run_barrier);
   cudaFree(c->iv_tile_hist);
   cudaFree(c->iv_hist);
+  cudaFree(c->ivr_hist);
   for (auto* p : c->ntab_dev) cudaFree(p);
   cudaFree(c->wt_host[0].member_at_pos);
   for (auto& w : c->wt_host) {
@@ -945,7 +948,10 @@ static int iv_fused_day(epi_ctx* c, const StepArgs& A, int32_t step, uint64_t se
   int blocks;
   iv_chunks(c->n, &chunk, &blocks);
   int rc = 0;
-  if (!c->iv_hist) rc = dalloc(&c->iv_hist, (size_t)2 * NUM_BUCKETS);
+  if (!c->iv_hist) {
+    rc = dalloc(&c->iv_hist, (size_t)2 * NUM_BUCKETS);
+    if (!rc) CK(cudaMemsetAsync(c->iv_hist, 0, (size_t)2 * NUM_BUCKETS * sizeof(unsigned long long), s));
+  }
   if (!rc && !c->iv_tile_hist) rc = dalloc(&c->iv_tile_hist, (size_t)blocks * NUM_BUCKETS);
   if (rc) return rc;
   const bool listed = p.den_enabled && p.testing_enabled && c->den_list != nullptr;
@@ -1227,9 +1233,93 @@ static int launch_run(epi_ctx* c, const epi_state* st, int32_t first, int32_t n_
   return 0;
 }
 
+// Intervention days in one persistent launch (k_iv_run): the fused
+// intervention day's conditions + one resident thread per agent.
+static bool persistent_iv_ok(epi_ctx* c, int32_t mode, int32_t precision) {
+  if (!c->persistent || !c->iv_fusion || mode != 1 || precision != EPI_F32 || !interventions_on(c->host))
+    return false;
+  if (partitioned(c) || c->net.n_agents < 2 || c->net.random_slots != RT_SLOTS || !batched(&c->net) ||
+      !push_fits(c) || c->net.colleague_draws > 8)
+    return false;
+  static int per_sm = -1;
+  if (per_sm < 0 &&
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_iv_run, RUN_MAX_THREADS, 0) != cudaSuccess)
+    per_sm = 0;
+  return per_sm >= 1 && run_threads(c->n) <= RUN_MAX_AGENTS;
+}
+
+static int launch_iv_run(epi_ctx* c, const epi_state* st, int32_t first, int32_t n_days, uint64_t seed,
+                         uint16_t* codes0, uint16_t* codes1, int64_t* records, int32_t* vax_open, cudaStream_t s) {
+  const epi_params& p = c->host;
+  if (p.vaccination_enabled && !vax_open) return fail(EPI_EARG, "vaccination enabled but no vax_open latch given");
+  int rc = 0;
+  if (!c->ivr_hist) rc = dalloc(&c->ivr_hist, (size_t)2 * IV_HIST);
+  if (!rc && !c->iv_tile_hist) {
+    int64_t chunk;
+    int blocks;
+    iv_chunks(c->n, &chunk, &blocks);
+    rc = dalloc(&c->iv_tile_hist, (size_t)(blocks > sm_count() ? blocks : sm_count()) * NUM_BUCKETS);
+  }
+  if (rc) return rc;
+  if (!c->run_barrier) CK(cudaMalloc((void**)&c->run_barrier, sizeof(unsigned)));
+  CK(cudaMemsetAsync(c->run_barrier, 0, sizeof(unsigned), s));
+  CK(cudaMemsetAsync(c->ivr_hist, 0, (size_t)2 * IV_HIST * sizeof(unsigned long long), s));
+  IvRunArgs R{};
+  R.A0 = make_args(c, st, first, seed, nullptr, nullptr, true);
+  R.seed = seed;
+  R.first_step = first;
+  R.n_days = n_days;
+  R.records = (long long*)records;
+  R.codes[0] = codes0;
+  R.codes[1] = codes1;
+  R.wt[0] = c->wt_host[0];
+  R.wt[1] = c->wt_host[1];
+  R.ring_t2 = c->ntab_dev[(first + n_days + 1) % 3];
+  R.mt = (const MsgTables*)c->msg_dev;
+  R.wrad = (const Radix*)c->ntab_dev[0]->wrad;
+  R.dn = c->ntab.dn;
+  R.barrier = c->run_barrier;
+  R.bucket = c->bucket;
+  R.hist = c->ivr_hist;
+  R.tile_hist = c->iv_tile_hist;
+  R.vax_open = vax_open;
+  const bool listed = p.den_enabled && p.testing_enabled && c->den_list != nullptr;
+  R.den_list = listed ? c->den_list : nullptr;
+  R.den_count = listed ? c->den_count : nullptr;
+  R.died_at = p.den_enabled ? c->died_at : nullptr;
+  R.den_lookback = p.den_lookback;
+  R.den = listed ? 1 : 0;
+  R.tests = p.testing_enabled ? 1 : 0;
+  R.post = (p.den_enabled || p.quarantine_enabled || p.vaccination_enabled) ? 1 : 0;
+  R.vax = p.vaccination_enabled ? 1 : 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)sm_count());
+  cfg.blockDim = dim3((unsigned)run_threads(c->n) + 32);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.numAttrs = 1;
+  if (c->hot.bytes > 0) {
+    attr[1].id = cudaLaunchAttributeAccessPolicyWindow;
+    attr[1].val.accessPolicyWindow.base_ptr = const_cast<void*>(c->hot.base);
+    attr[1].val.accessPolicyWindow.num_bytes = c->hot.bytes;
+    attr[1].val.accessPolicyWindow.hitRatio = c->hot.hit_ratio;
+    attr[1].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    attr[1].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    cfg.numAttrs = 2;
+  }
+  cfg.attrs = attr;
+  CK(cudaLaunchKernelEx(&cfg, k_iv_run, R, c->net));
+  c->merged_ready = first + n_days;
+  // the per-day path resumes with an empty histogram (k_iv_run used its own)
+  if (c->iv_hist) CK(cudaMemsetAsync(c->iv_hist, 0, (size_t)2 * NUM_BUCKETS * sizeof(unsigned long long), s));
+  return 0;
+}
+
 int epi_run_persistent(epi_ctx* c, int32_t mode, int32_t precision) {
   if (!c) return fail(EPI_EARG, "null ctx");
-  return c->has_net && persistent_ok(c, mode, precision) ? 1 : 0;
+  return c->has_net && (persistent_ok(c, mode, precision) || persistent_iv_ok(c, mode, precision)) ? 1 : 0;
 }
 
 int epi_quartiles(const int64_t* data, int64_t n_rep, int32_t horizon, int32_t rec_len, const int32_t* cols,
@@ -1268,6 +1358,26 @@ int epi_sim_run(epi_ctx* c, const epi_state* st, int32_t first_step, int32_t n_d
                 int32_t* vax_open, void* stream) {
   if (!c || !records || !codes0 || !codes1 || n_days < 0) return fail(EPI_EARG, "bad argument");
   CK(cudaMemsetAsync(records, 0, (size_t)n_days * EPI_REC_LEN * sizeof(int64_t), S(stream)));
+  const bool iv_run = n_days >= 2 && c->has_net && st && st->n_agents == c->n && persistent_iv_ok(c, mode, precision);
+  if (iv_run) {
+    // day 0 of the chain on the per-day path (tables, death days, counters);
+    // every later day in one launch
+    int d0 = 0;
+    if (c->merged_ready != first_step) {
+      const int t = first_step;
+      int rc = sim_step_impl(c, st, t, seed, mode, precision, (t & 1) ? codes1 : codes0, (t & 1) ? codes0 : codes1,
+                             records, vax_open, nullptr, stream, false);
+      if (rc) return rc;
+      d0 = 1;
+    }
+    if (n_days - d0 >= 1) {
+      // the per-day path's notifier list / histogram state is not carried over
+      if (c->den_count) CK(cudaMemsetAsync(c->den_count, 0, sizeof(int), S(stream)));
+      return launch_iv_run(c, st, first_step + d0, n_days - d0, seed, codes0, codes1,
+                           records + (size_t)d0 * EPI_REC_LEN, vax_open, S(stream));
+    }
+    return 0;
+  }
   if (n_days >= 2 && c->has_net && st && st->n_agents == c->n && persistent_ok(c, mode, precision)) {
     // the first day on the per-day path builds the day's tables (unless a
     // previous merged day already did); every later day in one launch

@@ -98,7 +98,7 @@ __device__ __forceinline__ uint32_t walk_inv(uint32_t y, const PermKeys& K, cons
 struct NetKeys {
   uint64_t rcount, rperm, wperm, wshift;
 };
-inline NetKeys make_net_keys(uint64_t g, int step) {
+__host__ __device__ inline NetKeys make_net_keys(uint64_t g, int step) {
   return NetKeys{key_prefix(g, step, P_NET_RCOUNT), key_prefix(g, step, P_NET_RPERM),
                  key_prefix(g, step, P_NET_WPERM), key_prefix(g, step, P_NET_WSHIFT)};
 }

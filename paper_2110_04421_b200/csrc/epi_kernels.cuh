@@ -1028,6 +1028,27 @@ __global__ void k_died_update(const uint16_t* __restrict__ codes, int64_t n, int
     if (code_dead(codes[c]) && died_at[c] == INT32_MAX) died_at[c] = step - 1;
 }
 
+// One (notifier, past day) item of the DEN regeneration, one warp: the
+// notifier's in-edges of that day enumerated again (who was dead that day:
+// died_at) and their sources marked notified.  `rk_w` = the warp's
+// shared-memory slot-key row.
+__device__ __forceinline__ void den_regen_item(const epi_net& net, const NetKeys& nk, int day, int64_t an,
+                                               PermKeys* rk_w, const Radix* wrad,
+                                               const int32_t* __restrict__ died_at, uint8_t* mark, int lane) {
+  if (lane < net.random_slots) rk_w[lane] = random_slot_keys(nk.rperm, lane);
+  __syncwarp();
+  auto code_of = [&](int64_t c) -> uint16_t {
+    if (died_at[c] < day) return CODE_DEAD;
+    return (uint16_t)(random_count(net, nk.rcount, c) << 8);
+  };
+  for_each_in_edge_f(net, nk, rk_w, wrad, code_of, an, code_of(an), lane, 32,
+                     [&](int64_t c, int, uint16_t) {
+                       if (!(mark[c] & FL_NOTIFIED))
+                         atomicOr((unsigned*)(mark + (c & ~3ll)), (unsigned)FL_NOTIFIED << (8 * (c & 3)));
+                     });
+  __syncwarp();
+}
+
 __global__ void __launch_bounds__(256) k_den_regen(epi_net net, DenRegen D, const int32_t* __restrict__ died_at,
                                                    const int32_t* __restrict__ notif, const int* n_notif,
                                                    uint8_t* __restrict__ mark, const Radix* __restrict__ wrad_g) {
@@ -1042,22 +1063,8 @@ __global__ void __launch_bounds__(256) k_den_regen(epi_net net, DenRegen D, cons
   // one warp per (notifier, day)
   const int64_t items = (int64_t)(*n_notif) * D.n_days;
   for (int64_t it = blockIdx.x * (int64_t)(blockDim.x >> 5) + warp; it < items; it += warps) {
-    const int64_t an = notif[it / D.n_days];
     const int d = (int)(it % D.n_days);
-    const int day = D.first_day + d;
-    const NetKeys& nk = D.nk[d];
-    if (lane < net.random_slots) rk[warp][lane] = random_slot_keys(nk.rperm, lane);
-    __syncwarp();
-    auto code_of = [&](int64_t c) -> uint16_t {
-      if (died_at[c] < day) return CODE_DEAD;
-      return (uint16_t)(random_count(net, nk.rcount, c) << 8);
-    };
-    for_each_in_edge_f(net, nk, rk[warp], wrad, code_of, an, code_of(an), lane, 32,
-                       [&](int64_t c, int, uint16_t) {
-                         if (!(mark[c] & FL_NOTIFIED))
-                           atomicOr((unsigned*)(mark + (c & ~3ll)), (unsigned)FL_NOTIFIED << (8 * (c & 3)));
-                       });
-    __syncwarp();
+    den_regen_item(net, D.nk[d], D.first_day + d, notif[it / D.n_days], rk[warp], wrad, died_at, mark, lane);
   }
 }
 

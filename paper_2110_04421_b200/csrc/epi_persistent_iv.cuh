@@ -1,0 +1,387 @@
+// Persistent intervention run: the fused intervention days of a config
+// network (epi_sim_run, fused mode, whole population, push tables) in ONE
+// launch, like k_fused_run for the days without interventions.  One block
+// per SM, one thread per agent for the whole run, a service warp; the day's
+// phases are separated by grid barriers instead of kernel boundaries:
+//   A  gather + transmission/progression + testing (k_fused_step + tests)
+//        | barrier (the notifier list is complete)            [DEN]
+//   B  DEN regeneration: one warp per (notifier, past day) (k_den_regen)
+//        | barrier (the notifications are complete)          [DEN]
+//   C  DEN follow-ups, dropout, immunity checks, eligibility buckets and the
+//      chunk histograms (k_iv_post_chunks); the active count into the day's
+//      histogram row
+//        | barrier (the day's histogram is complete)         [vaccination]
+//   D  vaccination plan per block + doses in id order, death days, record,
+//      next codes, tomorrow's push tables (k_finish_iv)
+//        | barrier (end of day)
+// The agent's static network data, own code and workplace position stay in
+// registers; its state is reloaded at the start of each day (phases B-D
+// change it through the shared per-phase functions).  The same per-agent
+// functions in the same order as the per-phase kernels: bitwise the same run
+// (tests/test_gpu_persistent.py).
+#pragma once
+
+#include "epi_persistent.cuh"
+
+namespace epi {
+
+struct IvRunArgs {
+  StepArgs A0;                    // P, st, flags, tau_lut (K and step are per day)
+  uint64_t seed;
+  int first_step, n_days;
+  long long* records;             // [n_days][EPI_REC_LEN], zeroed
+  uint16_t* codes[2];
+  WorkTables wt[2];
+  NetTables* ring_t2;
+  const MsgTables* mt;
+  const Radix* wrad;              // static workplace domains (DEN regeneration)
+  Radix dn;
+  unsigned* barrier;
+  uint8_t* bucket;
+  unsigned long long* hist;       // [2][NUM_BUCKETS + 1] by day parity (+ active count)
+  unsigned* tile_hist;            // [blocks][NUM_BUCKETS]
+  int32_t* vax_open;
+  int32_t* den_list;
+  int* den_count;
+  int32_t* died_at;
+  int den_lookback;
+  int den, tests, post, vax;      // phases present
+};
+
+constexpr int IV_HIST = NUM_BUCKETS + 1;
+
+__global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_net net) {
+  constexpr int HH = 8, DR = 8;
+  __shared__ MsgTables T;
+  __shared__ RecAcc racc[2];
+  __shared__ DayKeys dk[2];
+  __shared__ StepArgs As[2];
+  __shared__ Radix wrad[256];
+  __shared__ PermKeys rk_w[RUN_MAX_THREADS / 32][RT_SLOTS];
+  __shared__ int excl_s[RUN_MAX_THREADS / 32][32];
+  __shared__ uint16_t cn_s[RUN_MAX_THREADS / 32][32];
+  __shared__ uint8_t own_s[RUN_MAX_THREADS / 32][32 * RT_SLOTS];
+  __shared__ unsigned h_s[NUM_BUCKETS];
+  __shared__ unsigned long long hist_s[IV_HIST];
+  __shared__ int wsum_s[RUN_MAX_THREADS / 32];
+  __shared__ long long plan_s[2];
+  __shared__ int off_s;
+  load_msg_tables(T, R.mt);
+  rec_init(racc[0]);
+  rec_init(racc[1]);
+  for (int m = threadIdx.x; m < 256; m += blockDim.x) wrad[m] = R.wrad[m];
+  for (int i = threadIdx.x; i < NUM_BUCKETS; i += blockDim.x) h_s[i] = 0u;
+  const int warp = threadIdx.x >> 5, lane = lane_id();
+  const int nwa = (int)(blockDim.x >> 5) - 1;
+  const bool service = warp == nwa;
+  if (warp == 0) {
+    day_keys(dk[0], R.seed, R.first_step, lane);
+    __syncwarp();
+    if (lane == 0) {
+      As[0] = R.A0;
+      As[0].K = dk[0].K;
+      As[0].step = R.first_step;
+    }
+  }
+  const int64_t n = net.n_agents;
+  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t blo = blockIdx.x * per;
+  const int64_t bhi = blo + per < n ? blo + per : n;
+  const int64_t b = blo + threadIdx.x;
+  const bool valid = !service && b < bhi;
+  const uint32_t self = (uint32_t)b;
+  const int draws = net.colleague_draws;
+  const epi_state& st = R.A0.st;
+  int off = 0, sz = 0, w = -1, loc = 0, m = 0, base = 0;
+  uint16_t cb = CODE_DEAD;
+  uint32_t p = 0;
+  if (valid) {
+    off = net.hh_off[b];
+    sz = net.hh_size[b];
+    w = net.wp_id[b];
+    loc = net.wp_local[b];
+    cb = LDM(R.codes[R.first_step & 1] + b);
+    if (w >= 0) {
+      m = net.wp_size[w];
+      base = net.wp_base[w];
+      if (m >= 2) p = LDM(R.wt[R.first_step & 1].pos_of + base + loc);
+    }
+  }
+  const bool works = w >= 0 && m >= 2;
+  const int64_t start = b - off;
+  unsigned bar = 0;                        // barriers passed
+  __syncthreads();
+  for (int d = 0; d < R.n_days; ++d) {
+    const int t = R.first_step + d;
+    const int par = t & 1;
+    const DayKeys& D = dk[d & 1];
+    const StepArgs& A = As[d & 1];
+    RecAcc& rc = racc[d & 1];
+    const uint16_t* codes = R.codes[par];
+    uint16_t* codes_next = R.codes[par ^ 1];
+    const WorkTables& W = R.wt[par];
+    const WorkTables& Wn = R.wt[par ^ 1];
+    // ---- phase A ----------------------------------------------------------
+    if (service) {
+      if (d > 0) rec_flush_warp(racc[(d - 1) & 1], R.records + (size_t)(d - 1) * EPI_REC_LEN, t - 1, nwa, lane);
+      if (d + 1 < R.n_days) {
+        day_keys(dk[(d + 1) & 1], R.seed, t + 1, lane);
+        __syncwarp();
+        if (lane == 0) {
+          As[(d + 1) & 1] = R.A0;
+          As[(d + 1) & 1].K = dk[(d + 1) & 1].K;
+          As[(d + 1) & 1].step = t + 1;
+        }
+      }
+    } else {
+      AgentHot h{};
+      if (valid) h = load_hot(st, b);
+      unsigned edges = 0;
+      double lam = 0.0;
+      if (valid) {
+        const uint4* ri = (const uint4*)(W.rin + (size_t)b * RT_SLOTS);
+        const uint4 in0 = LDM(ri), in1 = LDM(ri + 1);
+        if (!code_dead(cb)) {
+          const uint4* ro = (const uint4*)(W.rout + (size_t)b * RT_SLOTS);
+          const int nb = code_count(cb);
+          const int nbe = nb < RT_SLOTS ? nb : RT_SLOTS;
+          const uint4 o0 = nbe > 0 ? LDM(ro) : make_uint4(self, self, self, self);
+          uint16_t hc[HH];
+#pragma unroll
+          for (int i = 0; i < HH; ++i)
+            hc[i] = (i < sz && start + i != b) ? LDM(codes + start + i) : (uint16_t)CODE_DEAD;
+          uint32_t sh[DR];
+          if (works) {
+            const uint64_t hw = fold(D.wshift, (uint64_t)w);
+#pragma unroll
+            for (int j4 = 0; j4 < DR; j4 += 4) {
+              const uint64_t hq = fold(hw, (uint64_t)(j4 >> 2));
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                sh[j4 + q] = 1u + ((((uint32_t)(hq >> (16 * q))) & 0xFFFFu) * (uint32_t)(m - 1) >> 16);
+            }
+          }
+          const uint32_t po0[4] = {o0.x, o0.y, o0.z, o0.w};
+          uint16_t co0[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            co0[q] = (q < nbe && po0[q] != self) ? LDM(codes + po0[q]) : (uint16_t)CODE_DEAD;
+          uint16_t wo[DR], wi[DR];
+#pragma unroll
+          for (int j = 0; j < DR; ++j) {
+            wo[j] = wi[j] = (uint16_t)CODE_DEAD;
+            if (works && j < draws) {
+              const uint32_t r = sh[j];
+              wo[j] = LDM(W.wcode + base + add_mod(p, r, (uint32_t)m));
+              wi[j] = LDM(W.wcode + base + sub_mod(p, r, (uint32_t)m));
+            }
+          }
+          float acc[3] = {0.f, 0.f, 0.f};
+#pragma unroll
+          for (int i = 0; i < HH; ++i) add_src(acc[0], edges, T.factor, hc[i]);
+          for (int i = HH; i < sz; ++i) {
+            if (start + i == b) continue;
+            add_src(acc[0], edges, T.factor, LDM(codes + start + i));
+          }
+#pragma unroll
+          for (int j = 0; j < DR; ++j) {
+            add_src(acc[1], edges, T.factor, wo[j]);
+            add_src(acc[1], edges, T.factor, wi[j]);
+          }
+          if (n >= 2) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) add_src(acc[2], edges, T.factor, co0[q]);
+            for (int j0 = 4; j0 < nbe; j0 += 4) {
+              const uint4 o = LDM(ro + (j0 >> 2));
+              const uint32_t po[4] = {o.x, o.y, o.z, o.w};
+              uint16_t co[4];
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                co[q] = (j0 + q < nbe && po[q] != self) ? LDM(codes + po[q]) : (uint16_t)CODE_DEAD;
+#pragma unroll
+              for (int q = 0; q < 4; ++q) add_src(acc[2], edges, T.factor, co[q]);
+            }
+            const uint4 inv[2] = {in0, in1};
+            const uint16_t* iv = (const uint16_t*)inv;
+#pragma unroll
+            for (int j = 0; j < RT_SLOTS; ++j) add_rin(acc[2], edges, T.factor, iv[j]);
+          }
+          const float tot = acc[0] * T.bfac[0] + acc[1] * T.bfac[1] + acc[2] * T.bfac[2];
+          if (h.stage == S_SUS && !(A.P->sterilizing && h.immune)) lam = (double)(tot * T.sfac[h.age]);
+        }
+        uint4* rw = (uint4*)(W.rin + (size_t)b * RT_SLOTS);
+        rw[0] = make_uint4(0, 0, 0, 0);
+        rw[1] = make_uint4(0, 0, 0, 0);
+      }
+      unsigned ev = 0;
+      if (valid) ev = transmit_progress_core(A.P, st, A.K, nullptr, t, A.tau_lut, b, lam, -1, h);
+      unsigned tested = 0;
+      if (R.tests) {
+        if (valid) {
+          uint8_t fl = (ev & 8u) ? FL_SYMPTOMATIC : A.flags[b];
+          tested = test_agent(A, b, h.stage, fl, R.den ? R.den_list : nullptr, R.den_count);
+          A.flags[b] = fl;
+        }
+        rec_add(rc, EPI_REC_TESTS, tested);
+      } else if (valid && (ev & 8u)) {
+        A.flags[b] = FL_SYMPTOMATIC;
+      }
+      rec_events(rc, ev);
+      rec_add(rc, EPI_REC_EDGES, edges);
+    }
+    // ---- phase B: DEN regeneration ----------------------------------------
+    const int first_day = t - R.den_lookback > 0 ? t - R.den_lookback : 0;
+    const int n_back = t - first_day;
+    if (R.den && R.tests && n_back > 0) {
+      grid_barrier(R.barrier, ++bar * gridDim.x);
+      if (!service) {
+        const int64_t items = (int64_t)LDM(R.den_count) * n_back;
+        const int64_t gw = (int64_t)blockIdx.x * nwa + warp, warps = (int64_t)gridDim.x * nwa;
+        for (int64_t it = gw; it < items; it += warps) {
+          const int dd = (int)(it % n_back);
+          const int day = first_day + dd;
+          den_regen_item(net, make_net_keys(R.seed, day), day, LDM(R.den_list + it / n_back), rk_w[warp], wrad,
+                         R.died_at, A.flags, lane);
+        }
+      }
+      grid_barrier(R.barrier, ++bar * gridDim.x);
+    }
+    // ---- phase C: follow-ups, dropout, immunity, eligibility ---------------
+    unsigned long long* hist = R.hist + (size_t)par * IV_HIST;
+    if (R.post) {
+      if (!service) {
+        unsigned notified = 0, active = 0;
+        if (valid) iv_post_agent(A, b, R.bucket, h_s, notified, active);
+        rec_add(rc, EPI_REC_NOTIFY, notified);
+        rec_add(rc, EPI_REC_ACTIVE, active);
+        if (R.vax) {
+          const unsigned wa = __reduce_add_sync(0xFFFFFFFFu, active);
+          if (lane == 0 && wa) atomicAdd(&hist[NUM_BUCKETS], (unsigned long long)wa);
+        }
+      }
+      if (R.vax) {
+        __syncthreads();
+        for (int i = threadIdx.x; i < NUM_BUCKETS; i += blockDim.x) {
+          const unsigned v = h_s[i];
+          R.tile_hist[(size_t)blockIdx.x * NUM_BUCKETS + i] = v;
+          if (v) atomicAdd(&hist[i], (unsigned long long)v);
+          h_s[i] = 0u;                      // next used in tomorrow's phase C
+        }
+        grid_barrier(R.barrier, ++bar * gridDim.x);
+      }
+    }
+    // ---- phase D: doses, record, next codes, tomorrow's tables -------------
+    long long cut = -1, rem = 0;
+    if (R.vax) {
+      for (int i = threadIdx.x; i < IV_HIST; i += blockDim.x) hist_s[i] = LDM(hist + i);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const epi_params* __restrict__ P = A.P;
+        int open = *R.vax_open;
+        if (!open && (double)hist_s[NUM_BUCKETS] >= P->start_trigger_count) open = 1;
+        long long c = -1, r = 0, doses = -1;
+        if (open && P->dose_budget > 0) {
+          long long cum = 0;
+          c = NUM_BUCKETS;
+          doses = -2;
+          for (int bk = 0; bk < NUM_BUCKETS; ++bk) {
+            const long long hb = (long long)hist_s[bk];
+            if (cum + hb >= P->dose_budget) { c = bk; r = P->dose_budget - cum; doses = P->dose_budget; break; }
+            cum += hb;
+          }
+          if (doses == -2) doses = cum;
+        }
+        if (blockIdx.x == 0) {
+          *R.vax_open = open;             // the latch only opens: a late reader derives the same
+          if (doses > 0) rc.v[0][EPI_REC_DOSES] += (unsigned)doses;
+        }
+        plan_s[0] = c;
+        plan_s[1] = r;
+        off_s = 0;
+      }
+      __syncthreads();
+      cut = plan_s[0];
+      rem = plan_s[1];
+      if (cut >= 0 && cut < NUM_BUCKETS) {
+        unsigned part = 0;
+        for (int bb = threadIdx.x; bb < (int)blockIdx.x; bb += blockDim.x)
+          part += LDM(R.tile_hist + (size_t)bb * NUM_BUCKETS + cut);
+        part = __reduce_add_sync(0xFFFFFFFFu, part);
+        if (lane == 0 && part) atomicAdd(&off_s, (int)part);
+      }
+      // cut-bucket rank of each agent in id order: warp ballots + warp offsets
+      const uint8_t bk = valid ? R.bucket[b] : NO_BUCKET;
+      const bool in_cut = cut >= 0 && cut < NUM_BUCKETS && bk == (uint8_t)cut;
+      const unsigned ball = __ballot_sync(0xFFFFFFFFu, in_cut);
+      if (lane == 0) wsum_s[warp] = __popc(ball);
+      __syncthreads();
+      int rank = off_s + __popc(ball & ((1u << lane) - 1u));
+      for (int ww = 0; ww < warp; ++ww) rank += wsum_s[ww];
+      if (valid && cut >= 0 && bk != NO_BUCKET && ((long long)bk < cut || (in_cut && (long long)rank < rem)))
+        give_dose(A, b, bk);
+      if (blockIdx.x == 0)                // tomorrow's histogram starts empty
+        for (int i = threadIdx.x; i < IV_HIST; i += blockDim.x) R.hist[(size_t)(par ^ 1) * IV_HIST + i] = 0;
+    }
+    if (!service) {
+      int stage = 0;
+      int32_t inf = 0;
+      uint16_t cn = 0;
+      if (valid) {
+        stage = st.stage[b];
+        inf = st.infected_at[b];
+        if (R.died_at && stage == S_DEAD && R.died_at[b] == INT32_MAX) R.died_at[b] = t;
+        cn = source_code(A.P, stage, inf, st.quarantine_until[b], t + 1);
+        if (stage == S_DEAD) cn |= CODE_DEAD;
+        else cn |= (uint16_t)(random_count(net, D.rcount_next, b) << 8);
+        codes_next[b] = cn;
+        A.flags[b] = 0;
+      }
+      rec_agent(rc, valid, stage, inf);
+      if (valid && works) {
+        const uint32_t q = walk_inv((uint32_t)loc, work_keys(D.wperm_next, w), make_radix((uint32_t)m));
+        Wn.wcode[base + q] = cn;
+        p = q;
+        if (d + 1 == R.n_days) {
+          Wn.pos_of[base + loc] = (uint8_t)q;
+          for (int j = loc; j < draws; j += m)
+            Wn.shift[(size_t)w * draws + j] = (uint8_t)work_shift(D.wshift_next, w, j, m);
+        }
+      }
+      int na = valid ? code_count(cn) : 0;
+      na = na < RT_SLOTS ? na : RT_SLOTS;
+      int incl = na;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+      const int excl = incl - na;
+      excl_s[warp][lane] = excl;
+      cn_s[warp][lane] = cn;
+      for (int i = 0; i < na; ++i) own_s[warp][excl + i] = (uint8_t)lane;
+      __syncwarp();
+      const int64_t wbase_agent = b - lane;
+      for (int k = lane; k < total; k += 32) {
+        const int l = own_s[warp][k];
+        const int j = k - excl_s[warp][l];
+        const uint32_t src = (uint32_t)(wbase_agent + l);
+        const uint32_t y = walk_fwd(src, D.rk_next[j], R.dn);
+        Wn.rout[(size_t)src * RT_SLOTS + j] = y;
+        if (y != src) Wn.rin[(size_t)y * RT_SLOTS + j] = cn_s[warp][l] | CODE_PRESENT;
+      }
+      cb = cn;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0 && R.den_count) *R.den_count = 0;   // tomorrow's notifier list
+    if (d + 1 < R.n_days) grid_barrier(R.barrier, ++bar * gridDim.x);
+  }
+  __syncthreads();
+  if (service)
+    rec_flush_warp(racc[(R.n_days - 1) & 1], R.records + (size_t)(R.n_days - 1) * EPI_REC_LEN,
+                   R.first_step + R.n_days - 1, nwa, lane);
+  if (blockIdx.x == 0 && threadIdx.x < RT_SLOTS && R.ring_t2 != nullptr)
+    R.ring_t2->rk[threadIdx.x] =
+        random_slot_keys(key_prefix(R.seed, R.first_step + R.n_days + 1, P_NET_RPERM), threadIdx.x);
+}
+
+}  // namespace epi
