@@ -62,7 +62,6 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
   __shared__ uint16_t cn_s[RUN_MAX_THREADS / 32][32];
   __shared__ uint8_t own_s[RUN_MAX_THREADS / 32][32 * RT_SLOTS];
   __shared__ unsigned h_s[NUM_BUCKETS];
-  __shared__ unsigned long long hist_s[IV_HIST];
   __shared__ int wsum_s[RUN_MAX_THREADS / 32];
   __shared__ long long plan_s[2];
   __shared__ int off_s;
@@ -229,114 +228,19 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
       rec_events(rc, ev);
       rec_add(rc, EPI_REC_EDGES, edges);
     }
-    // ---- phase B: DEN regeneration ----------------------------------------
-    const int first_day = t - R.den_lookback > 0 ? t - R.den_lookback : 0;
-    const int n_back = t - first_day;
-    if (R.den && R.tests && n_back > 0) {
-      grid_barrier(R.barrier, ++bar * gridDim.x);
-      if (!service) {
-        const int64_t items = (int64_t)LDM(R.den_count) * n_back;
-        const int64_t gw = (int64_t)blockIdx.x * nwa + warp, warps = (int64_t)gridDim.x * nwa;
-        for (int64_t it = gw; it < items; it += warps) {
-          const int dd = (int)(it % n_back);
-          const int day = first_day + dd;
-          den_regen_item(net, make_net_keys(R.seed, day), day, LDM(R.den_list + it / n_back), rk_w[warp], wrad,
-                         R.died_at, A.flags, lane);
-        }
-      }
-      grid_barrier(R.barrier, ++bar * gridDim.x);
-    }
-    // ---- phase C: follow-ups, dropout, immunity, eligibility ---------------
-    unsigned long long* hist = R.hist + (size_t)par * IV_HIST;
-    if (R.post) {
-      if (!service) {
-        unsigned notified = 0, active = 0;
-        if (valid) iv_post_agent(A, b, R.bucket, h_s, notified, active);
-        rec_add(rc, EPI_REC_NOTIFY, notified);
-        rec_add(rc, EPI_REC_ACTIVE, active);
-        if (R.vax) {
-          const unsigned wa = __reduce_add_sync(0xFFFFFFFFu, active);
-          if (lane == 0 && wa) atomicAdd(&hist[NUM_BUCKETS], (unsigned long long)wa);
-        }
-      }
-      if (R.vax) {
-        __syncthreads();
-        for (int i = threadIdx.x; i < NUM_BUCKETS; i += blockDim.x) {
-          const unsigned v = h_s[i];
-          R.tile_hist[(size_t)blockIdx.x * NUM_BUCKETS + i] = v;
-          if (v) atomicAdd(&hist[i], (unsigned long long)v);
-          h_s[i] = 0u;                      // next used in tomorrow's phase C
-        }
-        grid_barrier(R.barrier, ++bar * gridDim.x);
-      }
-    }
-    // ---- phase D: doses, record, next codes, tomorrow's tables -------------
-    long long cut = -1, rem = 0;
-    if (R.vax) {
-      for (int i = threadIdx.x; i < IV_HIST; i += blockDim.x) hist_s[i] = LDM(hist + i);
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        const epi_params* __restrict__ P = A.P;
-        int open = *R.vax_open;
-        if (!open && (double)hist_s[NUM_BUCKETS] >= P->start_trigger_count) open = 1;
-        long long c = -1, r = 0, doses = -1;
-        if (open && P->dose_budget > 0) {
-          long long cum = 0;
-          c = NUM_BUCKETS;
-          doses = -2;
-          for (int bk = 0; bk < NUM_BUCKETS; ++bk) {
-            const long long hb = (long long)hist_s[bk];
-            if (cum + hb >= P->dose_budget) { c = bk; r = P->dose_budget - cum; doses = P->dose_budget; break; }
-            cum += hb;
-          }
-          if (doses == -2) doses = cum;
-        }
-        if (blockIdx.x == 0) {
-          *R.vax_open = open;             // the latch only opens: a late reader derives the same
-          if (doses > 0) rc.v[0][EPI_REC_DOSES] += (unsigned)doses;
-        }
-        plan_s[0] = c;
-        plan_s[1] = r;
-        off_s = 0;
-      }
-      __syncthreads();
-      cut = plan_s[0];
-      rem = plan_s[1];
-      if (cut >= 0 && cut < NUM_BUCKETS) {
-        unsigned part = 0;
-        for (int bb = threadIdx.x; bb < (int)blockIdx.x; bb += blockDim.x)
-          part += LDM(R.tile_hist + (size_t)bb * NUM_BUCKETS + cut);
-        part = __reduce_add_sync(0xFFFFFFFFu, part);
-        if (lane == 0 && part) atomicAdd(&off_s, (int)part);
-      }
-      // cut-bucket rank of each agent in id order: warp ballots + warp offsets
-      const uint8_t bk = valid ? R.bucket[b] : NO_BUCKET;
-      const bool in_cut = cut >= 0 && cut < NUM_BUCKETS && bk == (uint8_t)cut;
-      const unsigned ball = __ballot_sync(0xFFFFFFFFu, in_cut);
-      if (lane == 0) wsum_s[warp] = __popc(ball);
-      __syncthreads();
-      int rank = off_s + __popc(ball & ((1u << lane) - 1u));
-      for (int ww = 0; ww < warp; ++ww) rank += wsum_s[ww];
-      if (valid && cut >= 0 && bk != NO_BUCKET && ((long long)bk < cut || (in_cut && (long long)rank < rem)))
-        give_dose(A, b, bk);
-      if (blockIdx.x == 0)                // tomorrow's histogram starts empty
-        for (int i = threadIdx.x; i < IV_HIST; i += blockDim.x) R.hist[(size_t)(par ^ 1) * IV_HIST + i] = 0;
-    }
-    if (!service) {
-      int stage = 0;
-      int32_t inf = 0;
+    // tomorrow's code and push tables: final once phase C's dropout has run
+    // (a dose only turns code-0 susceptibles into code-0 vaccinated agents),
+    // so they overlap the histogram barrier
+    auto next_day = [&]() {
       uint16_t cn = 0;
       if (valid) {
-        stage = st.stage[b];
-        inf = st.infected_at[b];
+        const int stage = st.stage[b];
         if (R.died_at && stage == S_DEAD && R.died_at[b] == INT32_MAX) R.died_at[b] = t;
-        cn = source_code(A.P, stage, inf, st.quarantine_until[b], t + 1);
+        cn = source_code(A.P, stage, st.infected_at[b], st.quarantine_until[b], t + 1);
         if (stage == S_DEAD) cn |= CODE_DEAD;
         else cn |= (uint16_t)(random_count(net, D.rcount_next, b) << 8);
         codes_next[b] = cn;
-        A.flags[b] = 0;
       }
-      rec_agent(rc, valid, stage, inf);
       if (valid && works) {
         const uint32_t q = walk_inv((uint32_t)loc, work_keys(D.wperm_next, w), make_radix((uint32_t)m));
         Wn.wcode[base + q] = cn;
@@ -371,6 +275,145 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
         if (y != src) Wn.rin[(size_t)y * RT_SLOTS + j] = cn_s[warp][l] | CODE_PRESENT;
       }
       cb = cn;
+    };
+    // ---- phase B: DEN regeneration ----------------------------------------
+    const int first_day = t - R.den_lookback > 0 ? t - R.den_lookback : 0;
+    const int n_back = t - first_day;
+    const bool phase_b = R.den && R.tests && n_back > 0;
+    if (phase_b) {
+      grid_barrier(R.barrier, ++bar * gridDim.x);
+      if (!service) {
+        const int64_t items = (int64_t)LDM(R.den_count) * n_back;
+        const int64_t gw = (int64_t)blockIdx.x * nwa + warp, warps = (int64_t)gridDim.x * nwa;
+        for (int64_t it = gw; it < items; it += warps) {
+          const int dd = (int)(it % n_back);
+          const int day = first_day + dd;
+          den_regen_item(net, make_net_keys(R.seed, day), day, LDM(R.den_list + it / n_back), rk_w[warp], wrad,
+                         R.died_at, A.flags, lane);
+        }
+      }
+      grid_barrier(R.barrier, ++bar * gridDim.x);
+    }
+    // ---- phase C: follow-ups, dropout, immunity, eligibility ---------------
+    unsigned long long* hist = R.hist + (size_t)par * IV_HIST;
+    if (R.post) {
+      if (!service) {
+        unsigned notified = 0, active = 0;
+        if (valid) iv_post_agent(A, b, R.bucket, h_s, notified, active);
+        rec_add(rc, EPI_REC_NOTIFY, notified);
+        rec_add(rc, EPI_REC_ACTIVE, active);
+        if (R.vax) {
+          const unsigned wa = __reduce_add_sync(0xFFFFFFFFu, active);
+          if (lane == 0 && wa) atomicAdd(&hist[NUM_BUCKETS], (unsigned long long)wa);
+        }
+      }
+      if (R.vax) {
+        // split barrier: arrive with the histogram, build tomorrow's code and
+        // tables, then wait
+        __syncthreads();
+        for (int i = threadIdx.x; i < NUM_BUCKETS; i += blockDim.x) {
+          const unsigned v = h_s[i];
+          R.tile_hist[(size_t)blockIdx.x * NUM_BUCKETS + i] = v;
+          if (v) atomicAdd(&hist[i], (unsigned long long)v);
+          h_s[i] = 0u;                      // next used in tomorrow's phase C
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          unsigned v;
+          asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(v) : "l"(R.barrier) : "memory");
+        }
+        if (!service) next_day();
+        __syncthreads();
+        ++bar;
+        if (threadIdx.x == 0) {
+          unsigned v;
+          do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(R.barrier) : "memory");
+          } while (v < bar * gridDim.x);
+        }
+        __syncthreads();
+      } else if (!service) {
+        next_day();
+      }
+    } else if (!service) {
+      next_day();
+    }
+    // ---- phase D: doses, record, next codes, tomorrow's tables -------------
+    long long cut = -1, rem = 0;
+    if (R.vax) {
+      if (warp == 0) {
+        // the plan (k_vax_plan) with one warp: lane l holds buckets 2l, 2l+1;
+        // the cut bucket is the first whose inclusive prefix reaches the budget
+        const epi_params* __restrict__ P = A.P;
+        const long long c0 = lane < NUM_BUCKETS / 2 ? (long long)LDM(hist + 2 * lane) : 0;
+        const long long c1 = lane < NUM_BUCKETS / 2 ? (long long)LDM(hist + 2 * lane + 1) : 0;
+        int open = *R.vax_open;
+        if (!open && (double)LDM(hist + NUM_BUCKETS) >= P->start_trigger_count) open = 1;
+        long long c = -1, r = 0, doses = -1;
+        const long long budget = P->dose_budget;
+        if (open && budget > 0) {
+          const long long pair = c0 + c1;
+          long long S = pair;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const long long v = __shfl_up_sync(0xFFFFFFFFu, S, o);
+            if (lane >= o) S += v;
+          }
+          const unsigned ball = __ballot_sync(0xFFFFFFFFu, S >= budget);
+          if (ball) {
+            const int L = __ffs(ball) - 1;
+            const long long E = __shfl_sync(0xFFFFFFFFu, S - pair, L);
+            const long long cA = __shfl_sync(0xFFFFFFFFu, c0, L);
+            if (E + cA >= budget) { c = 2 * L; r = budget - E; }
+            else { c = 2 * L + 1; r = budget - E - cA; }
+            doses = budget;
+          } else {
+            c = NUM_BUCKETS;                // everyone eligible gets a dose
+            doses = __shfl_sync(0xFFFFFFFFu, S, 31);
+          }
+        }
+        if (lane == 0) {
+          if (blockIdx.x == 0) {
+            *R.vax_open = open;           // the latch only opens: a late reader derives the same
+            if (doses > 0) rc.v[0][EPI_REC_DOSES] += (unsigned)doses;
+          }
+          plan_s[0] = c;
+          plan_s[1] = r;
+          off_s = 0;
+        }
+      }
+      __syncthreads();
+      cut = plan_s[0];
+      rem = plan_s[1];
+      if (cut >= 0 && cut < NUM_BUCKETS) {
+        unsigned part = 0;
+        for (int bb = threadIdx.x; bb < (int)blockIdx.x; bb += blockDim.x)
+          part += LDM(R.tile_hist + (size_t)bb * NUM_BUCKETS + cut);
+        part = __reduce_add_sync(0xFFFFFFFFu, part);
+        if (lane == 0 && part) atomicAdd(&off_s, (int)part);
+      }
+      // cut-bucket rank of each agent in id order: warp ballots + warp offsets
+      const uint8_t bk = valid ? R.bucket[b] : NO_BUCKET;
+      const bool in_cut = cut >= 0 && cut < NUM_BUCKETS && bk == (uint8_t)cut;
+      const unsigned ball = __ballot_sync(0xFFFFFFFFu, in_cut);
+      if (lane == 0) wsum_s[warp] = __popc(ball);
+      __syncthreads();
+      int rank = off_s + __popc(ball & ((1u << lane) - 1u));
+      for (int ww = 0; ww < warp; ++ww) rank += wsum_s[ww];
+      if (valid && cut >= 0 && bk != NO_BUCKET && ((long long)bk < cut || (in_cut && (long long)rank < rem)))
+        give_dose(A, b, bk);
+      if (blockIdx.x == 0)                // tomorrow's histogram starts empty
+        for (int i = threadIdx.x; i < IV_HIST; i += blockDim.x) R.hist[(size_t)(par ^ 1) * IV_HIST + i] = 0;
+    }
+    if (!service) {
+      int stage = 0;
+      int32_t inf = 0;
+      if (valid) {
+        stage = st.stage[b];
+        inf = st.infected_at[b];
+        A.flags[b] = 0;
+      }
+      rec_agent(rc, valid, stage, inf);
     }
     if (blockIdx.x == 0 && threadIdx.x == 0 && R.den_count) *R.den_count = 0;   // tomorrow's notifier list
     if (d + 1 < R.n_days) grid_barrier(R.barrier, ++bar * gridDim.x);
