@@ -105,6 +105,20 @@ constexpr int RUN_MAX_THREADS = RUN_MAX_AGENTS + 32;
 // grid barrier orders them after the writers' stores
 template <class T> __device__ __forceinline__ T LDM(const T* p) { return *p; }
 
+// The day's 8 colleague shifts r_j of workplace w (work_shift: four 16-bit
+// fields per hash), packed one byte each (r_j <= m - 1 <= 254).
+__device__ __forceinline__ uint2 day_shifts(uint64_t wshift_prefix, int w, int m) {
+  const uint64_t hw = fold(wshift_prefix, (uint64_t)w);
+  const uint64_t h0 = fold(hw, 0), h1 = fold(hw, 1);
+  uint32_t lo = 0, hi = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    lo |= (1u + ((((uint32_t)(h0 >> (16 * q))) & 0xFFFFu) * (uint32_t)(m - 1) >> 16)) << (8 * q);
+    hi |= (1u + ((((uint32_t)(h1 >> (16 * q))) & 0xFFFFu) * (uint32_t)(m - 1) >> 16)) << (8 * q);
+  }
+  return make_uint2(lo, hi);
+}
+
 __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_fused_run(RunArgs R, epi_net net) {
   constexpr int HH = 8, DR = 8;
   __shared__ MsgTables T;
@@ -151,6 +165,7 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_fused_run(RunArgs R, epi
   const int64_t start = b - off;
   const Radix rm = make_radix(works ? (uint32_t)m : 1u);
   __syncthreads();
+  uint2 shp = works ? day_shifts(dk[0].wshift, w, m) : make_uint2(0, 0);
   for (int d = 0; d < R.n_days; ++d) {
     const int t = R.first_step + d;
     const int par = t & 1;
@@ -180,17 +195,12 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_fused_run(RunArgs R, epi
 #pragma unroll
         for (int i = 0; i < HH; ++i)
           hc[i] = (i < sz && start + i != b) ? LDM(codes + start + i) : (uint16_t)CODE_DEAD;
-        // the day's colleague shifts r_j (work_shift), four per hash
+        // the day's colleague shifts r_j (hashed while the previous barrier waited)
         uint32_t sh[DR];
-        if (works) {
-          const uint64_t hw = fold(D.wshift, (uint64_t)w);
 #pragma unroll
-          for (int j4 = 0; j4 < DR; j4 += 4) {
-            const uint64_t hq = fold(hw, (uint64_t)(j4 >> 2));
-#pragma unroll
-            for (int q = 0; q < 4; ++q)
-              sh[j4 + q] = 1u + ((((uint32_t)(hq >> (16 * q))) & 0xFFFFu) * (uint32_t)(m - 1) >> 16);
-          }
+        for (int q = 0; q < 4; ++q) {
+          sh[q] = (shp.x >> (8 * q)) & 0xFFu;
+          sh[4 + q] = (shp.y >> (8 * q)) & 0xFFu;
         }
         // level 2
         const uint32_t po0[4] = {o0.x, o0.y, o0.z, o0.w};
@@ -299,7 +309,23 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_fused_run(RunArgs R, epi
     }
     cb = cn;
     }
-    if (d + 1 < R.n_days) grid_barrier(R.barrier, (unsigned)(d + 1) * gridDim.x);
+    if (d + 1 < R.n_days) {
+      // grid barrier, split: tomorrow's shifts (keys ready since the
+      // service warp's day) are hashed between arrive and wait
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        unsigned v;
+        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(v) : "l"(R.barrier) : "memory");
+      }
+      if (works) shp = day_shifts(dk[(d + 1) & 1].wshift, w, m);
+      if (threadIdx.x == 0) {
+        unsigned v;
+        do {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(R.barrier) : "memory");
+        } while (v < (unsigned)(d + 1) * gridDim.x);
+      }
+      __syncthreads();
+    }
   }
   __syncthreads();
   if (service)
