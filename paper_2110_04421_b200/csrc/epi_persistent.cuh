@@ -165,7 +165,12 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_fused_run(RunArgs R, epi
   const int64_t start = b - off;
   const Radix rm = make_radix(works ? (uint32_t)m : 1u);
   __syncthreads();
+  // state-independent values of the coming day, computed ahead (here, then
+  // between each barrier's arrive and wait): today's shifts, the slot count
+  // of tomorrow's code and tomorrow's workplace position
   uint2 shp = works ? day_shifts(dk[0].wshift, w, m) : make_uint2(0, 0);
+  int cnt_nx = valid ? random_count(net, dk[0].rcount_next, b) : 0;
+  uint32_t q_nx = works ? walk_inv((uint32_t)loc, work_keys(dk[0].wperm_next, w), rm) : 0u;
   for (int d = 0; d < R.n_days; ++d) {
     const int t = R.first_step + d;
     const int par = t & 1;
@@ -267,12 +272,12 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_fused_run(RunArgs R, epi
     if (valid) {
       cn = source_code(R.P, h.stage, h.infected_at, h.q_until, t + 1);
       if (h.stage == S_DEAD) cn |= CODE_DEAD;
-      else cn |= (uint16_t)(random_count(net, D.rcount_next, b) << 8);
+      else cn |= (uint16_t)(cnt_nx << 8);
       codes_next[b] = cn;
     }
     // tomorrow's push tables: the worker's position and its code there
     if (valid && works) {
-      const uint32_t q = walk_inv((uint32_t)loc, work_keys(D.wperm_next, w), rm);
+      const uint32_t q = q_nx;
       Wn.wcode[base + q] = cn;
       p = q;
       if (d + 1 == R.n_days) {         // position and shift tables for the per-day path
@@ -317,7 +322,11 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_fused_run(RunArgs R, epi
         unsigned v;
         asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(v) : "l"(R.barrier) : "memory");
       }
-      if (works) shp = day_shifts(dk[(d + 1) & 1].wshift, w, m);
+      if (works) {
+        shp = day_shifts(dk[(d + 1) & 1].wshift, w, m);
+        q_nx = walk_inv((uint32_t)loc, work_keys(dk[(d + 1) & 1].wperm_next, w), rm);
+      }
+      if (valid) cnt_nx = random_count(net, dk[(d + 1) & 1].rcount_next, b);
       if (threadIdx.x == 0) {
         unsigned v;
         do {
