@@ -110,6 +110,7 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
   const int64_t start = b - off;
   unsigned bar = 0;                        // barriers passed
   __syncthreads();
+  uint2 shp = works ? day_shifts(dk[0].wshift, w, m) : make_uint2(0, 0);   // the day's colleague shifts
   for (int d = 0; d < R.n_days; ++d) {
     const int t = R.first_step + d;
     const int par = t & 1;
@@ -150,15 +151,10 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
           for (int i = 0; i < HH; ++i)
             hc[i] = (i < sz && start + i != b) ? LDM(codes + start + i) : (uint16_t)CODE_DEAD;
           uint32_t sh[DR];
-          if (works) {
-            const uint64_t hw = fold(D.wshift, (uint64_t)w);
 #pragma unroll
-            for (int j4 = 0; j4 < DR; j4 += 4) {
-              const uint64_t hq = fold(hw, (uint64_t)(j4 >> 2));
-#pragma unroll
-              for (int q = 0; q < 4; ++q)
-                sh[j4 + q] = 1u + ((((uint32_t)(hq >> (16 * q))) & 0xFFFFu) * (uint32_t)(m - 1) >> 16);
-            }
+          for (int q = 0; q < 4; ++q) {
+            sh[q] = (shp.x >> (8 * q)) & 0xFFu;
+            sh[4 + q] = (shp.y >> (8 * q)) & 0xFFu;
           }
           const uint32_t po0[4] = {o0.x, o0.y, o0.z, o0.w};
           uint16_t co0[4];
@@ -416,7 +412,23 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
       rec_agent(rc, valid, stage, inf);
     }
     if (blockIdx.x == 0 && threadIdx.x == 0 && R.den_count) *R.den_count = 0;   // tomorrow's notifier list
-    if (d + 1 < R.n_days) grid_barrier(R.barrier, ++bar * gridDim.x);
+    if (d + 1 < R.n_days) {
+      // end of day, split: tomorrow's shifts hashed between arrive and wait
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        unsigned v;
+        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(v) : "l"(R.barrier) : "memory");
+      }
+      if (works) shp = day_shifts(dk[(d + 1) & 1].wshift, w, m);
+      ++bar;
+      if (threadIdx.x == 0) {
+        unsigned v;
+        do {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(R.barrier) : "memory");
+        } while (v < bar * gridDim.x);
+      }
+      __syncthreads();
+    }
   }
   __syncthreads();
   if (service)
