@@ -239,6 +239,63 @@ __device__ __forceinline__ unsigned transmit_progress_core(const epi_params* __r
   return ev;
 }
 
+// transmit_progress_core split in two for the persistent runs: the day's
+// decisions now (infection + entry stage, due transition + destination:
+// everything the day's record and tomorrow's code need), the scheduling of
+// the next transition (branch + delay draws, threshold tables: the longest
+// dependent chain) later, between the day's barrier arrive and wait — it
+// only feeds tomorrow's transition check.  Same draws, same results.
+// `pend` = the stage to schedule from, -1 if none.
+__device__ __forceinline__ unsigned transmit_progress_now(const epi_params* __restrict__ P, const epi_state& st,
+                                                          const StepKeys& K, int step, int64_t a, double lam,
+                                                          AgentHot& h, int& pend) {
+  unsigned ev = 0;
+  pend = -1;
+  bool infected = false;
+  if (h.stage == S_SUS && !(P->sterilizing && h.immune)) {
+    const double p = 1.0 - exp(-lam);
+    infected = lam > 0.0 && draw(K, nullptr, P_INFECTION, a) < p;
+    if (infected) {
+      int entry = P->targets[S_SUS][pick_branch(P, S_SUS, h.age, draw(K, nullptr, P_ENTRY, a))];
+      if (!P->sterilizing && h.immune) entry = S_ASYM;
+      h.stage = entry;
+      h.infected_at = step;
+      st.stage[a] = (int8_t)entry;
+      st.infected_at[a] = step;
+      pend = entry;
+      ev |= 1u;
+    }
+  }
+  // (after an infection the next transition is >= 1 day away)
+  if (!infected && h.nta == step) {
+    const int dest = h.next_stage;
+    h.stage = dest;
+    st.stage[a] = (int8_t)dest;
+    if (dest == S_DEAD) ev |= 2u;
+    if (dest == S_HOSP) ev |= 4u;
+    if (dest == S_MILD || dest == S_SEV) ev |= 8u;
+    if (dest == S_REC || dest == S_DEAD) {
+      h.next_stage = NEVER8;
+      h.nta = NEVER;
+      st.next_stage[a] = (int8_t)h.next_stage;
+      st.next_transition_at[a] = h.nta;
+    } else {
+      pend = dest;
+    }
+  }
+  return ev;
+}
+__device__ __forceinline__ void schedule_pending(const epi_params* __restrict__ P, const epi_state& st,
+                                                 const StepKeys& K, int step, const uint16_t* __restrict__ tau_lut,
+                                                 int64_t a, int pend, AgentHot& h) {
+  int nxt, delay;
+  schedule(P, pend, h.age, draw(K, nullptr, P_BRANCH, a), draw(K, nullptr, P_DELAY, a), nxt, delay, tau_lut);
+  h.next_stage = nxt;
+  h.nta = step + delay;
+  st.next_stage[a] = (int8_t)nxt;
+  st.next_transition_at[a] = h.nta;
+}
+
 __device__ __forceinline__ unsigned transmit_progress_hot(const StepArgs& A, int64_t a, double lam, int forced,
                                                           AgentHot& h) {
   return transmit_progress_core(A.P, A.st, A.K, A.inj, A.step, A.tau_lut, a, lam, forced, h);

@@ -176,6 +176,7 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_fused_run(RunArgs R, epi
     const int par = t & 1;
     const DayKeys& D = dk[d & 1];
     RecAcc& rc = racc[d & 1];
+    int pend = -1;                         // the day's deferred transition scheduling
     if (service) {
       // yesterday's record rows (complete since the barrier); tomorrow's keys
       if (d > 0) rec_flush_warp(racc[(d - 1) & 1], R.records + (size_t)(d - 1) * EPI_REC_LEN, t - 1, nwa, lane);
@@ -263,7 +264,7 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_fused_run(RunArgs R, epi
       rw[1] = make_uint4(0, 0, 0, 0);
     }
     unsigned ev = 0;
-    if (valid) ev = transmit_progress_core(R.P, R.st, D.K, nullptr, t, R.tau_lut, b, lam, -1, h);
+    if (valid) ev = transmit_progress_now(R.P, R.st, D.K, t, b, lam, h, pend);
     rec_events(rc, ev);
     rec_add(rc, EPI_REC_EDGES, edges);
     rec_agent(rc, valid, valid ? h.stage : 0, valid ? h.infected_at : 0);
@@ -322,6 +323,7 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_fused_run(RunArgs R, epi
         unsigned v;
         asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(v) : "l"(R.barrier) : "memory");
       }
+      if (pend >= 0) schedule_pending(R.P, R.st, D.K, t, R.tau_lut, b, pend, h);   // feeds tomorrow's check
       if (works) {
         shp = day_shifts(dk[(d + 1) & 1].wshift, w, m);
         q_nx = walk_inv((uint32_t)loc, work_keys(dk[(d + 1) & 1].wperm_next, w), rm);
@@ -334,6 +336,8 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_fused_run(RunArgs R, epi
         } while (v < (unsigned)(d + 1) * gridDim.x);
       }
       __syncthreads();
+    } else if (pend >= 0) {
+      schedule_pending(R.P, R.st, D.K, t, R.tau_lut, b, pend, h);
     }
   }
   __syncthreads();

@@ -117,6 +117,8 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
     const DayKeys& D = dk[d & 1];
     const StepArgs& A = As[d & 1];
     RecAcc& rc = racc[d & 1];
+    int pend = -1;                         // the day's deferred transition scheduling
+    int age = 0;
     const uint16_t* codes = R.codes[par];
     uint16_t* codes_next = R.codes[par ^ 1];
     const WorkTables& W = R.wt[par];
@@ -136,6 +138,7 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
     } else {
       AgentHot h{};
       if (valid) h = load_hot(st, b);
+      age = h.age;
       unsigned edges = 0;
       double lam = 0.0;
       if (valid) {
@@ -209,7 +212,7 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
         rw[1] = make_uint4(0, 0, 0, 0);
       }
       unsigned ev = 0;
-      if (valid) ev = transmit_progress_core(A.P, st, A.K, nullptr, t, A.tau_lut, b, lam, -1, h);
+      if (valid) ev = transmit_progress_now(A.P, st, A.K, t, b, lam, h, pend);
       unsigned tested = 0;
       if (R.tests) {
         if (valid) {
@@ -419,6 +422,11 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
         unsigned v;
         asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(v) : "l"(R.barrier) : "memory");
       }
+      if (pend >= 0) {                     // feeds tomorrow's transition check
+        AgentHot hs{};
+        hs.age = age;
+        schedule_pending(A.P, st, A.K, t, A.tau_lut, b, pend, hs);
+      }
       if (works) shp = day_shifts(dk[(d + 1) & 1].wshift, w, m);
       ++bar;
       if (threadIdx.x == 0) {
@@ -428,6 +436,10 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
         } while (v < bar * gridDim.x);
       }
       __syncthreads();
+    } else if (pend >= 0) {
+      AgentHot hs{};
+      hs.age = age;
+      schedule_pending(A.P, st, A.K, t, A.tau_lut, b, pend, hs);
     }
   }
   __syncthreads();
