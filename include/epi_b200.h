@@ -313,10 +313,12 @@ int epi_sim_run(epi_ctx *ctx, const epi_state *st, int32_t first_step, int32_t n
                 uint64_t seed, int32_t mode, int32_t precision, uint16_t *codes0,
                 uint16_t *codes1, int64_t *records, int32_t *vax_open, void *stream);
 
-/* epi_sim_run sends the days of a merged fused run (mode 1, fp32, no
- * interventions, whole population) to one persistent launch (k_fused_run:
- * one resident thread per agent, a grid barrier per day); bitwise the same
- * results as the per-day kernels.  on = 0 forces the per-day kernels. */
+/* epi_sim_run sends the days after the first of a fused run (mode 1, fp32,
+ * whole population, push tables, N <= 148 x 704) to one persistent launch:
+ * k_fused_run without interventions, k_iv_run with them (one resident thread
+ * per agent, grid barriers between a day's phases; intervention days need
+ * epi_set_iv_fusion on); bitwise the same results as the per-day kernels.
+ * on = 0 forces the per-day kernels. */
 int epi_set_persistent(epi_ctx *ctx, int32_t on);
 /* Replication summary (runner.py:195-207 `summarize`): quartiles q25/q50/q75
  * across n_rep <= 4096 replications, bitwise np.percentile (linear method).
