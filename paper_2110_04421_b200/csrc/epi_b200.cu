@@ -478,10 +478,11 @@ int epi_graph_load(epi_ctx* c, const int32_t* src, const int32_t* dst, const int
     if (rc) return rc;
     c->edge_cap = cap;
   }
-  k_coo_keys<<<grid_for(E, 256), 256, 0, s>>>(src, dst, kind, E, c->n, c->keys_in, c->gflags);
+  int sb = 1;
+  while ((1ll << sb) < c->n) ++sb;
+  k_coo_keys<<<grid_for(E, 256), 256, 0, s>>>(src, dst, kind, E, c->n, sb, c->keys_in, c->gflags);
   CKL();
-  int end_bit = 32;
-  while ((1ll << (end_bit - 32)) < c->n) ++end_bit;
+  const int end_bit = 2 * sb + 2;
   size_t need = 0;
   CK(cub::DeviceRadixSort::SortKeys(nullptr, need, c->keys_in, c->keys_out, (int)E, 0, end_bit, s));
   if (need > c->cub_bytes) {
@@ -491,7 +492,8 @@ int epi_graph_load(epi_ctx* c, const int32_t* src, const int32_t* dst, const int
     c->cub_bytes = need;
   }
   CK(cub::DeviceRadixSort::SortKeys(c->cub_tmp, need, c->keys_in, c->keys_out, (int)E, 0, end_bit, s));
-  k_rows_from_sorted<<<grid_for(E, 256), 256, 0, s>>>(c->keys_out, E, c->row_begin, c->row_len, c->entries);
+  k_rows_from_sorted<<<grid_for(E, 256), 256, 0, s>>>(c->keys_out, E, sb, c->n, c->row_begin, c->row_len,
+                                                      c->entries);
   CKL();
   k_rows_finish<<<grid_for(c->n, 256), 256, 0, s>>>(c->n, c->row_begin, c->row_len);
   CKL();

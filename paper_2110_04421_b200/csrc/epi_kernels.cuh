@@ -356,34 +356,41 @@ __global__ void k_codes(const epi_params* __restrict__ P, epi_state st, int step
 
 // ---------------------------------------------------------------------------
 // Graph-in: COO -> sort keys (dst << 32 | src << 2 | kind) + validation.
+// Keys packed into 2 sb + 2 bits (n <= 2^sb): dst << (sb + 2) | src << 2 |
+// kind, so the radix sort runs ceil((2 sb + 2) / 8) passes (5 at 100 k agents
+// instead of 7 with dst in the high word).  An edge with an index outside
+// [0, n) (flagged, the load is rejected) gets the all-ones key: it sorts last
+// and the row pass skips it, so nothing is written out of bounds.
 __global__ void k_coo_keys(const int32_t* __restrict__ src, const int32_t* __restrict__ dst,
-                           const int8_t* __restrict__ kind, int64_t E, int64_t n,
+                           const int8_t* __restrict__ kind, int64_t E, int64_t n, int sb,
                            uint64_t* __restrict__ keys, long long* flag_word) {
   unsigned fl = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < E;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int32_t s = src[i], d = dst[i];
     const int k = kind[i];
-    if (s < 0 || d < 0 || s >= n || d >= n) fl |= EPI_FLAG_INDEX;
+    const bool bad = s < 0 || d < 0 || s >= n || d >= n;
+    if (bad) fl |= EPI_FLAG_INDEX;
     if (s == d) fl |= EPI_FLAG_SELFLOOP;
     if (k < 0 || k > 2) fl |= EPI_FLAG_KIND;
-    const uint64_t ss = (uint64_t)(uint32_t)s & 0x3FFFFFFFull, dd = (uint64_t)(uint32_t)d & 0x7FFFFFFFull;
-    keys[i] = (dd << 32) | (ss << 2) | (uint64_t)(k & 3);
+    keys[i] = bad ? ~0ull : ((uint64_t)d << (sb + 2)) | ((uint64_t)s << 2) | (uint64_t)(k & 3);
   }
   if (fl) atomicOr((unsigned long long*)flag_word, (unsigned long long)fl);
 }
 
 // Row bounds of the sorted keys; entries = low 32 bits (src << 2 | kind).
-__global__ void k_rows_from_sorted(const uint64_t* __restrict__ keys, int64_t E,
+__global__ void k_rows_from_sorted(const uint64_t* __restrict__ keys, int64_t E, int sb, int64_t n,
                                    int64_t* __restrict__ row_begin, int32_t* __restrict__ row_len,
                                    uint32_t* __restrict__ entries) {
+  const int shift = sb + 2;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < E;
        i += (int64_t)gridDim.x * blockDim.x) {
     const uint64_t k = keys[i];
-    const int64_t d = (int64_t)(k >> 32);
-    entries[i] = (uint32_t)k;
-    if (i == 0 || (int64_t)(keys[i - 1] >> 32) != d) row_begin[d] = i;
-    if (i == E - 1 || (int64_t)(keys[i + 1] >> 32) != d) {
+    const int64_t d = (int64_t)(k >> shift);
+    if (d >= n) continue;                  // a rejected edge (all-ones key)
+    entries[i] = (uint32_t)(k & ((1ull << shift) - 1));
+    if (i == 0 || (int64_t)(keys[i - 1] >> shift) != d) row_begin[d] = i;
+    if (i == E - 1 || (int64_t)(keys[i + 1] >> shift) != d) {
       // length = i + 1 - begin; begin may be written by another thread, so
       // compute it by scanning back is avoided: store end, fix up later
       row_len[d] = (int32_t)(i + 1);   // temporarily the row end
