@@ -132,6 +132,26 @@ def test_hard_errors():
     assert ev.n_edges == 0 and ev.new_infections == 0 and eng.clock == 1
 
 
+def test_rejected_graph_leaves_the_engine_intact():
+    """Out-of-range indices (huge and negative dst) are rejected without
+    touching memory outside the row tables: the next valid graph still gives
+    the hazard of a fresh engine bitwise."""
+    tr = Trajectory("noiv")
+    g = tr.graph(0)
+    a = GpuEngine(tr.initial_cols(), tr.disease, tr.table, InterventionConfig(), tr.seed)
+    b = GpuEngine(tr.initial_cols(), tr.disease, tr.table, InterventionConfig(), tr.seed)
+    n = tr.n
+    for d in (n, n + 70_000, 2 ** 31 - 1, -5):
+        bad = StepGraph(0, np.concatenate([g.src, [0]]).astype(np.int32),
+                        np.concatenate([g.dst, [d]]).astype(np.int32),
+                        np.concatenate([g.kind, [0]]).astype(np.int8))
+        with pytest.raises(InvariantViolation, match="n_agents"):
+            a.step(bad)
+    assert a.clock == 0
+    assert np.array_equal(a.gather_exposure(g), b.gather_exposure(g))
+    assert np.array_equal(a.gather_exposure(g), tr.hazard(0)) if tr.hazard(0) is not None else True
+
+
 def test_star_graph_gather_equals_formula():
     from paper_2110_04421_b200.disease import edge_hazard
     tr = Trajectory("noiv")
