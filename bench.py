@@ -810,8 +810,8 @@ def run_refnet(a):
         "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": REFNET_DESC, "step": "one 180-step replication (GpuRealizer + "
-                   "GpuEngine resident, records on the device, one host sync per step for the "
-                   "realized edge count)",
+                   "GpuEngine resident, records and edge counts on the device, no host sync "
+                   "inside the 180 steps: the realizer's count feeds the graph load)",
                    "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
                    "l2": "not flushed; every step regenerates the graphs (> L2 traffic per step)"},
         "wall_s_per_sim": ms / a.steps / 1e3,

@@ -213,6 +213,14 @@ int epi_uniforms(uint64_t seed, int32_t step, int32_t purpose, const int64_t *id
 int epi_graph_load(epi_ctx *ctx, const int32_t *src, const int32_t *dst,
                    const int8_t *kind, int64_t n_edges, void *stream);
 
+/* epi_graph_load for a device-side producer: the first *count (device
+ * uint64) of the `capacity` entries are the edges; no host synchronisation
+ * (the rest of the buffer is ignored).  Not with exposure notification (the
+ * contact log needs the host count). */
+int epi_graph_load_counted(epi_ctx *ctx, const int32_t *src, const int32_t *dst,
+                           const int8_t *kind, const uint64_t *count, int64_t capacity,
+                           void *stream);
+
 /* Hazard per agent over the loaded graph at `step` (engine.py:77-117).
  * precision EPI_F64_CANONICAL writes double[N] bitwise equal to the
  * reference; EPI_F32 writes float[N]. */
@@ -399,6 +407,11 @@ int epi_refnet_destroy(epi_refnet_t *net);
 int epi_refnet_realize(epi_refnet_t *net, uint64_t seed, int32_t step, const uint8_t *dead,
                        int32_t *src, int32_t *dst, int8_t *kind, int64_t capacity,
                        int64_t *n_edges, void *stream);
+/* The same without synchronising: count[0] = edges, count[1] = error bits
+ * (1 capacity, 2 dedupe table, 4 stub overflow), both device uint64. */
+int epi_refnet_realize_counted(epi_refnet_t *net, uint64_t seed, int32_t step, const uint8_t *dead,
+                               int32_t *src, int32_t *dst, int8_t *kind, int64_t capacity,
+                               uint64_t *count, void *stream);
 
 #ifdef __cplusplus
 }

@@ -108,6 +108,7 @@ _SIGS = {
     "epi_struct_size": (_i64, [_i32]),
     "epi_uniforms": (_i32, [_u64, _i32, _i32, _p, _i64, _i32, _p, _p]),
     "epi_graph_load": (_i32, [_p, _p, _p, _p, _i64, _p]),
+    "epi_graph_load_counted": (_i32, [_p, _p, _p, _p, _p, _i64, _p]),
     "epi_gather": (_i32, [_p, C.POINTER(EpiState), _i32, _i32, _p, _p]),
     "epi_step": (_i32, [_p, C.POINTER(EpiState), _i32, _u64, _p, _p, _p, _i32, _p]),
     "epi_step_with_hazard": (_i32, [_p, C.POINTER(EpiState), _i32, _u64, _p, _p, _p, _p, _p]),
@@ -124,6 +125,7 @@ _SIGS = {
     "epi_refnet_create": (_i32, [C.POINTER(EpiRefnetDesc), C.POINTER(_p)]),
     "epi_refnet_destroy": (_i32, [_p]),
     "epi_refnet_realize": (_i32, [_p, _u64, _i32, _p, _p, _p, _p, _i64, C.POINTER(_i64), _p]),
+    "epi_refnet_realize_counted": (_i32, [_p, _u64, _i32, _p, _p, _p, _p, _i64, _p, _p]),
     "epi_net_csr": (_i32, [_p, _i32, C.POINTER(_p), C.POINTER(_p)]),
     "epi_seed_infections": (_i32, [_p, C.POINTER(EpiState), _u64, _p, _i64, _p]),
     "epi_assign_app": (_i32, [C.POINTER(EpiState), _u64, _d, _p]),

@@ -460,8 +460,24 @@ int epi_uniforms(uint64_t seed, int32_t step, int32_t purpose, const int64_t* id
   return 0;
 }
 
+static int graph_load_impl(epi_ctx* c, const int32_t* src, const int32_t* dst, const int8_t* kind, int64_t E,
+                           const unsigned long long* count, void* stream);
+
 int epi_graph_load(epi_ctx* c, const int32_t* src, const int32_t* dst, const int8_t* kind,
                    int64_t E, void* stream) {
+  return graph_load_impl(c, src, dst, kind, E, nullptr, stream);
+}
+
+int epi_graph_load_counted(epi_ctx* c, const int32_t* src, const int32_t* dst, const int8_t* kind,
+                           const uint64_t* count, int64_t capacity, void* stream) {
+  if (!count) return fail(EPI_EARG, "null count");
+  if (c && c->host.den_enabled)
+    return fail(EPI_EARG, "a device-counted graph cannot feed the exposure-notification contact log");
+  return graph_load_impl(c, src, dst, kind, capacity, (const unsigned long long*)count, stream);
+}
+
+static int graph_load_impl(epi_ctx* c, const int32_t* src, const int32_t* dst, const int8_t* kind, int64_t E,
+                           const unsigned long long* count, void* stream) {
   if (!c || E < 0) return fail(EPI_EARG, "bad argument");
   cudaStream_t s = S(stream);
   c->n_edges = E;
@@ -480,7 +496,7 @@ int epi_graph_load(epi_ctx* c, const int32_t* src, const int32_t* dst, const int
   }
   int sb = 1;
   while ((1ll << sb) < c->n) ++sb;
-  k_coo_keys<<<grid_for(E, 256), 256, 0, s>>>(src, dst, kind, E, c->n, sb, c->keys_in, c->gflags);
+  k_coo_keys<<<grid_for(E, 256), 256, 0, s>>>(src, dst, kind, E, c->n, sb, c->keys_in, c->gflags, count);
   CKL();
   const int end_bit = 2 * sb + 2;
   size_t need = 0;
@@ -1548,9 +1564,26 @@ int epi_refnet_destroy(epi_refnet_t* r) {
   return 0;
 }
 
+static int refnet_realize_impl(epi_refnet_t* r, uint64_t seed, int32_t step, const uint8_t* dead, int32_t* src,
+                               int32_t* dst, int8_t* kind, int64_t capacity, int64_t* n_edges, uint64_t* count_dev,
+                               void* stream);
+
 int epi_refnet_realize(epi_refnet_t* r, uint64_t seed, int32_t step, const uint8_t* dead, int32_t* src,
                        int32_t* dst, int8_t* kind, int64_t capacity, int64_t* n_edges, void* stream) {
-  if (!r || !dead || !src || !dst || !kind || !n_edges) return fail(EPI_EARG, "null argument");
+  if (!n_edges) return fail(EPI_EARG, "null argument");
+  return refnet_realize_impl(r, seed, step, dead, src, dst, kind, capacity, n_edges, nullptr, stream);
+}
+
+int epi_refnet_realize_counted(epi_refnet_t* r, uint64_t seed, int32_t step, const uint8_t* dead, int32_t* src,
+                               int32_t* dst, int8_t* kind, int64_t capacity, uint64_t* count, void* stream) {
+  if (!count) return fail(EPI_EARG, "null argument");
+  return refnet_realize_impl(r, seed, step, dead, src, dst, kind, capacity, nullptr, count, stream);
+}
+
+static int refnet_realize_impl(epi_refnet_t* r, uint64_t seed, int32_t step, const uint8_t* dead, int32_t* src,
+                               int32_t* dst, int8_t* kind, int64_t capacity, int64_t* n_edges, uint64_t* count_dev,
+                               void* stream) {
+  if (!r || !dead || !src || !dst || !kind) return fail(EPI_EARG, "null argument");
   cudaStream_t s = S(stream);
   RefScratch S = r->sc;
   S.out_src = src;
@@ -1581,6 +1614,10 @@ int epi_refnet_realize(epi_refnet_t* r, uint64_t seed, int32_t step, const uint8
   CKL();
   k_ref_pairs<1><<<grid_for(n * 4, 256), 256, 0, s>>>(r->net, S, K);
   CKL();
+  if (count_dev) {                          // no synchronisation: count + error bits stay on the device
+    CK(cudaMemcpyAsync(count_dev, S.counter, 2 * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
+    return 0;
+  }
   unsigned long long h[2] = {0, 0};
   CK(cudaMemcpyAsync(h, S.counter, sizeof(h), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));

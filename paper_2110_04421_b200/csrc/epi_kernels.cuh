@@ -361,12 +361,20 @@ __global__ void k_codes(const epi_params* __restrict__ P, epi_state st, int step
 // instead of 7 with dst in the high word).  An edge with an index outside
 // [0, n) (flagged, the load is rejected) gets the all-ones key: it sorts last
 // and the row pass skips it, so nothing is written out of bounds.
+// `count` (device, nullable): only the first *count of the E entries are
+// edges (a device-side producer's count); the rest get the all-ones key.
 __global__ void k_coo_keys(const int32_t* __restrict__ src, const int32_t* __restrict__ dst,
                            const int8_t* __restrict__ kind, int64_t E, int64_t n, int sb,
-                           uint64_t* __restrict__ keys, long long* flag_word) {
+                           uint64_t* __restrict__ keys, long long* flag_word,
+                           const unsigned long long* __restrict__ count = nullptr) {
   unsigned fl = 0;
+  const int64_t live = count ? (int64_t)(*count < (unsigned long long)E ? *count : (unsigned long long)E) : E;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < E;
        i += (int64_t)gridDim.x * blockDim.x) {
+    if (i >= live) {
+      keys[i] = ~0ull;
+      continue;
+    }
     const int32_t s = src[i], d = dst[i];
     const int k = kind[i];
     const bool bad = s < 0 || d < 0 || s >= n || d >= n;

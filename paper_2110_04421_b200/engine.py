@@ -240,6 +240,22 @@ class GpuEngine:
             self.contact_log._pushed()
         self.clock += 1
 
+    def advance_counted(self, step: int, src, dst, kind, count, record) -> None:
+        """`advance` for a device-side edge producer: the first count[0]
+        (device uint64) entries of the device arrays src/dst/kind are the
+        step's edges — no host synchronisation at all (a realizer loop can be
+        captured in a CUDA graph).  Graph flags accumulate as in advance()."""
+        if step != self.clock:
+            raise InvariantViolation(f"graph built for step {step}, engine clock is {self.clock}")
+        if not self.resident:
+            raise InvariantViolation("advance_counted() needs resident=True")
+        N.check(self._lib.epi_graph_load_counted(self._ctx, N.ptr(src), N.ptr(dst), N.ptr(kind), N.ptr(count),
+                                                 int(src.shape[0]), N.stream_handle()))
+        st = self.dev.struct()
+        N.check(self._lib.epi_step(self._ctx, C_ref(st), int(self.clock), _u64(self.seed),
+                                   N.ptr(record), N.ptr(self._vax), None, 0, N.stream_handle()))
+        self.clock += 1
+
     def step_with_hazard(self, hazard, injected=None) -> StepEvents:
         """Phases 1-6 with a caller-supplied float64 hazard (parity tests)."""
         import torch

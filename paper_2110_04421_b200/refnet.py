@@ -106,6 +106,20 @@ class GpuRealizer:
             self._lib.epi_refnet_destroy(h)
             self._h = None
 
+    def realize_counted(self, step: int, dead, count) -> None:
+        """Edges of `step` into the realizer's buffers (src/dst/kind views:
+        `buffers()`) without synchronising: count = device uint64[2] (edges,
+        error bits 1 capacity / 2 dedupe table / 4 stub overflow)."""
+        import torch
+        dead_t = dead.to(device=self.device, dtype=torch.uint8).contiguous()
+        self._dead_keep = dead_t
+        N.check(self._lib.epi_refnet_realize_counted(self._h, _u64(self.seed), int(step), N.ptr(dead_t),
+                                                     N.ptr(self._src), N.ptr(self._dst), N.ptr(self._kind),
+                                                     self.capacity, N.ptr(count), N.stream_handle()))
+
+    def buffers(self):
+        return self._src, self._dst, self._kind
+
     def realize(self, step: int, dead, copy: bool = True) -> StepGraph:
         """Edges of `step` for the given dead mask (bool[N], numpy or torch).
         copy=False returns views of the realizer's buffers, valid until the

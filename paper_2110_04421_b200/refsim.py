@@ -19,9 +19,12 @@ from __future__ import annotations
 
 import time
 
+import numpy as np
+
 from . import _native as N
 from .defaults import default_disease, default_progression
 from .engine import GpuEngine, StepEvents
+from .errors import ConfigError
 from .interventions import InterventionConfig
 from .keyed import replication_seed
 from .population import PopulationSpec, choose_seeds, synthesize
@@ -72,15 +75,28 @@ class ReferenceNativeSimulation:
         return ev
 
     def run(self, steps: int | None = None):
-        """The remaining steps with the state and the records on the device:
-        one host synchronisation per step (the realized edge count the sort
-        needs); graph flags checked once at the end.  Returns the StepEvents."""
+        """The remaining steps with the state, the edge counts and the records
+        on the device and no host synchronisation inside the loop (the
+        realizer's edge count goes to the graph load on the device); graph
+        flags and realizer errors checked once at the end.  Returns the
+        StepEvents."""
+        import torch
         first = self.clock
         last = self.horizon if steps is None else min(self.horizon, first + steps)
+        counts = torch.zeros((max(last - first, 1), 2), dtype=torch.int64, device=self.engine.device)
+        src, dst, kind = self.realizer.buffers()
         for t in range(first, last):
             dead = self.engine.dev.t["stage"] == 10
-            self.engine.advance(self.realizer.realize(t, dead, copy=False), self.records[t])
+            self.realizer.realize_counted(t, dead, counts[t - first])
+            self.engine.advance_counted(t, src, dst, kind, counts[t - first], self.records[t])
         self.engine.check_graph_flags()
+        err = int(np.bitwise_or.reduce(counts[:, 1].cpu().numpy()))
+        if err & 1:
+            raise ConfigError("edge output capacity exceeded")
+        if err & 2:
+            raise ConfigError("dedupe hash table full")
+        if err & 4:
+            raise ConfigError("more than 2^31 random-network stubs")
         rec = self.records[first:last].cpu().numpy()
         events = [StepEvents.from_record(r) for r in rec]
         self.interactions += sum(ev.n_edges for ev in events)
