@@ -142,10 +142,11 @@ struct epi_ctx {
   uint16_t* codes = nullptr;         // graph-in codes
   // graph-in CSR
   int64_t edge_cap = 0, n_edges = 0;
-  uint64_t *keys_in = nullptr, *keys_out = nullptr;
   uint32_t* entries = nullptr;
   int64_t* row_begin = nullptr;
   int32_t* row_len = nullptr;
+  int32_t* row_fill = nullptr;       // graph load: per-row scatter cursors
+  int64_t* row_len64 = nullptr;      // graph load: row lengths widened for the scan
   void* cub_tmp = nullptr;
   size_t cub_bytes = 0;
   const int32_t *g_src = nullptr, *g_dst = nullptr;   // current graph (device, caller-owned)
@@ -400,11 +401,11 @@ int epi_destroy(epi_ctx* c) {
   cudaFree(c->scratch_rec);
   cudaFree(c->gflags);
   cudaFree(c->codes);
-  cudaFree(c->keys_in);
-  cudaFree(c->keys_out);
   cudaFree(c->entries);
   cudaFree(c->row_begin);
   cudaFree(c->row_len);
+  cudaFree(c->row_fill);
+  cudaFree(c->row_len64);
   cudaFree(c->cub_tmp);
   cudaFree(c->net_dev);
   cudaFree(c->inj_dev);
@@ -488,30 +489,34 @@ static int graph_load_impl(epi_ctx* c, const int32_t* src, const int32_t* dst, c
   if (E == 0) return 0;
   if (E > c->edge_cap) {
     int64_t cap = E + E / 4;
-    int rc = dalloc(&c->keys_in, cap);
-    if (!rc) rc = dalloc(&c->keys_out, cap);
-    if (!rc) rc = dalloc(&c->entries, cap);
+    int rc = dalloc(&c->entries, cap);
     if (rc) return rc;
     c->edge_cap = cap;
   }
-  int sb = 1;
-  while ((1ll << sb) < c->n) ++sb;
-  k_coo_keys<<<grid_for(E, 256), 256, 0, s>>>(src, dst, kind, E, c->n, sb, c->keys_in, c->gflags, count);
+  // counting sort by destination + per-row sorts (canonical order)
+  if (!c->row_fill) {
+    int rc = dalloc(&c->row_fill, (size_t)c->n);
+    if (!rc) rc = dalloc(&c->row_len64, (size_t)c->n);
+    if (rc) return rc;
+  }
+  CK(cudaMemsetAsync(c->row_fill, 0, c->n * sizeof(int32_t), s));
+  k_coo_count<<<grid_for(E, 256), 256, 0, s>>>(src, dst, kind, E, c->n, c->row_len, c->gflags, count);
   CKL();
-  const int end_bit = 2 * sb + 2;
+  k_widen<<<grid_for(c->n, 256), 256, 0, s>>>(c->row_len, c->n, c->row_len64);
+  CKL();
   size_t need = 0;
-  CK(cub::DeviceRadixSort::SortKeys(nullptr, need, c->keys_in, c->keys_out, (int)E, 0, end_bit, s));
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, need, c->row_len64, c->row_begin, (int)c->n, s));
   if (need > c->cub_bytes) {
     cudaFree(c->cub_tmp);
     c->cub_tmp = nullptr;
     CK(cudaMalloc(&c->cub_tmp, need));
     c->cub_bytes = need;
   }
-  CK(cub::DeviceRadixSort::SortKeys(c->cub_tmp, need, c->keys_in, c->keys_out, (int)E, 0, end_bit, s));
-  k_rows_from_sorted<<<grid_for(E, 256), 256, 0, s>>>(c->keys_out, E, sb, c->n, c->row_begin, c->row_len,
-                                                      c->entries);
+  CK(cub::DeviceScan::ExclusiveSum(c->cub_tmp, need, c->row_len64, c->row_begin, (int)c->n, s));
+  k_coo_scatter<<<grid_for(E, 256), 256, 0, s>>>(src, dst, kind, E, c->n, c->row_begin, c->row_fill, c->entries,
+                                                 count);
   CKL();
-  k_rows_finish<<<grid_for(c->n, 256), 256, 0, s>>>(c->n, c->row_begin, c->row_len);
+  k_rows_sort<<<grid_for(c->n, 128), 128, 0, s>>>(c->n, c->row_begin, c->row_len, c->entries);
   CKL();
   return 0;
 }

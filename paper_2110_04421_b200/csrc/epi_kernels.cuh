@@ -356,63 +356,60 @@ __global__ void k_codes(const epi_params* __restrict__ P, epi_state st, int step
 
 // ---------------------------------------------------------------------------
 // Graph-in: COO -> sort keys (dst << 32 | src << 2 | kind) + validation.
-// Keys packed into 2 sb + 2 bits (n <= 2^sb): dst << (sb + 2) | src << 2 |
-// kind, so the radix sort runs ceil((2 sb + 2) / 8) passes (5 at 100 k agents
-// instead of 7 with dst in the high word).  An edge with an index outside
-// [0, n) (flagged, the load is rejected) gets the all-ones key: it sorts last
-// and the row pass skips it, so nothing is written out of bounds.
-// `count` (device, nullable): only the first *count of the E entries are
-// edges (a device-side producer's count); the rest get the all-ones key.
-__global__ void k_coo_keys(const int32_t* __restrict__ src, const int32_t* __restrict__ dst,
-                           const int8_t* __restrict__ kind, int64_t E, int64_t n, int sb,
-                           uint64_t* __restrict__ keys, long long* flag_word,
-                           const unsigned long long* __restrict__ count = nullptr) {
+
+// Row bounds of the sorted keys; entries = low 32 bits (src << 2 | kind).
+// Canonical CSR by counting sort (graph load): edges counted per
+// destination, rows placed by an exclusive scan, entries scattered, then each
+// row sorted by (src, kind) — the (dst, src, kind) order of np.lexsort
+// (engine.py:98) without a full radix sort of the edge keys.  Equal entries
+// are identical values, so the result does not depend on the scatter order.
+__global__ void k_coo_count(const int32_t* __restrict__ src, const int32_t* __restrict__ dst,
+                            const int8_t* __restrict__ kind, int64_t E, int64_t n,
+                            int32_t* __restrict__ row_len, long long* flag_word,
+                            const unsigned long long* __restrict__ count) {
   unsigned fl = 0;
   const int64_t live = count ? (int64_t)(*count < (unsigned long long)E ? *count : (unsigned long long)E) : E;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < E;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < live;
        i += (int64_t)gridDim.x * blockDim.x) {
-    if (i >= live) {
-      keys[i] = ~0ull;
-      continue;
-    }
     const int32_t s = src[i], d = dst[i];
     const int k = kind[i];
     const bool bad = s < 0 || d < 0 || s >= n || d >= n;
     if (bad) fl |= EPI_FLAG_INDEX;
     if (s == d) fl |= EPI_FLAG_SELFLOOP;
     if (k < 0 || k > 2) fl |= EPI_FLAG_KIND;
-    keys[i] = bad ? ~0ull : ((uint64_t)d << (sb + 2)) | ((uint64_t)s << 2) | (uint64_t)(k & 3);
+    if (!bad) atomicAdd(&row_len[d], 1);
   }
   if (fl) atomicOr((unsigned long long*)flag_word, (unsigned long long)fl);
 }
-
-// Row bounds of the sorted keys; entries = low 32 bits (src << 2 | kind).
-__global__ void k_rows_from_sorted(const uint64_t* __restrict__ keys, int64_t E, int sb, int64_t n,
-                                   int64_t* __restrict__ row_begin, int32_t* __restrict__ row_len,
-                                   uint32_t* __restrict__ entries) {
-  const int shift = sb + 2;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < E;
+__global__ void k_coo_scatter(const int32_t* __restrict__ src, const int32_t* __restrict__ dst,
+                              const int8_t* __restrict__ kind, int64_t E, int64_t n,
+                              const int64_t* __restrict__ row_begin, int32_t* __restrict__ fill,
+                              uint32_t* __restrict__ entries, const unsigned long long* __restrict__ count) {
+  const int64_t live = count ? (int64_t)(*count < (unsigned long long)E ? *count : (unsigned long long)E) : E;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < live;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const uint64_t k = keys[i];
-    const int64_t d = (int64_t)(k >> shift);
-    if (d >= n) continue;                  // a rejected edge (all-ones key)
-    entries[i] = (uint32_t)(k & ((1ull << shift) - 1));
-    if (i == 0 || (int64_t)(keys[i - 1] >> shift) != d) row_begin[d] = i;
-    if (i == E - 1 || (int64_t)(keys[i + 1] >> shift) != d) {
-      // length = i + 1 - begin; begin may be written by another thread, so
-      // compute it by scanning back is avoided: store end, fix up later
-      row_len[d] = (int32_t)(i + 1);   // temporarily the row end
+    const int32_t s = src[i], d = dst[i];
+    if (s < 0 || d < 0 || s >= n || d >= n) continue;
+    const int64_t pos = row_begin[d] + atomicAdd(&fill[d], 1);
+    entries[pos] = ((uint32_t)s << 2) | (uint32_t)(kind[i] & 3);
+  }
+}
+// one thread per row, insertion sort in place (rows are short: ~11 entries
+// per agent on the reference networks)
+__global__ void k_rows_sort(int64_t n, const int64_t* __restrict__ row_begin, const int32_t* __restrict__ row_len,
+                            uint32_t* __restrict__ entries) {
+  for (int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; d < n; d += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t* row = entries + row_begin[d];
+    const int len = row_len[d];
+    for (int i = 1; i < len; ++i) {
+      const uint32_t x = row[i];
+      int j = i - 1;
+      while (j >= 0 && row[j] > x) { row[j + 1] = row[j]; --j; }
+      row[j + 1] = x;
     }
   }
 }
-__global__ void k_rows_finish(int64_t n, const int64_t* __restrict__ row_begin,
-                              int32_t* __restrict__ row_len) {
-  for (int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; d < n;
-       d += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t end = row_len[d];
-    row_len[d] = end ? (int32_t)(end - row_begin[d]) : 0;
-  }
-}
+
 
 // ---------------------------------------------------------------------------
 // Gather / fused gather + update over a CSR given either by explicit
