@@ -6,6 +6,8 @@
 // the per-step padded CSR ring of an attached config network.
 #include <cub/device/device_radix_sort.cuh>
 
+#include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -462,7 +464,7 @@ int epi_uniforms(uint64_t seed, int32_t step, int32_t purpose, const int64_t* id
 }
 
 static int graph_load_impl(epi_ctx* c, const int32_t* src, const int32_t* dst, const int8_t* kind, int64_t E,
-                           const unsigned long long* count, void* stream);
+                           const unsigned long long* count, void* stream, bool rows_counted = false);
 
 int epi_graph_load(epi_ctx* c, const int32_t* src, const int32_t* dst, const int8_t* kind,
                    int64_t E, void* stream) {
@@ -477,16 +479,21 @@ int epi_graph_load_counted(epi_ctx* c, const int32_t* src, const int32_t* dst, c
   return graph_load_impl(c, src, dst, kind, capacity, (const unsigned long long*)count, stream);
 }
 
+// rows_counted: row_len already holds the in-edges per destination of the
+// first min(*count, E) edges, all valid (a device generator wrote them).
 static int graph_load_impl(epi_ctx* c, const int32_t* src, const int32_t* dst, const int8_t* kind, int64_t E,
-                           const unsigned long long* count, void* stream) {
+                           const unsigned long long* count, void* stream, bool rows_counted) {
   if (!c || E < 0) return fail(EPI_EARG, "bad argument");
   cudaStream_t s = S(stream);
   c->n_edges = E;
   c->g_src = src;
   c->g_dst = dst;
-  CK(cudaMemsetAsync(c->row_len, 0, c->n * sizeof(int32_t), s));
-  CK(cudaMemsetAsync(c->row_begin, 0, c->n * sizeof(int64_t), s));
-  if (E == 0) return 0;
+  if (!rows_counted) CK(cudaMemsetAsync(c->row_len, 0, c->n * sizeof(int32_t), s));
+  if (E == 0) {
+    CK(cudaMemsetAsync(c->row_len, 0, c->n * sizeof(int32_t), s));
+    CK(cudaMemsetAsync(c->row_begin, 0, c->n * sizeof(int64_t), s));
+    return 0;
+  }
   if (E > c->edge_cap) {
     int64_t cap = E + E / 4;
     int rc = dalloc(&c->entries, cap);
@@ -499,10 +506,11 @@ static int graph_load_impl(epi_ctx* c, const int32_t* src, const int32_t* dst, c
     if (!rc) rc = dalloc(&c->row_len64, (size_t)c->n);
     if (rc) return rc;
   }
-  CK(cudaMemsetAsync(c->row_fill, 0, c->n * sizeof(int32_t), s));
-  k_coo_count<<<grid_for(E, 256), 256, 0, s>>>(src, dst, kind, E, c->n, c->row_len, c->gflags, count);
-  CKL();
-  k_widen<<<grid_for(c->n, 256), 256, 0, s>>>(c->row_len, c->n, c->row_len64);
+  if (!rows_counted) {
+    k_coo_count<<<grid_for(E, 256), 256, 0, s>>>(src, dst, kind, E, c->n, c->row_len, c->gflags, count);
+    CKL();
+  }
+  k_widen_clear<<<grid_for(c->n, 256), 256, 0, s>>>(c->row_len, c->n, c->row_len64, c->row_fill);
   CKL();
   size_t need = 0;
   CK(cub::DeviceScan::ExclusiveSum(nullptr, need, c->row_len64, c->row_begin, (int)c->n, s));
@@ -1509,6 +1517,7 @@ struct epi_refnet_t {
   RefNet net{};
   RefScratch sc{};
   int64_t n_member_slots = 0;
+  int ws_blocks = 1;            // blocks per occupation: the largest lattice / 256
   void* scan_tmp = nullptr;
   size_t scan_bytes = 0;
 };
@@ -1539,6 +1548,29 @@ int epi_refnet_create(const epi_refnet_desc* d, epi_refnet_t** out) {
   if (!rc) rc = dalloc(&S.counter, 2);
   S.table_slots = d->table_slots;
   r->n_member_slots = d->n_member_slots;
+  if (!rc) {   // one-time host reads: the stub bound and the largest lattice
+    std::vector<double> deg((size_t)d->n_agents);
+    std::vector<int32_t> occ_start((size_t)d->n_occ + 1), occ_k((size_t)d->n_occ + 1);
+    if (cudaMemcpy(deg.data(), d->random_degree, deg.size() * sizeof(double), cudaMemcpyDeviceToHost) !=
+            cudaSuccess ||
+        (d->n_occ > 0 &&
+         (cudaMemcpy(occ_start.data(), d->occ_start, ((size_t)d->n_occ + 1) * sizeof(int32_t),
+                     cudaMemcpyDeviceToHost) != cudaSuccess ||
+          cudaMemcpy(occ_k.data(), d->occ_k, (size_t)d->n_occ * sizeof(int32_t), cudaMemcpyDeviceToHost) !=
+              cudaSuccess))) {
+      rc = fail(EPI_ECUDA, "descriptor read");
+    } else {
+      int64_t stubs = 0;
+      for (double x : deg) stubs += (int64_t)std::ceil(x > 0 ? x : 0.0);
+      S.max_stubs = stubs;
+      int64_t most = 0;
+      for (int j = 0; j < d->n_occ; ++j)
+        most = std::max(most, (int64_t)(occ_start[j + 1] - occ_start[j]) * std::max(occ_k[j] / 2, 0));
+      r->ws_blocks = (int)std::min<int64_t>(std::max<int64_t>((most + 255) / 256, 1), 1024);
+      rc = dalloc(&S.stub_owner, (size_t)stubs + 1);
+      if (!rc) rc = dalloc(&S.pair_uv, (size_t)(stubs / 2) + 1);
+    }
+  }
   if (!rc) {
     size_t need = 0;
     if (cub::DeviceScan::ExclusiveSum(nullptr, need, S.stub_count, S.stub_off, (int)(d->n_agents + 1)) !=
@@ -1564,6 +1596,8 @@ int epi_refnet_destroy(epi_refnet_t* r) {
   cudaFree(r->sc.stub_off);
   cudaFree(r->sc.table);
   cudaFree(r->sc.counter);
+  cudaFree(r->sc.stub_owner);
+  cudaFree(r->sc.pair_uv);
   cudaFree(r->scan_tmp);
   delete r;
   return 0;
@@ -1571,7 +1605,7 @@ int epi_refnet_destroy(epi_refnet_t* r) {
 
 static int refnet_realize_impl(epi_refnet_t* r, uint64_t seed, int32_t step, const uint8_t* dead, int32_t* src,
                                int32_t* dst, int8_t* kind, int64_t capacity, int64_t* n_edges, uint64_t* count_dev,
-                               void* stream);
+                               void* stream, int32_t* row_len = nullptr, bool counter_zeroed = false);
 
 int epi_refnet_realize(epi_refnet_t* r, uint64_t seed, int32_t step, const uint8_t* dead, int32_t* src,
                        int32_t* dst, int8_t* kind, int64_t capacity, int64_t* n_edges, void* stream) {
@@ -1587,7 +1621,7 @@ int epi_refnet_realize_counted(epi_refnet_t* r, uint64_t seed, int32_t step, con
 
 static int refnet_realize_impl(epi_refnet_t* r, uint64_t seed, int32_t step, const uint8_t* dead, int32_t* src,
                                int32_t* dst, int8_t* kind, int64_t capacity, int64_t* n_edges, uint64_t* count_dev,
-                               void* stream) {
+                               void* stream, int32_t* row_len, bool counter_zeroed) {
   if (!r || !dead || !src || !dst || !kind) return fail(EPI_EARG, "null argument");
   cudaStream_t s = S(stream);
   RefScratch S = r->sc;
@@ -1595,34 +1629,29 @@ static int refnet_realize_impl(epi_refnet_t* r, uint64_t seed, int32_t step, con
   S.out_dst = dst;
   S.out_kind = kind;
   S.capacity = capacity;
+  S.row_len = row_len;
   const int64_t n = r->net.n_agents;
-  CK(cudaMemsetAsync(S.counter, 0, 2 * sizeof(unsigned long long), s));
-  CK(cudaMemsetAsync(S.table, 0xFF, (size_t)S.table_slots * 2 * sizeof(unsigned long long), s));
-  k_ref_households<<<grid_for(n, 256), 256, 0, s>>>(r->net, dead, S);
-  CKL();
-  if (r->net.n_occ > 0) {
-    k_ref_occ_live<<<r->net.n_occ, 256, 0, s>>>(r->net, dead, S);
-    CKL();
-    const uint64_t ws = key_prefix(seed, step, P_REF_WS);
-    const dim3 g(8, r->net.n_occ);
-    k_ref_ws<0><<<g, 256, 0, s>>>(r->net, S, ws);
-    CKL();
-    k_ref_ws<1><<<g, 256, 0, s>>>(r->net, S, ws);
-    CKL();
-  }
-  k_ref_stub_count<<<grid_for(n, 256), 256, 0, s>>>(r->net, dead, S, key_prefix(seed, step, P_REF_STUB));
+  if (count_dev) S.counter = (unsigned long long*)count_dev;   // counted mode: the caller's words are the counter
+  if (!counter_zeroed) CK(cudaMemsetAsync(S.counter, 0, 2 * sizeof(unsigned long long), s));
+  // 1: households + stub counts (+ table clear)
+  k_ref_agents<<<grid_for(std::max<int64_t>(n, S.table_slots), 256), 256, 0, s>>>(
+      r->net, dead, S, key_prefix(seed, step, P_REF_STUB));
   CKL();
   size_t bytes = r->scan_bytes;
   CK(cub::DeviceScan::ExclusiveSum(r->scan_tmp, bytes, S.stub_count, S.stub_off, (int)(n + 1), s));
+  // 2: alive members per occupation + stub owners
+  k_ref_occ_stubs<<<r->net.n_occ + grid_for(n, kOccLiveThreads, 2), kOccLiveThreads, 0, s>>>(r->net, dead, S);
+  CKL();
+  // 3, 4: lattices + stub pairs, inserts then winners
+  const uint64_t ws = key_prefix(seed, step, P_REF_WS);
   const PermKeys K = random_slot_keys(key_prefix(seed, step, P_REF_PERM), 0);
-  k_ref_pairs<0><<<grid_for(n * 4, 256), 256, 0, s>>>(r->net, S, K);
+  const int ws_blocks = r->net.n_occ > 0 ? r->ws_blocks : 0;
+  const int links = ws_blocks * r->net.n_occ + grid_for(S.max_stubs / 2, 256);
+  k_ref_links<0><<<links, 256, 0, s>>>(r->net, S, ws, K, ws_blocks);
   CKL();
-  k_ref_pairs<1><<<grid_for(n * 4, 256), 256, 0, s>>>(r->net, S, K);
+  k_ref_links<1><<<links, 256, 0, s>>>(r->net, S, ws, K, ws_blocks);
   CKL();
-  if (count_dev) {                          // no synchronisation: count + error bits stay on the device
-    CK(cudaMemcpyAsync(count_dev, S.counter, 2 * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s));
-    return 0;
-  }
+  if (count_dev) return 0;                  // no synchronisation: count + error bits stay on the device
   unsigned long long h[2] = {0, 0};
   CK(cudaMemcpyAsync(h, S.counter, sizeof(h), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
@@ -1630,6 +1659,38 @@ static int refnet_realize_impl(epi_refnet_t* r, uint64_t seed, int32_t step, con
   if (h[1] & 1ull) return fail(EPI_EARG, "edge output capacity exceeded");
   if (h[1] & 2ull) return fail(EPI_EARG, "dedupe hash table full");
   if (h[1] & 4ull) return fail(EPI_EARG, "more than 2^31 random-network stubs");
+  return 0;
+}
+
+// The reference's replication loop (runner.py:138-150) for steps
+// [first, last) with every step issued from here: dead mask from the stage,
+// (graph_seed = the GraphRealizer's seed, seed = the Engine's),
+// realize (counted), graph load (counted), Engine.step.  No host
+// synchronisation; counts[(t - first) * 2 + {0, 1}] = edges / realizer error
+// bits, records[(t - first) * EPI_REC_LEN ...] = the step's record.
+int epi_refnet_run(epi_refnet_t* r, epi_ctx* c, const epi_state* st, uint64_t graph_seed, uint64_t seed,
+                   int32_t first, int32_t last,
+                   uint8_t* dead, int32_t* src, int32_t* dst, int8_t* kind, int64_t capacity, uint64_t* counts,
+                   int64_t* records, int32_t* vax_open, void* stream) {
+  if (!r || !c || !st || !dead || !counts || !records) return fail(EPI_EARG, "null argument");
+  if (st->n_agents != c->n || r->net.n_agents != c->n) return fail(EPI_EARG, "state size differs from context");
+  if (c->host.den_enabled)
+    return fail(EPI_EARG, "a device-counted graph cannot feed the exposure-notification contact log");
+  if (first < 0 || last < first) return fail(EPI_EARG, "bad step range");
+  cudaStream_t s = S(stream);
+  for (int32_t t = first; t < last; ++t) {
+    uint64_t* cnt = counts + 2 * (int64_t)(t - first);
+    k_dead_mask<<<grid_for(c->n, 256), 256, 0, s>>>(st->stage, c->n, dead, (unsigned long long*)cnt);
+    CKL();
+    // the realizer counts the in-edges it writes per destination straight into
+    // the graph load's row lengths (its edges are valid by construction)
+    int rc = refnet_realize_impl(r, graph_seed, t, dead, src, dst, kind, capacity, nullptr, cnt, stream, c->row_len,
+                                 true);
+    if (!rc) rc = graph_load_impl(c, src, dst, kind, capacity, (const unsigned long long*)cnt, stream, true);
+    if (!rc) rc = step_impl(c, st, t, seed, nullptr, records + (int64_t)(t - first) * EPI_REC_LEN, vax_open, nullptr,
+                            stream);
+    if (rc) return rc;
+  }
   return 0;
 }
 

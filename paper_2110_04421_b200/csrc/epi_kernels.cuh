@@ -394,22 +394,70 @@ __global__ void k_coo_scatter(const int32_t* __restrict__ src, const int32_t* __
     entries[pos] = ((uint32_t)s << 2) | (uint32_t)(kind[i] & 3);
   }
 }
-// one thread per row, insertion sort in place (rows are short: ~11 entries
-// per agent on the reference networks)
+// Canonical row order: ascending (src << 2 | kind).  One thread per row; a
+// row of <= 32 entries is sorted in registers by a bitonic network (padding
+// ~0u sorts last; a real entry is at most (2^30 - 1) << 2 | 2), longer rows
+// (none on the reference networks at its defaults) by insertion in place.
+template <int W>
+__device__ __forceinline__ void bitonic_regs(uint32_t (&v)[W]) {
+#pragma unroll
+  for (int k = 2; k <= W; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+#pragma unroll
+      for (int i = 0; i < W; ++i) {
+        const int l = i ^ j;
+        if (l > i) {
+          const uint32_t a = v[i], b = v[l];
+          const bool up = (i & k) == 0;
+          const uint32_t lo = a < b ? a : b, hi = a < b ? b : a;
+          v[i] = up ? lo : hi;
+          v[l] = up ? hi : lo;
+        }
+      }
+    }
+  }
+}
+template <int W>
+__device__ __forceinline__ void sort_row_regs(uint32_t* row, int len) {
+  uint32_t v[W];
+#pragma unroll
+  for (int i = 0; i < W; ++i) v[i] = i < len ? row[i] : ~0u;
+  bitonic_regs<W>(v);
+#pragma unroll
+  for (int i = 0; i < W; ++i)
+    if (i < len) row[i] = v[i];
+}
 __global__ void k_rows_sort(int64_t n, const int64_t* __restrict__ row_begin, const int32_t* __restrict__ row_len,
                             uint32_t* __restrict__ entries) {
   for (int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; d < n; d += (int64_t)gridDim.x * blockDim.x) {
     uint32_t* row = entries + row_begin[d];
     const int len = row_len[d];
-    for (int i = 1; i < len; ++i) {
-      const uint32_t x = row[i];
-      int j = i - 1;
-      while (j >= 0 && row[j] > x) { row[j + 1] = row[j]; --j; }
-      row[j + 1] = x;
+    if (len <= 1) continue;
+    if (len <= 8) {
+      sort_row_regs<8>(row, len);
+    } else if (len <= 16) {
+      sort_row_regs<16>(row, len);
+    } else if (len <= 32) {
+      sort_row_regs<32>(row, len);
+    } else {
+      for (int i = 1; i < len; ++i) {
+        const uint32_t x = row[i];
+        int j = i - 1;
+        while (j >= 0 && row[j] > x) { row[j + 1] = row[j]; --j; }
+        row[j + 1] = x;
+      }
     }
   }
 }
-
+// row lengths widened for the scan; the scatter's fill counters cleared
+__global__ void k_widen_clear(const int32_t* __restrict__ a, int64_t n, int64_t* __restrict__ out,
+                              int32_t* __restrict__ fill) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    out[i] = a[i];
+    fill[i] = 0;
+  }
+}
 
 // ---------------------------------------------------------------------------
 // Gather / fused gather + update over a CSR given either by explicit

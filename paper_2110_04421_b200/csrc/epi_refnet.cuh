@@ -50,6 +50,12 @@ struct RefScratch {
   int8_t* out_kind;
   unsigned long long* counter;  // [0] = edges written, [1] = flags
   int64_t capacity;
+  int32_t* stub_owner;          // [max_stubs]: agent of every stub (stub_off order)
+  int64_t max_stubs;            // sum of ceil(random_degree): bound on the stubs of a step
+  int2* pair_uv;                // [max_stubs / 2]: owners of stub pair i (pass 0 -> pass 1)
+  int32_t* row_len;             // nullable: in-edges per destination of the edges written
+                                // (the graph load's row lengths; the households kernel
+                                // initialises every row)
 };
 
 __device__ __forceinline__ double ref_u(uint64_t prefix, uint64_t idx, uint64_t k) {
@@ -79,17 +85,37 @@ __device__ __forceinline__ void emit2(const RefScratch& S, int64_t at, int32_t u
   if (at + 2 <= S.capacity) {
     S.out_src[at] = u; S.out_dst[at] = v; S.out_kind[at] = kind;
     S.out_src[at + 1] = v; S.out_dst[at + 1] = u; S.out_kind[at + 1] = kind;
+    if (S.row_len) {
+      atomicAdd(&S.row_len[u], 1);
+      atomicAdd(&S.row_len[v], 1);
+    }
   } else {
     atomicOr(&S.counter[1], 1ull);   // overflow flag
   }
 }
 
-// Households: each alive agent b emits c -> b for its alive co-members.
-__global__ void k_ref_households(RefNet net, const uint8_t* __restrict__ dead, RefScratch S) {
+// dead[a] = stage[a] == DEAD (the realizer's input, engine state on device);
+// block 0 also zeroes the step's counter words.
+__global__ void k_dead_mask(const int8_t* __restrict__ stage, int64_t n, uint8_t* __restrict__ dead,
+                            unsigned long long* counter) {
+  if (blockIdx.x == 0 && threadIdx.x < 2) counter[threadIdx.x] = 0;
+  for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < n; a += (int64_t)gridDim.x * blockDim.x)
+    dead[a] = stage[a] == S_DEAD ? 1 : 0;
+}
+
+// Launch 1 (per agent): households — each alive agent b emits c -> b for its
+// alive co-members — and the agent's random-network stub count; the dedupe
+// table is cleared on the side (first used by launch 3).
+__global__ void k_ref_agents(RefNet net, const uint8_t* __restrict__ dead, RefScratch S, uint64_t stub_prefix) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  ulonglong2* tab = reinterpret_cast<ulonglong2*>(S.table);
+  for (int64_t i = tid; i < S.table_slots; i += stride) tab[i] = make_ulonglong2(~0ull, ~0ull);
+  if (tid == 0) S.stub_count[net.n_agents] = 0;
   for (int64_t b0 = (int64_t)blockIdx.x * blockDim.x; b0 < net.n_agents; b0 += stride) {
     const int64_t b = b0 + threadIdx.x;
-    const bool alive = b < net.n_agents && !dead[b];
+    const bool in = b < net.n_agents;
+    const bool alive = in && !dead[b];
     const int st = alive ? net.hh_start[b] : 0, sz = alive ? net.hh_size[b] : 0;
     int cnt = 0;
     for (int i = 0; i < sz; ++i) {
@@ -109,24 +135,52 @@ __global__ void k_ref_households(RefNet net, const uint8_t* __restrict__ dead, R
         ++o;
       }
     }
+    if (in) {
+      if (S.row_len) {   // edges written into row b (all of them unless the output overflowed)
+        const int64_t room = S.capacity - at;
+        S.row_len[b] = (int32_t)(room >= cnt ? cnt : (room > 0 ? room : 0));
+      }
+      int c = 0;
+      if (alive) {
+        const double d = net.random_degree[b];
+        const double fl = floor(d);
+        c = (int)fl + (ref_u(stub_prefix, (uint64_t)b, 0) < d - fl ? 1 : 0);
+      }
+      S.stub_count[b] = c;
+    }
   }
 }
 
-// Alive positions inside every occupation (one block per occupation).
-__global__ void k_ref_occ_live(RefNet net, const uint8_t* __restrict__ dead, RefScratch S) {
-  typedef cub::BlockScan<int, 256> Scan;
+// Launch 2: blocks [0, n_occ) compact the alive members of occupation j (ids
+// ascending); the remaining blocks write the owner of every stub (agent a owns
+// stubs [stub_off[a], stub_off[a+1]); stub_off is launch 1's scan).
+constexpr int kOccLiveThreads = 1024;
+__global__ void __launch_bounds__(kOccLiveThreads) k_ref_occ_stubs(RefNet net, const uint8_t* __restrict__ dead,
+                                                                   RefScratch S) {
+  if ((int)blockIdx.x >= net.n_occ) {
+    if (S.stub_off[net.n_agents] > S.max_stubs) return;   // launch 3 flags it
+    const int64_t nb = gridDim.x - net.n_occ;
+    for (int64_t a = (blockIdx.x - net.n_occ) * (int64_t)blockDim.x + threadIdx.x; a < net.n_agents;
+         a += nb * blockDim.x) {
+      const int64_t b = S.stub_off[a], e = S.stub_off[a + 1];
+      for (int64_t q = b; q < e; ++q) S.stub_owner[q] = (int32_t)a;
+    }
+    return;
+  }
+  typedef cub::BlockScan<int, kOccLiveThreads> Scan;
   __shared__ typename Scan::TempStorage tmp;
   __shared__ int carry;
   const int j = blockIdx.x;
   const int lo = net.occ_start[j], hi = net.occ_start[j + 1];
   if (threadIdx.x == 0) carry = 0;
   __syncthreads();
-  for (int b0 = lo; b0 < hi; b0 += 256) {
+  for (int b0 = lo; b0 < hi; b0 += kOccLiveThreads) {
     const int i = b0 + threadIdx.x;
-    const int alive = (i < hi && !dead[net.occ_members[i]]) ? 1 : 0;
+    const int32_t a = i < hi ? net.occ_members[i] : 0;
+    const int alive = (i < hi && !dead[a]) ? 1 : 0;
     int ex, total;
     Scan(tmp).ExclusiveSum(alive, ex, total);
-    if (alive) S.live_members[lo + carry + ex] = net.occ_members[i];
+    if (alive) S.live_members[lo + carry + ex] = a;
     __syncthreads();
     if (threadIdx.x == 0) carry += total;
     __syncthreads();
@@ -168,11 +222,11 @@ __device__ __forceinline__ int64_t table_insert(const RefScratch& S, uint64_t ke
   return -1;
 }
 
-// Watts-Strogatz lattice edges of occupation j (one block per occupation;
-// threads over edge indices).  Pass 0 inserts rewired pairs, pass 1 emits.
+// Watts-Strogatz lattice edges of occupation j, chunk `bx` of `nbx` (threads
+// over edge indices).  Pass 0 inserts rewired pairs, pass 1 emits.
 template <int PASS>
-__global__ void k_ref_ws(RefNet net, RefScratch S, uint64_t ws_prefix) {
-  const int j = blockIdx.y;
+__device__ __forceinline__ void ws_block(const RefNet& net, const RefScratch& S, uint64_t ws_prefix, int j, int bx,
+                                         int nbx) {
   const int lo = net.occ_start[j];
   const int m = S.occ_live[j];
   const int kmax = 2 * ((m - 1) / 2);
@@ -181,8 +235,8 @@ __global__ void k_ref_ws(RefNet net, RefScratch S, uint64_t ws_prefix) {
   const int half = k / 2;
   const int64_t n_edges = (int64_t)half * m;
   const int span = m - k - 1;                   // non-neighbours of a node
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t e0 = (int64_t)blockIdx.x * blockDim.x; e0 < n_edges; e0 += stride) {
+  const int64_t stride = (int64_t)nbx * blockDim.x;
+  for (int64_t e0 = (int64_t)bx * blockDim.x; e0 < n_edges; e0 += stride) {
     const int64_t e = e0 + threadIdx.x;
     bool emit = false;
     int32_t u = 0, v = 0;
@@ -209,52 +263,34 @@ __global__ void k_ref_ws(RefNet net, RefScratch S, uint64_t ws_prefix) {
   }
 }
 
-// Stub counts of alive agents.
-__global__ void k_ref_stub_count(RefNet net, const uint8_t* __restrict__ dead, RefScratch S,
-                                 uint64_t stub_prefix) {
-  for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < net.n_agents;
-       a += (int64_t)gridDim.x * blockDim.x) {
-    int c = 0;
-    if (!dead[a]) {
-      const double d = net.random_degree[a];
-      const double fl = floor(d);
-      c = (int)fl + (ref_u(stub_prefix, (uint64_t)a, 0) < d - fl ? 1 : 0);
-    }
-    S.stub_count[a] = c;
-    if (a == 0) S.stub_count[net.n_agents] = 0;
-  }
-}
-
-__device__ __forceinline__ int32_t stub_owner(const RefScratch& S, int64_t n, int64_t q) {
-  int64_t a = 0, b = n;            // largest a with stub_off[a] <= q
-  while (b - a > 1) {
-    const int64_t mid = (a + b) >> 1;
-    if (S.stub_off[mid] <= q) a = mid; else b = mid;
-  }
-  return (int32_t)a;
-}
-
-// Stub pairs: positions (2i, 2i+1) of the keyed permutation of [0, S).
+// Stub pairs: positions (2i, 2i+1) of the keyed permutation of [0, S);
+// pass 0 resolves the owners (kept for pass 1) and inserts, pass 1 emits.
 template <int PASS>
-__global__ void k_ref_pairs(RefNet net, RefScratch S, PermKeys K) {
+__device__ __forceinline__ void pairs_block(const RefNet& net, const RefScratch& S, const PermKeys& K, int64_t bx,
+                                            int64_t nbx) {
   const int64_t n_stubs = S.stub_off[net.n_agents];
-  if (n_stubs >= (1ll << 31)) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) atomicOr(&S.counter[1], 4ull);
+  if (n_stubs >= (1ll << 31) || n_stubs > S.max_stubs) {
+    if (PASS == 0 && bx == 0 && threadIdx.x == 0) atomicOr(&S.counter[1], 4ull);
     return;
   }
   if (n_stubs < 2) return;
   const Radix d = make_radix((uint32_t)n_stubs);
   const int64_t n_pairs = n_stubs / 2;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < n_pairs; i0 += stride) {
+  const int64_t stride = nbx * blockDim.x;
+  for (int64_t i0 = bx * blockDim.x; i0 < n_pairs; i0 += stride) {
     const int64_t i = i0 + threadIdx.x;
     bool emit = false;
     int32_t u = 0, v = 0;
     if (i < n_pairs) {
-      const uint32_t s0 = walk_fwd((uint32_t)(2 * i), K, d);
-      const uint32_t s1 = walk_fwd((uint32_t)(2 * i + 1), K, d);
-      u = stub_owner(S, net.n_agents, s0);
-      v = stub_owner(S, net.n_agents, s1);
+      if (PASS == 0) {
+        u = S.stub_owner[walk_fwd((uint32_t)(2 * i), K, d)];
+        v = S.stub_owner[walk_fwd((uint32_t)(2 * i + 1), K, d)];
+        S.pair_uv[i] = make_int2(u, v);
+      } else {
+        const int2 uv = S.pair_uv[i];
+        u = uv.x;
+        v = uv.y;
+      }
       if (u != v) {
         const uint64_t key = pair_key((uint32_t)u, (uint32_t)v, 2);
         if (PASS == 0) table_insert(S, key, (uint64_t)i);
@@ -266,6 +302,18 @@ __global__ void k_ref_pairs(RefNet net, RefScratch S, PermKeys K) {
       if (emit) emit2(S, at, u, v, 2);
     }
   }
+}
+
+// Launches 3 (PASS 0: inserts) and 4 (PASS 1: winners emitted): blocks
+// [0, ws_blocks * n_occ) walk the occupations' lattices (ws_blocks chunks per
+// occupation), the remaining blocks the stub pairs.
+template <int PASS>
+__global__ void k_ref_links(RefNet net, RefScratch S, uint64_t ws_prefix, PermKeys K, int ws_blocks) {
+  const int nws = ws_blocks * net.n_occ;
+  if ((int)blockIdx.x < nws)
+    ws_block<PASS>(net, S, ws_prefix, blockIdx.x / ws_blocks, blockIdx.x % ws_blocks, ws_blocks);
+  else
+    pairs_block<PASS>(net, S, K, blockIdx.x - nws, gridDim.x - nws);
 }
 
 }  // namespace epi

@@ -111,7 +111,10 @@ class GpuRealizer:
         `buffers()`) without synchronising: count = device uint64[2] (edges,
         error bits 1 capacity / 2 dedupe table / 4 stub overflow)."""
         import torch
-        dead_t = dead.to(device=self.device, dtype=torch.uint8).contiguous()
+        if dead.dtype == torch.bool and dead.device == self.device and dead.is_contiguous():
+            dead_t = dead.view(torch.uint8)          # same bytes (0/1), no conversion launch
+        else:
+            dead_t = dead.to(device=self.device, dtype=torch.uint8).contiguous()
         self._dead_keep = dead_t
         N.check(self._lib.epi_refnet_realize_counted(self._h, _u64(self.seed), int(step), N.ptr(dead_t),
                                                      N.ptr(self._src), N.ptr(self._dst), N.ptr(self._kind),

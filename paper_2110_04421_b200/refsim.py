@@ -84,11 +84,8 @@ class ReferenceNativeSimulation:
         first = self.clock
         last = self.horizon if steps is None else min(self.horizon, first + steps)
         counts = torch.zeros((max(last - first, 1), 2), dtype=torch.int64, device=self.engine.device)
-        src, dst, kind = self.realizer.buffers()
-        for t in range(first, last):
-            dead = self.engine.dev.t["stage"] == 10
-            self.realizer.realize_counted(t, dead, counts[t - first])
-            self.engine.advance_counted(t, src, dst, kind, counts[t - first], self.records[t])
+        if last > first:
+            self.engine.advance_refnet(self.realizer, first, last, counts, self.records[first:last])
         self.engine.check_graph_flags()
         err = int(np.bitwise_or.reduce(counts[:, 1].cpu().numpy()))
         if err & 1:

@@ -184,3 +184,33 @@ def test_engine_independent_edges_mode_replays_reference_oracle(name):
     for step in range(tr.horizon):
         eng.step(tr.graph(step))
         compare_state(cols, tr, step)
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_gather_canonical_order_on_skewed_rows(seed):
+    """Graph load canonical order (k_rows_sort: register networks for rows of
+    <= 8 / 16 / 32 entries, insertion beyond) on rows of 0..90 in-edges with
+    duplicates and all kinds, shuffled: fp64 hazard bitwise vs the oracle."""
+    tr = Trajectory("noiv")
+    rng = np.random.default_rng(seed)
+    n = 400
+    cols = AgentColumns.allocate(n)
+    inf = rng.random(n) < 0.5
+    cols.stage[inf] = int(Stage.MILD_SYMPTOMATIC)
+    cols.infected_at[inf] = rng.integers(0, 6, int(inf.sum()))
+    cols.next_stage[inf] = int(Stage.RECOVERED)
+    cols.next_transition_at[inf] = 10_000
+    cols.age_band[:] = rng.integers(0, 9, n)
+    lens = np.concatenate([np.arange(91), rng.integers(0, 40, n - 91)])
+    dst = np.repeat(np.arange(n, dtype=np.int32), lens)
+    src = rng.integers(0, n - 1, len(dst)).astype(np.int32)
+    src[src >= dst] += 1                                  # no self loops
+    kind = rng.integers(0, 3, len(dst)).astype(np.int8)
+    assert np.unique(np.stack([src, dst, kind]), axis=1).shape[1] < len(dst)   # duplicate edges present
+    p = rng.permutation(len(dst))
+    g = StepGraph(6, src[p], dst[p], kind[p])
+    eng = GpuEngine(cols.copy(), tr.disease, tr.table, InterventionConfig(), 0)
+    eng.clock = 6
+    want = engine_np.hazard(cols, tr.disease, 6, g, True)
+    assert np.count_nonzero(want) > n // 4
+    assert np.array_equal(eng.gather_exposure(g), want)
