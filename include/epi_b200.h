@@ -415,13 +415,14 @@ int epi_refnet_realize_counted(epi_refnet_t *net, uint64_t seed, int32_t step, c
 
 /* The replication loop of the reference (runner.py:138-150, bench
  * runner.py:282-287) for steps [first, last), issued natively with no host
- * synchronisation (graph_seed: the realizer's, seed: the engine's): per step dead[N] (u8 scratch) = stage == DEAD, realize
- * into src/dst/kind (counted), load, epi_step.  counts = device uint64
- * [last-first][2] (edges, realizer error bits as epi_refnet_realize_counted),
- * records = device int64[last-first][EPI_REC_LEN].  Not with exposure
- * notification (its contact log needs host-known edge counts). */
+ * synchronisation (graph_seed: the realizer's, seed: the engine's): per step
+ * realize into src/dst/kind (capacity entries; the dead agents read from
+ * st->stage), load, epi_step.  counts = device uint64[last-first][2] (edges,
+ * realizer error bits as epi_refnet_realize_counted), records = device
+ * int64[last-first][EPI_REC_LEN]; both are zeroed and filled.  Not with
+ * exposure notification (its contact log needs host-known edge counts). */
 int epi_refnet_run(epi_refnet_t *net, epi_ctx *ctx, const epi_state *st, uint64_t graph_seed,
-                   uint64_t seed, int32_t first, int32_t last, uint8_t *dead, int32_t *src, int32_t *dst,
+                   uint64_t seed, int32_t first, int32_t last, int32_t *src, int32_t *dst,
                    int8_t *kind, int64_t capacity, uint64_t *counts, int64_t *records,
                    int32_t *vax_open, void *stream);
 

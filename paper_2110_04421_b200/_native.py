@@ -126,7 +126,7 @@ _SIGS = {
     "epi_refnet_destroy": (_i32, [_p]),
     "epi_refnet_realize": (_i32, [_p, _u64, _i32, _p, _p, _p, _p, _i64, C.POINTER(_i64), _p]),
     "epi_refnet_realize_counted": (_i32, [_p, _u64, _i32, _p, _p, _p, _p, _i64, _p, _p]),
-    "epi_refnet_run": (_i32, [_p, _p, C.POINTER(EpiState), _u64, _u64, _i32, _i32, _p, _p, _p, _p, _i64, _p, _p, _p,
+    "epi_refnet_run": (_i32, [_p, _p, C.POINTER(EpiState), _u64, _u64, _i32, _i32, _p, _p, _p, _i64, _p, _p, _p,
                               _p]),
     "epi_net_csr": (_i32, [_p, _i32, C.POINTER(_p), C.POINTER(_p)]),
     "epi_seed_infections": (_i32, [_p, C.POINTER(EpiState), _u64, _p, _i64, _p]),

@@ -15,6 +15,7 @@
 #include <vector>
 
 #include <cub/device/device_scan.cuh>
+#include <cuda/std/functional>
 
 #include "epi_kernels.cuh"
 #include "epi_msgpass.cuh"
@@ -148,7 +149,6 @@ struct epi_ctx {
   int64_t* row_begin = nullptr;
   int32_t* row_len = nullptr;
   int32_t* row_fill = nullptr;       // graph load: per-row scatter cursors
-  int64_t* row_len64 = nullptr;      // graph load: row lengths widened for the scan
   void* cub_tmp = nullptr;
   size_t cub_bytes = 0;
   const int32_t *g_src = nullptr, *g_dst = nullptr;   // current graph (device, caller-owned)
@@ -407,7 +407,6 @@ int epi_destroy(epi_ctx* c) {
   cudaFree(c->row_begin);
   cudaFree(c->row_len);
   cudaFree(c->row_fill);
-  cudaFree(c->row_len64);
   cudaFree(c->cub_tmp);
   cudaFree(c->net_dev);
   cudaFree(c->inj_dev);
@@ -501,31 +500,31 @@ static int graph_load_impl(epi_ctx* c, const int32_t* src, const int32_t* dst, c
     c->edge_cap = cap;
   }
   // counting sort by destination + per-row sorts (canonical order)
-  if (!c->row_fill) {
+  if (!c->row_fill) {   // zero here, and again after every load (k_rows_sort)
     int rc = dalloc(&c->row_fill, (size_t)c->n);
-    if (!rc) rc = dalloc(&c->row_len64, (size_t)c->n);
     if (rc) return rc;
+    CK(cudaMemsetAsync(c->row_fill, 0, c->n * sizeof(int32_t), s));
   }
   if (!rows_counted) {
     k_coo_count<<<grid_for(E, 256), 256, 0, s>>>(src, dst, kind, E, c->n, c->row_len, c->gflags, count);
     CKL();
   }
-  k_widen_clear<<<grid_for(c->n, 256), 256, 0, s>>>(c->row_len, c->n, c->row_len64, c->row_fill);
-  CKL();
   size_t need = 0;
-  CK(cub::DeviceScan::ExclusiveSum(nullptr, need, c->row_len64, c->row_begin, (int)c->n, s));
+  // int32 lengths, int64 offsets: the scan accumulates in int64 (init value type)
+  CK(cub::DeviceScan::ExclusiveScan(nullptr, need, c->row_len, c->row_begin, cuda::std::plus<>{}, (int64_t)0,
+                                    (int)c->n, s));
   if (need > c->cub_bytes) {
     cudaFree(c->cub_tmp);
     c->cub_tmp = nullptr;
     CK(cudaMalloc(&c->cub_tmp, need));
     c->cub_bytes = need;
   }
-  CK(cub::DeviceScan::ExclusiveSum(c->cub_tmp, need, c->row_len64, c->row_begin, (int)c->n, s));
-  k_coo_scatter<<<grid_for(E, 256), 256, 0, s>>>(src, dst, kind, E, c->n, c->row_begin, c->row_fill, c->entries,
-                                                 count);
-  CKL();
-  k_rows_sort<<<grid_for(c->n, 128), 128, 0, s>>>(c->n, c->row_begin, c->row_len, c->entries);
-  CKL();
+  CK(cub::DeviceScan::ExclusiveScan(c->cub_tmp, need, c->row_len, c->row_begin, cuda::std::plus<>{}, (int64_t)0,
+                                    (int)c->n, s));
+  CK(launch_pdl(k_coo_scatter, dim3(grid_for(E, 256)), dim3(256), 0, s, src, dst, kind, E, c->n,
+                (const int64_t*)c->row_begin, c->row_fill, c->entries, count));
+  CK(launch_pdl(k_rows_sort, dim3(grid_for(c->n, 128)), dim3(128), 0, s, c->n, (const int64_t*)c->row_begin,
+                (const int32_t*)c->row_len, c->entries, c->row_fill));
   return 0;
 }
 
@@ -586,12 +585,12 @@ static int push_ring(epi_ctx* c, cudaStream_t s) {
 
 static int step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t seed,
                      const double* hazard, int64_t* record, int32_t* vax_open,
-                     const double* const* injected, void* stream) {
+                     const double* const* injected, void* stream, bool rec_zeroed = false) {
   if (!c || !st) return fail(EPI_EARG, "null argument");
   if (st->n_agents != c->n) return fail(EPI_EARG, "state size differs from context");
   cudaStream_t s = S(stream);
   long long* rec = record ? (long long*)record : c->scratch_rec;
-  CK(cudaMemsetAsync(rec, 0, EPI_REC_LEN * sizeof(long long), s));
+  if (!(rec_zeroed && record)) CK(cudaMemsetAsync(rec, 0, EPI_REC_LEN * sizeof(long long), s));
   const Injected* inj = nullptr;
   int rc = upload_injected(c, injected, &inj, s);
   if (rc) return rc;
@@ -601,11 +600,12 @@ static int step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t see
   if (hazard) {
     k_update_from_hazard<<<grid, 256, 0, s>>>(A, hazard, iv ? 0 : 1);
   } else {
-    k_codes<<<grid, 256, 0, s>>>(c->P, *st, step, nullptr, 0, c->codes, 0, c->n);
-    CKL();
+    CK(launch_pdl(k_codes, dim3(grid), dim3(256), 0, s, c->P, *st, step, (const epi_net*)nullptr, (uint64_t)0,
+                  c->codes, (int64_t)0, c->n, (int32_t*)nullptr, (int64_t)0));
     CsrView g{c->entries, c->row_len, c->row_begin, 0, nullptr, nullptr};
-    k_pass<true, 1><<<grid, 256, 0, s>>>(A, g, c->codes, nullptr, c->host.rate_scale, iv ? 0 : 1,
-                                         nullptr, nullptr, 0, c->msg_dev);
+    CK(launch_pdl(k_pass<true, 1>, dim3(grid), dim3(256), 0, s, A, g, (const uint16_t*)c->codes, (void*)nullptr,
+                  c->host.rate_scale, iv ? 0 : 1, (uint16_t*)nullptr, (const epi_net*)nullptr, (uint64_t)0,
+                  (const MsgTables*)c->msg_dev));
   }
   CKL();
   if (iv) {
@@ -1603,26 +1603,28 @@ int epi_refnet_destroy(epi_refnet_t* r) {
   return 0;
 }
 
-static int refnet_realize_impl(epi_refnet_t* r, uint64_t seed, int32_t step, const uint8_t* dead, int32_t* src,
+static int refnet_realize_impl(epi_refnet_t* r, uint64_t seed, int32_t step, DeadView dead, int32_t* src,
                                int32_t* dst, int8_t* kind, int64_t capacity, int64_t* n_edges, uint64_t* count_dev,
                                void* stream, int32_t* row_len = nullptr, bool counter_zeroed = false);
 
 int epi_refnet_realize(epi_refnet_t* r, uint64_t seed, int32_t step, const uint8_t* dead, int32_t* src,
                        int32_t* dst, int8_t* kind, int64_t capacity, int64_t* n_edges, void* stream) {
   if (!n_edges) return fail(EPI_EARG, "null argument");
-  return refnet_realize_impl(r, seed, step, dead, src, dst, kind, capacity, n_edges, nullptr, stream);
+  return refnet_realize_impl(r, seed, step, DeadView{(const int8_t*)dead, 1}, src, dst, kind, capacity, n_edges,
+                             nullptr, stream);
 }
 
 int epi_refnet_realize_counted(epi_refnet_t* r, uint64_t seed, int32_t step, const uint8_t* dead, int32_t* src,
                                int32_t* dst, int8_t* kind, int64_t capacity, uint64_t* count, void* stream) {
   if (!count) return fail(EPI_EARG, "null argument");
-  return refnet_realize_impl(r, seed, step, dead, src, dst, kind, capacity, nullptr, count, stream);
+  return refnet_realize_impl(r, seed, step, DeadView{(const int8_t*)dead, 1}, src, dst, kind, capacity, nullptr,
+                             count, stream);
 }
 
-static int refnet_realize_impl(epi_refnet_t* r, uint64_t seed, int32_t step, const uint8_t* dead, int32_t* src,
+static int refnet_realize_impl(epi_refnet_t* r, uint64_t seed, int32_t step, DeadView dead, int32_t* src,
                                int32_t* dst, int8_t* kind, int64_t capacity, int64_t* n_edges, uint64_t* count_dev,
                                void* stream, int32_t* row_len, bool counter_zeroed) {
-  if (!r || !dead || !src || !dst || !kind) return fail(EPI_EARG, "null argument");
+  if (!r || !dead.p || !src || !dst || !kind) return fail(EPI_EARG, "null argument");
   cudaStream_t s = S(stream);
   RefScratch S = r->sc;
   S.out_src = src;
@@ -1634,23 +1636,20 @@ static int refnet_realize_impl(epi_refnet_t* r, uint64_t seed, int32_t step, con
   if (count_dev) S.counter = (unsigned long long*)count_dev;   // counted mode: the caller's words are the counter
   if (!counter_zeroed) CK(cudaMemsetAsync(S.counter, 0, 2 * sizeof(unsigned long long), s));
   // 1: households + stub counts (+ table clear)
-  k_ref_agents<<<grid_for(std::max<int64_t>(n, S.table_slots), 256), 256, 0, s>>>(
-      r->net, dead, S, key_prefix(seed, step, P_REF_STUB));
-  CKL();
+  CK(launch_pdl(k_ref_agents, dim3(grid_for(std::max<int64_t>(n, S.table_slots), 256)), dim3(256), 0, s, r->net,
+                dead, S, key_prefix(seed, step, P_REF_STUB)));
   size_t bytes = r->scan_bytes;
   CK(cub::DeviceScan::ExclusiveSum(r->scan_tmp, bytes, S.stub_count, S.stub_off, (int)(n + 1), s));
   // 2: alive members per occupation + stub owners
-  k_ref_occ_stubs<<<r->net.n_occ + grid_for(n, kOccLiveThreads, 2), kOccLiveThreads, 0, s>>>(r->net, dead, S);
-  CKL();
+  CK(launch_pdl(k_ref_occ_stubs, dim3(r->net.n_occ + grid_for(n, kOccLiveThreads, 2)), dim3(kOccLiveThreads), 0, s,
+                r->net, dead, S));
   // 3, 4: lattices + stub pairs, inserts then winners
   const uint64_t ws = key_prefix(seed, step, P_REF_WS);
   const PermKeys K = random_slot_keys(key_prefix(seed, step, P_REF_PERM), 0);
   const int ws_blocks = r->net.n_occ > 0 ? r->ws_blocks : 0;
   const int links = ws_blocks * r->net.n_occ + grid_for(S.max_stubs / 2, 256);
-  k_ref_links<0><<<links, 256, 0, s>>>(r->net, S, ws, K, ws_blocks);
-  CKL();
-  k_ref_links<1><<<links, 256, 0, s>>>(r->net, S, ws, K, ws_blocks);
-  CKL();
+  CK(launch_pdl(k_ref_links<0>, dim3(links), dim3(256), 0, s, r->net, S, ws, K, ws_blocks));
+  CK(launch_pdl(k_ref_links<1>, dim3(links), dim3(256), 0, s, r->net, S, ws, K, ws_blocks));
   if (count_dev) return 0;                  // no synchronisation: count + error bits stay on the device
   unsigned long long h[2] = {0, 0};
   CK(cudaMemcpyAsync(h, S.counter, sizeof(h), cudaMemcpyDeviceToHost, s));
@@ -1669,26 +1668,28 @@ static int refnet_realize_impl(epi_refnet_t* r, uint64_t seed, int32_t step, con
 // synchronisation; counts[(t - first) * 2 + {0, 1}] = edges / realizer error
 // bits, records[(t - first) * EPI_REC_LEN ...] = the step's record.
 int epi_refnet_run(epi_refnet_t* r, epi_ctx* c, const epi_state* st, uint64_t graph_seed, uint64_t seed,
-                   int32_t first, int32_t last,
-                   uint8_t* dead, int32_t* src, int32_t* dst, int8_t* kind, int64_t capacity, uint64_t* counts,
-                   int64_t* records, int32_t* vax_open, void* stream) {
-  if (!r || !c || !st || !dead || !counts || !records) return fail(EPI_EARG, "null argument");
+                   int32_t first, int32_t last, int32_t* src, int32_t* dst, int8_t* kind, int64_t capacity,
+                   uint64_t* counts, int64_t* records, int32_t* vax_open, void* stream) {
+  if (!r || !c || !st || !counts || !records) return fail(EPI_EARG, "null argument");
   if (st->n_agents != c->n || r->net.n_agents != c->n) return fail(EPI_EARG, "state size differs from context");
   if (c->host.den_enabled)
     return fail(EPI_EARG, "a device-counted graph cannot feed the exposure-notification contact log");
   if (first < 0 || last < first) return fail(EPI_EARG, "bad step range");
+  if (last == first) return 0;
   cudaStream_t s = S(stream);
+  const int64_t steps = last - first;
+  CK(cudaMemsetAsync(counts, 0, (size_t)steps * 2 * sizeof(uint64_t), s));
+  CK(cudaMemsetAsync(records, 0, (size_t)steps * EPI_REC_LEN * sizeof(int64_t), s));
+  const DeadView dead{st->stage, (int8_t)S_DEAD};   // the realizer reads the stage column in place
   for (int32_t t = first; t < last; ++t) {
     uint64_t* cnt = counts + 2 * (int64_t)(t - first);
-    k_dead_mask<<<grid_for(c->n, 256), 256, 0, s>>>(st->stage, c->n, dead, (unsigned long long*)cnt);
-    CKL();
     // the realizer counts the in-edges it writes per destination straight into
     // the graph load's row lengths (its edges are valid by construction)
     int rc = refnet_realize_impl(r, graph_seed, t, dead, src, dst, kind, capacity, nullptr, cnt, stream, c->row_len,
                                  true);
     if (!rc) rc = graph_load_impl(c, src, dst, kind, capacity, (const unsigned long long*)cnt, stream, true);
     if (!rc) rc = step_impl(c, st, t, seed, nullptr, records + (int64_t)(t - first) * EPI_REC_LEN, vax_open, nullptr,
-                            stream);
+                            stream, true);
     if (rc) return rc;
   }
   return 0;

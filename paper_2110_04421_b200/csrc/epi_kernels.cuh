@@ -345,6 +345,8 @@ __device__ __forceinline__ uint16_t next_code(const epi_params* __restrict__ P, 
 __global__ void k_codes(const epi_params* __restrict__ P, epi_state st, int step, const epi_net* net,
                         uint64_t rcount_prefix, uint16_t* __restrict__ codes, int64_t lo, int64_t hi,
                         int32_t* __restrict__ died_at = nullptr, int64_t n_all = 0) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t n = hi;
   for (int64_t a = lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < n;
        a += (int64_t)gridDim.x * blockDim.x)
@@ -385,13 +387,32 @@ __global__ void k_coo_scatter(const int32_t* __restrict__ src, const int32_t* __
                               const int8_t* __restrict__ kind, int64_t E, int64_t n,
                               const int64_t* __restrict__ row_begin, int32_t* __restrict__ fill,
                               uint32_t* __restrict__ entries, const unsigned long long* __restrict__ count) {
+  pdl_wait();
+  pdl_trigger();
   const int64_t live = count ? (int64_t)(*count < (unsigned long long)E ? *count : (unsigned long long)E) : E;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < live;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int32_t s = src[i], d = dst[i];
-    if (s < 0 || d < 0 || s >= n || d >= n) continue;
-    const int64_t pos = row_begin[d] + atomicAdd(&fill[d], 1);
-    entries[pos] = ((uint32_t)s << 2) | (uint32_t)(kind[i] & 3);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  // 4 edges per thread in flight: loads, then cursors, then stores
+  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < live; i0 += 4 * stride) {
+    int32_t s[4], d[4];
+    int8_t k[4];
+    bool ok[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int64_t i = i0 + q * stride;
+      const bool in = i < live;
+      s[q] = in ? src[i] : -1;
+      d[q] = in ? dst[i] : -1;
+      k[q] = in ? kind[i] : 0;
+    }
+    int64_t pos[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      ok[q] = !(s[q] < 0 || d[q] < 0 || s[q] >= n || d[q] >= n);
+      pos[q] = ok[q] ? row_begin[d[q]] + atomicAdd(&fill[d[q]], 1) : 0;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (ok[q]) entries[pos[q]] = ((uint32_t)s[q] << 2) | (uint32_t)(k[q] & 3);
   }
 }
 // Canonical row order: ascending (src << 2 | kind).  One thread per row; a
@@ -428,9 +449,13 @@ __device__ __forceinline__ void sort_row_regs(uint32_t* row, int len) {
   for (int i = 0; i < W; ++i)
     if (i < len) row[i] = v[i];
 }
+// (also re-zeroes the scatter's fill cursors, so they are zero at the next load)
 __global__ void k_rows_sort(int64_t n, const int64_t* __restrict__ row_begin, const int32_t* __restrict__ row_len,
-                            uint32_t* __restrict__ entries) {
+                            uint32_t* __restrict__ entries, int32_t* __restrict__ fill) {
+  pdl_wait();
+  pdl_trigger();
   for (int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; d < n; d += (int64_t)gridDim.x * blockDim.x) {
+    fill[d] = 0;
     uint32_t* row = entries + row_begin[d];
     const int len = row_len[d];
     if (len <= 1) continue;
@@ -448,14 +473,6 @@ __global__ void k_rows_sort(int64_t n, const int64_t* __restrict__ row_begin, co
         row[j + 1] = x;
       }
     }
-  }
-}
-// row lengths widened for the scan; the scatter's fill counters cleared
-__global__ void k_widen_clear(const int32_t* __restrict__ a, int64_t n, int64_t* __restrict__ out,
-                              int32_t* __restrict__ fill) {
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    out[i] = a[i];
-    fill[i] = 0;
   }
 }
 
@@ -539,11 +556,19 @@ __global__ void __launch_bounds__(256) k_pass(StepArgs A, CsrView g, const uint1
               ++j;
             }
           } else {
+            // entries and their code gathers 4 at a time (memory-level
+            // parallelism); the sum itself stays sequential in canonical order
             double h = 0.0;
-            for (int i = 0; i < len; ++i) {
-              const uint32_t x = e[i];
-              const uint16_t c = codes[x >> 2];
-              if (c & CODE_T_MASK) h = __dadd_rn(h, term_f64(P, rate_s, c, (int)(x & 3)));
+            for (int i0 = 0; i0 < len; i0 += 4) {
+              uint32_t x[4];
+              uint16_t c[4];
+#pragma unroll
+              for (int q = 0; q < 4; ++q) x[q] = i0 + q < len ? __ldg(e + i0 + q) : 0u;
+#pragma unroll
+              for (int q = 0; q < 4; ++q) c[q] = i0 + q < len ? codes[x[q] >> 2] : (uint16_t)0;
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+                if (c[q] & CODE_T_MASK) h = __dadd_rn(h, term_f64(P, rate_s, c[q], (int)(x[q] & 3)));
             }
             lam = h;
           }

@@ -62,23 +62,38 @@ __device__ __forceinline__ double ref_u(uint64_t prefix, uint64_t idx, uint64_t 
   return unit(fold(fold(prefix, idx), k));
 }
 
-// Warp-aggregated reservation of `n` output slots (n may differ per lane,
-// 0 for lanes with nothing to write).  Must be called by all 32 lanes: every
-// loop below runs whole warps (blockDim is a multiple of 32 and the trip
-// count is warp-uniform), with `valid` masking the tail.
-__device__ __forceinline__ int64_t reserve(unsigned long long* counter, int n) {
+// Block-aggregated reservation of `n` output slots (n may differ per
+// thread, 0 for threads with nothing to write): one atomic per block on the
+// single output counter.  Must be called by every thread
+// of the block (block-uniform loop trip counts); blockDim <= 1024.
+__device__ __forceinline__ int64_t reserve_block(unsigned long long* counter, int n) {
+  __shared__ int warp_tot[32];
+  __shared__ unsigned long long block_base;
   int incl = n;
-  const int lane = lane_id();
+  const int lane = lane_id(), warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const int v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
     if (lane >= o) incl += v;
   }
-  const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
-  unsigned long long base = 0;
-  if (lane == 31 && total) base = atomicAdd(counter, (unsigned long long)total);
-  base = __shfl_sync(0xFFFFFFFFu, base, 31);
-  return (int64_t)base + incl - n;
+  if (lane == 31) warp_tot[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const int t = lane < nw ? warp_tot[lane] : 0;
+    int x = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xFFFFFFFFu, x, o);
+      if (lane >= o) x += v;
+    }
+    if (lane < nw) warp_tot[lane] = x - t;                      // exclusive warp offsets
+    const int total = __shfl_sync(0xFFFFFFFFu, x, 31);
+    if (lane == 0) block_base = total ? atomicAdd(counter, (unsigned long long)total) : 0ull;
+  }
+  __syncthreads();
+  const int64_t at = (int64_t)block_base + warp_tot[warp] + incl - n;
+  __syncthreads();                                              // smem reusable by the next call
+  return at;
 }
 
 __device__ __forceinline__ void emit2(const RefScratch& S, int64_t at, int32_t u, int32_t v, int8_t kind) {
@@ -94,19 +109,20 @@ __device__ __forceinline__ void emit2(const RefScratch& S, int64_t at, int32_t u
   }
 }
 
-// dead[a] = stage[a] == DEAD (the realizer's input, engine state on device);
-// block 0 also zeroes the step's counter words.
-__global__ void k_dead_mask(const int8_t* __restrict__ stage, int64_t n, uint8_t* __restrict__ dead,
-                            unsigned long long* counter) {
-  if (blockIdx.x == 0 && threadIdx.x < 2) counter[threadIdx.x] = 0;
-  for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < n; a += (int64_t)gridDim.x * blockDim.x)
-    dead[a] = stage[a] == S_DEAD ? 1 : 0;
-}
+// Who is dead: a u8 mask (code 1) or the engine's stage column read in place
+// (code S_DEAD) — both one byte per agent.
+struct DeadView {
+  const int8_t* __restrict__ p;
+  int8_t code;
+  __device__ __forceinline__ bool operator[](int64_t i) const { return p[i] == code; }
+};
 
 // Launch 1 (per agent): households — each alive agent b emits c -> b for its
 // alive co-members — and the agent's random-network stub count; the dedupe
 // table is cleared on the side (first used by launch 3).
-__global__ void k_ref_agents(RefNet net, const uint8_t* __restrict__ dead, RefScratch S, uint64_t stub_prefix) {
+__global__ void k_ref_agents(RefNet net, DeadView dead, RefScratch S, uint64_t stub_prefix) {
+  pdl_wait();     // launched programmatically after the previous step kernel
+  pdl_trigger();
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   ulonglong2* tab = reinterpret_cast<ulonglong2*>(S.table);
@@ -122,7 +138,7 @@ __global__ void k_ref_agents(RefNet net, const uint8_t* __restrict__ dead, RefSc
       const int32_t c = net.hh_members[st + i];
       cnt += (c != b && !dead[c]) ? 1 : 0;
     }
-    const int64_t at = reserve(S.counter, cnt);
+    const int64_t at = reserve_block(S.counter, cnt);
     int o = 0;
     for (int i = 0; i < sz; ++i) {
       const int32_t c = net.hh_members[st + i];
@@ -155,8 +171,9 @@ __global__ void k_ref_agents(RefNet net, const uint8_t* __restrict__ dead, RefSc
 // ascending); the remaining blocks write the owner of every stub (agent a owns
 // stubs [stub_off[a], stub_off[a+1]); stub_off is launch 1's scan).
 constexpr int kOccLiveThreads = 1024;
-__global__ void __launch_bounds__(kOccLiveThreads) k_ref_occ_stubs(RefNet net, const uint8_t* __restrict__ dead,
-                                                                   RefScratch S) {
+__global__ void __launch_bounds__(kOccLiveThreads) k_ref_occ_stubs(RefNet net, DeadView dead, RefScratch S) {
+  pdl_wait();     // launched programmatically after the previous step kernel
+  pdl_trigger();
   if ((int)blockIdx.x >= net.n_occ) {
     if (S.stub_off[net.n_agents] > S.max_stubs) return;   // launch 3 flags it
     const int64_t nb = gridDim.x - net.n_occ;
@@ -257,7 +274,7 @@ __device__ __forceinline__ void ws_block(const RefNet& net, const RefScratch& S,
       }
     }
     if (PASS == 1) {
-      const int64_t at = reserve(S.counter, emit ? 2 : 0);
+      const int64_t at = reserve_block(S.counter, emit ? 2 : 0);
       if (emit) emit2(S, at, u, v, 1);
     }
   }
@@ -298,7 +315,7 @@ __device__ __forceinline__ void pairs_block(const RefNet& net, const RefScratch&
       }
     }
     if (PASS == 1) {
-      const int64_t at = reserve(S.counter, emit ? 2 : 0);
+      const int64_t at = reserve_block(S.counter, emit ? 2 : 0);
       if (emit) emit2(S, at, u, v, 2);
     }
   }
@@ -309,6 +326,8 @@ __device__ __forceinline__ void pairs_block(const RefNet& net, const RefScratch&
 // occupation), the remaining blocks the stub pairs.
 template <int PASS>
 __global__ void k_ref_links(RefNet net, RefScratch S, uint64_t ws_prefix, PermKeys K, int ws_blocks) {
+  pdl_wait();     // launched programmatically after the previous step kernel
+  pdl_trigger();
   const int nws = ws_blocks * net.n_occ;
   if ((int)blockIdx.x < nws)
     ws_block<PASS>(net, S, ws_prefix, blockIdx.x / ws_blocks, blockIdx.x % ws_blocks, ws_blocks);

@@ -259,7 +259,8 @@ class GpuEngine:
     def advance_refnet(self, realizer, first: int, last: int, counts, records) -> None:
         """Steps [first, last) of the reference's replication loop
         (runner.py:138-150) issued natively (`epi_refnet_run`): dead mask,
-        realizer, counted graph load and the step, per step, with no host
+        realizer (dead agents read from the stage column), counted graph load
+        and the step, per step, with no host
         synchronisation.  counts = device int64[last-first][2] (edges, realizer
         error bits), records = device int64[last-first][REC_LEN]."""
         import torch
@@ -269,13 +270,11 @@ class GpuEngine:
             raise InvariantViolation("advance_refnet() needs resident=True")
         if realizer.n_agents != self.cols.n_agents:
             raise InvariantViolation("realizer population size differs from the engine's")
-        if getattr(self, "_dead_scratch", None) is None:
-            self._dead_scratch = torch.empty(self.cols.n_agents, dtype=torch.uint8, device=self.device)
         src, dst, kind = realizer.buffers()
         st = self.dev.struct()
         N.check(self._lib.epi_refnet_run(realizer._h, self._ctx, C_ref(st), _u64(realizer.seed), _u64(self.seed),
                                          int(first), int(last),
-                                         N.ptr(self._dead_scratch), N.ptr(src), N.ptr(dst), N.ptr(kind),
+                                         N.ptr(src), N.ptr(dst), N.ptr(kind),
                                          int(src.shape[0]), N.ptr(counts), N.ptr(records), N.ptr(self._vax),
                                          N.stream_handle()))
         self.clock = last
