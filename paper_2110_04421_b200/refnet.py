@@ -47,18 +47,22 @@ class GpuRealizer:
         self.device = torch.device(device or "cuda")
         ids = np.arange(n, dtype=np.int64)
         # households: members grouped by id, per-agent start / size
-        order = np.argsort(hh, kind="stable")
+        if n and np.all(hh[1:] >= hh[:-1]):
+            order = ids                         # population.synthesize numbers households in order
+        else:
+            order = np.argsort(hh, kind="stable")
         sorted_hh = hh[order]
-        first = np.searchsorted(sorted_hh, sorted_hh, side="left")
-        last = np.searchsorted(sorted_hh, sorted_hh, side="right")
+        # group boundaries in the sorted ids: start slot and size of each group
+        starts = np.flatnonzero(np.concatenate(([True], sorted_hh[1:] != sorted_hh[:-1]))) if n else ids
+        sizes = np.diff(np.append(starts, n))
         hh_start = np.empty(n, np.int32)
         hh_size = np.empty(n, np.int32)
-        hh_start[order] = first
-        hh_size[order] = last - first
+        hh_start[order] = np.repeat(starts, sizes)
+        hh_size[order] = np.repeat(sizes, sizes)
         # occupations 1..n_occ: members in ascending id order
         n_occ = len(means)
         emp = occ > 0
-        occ_order = np.lexsort((ids[emp], occ[emp]))
+        occ_order = np.argsort(occ[emp], kind="stable")    # by occupation, ids ascending
         occ_members = ids[emp][occ_order]
         counts = np.bincount(occ[emp], minlength=n_occ + 1)[1:n_occ + 1]
         occ_start = np.concatenate(([0], np.cumsum(counts))).astype(np.int32)
