@@ -71,3 +71,48 @@ def test_device_resident_run_equals_step_by_step():
     b.engine.sync_to_host()
     assert np.array_equal(a.cols.stage, b.cols.stage)
     assert a.interactions == b.interactions
+
+
+def test_native_loop_in_chunks_equals_one_run():
+    """epi_refnet_run over [0,7) + [7,20) + the rest == one call, bitwise
+    (records, edge counts and final state)."""
+    import dataclasses as dc
+    tr = Trajectory("noiv")
+    a, b = _sim(tr), _sim(tr)
+    ev_a = a.run(7) + a.run(13) + a.run()
+    ev_b = b.run()
+    assert [dc.astuple(x) for x in ev_a] == [dc.astuple(x) for x in ev_b]
+    a.engine.sync_to_host()
+    b.engine.sync_to_host()
+    for c in ("stage", "infected_at", "next_stage", "next_transition_at"):
+        assert np.array_equal(getattr(a.cols, c), getattr(b.cols, c)), c
+
+
+def test_native_loop_output_overflow_is_an_error():
+    """A realizer output smaller than the step's graph: the native loop writes
+    nothing out of bounds (the graph load only sees the edges written) and
+    run() raises ConfigError at its end."""
+    import torch
+    from paper_2110_04421_b200.errors import ConfigError
+    tr = Trajectory("noiv")
+    sim = _sim(tr)
+    small = 64
+    r = sim.realizer
+    r._src, r._dst, r._kind = r._src[:small].clone(), r._dst[:small].clone(), r._kind[:small].clone()
+    with pytest.raises(ConfigError, match="capacity"):
+        sim.run(3)
+    torch.cuda.synchronize()
+
+
+def test_native_loop_rejects_exposure_notification():
+    """The contact log needs host-known edge counts: run() with DEN enabled is
+    a ConfigError before any step; step() still works."""
+    from paper_2110_04421_b200.errors import ConfigError
+    tr = Trajectory("alliv")
+    assert tr.iv.den_enabled
+    sim = _sim(tr)
+    with pytest.raises(ConfigError):
+        sim.run(2)
+    assert sim.clock == 0
+    sim.step()
+    assert sim.clock == 1
