@@ -504,13 +504,26 @@ __device__ __forceinline__ void for_each_in_code(const epi_net& net, const NetKe
 // slot.  A dead or absent source has code byte 0 and factor[0] = 0, and
 // acc + 0.0f == acc (acc >= +0), so the sums are bitwise those of skipping
 // it; `edges` counts the alive (resp. present) ones.
+// (`1 - dead bit` lets the unrolled callers fold the constant ones and add
+// two slots' dead bits per IADD3.)
 __device__ __forceinline__ void add_src(float& acc, unsigned& edges, const float* __restrict__ factor, uint16_t c) {
   acc += factor[c & 0xFF];
-  edges += ((unsigned)c >> 15) ^ 1u;
+  edges += 1u - ((unsigned)c >> 15);
 }
-__device__ __forceinline__ void add_rin(float& acc, unsigned& edges, const float* __restrict__ factor, uint16_t c) {
-  acc += factor[c & 0xFF];
-  edges += ((unsigned)c >> 14) & 1u;
+// A push row (RT_SLOTS codes as two uint4, low half of each word first): the
+// same adds in slot order; the present bits (14) of both halves of a word are
+// counted together in 16-bit lanes of one register.
+__device__ __forceinline__ void add_rin_row(float& acc, unsigned& edges, const float* __restrict__ factor,
+                                            uint4 in0, uint4 in1) {
+  const uint32_t w[8] = {in0.x, in0.y, in0.z, in0.w, in1.x, in1.y, in1.z, in1.w};
+  uint32_t pres = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    acc += factor[w[i] & 0xFF];
+    acc += factor[(w[i] >> 16) & 0xFF];
+    pres += (w[i] >> 14) & 0x00010001u;
+  }
+  edges += (pres & 0xFFFFu) + (pres >> 16);
 }
 
 // Branch-free per-kind sums of for_each_in_code without push rows (the
@@ -664,10 +677,8 @@ __device__ __forceinline__ void push_kind_sums(const epi_net& net, const WorkTab
 #pragma unroll
     for (int q = 0; q < 4; ++q) add_src(acc[2], edges, factor, co[q]);
   }
-  const uint4 inv[2] = {in0, in1};
-  const uint16_t* iv = (const uint16_t*)inv;
-#pragma unroll
-  for (int j = 0; j < RT_SLOTS; ++j) add_rin(acc[2], edges, factor, iv[j]);
+  static_assert(RT_SLOTS == 16, "push rows are two uint4");
+  add_rin_row(acc[2], edges, factor, in0, in1);
 }
 
 }  // namespace epi

@@ -250,10 +250,7 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_fused_run(RunArgs R, epi
 #pragma unroll
             for (int q = 0; q < 4; ++q) add_src(acc[2], edges, T.factor, co[q]);
           }
-          const uint4 inv[2] = {in0, in1};
-          const uint16_t* iv = (const uint16_t*)inv;
-#pragma unroll
-          for (int j = 0; j < RT_SLOTS; ++j) add_rin(acc[2], edges, T.factor, iv[j]);
+          add_rin_row(acc[2], edges, T.factor, in0, in1);
         }
         const float tot = acc[0] * T.bfac[0] + acc[1] * T.bfac[1] + acc[2] * T.bfac[2];
         if (h.stage == S_SUS && !(R.P->sterilizing && h.immune)) lam = (double)(tot * T.sfac[h.age]);
