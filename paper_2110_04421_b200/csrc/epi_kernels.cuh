@@ -925,7 +925,7 @@ struct DayTests {
   int* n_notif;
 };
 
-__global__ void __launch_bounds__(128, 6) k_fused_step(StepArgs A, epi_net net, NetKeys nk,
+__global__ void __launch_bounds__(128, 8) k_fused_step(StepArgs A, epi_net net, NetKeys nk,
                                                     const uint16_t* __restrict__ codes, double rate,
                                                     uint16_t* __restrict__ codes_next,
                                                     const epi_net* net_dev, uint64_t rcount_next,
