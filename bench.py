@@ -785,8 +785,9 @@ def run_refnet(a):
         sim = make(a.warmup + i)
         st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         st.record()
-        sim.run()
+        handle = sim.issue()       # the 180 steps (device work bracketed by the events)
         en.record()
+        sim.finish(handle)         # flags, error bits, per-step events (host; inside e2e)
         sim.engine.sync_to_host()
         torch.cuda.synchronize()
         t_all = time.perf_counter() - t0

@@ -143,6 +143,7 @@ struct epi_ctx {
   long long* scratch_rec = nullptr;  // record when the caller passes none
   long long* gflags = nullptr;       // graph validation bits (epi_graph_load)
   uint16_t* codes = nullptr;         // graph-in codes
+  uint16_t* codes_alt = nullptr;     // epi_refnet_run: the other buffer of the codes ping-pong
   // graph-in CSR
   int64_t edge_cap = 0, n_edges = 0;
   uint32_t* entries = nullptr;
@@ -403,6 +404,7 @@ int epi_destroy(epi_ctx* c) {
   cudaFree(c->scratch_rec);
   cudaFree(c->gflags);
   cudaFree(c->codes);
+  cudaFree(c->codes_alt);
   cudaFree(c->entries);
   cudaFree(c->row_begin);
   cudaFree(c->row_len);
@@ -583,9 +585,13 @@ static int push_ring(epi_ctx* c, cudaStream_t s) {
   return 0;
 }
 
+// codes_in: the step's codes already computed (k_codes skipped); codes_out:
+// the update writes the next step's codes there (only without interventions:
+// their phases change the state after the update).
 static int step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t seed,
                      const double* hazard, int64_t* record, int32_t* vax_open,
-                     const double* const* injected, void* stream, bool rec_zeroed = false) {
+                     const double* const* injected, void* stream, bool rec_zeroed = false,
+                     const uint16_t* codes_in = nullptr, uint16_t* codes_out = nullptr) {
   if (!c || !st) return fail(EPI_EARG, "null argument");
   if (st->n_agents != c->n) return fail(EPI_EARG, "state size differs from context");
   cudaStream_t s = S(stream);
@@ -600,11 +606,13 @@ static int step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t see
   if (hazard) {
     k_update_from_hazard<<<grid, 256, 0, s>>>(A, hazard, iv ? 0 : 1);
   } else {
-    CK(launch_pdl(k_codes, dim3(grid), dim3(256), 0, s, c->P, *st, step, (const epi_net*)nullptr, (uint64_t)0,
-                  c->codes, (int64_t)0, c->n, (int32_t*)nullptr, (int64_t)0));
+    if (!codes_in)
+      CK(launch_pdl(k_codes, dim3(grid), dim3(256), 0, s, c->P, *st, step, (const epi_net*)nullptr, (uint64_t)0,
+                    c->codes, (int64_t)0, c->n, (int32_t*)nullptr, (int64_t)0));
+    if (iv) codes_out = nullptr;
     CsrView g{c->entries, c->row_len, c->row_begin, 0, nullptr, nullptr};
-    CK(launch_pdl(k_pass<true, 1>, dim3(grid), dim3(256), 0, s, A, g, (const uint16_t*)c->codes, (void*)nullptr,
-                  c->host.rate_scale, iv ? 0 : 1, (uint16_t*)nullptr, (const epi_net*)nullptr, (uint64_t)0,
+    CK(launch_pdl(k_pass<true, 1>, dim3(grid), dim3(256), 0, s, A, g, codes_in ? codes_in : (const uint16_t*)c->codes,
+                  (void*)nullptr, c->host.rate_scale, iv ? 0 : 1, codes_out, (const epi_net*)nullptr, (uint64_t)0,
                   (const MsgTables*)c->msg_dev));
   }
   CKL();
@@ -1681,6 +1689,15 @@ int epi_refnet_run(epi_refnet_t* r, epi_ctx* c, const epi_state* st, uint64_t gr
   CK(cudaMemsetAsync(counts, 0, (size_t)steps * 2 * sizeof(uint64_t), s));
   CK(cudaMemsetAsync(records, 0, (size_t)steps * EPI_REC_LEN * sizeof(int64_t), s));
   const DeadView dead{st->stage, (int8_t)S_DEAD};   // the realizer reads the stage column in place
+  // Without interventions the update of step t writes the codes of step t+1
+  // (ping-pong between c->codes and c->codes_alt): no k_codes launch after
+  // the first step.
+  const bool chain = !interventions_on(c->host);
+  if (chain && !c->codes_alt) {
+    int rc = dalloc(&c->codes_alt, (size_t)c->n);
+    if (rc) return rc;
+  }
+  uint16_t* cbuf[2] = {c->codes, c->codes_alt};
   for (int32_t t = first; t < last; ++t) {
     uint64_t* cnt = counts + 2 * (int64_t)(t - first);
     // the realizer counts the in-edges it writes per destination straight into
@@ -1688,8 +1705,10 @@ int epi_refnet_run(epi_refnet_t* r, epi_ctx* c, const epi_state* st, uint64_t gr
     int rc = refnet_realize_impl(r, graph_seed, t, dead, src, dst, kind, capacity, nullptr, cnt, stream, c->row_len,
                                  true);
     if (!rc) rc = graph_load_impl(c, src, dst, kind, capacity, (const unsigned long long*)cnt, stream, true);
+    const int k = (t - first) & 1;
     if (!rc) rc = step_impl(c, st, t, seed, nullptr, records + (int64_t)(t - first) * EPI_REC_LEN, vax_open, nullptr,
-                            stream, true);
+                            stream, true, (chain && t > first) ? cbuf[k] : nullptr,
+                            chain ? cbuf[k ^ 1] : nullptr);
     if (rc) return rc;
   }
   return 0;

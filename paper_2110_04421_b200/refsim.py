@@ -80,12 +80,23 @@ class ReferenceNativeSimulation:
         realizer's edge count goes to the graph load on the device); graph
         flags and realizer errors checked once at the end.  Returns the
         StepEvents."""
+        return self.finish(self.issue(steps))
+
+    def issue(self, steps: int | None = None):
+        """Issue the remaining steps (or `steps` of them) on the current
+        stream and return a handle for finish(); nothing is synchronised."""
         import torch
         first = self.clock
         last = self.horizon if steps is None else min(self.horizon, first + steps)
         counts = torch.zeros((max(last - first, 1), 2), dtype=torch.int64, device=self.engine.device)
         if last > first:
             self.engine.advance_refnet(self.realizer, first, last, counts, self.records[first:last])
+        return first, last, counts
+
+    def finish(self, handle):
+        """Wait for issued steps, check the graph flags and the realizer's
+        error bits, and return their StepEvents."""
+        first, last, counts = handle
         self.engine.check_graph_flags()
         err = int(np.bitwise_or.reduce(counts[:, 1].cpu().numpy()))
         if err & 1:
