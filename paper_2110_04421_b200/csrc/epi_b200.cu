@@ -1002,7 +1002,7 @@ static int iv_fused_day(epi_ctx* c, const StepArgs& A, int32_t step, uint64_t se
     CKL();
     CK(cudaMemsetAsync(c->wt_host[par].rin, 0, (size_t)c->n * RT_SLOTS * sizeof(uint16_t), s));
     const bool has_work = c->net.n_member_slots > 0 && c->net.colleague_draws > 0;
-    const int wblocks = has_work ? grid_for(c->net.n_member_slots, 256, 4) : 0;
+    const int wblocks = has_work ? grid_for(c->net.n_member_slots, 256, 8) : 0;
     const int rblocks = grid_for(c->n, 256, 8);
     CK(launch_pdl_w(&c->hot, k_day_tables, dim3(wblocks + rblocks), dim3(256), 0, s, c->net, nk, c->wt_host[par],
                     codes_cur, (int64_t)0, c->n, wblocks, (const NetTables*)nt_today, nt_next,
@@ -1105,7 +1105,7 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
     if (use_wt) {
       if (push_rand && (step == 0 || merged))
         CK(cudaMemsetAsync(c->wt_host[par].rin, 0, (size_t)c->n * RT_SLOTS * sizeof(uint16_t), s));
-      const int wblocks = has_work ? grid_for(c->net.n_member_slots, 256, 4) : 0;
+      const int wblocks = has_work ? grid_for(c->net.n_member_slots, 256, 8) : 0;
       const int rblocks = push_rand ? grid_for(c->hi - c->lo, 256, 8) : 0;
       WorkTables w = c->wt_host[par];
       if (variant == 0) w.wcode = nullptr;
