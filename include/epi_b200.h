@@ -301,6 +301,15 @@ int epi_set_exchange(epi_ctx *ctx, epi_exchange_fn fn, void *user);
  * up to `max_agents` agents (-1 = while they fit in L2). */
 int epi_set_push_max(epi_ctx *ctx, int64_t max_agents);
 
+/* Debug export of the hazard the step kernels consume (test hook for the
+ * timed fp32 paths: k_fused_step, k_fused_run, k_iv_run, k_msg_pass<1>).
+ * While set, every step kernel of day t in [first_step, first_step + n_days)
+ * writes its agents' fp32 lambda -- the value fed to p = 1 - exp(-lambda),
+ * engine.py:157-161 -- to out[(t - first_step) * n_agents + agent]; 0 for
+ * non-targets (engine.py:109, 112-117).  `out` is a caller-owned device buffer
+ * of n_days * n_agents floats.  n_days = 0 turns the export off. */
+int epi_set_lambda_probe(epi_ctx *ctx, float *out, int32_t first_step, int32_t n_days);
+
 /* Bind a config network to the context and allocate its per-step padded CSR
  * (a ring of den_lookback slots when exposure notification is enabled). */
 int epi_net_attach(epi_ctx *ctx, const epi_net *net);

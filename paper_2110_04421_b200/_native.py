@@ -98,6 +98,7 @@ _SIGS = {
     "epi_set_infection_mode": (_i32, [_p, _i32]),
     "epi_pop_synthesize": (_i32, [C.POINTER(EpiPopSpec), _u64, C.POINTER(EpiPopOut), _p]),
     "epi_set_push_max": (_i32, [_p, _i64]),
+    "epi_set_lambda_probe": (_i32, [_p, _p, _i32, _i32]),
     "epi_set_persistent": (_i32, [_p, _i32]),
     "epi_set_iv_fusion": (_i32, [_p, _i32]),
     "epi_set_day_grid": (_i32, [_p, _i32]),

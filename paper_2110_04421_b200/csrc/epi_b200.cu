@@ -185,6 +185,7 @@ struct epi_ctx {
   unsigned long long* iv_hist = nullptr;   // [2][NUM_BUCKETS] eligibility histogram by day parity
   unsigned long long* ivr_hist = nullptr;  // k_iv_run: [2][NUM_BUCKETS + 1] (+ active count)
   unsigned* run_barrier = nullptr;   // arrival counter of k_fused_run's grid barrier
+  LamProbe probe{};                  // debug hazard export (epi_set_lambda_probe)
 };
 
 namespace {
@@ -226,6 +227,7 @@ StepArgs make_args(epi_ctx* c, const epi_state* st, int step, uint64_t seed, lon
   A.hi = c->hi;
   A.indep = c->indep;
   A.tau_lut = c->tau_lut;
+  A.probe = c->probe;
   return A;
 }
 
@@ -1000,7 +1002,10 @@ static int iv_fused_day(epi_ctx* c, const StepArgs& A, int32_t step, uint64_t se
     // the day's tables from scratch; the day-to-day counters to zero
     k_day_keys<<<1, 32, 0, s>>>(nt_today, nk.rperm, nullptr);
     CKL();
+    // both parities: tomorrow's may hold the scatter of a run that stopped
+    // before consuming it (then reset to an earlier day)
     CK(cudaMemsetAsync(c->wt_host[par].rin, 0, (size_t)c->n * RT_SLOTS * sizeof(uint16_t), s));
+    CK(cudaMemsetAsync(c->wt_host[par ^ 1].rin, 0, (size_t)c->n * RT_SLOTS * sizeof(uint16_t), s));
     const bool has_work = c->net.n_member_slots > 0 && c->net.colleague_draws > 0;
     const int wblocks = has_work ? grid_for(c->net.n_member_slots, 256, 8) : 0;
     const int rblocks = grid_for(c->n, 256, 8);
@@ -1103,8 +1108,12 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
       CKL();
     }
     if (use_wt) {
-      if (push_rand && (step == 0 || merged))
+      if (push_rand && (step == 0 || merged)) {
+        // a new chain: today's scatter target, and (merged) tomorrow's, which
+        // may hold the scatter of a run that stopped before consuming it
         CK(cudaMemsetAsync(c->wt_host[par].rin, 0, (size_t)c->n * RT_SLOTS * sizeof(uint16_t), s));
+        if (merged) CK(cudaMemsetAsync(c->wt_host[par ^ 1].rin, 0, (size_t)c->n * RT_SLOTS * sizeof(uint16_t), s));
+      }
       const int wblocks = has_work ? grid_for(c->net.n_member_slots, 256, 8) : 0;
       const int rblocks = push_rand ? grid_for(c->hi - c->lo, 256, 8) : 0;
       WorkTables w = c->wt_host[par];
@@ -1249,6 +1258,7 @@ static int launch_run(epi_ctx* c, const epi_state* st, int32_t first, int32_t n_
   R.tau_lut = c->tau_lut;
   R.dn = c->ntab.dn;
   R.barrier = c->run_barrier;
+  R.probe = c->probe;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)sm_count());
   cfg.blockDim = dim3((unsigned)run_threads(c->n) + 32);     // + the service warp
@@ -1383,6 +1393,15 @@ int epi_set_iv_fusion(epi_ctx* c, int32_t on) {
   if (!c) return fail(EPI_EARG, "null ctx");
   c->iv_fusion = on != 0;
   c->merged_ready = -1;
+  return 0;
+}
+
+int epi_set_lambda_probe(epi_ctx* c, float* out, int32_t first_step, int32_t n_days) {
+  if (!c || n_days < 0 || (n_days > 0 && !out)) return fail(EPI_EARG, "bad argument");
+  c->probe.out = n_days > 0 ? out : nullptr;
+  c->probe.n = c->n;
+  c->probe.first = first_step;
+  c->probe.days = n_days;
   return 0;
 }
 

@@ -74,6 +74,21 @@ __device__ __forceinline__ void rec_agent(RecAcc& s, bool valid, int stage, int3
 }
 
 // ---------------------------------------------------------------------------
+// Debug export of the hazard every step kernel feeds its Bernoulli
+// (epi_set_lambda_probe): out[(t - first) * n + agent] = the fp32 lambda of
+// day t, 0 for non-targets, for days first <= t < first + days.  It exists so
+// the timed kernels are checked against the oracle's gather_exposure
+// (engine.py:77-117) on the very values they consume.
+struct LamProbe {
+  float* out;
+  int64_t n;
+  int first, days;
+};
+__device__ __forceinline__ void probe_lambda(const LamProbe& p, int t, int64_t b, double lam) {
+  if (p.out != nullptr && (unsigned)(t - p.first) < (unsigned)p.days)
+    p.out[(size_t)(t - p.first) * (size_t)p.n + (size_t)b] = (float)lam;
+}
+
 // Kernel arguments shared by the step kernels.
 struct StepArgs {
   const epi_params* __restrict__ P;
@@ -86,6 +101,7 @@ struct StepArgs {
   int64_t lo, hi;             // owned agent rows [lo, hi) (partitioned runs)
   int indep;                  // independent-edges infection (oracle.py:185-192)
   const uint16_t* tau_lut;    // bucket table of delay_steps (or null: binary search)
+  LamProbe probe;             // debug export of the per-agent hazard (epi_set_lambda_probe)
 };
 
 // Shared tables for the fp32 message: factor[t | asym<<7] = rate*A*w[t],
@@ -985,6 +1001,7 @@ __global__ void __launch_bounds__(128, 8) k_fused_step(StepArgs A, epi_net net, 
       clear_rin_row(wt, b);
     }
     unsigned ev = 0;
+    if (valid) probe_lambda(A.probe, A.step, b, lam);
     if (valid) ev = transmit_progress_hot(A, b, lam, -1, h);
     if (tests.on) {
       // phase 3 + 4a on the agent's own state (k_iv_tests, fused)

@@ -143,6 +143,7 @@ __global__ void __launch_bounds__(MP_WARPS * 32, 3) k_msg_pass(StepArgs A, CsrVi
       double lam = 0.0;
       if (valid && h.stage == S_SUS && !(P->sterilizing && h.immune)) lam = (double)(acc * T.sfac[h.age]);
       unsigned ev = 0;
+      if (valid) probe_lambda(A.probe, A.step, a, lam);
       if (valid) ev = transmit_progress_hot(A, a, lam, -1, h);
       if (valid && (ev & 8u) && A.flags) A.flags[a] = FL_SYMPTOMATIC;
       rec_events(racc, ev);

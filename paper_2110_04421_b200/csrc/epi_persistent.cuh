@@ -56,6 +56,7 @@ struct RunArgs {
   const uint16_t* tau_lut;
   Radix dn;
   unsigned* barrier;              // zeroed arrival counter
+  LamProbe probe;
 };
 
 // Grid barrier between days: one arrival per block (acq_rel atomic on one
@@ -261,6 +262,7 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_fused_run(RunArgs R, epi
       rw[1] = make_uint4(0, 0, 0, 0);
     }
     unsigned ev = 0;
+    if (valid) probe_lambda(R.probe, t, b, lam);
     if (valid) ev = transmit_progress_now(R.P, R.st, D.K, t, b, lam, h, pend);
     rec_events(rc, ev);
     rec_add(rc, EPI_REC_EDGES, edges);

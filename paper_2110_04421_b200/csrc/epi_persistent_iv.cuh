@@ -209,6 +209,7 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
         rw[1] = make_uint4(0, 0, 0, 0);
       }
       unsigned ev = 0;
+      if (valid) probe_lambda(R.A0.probe, t, b, lam);
       if (valid) ev = transmit_progress_now(A.P, st, A.K, t, b, lam, h, pend);
       unsigned tested = 0;
       if (R.tests) {

@@ -225,6 +225,19 @@ class ConfigSimulation:
             N.ptr(self.codes[1]), N.ptr(self.rec[t]), N.ptr(self.vax), N.stream_handle()))
         self.clock = t + d
 
+    def lambda_probe(self, first_step: int, n_days: int):
+        """Export the fp32 hazard the step kernels consume on days
+        [first_step, first_step + n_days) into a [n_days, n] device tensor
+        (a test hook; n_days = 0 turns it off and returns None)."""
+        import torch
+        buf = None
+        if n_days > 0:
+            buf = torch.full((n_days, self.n), float("nan"), dtype=torch.float32, device=self.device)
+        self._probe = buf
+        N.check(self._lib.epi_set_lambda_probe(self._ctx, N.ptr(buf) if buf is not None else None,
+                                               int(first_step), int(n_days)))
+        return buf
+
     def uses_persistent_run(self) -> bool:
         """Whether run() sends its days after the first to k_fused_run."""
         r = self._lib.epi_run_persistent(self._ctx, 0 if self.mode == "csr" else 1,
