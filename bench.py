@@ -12,8 +12,9 @@ pass, fused infection/progression update and the per-day record.
 definition, runner.py:269,287) over all ranks, device-timed with CUDA events
 (max over ranks).  `e2e` = the same through the public API from pinned host
 buffers: initial state H2D + 180 days + time-series D2H, every step.
-`--impl reference` times the CPU oracle port of the reference engine on the
-same workload (bounded sample of days, all host cores), see DESIGN.md §6.
+`--impl reference` times the unmodified reference engine (epivec, installed
+into baseline/_ref) on the same workload, all host cores, each process
+walking through whole 180-day replications.
 """
 
 from __future__ import annotations
@@ -81,6 +82,20 @@ def workload_iv(name, dose_gap=21):
                                                     dose2_efficacy=0.9, dose_gap=dose_gap))
 
 
+def workload_string(a):
+    """config.workload -- identical in both arms (ours / --impl reference)."""
+    if a.workload == "config2":
+        return ("config2 (BASELINE.json configs[2]): config 1 + quarantine 14 d, testing "
+                f"(5 %, 2-day delay), DEN (app 0.5), vaccination 1 %/day, efficacy 0.5/0.9, "
+                f"dose gap {a.dose_gap} d")
+    if a.workload == "config0":
+        return ("config0 (BASELINE.json configs[0]): 10k agents, 180 days, households U{1..6} + "
+                "Poisson(5) random contacts, 10 seeds, no interventions")
+    return ("config1 (BASELINE.json configs[1]): 100k agents, 180 days, households U{1..6} + "
+            "workplaces U{10..50} x 8 colleague draws + Poisson(5) random contacts, 100 seeds, "
+            "no interventions")
+
+
 def dist_env():
     return (int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)),
             int(os.environ.get("WORLD_SIZE", 1)))
@@ -90,73 +105,20 @@ def dist_env():
 # CPU reference arm: oracle port of Engine.step + the config-network
 # restatement, one replica per process, bounded number of days.
 def _cpu_worker(args):
+    """cpu_baseline of our arm: the unmodified reference engine (baseline/_ref)
+    on one core, one replica of the workload, days 0.. until `seconds`."""
     workload, seed, seconds = args
     sys.path.insert(0, str(ROOT))
-    from oracle import confignet_np, engine_np
-    from paper_2110_04421_b200.confignet import synthesize
-    from paper_2110_04421_b200.defaults import default_disease, default_progression
-    from paper_2110_04421_b200.graph import StepGraph
-    from paper_2110_04421_b200.interventions import InterventionConfig
-    from paper_2110_04421_b200.sim import initial_columns
-    spec = workload_spec(workload)
-    pop = synthesize(spec, 0)
-    cols = initial_columns(pop)
-    disease, table = default_disease(), default_progression()
-    iv = workload_iv(workload) if workload != "config2" else workload_iv(workload, DOSE_GAP[0])
-    # seeding (population.py:151-177) with the oracle's keyed draws
-    from oracle import rng_np
-    ids = pop.seeds
-    entry = engine_np.pick(table.rules[0], cols.age_band[ids], rng_np.uniforms(seed, 0, 3, ids))
-    cols.stage[ids] = entry
-    cols.infected_at[ids] = 0
-    nxt, d = engine_np.schedule(table, entry, cols.age_band[ids], rng_np.uniforms(seed, 0, 4, ids),
-                                rng_np.uniforms(seed, 0, 5, ids))
-    cols.next_stage[ids] = nxt
-    cols.next_transition_at[ids] = d
-    eng = engine_np.OracleEngine(cols, disease, table, iv, seed)
+    from oracle.epivec_driver import ReferenceNativeReplica, ReferenceReplica, reference_interventions
+    if workload == "refnet":
+        rep = ReferenceNativeReplica(REFNET_AGENTS, seed, 0, REFNET_SEEDS)
+    else:
+        rep = ReferenceReplica(workload_spec(workload), seed,
+                               reference_interventions(workload == "config2", DOSE_GAP[0]))
     t0 = time.perf_counter()
     edges = days = 0
     while days < HORIZON and (time.perf_counter() - t0) < seconds:
-        src, dst, kind = confignet_np.realize(pop, seed, days, cols.stage == 10, canonical=False)
-        ev = eng.step(StepGraph(days, src, dst, kind))
-        edges += ev.n_edges
-        days += 1
-    return edges, days, time.perf_counter() - t0
-
-
-def _cpu_worker_refnet(args):
-    """The reference's own scenario (`epivec bench`) restated on the host: the
-    population mirror, the oracle engine (engine_np) and the oracle restatement
-    of the reference realizer (graphs_np), one replica, bounded steps."""
-    _, seed, seconds = args
-    sys.path.insert(0, str(ROOT))
-    from oracle import engine_np, graphs_np, rng_np
-    from paper_2110_04421_b200.defaults import default_disease, default_progression
-    from paper_2110_04421_b200.graph import StepGraph
-    from paper_2110_04421_b200.interventions import InterventionConfig
-    from paper_2110_04421_b200.keyed import replication_seed
-    from paper_2110_04421_b200.population import PopulationSpec, choose_seeds, synthesize
-    spec = PopulationSpec.default(REFNET_AGENTS)
-    rseed = replication_seed(seed, 0)
-    cols = synthesize(spec, rseed)
-    table = default_progression()
-    ids = choose_seeds(cols, REFNET_SEEDS, rseed)
-    entry = engine_np.pick(table.rules[0], cols.age_band[ids], rng_np.uniforms(rseed, 0, 3, ids))
-    cols.stage[ids] = entry
-    cols.infected_at[ids] = 0
-    nxt, d = engine_np.schedule(table, entry, cols.age_band[ids], rng_np.uniforms(rseed, 0, 4, ids),
-                                rng_np.uniforms(rseed, 0, 5, ids))
-    cols.next_stage[ids] = nxt
-    cols.next_transition_at[ids] = d
-    realizer = graphs_np.ReferenceRealizer(rseed, cols.household_id, cols.occupation, cols.random_degree,
-                                           spec.occupation_mean_interactions, spec.rewire_beta)
-    eng = engine_np.OracleEngine(cols, default_disease(), table, InterventionConfig(), rseed)
-    t0 = time.perf_counter()
-    edges = days = 0
-    while days < HORIZON and (time.perf_counter() - t0) < seconds:
-        src, dst, kind = realizer.realize(days, cols.stage == 10)
-        ev = eng.step(StepGraph(days, src, dst, kind))
-        edges += ev.n_edges
+        edges += rep.step().n_edges
         days += 1
     return edges, days, time.perf_counter() - t0
 
@@ -164,44 +126,106 @@ def _cpu_worker_refnet(args):
 REFNET_AGENTS, REFNET_SEEDS = 100_000, 10   # epivec bench --agents 100000 (scenario.py:53)
 
 
+def _ref_worker(conn, workload, dose_gap, base):
+    """A host process driving the UNMODIFIED reference engine
+    (`epivec.engine.Engine` from baseline/_ref) over whole 180-day
+    replications of the workload, one after another.  Each command
+    ("advance", seconds) simulates days until the budget is spent -- so over
+    the run every worker walks through the whole horizon, more than once --
+    and replies (directed edges, days, seconds)."""
+    sys.path.insert(0, str(ROOT))
+    from oracle.epivec_driver import ReferenceReplica, import_epivec, reference_interventions
+    from paper_2110_04421_b200.confignet import synthesize
+    import_epivec()
+    from epivec.runner import replication_seed
+    rep_i = 0
+    if workload == "refnet":
+        from oracle.epivec_driver import ReferenceNativeReplica
+
+        def fresh():
+            nonlocal rep_i
+            rep_i += 1
+            return ReferenceNativeReplica(REFNET_AGENTS, base, rep_i, REFNET_SEEDS)
+    else:
+        spec = workload_spec(workload)
+        pop = synthesize(spec, 0)
+        iv = reference_interventions(workload == "config2", dose_gap)
+
+        def fresh():
+            nonlocal rep_i
+            rep_i += 1
+            return ReferenceReplica(spec, replication_seed(base, rep_i), iv, pop=pop)
+    rep = fresh()
+    conn.send("ready")
+    while True:
+        cmd = conn.recv()
+        if cmd is None:
+            return
+        t0 = time.perf_counter()
+        edges = days = 0
+        while time.perf_counter() - t0 < cmd:
+            if rep.day >= HORIZON:
+                rep = fresh()       # a new replication (building it is inside the timed budget)
+            edges += rep.step().n_edges
+            days += 1
+        conn.send((edges, days, time.perf_counter() - t0))
+
+
 def run_reference(a):
+    """The reference arm: the unmodified reference engine on the host cores.
+    One step = every host process advances its own chain of whole 180-day
+    replications for a bounded slice of time (all processes in parallel);
+    value = directed edges gathered / wall time of the steps."""
     rank, _, world = dist_env()
     if rank != 0:
         return
-    from concurrent.futures import ProcessPoolExecutor
+    import multiprocessing as mp
     cores = os.cpu_count() or 1
-    total_e = total_t = 0.0
-    days_done = []
-    t_all = time.perf_counter()
+    # the whole --steps K --warmup W run within a few minutes
+    per_step = max(2.0, min(a.cpu_seconds / 2, 200.0 / max(1, a.steps + a.warmup)))
+    ctx = mp.get_context("fork")
+    pipes, procs = [], []
+    for w in range(cores):
+        here, there = ctx.Pipe()
+        p = ctx.Process(target=_ref_worker, args=(there, a.workload, a.dose_gap, 7000 + w), daemon=True)
+        p.start()
+        pipes.append(here)
+        procs.append(p)
+    for c in pipes:
+        assert c.recv() == "ready"
     steps = []
+    days_done = 0
     for i in range(a.warmup + a.steps):
         t0 = time.perf_counter()
-        with ProcessPoolExecutor(max_workers=cores) as pool:
-            worker = _cpu_worker_refnet if a.workload == "refnet" else _cpu_worker
-            res = list(pool.map(worker, [(a.workload, 1000 * i + w, a.cpu_seconds / 2)
-                                         for w in range(cores)]))
+        for c in pipes:
+            c.send(per_step)
+        res = [c.recv() for c in pipes]
         wall = time.perf_counter() - t0
         if i >= a.warmup:
-            e = sum(r[0] for r in res)
-            steps.append((e, wall))
-            days_done.append(sum(r[1] for r in res))
-        if time.perf_counter() - t_all > 240:
-            break
-    e = sum(s[0] for s in steps)
-    w = sum(s[1] for s in steps)
+            steps.append((sum(r[0] for r in res), wall))
+            days_done += sum(r[1] for r in res)
+    for c in pipes:
+        c.send(None)
+    for p in procs:
+        p.join(timeout=10)
+    e = sum(s_[0] for s_ in steps)
+    w = sum(s_[1] for s_ in steps)
     v = e / w
+    sample = (f"each step: {cores} processes x {per_step:.1f}s of the unmodified reference engine "
+              f"(epivec.engine.Engine from baseline/_ref, fp64) stepping whole 180-day replications "
+              f"in sequence (graphs: oracle/confignet_np restatement of the config generator); "
+              f"{days_done} simulated days over the timed steps ({days_done / max(1, cores):.0f} "
+              f"per process" + ("; every process covers the whole horizon" if days_done >= cores * HORIZON
+                                else "; early days of the horizon only: a short run") + ")")
     line = {
         "impl": "reference", "metric": "agent-interactions/sec", "value": v,
         "unit": "agent-interactions/s", "n_gpus": a.gpus, "steps": len(steps), "warmup": a.warmup,
         "ms_per_step": 1000 * w / max(1, len(steps)), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": REFNET_DESC if a.workload == "refnet" else
-                   f"{a.workload}: BASELINE.json configs[1], 100k agents, "
-                   "household+workplace+Poisson(5) random network, 100 seeds, no interventions",
-                   "parallelism": f"{cores} host processes x 1 replica each"},
-        "cpu_baseline": {"value": v, "unit": "agent-interactions/s", "cores": cores, "kind": "port",
-                         "sample": f"each step: {cores} replicas x first days of the 180-day sim, "
-                                   f"~{a.cpu_seconds / 2:.0f}s each (days simulated: {days_done})"},
+        "config": {"workload": REFNET_DESC if a.workload == "refnet" else workload_string(a),
+                   "parallelism": f"{cores} host processes"},
+        "cpu_baseline": {"value": v, "unit": "agent-interactions/s", "cores": cores,
+                         "kind": "reference", "sample": sample},
         "e2e": {"value": v, "unit": "agent-interactions/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -210,8 +234,9 @@ def run_reference(a):
 
 def cpu_baseline_single(workload, seconds):
     e, days, t = _cpu_worker((workload, 12345, seconds))
-    return {"value": e / t, "unit": "agent-interactions/s", "cores": 1, "kind": "port",
-            "sample": f"oracle engine_np + confignet_np, 1 replica, days 0-{days - 1} of 180 "
+    return {"value": e / t, "unit": "agent-interactions/s", "cores": 1, "kind": "reference",
+            "sample": f"unmodified reference engine (epivec.engine.Engine, baseline/_ref) on the "
+                      f"restated config generator, 1 replica, days 0-{days - 1} of 180 "
                       f"({e} directed edges in {t:.1f}s), single process"}
 
 
@@ -372,12 +397,7 @@ def run_ours(a):
         "ms_per_step": ms_total / a.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {
-            "workload": (f"config2 (BASELINE.json configs[2]): config 1 + quarantine 14 d, testing "
-                         f"(5 %, 2-day delay), DEN (app 0.5), vaccination 1 %/day, efficacy 0.5/0.9, "
-                         f"dose gap {a.dose_gap} d" if a.workload == "config2" else
-                         f"{a.workload} (BASELINE.json configs[1]): 100k agents, 180 days, "
-                         "households U{1..6} + workplaces U{10..50} x 8 colleague draws + "
-                         "Poisson(5) random contacts, 100 seeds, no interventions"),
+            "workload": workload_string(a),
             "mode": best["mode"], "step": "one full 180-day simulation (CUDA graph replay)",
             "kernel_path": prof.get("path", "one kernel sequence per day"),
             "replicas": f"{a.steps} timed replications per GPU, distinct seeds",
@@ -822,11 +842,12 @@ def run_refnet(a):
         "clocks": clocks,
     }
     if not a.no_cpu_baseline and world == 1:
-        e, days, t = _cpu_worker_refnet(("refnet", 12345, a.cpu_seconds))
+        e, days, t = _cpu_worker(("refnet", 12345, a.cpu_seconds))
         line["cpu_baseline"] = {"value": e / t, "unit": "agent-interactions/s", "cores": 1,
-                                "kind": "port", "sample": f"oracle engine_np + graphs_np reference "
-                                f"realizer, 1 replica, steps 0-{days - 1} of 180 ({e} directed "
-                                f"edges in {t:.1f}s), single process"}
+                                "kind": "reference", "sample": f"the reference's own scenario "
+                                f"(epivec initialize_run + GraphRealizer + Engine, baseline/_ref), "
+                                f"1 replica, steps 0-{days - 1} of 180 ({e} directed edges in "
+                                f"{t:.1f}s), single process"}
     print(json.dumps(line), flush=True)
 
 

@@ -338,7 +338,7 @@ int epi_sim_run(epi_ctx *ctx, const epi_state *st, int32_t first_step, int32_t n
  * on = 0 forces the per-day kernels. */
 int epi_set_persistent(epi_ctx *ctx, int32_t on);
 /* Replication summary (runner.py:195-207 `summarize`): quartiles q25/q50/q75
- * across n_rep <= 4096 replications, bitwise np.percentile (linear method).
+ * across n_rep replications (any count), bitwise np.percentile (linear method).
  * data: device int64 [n_rep][horizon][rec_len] (stacked records), cols:
  * device int32[n_cols] record columns, out: device double
  * [n_cols][horizon][3]. */

@@ -1,6 +1,8 @@
 """CPU restatement of the GPU reference-native generator — TEST INFRASTRUCTURE.
 
 Specification: paper_2110_04421_b200/csrc/epi_refnet.cuh (header comment);
+rewired occupation edges are re-drawn on collision, never dropped, as the
+reference's sequential rejection keeps n*k/2 edges (graphs.py:86-129);
 independent vectorised numpy implementation used as the bitwise checker of
 the CUDA kernels (row f1).  Output: canonical (dst, src, kind) order.
 """
@@ -24,6 +26,46 @@ def _dedupe_min(u, v, idx):
     first[1:] = key[order][1:] != key[order][:-1]
     keep = order[first]
     return u[keep], v[keep]
+
+
+WS_ROUNDS = 64
+
+
+def _rewire_rounds(seed, step, live, idx, p, i, m, half, span):
+    """Rewired lattice edges placed one-for-one (graphs.py:116-128 keeps the
+    undirected edge count at n*k/2): round 0 proposes u_1, the lowest edge
+    index keeps a contested pair; in round r >= 1 every unplaced edge
+    proposes u_{1+r}, pairs placed earlier are taken, the lowest index wins
+    among the round's new pairs; after WS_ROUNDS rounds an edge keeps its
+    lattice pair (p, p + i)."""
+    order = np.argsort(idx, kind="stable")
+    idx, p, i = idx[order], p[order], i[order]
+    taken = set()
+    out_u = np.empty(len(idx), np.int64)
+    out_v = np.empty(len(idx), np.int64)
+    pending = np.arange(len(idx))
+    for r in range(WS_ROUNDS + 1):
+        if not len(pending):
+            break
+        ids = idx[pending]
+        u1 = rng_np.uniforms(seed, step, P_WS, ids, 1 + r)
+        q = (p[pending] + half + 1 + (u1 * span).astype(np.int64)) % m
+        u, v = live[p[pending]], live[q]
+        keys = (np.minimum(u, v).astype(np.int64) << 31) | np.maximum(u, v).astype(np.int64)
+        won = np.zeros(len(pending), bool)
+        seen = set()
+        for t in range(len(pending)):            # ascending edge index
+            k = int(keys[t])
+            if k not in taken and k not in seen:
+                won[t] = True
+            seen.add(k)
+        taken.update(int(k) for k in keys[won])
+        out_u[pending[won]], out_v[pending[won]] = u[won], v[won]
+        pending = pending[~won]
+    if len(pending):                             # no free pair: the lattice pair
+        out_u[pending] = live[p[pending]]
+        out_v[pending] = live[(p[pending] + i[pending]) % m]
+    return out_u, out_v
 
 
 def realize(seed, step, household_id, occupation, random_degree, means, beta, dead):
@@ -63,7 +105,7 @@ def realize(seed, step, household_id, occupation, random_degree, means, beta, de
             q[rew] = (p[rew] + half + 1 + (u1 * span).astype(np.int64)) % m
         u, v = live[p], live[q]
         keep_u, keep_v = u[~rew], v[~rew]
-        ru, rv = _dedupe_min(u[rew], v[rew], idx[rew])
+        ru, rv = _rewire_rounds(seed, step, live, idx[rew], p[rew], i[rew], m, half, span)
         for a, b in ((keep_u, keep_v), (ru, rv)):
             S.append(np.concatenate([a, b])); D.append(np.concatenate([b, a]))
             K.append(np.ones(2 * len(a), np.int8))

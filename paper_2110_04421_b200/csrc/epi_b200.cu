@@ -150,6 +150,9 @@ struct epi_ctx {
   int64_t* row_begin = nullptr;
   int32_t* row_len = nullptr;
   int32_t* row_fill = nullptr;       // graph load: per-row scatter cursors
+  uint32_t* entries_tmp = nullptr;   // graph load: merge scratch of the long-row sort
+  int32_t* long_rows = nullptr;      // graph load: rows of > 32 in-edges (k_rows_sort_long)
+  unsigned* long_count = nullptr;
   void* cub_tmp = nullptr;
   size_t cub_bytes = 0;
   const int32_t *g_src = nullptr, *g_dst = nullptr;   // current graph (device, caller-owned)
@@ -411,6 +414,9 @@ int epi_destroy(epi_ctx* c) {
   cudaFree(c->row_begin);
   cudaFree(c->row_len);
   cudaFree(c->row_fill);
+  cudaFree(c->entries_tmp);
+  cudaFree(c->long_rows);
+  cudaFree(c->long_count);
   cudaFree(c->cub_tmp);
   cudaFree(c->net_dev);
   cudaFree(c->inj_dev);
@@ -500,8 +506,14 @@ static int graph_load_impl(epi_ctx* c, const int32_t* src, const int32_t* dst, c
   if (E > c->edge_cap) {
     int64_t cap = E + E / 4;
     int rc = dalloc(&c->entries, cap);
+    if (!rc) rc = dalloc(&c->entries_tmp, cap);
     if (rc) return rc;
     c->edge_cap = cap;
+  }
+  if (!c->long_rows) {
+    int rc = dalloc(&c->long_rows, (size_t)c->n);
+    if (!rc) rc = dalloc(&c->long_count, 1);
+    if (rc) return rc;
   }
   // counting sort by destination + per-row sorts (canonical order)
   if (!c->row_fill) {   // zero here, and again after every load (k_rows_sort)
@@ -526,9 +538,13 @@ static int graph_load_impl(epi_ctx* c, const int32_t* src, const int32_t* dst, c
   CK(cub::DeviceScan::ExclusiveScan(c->cub_tmp, need, c->row_len, c->row_begin, cuda::std::plus<>{}, (int64_t)0,
                                     (int)c->n, s));
   CK(launch_pdl(k_coo_scatter, dim3(grid_for(E, 256)), dim3(256), 0, s, src, dst, kind, E, c->n,
-                (const int64_t*)c->row_begin, c->row_fill, c->entries, count));
+                (const int64_t*)c->row_begin, c->row_fill, c->entries, count, c->long_count));
   CK(launch_pdl(k_rows_sort, dim3(grid_for(c->n, 128)), dim3(128), 0, s, c->n, (const int64_t*)c->row_begin,
-                (const int32_t*)c->row_len, c->entries, c->row_fill));
+                (const int32_t*)c->row_len, c->entries, c->row_fill, c->long_rows, c->long_count));
+  // rows of more than 32 in-edges: one block each (usually none: the blocks exit at once)
+  CK(launch_pdl(k_rows_sort_long, dim3(sm_count()), dim3(1024), 0, s, (const int64_t*)c->row_begin,
+                (const int32_t*)c->row_len, c->entries, c->entries_tmp, (const int32_t*)c->long_rows,
+                (const unsigned*)c->long_count));
   return 0;
 }
 
@@ -1375,8 +1391,13 @@ int epi_quartiles(const int64_t* data, int64_t n_rep, int32_t horizon, int32_t r
                   int32_t n_cols, double* out, void* stream) {
   if (!data || !cols || !out || n_rep < 1 || horizon < 0 || rec_len < 1 || n_cols < 0)
     return fail(EPI_EARG, "bad argument");
-  if (n_rep > SUMMARY_MAX_R) return fail(EPI_EARG, "more than 4096 replications per summary");
   if (horizon == 0 || n_cols == 0) return 0;
+  if (n_rep > SUMMARY_MAX_R) {
+    k_quartiles_large<<<dim3((unsigned)horizon, (unsigned)n_cols), 1024, 0, S(stream)>>>(data, n_rep, horizon,
+                                                                                        rec_len, cols, out);
+    CKL();
+    return 0;
+  }
   k_quartiles<<<dim3((unsigned)horizon, (unsigned)n_cols), 1024, 0, S(stream)>>>(data, (int)n_rep, horizon, rec_len,
                                                                                   cols, out);
   CKL();
@@ -1590,11 +1611,17 @@ int epi_refnet_create(const epi_refnet_desc* d, epi_refnet_t** out) {
       int64_t stubs = 0;
       for (double x : deg) stubs += (int64_t)std::ceil(x > 0 ? x : 0.0);
       S.max_stubs = stubs;
-      int64_t most = 0;
-      for (int j = 0; j < d->n_occ; ++j)
-        most = std::max(most, (int64_t)(occ_start[j + 1] - occ_start[j]) * std::max(occ_k[j] / 2, 0));
+      int64_t most = 0, lattice = 0;
+      for (int j = 0; j < d->n_occ; ++j) {
+        const int64_t e = (int64_t)(occ_start[j + 1] - occ_start[j]) * std::max(occ_k[j] / 2, 0);
+        most = std::max(most, e);
+        lattice += e;
+      }
+      S.loser_cap = lattice;
+      if (!rc) rc = dalloc(&S.ws_losers, (size_t)lattice + 1);
+      if (!rc) rc = dalloc(&S.n_losers, 1);
       r->ws_blocks = (int)std::min<int64_t>(std::max<int64_t>((most + 255) / 256, 1), 1024);
-      rc = dalloc(&S.stub_owner, (size_t)stubs + 1);
+      if (!rc) rc = dalloc(&S.stub_owner, (size_t)stubs + 1);
       if (!rc) rc = dalloc(&S.pair_uv, (size_t)(stubs / 2) + 1);
     }
   }
@@ -1625,6 +1652,8 @@ int epi_refnet_destroy(epi_refnet_t* r) {
   cudaFree(r->sc.counter);
   cudaFree(r->sc.stub_owner);
   cudaFree(r->sc.pair_uv);
+  cudaFree(r->sc.ws_losers);
+  cudaFree(r->sc.n_losers);
   cudaFree(r->scan_tmp);
   delete r;
   return 0;
@@ -1677,6 +1706,8 @@ static int refnet_realize_impl(epi_refnet_t* r, uint64_t seed, int32_t step, Dea
   const int links = ws_blocks * r->net.n_occ + grid_for(S.max_stubs / 2, 256);
   CK(launch_pdl(k_ref_links<0>, dim3(links), dim3(256), 0, s, r->net, S, ws, K, ws_blocks));
   CK(launch_pdl(k_ref_links<1>, dim3(links), dim3(256), 0, s, r->net, S, ws, K, ws_blocks));
+  // 5: rewired lattice edges whose pair was taken draw again (edge count preserved)
+  if (ws_blocks > 0) CK(launch_pdl(k_ref_ws_resolve, dim3(1), dim3(1024), 0, s, r->net, S, ws));
   if (count_dev) return 0;                  // no synchronisation: count + error bits stay on the device
   unsigned long long h[2] = {0, 0};
   CK(cudaMemcpyAsync(h, S.counter, sizeof(h), cudaMemcpyDeviceToHost, s));
@@ -1685,6 +1716,7 @@ static int refnet_realize_impl(epi_refnet_t* r, uint64_t seed, int32_t step, Dea
   if (h[1] & 1ull) return fail(EPI_EARG, "edge output capacity exceeded");
   if (h[1] & 2ull) return fail(EPI_EARG, "dedupe hash table full");
   if (h[1] & 4ull) return fail(EPI_EARG, "more than 2^31 random-network stubs");
+  if (h[1] & 8ull) return fail(EPI_EARG, "rewiring collision list overflow");
   return 0;
 }
 

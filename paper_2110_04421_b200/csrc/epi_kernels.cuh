@@ -402,9 +402,11 @@ __global__ void k_coo_count(const int32_t* __restrict__ src, const int32_t* __re
 __global__ void k_coo_scatter(const int32_t* __restrict__ src, const int32_t* __restrict__ dst,
                               const int8_t* __restrict__ kind, int64_t E, int64_t n,
                               const int64_t* __restrict__ row_begin, int32_t* __restrict__ fill,
-                              uint32_t* __restrict__ entries, const unsigned long long* __restrict__ count) {
+                              uint32_t* __restrict__ entries, const unsigned long long* __restrict__ count,
+                              unsigned* __restrict__ long_count) {
   pdl_wait();
   pdl_trigger();
+  if (blockIdx.x == 0 && threadIdx.x == 0) *long_count = 0u;   // k_rows_sort lists this load's long rows
   const int64_t live = count ? (int64_t)(*count < (unsigned long long)E ? *count : (unsigned long long)E) : E;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   // 4 edges per thread in flight: loads, then cursors, then stores
@@ -465,9 +467,13 @@ __device__ __forceinline__ void sort_row_regs(uint32_t* row, int len) {
   for (int i = 0; i < W; ++i)
     if (i < len) row[i] = v[i];
 }
-// (also re-zeroes the scatter's fill cursors, so they are zero at the next load)
+// (also re-zeroes the scatter's fill cursors, so they are zero at the next
+// load).  Rows of <= 32 entries are sorted in registers by their thread;
+// longer rows (hubs: a graph-in StepGraph may give one destination 1e5
+// in-edges) are listed for k_rows_sort_long, one block per row.
 __global__ void k_rows_sort(int64_t n, const int64_t* __restrict__ row_begin, const int32_t* __restrict__ row_len,
-                            uint32_t* __restrict__ entries, int32_t* __restrict__ fill) {
+                            uint32_t* __restrict__ entries, int32_t* __restrict__ fill,
+                            int32_t* __restrict__ long_rows, unsigned* __restrict__ long_count) {
   pdl_wait();
   pdl_trigger();
   for (int64_t d = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; d < n; d += (int64_t)gridDim.x * blockDim.x) {
@@ -482,13 +488,87 @@ __global__ void k_rows_sort(int64_t n, const int64_t* __restrict__ row_begin, co
     } else if (len <= 32) {
       sort_row_regs<32>(row, len);
     } else {
-      for (int i = 1; i < len; ++i) {
-        const uint32_t x = row[i];
-        int j = i - 1;
-        while (j >= 0 && row[j] > x) { row[j + 1] = row[j]; --j; }
-        row[j + 1] = x;
-      }
+      long_rows[atomicAdd(long_count, 1u)] = (int32_t)d;
     }
+  }
+}
+
+// Long rows: one 1024-thread block per row.  Tiles of LONG_TILE entries are
+// bitonic-sorted in shared memory, then merged pairwise (merge path: every
+// thread merges a contiguous slice of the output) between the row and a
+// scratch copy, log2(len / LONG_TILE) passes.  O(len log len) per row.
+constexpr int LONG_TILE = 8192;
+__device__ __forceinline__ int merge_path(const uint32_t* a, int la, const uint32_t* b, int lb, int diag) {
+  int lo = diag - lb > 0 ? diag - lb : 0, hi = diag < la ? diag : la;
+  while (lo < hi) {
+    const int i = (lo + hi) >> 1;
+    if (a[i] <= b[diag - 1 - i]) lo = i + 1;
+    else hi = i;
+  }
+  return lo;
+}
+__device__ __forceinline__ void merge_block(const uint32_t* a, int la, const uint32_t* b, int lb, uint32_t* out) {
+  const int total = la + lb;
+  const int chunk = (total + (int)blockDim.x - 1) / (int)blockDim.x;
+  const int d0 = threadIdx.x * chunk;
+  if (d0 >= total) return;
+  const int d1 = d0 + chunk < total ? d0 + chunk : total;
+  int ia = merge_path(a, la, b, lb, d0), ib = d0 - ia;
+  for (int k = d0; k < d1; ++k) {
+    if (ia < la && (ib >= lb || a[ia] <= b[ib])) out[k] = a[ia++];
+    else out[k] = b[ib++];
+  }
+}
+__global__ void __launch_bounds__(1024) k_rows_sort_long(const int64_t* __restrict__ row_begin,
+                                                         const int32_t* __restrict__ row_len,
+                                                         uint32_t* __restrict__ entries, uint32_t* __restrict__ tmp,
+                                                         const int32_t* __restrict__ long_rows,
+                                                         const unsigned* __restrict__ long_count) {
+  __shared__ uint32_t sm[LONG_TILE];
+  pdl_wait();
+  pdl_trigger();
+  const unsigned nl = *long_count;
+  for (unsigned r = blockIdx.x; r < nl; r += gridDim.x) {
+    const int32_t d = long_rows[r];
+    uint32_t* row = entries + row_begin[d];
+    uint32_t* aux = tmp + row_begin[d];
+    const int len = row_len[d];
+    for (int t0 = 0; t0 < len; t0 += LONG_TILE) {
+      const int tl = len - t0 < LONG_TILE ? len - t0 : LONG_TILE;
+      int p2 = 64;
+      while (p2 < tl) p2 <<= 1;
+      for (int i = threadIdx.x; i < p2; i += blockDim.x) sm[i] = i < tl ? row[t0 + i] : ~0u;
+      __syncthreads();
+      for (int k = 2; k <= p2; k <<= 1) {
+        for (int j = k >> 1; j > 0; j >>= 1) {
+          for (int i = threadIdx.x; i < p2; i += blockDim.x) {
+            const int l = i ^ j;
+            if (l > i) {
+              const uint32_t x = sm[i], y = sm[l];
+              if ((x > y) == ((i & k) == 0)) { sm[i] = y; sm[l] = x; }
+            }
+          }
+          __syncthreads();
+        }
+      }
+      for (int i = threadIdx.x; i < tl; i += blockDim.x) row[t0 + i] = sm[i];
+      __syncthreads();
+    }
+    uint32_t* a = row;
+    uint32_t* b = aux;
+    for (int w = LONG_TILE; w < len; w <<= 1) {
+      for (int m0 = 0; m0 < len; m0 += 2 * w) {
+        const int la = len - m0 < w ? len - m0 : w;
+        const int rest = len - m0 - la;
+        const int lb = rest < w ? rest : w;
+        merge_block(a + m0, la, a + m0 + la, lb, b + m0);
+      }
+      __syncthreads();
+      uint32_t* t = a; a = b; b = t;
+    }
+    if (a != row)
+      for (int i = threadIdx.x; i < len; i += blockDim.x) row[i] = a[i];
+    __syncthreads();
   }
 }
 

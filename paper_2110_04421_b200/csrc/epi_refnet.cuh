@@ -8,15 +8,22 @@
 //  * occupation j: ring lattice over its alive members in id order, k =
 //    min(round_to_even(mean_j), 2*floor((m-1)/2)); lattice edge e = (p, p+i),
 //    index e = (i-1)*m + p, is rewired iff u(e) < beta, to the position
-//    p + k/2 + 1 + floor(u'(e) * (m-k-1)) (uniform over p's non-neighbours;
-//    the reference instead rejects self/duplicates sequentially);
+//    p + k/2 + 1 + floor(u_1(e) * (m-k-1)) (uniform over p's non-neighbours);
+//    like the reference (graphs.py:116-128: "rewiring replaces edges
+//    one-for-one, so the undirected edge count is always n*k/2"), a rewired
+//    pair that collides with another is drawn again, never dropped: the
+//    lowest edge index keeps a contested pair, every other contender draws
+//    again from u_{1+r}(e) in round r (k_ref_ws_resolve), and a pair placed
+//    in an earlier round is never taken over.  An edge still unplaced after
+//    WS_ROUNDS draws keeps its lattice pair (the reference's "no free target:
+//    keep v"; free, since rewired targets are never lattice neighbours);
 //  * stub pairing: agent a gets floor(d_a) + [u(a) < frac(d_a)] stubs; stub q
 //    sits at position pi^{-1}(q) of a keyed Feistel permutation of [0, S);
 //    positions (2i, 2i+1) pair up; self pairs are dropped.
-// Duplicate undirected pairs (from rewiring or pairing) are resolved
-// deterministically: a pair survives only for its lowest edge / pair index
-// (atomicMin into an open-addressing hash table), matching the reference's
-// "keep first" rule (graphs.py:161-167) for stub pairs.
+// Duplicate undirected stub pairs are resolved deterministically: a pair
+// survives only for its lowest pair index (atomicMin into an open-addressing
+// hash table), matching the reference's "keep first" rule
+// (graphs.py:161-167).
 #pragma once
 
 #include "epi_confignet.cuh"
@@ -56,6 +63,10 @@ struct RefScratch {
   int32_t* row_len;             // nullable: in-edges per destination of the edges written
                                 // (the graph load's row lengths; the households kernel
                                 // initialises every row)
+  unsigned long long* ws_losers;  // rewired lattice edges that lost their first pair (edge
+                                  // index; ~0 once placed), appended by launch 4
+  unsigned* n_losers;             // zeroed by launch 1
+  int64_t loser_cap;              // the lattice edges of all occupations
 };
 
 __device__ __forceinline__ double ref_u(uint64_t prefix, uint64_t idx, uint64_t k) {
@@ -127,7 +138,10 @@ __global__ void k_ref_agents(RefNet net, DeadView dead, RefScratch S, uint64_t s
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   ulonglong2* tab = reinterpret_cast<ulonglong2*>(S.table);
   for (int64_t i = tid; i < S.table_slots; i += stride) tab[i] = make_ulonglong2(~0ull, ~0ull);
-  if (tid == 0) S.stub_count[net.n_agents] = 0;
+  if (tid == 0) {
+    S.stub_count[net.n_agents] = 0;
+    *S.n_losers = 0u;
+  }
   for (int64_t b0 = (int64_t)blockIdx.x * blockDim.x; b0 < net.n_agents; b0 += stride) {
     const int64_t b = b0 + threadIdx.x;
     const bool in = b < net.n_agents;
@@ -269,14 +283,103 @@ __device__ __forceinline__ void ws_block(const RefNet& net, const RefScratch& S,
         emit = PASS == 1;
       } else {
         const uint64_t key = pair_key((uint32_t)u, (uint32_t)v, 1);
-        if (PASS == 0) table_insert(S, key, idx);
-        else emit = table_is_winner(S, key, idx);
+        if (PASS == 0) {
+          table_insert(S, key, idx);
+        } else {
+          emit = table_is_winner(S, key, idx);
+          if (!emit) {                   // drawn again by k_ref_ws_resolve
+            const unsigned at = atomicAdd(S.n_losers, 1u);
+            if (at < S.loser_cap) S.ws_losers[at] = idx;
+            else atomicOr(&S.counter[1], 8ull);
+          }
+        }
       }
     }
     if (PASS == 1) {
       const int64_t at = reserve_block(S.counter, emit ? 2 : 0);
       if (emit) emit2(S, at, u, v, 1);
     }
+  }
+}
+
+// Launch 5: the rewired lattice edges whose first pair was taken draw
+// again, in rounds r = 1, 2, ... (one block; a handful of edges per step).
+// Round r: every unplaced edge proposes the pair of draw u_{1+r} and inserts
+// it with value r << 56 | edge index, so a pair placed in an earlier round
+// (smaller value) is never taken over and the lowest index wins among the
+// round's contenders; the winners are emitted.  Phases of a round are
+// separated by bar.sync; table words written in this launch are read with
+// ld.cg (the atomics are performed in L2).
+constexpr int WS_ROUNDS = 64;
+__global__ void __launch_bounds__(1024) k_ref_ws_resolve(RefNet net, RefScratch S, uint64_t ws_prefix) {
+  pdl_wait();
+  pdl_trigger();
+  const unsigned nl0 = *S.n_losers;
+  const unsigned nl = nl0 < S.loser_cap ? nl0 : (unsigned)S.loser_cap;
+  if (nl == 0) return;
+  // the proposal of loser li in round r (u, v, key, value)
+  auto propose = [&](unsigned li, int r, int32_t& u, int32_t& v, uint64_t& key, uint64_t& val) {
+    const uint64_t idx = S.ws_losers[li];
+    const int j = (int)(idx >> 40) - 1;
+    const int64_t e = (int64_t)(idx & ((1ull << 40) - 1));
+    const int lo = net.occ_start[j];
+    const int m = S.occ_live[j];
+    const int kmax = 2 * ((m - 1) / 2);
+    const int k = net.occ_k[j] < kmax ? net.occ_k[j] : kmax;
+    const int half = k / 2, span = m - k - 1;
+    const int i = (int)(e / m) + 1, p = (int)(e % m);
+    int q = (p + i) % m;                                        // r < 0: the lattice pair
+    if (r >= 0) q = (int)((p + half + 1 + (int)(ref_u(ws_prefix, idx, 1 + (uint64_t)r) * span)) % m);
+    u = S.live_members[lo + p];
+    v = S.live_members[lo + q];
+    key = pair_key((uint32_t)u, (uint32_t)v, 1);
+    val = ((uint64_t)(r < 0 ? 0 : r) << 56) | idx;
+  };
+  for (int r = 1; r <= WS_ROUNDS; ++r) {
+    for (unsigned li = threadIdx.x; li < nl; li += blockDim.x) {
+      if (S.ws_losers[li] == ~0ull) continue;
+      int32_t u, v; uint64_t key, val;
+      propose(li, r, u, v, key, val);
+      table_insert(S, key, val);
+    }
+    __syncthreads();
+    int left = 0;
+    for (unsigned b0 = 0; b0 < nl; b0 += blockDim.x) {          // block-uniform trips
+      const unsigned li = b0 + threadIdx.x;
+      bool won = false;
+      int32_t u = 0, v = 0;
+      if (li < nl && S.ws_losers[li] != ~0ull) {
+        uint64_t key, val;
+        propose(li, r, u, v, key, val);
+        uint64_t h = hash_slot(key, S.table_slots);
+        for (int64_t probe = 0; probe < S.table_slots; ++probe) {
+          const unsigned long long kk = __ldcg(S.table + 2 * h);
+          if (kk == key) { won = __ldcg(S.table + 2 * h + 1) == val; break; }
+          if (kk == ~0ull) break;
+          h = (h + 1) & (uint64_t)(S.table_slots - 1);
+        }
+        left += won ? 0 : 1;
+      }
+      const int64_t at = reserve_block(S.counter, won ? 2 : 0);
+      if (won) {
+        emit2(S, at, u, v, 1);
+        S.ws_losers[li] = ~0ull;
+      }
+    }
+    if (!__syncthreads_or(left)) return;
+  }
+  // no free pair in WS_ROUNDS draws: the lattice pair (never proposed by a
+  // rewired edge, so never taken)
+  for (unsigned b0 = 0; b0 < nl; b0 += blockDim.x) {
+    const unsigned li = b0 + threadIdx.x;
+    const bool keep = li < nl && S.ws_losers[li] != ~0ull;
+    int32_t u = 0, v = 0;
+    if (keep) {
+      uint64_t key, val;
+      propose(li, -1, u, v, key, val);
+    }
+    const int64_t at = reserve_block(S.counter, keep ? 2 : 0);
+    if (keep) emit2(S, at, u, v, 1);
   }
 }
 

@@ -101,6 +101,16 @@ class GpuEngine:
         self._vax = torch.zeros(1, dtype=torch.int32, device=self.device)
         self._rec = torch.zeros(N.REC_LEN, dtype=torch.int64, device=self.device)
 
+    def invalidate(self, why: str) -> None:
+        """Refuse every later step: a failure was detected after the state
+        had already moved on (a device-side loop checked at its end)."""
+        self._invalid = why
+
+    def _usable(self):
+        why = getattr(self, "_invalid", None)
+        if why:
+            raise InvariantViolation(f"engine state is invalid ({why}); rebuild it")
+
     def __del__(self):
         ctx = getattr(self, "_ctx", None)
         if ctx is not None and ctx.value:
@@ -143,7 +153,7 @@ class GpuEngine:
     # -- graph upload + validation (engine.py:124-133) ----------------------
     def _load(self, graph, check: bool = True):
         import torch
-        if graph.on_device:
+        if _on_device(graph):
             src, dst, kind = graph.src, graph.dst, graph.kind
         else:
             src = torch.from_numpy(np.ascontiguousarray(graph.src, np.int32)).to(self.device)
@@ -166,8 +176,8 @@ class GpuEngine:
         if f & N.FLAG_INDEX:
             if graph is None:
                 raise InvariantViolation(f"a graph references an agent >= n_agents {self.n}")
-            h = graph.to_host()
-            top = max(int(np.max(h.src)), int(np.max(h.dst)))
+            src, dst = _host(graph.src), _host(graph.dst)
+            top = max(int(np.max(src)), int(np.max(dst)))
             raise InvariantViolation(f"graph references agent {top} >= n_agents {self.n}")
         if f & N.FLAG_SELFLOOP:
             raise InvariantViolation("graph contains a self-loop")
@@ -200,6 +210,7 @@ class GpuEngine:
 
     # -- the step (engine.py:121-151) -----------------------------------------
     def step(self, graph, injected=None) -> StepEvents:
+        self._usable()
         if graph.step != self.clock:
             raise InvariantViolation(
                 f"graph built for step {graph.step}, engine clock is {self.clock}")
@@ -216,8 +227,9 @@ class GpuEngine:
             self.sync_to_host()
         if self.contact_log is not None:
             self.contact_log._pushed()
-        if self.check:
-            _raise_for_flags(int(rec[N.REC["flags"]]), self.clock, self.n)
+        # a negative hazard is always an error (engine.py:157-158); the state
+        # invariants (state.py:90-102) only when checking
+        _raise_for_flags(int(rec[N.REC["flags"]]), self.clock, self.n, self.check)
         ev = StepEvents.from_record(rec)
         self.clock += 1
         return ev
@@ -227,6 +239,7 @@ class GpuEngine:
         day's record goes to the device int64[EPI_REC_LEN] tensor `record`
         (StepEvents.from_record reads it later); graph validation flags
         accumulate until `check_graph_flags()`."""
+        self._usable()
         if graph.step != self.clock:
             raise InvariantViolation(
                 f"graph built for step {graph.step}, engine clock is {self.clock}")
@@ -245,6 +258,7 @@ class GpuEngine:
         (device uint64) entries of the device arrays src/dst/kind are the
         step's edges — no host synchronisation at all (a realizer loop can be
         captured in a CUDA graph).  Graph flags accumulate as in advance()."""
+        self._usable()
         if step != self.clock:
             raise InvariantViolation(f"graph built for step {step}, engine clock is {self.clock}")
         if not self.resident:
@@ -264,6 +278,7 @@ class GpuEngine:
         synchronisation.  counts = device int64[last-first][2] (edges, realizer
         error bits), records = device int64[last-first][REC_LEN]."""
         import torch
+        self._usable()
         if first != self.clock:
             raise InvariantViolation(f"graph built for step {first}, engine clock is {self.clock}")
         if not self.resident:
@@ -281,6 +296,7 @@ class GpuEngine:
 
     def step_with_hazard(self, hazard, injected=None) -> StepEvents:
         """Phases 1-6 with a caller-supplied float64 hazard (parity tests)."""
+        self._usable()
         import torch
         if not self.resident:
             self.sync_to_device()
@@ -293,6 +309,7 @@ class GpuEngine:
         rec = self._rec.cpu().numpy()
         if not self.resident:
             self.sync_to_host()
+        _raise_for_flags(int(rec[N.REC["flags"]]), self.clock, self.n, self.check)
         ev = StepEvents.from_record(rec)
         self.clock += 1
         return ev
@@ -301,9 +318,21 @@ class GpuEngine:
         return self._rec.cpu().numpy()
 
 
-def _raise_for_flags(f: int, step: int, n: int) -> None:
+def _on_device(graph) -> bool:
+    """Any StepGraph-shaped object: the reference's (numpy arrays,
+    graphs.py:30-51) or this package's (numpy or CUDA tensors)."""
+    return not isinstance(graph.src, np.ndarray) and hasattr(graph.src, "data_ptr")
+
+
+def _host(a) -> np.ndarray:
+    return a.cpu().numpy() if hasattr(a, "cpu") else np.asarray(a)
+
+
+def _raise_for_flags(f: int, step: int, n: int, check: bool = True) -> None:
     if f & N.FLAG_NEG_HAZARD:
         raise InvariantViolation("negative hazard out of gather")
+    if not check:
+        return
     if f & N.FLAG_STAGE_RANGE:
         raise InvariantViolation(f"step {step}: stage out of range")
     if f & N.FLAG_NO_TIMESTAMP:

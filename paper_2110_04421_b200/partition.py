@@ -80,6 +80,15 @@ class PartitionPlan:
         return lo, min(self.n_agents, lo + self.chunk)
 
 
+def _or_fold(parts):
+    """Bitwise OR of equally shaped integer tensors (the EPI_REC_FLAGS bits)."""
+    import torch
+    out = parts[0].clone()
+    for p in parts[1:]:
+        out = torch.bitwise_or(out, p)
+    return out
+
+
 class NcclCodeExchange:
     """All-gather of each rank's code chunk through a torch.distributed group."""
 
@@ -146,14 +155,18 @@ class NcclCodeExchange:
         t.copy_(acc)
 
     def reduce_records(self, rec):
-        """Sum the per-rank partial day records (step column kept)."""
+        """Sum the per-rank partial day records (step column kept; the flag
+        column is a bitmask, OR-ed: NCCL has no bitwise-or reduction, so the
+        flags are all-gathered and folded)."""
+        import torch
         import torch.distributed as dist
         step = rec[:, N.REC["step"]].clone()
         flags = rec[:, N.REC["flags"]].clone()
         dist.all_reduce(rec, group=self.group)
         rec[:, N.REC["step"]] = step
-        dist.all_reduce(flags, op=dist.ReduceOp.MAX, group=self.group)
-        rec[:, N.REC["flags"]] = flags
+        parts = [torch.empty_like(flags) for _ in range(self.plan.world)]
+        dist.all_gather(parts, flags, group=self.group)
+        rec[:, N.REC["flags"]] = _or_fold(parts)
         return rec
 
 
@@ -182,6 +195,7 @@ class LocalCodeExchange:
         for s in sims[1:]:
             out += s.rec
         out[:, N.REC["step"]] = sims[0].rec[:, N.REC["step"]]
+        out[:, N.REC["flags"]] = _or_fold([s.rec[:, N.REC["flags"]] for s in sims])
         return out
 
 

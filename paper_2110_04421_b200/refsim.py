@@ -98,14 +98,25 @@ class ReferenceNativeSimulation:
         error bits, and return their StepEvents."""
         first, last, counts = handle
         self.engine.check_graph_flags()
-        err = int(np.bitwise_or.reduce(counts[:, 1].cpu().numpy()))
-        if err & 1:
-            raise ConfigError("edge output capacity exceeded")
-        if err & 2:
-            raise ConfigError("dedupe hash table full")
-        if err & 4:
-            raise ConfigError("more than 2^31 random-network stubs")
+        errs = counts[:, 1].cpu().numpy() if last > first else np.zeros(0, np.int64)
+        bad = np.flatnonzero(errs)
+        if len(bad):
+            # the reference raises at the step that fails; here the steps after
+            # it already ran on a truncated graph: the state is unusable
+            t = first + int(bad[0])
+            err = int(errs[bad[0]])
+            what = ("edge output capacity exceeded" if err & 1 else "dedupe hash table full" if err & 2
+                    else "more than 2^31 random-network stubs" if err & 4
+                    else "rewiring collision list overflow")
+            self.engine.invalidate(f"realizer failed at step {t}: {what}")
+            raise ConfigError(f"step {t}: {what} (state invalid; rebuild the simulation)")
         rec = self.records[first:last].cpu().numpy()
+        neg = rec[:, N.REC["flags"]] & N.FLAG_NEG_HAZARD
+        if neg.any():
+            t = first + int(np.flatnonzero(neg)[0])
+            self.engine.invalidate(f"negative hazard at step {t}")
+            from .errors import InvariantViolation
+            raise InvariantViolation(f"step {t}: negative hazard out of gather")
         events = [StepEvents.from_record(r) for r in rec]
         self.interactions += sum(ev.n_edges for ev in events)
         return events

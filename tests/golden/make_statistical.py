@@ -15,7 +15,9 @@ them; DEN apps as runner.py:86-89.  Replication r uses seed
 replication_seed(1, r); the GPU side of the test uses replication_seed(0, r)
 (independent seeds).
 
-Run in the build container (needs /root/reference):
+The driver is `oracle/epivec_driver.ReferenceReplica` (shared with bench.py's
+reference arm).  Run in the build container (needs /root/reference or
+baseline/_ref):
     PYTHONPATH=/root/reference/pkg/src python tests/golden/make_statistical.py [case ...]
 """
 
@@ -44,67 +46,15 @@ CASES = {
 }
 
 
-def reference_interventions(enabled, gap):
-    """BASELINE.json configs[2] through the reference's own classes
-    (SURVEY §8(d) mapping)."""
-    from epivec.interventions import DenConfig, InterventionConfig, TestKind, VaccinePolicy
-    if not enabled:
-        return InterventionConfig()
-    return InterventionConfig(quarantine_enabled=True, testing_enabled=True,
-                              test_kind=TestKind("cfg2", 0.05, 2, 2), den_enabled=True,
-                              den=DenConfig(0.5), vaccination_enabled=True,
-                              vaccine=VaccinePolicy(daily_rate=0.01, dose1_efficacy=0.5,
-                                                    dose2_efficacy=0.9, dose_gap=gap))
-
-
-def reference_defaults():
-    from epivec.scenario import default_scenario
-    sc = default_scenario()
-    return sc.disease, sc.progression
-
-
 def one_replica(args):
     case, r = args
-    from epivec import rng as keyed
-    from epivec.engine import Engine
-    from epivec.graphs import StepGraph
-    from epivec.rng import Purpose
-    from epivec.runner import CSV_COLUMNS, _record_row, replication_seed
-    from epivec.state import AgentColumns
-    from oracle import confignet_np
-    from paper_2110_04421_b200.confignet import ConfigNetworkSpec, synthesize
-
+    from epivec.runner import replication_seed
+    from oracle.epivec_driver import ReferenceReplica, reference_interventions
+    from paper_2110_04421_b200.confignet import ConfigNetworkSpec
     cfg, iv_on, gap = CASES[case]
-    spec = ConfigNetworkSpec.config(cfg)
-    pop = synthesize(spec, 0)
-    seed = replication_seed(1, r)
-    disease, table = reference_defaults()
-    iv = reference_interventions(iv_on, gap)
-    n = spec.n_agents
-    cols = AgentColumns.allocate(n)
-    cols.age_band[:] = pop.age_band
-    cols.household_id[:] = pop.household_id
-    cols.occupation[:] = (pop.wp_id >= 0).astype(np.int16)
-    cols.random_degree[:] = spec.random_mean
-    ids = np.sort(pop.seeds.astype(np.int64))
-    entry = table.entry_stages(cols.age_band[ids], keyed.uniforms(seed, 0, Purpose.ENTRY_STAGE, ids))
-    cols.stage[ids] = entry
-    cols.infected_at[ids] = 0
-    nxt, delay = table.schedule_transitions(
-        entry, cols.age_band[ids], keyed.uniforms(seed, 0, Purpose.PROGRESSION_BRANCH, ids),
-        keyed.uniforms(seed, 0, Purpose.PROGRESSION_DELAY, ids))
-    cols.next_stage[ids] = nxt
-    cols.next_transition_at[ids] = delay
-    if iv.den_enabled:
-        u = keyed.uniforms(seed, 0, Purpose.DEN_APP, np.arange(n, dtype=np.int64))
-        cols.has_den_app[:] = u < iv.den.app_adoption
-    eng = Engine(cols, disease, table, iv, seed, check_invariants=False)
-    data = np.zeros((HORIZON, len(CSV_COLUMNS)), dtype=np.int64)
-    for t in range(HORIZON):
-        s, d, k = confignet_np.realize(pop, seed, t, cols.stage == 10, canonical=False)
-        ev = eng.step(StepGraph(t, s, d, k))
-        _record_row(data, t, cols, ev)
-    return r, data.astype(np.int32)
+    rep = ReferenceReplica(ConfigNetworkSpec.config(cfg), replication_seed(1, r),
+                           reference_interventions(iv_on, gap))
+    return r, rep.run(HORIZON).astype(np.int32)
 
 
 def main(cases):

@@ -214,3 +214,76 @@ def test_gather_canonical_order_on_skewed_rows(seed):
     want = engine_np.hazard(cols, tr.disease, 6, g, True)
     assert np.count_nonzero(want) > n // 4
     assert np.array_equal(eng.gather_exposure(g), want)
+
+
+def test_gather_canonical_order_on_hub_rows():
+    """Hubs: rows of 33 .. 100 000 in-edges go to the block sort
+    (k_rows_sort_long: shared-memory bitonic tiles + merge-path passes); the
+    fp64 hazard, summed in canonical (dst, src, kind) order, stays bitwise
+    equal to the oracle's lexsort + bincount (engine.py:98-108)."""
+    tr = Trajectory("noiv")
+    rng = np.random.default_rng(5)
+    n = 200_000
+    cols = AgentColumns.allocate(n)
+    long = [33, 64, 100, 1000, 8191, 8192, 8193, 20_000, 100_000]
+    inf = rng.random(n) < 0.3
+    inf[:len(long)] = False                               # the hubs are susceptible targets
+    cols.stage[inf] = int(Stage.MILD_SYMPTOMATIC)
+    cols.infected_at[inf] = rng.integers(0, 6, int(inf.sum()))
+    cols.next_stage[inf] = int(Stage.RECOVERED)
+    cols.next_transition_at[inf] = 10_000
+    cols.age_band[:] = rng.integers(0, 9, n)
+    lens = np.concatenate([long, rng.integers(0, 12, n - len(long))])
+    dst = np.repeat(np.arange(n, dtype=np.int32), lens)
+    src = rng.integers(0, n - 1, len(dst)).astype(np.int32)
+    src[src >= dst] += 1
+    kind = rng.integers(0, 3, len(dst)).astype(np.int8)
+    p = rng.permutation(len(dst))
+    g = StepGraph(6, src[p], dst[p], kind[p])
+    eng = GpuEngine(cols.copy(), tr.disease, tr.table, InterventionConfig(), 0)
+    eng.clock = 6
+    want = engine_np.hazard(cols, tr.disease, 6, g, True)
+    got = eng.gather_exposure(g)
+    assert np.count_nonzero(want[:len(long)]) == len(long)
+    assert np.array_equal(got, want), np.flatnonzero(got != want)[:10]
+    # a second load on the same engine (long-row list reset between loads)
+    g2 = StepGraph(6, src[::-1].copy(), dst[::-1].copy(), kind[::-1].copy())
+    assert np.array_equal(eng.gather_exposure(g2), want)
+
+
+@pytest.mark.parametrize("case", ["stage_range", "no_timestamp", "neg_hazard"])
+def test_invariant_flags_raise(case):
+    """state.py:90-102 through the device flags (rec_agent -> EPI_REC_FLAGS):
+    a stage outside 0..10 and a non-susceptible, non-vaccinated agent without
+    an infection timestamp raise InvariantViolation when checking (and pass
+    silently when not, as the reference's check_invariants=False); a negative
+    hazard (engine.py:157-158) raises in every mode."""
+    tr = Trajectory("noiv")
+    for check in (True, False):
+        cols = AgentColumns.allocate(64)
+        if case == "stage_range":
+            cols.stage[5] = 11
+        elif case == "no_timestamp":
+            cols.stage[9] = int(Stage.RECOVERED)          # infected_at stays NEVER
+        eng = GpuEngine(cols, tr.disease, tr.table, InterventionConfig(), 0, check_invariants=check)
+        if case == "neg_hazard":
+            hz = np.zeros(64)
+            hz[3] = -1e-3
+            with pytest.raises(InvariantViolation, match="negative hazard"):
+                eng.step_with_hazard(hz)
+            continue
+        msg = "stage out of range" if case == "stage_range" else "without infection timestamp"
+        if check:
+            with pytest.raises(InvariantViolation, match=msg):
+                eng.step(StepGraph.empty(0))
+        else:
+            eng.step(StepGraph.empty(0))
+            assert eng.clock == 1
+
+
+def test_engine_refuses_steps_after_invalidation():
+    tr = Trajectory("noiv")
+    eng = GpuEngine(AgentColumns.allocate(8), tr.disease, tr.table, InterventionConfig(), 0)
+    eng.invalidate("realizer failed at step 0: edge output capacity exceeded")
+    with pytest.raises(InvariantViolation, match="invalid"):
+        eng.step(StepGraph.empty(0))

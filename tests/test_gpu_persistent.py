@@ -142,7 +142,7 @@ def test_reset_after_a_partial_run_equals_a_fresh_run(iv_on):
     """A run stopped on an odd day leaves tomorrow's push-table scatter in the
     odd parity; reset() + run() must not see it (the chain start clears both
     parities).  Regression: day 1 of the rerun used to read stale rin rows."""
-    from tests.test_gpu_fused_lambda import config2_interventions
+    from test_gpu_fused_lambda import config2_interventions
     spec = ConfigNetworkSpec.config(1, n_agents=20_011, initial_infections=200)
     iv = config2_interventions() if iv_on else InterventionConfig()
     mk = lambda: ConfigSimulation(synthesize(spec, 5), default_disease(), default_progression(), iv, 9,

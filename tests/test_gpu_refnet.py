@@ -96,8 +96,9 @@ def test_family_sizes_match_reference_generator():
         counts_ref += np.bincount(ref.realize(t, dead)[2], minlength=3)
         counts_gpu += np.bincount(canon(r.realize(t, dead))[2], minlength=3)
     assert counts_gpu[0] == counts_ref[0]
-    # reference rejects duplicate rewires; this algorithm drops them (~beta^2 k/m)
-    assert abs(counts_gpu[1] - counts_ref[1]) <= 0.002 * counts_ref[1]
+    # both preserve every lattice edge one-for-one (graphs.py:91-93): n*k/2
+    # per occupation, exactly
+    assert counts_gpu[1] == counts_ref[1]
     # stub pairing: same stub law, same self/duplicate rules
     assert abs(counts_gpu[2] - counts_ref[2]) <= 0.01 * counts_ref[2]
 
@@ -163,3 +164,76 @@ def test_engine_on_device_graphs_bitwise_vs_oracle(name):
     for c in ("stage", "infected_at", "next_stage", "next_transition_at", "quarantine_until",
               "vaccine_status", "immune"):
         assert np.array_equal(getattr(cols_g, c), getattr(cols_o, c)), c
+
+
+# -- Watts-Strogatz properties of the reference's own tests, on the device ----
+# (test_graphs.py:68-114; adjacency_sets / mean_clustering restated from
+# test_graphs.py:16-40 as the brute-force oracle)
+
+def adjacency_sets(us, vs, n):
+    adj = [set() for _ in range(n)]
+    for u, v in zip(us.tolist(), vs.tolist()):
+        adj[u].add(v)
+        adj[v].add(u)
+    return adj
+
+
+def mean_clustering(adj):
+    coeffs = []
+    for nbrs in adj:
+        d = len(nbrs)
+        if d < 2:
+            coeffs.append(0.0)
+            continue
+        nb = sorted(nbrs)
+        links = sum(1 for i, a in enumerate(nb) for b in nb[i + 1:] if b in adj[a])
+        coeffs.append(2.0 * links / (d * (d - 1)))
+    return float(np.mean(coeffs))
+
+
+def one_occupation(n, k, beta, seed):
+    """n agents, every one in occupation 1 (mean k), alone in its household,
+    no random contacts: the realizer's graph is one small-world lattice."""
+    hh = np.arange(n, dtype=np.int64)
+    occ = np.ones(n, dtype=np.int8)
+    deg = np.zeros(n, dtype=np.float32)
+    return realizer(hh, occ, deg, seed, means=[float(k)], beta=beta), (hh, occ, deg)
+
+
+@pytest.mark.parametrize("n,half_k,beta,seed", [
+    (6, 1, 1.0, 0), (7, 2, 1.0, 3), (10, 2, 1.0, 1), (13, 1, 0.5, 5), (20, 2, 1.0, 8),
+    (33, 2, 0.1, 2), (60, 2, 1.0, 9), (60, 1, 0.5, 4), (1000, 3, 1.0, 6), (4000, 5, 0.1, 7)])
+def test_rewiring_never_changes_edge_count(n, half_k, beta, seed):
+    """test_graphs.py:76-92: len == n*k/2, no self loops, no duplicate pairs
+    -- for the device realizer, at every step, dead agents included; and
+    bitwise equal to the restatement (collisions re-drawn in rounds)."""
+    k = 2 * half_k
+    r, (hh, occ, deg) = one_occupation(n, k, beta, seed)
+    for step in range(8):
+        dead = np.zeros(n, bool)
+        if step >= 4:
+            dead[np.random.default_rng(step).random(n) < 0.1] = True
+        m = int((~dead).sum())
+        kk = min(k, 2 * ((m - 1) // 2))
+        s, d, kd = canon(r.realize(step, dead))
+        assert np.all(kd == 1)
+        want = m * kk // 2 if (m >= 3 and kk >= 2) else 0
+        assert len(s) == 2 * want, (step, len(s), 2 * want)
+        assert not np.any(s == d)
+        key = s.astype(np.int64) << 32 | d
+        assert len(np.unique(key)) == len(key)
+        ref = refnet_np.realize(seed, step, hh, occ, deg, [float(k)], beta, dead)
+        for a, b in zip((s, d, kd), ref):
+            assert np.array_equal(a, b), step
+
+
+def test_clustering_between_lattice_and_random():
+    """test_graphs.py:104-114 on the device realizer: 1000 nodes, k = 6."""
+    n, k = 1000, 6
+    values = {}
+    for beta in (0.0, 0.1, 1.0):
+        r, _ = one_occupation(n, k, beta, 7)
+        s, d, _ = canon(r.realize(0, np.zeros(n, bool)))
+        values[beta] = mean_clustering(adjacency_sets(s, d, n))
+    assert values[0.0] == pytest.approx(0.6, abs=1e-12)      # 3(k-2)/(4(k-1))
+    assert values[0.0] > values[0.1] > values[1.0]

@@ -56,3 +56,14 @@ def test_device_quartiles_of_simulation_records(R):
     s = summarize_device(stacked)
     ref = series_np.summarize_stacked(stacked.cpu().numpy())
     assert np.array_equal(np.stack([s[m] for m in SUMMARY_METRICS]), ref)
+
+
+@pytest.mark.parametrize("R,hi", [(4097, 100_000), (10_000, 7), (65_536, 2**40)])
+def test_device_quartiles_beyond_4096_replications(R, hi):
+    """More replications than the shared-memory sort holds: the
+    bisection kernel (k_quartiles_large) is bitwise np.percentile, ties and
+    wide values included."""
+    data = np.random.default_rng(R).integers(0, hi, size=(R, 6, 19), dtype=np.int64)
+    s = summarize_device(torch.from_numpy(data).cuda())
+    ref = series_np.summarize_stacked(data)
+    assert np.array_equal(np.stack([s[m] for m in SUMMARY_METRICS]), ref)

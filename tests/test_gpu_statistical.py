@@ -50,7 +50,7 @@ def _gpu_series(case):
     from paper_2110_04421_b200.interventions import InterventionConfig
     from paper_2110_04421_b200.keyed import replication_seed
     from paper_2110_04421_b200.sim import ConfigSimulation
-    from tests.test_gpu_fused_lambda import config2_interventions
+    from test_gpu_fused_lambda import config2_interventions
     cfg, iv_on, gap = CASES[case]
     pop = synthesize(ConfigNetworkSpec.config(cfg), 0)
     iv = config2_interventions(gap) if iv_on else InterventionConfig()

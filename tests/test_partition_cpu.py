@@ -46,7 +46,8 @@ def _worker(rank, world, port, n, q):
     rec = torch.zeros((4, N.REC_LEN), dtype=torch.int64)
     rec[:, N.REC["step"]] = torch.arange(4)
     rec[:, N.REC["edges"]] = 10 * (rank + 1)
-    rec[:, N.REC["flags"]] = rank
+    rec[:, N.REC["flags"]] = 8 << rank              # distinct flag bits per rank (a bitmask column)
+    rec[0, N.REC["flags"]] = 8                      # the same bit on both ranks on day 0
     ex.reduce_records(rec)
     # in-step exchanges of DEN / vaccination (row f2)
     flags = torch.zeros(n, dtype=torch.uint8)
@@ -95,4 +96,22 @@ def test_code_exchange_and_record_reduction_gloo_world2(n):
         assert np.array_equal(codes[:n], want)
         assert np.array_equal(rec[:, N.REC["step"]], np.arange(4))
         assert np.all(rec[:, N.REC["edges"]] == 30)
-        assert np.all(rec[:, N.REC["flags"]] == 1)
+        assert np.array_equal(rec[:, N.REC["flags"]], [8, 24, 24, 24])   # OR, not MAX / sum
+
+
+def test_local_exchange_ors_the_flag_column():
+    """the emulated ranks' record reduction ORs EPI_REC_FLAGS
+    (8 + 8 must stay 8, not become 16 = another flag)."""
+    from types import SimpleNamespace
+    from paper_2110_04421_b200.partition import LocalCodeExchange
+    recs = []
+    for r, fl in enumerate((8, 8 | 32)):
+        rec = torch.zeros((3, N.REC_LEN), dtype=torch.int64)
+        rec[:, N.REC["step"]] = torch.arange(3)
+        rec[:, N.REC["edges"]] = 5
+        rec[:, N.REC["flags"]] = fl
+        recs.append(SimpleNamespace(rec=rec))
+    out = LocalCodeExchange.reduce_records(recs)
+    assert torch.all(out[:, N.REC["flags"]] == 40)
+    assert torch.all(out[:, N.REC["edges"]] == 10)
+    assert torch.equal(out[:, N.REC["step"]], torch.arange(3))
