@@ -55,6 +55,8 @@ def parse():
                          "stream (default), or per-day kernels of replicas on concurrent streams")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-partition", action="store_true",
+                    help="skip the config-3 agent-range partition measured beside the headline")
     ap.add_argument("--no-message-pass", action="store_true",
                     help="skip the 10M-agent message-pass roofline probe")
     return ap.parse_args()
@@ -389,6 +391,11 @@ def run_ours(a):
             roof["traffic"] = tr["dram_bytes_read"] + tr["dram_bytes_write"]
             roof["traffic_source"] = tr["source"]
 
+    # north_star's multi-GPU path: config 3 partitioned over the same ranks
+    # (strong scaling), measured beside the headline at every N
+    part = None
+    if not a.no_partition and a.workload == "config1":
+        part = measure_partition(min(a.steps, 5), min(a.warmup, 2) or 1, rank, local_rank, world, dist)
     if rank != 0:
         return
     line = {
@@ -420,6 +427,8 @@ def run_ours(a):
     }
     if not a.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline_single(a.workload, a.cpu_seconds)
+    if part is not None:
+        line["partition_config3"] = part
     if not a.no_message_pass and world == 1:
         # north-star part (a) alone at BASELINE config-3 scale (10M agents):
         # the HBM-bound kernel of the decomposition, streamed 16-bit messages
@@ -602,69 +611,93 @@ def end_to_end(sim, a):
             "edges_per_step": edges}
 
 
-def run_config3(a):
-    """10M agents, agent-range partition over the ranks (NCCL code all-gather)."""
+def measure_partition(steps, warmup, rank, local_rank, world, dist):
+    """Config 3 (10M agents, config-1 networks, 180 days): one simulation
+    partitioned by agent range over the `world` ranks (strong scaling), the
+    per-day code all-gather over native NCCL inside the native day loop, the
+    whole run captured as one CUDA graph per rank; 1 rank = the whole
+    population on one GPU.  Device time, max over the ranks."""
     import torch
     from paper_2110_04421_b200 import _native as N
     from paper_2110_04421_b200.confignet import DevicePopulation
     from paper_2110_04421_b200.defaults import default_disease, default_progression
     from paper_2110_04421_b200.interventions import InterventionConfig
     from paper_2110_04421_b200.keyed import replication_seed
-    from paper_2110_04421_b200.partition import (NcclCodeExchange, PartitionedSimulation,
-                                                 PartitionPlan)
+    from paper_2110_04421_b200.partition import NcclComm, PartitionedSimulation, PartitionPlan
     from paper_2110_04421_b200.sim import ConfigSimulation
-    rank, local_rank, world = dist_env()
-    torch.cuda.set_device(local_rank)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl")
     spec = workload_spec("config3")
     pop = DevicePopulation(spec, 0)        # row f3: built on the device
     d, t, iv = default_disease(), default_progression(), InterventionConfig()
     seed = replication_seed(0, 0)
     if world > 1:
         plan = PartitionPlan(spec.n_agents, world)
-        sim = PartitionedSimulation(pop, d, t, iv, seed, plan, rank,
-                                    NcclCodeExchange(plan, rank), mode="fused", horizon=HORIZON)
+        comm = NcclComm.from_process_group()
+        sim = PartitionedSimulation(pop, d, t, iv, seed, plan, rank, comm=comm, mode="fused",
+                                    horizon=HORIZON)
     else:
         sim = ConfigSimulation(pop, d, t, iv, seed, mode="fused", horizon=HORIZON)
-    for _ in range(a.warmup):
-        sim.reset()
-        sim.run()
+    sim.capture()
+    for _ in range(warmup):
+        sim.replay()
     torch.cuda.synchronize()
     if dist:
         dist.barrier()
     clk = ClockSampler(local_rank)
     st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     st.record()
-    edges = 0
-    for _ in range(a.steps):
-        sim.reset()
-        sim.run()
+    for _ in range(steps):
+        sim.replay()
     en.record()
     torch.cuda.synchronize()
     clocks = clk.stop()
     ms = st.elapsed_time(en)
     rec = sim.rec.clone()
     if dist:
-        NcclCodeExchange(plan, rank).reduce_records(rec)
+        rec = reduce_partition_records(rec, world)
         tt = torch.tensor([ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
-    edges = float(rec[:, N.REC["edges"]].sum().item()) * a.steps
+    edges = float(rec[:, N.REC["edges"]].sum().item()) * steps
+    return {"workload": "config3 (BASELINE.json configs[3]): 10M agents, config-1 networks, 180 days, "
+                        "fused mode, no interventions",
+            "value": edges / (ms / 1e3), "unit": "agent-interactions/s", "n_gpus": world,
+            "steps": steps, "warmup": warmup, "ms_per_step": ms / steps, "scaling": "strong",
+            "wall_s_per_sim": ms / steps / 1e3,
+            "parallelism": (f"agent ranges x{world}: native NCCL all-gather of the 16-bit codes every "
+                            "day inside the native day loop, tomorrow's sigma tables on a side stream, "
+                            "one CUDA graph per rank" if world > 1 else "1 GPU"),
+            "l2": "not flushed: every day touches the 10M-agent state (~160 MB hot, 700 MB total) and "
+                  "tables, more than the 126 MB L2",
+            "clocks": clocks}
+
+
+def reduce_partition_records(rec, world):
+    """Sum the ranks' partial day records (flags OR-ed, step kept)."""
+    from paper_2110_04421_b200.partition import NcclCodeExchange, PartitionPlan
+    plan = PartitionPlan(workload_spec("config3").n_agents, world)
+    import torch.distributed as dist
+    return NcclCodeExchange(plan, dist.get_rank()).reduce_records(rec)
+
+
+def run_config3(a):
+    """10M agents, agent-range partition over the ranks (strong scaling)."""
+    import torch
+    rank, local_rank, world = dist_env()
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    m = measure_partition(a.steps, a.warmup, rank, local_rank, world, dist)
     if rank == 0:
+        clocks = m.pop("clocks")
         print(json.dumps({
-            "metric": "agent-interactions/sec", "value": edges / (ms / 1e3),
+            "metric": "agent-interactions/sec", "value": m["value"],
             "unit": "agent-interactions/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
-            "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "strong",
+            "ms_per_step": m["ms_per_step"], "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "config3 (BASELINE.json configs[3]): 10M agents, config-1 "
-                       "networks, 180 days, fused mode", "parallelism": f"agent ranges x{world}, "
-                       "NCCL all-gather of 16-bit codes per day" if world > 1 else "1 GPU",
-                       "l2": "not flushed: every day touches the 10M-agent state (~160 MB hot, "
-                       "700 MB total) and tables, more than the 126 MB L2"},
-            "wall_s_per_sim": ms / a.steps / 1e3, "clocks": clocks}), flush=True)
+            "config": {"workload": m["workload"], "parallelism": m["parallelism"], "l2": m["l2"]},
+            "wall_s_per_sim": m["wall_s_per_sim"], "clocks": clocks}), flush=True)
 
 
 def run_config4(a):

@@ -294,12 +294,43 @@ int epi_set_infection_mode(epi_ctx *ctx, int32_t mode);
 #define EPI_X_SUM_U64 2
 #define EPI_X_EXSCAN_I64 3
 #define EPI_X_OR_U8 4
+#define EPI_X_GATHER_U16 5   /* the per-day code all-gather (epi_set_code_exchange mode 1):
+                                buf = the uint16 code vector (world * count entries), every
+                                rank's chunk [rank * count, (rank + 1) * count) to every rank */
 typedef int (*epi_exchange_fn)(void *user, int32_t kind, void *buf, int64_t count, void *stream);
 int epi_set_exchange(epi_ctx *ctx, epi_exchange_fn fn, void *user);
 
 /* Whole-population runs build the random-slot push tables (96 B/agent) only
  * up to `max_agents` agents (-1 = while they fit in L2). */
 int epi_set_push_max(epi_ctx *ctx, int64_t max_agents);
+
+/* ---- Agent-range partitions over NCCL (SURVEY §8(b) abm_allgather_codes,
+ * §8(e)).  No reference counterpart: the reference runs one process per
+ * replication (runner.py:164-190) and never partitions a population.
+ *
+ * Rank 0 calls epi_comm_unique_id, ships the 128 bytes to its peers (any
+ * channel: torch.distributed here), every rank calls epi_comm_create with its
+ * rank on its current CUDA device (ncclCommInitRank; NCCL is opened at run
+ * time from libnccl.so.2, the one torch already loaded when present).
+ * epi_set_code_exchange(ctx, comm, 2, chunk) makes every day of
+ * epi_sim_step / epi_sim_run end with an in-place all-gather of the code
+ * vector (chunk codes per rank, ranks own rows [rank * chunk, ...)); mode 1
+ * routes the same exchange through the epi_set_exchange callback
+ * (EPI_X_GATHER_U16; emulated ranks in tests), mode 0 leaves it to the
+ * caller.  With NCCL the whole partitioned run can be captured in a CUDA
+ * graph.  epi_allgather_codes runs the exchange once (the day-0 codes). */
+typedef struct epi_comm epi_comm;
+int epi_comm_unique_id(uint8_t *out128);
+int epi_comm_create(const uint8_t *id128, int32_t world, int32_t rank, epi_comm **out);
+int epi_comm_destroy(epi_comm *comm);
+int epi_set_code_exchange(epi_ctx *ctx, epi_comm *comm, int32_t mode, int64_t chunk);
+int epi_allgather_codes(epi_ctx *ctx, uint16_t *codes, void *stream);
+
+/* Fused days without push tables (partitioned ranks, populations above the
+ * push-table cut-off): build tomorrow's code-independent workplace tables on a
+ * side stream while today's day kernel and the code exchange run (default on;
+ * results are identical either way). */
+int epi_set_sigma_ahead(epi_ctx *ctx, int32_t on);
 
 /* Debug export of the hazard the step kernels consume (test hook for the
  * timed fp32 paths: k_fused_step, k_fused_run, k_iv_run, k_msg_pass<1>).

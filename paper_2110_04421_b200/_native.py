@@ -99,6 +99,12 @@ _SIGS = {
     "epi_pop_synthesize": (_i32, [C.POINTER(EpiPopSpec), _u64, C.POINTER(EpiPopOut), _p]),
     "epi_set_push_max": (_i32, [_p, _i64]),
     "epi_set_lambda_probe": (_i32, [_p, _p, _i32, _i32]),
+    "epi_comm_unique_id": (_i32, [_p]),
+    "epi_comm_create": (_i32, [_p, _i32, _i32, _p]),
+    "epi_comm_destroy": (_i32, [_p]),
+    "epi_set_code_exchange": (_i32, [_p, _p, _i32, _i64]),
+    "epi_allgather_codes": (_i32, [_p, _p, _p]),
+    "epi_set_sigma_ahead": (_i32, [_p, _i32]),
     "epi_set_persistent": (_i32, [_p, _i32]),
     "epi_set_iv_fusion": (_i32, [_p, _i32]),
     "epi_set_day_grid": (_i32, [_p, _i32]),

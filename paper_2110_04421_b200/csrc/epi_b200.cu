@@ -16,6 +16,8 @@
 
 #include <cub/device/device_scan.cuh>
 #include <cuda/std/functional>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include "epi_kernels.cuh"
 #include "epi_msgpass.cuh"
@@ -119,7 +121,42 @@ int dalloc(T** p, size_t count) {
   return 0;
 }
 
+// NCCL, opened at run time (the process's libnccl.so.2 -- torch's when torch
+// is loaded -- so one NCCL serves both), for the per-day code all-gather of
+// agent-range partitioned runs.
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*error_string)(ncclResult_t) = nullptr;
+};
+const NcclApi* nccl_api() {
+  static NcclApi api;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+      api.get_unique_id = (decltype(api.get_unique_id))dlsym(h, "ncclGetUniqueId");
+      api.comm_init_rank = (decltype(api.comm_init_rank))dlsym(h, "ncclCommInitRank");
+      api.comm_destroy = (decltype(api.comm_destroy))dlsym(h, "ncclCommDestroy");
+      api.all_gather = (decltype(api.all_gather))dlsym(h, "ncclAllGather");
+      api.error_string = (decltype(api.error_string))dlsym(h, "ncclGetErrorString");
+      if (api.get_unique_id && api.comm_init_rank && api.comm_destroy && api.all_gather && api.error_string)
+        api.h = h;
+    }
+  }
+  return api.h ? &api : nullptr;
+}
+
 }  // namespace
+
+struct epi_comm {
+  ncclComm_t comm = nullptr;
+  int world = 1, rank = 0;
+};
 
 struct epi_ctx {
   HotWindow hot;                     // L2-persisting window (source codes)
@@ -175,7 +212,7 @@ struct epi_ctx {
   uint16_t* tau_lut = nullptr;       // bucket table of delay_steps
   NetTables ntab{};                  // host copy (static radix tables)
   NetTables* ntab_dev[3] = {nullptr, nullptr, nullptr};   // per-day keys, by step % 3
-  WorkTables wt_host[2]{};           // day tables by step parity (member_at_pos shared)
+  WorkTables wt_host[2]{};           // day tables by step parity
   WorkTables* wt_dev[2][3] = {};     // device structs per parity x variant (0 member tables,
                                      // 1 + wcode, 2 + rin/rout)
                                      //   0 csr (ids), 1 fused partitioned, 2 fused whole
@@ -189,6 +226,18 @@ struct epi_ctx {
   unsigned long long* ivr_hist = nullptr;  // k_iv_run: [2][NUM_BUCKETS + 1] (+ active count)
   unsigned* run_barrier = nullptr;   // arrival counter of k_fused_run's grid barrier
   LamProbe probe{};                  // debug hazard export (epi_set_lambda_probe)
+  // days of a fused run without push tables (partitioned ranks, populations
+  // above the L2 cut-off): tomorrow's sigma tables are built on a side
+  // stream while today's kernel and the code exchange run
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork_ev = nullptr, sigma_ev = nullptr;
+  int sigma_day = -1;                // the day whose sigma tables are (being) built ahead
+  uint64_t sigma_seed = 0;
+  int sigma_ahead = 1;               // epi_set_sigma_ahead
+  // the per-day code exchange of a partitioned run (epi_set_comm / callback)
+  int gather_mode = 0;               // 0: the caller exchanges; 1: xfn EPI_X_GATHER_U16; 2: NCCL
+  epi_comm* comm = nullptr;
+  int64_t gather_chunk = 0;          // codes per rank (the buffer holds world * chunk)
 };
 
 namespace {
@@ -433,6 +482,10 @@ int epi_destroy(epi_ctx* c) {
   cudaFree(c->ivr_hist);
   for (auto* p : c->ntab_dev) cudaFree(p);
   cudaFree(c->wt_host[0].member_at_pos);
+  cudaFree(c->wt_host[1].member_at_pos);
+  if (c->side) cudaStreamDestroy(c->side);
+  if (c->fork_ev) cudaEventDestroy(c->fork_ev);
+  if (c->sigma_ev) cudaEventDestroy(c->sigma_ev);
   for (auto& w : c->wt_host) {
     cudaFree(w.pos_of);
     cudaFree(w.shift);
@@ -936,12 +989,10 @@ int epi_net_attach(epi_ctx* c, const epi_net* net) {
   if (!rc) rc = dalloc(&c->net_toff, (size_t)((c->n + 31) / 32) * 33);
   if (rc) return rc;
   CK(cudaMemset(c->net_msgs, 0, n_msgs * sizeof(uint16_t)));
-  rc = dalloc(&c->wt_host[0].member_at_pos, (size_t)net->n_member_slots);
-  if (rc) return rc;
   for (int par = 0; par < 2; ++par) {
     WorkTables& w = c->wt_host[par];
-    w.member_at_pos = c->wt_host[0].member_at_pos;
-    rc = dalloc(&w.pos_of, (size_t)net->n_member_slots);
+    rc = dalloc(&w.member_at_pos, (size_t)net->n_member_slots);
+    if (!rc) rc = dalloc(&w.pos_of, (size_t)net->n_member_slots);
     if (!rc) rc = dalloc(&w.shift, (size_t)net->n_workplaces * (net->colleague_draws + 1));
     if (!rc) rc = dalloc(&w.wcode, (size_t)net->n_member_slots);
     if (!rc) rc = dalloc(&w.rout, (size_t)c->n * RT_SLOTS);
@@ -957,6 +1008,7 @@ int epi_net_attach(epi_ctx* c, const epi_net* net) {
     }
   }
   c->merged_ready = -1;
+  c->sigma_day = -1;
   return 0;
 }
 
@@ -1077,6 +1129,75 @@ static int iv_fused_day(epi_ctx* c, const StepArgs& A, int32_t step, uint64_t se
   return 0;
 }
 
+// Day tables of a fused day without push tables (partitioned ranks,
+// populations above the push-table cut-off), split so the code-independent
+// part overlaps: the sigma tables (member_at_pos / pos_of / shift of every
+// workplace, tomorrow's random-slot keys) depend on (seed, day) only and are
+// built one day ahead on a side stream, concurrently with today's day kernel
+// and the code exchange; only the workplace codes (k_wcode) wait for the
+// day's complete code vector.  Tomorrow's tables go to the other parity,
+// whose last readers (yesterday's kernels) precede the fork in stream order.
+static int sigma_day_tables(epi_ctx* c, int32_t step, uint64_t seed, const uint16_t* codes_cur, long long* rec_zero,
+                            cudaStream_t s) {
+  const int par = step & 1;
+  const int wblocks = grid_for(c->net.n_member_slots, 256, 8);
+  auto sigma_only = [&](int p) {
+    WorkTables w = c->wt_host[p];
+    w.wcode = nullptr;
+    w.rin = nullptr;
+    w.rout = nullptr;
+    return w;
+  };
+  if (c->sigma_day == step && c->sigma_seed == seed) {
+    CK(cudaStreamWaitEvent(s, c->sigma_ev, 0));
+    if (rec_zero) CK(cudaMemsetAsync(rec_zero, 0, EPI_REC_LEN * sizeof(long long), s));
+  } else {
+    CK(launch_pdl_w(&c->hot, k_day_tables, dim3(wblocks), dim3(256), 0, s, c->net, make_net_keys(seed, step),
+                    sigma_only(par), codes_cur, c->lo, c->hi, wblocks, (const NetTables*)c->ntab_dev[step % 3],
+                    c->ntab_dev[(step + 1) % 3], key_prefix(seed, step + 1, P_NET_RPERM), rec_zero));
+  }
+  CK(launch_pdl_w(&c->hot, k_wcode, dim3(grid_for(c->net.n_member_slots, 256, 4)), dim3(256), 0, s,
+                  (int64_t)c->net.n_member_slots, (const int32_t*)c->wt_host[par].member_at_pos, codes_cur,
+                  c->wt_host[par].wcode));
+  if (!c->side) {
+    CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&c->fork_ev, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->sigma_ev, cudaEventDisableTiming));
+  }
+  CK(cudaEventRecord(c->fork_ev, s));
+  CK(cudaStreamWaitEvent(c->side, c->fork_ev, 0));
+  CK(launch_pdl(k_day_tables, dim3(wblocks), dim3(256), 0, c->side, c->net, make_net_keys(seed, step + 1),
+                sigma_only(par ^ 1), codes_cur, c->lo, c->hi, wblocks, (const NetTables*)c->ntab_dev[(step + 1) % 3],
+                c->ntab_dev[(step + 2) % 3], key_prefix(seed, step + 2, P_NET_RPERM), (long long*)nullptr));
+  CK(cudaEventRecord(c->sigma_ev, c->side));
+  c->sigma_day = step + 1;
+  c->sigma_seed = seed;
+  return 0;
+}
+
+// Join the side stream into `s` (nothing may be left unjoined at the end of
+// a call: CUDA-graph capture, and callers timing the stream).
+static int join_side(epi_ctx* c, cudaStream_t s) {
+  if (c->side && c->sigma_day >= 0) CK(cudaStreamWaitEvent(s, c->sigma_ev, 0));
+  return 0;
+}
+
+// The per-day code exchange of a partitioned run: every rank's chunk of the
+// code vector it just wrote, to every rank, in place.
+static int gather_codes(epi_ctx* c, uint16_t* codes, cudaStream_t s) {
+  if (c->gather_mode == 2) {
+    const NcclApi* api = nccl_api();
+    const epi_comm* m = c->comm;
+    const size_t bytes = (size_t)c->gather_chunk * sizeof(uint16_t);
+    const ncclResult_t r = api->all_gather((const void*)(codes + (size_t)m->rank * c->gather_chunk), (void*)codes,
+                                           bytes, ncclUint8, m->comm, s);
+    if (r != ncclSuccess) return fail(EPI_ECUDA, std::string("ncclAllGather: ") + api->error_string(r));
+    return 0;
+  }
+  if (c->gather_mode == 1) return exchange(c, EPI_X_GATHER_U16, codes, c->gather_chunk, s);
+  return 0;
+}
+
 static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t seed, int32_t mode,
                          int32_t precision, const uint16_t* codes_cur, uint16_t* codes_next,
                          int64_t* record, int32_t* vax_open, void* const* ev, void* stream,
@@ -1135,9 +1256,15 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
       WorkTables w = c->wt_host[par];
       if (variant == 0) w.wcode = nullptr;
       if (variant < 2) { w.rin = nullptr; w.rout = nullptr; }
-      CK(launch_pdl_w(&c->hot, k_day_tables, dim3(wblocks + rblocks > 0 ? wblocks + rblocks : 1), dim3(256), 0, s,
-                    c->net, nk, w, codes_cur, c->lo, c->hi, wblocks, (const NetTables*)nt_today, nt_next,
-                    key_prefix(seed, step + 1, P_NET_RPERM), rec_zero));
+      if (mode == 1 && !push_rand && !iv && has_work && c->sigma_ahead) {
+        int rc = sigma_day_tables(c, step, seed, codes_cur, rec_zero, s);
+        if (rc) return rc;
+      } else {
+        CK(launch_pdl_w(&c->hot, k_day_tables, dim3(wblocks + rblocks > 0 ? wblocks + rblocks : 1), dim3(256), 0, s,
+                      c->net, nk, w, codes_cur, c->lo, c->hi, wblocks, (const NetTables*)nt_today, nt_next,
+                      key_prefix(seed, step + 1, P_NET_RPERM), rec_zero));
+        c->sigma_day = -1;
+      }
     } else {
       CK(launch_pdl(k_day_keys, dim3(1), dim3(32), 0, s, nt_next, key_prefix(seed, step + 1, P_NET_RPERM),
                     rec_zero));
@@ -1229,8 +1356,11 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
 int epi_sim_step(epi_ctx* c, const epi_state* st, int32_t step, uint64_t seed, int32_t mode,
                  int32_t precision, const uint16_t* codes_cur, uint16_t* codes_next, int64_t* record,
                  int32_t* vax_open, void* stream) {
-  return sim_step_impl(c, st, step, seed, mode, precision, codes_cur, codes_next, record, vax_open,
-                       nullptr, stream);
+  int rc = sim_step_impl(c, st, step, seed, mode, precision, codes_cur, codes_next, record, vax_open,
+                         nullptr, stream);
+  if (!rc) rc = gather_codes(c, codes_next, S(stream));
+  if (!rc) rc = join_side(c, S(stream));
+  return rc;
 }
 
 // k_fused_run: one block per SM, threads = the SM's agents rounded up to a warp
@@ -1417,6 +1547,69 @@ int epi_set_iv_fusion(epi_ctx* c, int32_t on) {
   return 0;
 }
 
+int epi_comm_unique_id(uint8_t* out) {
+  const NcclApi* api = nccl_api();
+  if (!api) return fail(EPI_ECUDA, "libnccl.so.2 not found");
+  if (!out) return fail(EPI_EARG, "null argument");
+  ncclUniqueId id;
+  const ncclResult_t r = api->get_unique_id(&id);
+  if (r != ncclSuccess) return fail(EPI_ECUDA, std::string("ncclGetUniqueId: ") + api->error_string(r));
+  std::memcpy(out, id.internal, NCCL_UNIQUE_ID_BYTES);
+  return 0;
+}
+
+int epi_comm_create(const uint8_t* id, int32_t world, int32_t rank, epi_comm** out) {
+  const NcclApi* api = nccl_api();
+  if (!api) return fail(EPI_ECUDA, "libnccl.so.2 not found");
+  if (!id || !out || world < 1 || rank < 0 || rank >= world) return fail(EPI_EARG, "bad argument");
+  ncclUniqueId uid;
+  std::memcpy(uid.internal, id, NCCL_UNIQUE_ID_BYTES);
+  epi_comm* m = new epi_comm();
+  m->world = world;
+  m->rank = rank;
+  const ncclResult_t r = api->comm_init_rank(&m->comm, world, uid, rank);
+  if (r != ncclSuccess) {
+    delete m;
+    return fail(EPI_ECUDA, std::string("ncclCommInitRank: ") + api->error_string(r));
+  }
+  *out = m;
+  return 0;
+}
+
+int epi_comm_destroy(epi_comm* m) {
+  if (!m) return 0;
+  const NcclApi* api = nccl_api();
+  if (api && m->comm) api->comm_destroy(m->comm);
+  delete m;
+  return 0;
+}
+
+int epi_set_code_exchange(epi_ctx* c, epi_comm* comm, int32_t mode, int64_t chunk) {
+  if (!c || mode < 0 || mode > 2 || (mode > 0 && chunk < 1)) return fail(EPI_EARG, "bad argument");
+  if (mode == 2) {
+    if (!comm) return fail(EPI_EARG, "NCCL code exchange without a communicator");
+    if ((int64_t)comm->world * chunk < c->n) return fail(EPI_EARG, "world * chunk does not cover the agents");
+    if (c->lo != (int64_t)comm->rank * chunk) return fail(EPI_EARG, "owned rows do not start at rank * chunk");
+  }
+  if (mode == 1 && !c->xfn) return fail(EPI_EARG, "callback code exchange without epi_set_exchange");
+  c->gather_mode = mode;
+  c->comm = mode == 2 ? comm : nullptr;
+  c->gather_chunk = chunk;
+  return 0;
+}
+
+int epi_allgather_codes(epi_ctx* c, uint16_t* codes, void* stream) {
+  if (!c || !codes) return fail(EPI_EARG, "null argument");
+  return gather_codes(c, codes, S(stream));
+}
+
+int epi_set_sigma_ahead(epi_ctx* c, int32_t on) {
+  if (!c) return fail(EPI_EARG, "null ctx");
+  c->sigma_ahead = on != 0;
+  c->sigma_day = -1;
+  return 0;
+}
+
 int epi_set_lambda_probe(epi_ctx* c, float* out, int32_t first_step, int32_t n_days) {
   if (!c || n_days < 0 || (n_days > 0 && !out)) return fail(EPI_EARG, "bad argument");
   c->probe.out = n_days > 0 ? out : nullptr;
@@ -1485,15 +1678,18 @@ int epi_sim_run(epi_ctx* c, const epi_state* st, int32_t first_step, int32_t n_d
     }
     return 0;
   }
+  // one day at a time (partitioned ranks: the day's code exchange between
+  // days; tomorrow's sigma tables on the side stream meanwhile)
   for (int d = 0; d < n_days; ++d) {
     const int t = first_step + d;
     uint16_t* cur = (t & 1) ? codes1 : codes0;
     uint16_t* nxt = (t & 1) ? codes0 : codes1;
     int rc = sim_step_impl(c, st, t, seed, mode, precision, cur, nxt, records + (size_t)d * EPI_REC_LEN,
                            vax_open, nullptr, stream, false);
+    if (!rc) rc = gather_codes(c, nxt, S(stream));
     if (rc) return rc;
   }
-  return 0;
+  return join_side(c, S(stream));
 }
 
 int epi_sim_step_timed(epi_ctx* c, const epi_state* st, int32_t step, uint64_t seed, int32_t mode,

@@ -1113,6 +1113,17 @@ __global__ void __launch_bounds__(128, 8) k_fused_step(StepArgs A, epi_net net, 
   rec_flush(racc, A.rec, A.step);
 }
 
+// The workplace codes of a day whose sigma tables were built ahead (without
+// codes): wcode[slot] = code of the worker at that position, once the day's
+// code vector is complete (after a partitioned run's all-gather).
+__global__ void __launch_bounds__(256) k_wcode(int64_t n_slots, const int32_t* __restrict__ member_at_pos,
+                                               const uint16_t* __restrict__ codes, uint16_t* __restrict__ wcode) {
+  pdl_wait();
+  pdl_trigger();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_slots; i += (int64_t)gridDim.x * blockDim.x)
+    wcode[i] = codes[member_at_pos[i]];
+}
+
 // Per-day tables.  Blocks [0, wblocks) own the workplace member slots (one
 // thread each: member_at_pos / pos_of / shift, and wcode in fused mode);
 // the remaining blocks own agent rows [lo, hi) for the random push tables:

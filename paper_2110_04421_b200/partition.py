@@ -37,7 +37,7 @@ from . import _native as N
 from .errors import ConfigError
 from .sim import ConfigSimulation
 
-_X_GATHER_U8, _X_SUM_U64, _X_EXSCAN_I64, _X_OR_U8 = 1, 2, 3, 4
+_X_GATHER_U8, _X_SUM_U64, _X_EXSCAN_I64, _X_OR_U8, _X_GATHER_U16 = 1, 2, 3, 4, 5
 
 
 class _DevArray:
@@ -87,6 +87,45 @@ def _or_fold(parts):
     for p in parts[1:]:
         out = torch.bitwise_or(out, p)
     return out
+
+
+class NcclComm:
+    """A native NCCL communicator (libepib200 `epi_comm`): the per-day code
+    all-gather runs inside the native day loop (epi_set_code_exchange mode
+    2), in place, on the simulation's stream -- no Python per day, no copy
+    of the send chunk, and the partitioned run can be captured in a CUDA
+    graph.  Rank 0 draws the NCCL unique id; `from_process_group` ships it
+    over torch.distributed."""
+
+    def __init__(self, world: int, rank: int, unique_id: bytes):
+        import ctypes
+        self._lib = N.lib()
+        self.world, self.rank = world, rank
+        buf = (ctypes.c_uint8 * 128).from_buffer_copy(unique_id)
+        h = N._p()
+        N.check(self._lib.epi_comm_create(buf, world, rank, ctypes.byref(h)))
+        self._h = h
+
+    @staticmethod
+    def unique_id() -> bytes:
+        import ctypes
+        buf = (ctypes.c_uint8 * 128)()
+        N.check(N.lib().epi_comm_unique_id(buf))
+        return bytes(buf)
+
+    @classmethod
+    def from_process_group(cls, group=None) -> "NcclComm":
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        box = [cls.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(box, src=0, group=group)
+        return cls(world, rank, box[0])
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            self._lib.epi_comm_destroy(h)
+            self._h = None
 
 
 class NcclCodeExchange:
@@ -274,19 +313,33 @@ class PartitionedSimulation(ConfigSimulation):
     """One rank of an agent-range partitioned config simulation."""
 
     def __init__(self, pop, disease, table, interventions, seed, plan: PartitionPlan, rank: int,
-                 exchange=None, **kw):
+                 exchange=None, comm: NcclComm | None = None, **kw):
+        """`comm`: the per-day code all-gather over native NCCL (inside the
+        day loop, capturable); otherwise `exchange` provides it (Python
+        callback from the native loop: NcclCodeExchange over
+        torch.distributed, ThreadExchange), or -- LocalCodeExchange -- the
+        caller exchanges between lockstep days.  `exchange` also provides
+        the in-step exchanges of DEN and vaccination."""
         needs_x = interventions.den_enabled or interventions.vaccination_enabled
         if needs_x and not hasattr(exchange, "sum_"):
             raise ConfigError("exposure notification and vaccination in a partitioned run need "
                               "an in-step exchange (NcclCodeExchange or ThreadExchange)")
-        self.plan, self.rank, self.exchange = plan, rank, exchange
+        if comm is not None and (comm.world != plan.world or comm.rank != rank):
+            raise ConfigError("the communicator's world/rank differ from the partition plan's")
+        self.plan, self.rank, self.exchange, self.comm = plan, rank, exchange, comm
         self._code_len = plan.padded
         self._ready = False          # no exchange from inside the constructor's reset()
         super().__init__(pop, disease, table, interventions, seed, **kw)
         self._ready = True
-        if needs_x:
+        callback = exchange is not None and not isinstance(exchange, LocalCodeExchange)
+        if needs_x or (callback and comm is None):
             self._hook = N.XFN(self._on_exchange)      # kept alive with the simulation
             N.check(self._lib.epi_set_exchange(self._ctx, self._hook, None))
+        if comm is not None:
+            N.check(self._lib.epi_set_code_exchange(self._ctx, comm._h, 2, plan.chunk))
+        elif callback:
+            N.check(self._lib.epi_set_code_exchange(self._ctx, None, 1, plan.chunk))
+        self._native_gather = comm is not None or callback
 
     def _on_exchange(self, _user, kind, buf, count, _stream):
         """Called by the native step (same thread, current stream)."""
@@ -299,6 +352,8 @@ class PartitionedSimulation(ConfigSimulation):
                 self.exchange.exscan_(_view(buf, count, "<i8"))
             elif kind == _X_OR_U8:
                 self.exchange.or_(_view(buf, count, "|u1"))
+            elif kind == _X_GATHER_U16:
+                self.exchange.exchange(_view(buf, self.plan.padded, "<i2"))
             else:
                 return 1
             return 0
@@ -317,23 +372,19 @@ class PartitionedSimulation(ConfigSimulation):
 
     def reset(self) -> None:
         super().reset()
-        if self._ready and self.exchange is not None and not isinstance(self.exchange, LocalCodeExchange):
-            self.exchange.exchange(self.codes[0])
+        if self._ready and self._native_gather:
+            # the day-0 codes of every rank (the native exchange, in place)
+            N.check(self._lib.epi_allgather_codes(self._ctx, N.ptr(self.codes[0]), N.stream_handle()))
 
-    def step(self) -> None:
-        t = self.clock
-        super().step()
-        if self.exchange is not None and not isinstance(self.exchange, LocalCodeExchange):
-            self.exchange.exchange(self.codes[(t + 1) & 1])
+    # step() / run(): the native day loop ends every day with the code
+    # exchange (epi_set_code_exchange), tomorrow's sigma tables built on a
+    # side stream meanwhile
 
     def capture(self):
-        raise ConfigError("a partitioned simulation exchanges with its peers between and "
-                          "inside days; run it day by day (run()) instead of as a CUDA graph")
-
-    def run(self, days: int | None = None) -> None:
-        # one day at a time: the code exchange sits between days
-        for _ in range(self.horizon - self.clock if days is None else days):
-            self.step()
+        if self.comm is None or self.iv.den_enabled or self.iv.vaccination_enabled:
+            raise ConfigError("only a partitioned run over native NCCL without in-step exchanges "
+                              "(DEN, vaccination) can be captured as a CUDA graph")
+        return super().capture()
 
 
 def run_emulated(pop, disease, table, interventions, seed, world: int, days: int, **kw):
@@ -372,8 +423,7 @@ def run_threaded(pop, disease, table, interventions, seed, world: int, days: int
                                                     ex.for_rank(r), horizon=days, **kw)
                 ex.barrier.wait()
                 sims[r].reset()      # exchanges the day-0 codes
-                for _ in range(days):
-                    sims[r].step()
+                sims[r].run()        # the native day loop; the code exchange ends every day
                 stream.synchronize()
         except BaseException as e:  # noqa: BLE001
             errors.append(e)
