@@ -55,6 +55,9 @@ def parse():
                          "stream (default), or per-day kernels of replicas on concurrent streams")
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--precision", choices=["f32", "f64"], default="f32",
+                    help="f64 = canonical-order fp64 message pass (csr mode only): bitwise the "
+                         "reference engine's hazard")
     ap.add_argument("--no-partition", action="store_true",
                     help="skip the config-3 agent-range partition measured beside the headline")
     ap.add_argument("--no-message-pass", action="store_true",
@@ -309,10 +312,12 @@ def run_ours(a):
     pop = synthesize(spec, 0)
     n_sims = a.warmup + a.steps
     modes = ["csr", "fused"] if a.mode == "auto" else [a.mode]
+    if a.precision == "f64":
+        modes = ["csr"]                  # fused mode is fp32 only
 
     def make(mode, i):
         seed = replication_seed(0, rank * 100_000 + i)
-        return ConfigSimulation(pop, disease, table, iv, seed, mode=mode, precision="f32",
+        return ConfigSimulation(pop, disease, table, iv, seed, mode=mode, precision=a.precision,
                                 horizon=HORIZON)
 
     # L2 flush buffer (> 126 MB L2), written between timed simulations
@@ -402,7 +407,7 @@ def run_ours(a):
         "metric": "agent-interactions/sec", "value": value, "unit": "agent-interactions/s",
         "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
         "ms_per_step": ms_total / a.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "vs_baseline": None, "dtype": a.precision, "data": "synthetic",
         "config": {
             "workload": workload_string(a),
             "mode": best["mode"], "step": "one full 180-day simulation (CUDA graph replay)",
@@ -464,7 +469,8 @@ def kernel_profile(sim, mode):
         handles = (ctypes.c_void_p * 4)(*[e.cuda_event for e in evs[t]])
         st = sim.state.struct()
         N.check(lib.epi_sim_step_timed(
-            sim._ctx, ctypes.byref(st), t, _u64(sim.seed), 0 if mode == "csr" else 1, N.F32,
+            sim._ctx, ctypes.byref(st), t, _u64(sim.seed), 0 if mode == "csr" else 1,
+            N.F64_CANONICAL if sim.precision == "f64" else N.F32,
             N.ptr(sim.codes[t & 1]), N.ptr(sim.codes[(t + 1) & 1]), N.ptr(sim.rec[t]),
             N.ptr(sim.vax), ctypes.addressof(handles), N.stream_handle()))
     torch.cuda.synchronize()

@@ -179,8 +179,16 @@ __device__ __forceinline__ uint32_t work_shift(uint64_t wshift_prefix, int w, in
 // Random-slot count n_{t,a} ~ Poisson(mean) truncated at `slots`.
 __device__ __forceinline__ int random_count(const epi_net& net, uint64_t rcount_prefix, int64_t a) {
   const double u = keyed_u(rcount_prefix, (uint64_t)a, 0);
+  // #{k < slots : u >= cdf[k]} for the non-decreasing cdf: a branch-free
+  // binary search (6 compares instead of up to 32)
+  const int slots = net.random_slots;
   int c = 0;
-  for (int k = 0; k < net.random_slots; ++k) c += (u >= net.poisson_cdf[k]) ? 1 : 0;
+#pragma unroll
+  for (int step = EPI_MAX_SLOTS / 2; step >= 1; step >>= 1) {
+    const int k = c + step - 1;
+    c += (k < slots && u >= net.poisson_cdf[k]) ? step : 0;
+  }
+  c += (c < slots && u >= net.poisson_cdf[c < EPI_MAX_SLOTS ? c : EPI_MAX_SLOTS - 1]) ? 1 : 0;
   return c;
 }
 

@@ -208,12 +208,12 @@ __device__ __forceinline__ unsigned transmit_progress_core(const epi_params* __r
   unsigned ev = 0;
   if (h.stage == S_SUS && !(P->sterilizing && h.immune)) {
     // lam == 0 gives p == 0 and u < p never holds: skip the draw
-    bool infect;
+    bool infect = false;
     if (forced >= 0) {
       infect = forced != 0;
     } else {
-      const double p = 1.0 - exp(-lam);
-      infect = lam > 0.0 && draw(K, inj, P_INFECTION, a) < p;
+      // p = 0 never infects: no exp, no draw for the (many) zero hazards
+      if (lam > 0.0) infect = draw(K, inj, P_INFECTION, a) < 1.0 - exp(-lam);
     }
     if (infect) {
       int entry = P->targets[S_SUS][pick_branch(P, S_SUS, h.age, draw(K, inj, P_ENTRY, a))];
@@ -269,8 +269,7 @@ __device__ __forceinline__ unsigned transmit_progress_now(const epi_params* __re
   pend = -1;
   bool infected = false;
   if (h.stage == S_SUS && !(P->sterilizing && h.immune)) {
-    const double p = 1.0 - exp(-lam);
-    infected = lam > 0.0 && draw(K, nullptr, P_INFECTION, a) < p;
+    if (lam > 0.0) infected = draw(K, nullptr, P_INFECTION, a) < 1.0 - exp(-lam);
     if (infected) {
       int entry = P->targets[S_SUS][pick_branch(P, S_SUS, h.age, draw(K, nullptr, P_ENTRY, a))];
       if (!P->sterilizing && h.immune) entry = S_ASYM;
