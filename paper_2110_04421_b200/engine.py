@@ -5,7 +5,9 @@ Same constructor, attributes (`cols`, `disease`, `table`, `iv`, `seed`,
 (`step(graph) -> StepEvents`, `gather_exposure(graph) -> float64[N]`); every
 phase runs on the GPU through libepib200:
 
-  step(graph):  graph -> device COO -> CUB sort into canonical CSR
+  step(graph):  graph -> device COO -> counting sort by destination + per-row
+                   sorts (register networks, block sort for long rows) into
+                   the canonical (dst, src, kind) CSR
                 -> fp64 message pass in (dst, src, kind) order (bitwise equal
                    to the reference) fused with transmission + progression
                 -> intervention phase kernels -> per-step record.

@@ -1,6 +1,6 @@
 """Scalar side of the keyed counter-based hash (host only).
 
-The per-agent draws all run on the device (`csrc/epi_rng.cuh`); the host only
+The per-agent draws all run on the device (`csrc/epi_common.cuh`); the host only
 needs the scalar prefix and seed derivations, e.g. to pick replication seeds.
 Same splitmix64 chain and constants as the reference
 (`pkg/src/epivec/rng.py:20-23, 60-108`): draws are a pure function of

@@ -153,3 +153,27 @@ def test_reset_after_a_partial_run_equals_a_fresh_run(iv_on):
     a.run()
     b.run()
     _same(a, b)
+
+
+def test_persistent_runs_are_deterministic_under_repetition():
+    """In lieu of racecheck (compute-sanitizer is closed on this GPU pool):
+    a race between blocks across k_fused_run's hand-rolled grid barrier, or
+    on its shared-memory record rows, would show up as run-to-run
+    differences.  20 replays of the captured config-1 run, L2 flushed in
+    between, must give the same records, codes and state bit for bit."""
+    spec = ConfigNetworkSpec.config(1)
+    pop = synthesize(spec, 2)
+    s = ConfigSimulation(pop, default_disease(), default_progression(), InterventionConfig(), 44, mode="fused")
+    assert s.uses_persistent_run()
+    s.capture()
+    s.replay()
+    torch.cuda.synchronize()
+    rec0, codes0, st0 = s.rec.clone(), s._codes_buf.clone(), s.state.t["stage"].clone()
+    flush = torch.empty(64 * 1024 * 1024, device="cuda")
+    for k in range(20):
+        flush.fill_(float(k))
+        s.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(s.rec, rec0), k
+        assert torch.equal(s._codes_buf, codes0), k
+        assert torch.equal(s.state.t["stage"], st0), k

@@ -27,8 +27,7 @@ from torch.profiler import ProfilerActivity, profile  # noqa: E402
 from paper_2110_04421_b200.confignet import DevicePopulation, ConfigNetworkSpec  # noqa: E402
 from paper_2110_04421_b200.defaults import default_disease, default_progression  # noqa: E402
 from paper_2110_04421_b200.interventions import InterventionConfig  # noqa: E402
-from paper_2110_04421_b200.partition import (NcclComm, PartitionedSimulation, PartitionPlan,  # noqa: E402
-                                             run_threaded)
+from paper_2110_04421_b200.partition import NcclComm, PartitionedSimulation, PartitionPlan  # noqa: E402
 
 
 def kernels(prof):
@@ -72,11 +71,41 @@ def main():
         sim.run(a.days)
         torch.cuda.synchronize()
     show(f"1 rank, native NCCL, {a.agents} agents, days 20-{20 + a.days - 1}", kernels(prof))
-    # 2 ranks emulated on one GPU
+    # 2 ranks emulated on one GPU: built first, then only their days profiled
+    import threading
+    from paper_2110_04421_b200.partition import ThreadExchange
+    plan2 = PartitionPlan(spec.n_agents, 2)
+    ex = ThreadExchange(plan2)
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    sims = []
+    for r in range(2):
+        with torch.cuda.stream(streams[r]):
+            sims.append(PartitionedSimulation(pop, d, t, iv, 3, plan2, r, ex.for_rank(r), mode="fused",
+                                              horizon=40))
+    torch.cuda.synchronize()
+
+    def rank_main(r, days):
+        with torch.cuda.stream(streams[r]):
+            if days is None:
+                sims[r].reset()
+            else:
+                sims[r].run(days)
+            streams[r].synchronize()
+
+    def both(days):
+        th = [threading.Thread(target=rank_main, args=(r, days)) for r in range(2)]
+        for x in th:
+            x.start()
+        for x in th:
+            x.join()
+    both(None)
+    both(20)
+    torch.cuda.synchronize()
     with profile(activities=[ProfilerActivity.CUDA]) as prof2:
-        run_threaded(pop, d, t, iv, 3, 2, a.days + 2, mode="fused", push_max=0)
+        both(a.days)
         torch.cuda.synchronize()
-    show(f"2 emulated ranks (threads, own streams), {a.agents} agents, days 0-{a.days + 1}", kernels(prof2))
+    show(f"2 emulated ranks (host threads, own streams, code exchange by the EPI_X_GATHER_U16 callback: "
+         f"device copies), {a.agents} agents, days 20-{20 + a.days - 1}", kernels(prof2))
 
 
 if __name__ == "__main__":
