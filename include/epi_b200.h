@@ -332,11 +332,6 @@ int epi_allgather_codes(epi_ctx *ctx, uint16_t *codes, void *stream);
  * results are identical either way). */
 int epi_set_sigma_ahead(epi_ctx *ctx, int32_t on);
 
-/* k_fused_run (the persistent whole-run kernel): agents per agent warp,
- * 1..32 (default 32).  Fewer lanes spread a block's agents over more warps;
- * results are identical. */
-int epi_set_run_lanes(epi_ctx *ctx, int32_t lanes);
-
 /* Debug export of the hazard the step kernels consume (test hook for the
  * timed fp32 paths: k_fused_step, k_fused_run, k_iv_run, k_msg_pass<1>).
  * While set, every step kernel of day t in [first_step, first_step + n_days)

@@ -105,7 +105,6 @@ _SIGS = {
     "epi_set_code_exchange": (_i32, [_p, _p, _i32, _i64]),
     "epi_allgather_codes": (_i32, [_p, _p, _p]),
     "epi_set_sigma_ahead": (_i32, [_p, _i32]),
-    "epi_set_run_lanes": (_i32, [_p, _i32]),
     "epi_set_persistent": (_i32, [_p, _i32]),
     "epi_set_iv_fusion": (_i32, [_p, _i32]),
     "epi_set_day_grid": (_i32, [_p, _i32]),

@@ -227,7 +227,6 @@ struct epi_ctx {
   unsigned long long* ivr_hist = nullptr;  // k_iv_run: [2][NUM_BUCKETS + 1] (+ active count)
   unsigned* run_barrier = nullptr;   // arrival counter of k_fused_run's grid barrier
   LamProbe probe{};                  // debug hazard export (epi_set_lambda_probe)
-  int run_lanes = 32;                // k_fused_run: agents per agent warp (epi_set_run_lanes)
   // days of a fused run without push tables (partitioned ranks, populations
   // above the L2 cut-off): tomorrow's sigma tables are built on a side
   // stream while today's kernel and the code exchange run
@@ -1366,10 +1365,10 @@ int epi_sim_step(epi_ctx* c, const epi_state* st, int32_t step, uint64_t seed, i
 }
 
 // k_fused_run: one block per SM, threads = the SM's agents rounded up to a warp
-static int64_t run_threads(int64_t n, int lanes = 32) {
+static int64_t run_threads(int64_t n) {
   const int64_t sms = sm_count();
   const int64_t per = (n + sms - 1) / sms;
-  return (per + lanes - 1) / lanes * 32;
+  return (per + 31) / 32 * 32;
 }
 
 // Can the merged days of a run go to k_fused_run (one co-resident thread per
@@ -1383,7 +1382,7 @@ static bool persistent_ok(epi_ctx* c, int32_t mode, int32_t precision) {
   if (per_sm < 0 &&
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fused_run, RUN_MAX_THREADS, 0) != cudaSuccess)
     per_sm = 0;
-  return per_sm >= 1 && run_threads(c->n, c->run_lanes) <= RUN_MAX_AGENTS;
+  return per_sm >= 1 && run_threads(c->n) <= RUN_MAX_AGENTS;
 }
 
 static int launch_run(epi_ctx* c, const epi_state* st, int32_t first, int32_t n_days, uint64_t seed,
@@ -1407,10 +1406,9 @@ static int launch_run(epi_ctx* c, const epi_state* st, int32_t first, int32_t n_
   R.dn = c->ntab.dn;
   R.barrier = c->run_barrier;
   R.probe = c->probe;
-  R.lanes = c->run_lanes;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)sm_count());
-  cfg.blockDim = dim3((unsigned)run_threads(c->n, c->run_lanes) + 32);     // + the service warp
+  cfg.blockDim = dim3((unsigned)run_threads(c->n) + 32);     // + the service warp
   cfg.stream = s;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeCooperative;     // every block resident: the grid barrier is safe
@@ -1604,12 +1602,6 @@ int epi_set_code_exchange(epi_ctx* c, epi_comm* comm, int32_t mode, int64_t chun
 int epi_allgather_codes(epi_ctx* c, uint16_t* codes, void* stream) {
   if (!c || !codes) return fail(EPI_EARG, "null argument");
   return gather_codes(c, codes, S(stream));
-}
-
-int epi_set_run_lanes(epi_ctx* c, int32_t lanes) {
-  if (!c || lanes < 1 || lanes > 32) return fail(EPI_EARG, "lanes must be in [1, 32]");
-  c->run_lanes = lanes;
-  return 0;
 }
 
 int epi_set_sigma_ahead(epi_ctx* c, int32_t on) {

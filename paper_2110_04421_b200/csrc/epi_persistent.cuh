@@ -57,8 +57,6 @@ struct RunArgs {
   Radix dn;
   unsigned* barrier;              // zeroed arrival counter
   LamProbe probe;
-  int lanes;                      // agents per agent warp (<= 32; fewer spreads a block's
-                                  // agents over more warps)
 };
 
 // Grid barrier between days: one arrival per block (acq_rel atomic on one
@@ -102,7 +100,7 @@ constexpr int RUN_MAX_DAYS = 1 << 20;      // days per launch (no per-day state)
 // one block per SM: up to 704 agent threads (one agent each) + one service
 // warp that flushes yesterday's record and computes tomorrow's keys while
 // the agent warps work
-constexpr int RUN_MAX_AGENTS = 736;     // 24 warps x 80 registers: no spills
+constexpr int RUN_MAX_AGENTS = 704;
 constexpr int RUN_MAX_THREADS = RUN_MAX_AGENTS + 32;
 // loads of data written during the run: plain (coherent) global loads; the
 // grid barrier orders them after the writers' stores
@@ -142,8 +140,8 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_fused_run(RunArgs R, epi
   const int64_t per = (n + gridDim.x - 1) / gridDim.x;
   const int64_t blo = blockIdx.x * per;
   const int64_t bhi = blo + per < n ? blo + per : n;
-  const int64_t b = blo + (int64_t)warp * R.lanes + lane;
-  const bool valid = !service && lane < R.lanes && b < bhi;
+  const int64_t b = blo + threadIdx.x;
+  const bool valid = !service && b < bhi;
   const uint32_t self = (uint32_t)b;
   const int draws = net.colleague_draws;
   // static network data and the agent's state, once
