@@ -389,12 +389,16 @@ def run_ours(a):
     roof["peak"] = peak
     roof["frac"] = roof["achieved"] / peak
     roof["peak_source"] = "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6.65 TB/s"
-    tfile = ROOT / "profiles" / "r01_traffic.json"
+    tfile = ROOT / "profiles" / "r02_traffic.json"
     if tfile.exists():
         tr = json.loads(tfile.read_text()).get(roof["kernel"])
         if tr:
             roof["traffic"] = tr["dram_bytes_read"] + tr["dram_bytes_write"]
             roof["traffic_source"] = tr["source"]
+            # HBM is not what binds these kernels: their working set is
+            # L2-resident; the ncu ceilings that do bind ride along
+            if "ceilings" in tr:
+                roof["binding_ceilings"] = tr["ceilings"]
 
     # north_star's multi-GPU path: config 3 partitioned over the same ranks
     # (strong scaling), measured beside the headline at every N
