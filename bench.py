@@ -371,7 +371,8 @@ def run_ours(a):
     prof = profs[best["mode"]]
     # --- end to end through the public API from pinned host buffers (every
     # rank; whole-job value = summed edges / max time over the ranks)
-    e2e = end_to_end(make(best["mode"], 0), a)
+    e2e = end_to_end(make(best["mode"], 0), a, make(best["mode"], 0))
+    serial = end_to_end(make(best["mode"], 0), a)      # copy in, run, copy out: nothing hidden
     if dist:
         t = torch.tensor([e2e["ms_per_step"], e2e["edges_per_step"]], device="cuda", dtype=torch.float64)
         dist.all_reduce(t[:1], op=dist.ReduceOp.MAX)
@@ -381,6 +382,7 @@ def run_ours(a):
         e2e["h2d_bytes_per_step"] *= world
         e2e["d2h_bytes_per_step"] *= world
     e2e.pop("edges_per_step")
+    e2e["serial"] = {"value": serial["value"], "ms_per_step": serial["ms_per_step"], "copies": serial["copies"]}
 
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) \
         if (ROOT / "MEASURED_PEAKS.json").exists() else {}
@@ -582,43 +584,56 @@ def persistent_profile(sim):
                          "bytes_model": f"{b_day // n} B per agent-day (DESIGN.md §4), x 179 days per launch"}}
 
 
-def end_to_end(sim, a):
-    """Public API from pinned host memory: upload initial state, simulate 180
-    days, read the time series back — every step."""
+def end_to_end(sim, a, sim2=None):
+    """Public API from pinned host memory, every step: upload the initial
+    state (all 22 columns, 7 MB), simulate 180 days, read the 19-column time
+    series back.  With `sim2` the steps go through `sim.HostPipeline`: the
+    copies of step k +- 1 run on a copy stream under the compute of step k."""
     import torch
-    from paper_2110_04421_b200.state import COLUMN_SPECS
-    host = sim.initial_host_columns()
-    pinned = {}
-    for name, dt, _ in COLUMN_SPECS:
-        arr = np.ascontiguousarray(getattr(host, name))
-        if arr.dtype == np.bool_:
-            arr = arr.view(np.uint8)
-        pinned[name] = torch.from_numpy(arr).pin_memory()
-    out = torch.empty((sim.horizon, 19), dtype=torch.int64).pin_memory()
-    sim.capture()
+    from paper_2110_04421_b200.sim import HostPipeline, pinned_columns
+    pinned = pinned_columns(sim.initial_host_columns())
+    outs = [torch.empty((sim.horizon, 19), dtype=torch.int64).pin_memory() for _ in range(2)]
     h2d = sum(int(t.numel() * t.element_size()) for t in pinned.values())
-    d2h = int(out.numel() * out.element_size())
+    d2h = int(outs[0].numel() * outs[0].element_size())
+    if sim2 is not None:
+        pipe = HostPipeline([sim, sim2])
+        k0 = 0
+        for _ in range(a.warmup):
+            pipe.submit(k0, pinned, outs[k0 & 1])
+            k0 += 1
+        pipe.drain()
+        torch.cuda.synchronize()
+        st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        st.record()
+        for k in range(a.steps):
+            pipe.submit(k0 + k, pinned, outs[(k0 + k) & 1])
+        pipe.drain()
+        en.record()
+        torch.cuda.synchronize()
+        mode = "pipelined: copies of the neighbouring steps under the compute (sim.HostPipeline)"
+    else:
+        sim.capture()
 
-    def once():
-        for name, t in pinned.items():
-            sim.initial.t[name].copy_(t, non_blocking=True)
-        sim.replay()
-        out.copy_(sim.rec[:, :19], non_blocking=True)
-
-    for _ in range(a.warmup):
-        once()
-    torch.cuda.synchronize()
-    st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    st.record()
-    for _ in range(a.steps):
-        once()
-    en.record()
-    torch.cuda.synchronize()
+        def once():
+            for name, t in pinned.items():
+                sim.initial.t[name].copy_(t, non_blocking=True)
+            sim.replay()
+            outs[0].copy_(sim.rec[:, :19], non_blocking=True)
+        for _ in range(a.warmup):
+            once()
+        torch.cuda.synchronize()
+        st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        st.record()
+        for _ in range(a.steps):
+            once()
+        en.record()
+        torch.cuda.synchronize()
+        mode = "serial: copy in, simulate, copy out"
     ms = st.elapsed_time(en) / a.steps
     edges = float(sim.records()[:, 19].sum())
     return {"value": edges / (ms / 1000.0), "unit": "agent-interactions/s",
             "ms_per_step": ms, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-            "edges_per_step": edges}
+            "edges_per_step": edges, "copies": mode}
 
 
 def measure_partition(steps, warmup, rank, local_rank, world, dist):

@@ -149,7 +149,8 @@ def load_library(path: os.PathLike | str | None = None) -> C.CDLL:
     global _lib
     if _lib is not None and path is None:
         return _lib
-    p = Path(path) if path else LIB_PATH
+    # EPI_B200_LIB: an alternative build of the library (A/B timing of kernel variants)
+    p = Path(path) if path else Path(os.environ.get("EPI_B200_LIB", LIB_PATH))
     if not p.exists():
         raise DeviceError(f"{p} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
     lib = C.CDLL(str(p))

@@ -269,6 +269,7 @@ class ConfigSimulation:
         self._graph.replay()
         self.clock = self.horizon
 
+
     # -- outputs ----------------------------------------------------------------
     def records(self) -> np.ndarray:
         return self.rec[:self.clock].cpu().numpy()
@@ -317,3 +318,71 @@ def csr_to_graph(step, entries, row_len, cap) -> StepGraph:
     src = (e >> 2).to(torch.int32) & 0x3FFFFFFF
     kind = (e & 3).to(torch.int8)
     return StepGraph(step, src.contiguous(), dst.contiguous(), kind.contiguous())
+
+
+def pinned_columns(cols: AgentColumns) -> dict:
+    """The columns of a host `AgentColumns` as pinned tensors (the staging
+    buffers of `run_from_host`)."""
+    import torch
+    from .state import COLUMN_SPECS
+    out = {}
+    for name, dt, _ in COLUMN_SPECS:
+        arr = np.ascontiguousarray(getattr(cols, name), dtype=dt)
+        out[name] = torch.from_numpy(arr.view(np.uint8) if arr.dtype == np.bool_ else arr).pin_memory()
+    return out
+
+
+class HostPipeline:
+    """Whole simulations from host memory to host memory, pipelined: while
+    one captured simulation runs on the compute stream, the next one's
+    initial state is copied in (pinned host -> HBM, upload stream) and the
+    previous one's time series copied out (HBM -> pinned host, download
+    stream), so the copies hide under the compute.  Two simulations of the same population
+    alternate (`sims`); step k runs sims[k % 2].
+
+        pipe = HostPipeline([sim_a, sim_b])
+        for k, cols in enumerate(batches):             # pinned_columns(...)
+            pipe.submit(k, cols, out[k])               # out[k]: pinned int64 [horizon, 19]
+        pipe.drain()
+    """
+
+    def __init__(self, sims):
+        import torch
+        if len(sims) != 2:
+            raise ConfigError("HostPipeline alternates two simulations")
+        self.sims = sims
+        for s in sims:
+            if s._graph is None:
+                s.capture()
+        self.up = torch.cuda.Stream()
+        self.down = torch.cuda.Stream()
+        self.main = torch.cuda.current_stream()
+        self.done = [torch.cuda.Event(), torch.cuda.Event()]
+        self.uploaded = [torch.cuda.Event(), torch.cuda.Event()]
+        self.downloaded = [torch.cuda.Event(), torch.cuda.Event()]
+        self._used = [False, False]
+
+    def submit(self, k: int, host_cols: dict, out) -> None:
+        import torch
+        i = k & 1
+        s = self.sims[i]
+        with torch.cuda.stream(self.up):
+            if self._used[i]:
+                self.up.wait_event(self.done[i])     # its previous run no longer reads `initial`
+            for name, t in host_cols.items():
+                s.initial.t[name].copy_(t, non_blocking=True)
+            self.uploaded[i].record(self.up)
+        self.main.wait_event(self.uploaded[i])
+        if self._used[i]:
+            self.main.wait_event(self.downloaded[i])   # its last records are out
+        s.replay()
+        self.done[i].record(self.main)
+        self._used[i] = True
+        with torch.cuda.stream(self.down):
+            self.down.wait_event(self.done[i])
+            out.copy_(s.rec[:, SERIES_COLUMNS], non_blocking=True)
+            self.downloaded[i].record(self.down)
+
+    def drain(self) -> None:
+        """Make the compute stream wait for the last copies out."""
+        self.main.wait_stream(self.down)

@@ -177,3 +177,34 @@ def test_persistent_runs_are_deterministic_under_repetition():
         assert torch.equal(s.rec, rec0), k
         assert torch.equal(s._codes_buf, codes0), k
         assert torch.equal(s.state.t["stage"], st0), k
+
+
+def test_host_pipeline_results_equal_serial_runs():
+    """sim.HostPipeline (copies of neighbouring steps under the compute):
+    every step's time series equals the serial copy-in / run / copy-out."""
+    from paper_2110_04421_b200.keyed import replication_seed
+    from paper_2110_04421_b200.sim import HostPipeline, pinned_columns
+    spec = ConfigNetworkSpec.config(1, n_agents=20_011, initial_infections=200)
+    pop = synthesize(spec, 3)
+    d, t, iv = default_disease(), default_progression(), InterventionConfig()
+    sims = [ConfigSimulation(pop, d, t, iv, 13, mode="fused", horizon=90) for _ in range(2)]
+    inits = []
+    for r in range(5):       # different initial states: seeded by different replications
+        other = ConfigSimulation(pop, d, t, iv, replication_seed(0, r), mode="fused", horizon=90)
+        inits.append(other.initial_host_columns())
+    want = []
+    for c in inits:
+        ref = ConfigSimulation(pop, d, t, iv, 13, mode="fused", horizon=90)
+        ref.initial.upload(c)
+        ref.reset()
+        ref.run()
+        want.append(ref.time_series())
+    pipe = HostPipeline(sims)
+    outs = [torch.empty((90, 19), dtype=torch.int64).pin_memory() for _ in inits]
+    for k, c in enumerate(inits):
+        pipe.submit(k, pinned_columns(c), outs[k])
+    pipe.drain()
+    torch.cuda.synchronize()
+    for k in range(len(inits)):
+        assert np.array_equal(outs[k].numpy(), want[k]), k
+    assert not np.array_equal(want[0], want[1])
