@@ -1378,6 +1378,50 @@ __device__ __forceinline__ void iv_post_agent(const StepArgs& A, int64_t a, uint
   }
 }
 
+// iv_post_agent in two parts for k_iv_run, which takes the eligibility into
+// the day's first phase (see there): the vaccination bucket + active count,
+// and the rest (DEN follow-up, dropout, due immunity checks) in order.
+__device__ __forceinline__ uint8_t iv_elig_agent(const StepArgs& A, int64_t a, unsigned* h, unsigned& active) {
+  const epi_params* __restrict__ P = A.P;
+  const epi_state& st = A.st;
+  const int stage = st.stage[a];
+  active = active_stage(stage);
+  const bool blocked = stage == S_DEAD || stage == S_HOSP || stage == S_ICU;
+  const int vs = st.vaccine_status[a];
+  const bool d1 = vs == 0 && !blocked;
+  const int32_t d1at = st.dose1_at[a];
+  const bool d2 = vs == 1 && d1at != NEVER && A.step >= d1at + P->dose_gap && !blocked;
+  uint8_t bk = NO_BUCKET;
+  if (d1 || d2) {
+    const int age = st.age_band[a];
+    int group;
+    if (P->strategy == 0) group = d2 ? 0 : 1;
+    else if (P->strategy == 1) group = d2 ? 1 : 0;
+    else group = (age >= P->elderly_band) ? 0 : (d2 ? 2 : 1);
+    bk = (uint8_t)((group * 9 + (8 - age)) * 2 + (d2 ? 1 : 0));
+    atomicAdd(&h[bk], 1u);
+  }
+  return bk;
+}
+__device__ __forceinline__ void iv_post_rest_agent(const StepArgs& A, int64_t a, unsigned& notified) {
+  const epi_params* __restrict__ P = A.P;
+  const epi_state& st = A.st;
+  const int step = A.step;
+  const uint8_t fl = A.flags[a];
+  if (P->den_enabled && (fl & FL_NOTIFIED) && st.has_den_app[a] &&
+      st.quarantine_until[a] <= step && st.stage[a] != S_DEAD) {
+    notified = 1;
+    if (draw(A.K, A.inj, P_DEN, a) < P->den_compliance) st.den_test_due_at[a] = step + 1;
+  }
+  if (P->quarantine_enabled && st.quarantine_until[a] > step && st.quarantine_started_at[a] < step) {
+    if (draw(A.K, A.inj, P_QDROP, a) < P->quarantine_dropout) st.quarantine_until[a] = step;
+  }
+  if (P->vaccination_enabled && st.immunity_check_at[a] == step) {
+    const int dose = st.immunity_check_dose[a];
+    if (dose == 1 || dose == 2) realize_immunity(A, a, dose);
+  }
+}
+
 __global__ void k_iv_post(StepArgs A, uint8_t* __restrict__ bucket, unsigned long long* __restrict__ hist) {
   __shared__ RecAcc racc;
   __shared__ unsigned h[NUM_BUCKETS];

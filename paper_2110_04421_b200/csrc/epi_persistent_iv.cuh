@@ -119,6 +119,8 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
     RecAcc& rc = racc[d & 1];
     int pend = -1;                         // the day's deferred transition scheduling
     int age = 0;
+    uint8_t bk = NO_BUCKET;                // the agent's vaccination bucket of the day
+    unsigned long long* hist = R.hist + (size_t)par * IV_HIST;
     const uint16_t* codes = R.codes[par];
     uint16_t* codes_next = R.codes[par ^ 1];
     const WorkTables& W = R.wt[par];
@@ -224,10 +226,31 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
       }
       rec_events(rc, ev);
       rec_add(rc, EPI_REC_EDGES, edges);
+      // the vaccination eligibility of the day (bucket + active count,
+      // engine.py:286-302), here in phase A: none of the phases between
+      // (test delivery, DEN follow-ups, dropout, immunity realisation) changes
+      // a stage's active / blocked class, a vaccine status or a dose date, so
+      // the histogram is complete at the first barrier of the day
+      if (R.vax) {
+        unsigned active = 0;
+        if (valid) bk = iv_elig_agent(A, b, h_s, active);
+        rec_add(rc, EPI_REC_ACTIVE, active);
+        const unsigned wa = __reduce_add_sync(0xFFFFFFFFu, active);
+        if (lane == 0 && wa) atomicAdd(&hist[NUM_BUCKETS], (unsigned long long)wa);
+      }
+    }
+    if (R.vax) {
+      // the block's histogram to the day's histogram and to its tile row
+      __syncthreads();
+      for (int i = threadIdx.x; i < NUM_BUCKETS; i += blockDim.x) {
+        const unsigned v = h_s[i];
+        R.tile_hist[(size_t)blockIdx.x * NUM_BUCKETS + i] = v;
+        if (v) atomicAdd(&hist[i], (unsigned long long)v);
+        h_s[i] = 0u;                        // next used in tomorrow's phase A
+      }
     }
     // tomorrow's code and push tables: final once phase C's dropout has run
-    // (a dose only turns code-0 susceptibles into code-0 vaccinated agents),
-    // so they overlap the histogram barrier
+    // (a dose only turns code-0 susceptibles into code-0 vaccinated agents)
     auto next_day = [&]() {
       uint16_t cn = 0;
       if (valid) {
@@ -277,8 +300,9 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
     const int first_day = t - R.den_lookback > 0 ? t - R.den_lookback : 0;
     const int n_back = t - first_day;
     const bool phase_b = R.den && R.tests && n_back > 0;
+    // barrier 1: the notifier list and the eligibility histogram are complete
+    if (phase_b || R.vax) grid_barrier(R.barrier, ++bar * gridDim.x);
     if (phase_b) {
-      grid_barrier(R.barrier, ++bar * gridDim.x);
       if (!service) {
         const int64_t items = (int64_t)LDM(R.den_count) * n_back;
         const int64_t gw = (int64_t)blockIdx.x * nwa + warp, warps = (int64_t)gridDim.x * nwa;
@@ -289,53 +313,12 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
                          R.died_at, A.flags, lane);
         }
       }
+      // barrier 2: the notifications are complete
       grid_barrier(R.barrier, ++bar * gridDim.x);
     }
-    // ---- phase C: follow-ups, dropout, immunity, eligibility ---------------
-    unsigned long long* hist = R.hist + (size_t)par * IV_HIST;
-    if (R.post) {
-      if (!service) {
-        unsigned notified = 0, active = 0;
-        if (valid) iv_post_agent(A, b, R.bucket, h_s, notified, active);
-        rec_add(rc, EPI_REC_NOTIFY, notified);
-        rec_add(rc, EPI_REC_ACTIVE, active);
-        if (R.vax) {
-          const unsigned wa = __reduce_add_sync(0xFFFFFFFFu, active);
-          if (lane == 0 && wa) atomicAdd(&hist[NUM_BUCKETS], (unsigned long long)wa);
-        }
-      }
-      if (R.vax) {
-        // split barrier: arrive with the histogram, build tomorrow's code and
-        // tables, then wait
-        __syncthreads();
-        for (int i = threadIdx.x; i < NUM_BUCKETS; i += blockDim.x) {
-          const unsigned v = h_s[i];
-          R.tile_hist[(size_t)blockIdx.x * NUM_BUCKETS + i] = v;
-          if (v) atomicAdd(&hist[i], (unsigned long long)v);
-          h_s[i] = 0u;                      // next used in tomorrow's phase C
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-          unsigned v;
-          asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(v) : "l"(R.barrier) : "memory");
-        }
-        if (!service) next_day();
-        __syncthreads();
-        ++bar;
-        if (threadIdx.x == 0) {
-          unsigned v;
-          do {
-            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(R.barrier) : "memory");
-          } while (v < bar * gridDim.x);
-        }
-        __syncthreads();
-      } else if (!service) {
-        next_day();
-      }
-    } else if (!service) {
-      next_day();
-    }
-    // ---- phase D: doses, record, next codes, tomorrow's tables -------------
+    // ---- phase C+D: the vaccination plan (every block derives it from the
+    // complete histogram), follow-ups / dropout / immunity, doses in id order,
+    // tomorrow's codes and tables ---------------------------------------------
     long long cut = -1, rem = 0;
     if (R.vax) {
       if (warp == 0) {
@@ -389,8 +372,14 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
         part = __reduce_add_sync(0xFFFFFFFFu, part);
         if (lane == 0 && part) atomicAdd(&off_s, (int)part);
       }
+    }
+    if (R.post && !service) {
+      unsigned notified = 0;
+      if (valid) iv_post_rest_agent(A, b, notified);   // before the dose: engine.py:275-283 then 293-335
+      rec_add(rc, EPI_REC_NOTIFY, notified);
+    }
+    if (R.vax) {
       // cut-bucket rank of each agent in id order: warp ballots + warp offsets
-      const uint8_t bk = valid ? R.bucket[b] : NO_BUCKET;
       const bool in_cut = cut >= 0 && cut < NUM_BUCKETS && bk == (uint8_t)cut;
       const unsigned ball = __ballot_sync(0xFFFFFFFFu, in_cut);
       if (lane == 0) wsum_s[warp] = __popc(ball);
@@ -402,6 +391,7 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
       if (blockIdx.x == 0)                // tomorrow's histogram starts empty
         for (int i = threadIdx.x; i < IV_HIST; i += blockDim.x) R.hist[(size_t)(par ^ 1) * IV_HIST + i] = 0;
     }
+    if (!service) next_day();
     if (!service) {
       int stage = 0;
       int32_t inf = 0;
