@@ -967,8 +967,8 @@ int epi_net_attach(epi_ctx* c, const epi_net* net) {
     if (c->host.den_lookback > DEN_MAX_DAYS) return fail(EPI_EARG, "den.lookback > 16 on config networks");
     rc = dalloc(&c->died_at, (size_t)c->n);
     if (!rc) rc = dalloc(&c->den_mark, (size_t)c->n + 4);
-    if (!rc) rc = dalloc(&c->den_list, (size_t)c->n);
-    if (!rc) rc = dalloc(&c->den_count, 1);
+    if (!rc) rc = dalloc(&c->den_list, 2 * (size_t)c->n);     // [2][n]: k_iv_run uses both day parities
+    if (!rc) rc = dalloc(&c->den_count, 2);
     if (rc) return rc;
     k_fill_i32<<<grid_for(c->n, 256), 256>>>(c->died_at, c->n, INT32_MAX);
     CKL();
@@ -1482,6 +1482,7 @@ static int launch_iv_run(epi_ctx* c, const epi_state* st, int32_t first, int32_t
   const bool listed = p.den_enabled && p.testing_enabled && c->den_list != nullptr;
   R.den_list = listed ? c->den_list : nullptr;
   R.den_count = listed ? c->den_count : nullptr;
+  R.den_stride = c->n;
   R.died_at = p.den_enabled ? c->died_at : nullptr;
   R.den_lookback = p.den_lookback;
   R.den = listed ? 1 : 0;
@@ -1645,7 +1646,7 @@ int epi_sim_run(epi_ctx* c, const epi_state* st, int32_t first_step, int32_t n_d
     }
     if (n_days - d0 >= 1) {
       // the per-day path's notifier list / histogram state is not carried over
-      if (c->den_count) CK(cudaMemsetAsync(c->den_count, 0, sizeof(int), S(stream)));
+      if (c->den_count) CK(cudaMemsetAsync(c->den_count, 0, 2 * sizeof(int), S(stream)));
       return launch_iv_run(c, st, first_step + d0, n_days - d0, seed, codes0, codes1,
                            records + (size_t)d0 * EPI_REC_LEN, vax_open, S(stream));
     }

@@ -1403,15 +1403,17 @@ __device__ __forceinline__ uint8_t iv_elig_agent(const StepArgs& A, int64_t a, u
   }
   return bk;
 }
-__device__ __forceinline__ void iv_post_rest_agent(const StepArgs& A, int64_t a, unsigned& notified) {
+// (k_iv_run applies the DEN follow-up itself, the next morning: den = false)
+__device__ __forceinline__ void iv_post_rest_agent(const StepArgs& A, int64_t a, bool den) {
   const epi_params* __restrict__ P = A.P;
   const epi_state& st = A.st;
   const int step = A.step;
-  const uint8_t fl = A.flags[a];
-  if (P->den_enabled && (fl & FL_NOTIFIED) && st.has_den_app[a] &&
-      st.quarantine_until[a] <= step && st.stage[a] != S_DEAD) {
-    notified = 1;
-    if (draw(A.K, A.inj, P_DEN, a) < P->den_compliance) st.den_test_due_at[a] = step + 1;
+  if (den) {
+    const uint8_t fl = A.flags[a];
+    if (P->den_enabled && (fl & FL_NOTIFIED) && st.has_den_app[a] &&
+        st.quarantine_until[a] <= step && st.stage[a] != S_DEAD) {
+      if (draw(A.K, A.inj, P_DEN, a) < P->den_compliance) st.den_test_due_at[a] = step + 1;
+    }
   }
   if (P->quarantine_enabled && st.quarantine_until[a] > step && st.quarantine_started_at[a] < step) {
     if (draw(A.K, A.inj, P_QDROP, a) < P->quarantine_dropout) st.quarantine_until[a] = step;

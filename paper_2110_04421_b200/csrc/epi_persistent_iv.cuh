@@ -41,14 +41,33 @@ struct IvRunArgs {
   unsigned long long* hist;       // [2][NUM_BUCKETS + 1] by day parity (+ active count)
   unsigned* tile_hist;            // [blocks][NUM_BUCKETS]
   int32_t* vax_open;
-  int32_t* den_list;
-  int* den_count;
+  int32_t* den_list;              // [2][den_stride] by day parity
+  int* den_count;                 // [2] by day parity
+  int64_t den_stride;
   int32_t* died_at;
   int den_lookback;
   int den, tests, post, vax;      // phases present
 };
 
 constexpr int IV_HIST = NUM_BUCKETS + 1;
+
+// Phase 4b of day t - 1 for agent b, applied at the start of day t:
+// notified (marked by a notifier's contact regeneration) and eligible then
+// -> den_test_due_at = t with the compliance draw of day t - 1
+// (engine.py:244-262); counted in day t - 1's record; the day's flags cleared.
+__device__ __forceinline__ void den_follow_up(const IvRunArgs& R, int64_t b, bool valid, bool den_ok,
+                                              uint64_t den_pref, int t, RecAcc& rc_prev) {
+  unsigned notified = 0;
+  if (valid) {
+    const uint8_t fl = R.A0.flags[b];
+    if (den_ok && (fl & FL_NOTIFIED)) {
+      notified = 1;
+      if (keyed_u(den_pref, (uint64_t)b, 0) < R.A0.P->den_compliance) R.A0.st.den_test_due_at[b] = t;
+    }
+    R.A0.flags[b] = 0;
+  }
+  rec_add(rc_prev, EPI_REC_NOTIFY, notified);
+}
 
 __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_net net) {
   constexpr int HH = 8, DR = 8;
@@ -109,6 +128,12 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
   const bool works = w >= 0 && m >= 2;
   const int64_t start = b - off;
   unsigned bar = 0;                        // barriers passed
+  // DEN: whether the agent could be notified today (engine.py:253-256:
+  // has the app, not quarantined, alive -- after today's test delivery,
+  // before dropout) and today's compliance-draw key; the notification itself
+  // is applied at the start of tomorrow, once every block's marks are in
+  bool den_ok = false;
+  uint64_t den_pref = 0;
   __syncthreads();
   uint2 shp = works ? day_shifts(dk[0].wshift, w, m) : make_uint2(0, 0);   // the day's colleague shifts
   for (int d = 0; d < R.n_days; ++d) {
@@ -125,6 +150,13 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
     uint16_t* codes_next = R.codes[par ^ 1];
     const WorkTables& W = R.wt[par];
     const WorkTables& Wn = R.wt[par ^ 1];
+    if (R.den && d > 0) {
+      // yesterday's exposure notifications (phase 4b of t - 1): the marks of
+      // every block are complete since the barrier; counted in yesterday's
+      // record, which the service warp flushes after this
+      if (!service) den_follow_up(R, b, valid, den_ok, den_pref, t, racc[(d - 1) & 1]);
+      __syncthreads();
+    }
     // ---- phase A ----------------------------------------------------------
     if (service) {
       if (d > 0) rec_flush_warp(racc[(d - 1) & 1], R.records + (size_t)(d - 1) * EPI_REC_LEN, t - 1, nwa, lane);
@@ -217,8 +249,13 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
       if (R.tests) {
         if (valid) {
           uint8_t fl = (ev & 8u) ? FL_SYMPTOMATIC : A.flags[b];
-          tested = test_agent(A, b, h.stage, fl, R.den ? R.den_list : nullptr, R.den_count);
+          tested = test_agent(A, b, h.stage, fl, R.den ? R.den_list + (size_t)par * R.den_stride : nullptr,
+                              R.den_count ? R.den_count + par : nullptr);
           A.flags[b] = fl;
+        }
+        if (R.den) {
+          den_ok = valid && st.has_den_app[b] && st.quarantine_until[b] <= t && h.stage != S_DEAD;
+          den_pref = A.K.p[P_DEN];
         }
         rec_add(rc, EPI_REC_TESTS, tested);
       } else if (valid && (ev & 8u)) {
@@ -304,17 +341,19 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
     if (phase_b || R.vax) grid_barrier(R.barrier, ++bar * gridDim.x);
     if (phase_b) {
       if (!service) {
-        const int64_t items = (int64_t)LDM(R.den_count) * n_back;
-        const int64_t gw = (int64_t)blockIdx.x * nwa + warp, warps = (int64_t)gridDim.x * nwa;
+        const int64_t items = (int64_t)LDM(R.den_count + par) * n_back;
+        const int32_t* list = R.den_list + (size_t)par * R.den_stride;
+        // items spread over the blocks first (a few hundred items: one per
+        // block and warp, so no block carries more than its share)
+        const int64_t gw = (int64_t)warp * gridDim.x + blockIdx.x, warps = (int64_t)gridDim.x * nwa;
         for (int64_t it = gw; it < items; it += warps) {
           const int dd = (int)(it % n_back);
           const int day = first_day + dd;
-          den_regen_item(net, make_net_keys(R.seed, day), day, LDM(R.den_list + it / n_back), rk_w[warp], wrad,
+          den_regen_item(net, make_net_keys(R.seed, day), day, LDM(list + it / n_back), rk_w[warp], wrad,
                          R.died_at, A.flags, lane);
         }
       }
-      // barrier 2: the notifications are complete
-      grid_barrier(R.barrier, ++bar * gridDim.x);
+      // no barrier: nothing until tomorrow reads the marks (see den_ok)
     }
     // ---- phase C+D: the vaccination plan (every block derives it from the
     // complete histogram), follow-ups / dropout / immunity, doses in id order,
@@ -373,11 +412,8 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
         if (lane == 0 && part) atomicAdd(&off_s, (int)part);
       }
     }
-    if (R.post && !service) {
-      unsigned notified = 0;
-      if (valid) iv_post_rest_agent(A, b, notified);   // before the dose: engine.py:275-283 then 293-335
-      rec_add(rc, EPI_REC_NOTIFY, notified);
-    }
+    if (R.post && !service && valid) iv_post_rest_agent(A, b, false);   // dropout, due immunity checks
+    if (blockIdx.x == 0 && threadIdx.x == 0 && R.den_count) R.den_count[par ^ 1] = 0;   // tomorrow's list
     if (R.vax) {
       // cut-bucket rank of each agent in id order: warp ballots + warp offsets
       const bool in_cut = cut >= 0 && cut < NUM_BUCKETS && bk == (uint8_t)cut;
@@ -398,11 +434,10 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
       if (valid) {
         stage = st.stage[b];
         inf = st.infected_at[b];
-        A.flags[b] = 0;
+        if (!R.den) A.flags[b] = 0;       // (with DEN: cleared by tomorrow's follow-up)
       }
       rec_agent(rc, valid, stage, inf);
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0 && R.den_count) *R.den_count = 0;   // tomorrow's notifier list
     if (d + 1 < R.n_days) {
       // end of day, split: tomorrow's shifts hashed between arrive and wait
       __syncthreads();
@@ -429,6 +464,13 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
       hs.age = age;
       schedule_pending(A.P, st, A.K, t, A.tau_lut, b, pend, hs);
     }
+  }
+  if (R.den) {
+    // the last day's notifications, once every block's marks are in
+    grid_barrier(R.barrier, ++bar * gridDim.x);
+    if (!service)
+      den_follow_up(R, b, valid, den_ok, den_pref, R.first_step + R.n_days, racc[(R.n_days - 1) & 1]);
+    if (blockIdx.x == 0 && threadIdx.x == 0 && R.den_count) R.den_count[0] = R.den_count[1] = 0;
   }
   __syncthreads();
   if (service)
