@@ -216,9 +216,11 @@ def run_reference(a):
     e = sum(s_[0] for s_ in steps)
     w = sum(s_[1] for s_ in steps)
     v = e / w
+    graphs = ("the reference's own GraphRealizer, runner.initialize_run" if a.workload == "refnet" else
+              "oracle/confignet_np restatement of the config generator")
     sample = (f"each step: {cores} processes x {per_step:.1f}s of the unmodified reference engine "
               f"(epivec.engine.Engine from baseline/_ref, fp64) stepping whole 180-day replications "
-              f"in sequence (graphs: oracle/confignet_np restatement of the config generator); "
+              f"in sequence (graphs: {graphs}); "
               f"{days_done} simulated days over the timed steps ({days_done / max(1, cores):.0f} "
               f"per process" + ("; every process covers the whole horizon" if days_done >= cores * HORIZON
                                 else "; early days of the horizon only: a short run") + ")")

@@ -1818,6 +1818,8 @@ int epi_refnet_create(const epi_refnet_desc* d, epi_refnet_t** out) {
       S.loser_cap = lattice;
       if (!rc) rc = dalloc(&S.ws_losers, (size_t)lattice + 1);
       if (!rc) rc = dalloc(&S.n_losers, 1);
+      if (!rc) rc = dalloc(&S.links_done, 1);
+      if (!rc && cudaMemset(S.links_done, 0, sizeof(unsigned)) != cudaSuccess) rc = fail(EPI_ECUDA, "memset");
       r->ws_blocks = (int)std::min<int64_t>(std::max<int64_t>((most + 255) / 256, 1), 1024);
       if (!rc) rc = dalloc(&S.stub_owner, (size_t)stubs + 1);
       if (!rc) rc = dalloc(&S.pair_uv, (size_t)(stubs / 2) + 1);
@@ -1852,6 +1854,7 @@ int epi_refnet_destroy(epi_refnet_t* r) {
   cudaFree(r->sc.pair_uv);
   cudaFree(r->sc.ws_losers);
   cudaFree(r->sc.n_losers);
+  cudaFree(r->sc.links_done);
   cudaFree(r->scan_tmp);
   delete r;
   return 0;
@@ -1904,8 +1907,8 @@ static int refnet_realize_impl(epi_refnet_t* r, uint64_t seed, int32_t step, Dea
   const int links = ws_blocks * r->net.n_occ + grid_for(S.max_stubs / 2, 256);
   CK(launch_pdl(k_ref_links<0>, dim3(links), dim3(256), 0, s, r->net, S, ws, K, ws_blocks));
   CK(launch_pdl(k_ref_links<1>, dim3(links), dim3(256), 0, s, r->net, S, ws, K, ws_blocks));
-  // 5: rewired lattice edges whose pair was taken draw again (edge count preserved)
-  if (ws_blocks > 0) CK(launch_pdl(k_ref_ws_resolve, dim3(1), dim3(1024), 0, s, r->net, S, ws));
+  // (the rewired lattice edges whose pair was taken draw again in launch 4's
+  // last block: the edge count is preserved)
   if (count_dev) return 0;                  // no synchronisation: count + error bits stay on the device
   unsigned long long h[2] = {0, 0};
   CK(cudaMemcpyAsync(h, S.counter, sizeof(h), cudaMemcpyDeviceToHost, s));

@@ -13,7 +13,8 @@
 //    one-for-one, so the undirected edge count is always n*k/2"), a rewired
 //    pair that collides with another is drawn again, never dropped: the
 //    lowest edge index keeps a contested pair, every other contender draws
-//    again from u_{1+r}(e) in round r (k_ref_ws_resolve), and a pair placed
+//    again from u_{1+r}(e) in round r (ws_resolve_block, run by the last block of
+//    launch 4), and a pair placed
 //    in an earlier round is never taken over.  An edge still unplaced after
 //    WS_ROUNDS draws keeps its lattice pair (the reference's "no free target:
 //    keep v"; free, since rewired targets are never lattice neighbours);
@@ -67,6 +68,7 @@ struct RefScratch {
                                   // index; ~0 once placed), appended by launch 4
   unsigned* n_losers;             // zeroed by launch 1
   int64_t loser_cap;              // the lattice edges of all occupations
+  unsigned* links_done;           // blocks of launch 4 finished (the last one resolves; reset by it)
 };
 
 __device__ __forceinline__ double ref_u(uint64_t prefix, uint64_t idx, uint64_t k) {
@@ -287,7 +289,7 @@ __device__ __forceinline__ void ws_block(const RefNet& net, const RefScratch& S,
           table_insert(S, key, idx);
         } else {
           emit = table_is_winner(S, key, idx);
-          if (!emit) {                   // drawn again by k_ref_ws_resolve
+          if (!emit) {                   // drawn again by ws_resolve_block
             const unsigned at = atomicAdd(S.n_losers, 1u);
             if (at < S.loser_cap) S.ws_losers[at] = idx;
             else atomicOr(&S.counter[1], 8ull);
@@ -302,7 +304,7 @@ __device__ __forceinline__ void ws_block(const RefNet& net, const RefScratch& S,
   }
 }
 
-// Launch 5: the rewired lattice edges whose first pair was taken draw
+// Launch 4's last block: the rewired lattice edges whose first pair was taken draw
 // again, in rounds r = 1, 2, ... (one block; a handful of edges per step).
 // Round r: every unplaced edge proposes the pair of draw u_{1+r} and inserts
 // it with value r << 56 | edge index, so a pair placed in an earlier round
@@ -311,15 +313,13 @@ __device__ __forceinline__ void ws_block(const RefNet& net, const RefScratch& S,
 // separated by bar.sync; table words written in this launch are read with
 // ld.cg (the atomics are performed in L2).
 constexpr int WS_ROUNDS = 64;
-__global__ void __launch_bounds__(1024) k_ref_ws_resolve(RefNet net, RefScratch S, uint64_t ws_prefix) {
-  pdl_wait();
-  pdl_trigger();
-  const unsigned nl0 = *S.n_losers;
+__device__ __forceinline__ void ws_resolve_block(const RefNet& net, const RefScratch& S, uint64_t ws_prefix) {
+  const unsigned nl0 = __ldcg(S.n_losers);
   const unsigned nl = nl0 < S.loser_cap ? nl0 : (unsigned)S.loser_cap;
   if (nl == 0) return;
   // the proposal of loser li in round r (u, v, key, value)
   auto propose = [&](unsigned li, int r, int32_t& u, int32_t& v, uint64_t& key, uint64_t& val) {
-    const uint64_t idx = S.ws_losers[li];
+    const uint64_t idx = __ldcg(S.ws_losers + li);
     const int j = (int)(idx >> 40) - 1;
     const int64_t e = (int64_t)(idx & ((1ull << 40) - 1));
     const int lo = net.occ_start[j];
@@ -337,7 +337,7 @@ __global__ void __launch_bounds__(1024) k_ref_ws_resolve(RefNet net, RefScratch 
   };
   for (int r = 1; r <= WS_ROUNDS; ++r) {
     for (unsigned li = threadIdx.x; li < nl; li += blockDim.x) {
-      if (S.ws_losers[li] == ~0ull) continue;
+      if (__ldcg(S.ws_losers + li) == ~0ull) continue;
       int32_t u, v; uint64_t key, val;
       propose(li, r, u, v, key, val);
       table_insert(S, key, val);
@@ -348,7 +348,7 @@ __global__ void __launch_bounds__(1024) k_ref_ws_resolve(RefNet net, RefScratch 
       const unsigned li = b0 + threadIdx.x;
       bool won = false;
       int32_t u = 0, v = 0;
-      if (li < nl && S.ws_losers[li] != ~0ull) {
+      if (li < nl && __ldcg(S.ws_losers + li) != ~0ull) {
         uint64_t key, val;
         propose(li, r, u, v, key, val);
         uint64_t h = hash_slot(key, S.table_slots);
@@ -372,7 +372,7 @@ __global__ void __launch_bounds__(1024) k_ref_ws_resolve(RefNet net, RefScratch 
   // rewired edge, so never taken)
   for (unsigned b0 = 0; b0 < nl; b0 += blockDim.x) {
     const unsigned li = b0 + threadIdx.x;
-    const bool keep = li < nl && S.ws_losers[li] != ~0ull;
+    const bool keep = li < nl && __ldcg(S.ws_losers + li) != ~0ull;
     int32_t u = 0, v = 0;
     if (keep) {
       uint64_t key, val;
@@ -436,6 +436,20 @@ __global__ void k_ref_links(RefNet net, RefScratch S, uint64_t ws_prefix, PermKe
     ws_block<PASS>(net, S, ws_prefix, blockIdx.x / ws_blocks, blockIdx.x % ws_blocks, ws_blocks);
   else
     pairs_block<PASS>(net, S, K, blockIdx.x - nws, gridDim.x - nws);
+  if (PASS == 1 && net.n_occ > 0) {
+    // the last block to finish places the rewired edges whose pair was
+    // taken (no launch of its own: threadFence-reduction pattern)
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(S.links_done, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (last) {
+      __threadfence();
+      ws_resolve_block(net, S, ws_prefix);
+      if (threadIdx.x == 0) *S.links_done = 0u;
+    }
+  }
 }
 
 }  // namespace epi
