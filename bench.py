@@ -592,10 +592,11 @@ def end_to_end(sim, a, sim2=None):
     series back.  With `sim2` the steps go through `sim.HostPipeline`: the
     copies of step k +- 1 run on a copy stream under the compute of step k."""
     import torch
-    from paper_2110_04421_b200.sim import HostPipeline, pinned_columns
-    pinned = pinned_columns(sim.initial_host_columns())
+    from paper_2110_04421_b200.sim import HostPipeline
+    # the initial state in the device arena's layout, pinned: one copy in
+    pinned = sim.initial.host_arena(sim.initial_host_columns())
     outs = [torch.empty((sim.horizon, 19), dtype=torch.int64).pin_memory() for _ in range(2)]
-    h2d = sum(int(t.numel() * t.element_size()) for t in pinned.values())
+    h2d = int(pinned.numel())
     d2h = int(outs[0].numel() * outs[0].element_size())
     if sim2 is not None:
         pipe = HostPipeline([sim, sim2])
@@ -617,8 +618,7 @@ def end_to_end(sim, a, sim2=None):
         sim.capture()
 
         def once():
-            for name, t in pinned.items():
-                sim.initial.t[name].copy_(t, non_blocking=True)
+            sim.initial.arena.copy_(pinned, non_blocking=True)
             sim.replay()
             outs[0].copy_(sim.rec[:, :19], non_blocking=True)
         for _ in range(a.warmup):

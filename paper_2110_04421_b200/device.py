@@ -3,8 +3,9 @@
 `pack_params` flattens DiseaseParams / ProgressionTable / InterventionConfig
 (this package's or the reference's own classes: only attribute names are
 used) into the POD `epi_params` of the C ABI.  `DeviceColumns` holds one CUDA
-buffer per AgentColumns column with the same dtype (state.py:21-75), so host
-<-> device transfers are flat copies.
+buffer per AgentColumns column with the same dtype (state.py:21-75), views
+into one arena, so host <-> device transfers are flat copies and a whole
+state copies in one.
 """
 
 from __future__ import annotations
@@ -90,15 +91,28 @@ def pack_params(disease, table, interventions, n_agents: int) -> N.EpiParams:
 
 
 class DeviceColumns:
-    """One CUDA tensor per AgentColumns column (identical dtypes)."""
+    """One CUDA tensor per AgentColumns column (identical dtypes), all views
+    into one device arena (256-byte aligned columns), so copying a whole
+    state -- reset() to the initial state, once per simulation and inside
+    every captured run -- is one copy, not 22."""
+
+    ALIGN = 256
 
     def __init__(self, n_agents: int, device=None):
         import torch
         self.n_agents = n_agents
         self.device = torch.device(device or "cuda")
+        offs, at = [], 0
+        for name, dt, _ in COLUMN_SPECS:
+            offs.append(at)
+            at += -(-(n_agents * np.dtype(dt).itemsize) // self.ALIGN) * self.ALIGN
+        self.arena = torch.empty(max(at, self.ALIGN), dtype=torch.uint8, device=self.device)
         self.t = {}
-        for name, dt, fill in COLUMN_SPECS:
-            self.t[name] = torch.full((n_agents,), fill, dtype=_torch_dtype(dt), device=self.device)
+        for (name, dt, fill), off in zip(COLUMN_SPECS, offs):
+            nb = n_agents * np.dtype(dt).itemsize
+            v = self.arena[off:off + nb].view(_torch_dtype(dt))
+            v.fill_(fill)
+            self.t[name] = v
 
     @classmethod
     def from_host(cls, cols, device=None) -> "DeviceColumns":
@@ -127,15 +141,28 @@ class DeviceColumns:
         self.download(cols)
         return cols
 
+    def host_arena(self, cols, pin: bool = True):
+        """A host `AgentColumns` packed in this arena's layout (a pinned uint8
+        tensor): uploading it is one copy (`arena.copy_(host, non_blocking)`)."""
+        import torch
+        buf = torch.zeros(self.arena.numel(), dtype=torch.uint8)
+        base = self.arena.data_ptr()
+        for name, dt, _ in COLUMN_SPECS:
+            off = self.t[name].data_ptr() - base
+            arr = np.ascontiguousarray(getattr(cols, name), dtype=dt)
+            raw = arr.view(np.uint8).reshape(-1)
+            buf[off:off + raw.size] = torch.from_numpy(raw.copy())
+        return buf.pin_memory() if pin else buf
+
     def clone(self) -> "DeviceColumns":
-        d = DeviceColumns.__new__(DeviceColumns)
-        d.n_agents, d.device = self.n_agents, self.device
-        d.t = {k: v.clone() for k, v in self.t.items()}
+        d = DeviceColumns(self.n_agents, self.device)
+        d.arena.copy_(self.arena)
         return d
 
     def copy_from(self, other: "DeviceColumns") -> None:
-        for k, v in self.t.items():
-            v.copy_(other.t[k])
+        if other.n_agents != self.n_agents:
+            raise ConfigError("state sizes differ")
+        self.arena.copy_(other.arena)          # one copy for the 22 columns
 
     def struct(self) -> N.EpiState:
         s = N.EpiState()

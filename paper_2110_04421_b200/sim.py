@@ -362,15 +362,20 @@ class HostPipeline:
         self.downloaded = [torch.cuda.Event(), torch.cuda.Event()]
         self._used = [False, False]
 
-    def submit(self, k: int, host_cols: dict, out) -> None:
+    def submit(self, k: int, host_cols, out) -> None:
+        """host_cols: a pinned arena (`DeviceColumns.host_arena`, one copy)
+        or a dict of pinned columns (`pinned_columns`)."""
         import torch
         i = k & 1
         s = self.sims[i]
         with torch.cuda.stream(self.up):
             if self._used[i]:
                 self.up.wait_event(self.done[i])     # its previous run no longer reads `initial`
-            for name, t in host_cols.items():
-                s.initial.t[name].copy_(t, non_blocking=True)
+            if isinstance(host_cols, dict):
+                for name, t in host_cols.items():
+                    s.initial.t[name].copy_(t, non_blocking=True)
+            else:
+                s.initial.arena.copy_(host_cols, non_blocking=True)
             self.uploaded[i].record(self.up)
         self.main.wait_event(self.uploaded[i])
         if self._used[i]:

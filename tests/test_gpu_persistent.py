@@ -201,8 +201,8 @@ def test_host_pipeline_results_equal_serial_runs():
         want.append(ref.time_series())
     pipe = HostPipeline(sims)
     outs = [torch.empty((90, 19), dtype=torch.int64).pin_memory() for _ in inits]
-    for k, c in enumerate(inits):
-        pipe.submit(k, pinned_columns(c), outs[k])
+    for k, c in enumerate(inits):   # pinned column dicts and pinned arenas (one copy)
+        pipe.submit(k, pinned_columns(c) if k % 2 else sims[0].initial.host_arena(c), outs[k])
     pipe.drain()
     torch.cuda.synchronize()
     for k in range(len(inits)):
