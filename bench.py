@@ -184,6 +184,13 @@ def run_reference(a):
     rank, _, world = dist_env()
     if rank != 0:
         return
+    try:
+        from oracle.epivec_driver import import_epivec
+        import_epivec()
+    except ImportError as e:
+        print(json.dumps({"impl": "reference", "unavailable": f"the reference (epivec) is not installed in "
+                          f"baseline/_ref (tools/install_reference.sh): {e}"}), flush=True)
+        return
     import multiprocessing as mp
     cores = os.cpu_count() or 1
     # the whole --steps K --warmup W run within a few minutes
@@ -240,7 +247,11 @@ def run_reference(a):
 
 
 def cpu_baseline_single(workload, seconds):
-    e, days, t = _cpu_worker((workload, 12345, seconds))
+    try:
+        e, days, t = _cpu_worker((workload, 12345, seconds))
+    except ImportError as err:
+        return {"value": None, "unit": "agent-interactions/s", "cores": 1, "kind": "reference",
+                "sample": f"unavailable: the reference (epivec) is not installed in baseline/_ref ({err})"}
     return {"value": e / t, "unit": "agent-interactions/s", "cores": 1, "kind": "reference",
             "sample": f"unmodified reference engine (epivec.engine.Engine, baseline/_ref) on the "
                       f"restated config generator, 1 replica, days 0-{days - 1} of 180 "
