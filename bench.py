@@ -913,7 +913,11 @@ def run_refnet(a):
         "clocks": clocks,
     }
     if not a.no_cpu_baseline and world == 1:
-        e, days, t = _cpu_worker(("refnet", 12345, a.cpu_seconds))
+        try:
+            e, days, t = _cpu_worker(("refnet", 12345, a.cpu_seconds))
+        except ImportError as err:
+            e, days, t = 0, 0, float("nan")
+            line["cpu_baseline_error"] = f"the reference (epivec) is not installed in baseline/_ref ({err})"
         line["cpu_baseline"] = {"value": e / t, "unit": "agent-interactions/s", "cores": 1,
                                 "kind": "reference", "sample": f"the reference's own scenario "
                                 f"(epivec initialize_run + GraphRealizer + Engine, baseline/_ref), "
