@@ -17,7 +17,8 @@ if "--iv" in sys.argv:
     from bench import workload_iv
     iv = workload_iv("config2")
 reps = int(next((a for a in sys.argv[1:] if a.isdigit()), "20"))
-spec = ConfigNetworkSpec.config(1)
+cfg = 0 if "--config0" in sys.argv else 1
+spec = ConfigNetworkSpec.config(cfg)
 pop = synthesize(spec, 0)
 flush = torch.empty(384 * 1024 * 1024 // 4, device="cuda")
 mk = lambda p: ConfigSimulation(pop, default_disease(), default_progression(), iv, 3, mode="fused", persistent=p)
