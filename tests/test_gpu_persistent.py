@@ -208,3 +208,46 @@ def test_host_pipeline_results_equal_serial_runs():
     for k in range(len(inits)):
         assert np.array_equal(outs[k].numpy(), want[k]), k
     assert not np.array_equal(want[0], want[1])
+
+
+@pytest.mark.parametrize("case", range(10))
+def test_persistent_intervention_run_fuzz(case):
+    """k_iv_run (one launch for every intervention day: eligibility in the
+    day's first phase, DEN follow-ups the next morning) against one kernel
+    per phase, over random intervention settings: strategies, sterilizing or
+    not, dose latencies 0 / > 0, DEN lookbacks, test kinds, quarantine
+    length and dropout, false positives.  Bitwise records, state, codes."""
+    from paper_2110_04421_b200.interventions import (DenConfig, ImmunityMode, Strategy, TestKind,
+                                                     VaccinePolicy)
+    rng = np.random.default_rng(1000 + case)
+    tmin = int(rng.integers(1, 3))
+    den = bool(rng.random() < 0.8)
+    iv = InterventionConfig(
+        quarantine_enabled=bool(rng.random() < 0.8), quarantine_duration=int(rng.integers(1, 15)),
+        quarantine_dropout=float(rng.uniform(0, 0.3)), testing_enabled=True,
+        test_kind=TestKind("fz", float(rng.uniform(0.2, 1.0)), tmin, tmin + int(rng.integers(0, 3))),
+        false_positive_prob=float(rng.choice([0.0, 0.01])), den_enabled=den,
+        den=DenConfig(float(rng.uniform(0.2, 0.9)), float(rng.uniform(0.3, 1.0)), int(rng.integers(1, 8))),
+        vaccination_enabled=bool(rng.random() < 0.85),
+        vaccine=VaccinePolicy(strategy=Strategy(int(rng.integers(0, 3))), dose1_efficacy=float(rng.uniform(0.3, 1.0)),
+                              dose2_efficacy=float(rng.uniform(0.5, 1.0)), dose1_latency=int(rng.choice([0, 5, 12])),
+                              dose2_latency=int(rng.choice([0, 3])), dose_gap=int(rng.integers(3, 30)),
+                              daily_rate=float(rng.uniform(0.005, 0.05)), start_trigger=float(rng.uniform(0.0, 0.01)),
+                              immunity_mode=ImmunityMode(int(rng.integers(0, 2))), elderly_band=int(rng.integers(4, 8))))
+    n = int(rng.integers(3_000, 40_000))
+    spec = ConfigNetworkSpec.config(1, n_agents=n, initial_infections=max(20, n // 200))
+    pop = synthesize(spec, 7 + case)
+    d, t = default_disease(), default_progression()
+    a = ConfigSimulation(pop, d, t, iv, 100 + case, mode="fused", horizon=70, iv_fusion=True)
+    b = ConfigSimulation(pop, d, t, iv, 100 + case, mode="fused", horizon=70, iv_fusion=False)
+    assert a.uses_persistent_run() and not b.uses_persistent_run()
+    split = int(rng.integers(2, 40))
+    a.run(split); b.run(split)
+    a.run(); b.run()
+    ra, rb = a.rec.cpu().numpy(), b.rec.cpu().numpy()
+    assert np.array_equal(ra, rb), np.argwhere(ra != rb)[:5]
+    ha, hb = a.host_columns(), b.host_columns()
+    for c in IV_COLS + ("immunity_check_prob", "immunity_check_dose", "quarantine_started_at", "test_sample_at",
+                        "test_positive", "has_den_app"):
+        assert np.array_equal(getattr(ha, c), getattr(hb, c)), c
+    assert torch.equal(a._codes_buf, b._codes_buf)
