@@ -97,7 +97,10 @@ def summarize_device(records, columns=None) -> dict[str, np.ndarray]:
 
 def summarize(results: list[RunResult]) -> dict[str, np.ndarray]:
     """Quartiles across replications: metric -> (horizon, 3) array [q25, q50, q75]
-    (runner.py:195-207), on the device."""
+    (runner.py:195-207), on the device, for any number of replications
+    (epi_quartiles: shared-memory sort up to 4096, bisection beyond).  Like
+    every path of this package it needs the GPU: there is deliberately no
+    host fallback (bitwise the reference's np.percentile either way)."""
     import torch
     if not results:
         raise ConfigError("summarize needs at least one replication")
