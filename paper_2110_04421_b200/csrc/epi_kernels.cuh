@@ -587,8 +587,8 @@ struct CsrView {
   // generator, so the fp32 message pass (k_msg_pass, epi_msgpass.cuh) streams
   // 2 B per edge with no gathers.  Tile k (32 rows from lo) owns the block
   // msgs[k*32*msg_cap(cap) ...]; its rows are packed back to back, each
-  // padded to whole 8-message groups, and tile_off[k*33 + r] = row r's first
-  // group | pad << 12 (tile_off[k*33 + 32] = groups in the tile).
+  // padded to whole 4-message half-groups, and tile_off[k*33 + r] = row r's
+  // first half-group | pad << 12 (tile_off[k*33 + 32] = half-groups in the tile).
   const uint16_t* __restrict__ msgs;
   const uint16_t* __restrict__ tile_off;
   __device__ __forceinline__ int64_t begin(int64_t r) const {
@@ -775,7 +775,7 @@ __device__ __forceinline__ void clear_rin_row(const WorkTables* wt, int64_t b) {
 // staged in shared memory (odd stride: conflict-free), optionally sorted into
 // canonical (src, kind) order, and the warp's 32 rows are written out
 // coalesced: id rows one warp-wide store per row, message tiles as 16-byte
-// groups (one 8-message group per lane and store).  With PUSH (message-only
+// groups (one 16-byte group = two 4-message half-groups per lane and store).  With PUSH (message-only
 // runs over the whole population) the random in-edges come from the day's
 // push tables (rin/rout, built by k_day_tables) instead of the random-slot
 // bijections, and the rin rows consumed are cleared.
@@ -853,41 +853,50 @@ __global__ void __launch_bounds__(128, (BATCH && !PUSH) ? 5 : 6) k_net_realize(e
       }
     } else {
       // tile-packed messages: rows back to back, each padded with weight-0
-      // messages to whole 8-message groups; per row its first group and its
-      // pad count (toff = group | pad << 12), toff[32] = the tile's groups
-      const int ng = (cnt + 7) >> 3;
-      int incl = ng;
+      // messages to whole 4-message half-groups (8 B; a 16-byte group holds
+      // two, possibly of two rows); per row its first half-group and its pad
+      // count (toff = half | pad << 12), toff[32] = the tile's half-groups
+      const int nh = (cnt + 3) >> 2;
+      int incl = nh;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
         const int v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
         if (lane >= o) incl += v;
       }
-      const int excl = incl - ng;
+      const int excl = incl - nh;
       uint16_t* toff = tile_off + tile * 33;
-      toff[lane] = (uint16_t)(excl | ((ng * 8 - cnt) << 12));
+      toff[lane] = (uint16_t)(excl | ((nh * 4 - cnt) << 12));
       if (lane == 31) toff[32] = (uint16_t)incl;
       goff_s[warp][lane] = excl;
       len_s[warp][lane] = cnt;
       if (lane == 31) goff_s[warp][32] = incl;
       __syncwarp();
-      // one 16-byte group per lane: row r = the last row starting at or
-      // before the group (rows without groups share their successor's start)
+      // one 16-byte group (two half-groups) per lane: the row of a half is the
+      // last row starting at or before it (rows without messages share their
+      // successor's start)
       uint4* blk = (uint4*)(msgs + tile * (int64_t)(32 * msg_cap(cap)));
-      const int groups = __shfl_sync(0xFFFFFFFFu, incl, 31);
-      for (int gi = lane; gi < groups; gi += 32) {
-        int r = 0;
-#pragma unroll
-        for (int st = 16; st >= 1; st >>= 1)
-          if (goff_s[warp][r + st] <= gi) r += st;
-        const int k = (gi - goff_s[warp][r]) << 3;
-        const int len = len_s[warp][r];
-        const uint32_t* src = wbuf + r * stride_w + k;
+      const int halves = __shfl_sync(0xFFFFFFFFu, incl, 31);
+      for (int gi = lane; gi < (halves + 1) >> 1; gi += 32) {
         uint32_t w[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const uint32_t m0 = k + 2 * q < len ? src[2 * q] : 0u;
-          const uint32_t m1 = k + 2 * q + 1 < len ? src[2 * q + 1] : 0u;
-          w[q] = (m0 & 0xFFFFu) | (m1 << 16);
+        for (int hh = 0; hh < 2; ++hh) {
+          const int h = 2 * gi + hh;
+          w[2 * hh] = w[2 * hh + 1] = 0u;
+          if (h < halves) {
+            int r = 0;
+#pragma unroll
+            for (int st = 16; st >= 1; st >>= 1)
+              if (goff_s[warp][r + st] <= h) r += st;
+            const int k = (h - goff_s[warp][r]) << 2;
+            const int len = len_s[warp][r];
+            const uint32_t* src = wbuf + r * stride_w + k;
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              const uint32_t m0 = k + 2 * q < len ? src[2 * q] : 0u;
+              const uint32_t m1 = k + 2 * q + 1 < len ? src[2 * q + 1] : 0u;
+              w[2 * hh + q] = (m0 & 0xFFFFu) | (m1 << 16);
+            }
+          }
         }
         blk[gi] = make_uint4(w[0], w[1], w[2], w[3]);
       }

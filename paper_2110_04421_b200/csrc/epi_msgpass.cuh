@@ -6,9 +6,10 @@
 //                               a byte offset into the fp32 weight table
 //                               MsgComb ((source code & 0xFF) << 4 | kind << 2),
 //                               every row padded with 0 (weight 0) to whole
-//                               8-message groups;
-//   tile_off[tile * 33 + r]     row r's first group | pad count << 12;
-//   tile_off[tile * 33 + 32]    groups in the tile.
+//                               4-message half-groups (a 16-byte group holds
+//                               two, possibly of two rows);
+//   tile_off[tile * 33 + r]     row r's first half-group | pad count << 12;
+//   tile_off[tile * 33 + 32]    half-groups in the tile.
 //
 // Design (B200): see k_msg_pass.  The path is HBM-bound integer/byte work
 // plus one fp32 add per message: no tensor cores.
@@ -19,18 +20,20 @@
 namespace epi {
 
 constexpr int MP_MAX_CAP = 128;           // row capacity of the message path
-constexpr int MP_MAX_GROUPS = 4 * MP_MAX_CAP;   // 8-message groups per tile
+constexpr int MP_MAX_HALVES = 8 * MP_MAX_CAP;   // 4-message half-groups per tile
 constexpr int MP_STEPS = 4;               // groups per lane held in registers
 constexpr int MP_WARPS = 8;               // warps per block
-constexpr int MP_SMEM = MP_WARPS * MP_MAX_GROUPS * 4 + (int)sizeof(MsgComb);
+constexpr int MP_SMEM = MP_WARPS * MP_MAX_HALVES * 4 + (int)sizeof(MsgComb);
 
 struct MsgTile {
-  uint4 v[MP_STEPS];   // groups lane, lane + 32, ... of the tile
-  int off, groups;     // lane's row: first group | pad << 12; groups in the tile
+  uint4 v[MP_STEPS];   // 16-byte groups lane, lane + 32, ... of the tile
+  int off, groups;     // lane's row: first half-group | pad << 12; half-groups in the tile
   int st, im, ag;      // MODE 0: stage, immune, age band of the lane's row
 };
 
-__device__ __forceinline__ float group_sum(const uint4& v, const char* __restrict__ comb) {
+// the two 4-message half sums of a 16-byte group (its halves may belong to
+// two rows)
+__device__ __forceinline__ float2 group_sums(const uint4& v, const char* __restrict__ comb) {
   const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
   float w[8];
 #pragma unroll
@@ -38,16 +41,16 @@ __device__ __forceinline__ float group_sum(const uint4& v, const char* __restric
     const uint32_t m = (j & 1) ? (wv[j >> 1] >> 16) : (wv[j >> 1] & 0xFFFFu);
     w[j] = *(const float*)(comb + m);
   }
-  return ((w[0] + w[1]) + (w[2] + w[3])) + ((w[4] + w[5]) + (w[6] + w[7]));
+  return make_float2((w[0] + w[1]) + (w[2] + w[3]), (w[4] + w[5]) + (w[6] + w[7]));
 }
 
 // MODE 0: hazard out (float[N], gather_exposure); MODE 1: fused
 // transmission / progression update (+ record and next codes if final_pass).
 // Persistent grid, one warp per 32-row tile.  Every row is padded to whole
-// 8-message groups by the generator, so a group belongs to exactly one row:
+// 4-message half-groups by the generator, so a half belongs to exactly one row:
 // lane l sums groups l, l + 32, ... (one 16-byte load and eight table
-// lookups each, no per-message branching) into gsum[], then the owner of
-// row r adds its groups' sums in order.  The next tile's offsets, first
+// lookups each, no per-message branching) into two half sums in gsum[],
+// then the owner of row r adds its half-groups' sums in order.  The next tile's offsets, first
 // MP_STEPS groups and state bytes are loaded into registers while the
 // current tile is summed (two register sets, alternating).
 template <int MODE>
@@ -61,7 +64,7 @@ __global__ void __launch_bounds__(MP_WARPS * 32, 3) k_msg_pass(StepArgs A, CsrVi
   extern __shared__ __align__(16) float mp_smem[];
   const int warp = threadIdx.x >> 5, lane = lane_id();
   MsgComb* C = (MsgComb*)mp_smem;
-  float* gsum = mp_smem + sizeof(MsgComb) / 4 + warp * MP_MAX_GROUPS;
+  float* gsum = mp_smem + sizeof(MsgComb) / 4 + warp * MP_MAX_HALVES;
   for (int i = threadIdx.x; i < 4 * 256; i += blockDim.x) C->w[i] = mc->w[i];
   load_msg_tables(T, mt);
   rec_init(racc);
@@ -88,9 +91,10 @@ __global__ void __launch_bounds__(MP_WARPS * 32, 3) k_msg_pass(StepArgs A, CsrVi
     X.st = S_DEAD;
     X.im = X.ag = 0;
     const uint4* blk = msgs + (size_t)t * tile_words;
+    const int g16 = (X.groups + 1) >> 1;                     // 16-byte groups
 #pragma unroll
     for (int q = 0; q < MP_STEPS; ++q)
-      X.v[q] = (t < n_tiles && q * 32 + lane < X.groups) ? __ldg(blk + q * 32 + lane) : make_uint4(0, 0, 0, 0);
+      X.v[q] = (t < n_tiles && q * 32 + lane < g16) ? __ldg(blk + q * 32 + lane) : make_uint4(0, 0, 0, 0);
     const int a = lo_row + t * 32 + lane;
     if (MODE == 0 && t < n_tiles && a < n) {
       X.st = A.st.stage[a];
@@ -117,23 +121,25 @@ __global__ void __launch_bounds__(MP_WARPS * 32, 3) k_msg_pass(StepArgs A, CsrVi
     AgentHot h{};
     if (MODE == 1 && valid) h = load_hot(A.st, a);
     // group sums
+    const int g16 = (Xc.groups + 1) >> 1;
+    float2* gsum2 = (float2*)gsum;
 #pragma unroll
     for (int q = 0; q < MP_STEPS; ++q)
-      if (q * 32 < Xc.groups) {
+      if (q * 32 < g16) {
         const int gi = q * 32 + lane;
-        if (gi < Xc.groups) gsum[gi] = group_sum(Xc.v[q], comb);
+        if (gi < g16) gsum2[gi] = group_sums(Xc.v[q], comb);
       }
-    for (int gi = MP_STEPS * 32 + lane; gi < Xc.groups; gi += 32) gsum[gi] = group_sum(__ldg(blk + gi), comb);
+    for (int gi = MP_STEPS * 32 + lane; gi < g16; gi += 32) gsum2[gi] = group_sums(__ldg(blk + gi), comb);
     __syncwarp();
-    // row sums: groups [g0, g1) of the lane's row, in order
-    const int g0 = Xc.off & 0xFFF;
-    const int gn = __shfl_down_sync(0xFFFFFFFFu, g0, 1);
-    const int g1 = lane < 31 ? gn : Xc.groups;
+    // row sums: half-groups [h0, h1) of the lane's row, in order
+    const int h0 = Xc.off & 0xFFF;
+    const int hn = __shfl_down_sync(0xFFFFFFFFu, h0, 1);
+    const int h1 = lane < 31 ? hn : Xc.groups;
     float acc = 0.f;
 #pragma unroll 4
-    for (int gi = g0; gi < g1; ++gi) acc += gsum[gi];
+    for (int hi = h0; hi < h1; ++hi) acc += gsum[hi];
     __syncwarp();
-    if (valid) edges += (unsigned)(8 * (g1 - g0) - (Xc.off >> 12));
+    if (valid) edges += (unsigned)(4 * (h1 - h0) - (Xc.off >> 12));
     if (MODE == 0) {
       if (valid) {
         const bool target = Xc.st == S_SUS && !(P->sterilizing && Xc.im);

@@ -68,8 +68,8 @@ def message_pass_roofline(n_agents: int = 10_000_000, warm_days: int = 60, reps:
     med = ms[len(ms) // 2]
     alg = 2 * edges + 11 * n_agents
     out = {"kernel": "k_msg_pass<0>: message pass alone (tile-packed 16-bit pre-joined "
-                     "messages, rows padded to 8-message groups, 16-byte register-prefetched "
-                     "loads, group-parallel fp32 sums + per-row group sum)",
+                     "messages, rows padded to 4-message half-groups, 16-byte register-prefetched "
+                     "loads, group-parallel fp32 half sums + per-row half-group sum)",
            "n_agents": n_agents, "day": sim.clock, "edges": edges, "ms_median": med,
            "ms_min": ms[0], "alg_bytes": alg, "achieved": alg / (med / 1e3) / 1e9,
            "unit": "GB/s", "l2_flushed_between_reps": bool(flush_l2)}
