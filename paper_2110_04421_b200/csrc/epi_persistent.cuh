@@ -102,6 +102,13 @@ constexpr int RUN_MAX_DAYS = 1 << 20;      // days per launch (no per-day state)
 // the agent warps work
 constexpr int RUN_MAX_AGENTS = 704;
 constexpr int RUN_MAX_THREADS = RUN_MAX_AGENTS + 32;
+// The block's out-rows (rout: each agent's random out-partners of the day)
+// live in dynamic shared memory for the whole run: the block writes them
+// itself (its own push items) and only it reads them, so the global table
+// is written on the last day only (for the per-day path).  Row stride 20
+// words: a quarter warp's 16-byte row reads hit distinct banks.
+constexpr int RUN_OUT_STRIDE = RT_SLOTS + 4;
+constexpr size_t RUN_DYN_SMEM = (size_t)RUN_MAX_AGENTS * RUN_OUT_STRIDE * sizeof(uint32_t);
 // loads of data written during the run: plain (coherent) global loads; the
 // grid barrier orders them after the writers' stores
 template <class T> __device__ __forceinline__ T LDM(const T* p) { return *p; }
@@ -128,6 +135,9 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_fused_run(RunArgs R, epi
   __shared__ uint16_t cn_s[RUN_MAX_THREADS / 32][32];
   __shared__ uint8_t own_s[RUN_MAX_THREADS / 32][32 * RT_SLOTS];
   __shared__ DayKeys dk[2];                // keys by day parity
+  __shared__ uint16_t hcode_s[2][RUN_MAX_AGENTS];   // the block's codes by day parity
+  extern __shared__ uint4 run_dyn_s[];
+  uint32_t* const out_s = (uint32_t*)run_dyn_s;    // [agent][RUN_OUT_STRIDE]
   load_msg_tables(T, R.mt);
   rec_init(racc[0]);
   rec_init(racc[1]);
@@ -161,7 +171,15 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_fused_run(RunArgs R, epi
       base = net.wp_base[w];
       if (m >= 2) p = LDM(R.wt[R.first_step & 1].pos_of + base + loc);
     }
+    hcode_s[R.first_step & 1][threadIdx.x] = cb;
+    const uint4* ro = (const uint4*)(R.wt[R.first_step & 1].rout + (size_t)b * RT_SLOTS);
+    uint4* os = (uint4*)(out_s + threadIdx.x * RUN_OUT_STRIDE);
+#pragma unroll
+    for (int q = 0; q < RT_SLOTS / 4; ++q) os[q] = LDM(ro + q);
   }
+  // household members inside the block's range are read from hcode_s
+  const int hl0 = (int)threadIdx.x - off;
+  const int nloc = (int)(bhi - blo);
   const bool works = w >= 0 && m >= 2;
   const int64_t start = b - off;
   const Radix rm = make_radix(works ? (uint32_t)m : 1u);
@@ -187,6 +205,7 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_fused_run(RunArgs R, epi
     uint16_t* codes_next = R.codes[par ^ 1];
     const WorkTables& W = R.wt[par];
     const WorkTables& Wn = R.wt[par ^ 1];
+    const uint16_t* hcs = hcode_s[par];
     unsigned edges = 0;
     double lam = 0.0;
     if (valid) {
@@ -194,14 +213,17 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_fused_run(RunArgs R, epi
       const uint4* ri = (const uint4*)(W.rin + (size_t)b * RT_SLOTS);
       const uint4 in0 = LDM(ri), in1 = LDM(ri + 1);
       if (!code_dead(cb)) {
-        const uint4* ro = (const uint4*)(W.rout + (size_t)b * RT_SLOTS);
+        const uint4* ro = (const uint4*)(out_s + threadIdx.x * RUN_OUT_STRIDE);
         const int nb = code_count(cb);
         const int nbe = nb < RT_SLOTS ? nb : RT_SLOTS;
-        const uint4 o0 = nbe > 0 ? LDM(ro) : make_uint4(self, self, self, self);
+        const uint4 o0 = nbe > 0 ? ro[0] : make_uint4(self, self, self, self);
+        auto hh_code = [&](int i) -> uint16_t {
+          return (unsigned)(hl0 + i) < (unsigned)nloc ? hcs[hl0 + i] : LDM(codes + start + i);
+        };
         uint16_t hc[HH];
 #pragma unroll
         for (int i = 0; i < HH; ++i)
-          hc[i] = (i < sz && start + i != b) ? LDM(codes + start + i) : (uint16_t)CODE_DEAD;
+          hc[i] = (i < sz && start + i != b) ? hh_code(i) : (uint16_t)CODE_DEAD;
         // the day's colleague shifts r_j (hashed while the previous barrier waited)
         uint32_t sh[DR];
 #pragma unroll
@@ -231,7 +253,7 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_fused_run(RunArgs R, epi
         for (int i = 0; i < HH; ++i) add_src(acc[0], edges, T.factor, hc[i]);
         for (int i = HH; i < sz; ++i) {
           if (start + i == b) continue;
-          add_src(acc[0], edges, T.factor, LDM(codes + start + i));
+          add_src(acc[0], edges, T.factor, hh_code(i));
         }
 #pragma unroll
         for (int j = 0; j < DR; ++j) {
@@ -242,7 +264,7 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_fused_run(RunArgs R, epi
 #pragma unroll
           for (int q = 0; q < 4; ++q) add_src(acc[2], edges, T.factor, co0[q]);
           for (int j0 = 4; j0 < nbe; j0 += 4) {
-            const uint4 o = LDM(ro + (j0 >> 2));
+            const uint4 o = ro[j0 >> 2];
             const uint32_t po[4] = {o.x, o.y, o.z, o.w};
             uint16_t co[4];
 #pragma unroll
@@ -274,6 +296,7 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_fused_run(RunArgs R, epi
       if (h.stage == S_DEAD) cn |= CODE_DEAD;
       else cn |= (uint16_t)(cnt_nx << 8);
       codes_next[b] = cn;
+      hcode_s[par ^ 1][threadIdx.x] = cn;
     }
     // tomorrow's push tables: the worker's position and its code there
     if (valid && works) {
@@ -308,7 +331,8 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_fused_run(RunArgs R, epi
         const int j = k - excl_s[warp][l];
         const uint32_t src = (uint32_t)(wbase_agent + l);
         const uint32_t y = walk_fwd(src, D.rk_next[j], R.dn);
-        Wn.rout[(size_t)src * RT_SLOTS + j] = y;
+        out_s[(warp * 32 + l) * RUN_OUT_STRIDE + j] = y;
+        if (d + 1 == R.n_days) Wn.rout[(size_t)src * RT_SLOTS + j] = y;
         if (y != src) Wn.rin[(size_t)y * RT_SLOTS + j] = cn_s[warp][l] | CODE_PRESENT;
       }
     }
