@@ -84,6 +84,9 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
   __shared__ int wsum_s[RUN_MAX_THREADS / 32];
   __shared__ long long plan_s[2];
   __shared__ int off_s;
+  __shared__ uint16_t hcode_s[2][RUN_MAX_AGENTS];   // the block's codes by day parity
+  extern __shared__ uint4 run_dyn_s[];
+  uint32_t* const out_s = (uint32_t*)run_dyn_s;    // out-rows [agent][RUN_OUT_STRIDE] (as k_fused_run)
   load_msg_tables(T, R.mt);
   rec_init(racc[0]);
   rec_init(racc[1]);
@@ -124,7 +127,14 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
       base = net.wp_base[w];
       if (m >= 2) p = LDM(R.wt[R.first_step & 1].pos_of + base + loc);
     }
+    hcode_s[R.first_step & 1][threadIdx.x] = cb;
+    const uint4* ro = (const uint4*)(R.wt[R.first_step & 1].rout + (size_t)b * RT_SLOTS);
+    uint4* os = (uint4*)(out_s + threadIdx.x * RUN_OUT_STRIDE);
+#pragma unroll
+    for (int q = 0; q < RT_SLOTS / 4; ++q) os[q] = LDM(ro + q);
   }
+  const int hl0 = (int)threadIdx.x - off;  // household members inside the block: from hcode_s
+  const int nloc = (int)(bhi - blo);
   const bool works = w >= 0 && m >= 2;
   const int64_t start = b - off;
   unsigned bar = 0;                        // barriers passed
@@ -179,14 +189,18 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
         const uint4* ri = (const uint4*)(W.rin + (size_t)b * RT_SLOTS);
         const uint4 in0 = LDM(ri), in1 = LDM(ri + 1);
         if (!code_dead(cb)) {
-          const uint4* ro = (const uint4*)(W.rout + (size_t)b * RT_SLOTS);
+          const uint4* ro = (const uint4*)(out_s + threadIdx.x * RUN_OUT_STRIDE);
           const int nb = code_count(cb);
           const int nbe = nb < RT_SLOTS ? nb : RT_SLOTS;
-          const uint4 o0 = nbe > 0 ? LDM(ro) : make_uint4(self, self, self, self);
+          const uint4 o0 = nbe > 0 ? ro[0] : make_uint4(self, self, self, self);
+          const uint16_t* hcs = hcode_s[par];
+          auto hh_code = [&](int i) -> uint16_t {
+            return (unsigned)(hl0 + i) < (unsigned)nloc ? hcs[hl0 + i] : LDM(codes + start + i);
+          };
           uint16_t hc[HH];
 #pragma unroll
           for (int i = 0; i < HH; ++i)
-            hc[i] = (i < sz && start + i != b) ? LDM(codes + start + i) : (uint16_t)CODE_DEAD;
+            hc[i] = (i < sz && start + i != b) ? hh_code(i) : (uint16_t)CODE_DEAD;
           uint32_t sh[DR];
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
@@ -213,7 +227,7 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
           for (int i = 0; i < HH; ++i) add_src(acc[0], edges, T.factor, hc[i]);
           for (int i = HH; i < sz; ++i) {
             if (start + i == b) continue;
-            add_src(acc[0], edges, T.factor, LDM(codes + start + i));
+            add_src(acc[0], edges, T.factor, hh_code(i));
           }
 #pragma unroll
           for (int j = 0; j < DR; ++j) {
@@ -224,7 +238,7 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
 #pragma unroll
             for (int q = 0; q < 4; ++q) add_src(acc[2], edges, T.factor, co0[q]);
             for (int j0 = 4; j0 < nbe; j0 += 4) {
-              const uint4 o = LDM(ro + (j0 >> 2));
+              const uint4 o = ro[j0 >> 2];
               const uint32_t po[4] = {o.x, o.y, o.z, o.w};
               uint16_t co[4];
 #pragma unroll
@@ -297,6 +311,7 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
         if (stage == S_DEAD) cn |= CODE_DEAD;
         else cn |= (uint16_t)(random_count(net, D.rcount_next, b) << 8);
         codes_next[b] = cn;
+        hcode_s[par ^ 1][threadIdx.x] = cn;
       }
       if (valid && works) {
         const uint32_t q = walk_inv((uint32_t)loc, work_keys(D.wperm_next, w), make_radix((uint32_t)m));
@@ -328,7 +343,8 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
         const int j = k - excl_s[warp][l];
         const uint32_t src = (uint32_t)(wbase_agent + l);
         const uint32_t y = walk_fwd(src, D.rk_next[j], R.dn);
-        Wn.rout[(size_t)src * RT_SLOTS + j] = y;
+        out_s[(warp * 32 + l) * RUN_OUT_STRIDE + j] = y;
+        if (d + 1 == R.n_days) Wn.rout[(size_t)src * RT_SLOTS + j] = y;
         if (y != src) Wn.rin[(size_t)y * RT_SLOTS + j] = cn_s[warp][l] | CODE_PRESENT;
       }
       cb = cn;
