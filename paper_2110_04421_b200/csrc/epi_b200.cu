@@ -1443,9 +1443,9 @@ static bool persistent_iv_ok(epi_ctx* c, int32_t mode, int32_t precision) {
     return false;
   static int per_sm = -1;
   if (per_sm < 0 &&
-      (cudaFuncSetAttribute(k_iv_run, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RUN_DYN_SMEM) !=
+      (cudaFuncSetAttribute(k_iv_run, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)IV_DYN_SMEM) !=
            cudaSuccess ||
-       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_iv_run, RUN_MAX_THREADS, RUN_DYN_SMEM) !=
+       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_iv_run, RUN_MAX_THREADS, IV_DYN_SMEM) !=
            cudaSuccess))
     per_sm = 0;
   return per_sm >= 1 && run_threads(c->n) <= RUN_MAX_AGENTS;
@@ -1499,7 +1499,7 @@ static int launch_iv_run(epi_ctx* c, const epi_state* st, int32_t first, int32_t
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)sm_count());
   cfg.blockDim = dim3((unsigned)run_threads(c->n) + 32);
-  cfg.dynamicSmemBytes = RUN_DYN_SMEM;
+  cfg.dynamicSmemBytes = IV_DYN_SMEM;
   cfg.stream = s;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeCooperative;

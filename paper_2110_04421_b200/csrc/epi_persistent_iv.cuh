@@ -50,6 +50,8 @@ struct IvRunArgs {
 };
 
 constexpr int IV_HIST = NUM_BUCKETS + 1;
+constexpr int IV_HW_WORDS = 2 * (RUN_MAX_THREADS / 32) * NUM_BUCKETS;
+constexpr size_t IV_DYN_SMEM = RUN_DYN_SMEM + IV_HW_WORDS * sizeof(unsigned);
 
 // Phase 4b of day t - 1 for agent b, applied at the start of day t:
 // notified (marked by a notifier's contact regeneration) and eligible then
@@ -80,18 +82,18 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
   __shared__ int excl_s[RUN_MAX_THREADS / 32][32];
   __shared__ uint16_t cn_s[RUN_MAX_THREADS / 32][32];
   __shared__ uint8_t own_s[RUN_MAX_THREADS / 32][32 * RT_SLOTS];
-  __shared__ unsigned h_s[NUM_BUCKETS];
-  __shared__ int wsum_s[RUN_MAX_THREADS / 32];
-  __shared__ long long plan_s[2];
-  __shared__ int off_s;
   __shared__ uint16_t hcode_s[2][RUN_MAX_AGENTS];   // the block's codes by day parity
   extern __shared__ uint4 run_dyn_s[];
   uint32_t* const out_s = (uint32_t*)run_dyn_s;    // out-rows [agent][RUN_OUT_STRIDE] (as k_fused_run)
+  // per-warp eligibility histograms by day parity [2][warps][NUM_BUCKETS]:
+  // the block's histogram is their sum, and a warp's rank offset in the cut
+  // bucket is the sum over the warps before it (no block barrier for either)
+  unsigned* const hw_s = (unsigned*)(out_s + (size_t)RUN_MAX_AGENTS * RUN_OUT_STRIDE);
   load_msg_tables(T, R.mt);
   rec_init(racc[0]);
   rec_init(racc[1]);
   for (int m = threadIdx.x; m < 256; m += blockDim.x) wrad[m] = R.wrad[m];
-  for (int i = threadIdx.x; i < NUM_BUCKETS; i += blockDim.x) h_s[i] = 0u;
+  for (int i = threadIdx.x; i < IV_HW_WORDS; i += blockDim.x) hw_s[i] = 0u;
   const int warp = threadIdx.x >> 5, lane = lane_id();
   const int nwa = (int)(blockDim.x >> 5) - 1;
   const bool service = warp == nwa;
@@ -160,16 +162,21 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
     uint16_t* codes_next = R.codes[par ^ 1];
     const WorkTables& W = R.wt[par];
     const WorkTables& Wn = R.wt[par ^ 1];
+    const int first_day = t - R.den_lookback > 0 ? t - R.den_lookback : 0;
+    const int n_back = t - first_day;
+    const bool phase_b = R.den && R.tests && n_back > 0;
+    const bool bar1 = phase_b || R.vax;    // a grid barrier after phase A
     if (R.den && d > 0) {
       // yesterday's exposure notifications (phase 4b of t - 1): the marks of
       // every block are complete since the barrier; counted in yesterday's
-      // record, which the service warp flushes after this
+      // record, which the service warp flushes after barrier 1 (or after this)
       if (!service) den_follow_up(R, b, valid, den_ok, den_pref, t, racc[(d - 1) & 1]);
-      __syncthreads();
+      if (!bar1) __syncthreads();
     }
     // ---- phase A ----------------------------------------------------------
     if (service) {
-      if (d > 0) rec_flush_warp(racc[(d - 1) & 1], R.records + (size_t)(d - 1) * EPI_REC_LEN, t - 1, nwa, lane);
+      if (d > 0 && !bar1)
+        rec_flush_warp(racc[(d - 1) & 1], R.records + (size_t)(d - 1) * EPI_REC_LEN, t - 1, nwa, lane);
       if (d + 1 < R.n_days) {
         day_keys(dk[(d + 1) & 1], R.seed, t + 1, lane);
         __syncwarp();
@@ -284,7 +291,7 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
       // the histogram is complete at the first barrier of the day
       if (R.vax) {
         unsigned active = 0;
-        if (valid) bk = iv_elig_agent(A, b, h_s, active);
+        if (valid) bk = iv_elig_agent(A, b, hw_s + ((size_t)par * (RUN_MAX_THREADS / 32) + warp) * NUM_BUCKETS, active);
         rec_add(rc, EPI_REC_ACTIVE, active);
         const unsigned wa = __reduce_add_sync(0xFFFFFFFFu, active);
         if (lane == 0 && wa) atomicAdd(&hist[NUM_BUCKETS], (unsigned long long)wa);
@@ -293,12 +300,16 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
     if (R.vax) {
       // the block's histogram to the day's histogram and to its tile row
       __syncthreads();
+      const unsigned* hw = hw_s + (size_t)par * (RUN_MAX_THREADS / 32) * NUM_BUCKETS;
+      unsigned* hw_next = hw_s + (size_t)(par ^ 1) * (RUN_MAX_THREADS / 32) * NUM_BUCKETS;
       for (int i = threadIdx.x; i < NUM_BUCKETS; i += blockDim.x) {
-        const unsigned v = h_s[i];
+        unsigned v = 0;
+        for (int ww = 0; ww < nwa; ++ww) v += hw[ww * NUM_BUCKETS + i];
         R.tile_hist[(size_t)blockIdx.x * NUM_BUCKETS + i] = v;
         if (v) atomicAdd(&hist[i], (unsigned long long)v);
-        h_s[i] = 0u;                        // next used in tomorrow's phase A
       }
+      // tomorrow's rows start empty (yesterday's doses, their last reader, are done)
+      for (int i = threadIdx.x; i < (RUN_MAX_THREADS / 32) * NUM_BUCKETS; i += blockDim.x) hw_next[i] = 0u;
     }
     // tomorrow's code and push tables: final once phase C's dropout has run
     // (a dose only turns code-0 susceptibles into code-0 vaccinated agents)
@@ -350,11 +361,12 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
       cb = cn;
     };
     // ---- phase B: DEN regeneration ----------------------------------------
-    const int first_day = t - R.den_lookback > 0 ? t - R.den_lookback : 0;
-    const int n_back = t - first_day;
-    const bool phase_b = R.den && R.tests && n_back > 0;
     // barrier 1: the notifier list and the eligibility histogram are complete
-    if (phase_b || R.vax) grid_barrier(R.barrier, ++bar * gridDim.x);
+    if (bar1) {
+      grid_barrier(R.barrier, ++bar * gridDim.x);
+      if (service && d > 0)               // yesterday's record (incl. this morning's follow-ups)
+        rec_flush_warp(racc[(d - 1) & 1], R.records + (size_t)(d - 1) * EPI_REC_LEN, t - 1, nwa, lane);
+    }
     if (phase_b) {
       if (!service) {
         const int64_t items = (int64_t)LDM(R.den_count + par) * n_back;
@@ -374,73 +386,59 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
     // ---- phase C+D: the vaccination plan (every block derives it from the
     // complete histogram), follow-ups / dropout / immunity, doses in id order,
     // tomorrow's codes and tables ---------------------------------------------
-    long long cut = -1, rem = 0;
-    if (R.vax) {
-      if (warp == 0) {
-        // the plan (k_vax_plan) with one warp: lane l holds buckets 2l, 2l+1;
-        // the cut bucket is the first whose inclusive prefix reaches the budget
-        const epi_params* __restrict__ P = A.P;
-        const long long c0 = lane < NUM_BUCKETS / 2 ? (long long)LDM(hist + 2 * lane) : 0;
-        const long long c1 = lane < NUM_BUCKETS / 2 ? (long long)LDM(hist + 2 * lane + 1) : 0;
-        int open = *R.vax_open;
-        if (!open && (double)LDM(hist + NUM_BUCKETS) >= P->start_trigger_count) open = 1;
-        long long c = -1, r = 0, doses = -1;
-        const long long budget = P->dose_budget;
-        if (open && budget > 0) {
-          const long long pair = c0 + c1;
-          long long S = pair;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const long long v = __shfl_up_sync(0xFFFFFFFFu, S, o);
-            if (lane >= o) S += v;
-          }
-          const unsigned ball = __ballot_sync(0xFFFFFFFFu, S >= budget);
-          if (ball) {
-            const int L = __ffs(ball) - 1;
-            const long long E = __shfl_sync(0xFFFFFFFFu, S - pair, L);
-            const long long cA = __shfl_sync(0xFFFFFFFFu, c0, L);
-            if (E + cA >= budget) { c = 2 * L; r = budget - E; }
-            else { c = 2 * L + 1; r = budget - E - cA; }
-            doses = budget;
-          } else {
-            c = NUM_BUCKETS;                // everyone eligible gets a dose
-            doses = __shfl_sync(0xFFFFFFFFu, S, 31);
-          }
-        }
-        if (lane == 0) {
-          if (blockIdx.x == 0) {
-            *R.vax_open = open;           // the latch only opens: a late reader derives the same
-            if (doses > 0) rc.v[0][EPI_REC_DOSES] += (unsigned)doses;
-          }
-          plan_s[0] = c;
-          plan_s[1] = r;
-          off_s = 0;
-        }
-      }
-      __syncthreads();
-      cut = plan_s[0];
-      rem = plan_s[1];
-      if (cut >= 0 && cut < NUM_BUCKETS) {
-        unsigned part = 0;
-        for (int bb = threadIdx.x; bb < (int)blockIdx.x; bb += blockDim.x)
-          part += LDM(R.tile_hist + (size_t)bb * NUM_BUCKETS + cut);
-        part = __reduce_add_sync(0xFFFFFFFFu, part);
-        if (lane == 0 && part) atomicAdd(&off_s, (int)part);
-      }
-    }
-    if (R.post && !service && valid) iv_post_rest_agent(A, b, false);   // dropout, due immunity checks
+    // dropout and due immunity checks first: independent of the plan
+    if (R.post && !service && valid) iv_post_rest_agent(A, b, false);
     if (blockIdx.x == 0 && threadIdx.x == 0 && R.den_count) R.den_count[par ^ 1] = 0;   // tomorrow's list
     if (R.vax) {
-      // cut-bucket rank of each agent in id order: warp ballots + warp offsets
+      // the plan (k_vax_plan), derived by every warp from the complete
+      // histogram (no block barrier): lane l holds buckets 2l, 2l+1; the cut
+      // bucket is the first whose inclusive prefix reaches the budget
+      const epi_params* __restrict__ P = A.P;
+      const long long c0 = lane < NUM_BUCKETS / 2 ? (long long)LDM(hist + 2 * lane) : 0;
+      const long long c1 = lane < NUM_BUCKETS / 2 ? (long long)LDM(hist + 2 * lane + 1) : 0;
+      int open = *R.vax_open;
+      if (!open && (double)LDM(hist + NUM_BUCKETS) >= P->start_trigger_count) open = 1;
+      long long cut = -1, rem = 0, doses = -1;
+      const long long budget = P->dose_budget;
+      if (open && budget > 0) {
+        const long long pair = c0 + c1;
+        long long S = pair;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const long long v = __shfl_up_sync(0xFFFFFFFFu, S, o);
+          if (lane >= o) S += v;
+        }
+        const unsigned ball = __ballot_sync(0xFFFFFFFFu, S >= budget);
+        if (ball) {
+          const int L = __ffs(ball) - 1;
+          const long long E = __shfl_sync(0xFFFFFFFFu, S - pair, L);
+          const long long cA = __shfl_sync(0xFFFFFFFFu, c0, L);
+          if (E + cA >= budget) { cut = 2 * L; rem = budget - E; }
+          else { cut = 2 * L + 1; rem = budget - E - cA; }
+          doses = budget;
+        } else {
+          cut = NUM_BUCKETS;                // everyone eligible gets a dose
+          doses = __shfl_sync(0xFFFFFFFFu, S, 31);
+        }
+      }
+      if (blockIdx.x == 0 && warp == 0 && lane == 0) {
+        *R.vax_open = open;                 // the latch only opens: a late reader derives the same
+        if (doses > 0) rc.v[0][EPI_REC_DOSES] += (unsigned)doses;
+      }
+      // cut-bucket rank of each agent in id order: the blocks before (their
+      // tile rows), the warps before (their histogram rows), the lanes before
       const bool in_cut = cut >= 0 && cut < NUM_BUCKETS && bk == (uint8_t)cut;
-      const unsigned ball = __ballot_sync(0xFFFFFFFFu, in_cut);
-      if (lane == 0) wsum_s[warp] = __popc(ball);
-      __syncthreads();
-      int rank = off_s + __popc(ball & ((1u << lane) - 1u));
-      for (int ww = 0; ww < warp; ++ww) rank += wsum_s[ww];
-      if (valid && cut >= 0 && bk != NO_BUCKET && ((long long)bk < cut || (in_cut && (long long)rank < rem)))
-        give_dose(A, b, bk);
-      if (blockIdx.x == 0)                // tomorrow's histogram starts empty
+      if (cut >= 0 && cut < NUM_BUCKETS && !service) {
+        const unsigned ball = __ballot_sync(0xFFFFFFFFu, in_cut);
+        unsigned part = 0;
+        for (int bb = lane; bb < (int)blockIdx.x; bb += 32) part += LDM(R.tile_hist + (size_t)bb * NUM_BUCKETS + cut);
+        if (lane < warp) part += hw_s[((size_t)par * (RUN_MAX_THREADS / 32) + lane) * NUM_BUCKETS + cut];
+        const long long rank = (long long)__reduce_add_sync(0xFFFFFFFFu, part) + __popc(ball & ((1u << lane) - 1u));
+        if (valid && bk != NO_BUCKET && ((long long)bk < cut || (in_cut && rank < rem))) give_dose(A, b, bk);
+      } else if (valid && cut >= 0 && bk != NO_BUCKET) {
+        give_dose(A, b, bk);                // cut == NUM_BUCKETS: every eligible agent
+      }
+      if (blockIdx.x == 0)                  // tomorrow's histogram starts empty
         for (int i = threadIdx.x; i < IV_HIST; i += blockDim.x) R.hist[(size_t)(par ^ 1) * IV_HIST + i] = 0;
     }
     if (!service) next_day();
