@@ -224,7 +224,8 @@ struct epi_ctx {
   int day_blocks_per_sm = 16;        // k_fused_step grid cap (concurrent replicas: 1)
   unsigned* iv_tile_hist = nullptr;  // [chunks][NUM_BUCKETS]
   unsigned long long* iv_hist = nullptr;   // [2][NUM_BUCKETS] eligibility histogram by day parity
-  unsigned long long* ivr_hist = nullptr;  // k_iv_run: [2][NUM_BUCKETS + 1] (+ active count)
+  unsigned long long* ivr_hist = nullptr;  // k_iv_run: [3][NUM_BUCKETS + 1] (+ active count)
+  unsigned* ivr_tile_hist = nullptr;       // k_iv_run: [2][SMs][NUM_BUCKETS]
   unsigned* run_barrier = nullptr;   // arrival counter of k_fused_run's grid barrier
   LamProbe probe{};                  // debug hazard export (epi_set_lambda_probe)
   // days of a fused run without push tables (partitioned ranks, populations
@@ -481,6 +482,7 @@ int epi_destroy(epi_ctx* c) {
   cudaFree(c->iv_tile_hist);
   cudaFree(c->iv_hist);
   cudaFree(c->ivr_hist);
+  cudaFree(c->ivr_tile_hist);
   for (auto* p : c->ntab_dev) cudaFree(p);
   cudaFree(c->wt_host[0].member_at_pos);
   cudaFree(c->wt_host[1].member_at_pos);
@@ -1456,17 +1458,12 @@ static int launch_iv_run(epi_ctx* c, const epi_state* st, int32_t first, int32_t
   const epi_params& p = c->host;
   if (p.vaccination_enabled && !vax_open) return fail(EPI_EARG, "vaccination enabled but no vax_open latch given");
   int rc = 0;
-  if (!c->ivr_hist) rc = dalloc(&c->ivr_hist, (size_t)2 * IV_HIST);
-  if (!rc && !c->iv_tile_hist) {
-    int64_t chunk;
-    int blocks;
-    iv_chunks(c->n, &chunk, &blocks);
-    rc = dalloc(&c->iv_tile_hist, (size_t)(blocks > sm_count() ? blocks : sm_count()) * NUM_BUCKETS);
-  }
+  if (!c->ivr_hist) rc = dalloc(&c->ivr_hist, (size_t)3 * IV_HIST);
+  if (!rc && !c->ivr_tile_hist) rc = dalloc(&c->ivr_tile_hist, (size_t)2 * sm_count() * NUM_BUCKETS);
   if (rc) return rc;
   if (!c->run_barrier) CK(cudaMalloc((void**)&c->run_barrier, sizeof(unsigned)));
   CK(cudaMemsetAsync(c->run_barrier, 0, sizeof(unsigned), s));
-  CK(cudaMemsetAsync(c->ivr_hist, 0, (size_t)2 * IV_HIST * sizeof(unsigned long long), s));
+  CK(cudaMemsetAsync(c->ivr_hist, 0, (size_t)3 * IV_HIST * sizeof(unsigned long long), s));
   IvRunArgs R{};
   R.A0 = make_args(c, st, first, seed, nullptr, nullptr, true);
   R.seed = seed;
@@ -1484,7 +1481,7 @@ static int launch_iv_run(epi_ctx* c, const epi_state* st, int32_t first, int32_t
   R.barrier = c->run_barrier;
   R.bucket = c->bucket;
   R.hist = c->ivr_hist;
-  R.tile_hist = c->iv_tile_hist;
+  R.tile_hist = c->ivr_tile_hist;
   R.vax_open = vax_open;
   const bool listed = p.den_enabled && p.testing_enabled && c->den_list != nullptr;
   R.den_list = listed ? c->den_list : nullptr;

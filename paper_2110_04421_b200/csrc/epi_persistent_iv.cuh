@@ -3,22 +3,20 @@
 // launch, like k_fused_run for the days without interventions.  One block
 // per SM, one thread per agent for the whole run, a service warp; the day's
 // phases are separated by grid barriers instead of kernel boundaries:
-//   A  gather + transmission/progression + testing (k_fused_step + tests)
-//        | barrier (the notifier list is complete)            [DEN]
+//   0  the DEN follow-ups of yesterday's notifications (engine.py:244-262)
+//   A  gather + transmission/progression + testing (k_fused_step + tests),
+//      the vaccination eligibility (per-warp histograms -> the day's
+//      histogram), dropout and due immunity checks, death days, tomorrow's
+//      codes and push tables
+//        | barrier 1 (notifier list, histogram, codes complete) [DEN or vaccination]
 //   B  DEN regeneration: one warp per (notifier, past day) (k_den_regen)
-//        | barrier (the notifications are complete)          [DEN]
-//   C  DEN follow-ups, dropout, immunity checks, eligibility buckets and the
-//      chunk histograms (k_iv_post_chunks); the active count into the day's
-//      histogram row
-//        | barrier (the day's histogram is complete)         [vaccination]
-//   D  vaccination plan per block + doses in id order, death days, record,
-//      next codes, tomorrow's push tables (k_finish_iv)
-//        | barrier (end of day)
+//   C  vaccination plan (every warp derives it) + doses in id order, record
+//        | barrier (end of day: the DEN marks are complete)
 // The agent's static network data, own code and workplace position stay in
-// registers; its state is reloaded at the start of each day (phases B-D
-// change it through the shared per-phase functions).  The same per-agent
-// functions in the same order as the per-phase kernels: bitwise the same run
-// (tests/test_gpu_persistent.py).
+// registers; its state is reloaded at the start of each day (the later
+// phases change it through the shared per-phase functions).  The same
+// per-agent functions in the same order as the per-phase kernels: bitwise
+// the same run (tests/test_gpu_persistent.py).
 #pragma once
 
 #include "epi_persistent.cuh"
@@ -38,8 +36,8 @@ struct IvRunArgs {
   Radix dn;
   unsigned* barrier;
   uint8_t* bucket;
-  unsigned long long* hist;       // [2][NUM_BUCKETS + 1] by day parity (+ active count)
-  unsigned* tile_hist;            // [blocks][NUM_BUCKETS]
+  unsigned long long* hist;       // [3][NUM_BUCKETS + 1] by run day mod 3 (+ active count), zeroed
+  unsigned* tile_hist;            // [2][blocks][NUM_BUCKETS] by run day parity
   int32_t* vax_open;
   int32_t* den_list;              // [2][den_stride] by day parity
   int* den_count;                 // [2] by day parity
@@ -50,7 +48,8 @@ struct IvRunArgs {
 };
 
 constexpr int IV_HIST = NUM_BUCKETS + 1;
-constexpr int IV_HW_WORDS = 2 * (RUN_MAX_THREADS / 32) * NUM_BUCKETS;
+constexpr int IV_HW_ROW = NUM_BUCKETS + 1;           // + the warp's active count
+constexpr int IV_HW_WORDS = 2 * (RUN_MAX_THREADS / 32) * IV_HW_ROW;
 constexpr size_t IV_DYN_SMEM = RUN_DYN_SMEM + IV_HW_WORDS * sizeof(unsigned);
 
 // Phase 4b of day t - 1 for agent b, applied at the start of day t:
@@ -74,9 +73,11 @@ __device__ __forceinline__ void den_follow_up(const IvRunArgs& R, int64_t b, boo
 __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_net net) {
   constexpr int HH = 8, DR = 8;
   __shared__ MsgTables T;
-  __shared__ RecAcc racc[2];
-  __shared__ DayKeys dk[2];
-  __shared__ StepArgs As[2];
+  // record rows, keys and step arguments by run day mod 3: without DEN a day
+  // has one grid barrier, and a warp still dosing day d must not see day d + 2's
+  __shared__ RecAcc racc[3];
+  __shared__ DayKeys dk[3];
+  __shared__ StepArgs As[3];
   __shared__ Radix wrad[256];
   __shared__ PermKeys rk_w[RUN_MAX_THREADS / 32][RT_SLOTS];
   __shared__ int excl_s[RUN_MAX_THREADS / 32][32];
@@ -85,13 +86,14 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
   __shared__ uint16_t hcode_s[2][RUN_MAX_AGENTS];   // the block's codes by day parity
   extern __shared__ uint4 run_dyn_s[];
   uint32_t* const out_s = (uint32_t*)run_dyn_s;    // out-rows [agent][RUN_OUT_STRIDE] (as k_fused_run)
-  // per-warp eligibility histograms by day parity [2][warps][NUM_BUCKETS]:
+  // per-warp eligibility histograms by day parity [2][warps][NUM_BUCKETS + 1]:
   // the block's histogram is their sum, and a warp's rank offset in the cut
   // bucket is the sum over the warps before it (no block barrier for either)
   unsigned* const hw_s = (unsigned*)(out_s + (size_t)RUN_MAX_AGENTS * RUN_OUT_STRIDE);
   load_msg_tables(T, R.mt);
   rec_init(racc[0]);
   rec_init(racc[1]);
+  rec_init(racc[2]);
   for (int m = threadIdx.x; m < 256; m += blockDim.x) wrad[m] = R.wrad[m];
   for (int i = threadIdx.x; i < IV_HW_WORDS; i += blockDim.x) hw_s[i] = 0u;
   const int warp = threadIdx.x >> 5, lane = lane_id();
@@ -151,13 +153,15 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
   for (int d = 0; d < R.n_days; ++d) {
     const int t = R.first_step + d;
     const int par = t & 1;
-    const DayKeys& D = dk[d & 1];
-    const StepArgs& A = As[d & 1];
-    RecAcc& rc = racc[d & 1];
+    const int d3 = d % 3, d3p = (d + 2) % 3, d3n = (d + 1) % 3;   // today, yesterday, tomorrow
+    const DayKeys& D = dk[d3];
+    const StepArgs& A = As[d3];
+    RecAcc& rc = racc[d3];
     int pend = -1;                         // the day's deferred transition scheduling
     int age = 0;
     uint8_t bk = NO_BUCKET;                // the agent's vaccination bucket of the day
-    unsigned long long* hist = R.hist + (size_t)par * IV_HIST;
+    unsigned long long* hist = R.hist + (size_t)d3 * IV_HIST;
+    unsigned* tile_hist = R.tile_hist + (size_t)(d & 1) * gridDim.x * NUM_BUCKETS;
     const uint16_t* codes = R.codes[par];
     uint16_t* codes_next = R.codes[par ^ 1];
     const WorkTables& W = R.wt[par];
@@ -166,24 +170,76 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
     const int n_back = t - first_day;
     const bool phase_b = R.den && R.tests && n_back > 0;
     const bool bar1 = phase_b || R.vax;    // a grid barrier after phase A
+    // tomorrow's code and push tables, at the end of phase A: final once the
+    // agent's dropout has run; the later phases (DEN marks, doses) do not
+    // change a code (a dose only turns code-0 susceptibles into code-0
+    // vaccinated agents), so they are complete at barrier 1 and the DEN
+    // regeneration after it overlaps nothing but the plan and the doses
+    auto next_day = [&]() {
+      uint16_t cn = 0;
+      if (valid) {
+        const int stage = st.stage[b];
+        if (R.died_at && stage == S_DEAD && R.died_at[b] == INT32_MAX) R.died_at[b] = t;
+        cn = source_code(A.P, stage, st.infected_at[b], st.quarantine_until[b], t + 1);
+        if (stage == S_DEAD) cn |= CODE_DEAD;
+        else cn |= (uint16_t)(random_count(net, D.rcount_next, b) << 8);
+        codes_next[b] = cn;
+        hcode_s[par ^ 1][threadIdx.x] = cn;
+      }
+      if (valid && works) {
+        const uint32_t q = walk_inv((uint32_t)loc, work_keys(D.wperm_next, w), make_radix((uint32_t)m));
+        Wn.wcode[base + q] = cn;
+        p = q;
+        if (d + 1 == R.n_days) {
+          Wn.pos_of[base + loc] = (uint8_t)q;
+          for (int j = loc; j < draws; j += m)
+            Wn.shift[(size_t)w * draws + j] = (uint8_t)work_shift(D.wshift_next, w, j, m);
+        }
+      }
+      int na = valid ? code_count(cn) : 0;
+      na = na < RT_SLOTS ? na : RT_SLOTS;
+      int incl = na;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+      const int excl = incl - na;
+      excl_s[warp][lane] = excl;
+      cn_s[warp][lane] = cn;
+      for (int i = 0; i < na; ++i) own_s[warp][excl + i] = (uint8_t)lane;
+      __syncwarp();
+      const int64_t wbase_agent = b - lane;
+      for (int k = lane; k < total; k += 32) {
+        const int l = own_s[warp][k];
+        const int j = k - excl_s[warp][l];
+        const uint32_t src = (uint32_t)(wbase_agent + l);
+        const uint32_t y = walk_fwd(src, D.rk_next[j], R.dn);
+        out_s[(warp * 32 + l) * RUN_OUT_STRIDE + j] = y;
+        if (d + 1 == R.n_days) Wn.rout[(size_t)src * RT_SLOTS + j] = y;
+        if (y != src) Wn.rin[(size_t)y * RT_SLOTS + j] = cn_s[warp][l] | CODE_PRESENT;
+      }
+      cb = cn;
+    };
     if (R.den && d > 0) {
       // yesterday's exposure notifications (phase 4b of t - 1): the marks of
       // every block are complete since the barrier; counted in yesterday's
       // record, which the service warp flushes after barrier 1 (or after this)
-      if (!service) den_follow_up(R, b, valid, den_ok, den_pref, t, racc[(d - 1) & 1]);
+      if (!service) den_follow_up(R, b, valid, den_ok, den_pref, t, racc[d3p]);
       if (!bar1) __syncthreads();
     }
     // ---- phase A ----------------------------------------------------------
     if (service) {
       if (d > 0 && !bar1)
-        rec_flush_warp(racc[(d - 1) & 1], R.records + (size_t)(d - 1) * EPI_REC_LEN, t - 1, nwa, lane);
+        rec_flush_warp(racc[d3p], R.records + (size_t)(d - 1) * EPI_REC_LEN, t - 1, nwa, lane);
       if (d + 1 < R.n_days) {
-        day_keys(dk[(d + 1) & 1], R.seed, t + 1, lane);
+        day_keys(dk[d3n], R.seed, t + 1, lane);
         __syncwarp();
         if (lane == 0) {
-          As[(d + 1) & 1] = R.A0;
-          As[(d + 1) & 1].K = dk[(d + 1) & 1].K;
-          As[(d + 1) & 1].step = t + 1;
+          As[d3n] = R.A0;
+          As[d3n].K = dk[d3n].K;
+          As[d3n].step = t + 1;
         }
       }
     } else {
@@ -291,81 +347,37 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
       // the histogram is complete at the first barrier of the day
       if (R.vax) {
         unsigned active = 0;
-        if (valid) bk = iv_elig_agent(A, b, hw_s + ((size_t)par * (RUN_MAX_THREADS / 32) + warp) * NUM_BUCKETS, active);
+        if (valid) bk = iv_elig_agent(A, b, hw_s + ((size_t)par * (RUN_MAX_THREADS / 32) + warp) * IV_HW_ROW, active);
         rec_add(rc, EPI_REC_ACTIVE, active);
         const unsigned wa = __reduce_add_sync(0xFFFFFFFFu, active);
-        if (lane == 0 && wa) atomicAdd(&hist[NUM_BUCKETS], (unsigned long long)wa);
+        if (lane == 0) hw_s[((size_t)par * (RUN_MAX_THREADS / 32) + warp) * IV_HW_ROW + NUM_BUCKETS] = wa;
       }
+      // dropout and due immunity checks (independent of the plan), then
+      // tomorrow's code and push tables
+      if (R.post && valid) iv_post_rest_agent(A, b, false);
+      next_day();
     }
     if (R.vax) {
       // the block's histogram to the day's histogram and to its tile row
       __syncthreads();
-      const unsigned* hw = hw_s + (size_t)par * (RUN_MAX_THREADS / 32) * NUM_BUCKETS;
-      unsigned* hw_next = hw_s + (size_t)(par ^ 1) * (RUN_MAX_THREADS / 32) * NUM_BUCKETS;
-      for (int i = threadIdx.x; i < NUM_BUCKETS; i += blockDim.x) {
+      // (and the block's active count: one atomic per block)
+      const unsigned* hw = hw_s + (size_t)par * (RUN_MAX_THREADS / 32) * IV_HW_ROW;
+      unsigned* hw_next = hw_s + (size_t)(par ^ 1) * (RUN_MAX_THREADS / 32) * IV_HW_ROW;
+      for (int i = threadIdx.x; i < IV_HW_ROW; i += blockDim.x) {
         unsigned v = 0;
-        for (int ww = 0; ww < nwa; ++ww) v += hw[ww * NUM_BUCKETS + i];
-        R.tile_hist[(size_t)blockIdx.x * NUM_BUCKETS + i] = v;
+        for (int ww = 0; ww < nwa; ++ww) v += hw[ww * IV_HW_ROW + i];
+        if (i < NUM_BUCKETS) tile_hist[(size_t)blockIdx.x * NUM_BUCKETS + i] = v;
         if (v) atomicAdd(&hist[i], (unsigned long long)v);
       }
       // tomorrow's rows start empty (yesterday's doses, their last reader, are done)
-      for (int i = threadIdx.x; i < (RUN_MAX_THREADS / 32) * NUM_BUCKETS; i += blockDim.x) hw_next[i] = 0u;
+      for (int i = threadIdx.x; i < (RUN_MAX_THREADS / 32) * IV_HW_ROW; i += blockDim.x) hw_next[i] = 0u;
     }
-    // tomorrow's code and push tables: final once phase C's dropout has run
-    // (a dose only turns code-0 susceptibles into code-0 vaccinated agents)
-    auto next_day = [&]() {
-      uint16_t cn = 0;
-      if (valid) {
-        const int stage = st.stage[b];
-        if (R.died_at && stage == S_DEAD && R.died_at[b] == INT32_MAX) R.died_at[b] = t;
-        cn = source_code(A.P, stage, st.infected_at[b], st.quarantine_until[b], t + 1);
-        if (stage == S_DEAD) cn |= CODE_DEAD;
-        else cn |= (uint16_t)(random_count(net, D.rcount_next, b) << 8);
-        codes_next[b] = cn;
-        hcode_s[par ^ 1][threadIdx.x] = cn;
-      }
-      if (valid && works) {
-        const uint32_t q = walk_inv((uint32_t)loc, work_keys(D.wperm_next, w), make_radix((uint32_t)m));
-        Wn.wcode[base + q] = cn;
-        p = q;
-        if (d + 1 == R.n_days) {
-          Wn.pos_of[base + loc] = (uint8_t)q;
-          for (int j = loc; j < draws; j += m)
-            Wn.shift[(size_t)w * draws + j] = (uint8_t)work_shift(D.wshift_next, w, j, m);
-        }
-      }
-      int na = valid ? code_count(cn) : 0;
-      na = na < RT_SLOTS ? na : RT_SLOTS;
-      int incl = na;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-        if (lane >= o) incl += v;
-      }
-      const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
-      const int excl = incl - na;
-      excl_s[warp][lane] = excl;
-      cn_s[warp][lane] = cn;
-      for (int i = 0; i < na; ++i) own_s[warp][excl + i] = (uint8_t)lane;
-      __syncwarp();
-      const int64_t wbase_agent = b - lane;
-      for (int k = lane; k < total; k += 32) {
-        const int l = own_s[warp][k];
-        const int j = k - excl_s[warp][l];
-        const uint32_t src = (uint32_t)(wbase_agent + l);
-        const uint32_t y = walk_fwd(src, D.rk_next[j], R.dn);
-        out_s[(warp * 32 + l) * RUN_OUT_STRIDE + j] = y;
-        if (d + 1 == R.n_days) Wn.rout[(size_t)src * RT_SLOTS + j] = y;
-        if (y != src) Wn.rin[(size_t)y * RT_SLOTS + j] = cn_s[warp][l] | CODE_PRESENT;
-      }
-      cb = cn;
-    };
     // ---- phase B: DEN regeneration ----------------------------------------
     // barrier 1: the notifier list and the eligibility histogram are complete
     if (bar1) {
       grid_barrier(R.barrier, ++bar * gridDim.x);
       if (service && d > 0)               // yesterday's record (incl. this morning's follow-ups)
-        rec_flush_warp(racc[(d - 1) & 1], R.records + (size_t)(d - 1) * EPI_REC_LEN, t - 1, nwa, lane);
+        rec_flush_warp(racc[d3p], R.records + (size_t)(d - 1) * EPI_REC_LEN, t - 1, nwa, lane);
     }
     if (phase_b) {
       if (!service) {
@@ -383,88 +395,95 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
       }
       // no barrier: nothing until tomorrow reads the marks (see den_ok)
     }
-    // ---- phase C+D: the vaccination plan (every block derives it from the
-    // complete histogram), follow-ups / dropout / immunity, doses in id order,
-    // tomorrow's codes and tables ---------------------------------------------
-    // dropout and due immunity checks first: independent of the plan
-    if (R.post && !service && valid) iv_post_rest_agent(A, b, false);
+    // ---- phase C: the vaccination plan (every warp derives it from the
+    // complete histogram) and the doses in id order -------------------------
     if (blockIdx.x == 0 && threadIdx.x == 0 && R.den_count) R.den_count[par ^ 1] = 0;   // tomorrow's list
-    if (R.vax) {
-      // the plan (k_vax_plan), derived by every warp from the complete
-      // histogram (no block barrier): lane l holds buckets 2l, 2l+1; the cut
-      // bucket is the first whose inclusive prefix reaches the budget
-      const epi_params* __restrict__ P = A.P;
-      const long long c0 = lane < NUM_BUCKETS / 2 ? (long long)LDM(hist + 2 * lane) : 0;
-      const long long c1 = lane < NUM_BUCKETS / 2 ? (long long)LDM(hist + 2 * lane + 1) : 0;
-      int open = *R.vax_open;
-      if (!open && (double)LDM(hist + NUM_BUCKETS) >= P->start_trigger_count) open = 1;
-      long long cut = -1, rem = 0, doses = -1;
-      const long long budget = P->dose_budget;
-      if (open && budget > 0) {
-        const long long pair = c0 + c1;
-        long long S = pair;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const long long v = __shfl_up_sync(0xFFFFFFFFu, S, o);
-          if (lane >= o) S += v;
+    // the vaccination plan (every warp derives it from the complete
+    // histogram, barrier 1) and the doses in id order; the day's record rows.
+    // Thread-local writes only: with DEN in the end barrier's window, else
+    // right after barrier 1
+    auto finish_day = [&]() {
+      if (R.vax) {
+        // the plan (k_vax_plan), derived by every warp from the complete
+        // histogram (no block barrier): lane l holds buckets 2l, 2l+1; the cut
+        // bucket is the first whose inclusive prefix reaches the budget
+        const epi_params* __restrict__ P = A.P;
+        const long long c0 = lane < NUM_BUCKETS / 2 ? (long long)LDM(hist + 2 * lane) : 0;
+        const long long c1 = lane < NUM_BUCKETS / 2 ? (long long)LDM(hist + 2 * lane + 1) : 0;
+        int open = *R.vax_open;
+        if (!open && (double)LDM(hist + NUM_BUCKETS) >= P->start_trigger_count) open = 1;
+        long long cut = -1, rem = 0, doses = -1;
+        const long long budget = P->dose_budget;
+        if (open && budget > 0) {
+          const long long pair = c0 + c1;
+          long long S = pair;
+  #pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const long long v = __shfl_up_sync(0xFFFFFFFFu, S, o);
+            if (lane >= o) S += v;
+          }
+          const unsigned ball = __ballot_sync(0xFFFFFFFFu, S >= budget);
+          if (ball) {
+            const int L = __ffs(ball) - 1;
+            const long long E = __shfl_sync(0xFFFFFFFFu, S - pair, L);
+            const long long cA = __shfl_sync(0xFFFFFFFFu, c0, L);
+            if (E + cA >= budget) { cut = 2 * L; rem = budget - E; }
+            else { cut = 2 * L + 1; rem = budget - E - cA; }
+            doses = budget;
+          } else {
+            cut = NUM_BUCKETS;                // everyone eligible gets a dose
+            doses = __shfl_sync(0xFFFFFFFFu, S, 31);
+          }
         }
-        const unsigned ball = __ballot_sync(0xFFFFFFFFu, S >= budget);
-        if (ball) {
-          const int L = __ffs(ball) - 1;
-          const long long E = __shfl_sync(0xFFFFFFFFu, S - pair, L);
-          const long long cA = __shfl_sync(0xFFFFFFFFu, c0, L);
-          if (E + cA >= budget) { cut = 2 * L; rem = budget - E; }
-          else { cut = 2 * L + 1; rem = budget - E - cA; }
-          doses = budget;
-        } else {
-          cut = NUM_BUCKETS;                // everyone eligible gets a dose
-          doses = __shfl_sync(0xFFFFFFFFu, S, 31);
+        if (blockIdx.x == 0 && warp == 0 && lane == 0) {
+          *R.vax_open = open;                 // the latch only opens: a late reader derives the same
+          if (doses > 0) rc.v[0][EPI_REC_DOSES] += (unsigned)doses;
+        }
+        // cut-bucket rank of each agent in id order: the blocks before (their
+        // tile rows), the warps before (their histogram rows), the lanes before
+        const bool in_cut = cut >= 0 && cut < NUM_BUCKETS && bk == (uint8_t)cut;
+        if (cut >= 0 && cut < NUM_BUCKETS && !service) {
+          const unsigned ball = __ballot_sync(0xFFFFFFFFu, in_cut);
+          unsigned part = 0;
+          for (int bb = lane; bb < (int)blockIdx.x; bb += 32) part += LDM(tile_hist + (size_t)bb * NUM_BUCKETS + cut);
+          if (lane < warp) part += hw_s[((size_t)par * (RUN_MAX_THREADS / 32) + lane) * IV_HW_ROW + cut];
+          const long long rank = (long long)__reduce_add_sync(0xFFFFFFFFu, part) + __popc(ball & ((1u << lane) - 1u));
+          if (valid && bk != NO_BUCKET && ((long long)bk < cut || (in_cut && rank < rem))) give_dose(A, b, bk);
+        } else if (valid && cut >= 0 && bk != NO_BUCKET) {
+          give_dose(A, b, bk);                // cut == NUM_BUCKETS: every eligible agent
         }
       }
-      if (blockIdx.x == 0 && warp == 0 && lane == 0) {
-        *R.vax_open = open;                 // the latch only opens: a late reader derives the same
-        if (doses > 0) rc.v[0][EPI_REC_DOSES] += (unsigned)doses;
+      {
+        int stage = 0;
+        int32_t inf = 0;
+        if (valid) {
+          stage = st.stage[b];
+          inf = st.infected_at[b];
+          if (!R.den) A.flags[b] = 0;       // (with DEN: cleared by tomorrow's follow-up)
+        }
+        rec_agent(rc, valid, stage, inf);
       }
-      // cut-bucket rank of each agent in id order: the blocks before (their
-      // tile rows), the warps before (their histogram rows), the lanes before
-      const bool in_cut = cut >= 0 && cut < NUM_BUCKETS && bk == (uint8_t)cut;
-      if (cut >= 0 && cut < NUM_BUCKETS && !service) {
-        const unsigned ball = __ballot_sync(0xFFFFFFFFu, in_cut);
-        unsigned part = 0;
-        for (int bb = lane; bb < (int)blockIdx.x; bb += 32) part += LDM(R.tile_hist + (size_t)bb * NUM_BUCKETS + cut);
-        if (lane < warp) part += hw_s[((size_t)par * (RUN_MAX_THREADS / 32) + lane) * NUM_BUCKETS + cut];
-        const long long rank = (long long)__reduce_add_sync(0xFFFFFFFFu, part) + __popc(ball & ((1u << lane) - 1u));
-        if (valid && bk != NO_BUCKET && ((long long)bk < cut || (in_cut && rank < rem))) give_dose(A, b, bk);
-      } else if (valid && cut >= 0 && bk != NO_BUCKET) {
-        give_dose(A, b, bk);                // cut == NUM_BUCKETS: every eligible agent
-      }
-      if (blockIdx.x == 0)                  // tomorrow's histogram starts empty
-        for (int i = threadIdx.x; i < IV_HIST; i += blockDim.x) R.hist[(size_t)(par ^ 1) * IV_HIST + i] = 0;
-    }
-    if (!service) next_day();
-    if (!service) {
-      int stage = 0;
-      int32_t inf = 0;
-      if (valid) {
-        stage = st.stage[b];
-        inf = st.infected_at[b];
-        if (!R.den) A.flags[b] = 0;       // (with DEN: cleared by tomorrow's follow-up)
-      }
-      rec_agent(rc, valid, stage, inf);
-    }
-    if (d + 1 < R.n_days) {
-      // end of day, split: tomorrow's shifts hashed between arrive and wait
+    };
+    if (R.vax && blockIdx.x == 0)           // the histogram of day d + 2 starts empty
+      for (int i = threadIdx.x; i < IV_HIST; i += blockDim.x) R.hist[(size_t)d3p * IV_HIST + i] = 0;
+    // end of day: a grid barrier when DEN marks were made today (tomorrow's
+    // follow-ups read them) or when there was no barrier 1 (tomorrow's codes)
+    const bool end_bar = d + 1 < R.n_days && (phase_b || !bar1);
+    if (end_bar) {
+      // end of day, split: the plan, the doses and tomorrow's shifts between
+      // arrive and wait
       __syncthreads();
       if (threadIdx.x == 0) {
         unsigned v;
         asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(v) : "l"(R.barrier) : "memory");
       }
+      if (!service) finish_day();
       if (pend >= 0) {                     // feeds tomorrow's transition check
         AgentHot hs{};
         hs.age = age;
         schedule_pending(A.P, st, A.K, t, A.tau_lut, b, pend, hs);
       }
-      if (works) shp = day_shifts(dk[(d + 1) & 1].wshift, w, m);
+      if (works) shp = day_shifts(dk[d3n].wshift, w, m);
       ++bar;
       if (threadIdx.x == 0) {
         unsigned v;
@@ -473,22 +492,26 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
         } while (v < bar * gridDim.x);
       }
       __syncthreads();
-    } else if (pend >= 0) {
-      AgentHot hs{};
-      hs.age = age;
-      schedule_pending(A.P, st, A.K, t, A.tau_lut, b, pend, hs);
+    } else {
+      if (!service) finish_day();
+      if (pend >= 0) {
+        AgentHot hs{};
+        hs.age = age;
+        schedule_pending(A.P, st, A.K, t, A.tau_lut, b, pend, hs);
+      }
+      if (d + 1 < R.n_days && works) shp = day_shifts(dk[d3n].wshift, w, m);
     }
   }
   if (R.den) {
     // the last day's notifications, once every block's marks are in
     grid_barrier(R.barrier, ++bar * gridDim.x);
     if (!service)
-      den_follow_up(R, b, valid, den_ok, den_pref, R.first_step + R.n_days, racc[(R.n_days - 1) & 1]);
+      den_follow_up(R, b, valid, den_ok, den_pref, R.first_step + R.n_days, racc[(R.n_days - 1) % 3]);
     if (blockIdx.x == 0 && threadIdx.x == 0 && R.den_count) R.den_count[0] = R.den_count[1] = 0;
   }
   __syncthreads();
   if (service)
-    rec_flush_warp(racc[(R.n_days - 1) & 1], R.records + (size_t)(R.n_days - 1) * EPI_REC_LEN,
+    rec_flush_warp(racc[(R.n_days - 1) % 3], R.records + (size_t)(R.n_days - 1) * EPI_REC_LEN,
                    R.first_step + R.n_days - 1, nwa, lane);
   if (blockIdx.x == 0 && threadIdx.x < RT_SLOTS && R.ring_t2 != nullptr)
     R.ring_t2->rk[threadIdx.x] =
