@@ -571,12 +571,12 @@ def persistent_profile(sim):
     n, days = sim.n, sim.horizon - 1
     iv = sim.iv
     has_iv = iv.testing_enabled or iv.quarantine_enabled or iv.den_enabled or iv.vaccination_enabled
-    # per agent-day, state in registers: own code write 2 + push rows read
-    # (rin 32 + rout 64) + rin clear 32 + next-day scatter ~16 = 146 B; on
-    # intervention days + the agent's state reloaded (16) and the
-    # intervention columns read and written (testing, DEN, dropout, doses,
-    # buckets: ~44) = 206 B
-    b_day = (206 if has_iv else 146) * n
+    # per agent-day, state in registers and the out-rows (rout) in shared
+    # memory: own code write 2 + in-row read 32 + in-row clear 32 + next-day
+    # scatter ~16 = 82 B; on intervention days + the agent's state reloaded
+    # (16) and the intervention columns read and written (testing, DEN,
+    # dropout, doses, buckets: ~44) = 142 B
+    b_day = (142 if has_iv else 82) * n
     b_day0 = (16 + 2 + 32 + 64 + 32 + 16) * n + (32 + 10 + 1) * n      # + day-0 tables
     total = day0 + run
     name = "k_iv_run" if has_iv else "k_fused_run"

@@ -304,6 +304,12 @@ int epi_set_exchange(epi_ctx *ctx, epi_exchange_fn fn, void *user);
  * up to `max_agents` agents (-1 = while they fit in L2). */
 int epi_set_push_max(epi_ctx *ctx, int64_t max_agents);
 
+/* Beyond the push tables, whole-population fused days without interventions
+ * push only infectious sources into sparse in-rows (32 B/agent, in HBM)
+ * instead of evaluating the 16 inverse slot bijections per agent (default
+ * on; bitwise the same records either way). */
+int epi_set_sparse_push(epi_ctx *ctx, int32_t on);
+
 /* ---- Agent-range partitions over NCCL (SURVEY §8(b) abm_allgather_codes,
  * §8(e)).  No reference counterpart: the reference runs one process per
  * replication (runner.py:164-190) and never partitions a population.

@@ -98,6 +98,7 @@ _SIGS = {
     "epi_set_infection_mode": (_i32, [_p, _i32]),
     "epi_pop_synthesize": (_i32, [C.POINTER(EpiPopSpec), _u64, C.POINTER(EpiPopOut), _p]),
     "epi_set_push_max": (_i32, [_p, _i64]),
+    "epi_set_sparse_push": (_i32, [_p, _i32]),
     "epi_set_lambda_probe": (_i32, [_p, _p, _i32, _i32]),
     "epi_comm_unique_id": (_i32, [_p]),
     "epi_comm_create": (_i32, [_p, _i32, _i32, _p]),

@@ -214,10 +214,13 @@ struct epi_ctx {
   NetTables ntab{};                  // host copy (static radix tables)
   NetTables* ntab_dev[3] = {nullptr, nullptr, nullptr};   // per-day keys, by step % 3
   WorkTables wt_host[2]{};           // day tables by step parity
-  WorkTables* wt_dev[2][3] = {};     // device structs per parity x variant (0 member tables,
-                                     // 1 + wcode, 2 + rin/rout)
-                                     //   0 csr (ids), 1 fused partitioned, 2 fused whole
+  WorkTables* wt_dev[2][4] = {};     // device structs per parity x variant (0 member tables,
+                                     // 1 + wcode, 2 + rin/rout, 3 + rin)
+                                     //   0 csr (ids), 1 fused partitioned, 2 fused whole,
+                                     //   3 fused whole beyond the push tables (sparse rows)
   int merged_ready = -1;             // day whose tables the previous merged kernel built
+  int sparse_push = 1;               // sparse push rows beyond the push tables (epi_set_sparse_push)
+  int sparse_ready = -1;             // day whose sparse rows the previous day kernel pushed
   Injected* inj_dev = nullptr;
   int persistent = 1;                // epi_sim_run: one launch for the merged days
   int iv_fusion = 1;                 // intervention days in 4 launches (k_iv_post_chunks, k_finish_iv)
@@ -943,6 +946,8 @@ int epi_set_exchange(epi_ctx* c, epi_exchange_fn fn, void* user) {
 int epi_set_push_max(epi_ctx* c, int64_t max_agents) {
   if (!c) return fail(EPI_EARG, "null ctx");
   c->push_max = max_agents < 0 ? -1 : (int)(max_agents > 0x7FFFFFFF ? 0x7FFFFFFF : max_agents);
+  c->merged_ready = -1;
+  c->sparse_ready = -1;
   return 0;
 }
 
@@ -1002,15 +1007,17 @@ int epi_net_attach(epi_ctx* c, const epi_net* net) {
     if (!rc) rc = dalloc(&w.rin, (size_t)c->n * RT_SLOTS);
     if (rc) return rc;
     CK(cudaMemset(w.rin, 0, (size_t)c->n * RT_SLOTS * sizeof(uint16_t)));
-    for (int var = 0; var < 3; ++var) {
+    for (int var = 0; var < 4; ++var) {
       WorkTables v = w;
       if (var == 0) v.wcode = nullptr;
       if (var < 2) { v.rin = nullptr; v.rout = nullptr; }
+      if (var == 3) v.rout = nullptr;
       if (!c->wt_dev[par][var]) CK(cudaMalloc((void**)&c->wt_dev[par][var], sizeof(WorkTables)));
       CK(cudaMemcpy(c->wt_dev[par][var], &v, sizeof(WorkTables), cudaMemcpyHostToDevice));
     }
   }
   c->merged_ready = -1;
+  c->sparse_ready = -1;
   c->sigma_day = -1;
   return 0;
 }
@@ -1128,6 +1135,7 @@ static int iv_fused_day(epi_ctx* c, const StepArgs& A, int32_t step, uint64_t se
                   rcount_next, (const uint8_t*)c->bucket, V, p.den_enabled ? c->died_at : (int32_t*)nullptr,
                   listed ? c->den_count : (int*)nullptr, c->net, nx, c->ntab.dn));
   c->merged_ready = step + 1;
+  c->sparse_ready = -1;
   if (ev) CK(cudaEventRecord((cudaEvent_t)ev[3], s));
   return 0;
 }
@@ -1235,6 +1243,11 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
   const bool push_rand = (mode == 1 || msg_only) && c->lo == 0 && c->hi == c->n && c->net.n_agents >= 2 &&
                          c->net.random_slots == RT_SLOTS && batched(&c->net) && push_fits(c);
   const bool merged = mode == 1 && push_rand && !iv;
+  // beyond the push tables, whole-population fused days without interventions
+  // push only infectious sources into sparse in-rows (sparse_kind_sums):
+  // tomorrow's rows in today's epilogue, a chain's first rows seeded here
+  const bool sparse = mode == 1 && !push_rand && !iv && c->sparse_push && c->lo == 0 && c->hi == c->n &&
+                      c->net.n_agents >= 2 && c->net.random_slots == RT_SLOTS && batched(&c->net);
   if (mode == 1 && push_rand && iv && c->iv_fusion)
     return iv_fused_day(c, A, step, seed, codes_cur, codes_next, rec, zero_record, vax_open, ev, s);
   const bool use_wt = (mode == 0 && (push_rand || (has_work && batched(&c->net)))) || mode == 1;
@@ -1273,7 +1286,14 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
                     rec_zero));
     }
   }
-  const WorkTables* wt = use_wt ? c->wt_dev[par][variant] : nullptr;
+  if (sparse && c->sparse_ready != step) {
+    CK(cudaMemsetAsync(c->wt_host[par].rin, 0, (size_t)c->n * RT_SLOTS * sizeof(uint16_t), s));
+    CK(cudaMemsetAsync(c->wt_host[par ^ 1].rin, 0, (size_t)c->n * RT_SLOTS * sizeof(uint16_t), s));
+    k_sparse_seed<<<grid_for(c->n, 256, 8), 256, 0, s>>>(codes_cur, c->n, (const NetTables*)nt_today,
+                                                           c->wt_host[par].rin);
+    CKL();
+  }
+  const WorkTables* wt = use_wt ? c->wt_dev[par][sparse ? 3 : variant] : nullptr;
   if (mode == 0) {
     // fp32 without contact log: the generator writes pre-joined messages and
     // the message pass streams them; otherwise ids (export, DEN, fp64 order)
@@ -1286,6 +1306,7 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
     if (rc) return rc;
     c->net_slot_step[slot] = msg_only ? -1 : step;
     c->merged_ready = -1;
+    c->sparse_ready = -1;
     if (ev) CK(cudaEventRecord((cudaEvent_t)ev[1], s));
     CsrView g{entries, row_len, nullptr, c->net.row_cap, msgs, c->net_toff};
     if (precision == EPI_F64_CANONICAL)
@@ -1311,11 +1332,17 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
       nx.keys_out = c->ntab_dev[(step + 2) % 3];
       nx.rperm_t2 = key_prefix(seed, step + 2, P_NET_RPERM);
       nx.nk = make_net_keys(seed, step + 1);
+    } else if (sparse) {
+      nx.wt = c->wt_dev[par ^ 1][3];
+      nx.keys = nt_next;                  // (written by today's day tables; the day after's too)
+      nx.keys_out = nullptr;
     }
     CK(launch_pdl_w(&c->hot, k_fused_step, dim3(fgrid), dim3(128), 0, s, A, c->net, nk, codes_cur,
                   c->host.rate_scale, codes_next, (const epi_net*)c->net_dev, rcount_next, iv ? 0 : 1, wt,
-                  (const MsgTables*)c->msg_dev, (const NetTables*)nt_today, nx, push_rand ? 1 : 0, DayTests{}));
+                  (const MsgTables*)c->msg_dev, (const NetTables*)nt_today, nx, push_rand ? 1 : (sparse ? 2 : 0),
+                  DayTests{}));
     c->merged_ready = merged ? step + 1 : -1;
+    c->sparse_ready = sparse ? step + 1 : -1;
   }
   if (ev) CK(cudaEventRecord((cudaEvent_t)ev[2], s));
   if (iv) {
@@ -1432,6 +1459,7 @@ static int launch_run(epi_ctx* c, const epi_state* st, int32_t first, int32_t n_
   cfg.attrs = attr;
   CK(cudaLaunchKernelEx(&cfg, k_fused_run, R, c->net));
   c->merged_ready = first + n_days;
+  c->sparse_ready = -1;
   return 0;
 }
 
@@ -1514,6 +1542,7 @@ static int launch_iv_run(epi_ctx* c, const epi_state* st, int32_t first, int32_t
   cfg.attrs = attr;
   CK(cudaLaunchKernelEx(&cfg, k_iv_run, R, c->net));
   c->merged_ready = first + n_days;
+  c->sparse_ready = -1;
   // the per-day path resumes with an empty histogram (k_iv_run used its own)
   if (c->iv_hist) CK(cudaMemsetAsync(c->iv_hist, 0, (size_t)2 * NUM_BUCKETS * sizeof(unsigned long long), s));
   return 0;
@@ -1547,10 +1576,18 @@ int epi_set_day_grid(epi_ctx* c, int32_t blocks_per_sm) {
   return 0;
 }
 
+int epi_set_sparse_push(epi_ctx* c, int32_t on) {
+  if (!c) return fail(EPI_EARG, "null ctx");
+  c->sparse_push = on != 0;
+  c->sparse_ready = -1;
+  return 0;
+}
+
 int epi_set_iv_fusion(epi_ctx* c, int32_t on) {
   if (!c) return fail(EPI_EARG, "null ctx");
   c->iv_fusion = on != 0;
   c->merged_ready = -1;
+  c->sparse_ready = -1;
   return 0;
 }
 
@@ -1722,6 +1759,7 @@ int epi_net_generate(epi_ctx* c, int32_t step, uint64_t seed, const uint16_t* co
   w.rin = nullptr;
   w.rout = nullptr;
   c->merged_ready = -1;
+  c->sparse_ready = -1;
   if (has_work) {
     k_day_tables<<<grid_for(c->net.n_member_slots, 256, 4), 256, 0, s>>>(
         c->net, nk, w, codes_cur, c->lo, c->hi, grid_for(c->net.n_member_slots, 256, 4), nt,

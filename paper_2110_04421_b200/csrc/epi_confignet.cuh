@@ -601,6 +601,68 @@ __device__ __forceinline__ void code_kind_sums(const epi_net& net, const PermKey
   }
 }
 
+// code_kind_sums with the random in-partners from a SPARSE push row instead
+// of 16 inverse slot walks (whole-population runs too large for the full
+// push tables): rin[b][j] holds the code of the in-partner of slot j only if
+// that source is infectious (code byte != 0); every other slot is 0, and
+// factor[0] = 0, so the slot-ordered sum is bitwise that of code_kind_sums.
+// The in-edge count cannot come from the row: summed over the population the
+// random in-edges between alive agents equal the random out-edges between
+// alive agents (each is one (source, slot) pair seen from either end), so
+// each alive agent counts its alive out-partners twice.  Only the record's
+// population total uses `edges`.
+__device__ __forceinline__ void sparse_kind_sums(const epi_net& net, const PermKeys* __restrict__ rk,
+                                                 const Radix& dn, const WorkTables* __restrict__ wt,
+                                                 const uint16_t* __restrict__ codes, int64_t b, uint16_t code_b,
+                                                 const float* __restrict__ factor, float acc[3],
+                                                 unsigned& edges) {
+  const uint4* ri = (const uint4*)(wt->rin + (size_t)b * RT_SLOTS);
+  const uint4 in0 = ri[0], in1 = ri[1];          // issued first: the row's latency under the rest
+  {
+    const int off = net.hh_off[b];
+    const int sz = net.hh_size[b];
+    const int64_t start = b - off;
+    for (int i = 0; i < sz; ++i) {
+      const int64_t c = start + i;
+      add_src(acc[0], edges, factor, c == b ? (uint16_t)CODE_DEAD : codes[c]);
+    }
+  }
+  const int w = net.wp_id[b];
+  if (w >= 0) {
+    const int m = net.wp_size[w];
+    if (m >= 2) {
+      const int base = net.wp_base[w];
+      const int draws = net.colleague_draws;
+      const uint32_t p = wt->pos_of[base + net.wp_local[b]];
+      const uint8_t* sh = wt->shift + (size_t)w * draws;
+      const uint16_t* wc = wt->wcode + base;
+      for (int j = 0; j < draws; ++j) {
+        const uint32_t r = sh[j];
+        add_src(acc[1], edges, factor, wc[add_mod(p, r, (uint32_t)m)]);
+        add_src(acc[1], edges, factor, wc[sub_mod(p, r, (uint32_t)m)]);
+      }
+    }
+  }
+  if (net.n_agents < 2) return;
+  const uint32_t self = (uint32_t)b;
+  const int nb = code_count(code_b);
+  const int nbe = nb < RT_SLOTS ? nb : RT_SLOTS;
+  unsigned eo = 0;
+  for (int j0 = 0; j0 < nbe; j0 += 4) {
+    uint32_t po[4];
+    uint16_t co[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) po[q] = (j0 + q < nbe) ? walk_fwd(self, rk[j0 + q], dn) : self;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) co[q] = po[q] != self ? codes[po[q]] : (uint16_t)CODE_DEAD;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) add_src(acc[2], eo, factor, co[q]);
+  }
+  edges += 2u * eo;
+  unsigned present = 0;                          // (the row's present bits: infectious in-partners only)
+  add_rin_row(acc[2], present, factor, in0, in1);
+}
+
 // Push-table form of for_each_in_code for the fused day kernel, written so
 // that every load of a level is issued before any of them is consumed
 // (memory-level parallelism for the ~21 warps per SM of a 100k-agent day):

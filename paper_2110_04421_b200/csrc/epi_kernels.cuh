@@ -1012,11 +1012,64 @@ __device__ __forceinline__ void push_next_day(const epi_net& net, const NextTabl
   __syncwarp();
 }
 
+// Tomorrow's SPARSE push rows (sparse_kind_sums): only agents whose
+// next-day code is infectious (code byte != 0) scatter rin[pi_j(b)][j] =
+// cn | PRESENT for their slots j < n; the warp's items flattened 32 at a
+// time.  No out-rows (the day kernel walks the out-partners itself).
+__device__ __forceinline__ void push_next_sparse(const NextTables& nx, bool valid, uint16_t cn,
+                                                 const PermKeys* rk_next, const Radix& dn, int* excl_w,
+                                                 uint16_t* cn_w, uint8_t* own_w, int64_t wbase_agent, int lane) {
+  const WorkTables& W = *nx.wt;
+  int na = (valid && (cn & 0xFF) != 0) ? code_count(cn) : 0;
+  na = na < RT_SLOTS ? na : RT_SLOTS;
+  int incl = na;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  const int total = __shfl_sync(0xFFFFFFFFu, incl, 31);
+  if (total == 0) return;                        // (warp-uniform)
+  const int excl = incl - na;
+  excl_w[lane] = excl;
+  cn_w[lane] = cn;
+  for (int i = 0; i < na; ++i) own_w[excl + i] = (uint8_t)lane;
+  __syncwarp();
+  for (int k = lane; k < total; k += 32) {
+    const int l = own_w[k];
+    const int j = k - excl_w[l];
+    const uint32_t src = (uint32_t)(wbase_agent + l);
+    const uint32_t y = walk_fwd(src, rk_next[j], dn);
+    if (y != src) W.rin[(size_t)y * RT_SLOTS + j] = cn_w[l] | CODE_PRESENT;
+  }
+  __syncwarp();
+}
+
+// The first day of a sparse-push chain: today's rows from today's codes.
+__global__ void __launch_bounds__(256) k_sparse_seed(const uint16_t* __restrict__ codes, int64_t n,
+                                                     const NetTables* __restrict__ NTp, uint16_t* __restrict__ rin) {
+  __shared__ PermKeys rk[RT_SLOTS];
+  if (threadIdx.x < RT_SLOTS) rk[threadIdx.x] = NTp->rk[threadIdx.x];
+  __syncthreads();
+  const Radix dn = NTp->dn;
+  for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < n; b += (int64_t)gridDim.x * blockDim.x) {
+    const uint16_t c = codes[b];
+    if ((c & 0xFF) == 0) continue;
+    int na = code_count(c);
+    na = na < RT_SLOTS ? na : RT_SLOTS;
+    for (int j = 0; j < na; ++j) {
+      const uint32_t y = walk_fwd((uint32_t)b, rk[j], dn);
+      if (y != (uint32_t)b) rin[(size_t)y * RT_SLOTS + j] = c | CODE_PRESENT;
+    }
+  }
+}
+
 // tomorrow's random-slot keys into shared memory; block 0 writes those of
-// the day after into the ring (all threads call; ends with a bar.sync)
+// the day after into the ring unless another kernel does (all threads call;
+// ends with a bar.sync)
 __device__ __forceinline__ void load_next_keys(const NextTables& nx, PermKeys* rk_next) {
   for (int j = threadIdx.x; j < EPI_MAX_SLOTS; j += blockDim.x) rk_next[j] = nx.keys->rk[j];
-  if (blockIdx.x == 0 && threadIdx.x < EPI_MAX_SLOTS)
+  if (blockIdx.x == 0 && threadIdx.x < EPI_MAX_SLOTS && nx.keys_out != nullptr)
     nx.keys_out->rk[threadIdx.x] = random_slot_keys(nx.rperm_t2, threadIdx.x);
   __syncthreads();
 }
@@ -1046,8 +1099,9 @@ __global__ void __launch_bounds__(128, 8) k_fused_step(StepArgs A, epi_net net, 
   __shared__ uint8_t own_s[4][32 * RT_SLOTS];
   load_msg_tables(T, mt);
   // with the day's push tables (random rows + workplace codes) only the agent
-  // domain is needed; the epilogue derives workplace domains on the fly
-  if (push) {
+  // domain is needed; the epilogue derives workplace domains on the fly.
+  // push: 0 none (inverse slot walks), 1 push tables, 2 sparse push rows
+  if (push == 1) {
     if (threadIdx.x < (int)(sizeof(Radix) / 4))
       ((uint32_t*)&NT.dn)[threadIdx.x] = ((const uint32_t*)&NTp->dn)[threadIdx.x];
   } else {
@@ -1079,8 +1133,10 @@ __global__ void __launch_bounds__(128, 8) k_fused_step(StepArgs A, epi_net net, 
         // one sum per network kind (the kind is a constant at every visit),
         // scaled by B[kind] once
         float acc[3] = {0.f, 0.f, 0.f};
-        if (push)
+        if (push == 1)
           push_kind_sums(net, wt, codes, b, cb, T.factor, acc, edges);
+        else if (push == 2)
+          sparse_kind_sums(net, NT.rk, dn, wt, codes, b, cb, T.factor, acc, edges);
         else
           code_kind_sums(net, NT.rk, dn, wt, codes, b, cb, T.factor, acc, edges);
         const float tot = acc[0] * T.bfac[0] + acc[1] * T.bfac[1] + acc[2] * T.bfac[2];
@@ -1112,7 +1168,10 @@ __global__ void __launch_bounds__(128, 8) k_fused_step(StepArgs A, epi_net net, 
         cn = next_code_hot(A.P, h, b, A.step + 1, net_dev, rcount_next);
         codes_next[b] = cn;
       }
-      if (merge)
+      if (merge && push == 2)
+        push_next_sparse(nx, valid, cn, rk_next, dn, excl_s[warp], cn_s[warp], own_s[warp],
+                         base + (threadIdx.x & ~31), lane);
+      else if (merge)
         push_next_day(net, nx, valid, b, cn, rk_next, dn, excl_s[warp], cn_s[warp], own_s[warp],
                       base + (threadIdx.x & ~31), lane);
     }

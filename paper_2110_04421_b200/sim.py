@@ -94,7 +94,7 @@ class ConfigSimulation:
     def __init__(self, pop: ConfigPopulation, disease, table, interventions, seed: int,
                  mode: str = "csr", precision: str = "f32", horizon: int = 180,
                  device=None, initial=None, push_max: int | None = None, persistent: bool = True,
-                 iv_fusion: bool = True, day_blocks_per_sm: int = 0):
+                 iv_fusion: bool = True, day_blocks_per_sm: int = 0, sparse_push: bool = True):
         import torch
         if mode not in ("csr", "fused"):
             raise ConfigError(f"unknown mode {mode!r}")
@@ -119,6 +119,8 @@ class ConfigSimulation:
         self._after_attach()
         if push_max is not None:
             N.check(self._lib.epi_set_push_max(self._ctx, int(push_max)))
+        # beyond the push tables: sparse push rows (else 16 inverse slot walks per agent)
+        N.check(self._lib.epi_set_sparse_push(self._ctx, int(bool(sparse_push))))
         # run(): merged fused days in one persistent launch (else one kernel per day)
         N.check(self._lib.epi_set_persistent(self._ctx, int(bool(persistent))))
         # fused-mode intervention days in 4 launches (else one kernel per phase)
