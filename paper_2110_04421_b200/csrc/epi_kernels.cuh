@@ -1040,7 +1040,7 @@ __device__ __forceinline__ void push_next_sparse(const NextTables& nx, bool vali
     const int j = k - excl_w[l];
     const uint32_t src = (uint32_t)(wbase_agent + l);
     const uint32_t y = walk_fwd(src, rk_next[j], dn);
-    if (y != src) W.rin[(size_t)y * RT_SLOTS + j] = cn_w[l] | CODE_PRESENT;
+    if (y != src) __stcs(W.rin + (size_t)y * RT_SLOTS + j, (unsigned short)(cn_w[l] | CODE_PRESENT));
   }
   __syncwarp();
 }
@@ -1142,7 +1142,13 @@ __global__ void __launch_bounds__(128, 8) k_fused_step(StepArgs A, epi_net net, 
         const float tot = acc[0] * T.bfac[0] + acc[1] * T.bfac[1] + acc[2] * T.bfac[2];
         if (h.stage == S_SUS && !(A.P->sterilizing && h.immune)) lam = (double)(tot * T.sfac[h.age]);
       }
-      clear_rin_row(wt, b);
+      if (push == 2) {                     // (sparse rows: streamed, evict-first)
+        uint4* row = (uint4*)(wt->rin + (size_t)b * RT_SLOTS);
+        __stcs(row, make_uint4(0, 0, 0, 0));
+        __stcs(row + 1, make_uint4(0, 0, 0, 0));
+      } else {
+        clear_rin_row(wt, b);
+      }
     }
     unsigned ev = 0;
     if (valid) probe_lambda(A.probe, A.step, b, lam);
