@@ -221,6 +221,7 @@ struct epi_ctx {
   int merged_ready = -1;             // day whose tables the previous merged kernel built
   int sparse_push = 1;               // sparse push rows beyond the push tables (epi_set_sparse_push)
   int sparse_ready = -1;             // day whose sparse rows the previous day kernel pushed
+  int sparse_clean = -1;             // day whose sparse rows are all zero (the chain goes on)
   Injected* inj_dev = nullptr;
   int persistent = 1;                // epi_sim_run: one launch for the merged days
   int iv_fusion = 1;                 // intervention days in 4 launches (k_iv_post_chunks, k_finish_iv)
@@ -948,6 +949,7 @@ int epi_set_push_max(epi_ctx* c, int64_t max_agents) {
   c->push_max = max_agents < 0 ? -1 : (int)(max_agents > 0x7FFFFFFF ? 0x7FFFFFFF : max_agents);
   c->merged_ready = -1;
   c->sparse_ready = -1;
+  c->sparse_clean = -1;
   return 0;
 }
 
@@ -1018,6 +1020,7 @@ int epi_net_attach(epi_ctx* c, const epi_net* net) {
   }
   c->merged_ready = -1;
   c->sparse_ready = -1;
+  c->sparse_clean = -1;
   c->sigma_day = -1;
   return 0;
 }
@@ -1136,6 +1139,7 @@ static int iv_fused_day(epi_ctx* c, const StepArgs& A, int32_t step, uint64_t se
                   listed ? c->den_count : (int*)nullptr, c->net, nx, c->ntab.dn));
   c->merged_ready = step + 1;
   c->sparse_ready = -1;
+  c->sparse_clean = -1;
   if (ev) CK(cudaEventRecord((cudaEvent_t)ev[3], s));
   return 0;
 }
@@ -1243,11 +1247,13 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
   const bool push_rand = (mode == 1 || msg_only) && c->lo == 0 && c->hi == c->n && c->net.n_agents >= 2 &&
                          c->net.random_slots == RT_SLOTS && batched(&c->net) && push_fits(c);
   const bool merged = mode == 1 && push_rand && !iv;
-  // beyond the push tables, whole-population fused days without interventions
-  // push only infectious sources into sparse in-rows (sparse_kind_sums):
-  // tomorrow's rows in today's epilogue, a chain's first rows seeded here
-  const bool sparse = mode == 1 && !push_rand && !iv && c->sparse_push && c->lo == 0 && c->hi == c->n &&
-                      c->net.n_agents >= 2 && c->net.random_slots == RT_SLOTS && batched(&c->net);
+  // beyond the push tables (and on partitioned ranks), fused days without
+  // interventions push only infectious sources into sparse in-rows
+  // (sparse_kind_sums): a whole population's tomorrow in today's epilogue, a
+  // chain's first rows and every day of a partitioned rank seeded here
+  const bool whole = c->lo == 0 && c->hi == c->n;
+  const bool sparse = mode == 1 && !push_rand && !iv && c->sparse_push && c->net.n_agents >= 2 &&
+                      c->net.random_slots == RT_SLOTS && batched(&c->net);
   if (mode == 1 && push_rand && iv && c->iv_fusion)
     return iv_fused_day(c, A, step, seed, codes_cur, codes_next, rec, zero_record, vax_open, ev, s);
   const bool use_wt = (mode == 0 && (push_rand || (has_work && batched(&c->net)))) || mode == 1;
@@ -1287,9 +1293,11 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
     }
   }
   if (sparse && c->sparse_ready != step) {
-    CK(cudaMemsetAsync(c->wt_host[par].rin, 0, (size_t)c->n * RT_SLOTS * sizeof(uint16_t), s));
-    CK(cudaMemsetAsync(c->wt_host[par ^ 1].rin, 0, (size_t)c->n * RT_SLOTS * sizeof(uint16_t), s));
-    k_sparse_seed<<<grid_for(c->n, 256, 8), 256, 0, s>>>(codes_cur, c->n, (const NetTables*)nt_today,
+    if (c->sparse_clean != step) {        // a new chain: both parities start empty
+      CK(cudaMemsetAsync(c->wt_host[par].rin, 0, (size_t)c->n * RT_SLOTS * sizeof(uint16_t), s));
+      CK(cudaMemsetAsync(c->wt_host[par ^ 1].rin, 0, (size_t)c->n * RT_SLOTS * sizeof(uint16_t), s));
+    }
+    k_sparse_seed<<<grid_for(c->n, 256, 8), 256, 0, s>>>(codes_cur, c->n, c->lo, c->hi, (const NetTables*)nt_today,
                                                            c->wt_host[par].rin);
     CKL();
   }
@@ -1307,6 +1315,7 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
     c->net_slot_step[slot] = msg_only ? -1 : step;
     c->merged_ready = -1;
     c->sparse_ready = -1;
+    c->sparse_clean = -1;
     if (ev) CK(cudaEventRecord((cudaEvent_t)ev[1], s));
     CsrView g{entries, row_len, nullptr, c->net.row_cap, msgs, c->net_toff};
     if (precision == EPI_F64_CANONICAL)
@@ -1332,7 +1341,7 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
       nx.keys_out = c->ntab_dev[(step + 2) % 3];
       nx.rperm_t2 = key_prefix(seed, step + 2, P_NET_RPERM);
       nx.nk = make_net_keys(seed, step + 1);
-    } else if (sparse) {
+    } else if (sparse && whole) {
       nx.wt = c->wt_dev[par ^ 1][3];
       nx.keys = nt_next;                  // (written by today's day tables; the day after's too)
       nx.keys_out = nullptr;
@@ -1342,7 +1351,8 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
                   (const MsgTables*)c->msg_dev, (const NetTables*)nt_today, nx, push_rand ? 1 : (sparse ? 2 : 0),
                   DayTests{}));
     c->merged_ready = merged ? step + 1 : -1;
-    c->sparse_ready = sparse ? step + 1 : -1;
+    c->sparse_ready = sparse && whole ? step + 1 : -1;
+    c->sparse_clean = sparse ? step + 1 : -1;   // (the day's consumed rows were cleared)
   }
   if (ev) CK(cudaEventRecord((cudaEvent_t)ev[2], s));
   if (iv) {
@@ -1460,6 +1470,7 @@ static int launch_run(epi_ctx* c, const epi_state* st, int32_t first, int32_t n_
   CK(cudaLaunchKernelEx(&cfg, k_fused_run, R, c->net));
   c->merged_ready = first + n_days;
   c->sparse_ready = -1;
+  c->sparse_clean = -1;
   return 0;
 }
 
@@ -1543,6 +1554,7 @@ static int launch_iv_run(epi_ctx* c, const epi_state* st, int32_t first, int32_t
   CK(cudaLaunchKernelEx(&cfg, k_iv_run, R, c->net));
   c->merged_ready = first + n_days;
   c->sparse_ready = -1;
+  c->sparse_clean = -1;
   // the per-day path resumes with an empty histogram (k_iv_run used its own)
   if (c->iv_hist) CK(cudaMemsetAsync(c->iv_hist, 0, (size_t)2 * NUM_BUCKETS * sizeof(unsigned long long), s));
   return 0;
@@ -1580,6 +1592,7 @@ int epi_set_sparse_push(epi_ctx* c, int32_t on) {
   if (!c) return fail(EPI_EARG, "null ctx");
   c->sparse_push = on != 0;
   c->sparse_ready = -1;
+  c->sparse_clean = -1;
   return 0;
 }
 
@@ -1588,6 +1601,7 @@ int epi_set_iv_fusion(epi_ctx* c, int32_t on) {
   c->iv_fusion = on != 0;
   c->merged_ready = -1;
   c->sparse_ready = -1;
+  c->sparse_clean = -1;
   return 0;
 }
 
@@ -1760,6 +1774,7 @@ int epi_net_generate(epi_ctx* c, int32_t step, uint64_t seed, const uint16_t* co
   w.rout = nullptr;
   c->merged_ready = -1;
   c->sparse_ready = -1;
+  c->sparse_clean = -1;
   if (has_work) {
     k_day_tables<<<grid_for(c->net.n_member_slots, 256, 4), 256, 0, s>>>(
         c->net, nk, w, codes_cur, c->lo, c->hi, grid_for(c->net.n_member_slots, 256, 4), nt,

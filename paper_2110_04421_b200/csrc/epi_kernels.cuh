@@ -1045,9 +1045,14 @@ __device__ __forceinline__ void push_next_sparse(const NextTables& nx, bool vali
   __syncwarp();
 }
 
-// The first day of a sparse-push chain: today's rows from today's codes.
-__global__ void __launch_bounds__(256) k_sparse_seed(const uint16_t* __restrict__ codes, int64_t n,
-                                                     const NetTables* __restrict__ NTp, uint16_t* __restrict__ rin) {
+// Today's sparse rows from today's codes: the first day of a whole-population
+// chain (later days come from the previous day's epilogue), and every day of
+// a partitioned rank, whose in-partners may live on any rank: all n sources
+// are scanned (the day's code vector is complete after the all-gather) and
+// only pushes into the rank's own rows [lo, hi) are kept.
+__global__ void __launch_bounds__(256) k_sparse_seed(const uint16_t* __restrict__ codes, int64_t n, int64_t lo,
+                                                     int64_t hi, const NetTables* __restrict__ NTp,
+                                                     uint16_t* __restrict__ rin) {
   __shared__ PermKeys rk[RT_SLOTS];
   if (threadIdx.x < RT_SLOTS) rk[threadIdx.x] = NTp->rk[threadIdx.x];
   __syncthreads();
@@ -1059,7 +1064,7 @@ __global__ void __launch_bounds__(256) k_sparse_seed(const uint16_t* __restrict_
     na = na < RT_SLOTS ? na : RT_SLOTS;
     for (int j = 0; j < na; ++j) {
       const uint32_t y = walk_fwd((uint32_t)b, rk[j], dn);
-      if (y != (uint32_t)b) rin[(size_t)y * RT_SLOTS + j] = c | CODE_PRESENT;
+      if (y != (uint32_t)b && (int64_t)y >= lo && (int64_t)y < hi) rin[(size_t)y * RT_SLOTS + j] = c | CODE_PRESENT;
     }
   }
 }

@@ -64,3 +64,23 @@ def test_sparse_rows_chunked_reset_and_graph_replay():
         sp.replay()
     assert np.array_equal(sp.rec.cpu().numpy(), ref.rec.cpu().numpy())
     assert torch.equal(sp._codes_buf, ref._codes_buf)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("sparse", [True, False])
+def test_partitioned_ranks_sparse_rows_on_and_off_equal_single(world, sparse):
+    """Partitioned ranks (host threads, the per-day code all-gather): with
+    sparse rows every rank seeds its own rows from all infectious sources
+    after the gather; without, 16 inverse walks per owned agent.  Both are
+    bitwise the single-rank run (push tables)."""
+    from paper_2110_04421_b200.partition import run_threaded
+    pop = synthesize(ConfigNetworkSpec.config(1, n_agents=15000, initial_infections=80), 8)
+    d, t, iv = default_disease(), default_progression(), InterventionConfig()
+    ref = ConfigSimulation(pop, d, t, iv, 23, mode="fused", horizon=50)
+    ref.run()
+    sims, rec = run_threaded(pop, d, t, iv, 23, world, 50, mode="fused", sparse_push=sparse)
+    assert np.array_equal(rec.cpu().numpy(), ref.rec.cpu().numpy())
+    full = ref.host_columns()
+    for s in sims:
+        lo, hi = s.plan.rows(s.rank)
+        assert np.array_equal(s.host_columns().stage[lo:hi], full.stage[lo:hi])
