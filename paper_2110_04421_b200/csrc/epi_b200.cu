@@ -12,7 +12,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include <cub/device/device_scan.cuh>
@@ -113,12 +115,93 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
   return launch_pdl_w(nullptr, kernel, grid, block, smem, s, args...);
 }
 
+// Device buffers of contexts come from a process-wide cache: epi_destroy
+// synchronises the device once and returns its buffers to the cache, and the
+// next context asking for the same (256-byte rounded) size reuses them.  A
+// caller building many short-lived engines (the reference's own test suite
+// builds ~20 000) otherwise pays a cudaFree per buffer -- each a device
+// synchronisation and an unmap, ~100 ms for a garbage-collection pass that
+// finalises a few hundred engines at once.  At most 1 GiB stays cached.
+namespace {
+struct DevCache {
+  std::mutex m;
+  std::unordered_map<void*, size_t> live;              // cache-managed pointer -> bytes
+  std::unordered_multimap<size_t, void*> idle;
+  size_t idle_bytes = 0;
+};
+DevCache& dcache() {
+  static DevCache* c = new DevCache;                    // never destroyed: used until process exit
+  return *c;
+}
+constexpr size_t DCACHE_CAP = (size_t)1 << 30;
+}  // namespace
+
+cudaError_t dmalloc(void** p, size_t bytes) {
+  bytes = ((bytes ? bytes : 1) + 255) & ~(size_t)255;
+  DevCache& c = dcache();
+  {
+    std::lock_guard<std::mutex> g(c.m);
+    auto it = c.idle.find(bytes);
+    if (it != c.idle.end()) {
+      *p = it->second;
+      c.idle.erase(it);
+      c.idle_bytes -= bytes;
+      c.live[*p] = bytes;
+      return cudaSuccess;
+    }
+  }
+  cudaError_t e = cudaMalloc(p, bytes);
+  if (e == cudaErrorMemoryAllocation) {                 // give the cached buffers back and retry
+    cudaGetLastError();
+    std::lock_guard<std::mutex> g(c.m);
+    for (auto& kv : c.idle) cudaFree(kv.second);
+    c.idle.clear();
+    c.idle_bytes = 0;
+    e = cudaMalloc(p, bytes);
+  }
+  if (e == cudaSuccess) {
+    std::lock_guard<std::mutex> g(c.m);
+    c.live[*p] = bytes;
+  }
+  return e;
+}
+// Free now (cudaFree: synchronous), cache-managed or not.
+void dfree_now(void* p) {
+  if (!p) return;
+  {
+    DevCache& c = dcache();
+    std::lock_guard<std::mutex> g(c.m);
+    c.live.erase(p);
+  }
+  cudaFree(p);
+}
+// Return to the cache; only after the device has been synchronised (no
+// kernel may still use the buffer when the next context receives it).
+void dput(void* p) {
+  if (!p) return;
+  DevCache& c = dcache();
+  {
+    std::lock_guard<std::mutex> g(c.m);
+    auto it = c.live.find(p);
+    if (it != c.live.end()) {
+      const size_t b = it->second;
+      c.live.erase(it);
+      if (c.idle_bytes + b <= DCACHE_CAP) {
+        c.idle.emplace(b, p);
+        c.idle_bytes += b;
+        return;
+      }
+    }
+  }
+  cudaFree(p);
+}
+
 template <class T>
 int dalloc(T** p, size_t count) {
-  if (*p) cudaFree(*p);
+  if (*p) dfree_now(*p);
   *p = nullptr;
   if (count == 0) count = 1;
-  CK(cudaMalloc((void**)p, count * sizeof(T)));
+  CK(dmalloc((void**)p, count * sizeof(T)));
   return 0;
 }
 
@@ -254,19 +337,19 @@ int upload_params(epi_ctx* c, const epi_params* p) {
   for (int i = 0; i < p->n_specs; ++i)
     if (p->tau_len[i] < 0 || p->tau_len[i] > EPI_MAX_TAUS) return fail(EPI_EARG, "tau table too long");
   c->host = *p;
-  if (!c->P) CK(cudaMalloc((void**)&c->P, sizeof(epi_params)));
+  if (!c->P) CK(dmalloc((void**)&c->P, sizeof(epi_params)));
   CK(cudaMemcpy(c->P, p, sizeof(epi_params), cudaMemcpyHostToDevice));
   MsgTables mt;
   fill_msg_tables(mt, *p, p->rate_scale);
-  if (!c->msg_dev) CK(cudaMalloc((void**)&c->msg_dev, sizeof(MsgTables)));
+  if (!c->msg_dev) CK(dmalloc((void**)&c->msg_dev, sizeof(MsgTables)));
   CK(cudaMemcpy(c->msg_dev, &mt, sizeof(MsgTables), cudaMemcpyHostToDevice));
   static MsgComb mc;   // 4 KB: not on the stack
   fill_msg_comb(mc, *p, p->rate_scale);
-  if (!c->comb_dev) CK(cudaMalloc((void**)&c->comb_dev, sizeof(MsgComb)));
+  if (!c->comb_dev) CK(dmalloc((void**)&c->comb_dev, sizeof(MsgComb)));
   CK(cudaMemcpy(c->comb_dev, &mc, sizeof(MsgComb), cudaMemcpyHostToDevice));
   std::vector<uint16_t> lut((size_t)EPI_MAX_SPECS * TAU_LUT);
   fill_tau_lut(lut.data(), *p);
-  if (!c->tau_lut) CK(cudaMalloc((void**)&c->tau_lut, lut.size() * sizeof(uint16_t)));
+  if (!c->tau_lut) CK(dmalloc((void**)&c->tau_lut, lut.size() * sizeof(uint16_t)));
   CK(cudaMemcpy(c->tau_lut, lut.data(), lut.size() * sizeof(uint16_t), cudaMemcpyHostToDevice));
   return 0;
 }
@@ -294,7 +377,7 @@ int upload_injected(epi_ctx* c, const double* const* injected, const Injected** 
   if (!injected) return 0;
   Injected h;
   for (int i = 0; i < 12; ++i) h.u[i] = injected[i];
-  if (!c->inj_dev) CK(cudaMalloc((void**)&c->inj_dev, sizeof(Injected)));
+  if (!c->inj_dev) CK(dmalloc((void**)&c->inj_dev, sizeof(Injected)));
   CK(cudaMemcpyAsync(c->inj_dev, &h, sizeof(Injected), cudaMemcpyHostToDevice, s));
   *out = c->inj_dev;
   return 0;
@@ -389,6 +472,14 @@ static bool push_fits(const epi_ctx* c) {
   return (double)c->n * 96.0 <= (double)l2;
 }
 
+// Could the days of a run go to the persistent kernels (one co-resident
+// thread per agent, epi_set_persistent on)?  (persistent_ok adds the rest.)
+static bool run_fits(const epi_ctx* c) {
+  const int64_t sms = sm_count();
+  const int64_t threads = ((c->n + sms - 1) / sms + 31) / 32 * 32;     // (run_threads)
+  return c->persistent && c->net.colleague_draws <= 8 && threads <= RUN_MAX_AGENTS;
+}
+
 // k_msg_pass: per-warp segment scratch
 static int msg_pass_smem(int) { return MP_SMEM; }
 
@@ -455,58 +546,59 @@ int epi_create(const epi_params* params, int64_t n_agents, epi_ctx** out) {
 
 int epi_destroy(epi_ctx* c) {
   if (!c) return 0;
-  cudaFree(c->P);
-  cudaFree(c->flags);
-  cudaFree(c->bucket);
-  cudaFree(c->hist);
-  cudaFree(c->plan);
-  cudaFree(c->tile_off);
-  cudaFree(c->scratch_rec);
-  cudaFree(c->gflags);
-  cudaFree(c->codes);
-  cudaFree(c->codes_alt);
-  cudaFree(c->entries);
-  cudaFree(c->row_begin);
-  cudaFree(c->row_len);
-  cudaFree(c->row_fill);
-  cudaFree(c->entries_tmp);
-  cudaFree(c->long_rows);
-  cudaFree(c->long_count);
-  cudaFree(c->cub_tmp);
-  cudaFree(c->net_dev);
-  cudaFree(c->inj_dev);
-  cudaFree(c->msg_dev);
-  cudaFree(c->comb_dev);
-  cudaFree(c->tau_lut);
-  cudaFree(c->died_at);
-  cudaFree(c->den_mark);
-  cudaFree(c->den_list);
-  cudaFree(c->den_count);
-  cudaFree(c->run_barrier);
-  cudaFree(c->iv_tile_hist);
-  cudaFree(c->iv_hist);
-  cudaFree(c->ivr_hist);
-  cudaFree(c->ivr_tile_hist);
-  for (auto* p : c->ntab_dev) cudaFree(p);
-  cudaFree(c->wt_host[0].member_at_pos);
-  cudaFree(c->wt_host[1].member_at_pos);
+  cudaDeviceSynchronize();             // no kernel of this context may still use its buffers
+  dput(c->P);
+  dput(c->flags);
+  dput(c->bucket);
+  dput(c->hist);
+  dput(c->plan);
+  dput(c->tile_off);
+  dput(c->scratch_rec);
+  dput(c->gflags);
+  dput(c->codes);
+  dput(c->codes_alt);
+  dput(c->entries);
+  dput(c->row_begin);
+  dput(c->row_len);
+  dput(c->row_fill);
+  dput(c->entries_tmp);
+  dput(c->long_rows);
+  dput(c->long_count);
+  dput(c->cub_tmp);
+  dput(c->net_dev);
+  dput(c->inj_dev);
+  dput(c->msg_dev);
+  dput(c->comb_dev);
+  dput(c->tau_lut);
+  dput(c->died_at);
+  dput(c->den_mark);
+  dput(c->den_list);
+  dput(c->den_count);
+  dput(c->run_barrier);
+  dput(c->iv_tile_hist);
+  dput(c->iv_hist);
+  dput(c->ivr_hist);
+  dput(c->ivr_tile_hist);
+  for (auto* p : c->ntab_dev) dput(p);
+  dput(c->wt_host[0].member_at_pos);
+  dput(c->wt_host[1].member_at_pos);
   if (c->side) cudaStreamDestroy(c->side);
   if (c->fork_ev) cudaEventDestroy(c->fork_ev);
   if (c->sigma_ev) cudaEventDestroy(c->sigma_ev);
   for (auto& w : c->wt_host) {
-    cudaFree(w.pos_of);
-    cudaFree(w.shift);
-    cudaFree(w.wcode);
-    cudaFree(w.rout);
-    cudaFree(w.rin);
+    dput(w.pos_of);
+    dput(w.shift);
+    dput(w.wcode);
+    dput(w.rout);
+    dput(w.rin);
   }
   for (auto& row : c->wt_dev)
-    for (auto* p : row) cudaFree(p);
-  for (auto& s : c->ring) { cudaFree(s.src); cudaFree(s.dst); }
-  for (auto* p : c->net_entries) cudaFree(p);
-  for (auto* p : c->net_rowlen) cudaFree(p);
-  cudaFree(c->net_msgs);
-  cudaFree(c->net_toff);
+    for (auto* p : row) dput(p);
+  for (auto& s : c->ring) { dput(s.src); dput(s.dst); }
+  for (auto* p : c->net_entries) dput(p);
+  for (auto* p : c->net_rowlen) dput(p);
+  dput(c->net_msgs);
+  dput(c->net_toff);
   delete c;
   return 0;
 }
@@ -590,9 +682,9 @@ static int graph_load_impl(epi_ctx* c, const int32_t* src, const int32_t* dst, c
   CK(cub::DeviceScan::ExclusiveScan(nullptr, need, c->row_len, c->row_begin, cuda::std::plus<>{}, (int64_t)0,
                                     (int)c->n, s));
   if (need > c->cub_bytes) {
-    cudaFree(c->cub_tmp);
+    dfree_now(c->cub_tmp);
     c->cub_tmp = nullptr;
-    CK(cudaMalloc(&c->cub_tmp, need));
+    CK(dmalloc(&c->cub_tmp, need));
     c->cub_bytes = need;
   }
   CK(cub::DeviceScan::ExclusiveScan(c->cub_tmp, need, c->row_len, c->row_begin, cuda::std::plus<>{}, (int64_t)0,
@@ -641,7 +733,7 @@ int epi_gather(epi_ctx* c, const epi_state* st, int32_t step, int32_t precision,
 static int push_ring(epi_ctx* c, cudaStream_t s) {
   const int L = c->host.den_lookback;
   if ((int)c->ring.size() != L) {
-    for (auto& sl : c->ring) { cudaFree(sl.src); cudaFree(sl.dst); }
+    for (auto& sl : c->ring) { dfree_now(sl.src); dfree_now(sl.dst); }
     c->ring.assign(L, epi_ctx::Slot{});
     c->ring_head = 0;
     c->ring_count = 0;
@@ -845,7 +937,7 @@ int epi_pop_synthesize(const epi_pop_spec* sp, uint64_t seed, const epi_pop_out*
     for (void* p : {(void*)worker, (void*)size_k, (void*)ends, (void*)nW, (void*)wsz, (void*)wend,
                     (void*)seed_key, (void*)key_sorted, (void*)wkey, (void*)wkey_sorted, (void*)ids,
                     (void*)ids_sorted, (void*)workers, (void*)seed32, tmp})
-      if (p) cudaFree(p);
+      if (p) dfree_now(p);
   };
   int rc = 0;
   rc = rc ? rc : dalloc(&worker, n);
@@ -963,11 +1055,11 @@ int epi_net_attach(epi_ctx* c, const epi_net* net) {
   c->net = *net;
   fill_net_tables(c->ntab, *net, 0);
   for (int i = 0; i < 3; ++i) {
-    if (!c->ntab_dev[i]) CK(cudaMalloc((void**)&c->ntab_dev[i], sizeof(NetTables)));
+    if (!c->ntab_dev[i]) CK(dmalloc((void**)&c->ntab_dev[i], sizeof(NetTables)));
     CK(cudaMemcpy(c->ntab_dev[i], &c->ntab, sizeof(NetTables), cudaMemcpyHostToDevice));
   }
   c->has_net = true;
-  if (!c->net_dev) CK(cudaMalloc((void**)&c->net_dev, sizeof(epi_net)));
+  if (!c->net_dev) CK(dmalloc((void**)&c->net_dev, sizeof(epi_net)));
   CK(cudaMemcpy(c->net_dev, net, sizeof(epi_net), cudaMemcpyHostToDevice));
   // one CSR slot (id rows for fp64 order / export); DEN regenerates past
   // days' contacts instead of keeping a contact log
@@ -982,8 +1074,8 @@ int epi_net_attach(epi_ctx* c, const epi_net* net) {
     k_fill_i32<<<grid_for(c->n, 256), 256>>>(c->died_at, c->n, INT32_MAX);
     CKL();
   }
-  for (auto* p : c->net_entries) cudaFree(p);
-  for (auto* p : c->net_rowlen) cudaFree(p);
+  for (auto* p : c->net_entries) dfree_now(p);
+  for (auto* p : c->net_rowlen) dfree_now(p);
   c->net_entries.assign(slots, nullptr);
   c->net_rowlen.assign(slots, nullptr);
   c->net_slot_step.assign(slots, -1);
@@ -1014,7 +1106,7 @@ int epi_net_attach(epi_ctx* c, const epi_net* net) {
       if (var == 0) v.wcode = nullptr;
       if (var < 2) { v.rin = nullptr; v.rout = nullptr; }
       if (var == 3) v.rout = nullptr;
-      if (!c->wt_dev[par][var]) CK(cudaMalloc((void**)&c->wt_dev[par][var], sizeof(WorkTables)));
+      if (!c->wt_dev[par][var]) CK(dmalloc((void**)&c->wt_dev[par][var], sizeof(WorkTables)));
       CK(cudaMemcpy(c->wt_dev[par][var], &v, sizeof(WorkTables), cudaMemcpyHostToDevice));
     }
   }
@@ -1244,8 +1336,13 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
   const bool has_work = c->net.n_member_slots > 0 && c->net.colleague_draws > 0;
   // csr mode writes messages only in fp32 without a contact log
   const bool msg_only = mode == 0 && precision == EPI_F32 && c->net.row_cap <= MP_MAX_CAP;
+  // Fused days without interventions use the full push tables only where a
+  // persistent run (k_fused_run) can follow, which needs them: elsewhere the
+  // sparse rows measured faster at every size (tools/push_vs_sparse.py:
+  // 200 k agents 6.1 vs 7.1 ms per simulation, 1 M 21.7 vs 35.0 ms).
+  const bool prefer_sparse = mode == 1 && !iv && c->sparse_push && !run_fits(c);
   const bool push_rand = (mode == 1 || msg_only) && c->lo == 0 && c->hi == c->n && c->net.n_agents >= 2 &&
-                         c->net.random_slots == RT_SLOTS && batched(&c->net) && push_fits(c);
+                         c->net.random_slots == RT_SLOTS && batched(&c->net) && push_fits(c) && !prefer_sparse;
   const bool merged = mode == 1 && push_rand && !iv;
   // beyond the push tables (and on partitioned ranks), fused days without
   // interventions push only infectious sources into sparse in-rows
@@ -1429,7 +1526,7 @@ static bool persistent_ok(epi_ctx* c, int32_t mode, int32_t precision) {
 
 static int launch_run(epi_ctx* c, const epi_state* st, int32_t first, int32_t n_days, uint64_t seed,
                       uint16_t* codes0, uint16_t* codes1, int64_t* records, cudaStream_t s) {
-  if (!c->run_barrier) CK(cudaMalloc((void**)&c->run_barrier, sizeof(unsigned)));
+  if (!c->run_barrier) CK(dmalloc((void**)&c->run_barrier, sizeof(unsigned)));
   CK(cudaMemsetAsync(c->run_barrier, 0, sizeof(unsigned), s));
   RunArgs R{};
   R.P = c->P;
@@ -1500,7 +1597,7 @@ static int launch_iv_run(epi_ctx* c, const epi_state* st, int32_t first, int32_t
   if (!c->ivr_hist) rc = dalloc(&c->ivr_hist, (size_t)3 * IV_HIST);
   if (!rc && !c->ivr_tile_hist) rc = dalloc(&c->ivr_tile_hist, (size_t)2 * sm_count() * NUM_BUCKETS);
   if (rc) return rc;
-  if (!c->run_barrier) CK(cudaMalloc((void**)&c->run_barrier, sizeof(unsigned)));
+  if (!c->run_barrier) CK(dmalloc((void**)&c->run_barrier, sizeof(unsigned)));
   CK(cudaMemsetAsync(c->run_barrier, 0, sizeof(unsigned), s));
   CK(cudaMemsetAsync(c->ivr_hist, 0, (size_t)3 * IV_HIST * sizeof(unsigned long long), s));
   IvRunArgs R{};
@@ -1902,18 +1999,18 @@ int epi_refnet_create(const epi_refnet_desc* d, epi_refnet_t** out) {
 
 int epi_refnet_destroy(epi_refnet_t* r) {
   if (!r) return 0;
-  cudaFree(r->sc.live_members);
-  cudaFree(r->sc.occ_live);
-  cudaFree(r->sc.stub_count);
-  cudaFree(r->sc.stub_off);
-  cudaFree(r->sc.table);
-  cudaFree(r->sc.counter);
-  cudaFree(r->sc.stub_owner);
-  cudaFree(r->sc.pair_uv);
-  cudaFree(r->sc.ws_losers);
-  cudaFree(r->sc.n_losers);
-  cudaFree(r->sc.links_done);
-  cudaFree(r->scan_tmp);
+  dfree_now(r->sc.live_members);
+  dfree_now(r->sc.occ_live);
+  dfree_now(r->sc.stub_count);
+  dfree_now(r->sc.stub_off);
+  dfree_now(r->sc.table);
+  dfree_now(r->sc.counter);
+  dfree_now(r->sc.stub_owner);
+  dfree_now(r->sc.pair_uv);
+  dfree_now(r->sc.ws_losers);
+  dfree_now(r->sc.n_losers);
+  dfree_now(r->sc.links_done);
+  dfree_now(r->scan_tmp);
   delete r;
   return 0;
 }

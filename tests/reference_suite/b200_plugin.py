@@ -50,3 +50,36 @@ def pytest_configure(config):
 
 def pytest_terminal_summary(terminalreporter):
     terminalreporter.write_line(f"b200_plugin: GpuEngine instances built by the suite: {CALLS['engines']}")
+
+
+# Diagnostics (off by default): B200_PLUGIN_BENCH_LOG=<file> appends every
+# runner.bench report (engine and oracle) with its wall time to <file>.
+import os as _os
+
+if _os.environ.get("B200_PLUGIN_BENCH_LOG"):
+    _bench = epivec.runner.bench
+
+    import gc as _gc
+    import time as _time
+    _gc_log = []
+    _gc_t = {}
+
+    def _gc_cb(phase, info):
+        if phase == "start":
+            _gc_t["t"] = _time.perf_counter()
+        else:
+            dt = _time.perf_counter() - _gc_t.get("t", _time.perf_counter())
+            if dt > 0.005:
+                _gc_log.append(f"gc gen{info['generation']} {dt * 1e3:.1f} ms collected {info['collected']}")
+
+    _gc.callbacks.append(_gc_cb)
+
+    def _logged_bench(config, use_oracle=False):
+        del _gc_log[:]
+        rep = _bench(config, use_oracle=use_oracle)
+        with open(_os.environ["B200_PLUGIN_BENCH_LOG"], "a") as f:
+            f.write(f"{'oracle' if use_oracle else 'engine'} n={rep.n_agents} steps={rep.steps} "
+                    f"wall={rep.wall_seconds * 1e3:.1f} ms {'; '.join(_gc_log)}\n")
+        return rep
+
+    epivec.runner.bench = _logged_bench
