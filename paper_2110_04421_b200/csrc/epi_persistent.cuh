@@ -261,8 +261,9 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_fused_run(RunArgs R, epi
           add_src(acc[1], edges, T.factor, wi[j]);
         }
         if (n >= 2) {
+          unsigned eo = 0;
 #pragma unroll
-          for (int q = 0; q < 4; ++q) add_src(acc[2], edges, T.factor, co0[q]);
+          for (int q = 0; q < 4; ++q) add_src(acc[2], eo, T.factor, co0[q]);
           for (int j0 = 4; j0 < nbe; j0 += 4) {
             const uint4 o = ro[j0 >> 2];
             const uint32_t po[4] = {o.x, o.y, o.z, o.w};
@@ -271,9 +272,14 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_fused_run(RunArgs R, epi
             for (int q = 0; q < 4; ++q)
               co[q] = (j0 + q < nbe && po[q] != self) ? LDM(codes + po[q]) : (uint16_t)CODE_DEAD;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) add_src(acc[2], edges, T.factor, co[q]);
+            for (int q = 0; q < 4; ++q) add_src(acc[2], eo, T.factor, co[q]);
           }
-          add_rin_row(acc[2], edges, T.factor, in0, in1);
+          // random in-edges between alive agents total the random out-edges
+          // (each is one (source, slot) pair seen from either end): counted as
+          // twice the out-partners, so the rows may be sparse (infectious only)
+          edges += 2u * eo;
+          unsigned present = 0;
+          add_rin_row(acc[2], present, T.factor, in0, in1);
         }
         const float tot = acc[0] * T.bfac[0] + acc[1] * T.bfac[1] + acc[2] * T.bfac[2];
         if (h.stage == S_SUS && !(R.P->sterilizing && h.immune)) lam = (double)(tot * T.sfac[h.age]);
@@ -333,7 +339,10 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_fused_run(RunArgs R, epi
         const uint32_t y = walk_fwd(src, D.rk_next[j], R.dn);
         out_s[(warp * 32 + l) * RUN_OUT_STRIDE + j] = y;
         if (d + 1 == R.n_days) Wn.rout[(size_t)src * RT_SLOTS + j] = y;
-        if (y != src) Wn.rin[(size_t)y * RT_SLOTS + j] = cn_s[warp][l] | CODE_PRESENT;
+        // only infectious sources (code byte != 0) feed a lambda; the last
+        // day's rows are complete (the per-day path counts their present bits)
+        if (y != src && ((cn_s[warp][l] & 0xFF) != 0 || d + 1 == R.n_days))
+          Wn.rin[(size_t)y * RT_SLOTS + j] = cn_s[warp][l] | CODE_PRESENT;
       }
     }
     cb = cn;
