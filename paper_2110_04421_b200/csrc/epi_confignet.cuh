@@ -533,6 +533,15 @@ __device__ __forceinline__ void add_rin_row(float& acc, unsigned& edges, const f
   }
   edges += (pres & 0xFFFFu) + (pres >> 16);
 }
+// A sparse in-row (infectious in-partners only, the rest 0): the same
+// slot-ordered adds, skipped when the row is empty -- sixteen additions of
+// +0.0f leave a sum >= +0 unchanged, so the result is bitwise add_rin_row's.
+__device__ __forceinline__ void add_rin_row_sparse(float& acc, const float* __restrict__ factor, uint4 in0,
+                                                   uint4 in1) {
+  if ((in0.x | in0.y | in0.z | in0.w | in1.x | in1.y | in1.z | in1.w) == 0u) return;
+  unsigned present = 0;
+  add_rin_row(acc, present, factor, in0, in1);
+}
 
 // Branch-free per-kind sums of for_each_in_code without push rows (the
 // fused day kernel of partitioned ranks and of runs too large for the push
@@ -661,8 +670,7 @@ __device__ __forceinline__ void sparse_kind_sums(const epi_net& net, const PermK
     for (int q = 0; q < 4; ++q) add_src(acc[2], eo, factor, co[q]);
   }
   edges += 2u * eo;
-  unsigned present = 0;                          // (the row's present bits: infectious in-partners only)
-  add_rin_row(acc[2], present, factor, in0, in1);
+  add_rin_row_sparse(acc[2], factor, in0, in1);
 }
 
 // Push-table form of for_each_in_code for the fused day kernel, written so

@@ -318,15 +318,17 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
             // (each is one (source, slot) pair seen from either end): counted as
             // twice the out-partners, so the rows may be sparse (infectious only)
             edges += 2u * eo;
-            unsigned present = 0;
-            add_rin_row(acc[2], present, T.factor, in0, in1);
+            add_rin_row_sparse(acc[2], T.factor, in0, in1);
           }
           const float tot = acc[0] * T.bfac[0] + acc[1] * T.bfac[1] + acc[2] * T.bfac[2];
           if (h.stage == S_SUS && !(A.P->sterilizing && h.immune)) lam = (double)(tot * T.sfac[h.age]);
         }
-        uint4* rw = (uint4*)(W.rin + (size_t)b * RT_SLOTS);
-        rw[0] = make_uint4(0, 0, 0, 0);
-        rw[1] = make_uint4(0, 0, 0, 0);
+        // (only infectious in-partners write it: most rows are already empty)
+        if ((in0.x | in0.y | in0.z | in0.w | in1.x | in1.y | in1.z | in1.w) != 0u) {
+          uint4* rw = (uint4*)(W.rin + (size_t)b * RT_SLOTS);
+          rw[0] = make_uint4(0, 0, 0, 0);
+          rw[1] = make_uint4(0, 0, 0, 0);
+        }
       }
       unsigned ev = 0;
       if (valid) probe_lambda(R.A0.probe, t, b, lam);
