@@ -518,6 +518,24 @@ __device__ __forceinline__ void add_src(float& acc, unsigned& edges, const float
   acc += factor[c & 0xFF];
   edges += 1u - ((unsigned)c >> 15);
 }
+// A group of K sources in visit order: the edge count branch-free, the factor
+// adds only when some source of the group is infectious (code byte != 0).
+// Skipped adds are all +0.0f on a sum >= +0, so the result is bitwise that
+// of K add_src calls; most groups of most days have no infectious source.
+template <int K>
+__device__ __forceinline__ void add_src_group(float& acc, unsigned& edges, const float* __restrict__ factor,
+                                              const uint16_t* c) {
+  unsigned any = 0;
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    any |= c[i];
+    edges += 1u - ((unsigned)c[i] >> 15);
+  }
+  if (any & 0xFFu) {
+#pragma unroll
+    for (int i = 0; i < K; ++i) acc += factor[c[i] & 0xFF];
+  }
+}
 // A push row (RT_SLOTS codes as two uint4, low half of each word first): the
 // same adds in slot order; the present bits (14) of both halves of a word are
 // counted together in 16-bit lanes of one register.

@@ -289,21 +289,21 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
             }
           }
           float acc[3] = {0.f, 0.f, 0.f};
-#pragma unroll
-          for (int i = 0; i < HH; ++i) add_src(acc[0], edges, T.factor, hc[i]);
+          add_src_group<HH>(acc[0], edges, T.factor, hc);
           for (int i = HH; i < sz; ++i) {
             if (start + i == b) continue;
             add_src(acc[0], edges, T.factor, hh_code(i));
           }
+          uint16_t wio[2 * DR];                 // visit order: out, in per draw
 #pragma unroll
           for (int j = 0; j < DR; ++j) {
-            add_src(acc[1], edges, T.factor, wo[j]);
-            add_src(acc[1], edges, T.factor, wi[j]);
+            wio[2 * j] = wo[j];
+            wio[2 * j + 1] = wi[j];
           }
+          add_src_group<2 * DR>(acc[1], edges, T.factor, wio);
           if (n >= 2) {
             unsigned eo = 0;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) add_src(acc[2], eo, T.factor, co0[q]);
+            add_src_group<4>(acc[2], eo, T.factor, co0);
             for (int j0 = 4; j0 < nbe; j0 += 4) {
               const uint4 o = ro[j0 >> 2];
               const uint32_t po[4] = {o.x, o.y, o.z, o.w};
@@ -311,8 +311,7 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
 #pragma unroll
               for (int q = 0; q < 4; ++q)
                 co[q] = (j0 + q < nbe && po[q] != self) ? LDM(codes + po[q]) : (uint16_t)CODE_DEAD;
-#pragma unroll
-              for (int q = 0; q < 4; ++q) add_src(acc[2], eo, T.factor, co[q]);
+              add_src_group<4>(acc[2], eo, T.factor, co);
             }
             // random in-edges between alive agents total the random out-edges
             // (each is one (source, slot) pair seen from either end): counted as
