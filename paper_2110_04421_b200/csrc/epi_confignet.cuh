@@ -642,7 +642,7 @@ __device__ __forceinline__ void sparse_kind_sums(const epi_net& net, const PermK
                                                  const Radix& dn, const WorkTables* __restrict__ wt,
                                                  const uint16_t* __restrict__ codes, int64_t b, uint16_t code_b,
                                                  const float* __restrict__ factor, float acc[3],
-                                                 unsigned& edges) {
+                                                 unsigned& edges, bool& row_used) {
   // the rows stream through L2 once a day (640 MB at 10 M agents): evict-first,
   // so they do not push the codes and the state out
   const uint4* ri = (const uint4*)(wt->rin + (size_t)b * RT_SLOTS);
@@ -688,6 +688,7 @@ __device__ __forceinline__ void sparse_kind_sums(const epi_net& net, const PermK
     for (int q = 0; q < 4; ++q) add_src(acc[2], eo, factor, co[q]);
   }
   edges += 2u * eo;
+  row_used = (in0.x | in0.y | in0.z | in0.w | in1.x | in1.y | in1.z | in1.w) != 0u;
   add_rin_row_sparse(acc[2], factor, in0, in1);
 }
 

@@ -1134,6 +1134,7 @@ __global__ void __launch_bounds__(128, 8) k_fused_step(StepArgs A, epi_net net, 
     if (valid) h = load_hot(A.st, b);      // issued before the gather's loads
     if (valid) {
       const uint16_t cb = codes[b];
+      bool row_used = true;                // (sparse rows: cleared only when non-empty)
       if (!code_dead(cb)) {
         // one sum per network kind (the kind is a constant at every visit),
         // scaled by B[kind] once
@@ -1141,7 +1142,7 @@ __global__ void __launch_bounds__(128, 8) k_fused_step(StepArgs A, epi_net net, 
         if (push == 1)
           push_kind_sums(net, wt, codes, b, cb, T.factor, acc, edges);
         else if (push == 2)
-          sparse_kind_sums(net, NT.rk, dn, wt, codes, b, cb, T.factor, acc, edges);
+          sparse_kind_sums(net, NT.rk, dn, wt, codes, b, cb, T.factor, acc, edges, row_used);
         else
           code_kind_sums(net, NT.rk, dn, wt, codes, b, cb, T.factor, acc, edges);
         const float tot = acc[0] * T.bfac[0] + acc[1] * T.bfac[1] + acc[2] * T.bfac[2];
@@ -1149,8 +1150,10 @@ __global__ void __launch_bounds__(128, 8) k_fused_step(StepArgs A, epi_net net, 
       }
       if (push == 2) {                     // (sparse rows: streamed, evict-first)
         uint4* row = (uint4*)(wt->rin + (size_t)b * RT_SLOTS);
-        __stcs(row, make_uint4(0, 0, 0, 0));
-        __stcs(row + 1, make_uint4(0, 0, 0, 0));
+        if (row_used) {
+          __stcs(row, make_uint4(0, 0, 0, 0));
+          __stcs(row + 1, make_uint4(0, 0, 0, 0));
+        }
       } else {
         clear_rin_row(wt, b);
       }
