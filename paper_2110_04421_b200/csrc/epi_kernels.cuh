@@ -1230,27 +1230,35 @@ __global__ void __launch_bounds__(256) k_day_tables(epi_net net, NetKeys nk, Wor
   if (blockIdx.x == 0 && rec && threadIdx.x < EPI_REC_LEN) rec[threadIdx.x] = 0;
   const int draws = net.colleague_draws;
   if ((int)blockIdx.x < wblocks) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < net.n_member_slots;
-         i += (int64_t)wblocks * blockDim.x) {
-      if (draws <= 0) break;
-      const int32_t c = net.wp_members[i];
-      const int w = net.wp_id[c];
+    // one warp per workplace (m <= 255 members, lanes over its positions):
+    // the workplace's size, base and permutation keys once, then per position
+    // q the member at sigma(q) -- two dependent loads instead of four per slot
+    if (draws <= 0) return;
+    const int warp = threadIdx.x >> 5, lane = lane_id();
+    const int64_t wwarps = (int64_t)wblocks * (blockDim.x >> 5);
+    for (int64_t w = blockIdx.x * (int64_t)(blockDim.x >> 5) + warp; w < net.n_workplaces; w += wwarps) {
       const int base = net.wp_base[w];
       const int m = net.wp_size[w];
-      const uint32_t q = (uint32_t)(i - base);
-      int32_t who = c;
-      if (m >= 2) {
-        const PermKeys K = work_keys(nk.wperm, w);
-        const uint32_t loc = walk_fwd(q, K, NT.wrad[m]);
-        who = net.wp_members[base + loc];
-        wt.pos_of[base + loc] = (uint8_t)q;
-        for (int j = (int)q; j < draws; j += m)
-          wt.shift[(size_t)w * draws + j] = (uint8_t)work_shift(nk.wshift, w, j, m);
-      } else {
-        wt.pos_of[i] = 0;
+      if (m < 2) {
+        if (lane < m) {
+          const int32_t c = net.wp_members[base + lane];
+          wt.pos_of[base + lane] = 0;
+          wt.member_at_pos[base + lane] = c;
+          if (wt.wcode) wt.wcode[base + lane] = codes[c];
+        }
+        continue;
       }
-      wt.member_at_pos[i] = who;
-      if (wt.wcode) wt.wcode[i] = codes[who];
+      const PermKeys K = work_keys(nk.wperm, (int)w);
+      const Radix d = NT.wrad[m];
+      for (int q = lane; q < m; q += 32) {
+        const uint32_t loc = walk_fwd((uint32_t)q, K, d);
+        const int32_t who = net.wp_members[base + loc];
+        wt.pos_of[base + loc] = (uint8_t)q;
+        for (int j = q; j < draws; j += m)
+          wt.shift[(size_t)w * draws + j] = (uint8_t)work_shift(nk.wshift, (int)w, j, m);
+        wt.member_at_pos[base + q] = who;
+        if (wt.wcode) wt.wcode[base + q] = codes[who];
+      }
     }
     return;
   }
