@@ -1263,7 +1263,7 @@ static int sigma_day_tables(epi_ctx* c, int32_t step, uint64_t seed, const uint1
                     sigma_only(par), codes_cur, c->lo, c->hi, wblocks, (const NetTables*)c->ntab_dev[step % 3],
                     c->ntab_dev[(step + 1) % 3], key_prefix(seed, step + 1, P_NET_RPERM), rec_zero));
   }
-  CK(launch_pdl_w(&c->hot, k_wcode, dim3(grid_for(c->net.n_member_slots, 256, 4)), dim3(256), 0, s,
+  CK(launch_pdl_w(&c->hot, k_wcode, dim3(grid_for(c->net.n_member_slots, 256 * 4, 8)), dim3(256), 0, s,
                   (int64_t)c->net.n_member_slots, (const int32_t*)c->wt_host[par].member_at_pos, codes_cur,
                   c->wt_host[par].wcode));
   if (!c->side) {

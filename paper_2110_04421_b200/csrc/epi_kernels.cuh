@@ -1201,8 +1201,20 @@ __global__ void __launch_bounds__(256) k_wcode(int64_t n_slots, const int32_t* _
                                                const uint16_t* __restrict__ codes, uint16_t* __restrict__ wcode) {
   pdl_wait();
   pdl_trigger();
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_slots; i += (int64_t)gridDim.x * blockDim.x)
-    wcode[i] = codes[member_at_pos[i]];
+  // four slots per thread per pass, every load of a level issued before any
+  // use (the code gather is one dependent level after member_at_pos)
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < n_slots; i0 += 4 * stride) {
+    int32_t who[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) who[u] = i0 + u * stride < n_slots ? member_at_pos[i0 + u * stride] : -1;
+    uint16_t cw[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) cw[u] = who[u] >= 0 ? codes[who[u]] : (uint16_t)0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (who[u] >= 0) wcode[i0 + u * stride] = cw[u];
+  }
 }
 
 // Per-day tables.  Blocks [0, wblocks) own the workplace member slots (one
