@@ -477,7 +477,7 @@ static bool push_fits(const epi_ctx* c) {
 static bool run_fits(const epi_ctx* c) {
   const int64_t sms = sm_count();
   const int64_t threads = ((c->n + sms - 1) / sms + 31) / 32 * 32;     // (run_threads)
-  return c->persistent && c->net.colleague_draws <= 8 && threads <= RUN_MAX_AGENTS;
+  return c->persistent && c->net.colleague_draws <= 8 && threads <= RUN_BIG_AGENTS;
 }
 
 // k_msg_pass: per-warp segment scratch
@@ -1514,14 +1514,32 @@ static bool persistent_ok(epi_ctx* c, int32_t mode, int32_t precision) {
   if (partitioned(c) || c->net.n_agents < 2 || c->net.random_slots != RT_SLOTS || !batched(&c->net) ||
       !push_fits(c) || c->net.colleague_draws > 8)
     return false;
-  static int per_sm = -1;
-  if (per_sm < 0 &&
-      (cudaFuncSetAttribute(k_fused_run, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RUN_DYN_SMEM) !=
-           cudaSuccess ||
-       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_fused_run, RUN_MAX_THREADS, RUN_DYN_SMEM) !=
-           cudaSuccess))
-    per_sm = 0;
-  return per_sm >= 1 && run_threads(c->n) <= RUN_MAX_AGENTS;
+  const int64_t threads = run_threads(c->n);
+  if (threads > RUN_BIG_AGENTS) return false;
+  const bool big = threads > RUN_MAX_AGENTS;
+  static int per_sm[2] = {-1, -1};
+  int& ps = per_sm[big ? 1 : 0];
+  if (ps < 0) {
+    cudaError_t e;
+    if (big) {
+      e = cudaFuncSetAttribute(k_fused_run<RUN_BIG_THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)run_dyn_smem<RUN_BIG_THREADS>());
+      if (e == cudaSuccess)
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, k_fused_run<RUN_BIG_THREADS>, RUN_BIG_THREADS,
+                                                          run_dyn_smem<RUN_BIG_THREADS>());
+    } else {
+      e = cudaFuncSetAttribute(k_fused_run<RUN_MAX_THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)run_dyn_smem<RUN_MAX_THREADS>());
+      if (e == cudaSuccess)
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, k_fused_run<RUN_MAX_THREADS>, RUN_MAX_THREADS,
+                                                          run_dyn_smem<RUN_MAX_THREADS>());
+    }
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      ps = 0;
+    }
+  }
+  return ps >= 1;
 }
 
 static int launch_run(epi_ctx* c, const epi_state* st, int32_t first, int32_t n_days, uint64_t seed,
@@ -1547,8 +1565,9 @@ static int launch_run(epi_ctx* c, const epi_state* st, int32_t first, int32_t n_
   R.probe = c->probe;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)sm_count());
+  const bool big = run_threads(c->n) > RUN_MAX_AGENTS;      // (the 1024-thread variant)
   cfg.blockDim = dim3((unsigned)run_threads(c->n) + 32);     // + the service warp
-  cfg.dynamicSmemBytes = RUN_DYN_SMEM;
+  cfg.dynamicSmemBytes = big ? run_dyn_smem<RUN_BIG_THREADS>() : run_dyn_smem<RUN_MAX_THREADS>();
   cfg.stream = s;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeCooperative;     // every block resident: the grid barrier is safe
@@ -1564,7 +1583,8 @@ static int launch_run(epi_ctx* c, const epi_state* st, int32_t first, int32_t n_
     cfg.numAttrs = 2;
   }
   cfg.attrs = attr;
-  CK(cudaLaunchKernelEx(&cfg, k_fused_run, R, c->net));
+  if (big) CK(cudaLaunchKernelEx(&cfg, k_fused_run<RUN_BIG_THREADS>, R, c->net));
+  else CK(cudaLaunchKernelEx(&cfg, k_fused_run<RUN_MAX_THREADS>, R, c->net));
   c->merged_ready = first + n_days;
   c->sparse_ready = -1;
   c->sparse_clean = -1;

@@ -109,6 +109,11 @@ constexpr int RUN_MAX_THREADS = RUN_MAX_AGENTS + 32;
 // words: a quarter warp's 16-byte row reads hit distinct banks.
 constexpr int RUN_OUT_STRIDE = RT_SLOTS + 4;
 constexpr size_t RUN_DYN_SMEM = (size_t)RUN_MAX_AGENTS * RUN_OUT_STRIDE * sizeof(uint32_t);
+// k_fused_run also comes as a 1024-thread block (992 agents per SM, at most 64
+// registers) for populations between 104 k and 147 k agents
+constexpr int RUN_BIG_THREADS = 1024;
+constexpr int RUN_BIG_AGENTS = RUN_BIG_THREADS - 32;
+template <int MAXT> constexpr size_t run_dyn_smem() { return (size_t)(MAXT - 32) * RUN_OUT_STRIDE * sizeof(uint32_t); }
 // loads of data written during the run: plain (coherent) global loads; the
 // grid barrier orders them after the writers' stores
 template <class T> __device__ __forceinline__ T LDM(const T* p) { return *p; }
@@ -127,15 +132,16 @@ __device__ __forceinline__ uint2 day_shifts(uint64_t wshift_prefix, int w, int m
   return make_uint2(lo, hi);
 }
 
-__global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_fused_run(RunArgs R, epi_net net) {
+template <int MAXT>
+__global__ void __launch_bounds__(MAXT, 1) k_fused_run(RunArgs R, epi_net net) {
   constexpr int HH = 8, DR = 8;
   __shared__ MsgTables T;
   __shared__ RecAcc racc[2];               // record rows by day parity
-  __shared__ int excl_s[RUN_MAX_THREADS / 32][32];
-  __shared__ uint16_t cn_s[RUN_MAX_THREADS / 32][32];
-  __shared__ uint8_t own_s[RUN_MAX_THREADS / 32][32 * RT_SLOTS];
+  __shared__ int excl_s[MAXT / 32][32];
+  __shared__ uint16_t cn_s[MAXT / 32][32];
+  __shared__ uint8_t own_s[MAXT / 32][32 * RT_SLOTS];
   __shared__ DayKeys dk[2];                // keys by day parity
-  __shared__ uint16_t hcode_s[2][RUN_MAX_AGENTS];   // the block's codes by day parity
+  __shared__ uint16_t hcode_s[2][MAXT - 32];     // the block's codes by day parity
   extern __shared__ uint4 run_dyn_s[];
   uint32_t* const out_s = (uint32_t*)run_dyn_s;    // [agent][RUN_OUT_STRIDE]
   load_msg_tables(T, R.mt);

@@ -35,7 +35,8 @@ def _same(a, b):
         assert np.array_equal(getattr(ha, c), getattr(hb, c)), c
 
 
-@pytest.mark.parametrize("cfg,n,seeds", [(1, 100_000, 100), (0, 10_000, 10), (1, 6007, 300), (1, 129, 20)])
+@pytest.mark.parametrize("cfg,n,seeds", [(1, 100_000, 100), (0, 10_000, 10), (1, 6007, 300), (1, 129, 20),
+                                         (1, 130_000, 130)])     # (the 1024-thread variant: > 104 k agents)
 def test_persistent_run_equals_per_day(cfg, n, seeds):
     a, b = _pair(cfg, n, seeds, 21, 180)
     assert a.uses_persistent_run() and not b.uses_persistent_run()
@@ -126,8 +127,8 @@ def test_fused_intervention_day_graph_replay():
 
 
 def test_persistent_only_where_one_wave_fits():
-    """Above 148 x 704 agents (one agent per thread, one block per SM) the
-    run falls back to one kernel per day."""
+    """Above 148 x 992 agents (one agent per thread, one 1024-thread block
+    per SM) the run falls back to one kernel per day."""
     spec = ConfigNetworkSpec.config(1, n_agents=150_000, initial_infections=50)
     pop = synthesize(spec, 5)
     sim = ConfigSimulation(pop, default_disease(), default_progression(), InterventionConfig(), 1,
