@@ -150,6 +150,11 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
   uint64_t den_pref = 0;
   __syncthreads();
   uint2 shp = works ? day_shifts(dk[0].wshift, w, m) : make_uint2(0, 0);   // the day's colleague shifts
+  // the agent's hot state for the coming day: only its own thread writes it,
+  // so it is reloaded once the day's last write (doses, transition
+  // scheduling) is done -- between the end barrier's arrive and wait
+  AgentHot hp{};
+  if (valid) hp = load_hot(st, b);
   for (int d = 0; d < R.n_days; ++d) {
     const int t = R.first_step + d;
     const int par = t & 1;
@@ -246,8 +251,7 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
         }
       }
     } else {
-      AgentHot h{};
-      if (valid) h = load_hot(st, b);
+      AgentHot h = hp;
       age = h.age;
       unsigned edges = 0;
       double lam = 0.0;
@@ -494,6 +498,7 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
         schedule_pending(A.P, st, A.K, t, A.tau_lut, b, pend, hs);
       }
       if (works) shp = day_shifts(dk[d3n].wshift, w, m);
+      if (valid) hp = load_hot(st, b);
       ++bar;
       if (threadIdx.x == 0) {
         unsigned v;
@@ -510,6 +515,7 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
         schedule_pending(A.P, st, A.K, t, A.tau_lut, b, pend, hs);
       }
       if (d + 1 < R.n_days && works) shp = day_shifts(dk[d3n].wshift, w, m);
+      if (d + 1 < R.n_days && valid) hp = load_hot(st, b);
     }
   }
   if (R.den) {
