@@ -59,21 +59,30 @@ struct RunArgs {
   LamProbe probe;
 };
 
-// Grid barrier between days: one arrival per block (acq_rel atomic on one
+// Grid barrier between days: one arrival per block (release reduction on one
 // counter) after a bar.sync, so every store of the block's day precedes it;
 // thread 0 polls with acquire loads and the closing bar.sync extends the
 // order to the block.  The last block to arrive releases the grid at once
 // (measured 1.3 us from its arrival).  One block per SM keeps the arrivals at
 // 148 (1.2 us per barrier, tools/micro/grid_barrier.cu; cg::grid.sync with 6
 // blocks per SM: 1.9 us).
+// Arrival: a release reduction (the block's stores of the day, ordered
+// before it by the bar.sync, precede it; no value comes back).
+__device__ __forceinline__ void grid_arrive(unsigned* bar) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+}
+// Wait: acquire loads until every block has arrived `target` times in all.
+__device__ __forceinline__ void grid_wait(const unsigned* bar, unsigned target) {
+  unsigned v;
+  do {
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+  } while (v < target);
+}
 __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned target) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    unsigned v;
-    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(v) : "l"(bar) : "memory");
-    do {
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
-    } while (v < target);
+    grid_arrive(bar);
+    grid_wait(bar, target);
   }
   __syncthreads();
 }
@@ -358,22 +367,14 @@ __global__ void __launch_bounds__(MAXT, 1) k_fused_run(RunArgs R, epi_net net) {
       // grid barrier, split: tomorrow's shifts (keys ready since the
       // service warp's day) are hashed between arrive and wait
       __syncthreads();
-      if (threadIdx.x == 0) {
-        unsigned v;
-        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(v) : "l"(R.barrier) : "memory");
-      }
+      if (threadIdx.x == 0) grid_arrive(R.barrier);
       if (pend >= 0) schedule_pending(R.P, R.st, D.K, t, R.tau_lut, b, pend, h);   // feeds tomorrow's check
       if (works) {
         shp = day_shifts(dk[(d + 1) & 1].wshift, w, m);
         q_nx = walk_inv((uint32_t)loc, work_keys(dk[(d + 1) & 1].wperm_next, w), rm);
       }
       if (valid) cnt_nx = random_count(net, dk[(d + 1) & 1].rcount_next, b);
-      if (threadIdx.x == 0) {
-        unsigned v;
-        do {
-          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(R.barrier) : "memory");
-        } while (v < (unsigned)(d + 1) * gridDim.x);
-      }
+      if (threadIdx.x == 0) grid_wait(R.barrier, (unsigned)(d + 1) * gridDim.x);
       __syncthreads();
     } else if (pend >= 0) {
       schedule_pending(R.P, R.st, D.K, t, R.tau_lut, b, pend, h);

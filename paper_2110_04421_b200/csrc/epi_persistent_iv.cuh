@@ -487,10 +487,7 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
       // end of day, split: the plan, the doses and tomorrow's shifts between
       // arrive and wait
       __syncthreads();
-      if (threadIdx.x == 0) {
-        unsigned v;
-        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(v) : "l"(R.barrier) : "memory");
-      }
+      if (threadIdx.x == 0) grid_arrive(R.barrier);
       if (!service) finish_day();
       if (pend >= 0) {                     // feeds tomorrow's transition check
         AgentHot hs{};
@@ -500,12 +497,7 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
       if (works) shp = day_shifts(dk[d3n].wshift, w, m);
       if (valid) hp = load_hot(st, b);
       ++bar;
-      if (threadIdx.x == 0) {
-        unsigned v;
-        do {
-          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(R.barrier) : "memory");
-        } while (v < bar * gridDim.x);
-      }
+      if (threadIdx.x == 0) grid_wait(R.barrier, bar * gridDim.x);
       __syncthreads();
     } else {
       if (!service) finish_day();
