@@ -287,3 +287,35 @@ def test_engine_refuses_steps_after_invalidation():
     eng.invalidate("realizer failed at step 0: edge output capacity exceeded")
     with pytest.raises(InvariantViolation, match="invalid"):
         eng.step(StepGraph.empty(0))
+
+
+def test_recycled_context_buffers_replay_bitwise():
+    """Contexts return their device buffers to a process-wide cache on
+    destruction and the next context of the same sizes reuses them
+    (epi_destroy): the reference trajectory with every intervention replays
+    bitwise on engines built one after another, each on buffers the previous
+    one left dirty, with engines of other sizes built in between."""
+    import gc
+    tr = Trajectory("alliv")
+    for rep in range(4):
+        cols = tr.initial_cols()
+        eng = GpuEngine(cols, tr.disease, tr.table, tr.iv, tr.seed)
+        for step in range(tr.horizon):
+            ev = eng.step(tr.graph(step))
+            got = [ev.n_edges, ev.new_infections, ev.deaths, ev.hospitalizations,
+                   ev.tests_administered, ev.doses_given, ev.notifications_sent]
+            assert got == tr.events[step].tolist(), f"rep {rep}: events differ at step {step}"
+            compare_state(cols, tr, step)
+        del eng
+        gc.collect()
+        # engines of other sizes in between, stepped once (their dirty
+        # buffers join the cache too)
+        rng = np.random.default_rng(rep)
+        for n in (17, 300 + rep):
+            other = AgentColumns.allocate(n)
+            e2 = GpuEngine(other, tr.disease, tr.table, tr.iv, tr.seed)
+            src = rng.integers(0, n, 4 * n).astype(np.int32)
+            dst = (src + 1 + rng.integers(0, n - 1, 4 * n)) % n
+            e2.step(StepGraph(0, src, dst.astype(np.int32), np.zeros(4 * n, np.int8)))
+            del e2
+        gc.collect()
