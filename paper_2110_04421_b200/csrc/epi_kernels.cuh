@@ -184,6 +184,20 @@ struct AgentHot {
   int stage, immune, age, next_stage;
   int32_t nta, infected_at, q_until;
 };
+// The same fields read once per day as a stream (evict-first in L2: at 10 M
+// agents the random gathers' tables -- codes, colleague positions and codes --
+// should keep L2, not the agents' own columns).
+__device__ __forceinline__ AgentHot load_hot_stream(const epi_state& st, int64_t a) {
+  AgentHot h;
+  h.stage = __ldcs(st.stage + a);
+  h.immune = __ldcs(st.immune + a);
+  h.age = __ldcs(st.age_band + a);
+  h.next_stage = __ldcs(st.next_stage + a);
+  h.nta = __ldcs(st.next_transition_at + a);
+  h.infected_at = __ldcs(st.infected_at + a);
+  h.q_until = __ldcs(st.quarantine_until + a);
+  return h;
+}
 __device__ __forceinline__ AgentHot load_hot(const epi_state& st, int64_t a) {
   AgentHot h;
   h.stage = st.stage[a];
@@ -1131,7 +1145,7 @@ __global__ void __launch_bounds__(128, 8) k_fused_step(StepArgs A, epi_net net, 
     unsigned edges = 0;
     double lam = 0.0;
     AgentHot h{};
-    if (valid) h = load_hot(A.st, b);      // issued before the gather's loads
+    if (valid) h = push == 2 ? load_hot_stream(A.st, b) : load_hot(A.st, b);   // before the gather's loads
     if (valid) {
       const uint16_t cb = codes[b];
       bool row_used = true;                // (sparse rows: cleared only when non-empty)
