@@ -169,3 +169,37 @@ def test_message_pass_fuzz_within_1e5(seed):
     assert np.all(np.abs(got[nz] - ref[nz]) <= 1e-5 * ref[nz])
     assert np.all(got[~nz] == 0)
     assert int(rec[19]) == len(src)
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_sparse_rows_fuzz_bitwise(seed):
+    """Sparse in-rows (infectious sources only, in-edges counted from the
+    out-edges) on random network specs and dispersed epidemics: 40 fused days
+    bitwise equal -- records, codes, stages -- to the inverse bijections and
+    to the full push tables (persistent run), whole population and 2
+    emulated ranks."""
+    from paper_2110_04421_b200.defaults import default_disease
+    from paper_2110_04421_b200.partition import run_threaded
+    rng = np.random.default_rng(900 + seed)
+    hh = tuple(sorted(set(int(x) for x in rng.integers(1, 12, 3))))
+    probs = rng.dirichlet(np.ones(len(hh)))
+    spec = ConfigNetworkSpec(
+        n_agents=int(rng.choice([64, 999, 4096, 20011])),
+        household_sizes=hh, household_probs=tuple(float(p) for p in probs / probs.sum()),
+        worker_bands=tuple(int(b) for b in rng.choice(9, int(rng.integers(0, 9)), replace=False)),
+        wp_min=int(rng.integers(2, 20)), wp_max=int(rng.integers(20, 255)),
+        colleague_draws=int(rng.choice([0, 1, 4, 8])),
+        random_mean=float(rng.uniform(0, 12)), random_slots=16,
+        initial_infections=int(rng.integers(1, 60)))
+    pop = synthesize(spec, int(rng.integers(0, 2**62)))
+    d, t, iv = default_disease(), default_progression(), InterventionConfig()
+    seed_sim = int(rng.integers(0, 2**63))
+    mk = lambda **kw: ConfigSimulation(pop, d, t, iv, seed_sim, mode="fused", horizon=40, **kw)
+    full, inv, sp = mk(), mk(push_max=0, sparse_push=False), mk(push_max=0)
+    for s in (full, inv, sp):
+        s.run()
+    for s in (full, inv):
+        assert np.array_equal(sp.rec.cpu().numpy(), s.rec.cpu().numpy())
+        assert torch.equal(sp._codes_buf, s._codes_buf)
+    _, rec2 = run_threaded(pop, d, t, iv, seed_sim, 2, 40, mode="fused")
+    assert np.array_equal(rec2.cpu().numpy(), sp.rec.cpu().numpy())
