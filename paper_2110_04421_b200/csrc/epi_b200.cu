@@ -314,6 +314,7 @@ struct epi_ctx {
   unsigned long long* ivr_hist = nullptr;  // k_iv_run: [3][NUM_BUCKETS + 1] (+ active count)
   unsigned* ivr_tile_hist = nullptr;       // k_iv_run: [2][SMs][NUM_BUCKETS]
   unsigned* run_barrier = nullptr;   // arrival counter of k_fused_run's grid barrier
+  uint4* run_wtab = nullptr;         // k_fused_run's per-workplace window values [2][W][2]
   LamProbe probe{};                  // debug hazard export (epi_set_lambda_probe)
   // days of a fused run without push tables (partitioned ranks, populations
   // above the L2 cut-off): tomorrow's sigma tables are built on a side
@@ -575,6 +576,7 @@ int epi_destroy(epi_ctx* c) {
   dput(c->den_list);
   dput(c->den_count);
   dput(c->run_barrier);
+  dput(c->run_wtab);
   dput(c->iv_tile_hist);
   dput(c->iv_hist);
   dput(c->ivr_hist);
@@ -1545,6 +1547,10 @@ static bool persistent_ok(epi_ctx* c, int32_t mode, int32_t precision) {
 static int launch_run(epi_ctx* c, const epi_state* st, int32_t first, int32_t n_days, uint64_t seed,
                       uint16_t* codes0, uint16_t* codes1, int64_t* records, cudaStream_t s) {
   if (!c->run_barrier) CK(dmalloc((void**)&c->run_barrier, sizeof(unsigned)));
+  if (!c->run_wtab) {
+    int rc = dalloc(&c->run_wtab, (size_t)4 * (c->net.n_workplaces > 0 ? c->net.n_workplaces : 1));
+    if (rc) return rc;
+  }
   CK(cudaMemsetAsync(c->run_barrier, 0, sizeof(unsigned), s));
   RunArgs R{};
   R.P = c->P;
@@ -1563,6 +1569,7 @@ static int launch_run(epi_ctx* c, const epi_state* st, int32_t first, int32_t n_
   R.dn = c->ntab.dn;
   R.barrier = c->run_barrier;
   R.probe = c->probe;
+  R.wtab = c->run_wtab;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)sm_count());
   const bool big = run_threads(c->n) > RUN_MAX_AGENTS;      // (the 1024-thread variant)

@@ -57,6 +57,7 @@ struct RunArgs {
   Radix dn;
   unsigned* barrier;              // zeroed arrival counter
   LamProbe probe;
+  uint4* wtab;                    // [2][n_workplaces][2]: per-workplace window values by day parity
 };
 
 // Grid barrier between days: one arrival per block (release reduction on one
@@ -141,6 +142,22 @@ __device__ __forceinline__ uint2 day_shifts(uint64_t wshift_prefix, int w, int m
   return make_uint2(lo, hi);
 }
 
+// The per-workplace values of the barrier window after a day (the colleague
+// shifts of the coming day, the permutation keys of the day after), computed
+// once per workplace by the service warps a day ahead instead of by every
+// member: entry = {fold(fold(wperm, w), 0) (64 bits), fold(fold(wperm, w), 1)
+// low 32 bits, 0}, {shifts.x, shifts.y}.
+__device__ __forceinline__ PermKeys work_keys_from(uint64_t ha, uint32_t hb) {
+  PermKeys K;
+  K.k1[0] = (uint32_t)(ha & 0xFFFF);
+  K.k2[0] = (uint32_t)((ha >> 16) & 0xFFFF) | 1u;
+  K.k1[1] = (uint32_t)((ha >> 32) & 0xFFFF);
+  K.k2[1] = (uint32_t)((ha >> 48) & 0xFFFF) | 1u;
+  K.k1[2] = hb & 0xFFFF;
+  K.k2[2] = ((hb >> 16) & 0xFFFF) | 1u;
+  return K;
+}
+
 template <int MAXT>
 __global__ void __launch_bounds__(MAXT, 1) k_fused_run(RunArgs R, epi_net net) {
   constexpr int HH = 8, DR = 8;
@@ -215,6 +232,25 @@ __global__ void __launch_bounds__(MAXT, 1) k_fused_run(RunArgs R, epi_net net) {
       // yesterday's record rows (complete since the barrier); tomorrow's keys
       if (d > 0) rec_flush_warp(racc[(d - 1) & 1], R.records + (size_t)(d - 1) * EPI_REC_LEN, t - 1, nwa, lane);
       if (d + 1 < R.n_days) day_keys(dk[(d + 1) & 1], R.seed, t + 1, lane);
+      if (d + 2 < R.n_days) {
+        // the workplace values of the window after day d + 1: shifts of
+        // t + 2, permutation keys of t + 3 (this block's share of the workplaces)
+        const uint64_t wsh = key_prefix(R.seed, t + 2, P_NET_WSHIFT);
+        const uint64_t wpm = key_prefix(R.seed, t + 3, P_NET_WPERM);
+        const int nW = net.n_workplaces;
+        const int per_w = (nW + (int)gridDim.x - 1) / (int)gridDim.x;
+        const int w_lo = (int)blockIdx.x * per_w, w_hi = w_lo + per_w < nW ? w_lo + per_w : nW;
+        uint4* tab = R.wtab + (size_t)((d + 1) & 1) * 2 * nW;
+        for (int ww = w_lo + lane; ww < w_hi; ww += 32) {
+          const int mm = net.wp_size[ww];
+          if (mm < 2) continue;
+          const uint64_t hw = fold(wpm, (uint64_t)ww);
+          const uint64_t ha = fold(hw, 0), hb = fold(hw, 1);
+          const uint2 sh = day_shifts(wsh, ww, mm);
+          tab[2 * ww] = make_uint4((uint32_t)ha, (uint32_t)(ha >> 32), (uint32_t)hb, 0u);
+          tab[2 * ww + 1] = make_uint4(sh.x, sh.y, 0u, 0u);
+        }
+      }
     } else {
     const uint16_t* codes = R.codes[par];
     uint16_t* codes_next = R.codes[par ^ 1];
@@ -370,8 +406,15 @@ __global__ void __launch_bounds__(MAXT, 1) k_fused_run(RunArgs R, epi_net net) {
       if (threadIdx.x == 0) grid_arrive(R.barrier);
       if (pend >= 0) schedule_pending(R.P, R.st, D.K, t, R.tau_lut, b, pend, h);   // feeds tomorrow's check
       if (works) {
-        shp = day_shifts(dk[(d + 1) & 1].wshift, w, m);
-        q_nx = walk_inv((uint32_t)loc, work_keys(dk[(d + 1) & 1].wperm_next, w), rm);
+        if (d >= 1) {                      // computed by a service warp during day d - 1
+          const uint4* e = R.wtab + (size_t)(d & 1) * 2 * net.n_workplaces + 2 * w;
+          const uint4 e0 = LDM(e), e1 = LDM(e + 1);
+          shp = make_uint2(e1.x, e1.y);
+          q_nx = walk_inv((uint32_t)loc, work_keys_from(((uint64_t)e0.y << 32) | e0.x, e0.z), rm);
+        } else {
+          shp = day_shifts(dk[(d + 1) & 1].wshift, w, m);
+          q_nx = walk_inv((uint32_t)loc, work_keys(dk[(d + 1) & 1].wperm_next, w), rm);
+        }
       }
       if (valid) cnt_nx = random_count(net, dk[(d + 1) & 1].rcount_next, b);
       if (threadIdx.x == 0) grid_wait(R.barrier, (unsigned)(d + 1) * gridDim.x);
