@@ -1656,6 +1656,11 @@ static int launch_iv_run(epi_ctx* c, const epi_state* st, int32_t first, int32_t
   R.tests = p.testing_enabled ? 1 : 0;
   R.post = (p.den_enabled || p.quarantine_enabled || p.vaccination_enabled) ? 1 : 0;
   R.vax = p.vaccination_enabled ? 1 : 0;
+  if (!c->run_wtab) {
+    int rc2 = dalloc(&c->run_wtab, (size_t)4 * (c->net.n_workplaces > 0 ? c->net.n_workplaces : 1));
+    if (rc2) return rc2;
+  }
+  R.wtab = c->run_wtab;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)sm_count());
   cfg.blockDim = dim3((unsigned)run_threads(c->n) + 32);
