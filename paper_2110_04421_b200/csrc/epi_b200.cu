@@ -314,7 +314,7 @@ struct epi_ctx {
   unsigned long long* ivr_hist = nullptr;  // k_iv_run: [3][NUM_BUCKETS + 1] (+ active count)
   unsigned* ivr_tile_hist = nullptr;       // k_iv_run: [2][SMs][NUM_BUCKETS]
   unsigned* run_barrier = nullptr;   // arrival counter of k_fused_run's grid barrier
-  uint4* run_wtab = nullptr;         // k_fused_run's per-workplace window values [2][W][2]
+  uint4* run_wtab = nullptr;         // per-workplace window values of the persistent runs [3][W][2]
   LamProbe probe{};                  // debug hazard export (epi_set_lambda_probe)
   // days of a fused run without push tables (partitioned ranks, populations
   // above the L2 cut-off): tomorrow's sigma tables are built on a side
@@ -1548,7 +1548,7 @@ static int launch_run(epi_ctx* c, const epi_state* st, int32_t first, int32_t n_
                       uint16_t* codes0, uint16_t* codes1, int64_t* records, cudaStream_t s) {
   if (!c->run_barrier) CK(dmalloc((void**)&c->run_barrier, sizeof(unsigned)));
   if (!c->run_wtab) {
-    int rc = dalloc(&c->run_wtab, (size_t)4 * (c->net.n_workplaces > 0 ? c->net.n_workplaces : 1));
+    int rc = dalloc(&c->run_wtab, (size_t)6 * (c->net.n_workplaces > 0 ? c->net.n_workplaces : 1));
     if (rc) return rc;
   }
   CK(cudaMemsetAsync(c->run_barrier, 0, sizeof(unsigned), s));
@@ -1657,7 +1657,7 @@ static int launch_iv_run(epi_ctx* c, const epi_state* st, int32_t first, int32_t
   R.post = (p.den_enabled || p.quarantine_enabled || p.vaccination_enabled) ? 1 : 0;
   R.vax = p.vaccination_enabled ? 1 : 0;
   if (!c->run_wtab) {
-    int rc2 = dalloc(&c->run_wtab, (size_t)4 * (c->net.n_workplaces > 0 ? c->net.n_workplaces : 1));
+    int rc2 = dalloc(&c->run_wtab, (size_t)6 * (c->net.n_workplaces > 0 ? c->net.n_workplaces : 1));
     if (rc2) return rc2;
   }
   R.wtab = c->run_wtab;

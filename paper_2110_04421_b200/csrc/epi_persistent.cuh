@@ -57,7 +57,7 @@ struct RunArgs {
   Radix dn;
   unsigned* barrier;              // zeroed arrival counter
   LamProbe probe;
-  uint4* wtab;                    // [2][n_workplaces][2]: per-workplace window values by day parity
+  uint4* wtab;                    // [3][n_workplaces][2]: per-workplace window values by run day mod 3 (a slow block may still read day d's while a fast one writes day d + 1's)
 };
 
 // Grid barrier between days: one arrival per block (release reduction on one
@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_fused_run(RunArgs R, epi_net net) {
         const int nW = net.n_workplaces;
         const int per_w = (nW + (int)gridDim.x - 1) / (int)gridDim.x;
         const int w_lo = (int)blockIdx.x * per_w, w_hi = w_lo + per_w < nW ? w_lo + per_w : nW;
-        uint4* tab = R.wtab + (size_t)((d + 1) & 1) * 2 * nW;
+        uint4* tab = R.wtab + (size_t)((d + 1) % 3) * 2 * nW;
         for (int ww = w_lo + lane; ww < w_hi; ww += 32) {
           const int mm = net.wp_size[ww];
           if (mm < 2) continue;
@@ -407,7 +407,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_fused_run(RunArgs R, epi_net net) {
       if (pend >= 0) schedule_pending(R.P, R.st, D.K, t, R.tau_lut, b, pend, h);   // feeds tomorrow's check
       if (works) {
         if (d >= 1) {                      // computed by a service warp during day d - 1
-          const uint4* e = R.wtab + (size_t)(d & 1) * 2 * net.n_workplaces + 2 * w;
+          const uint4* e = R.wtab + (size_t)(d % 3) * 2 * net.n_workplaces + 2 * w;
           const uint4 e0 = LDM(e), e1 = LDM(e + 1);
           shp = make_uint2(e1.x, e1.y);
           q_nx = walk_inv((uint32_t)loc, work_keys_from(((uint64_t)e0.y << 32) | e0.x, e0.z), rm);

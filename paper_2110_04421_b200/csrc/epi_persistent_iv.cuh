@@ -45,7 +45,7 @@ struct IvRunArgs {
   int32_t* died_at;
   int den_lookback;
   int den, tests, post, vax;      // phases present
-  uint4* wtab;                    // [2][n_workplaces][2]: per-workplace permutation keys + domain by day parity
+  uint4* wtab;                    // [3][n_workplaces][2]: per-workplace keys, domain, shifts by run day mod 3
 };
 
 constexpr int IV_HIST = NUM_BUCKETS + 1;
@@ -195,10 +195,10 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
       if (valid && works) {
         uint32_t q;
         if (d >= 1) {                      // keys + domain by a service warp during day d - 1
-          const uint4* e = R.wtab + (size_t)(d & 1) * 2 * net.n_workplaces + 2 * w;
+          const uint4* e = R.wtab + (size_t)(d % 3) * 2 * net.n_workplaces + 2 * w;
           const uint4 e0 = LDM(e), e1 = LDM(e + 1);
           q = walk_inv((uint32_t)loc, work_keys_from(((uint64_t)e0.y << 32) | e0.x, e0.z),
-                       Radix{e1.x, e1.y, e1.z, e1.w});
+                       Radix{e1.x & 0xFFu, (e1.x >> 8) & 0xFFu, (e1.x >> 16) & 0xFFu, e1.y});
         } else {
           q = walk_inv((uint32_t)loc, work_keys(D.wperm_next, w), make_radix((uint32_t)m));
         }
@@ -259,20 +259,23 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
           As[d3n].step = t + 1;
         }
         // tomorrow's per-workplace permutation keys (of t + 2) and domains,
-        // this block's share of the workplaces, read by the workers tomorrow
+        // and the colleague shifts of t + 2 (read in tomorrow's end-of-day
+        // window), this block's share of the workplaces
         const uint64_t wpm = key_prefix(R.seed, t + 2, P_NET_WPERM);
+        const uint64_t wsh = key_prefix(R.seed, t + 2, P_NET_WSHIFT);
         const int nW = net.n_workplaces;
         const int per_w = (nW + (int)gridDim.x - 1) / (int)gridDim.x;
         const int w_lo = (int)blockIdx.x * per_w, w_hi = w_lo + per_w < nW ? w_lo + per_w : nW;
-        uint4* tab = R.wtab + (size_t)((d + 1) & 1) * 2 * nW;
+        uint4* tab = R.wtab + (size_t)((d + 1) % 3) * 2 * nW;
         for (int ww = w_lo + lane; ww < w_hi; ww += 32) {
           const int mm = net.wp_size[ww];
           if (mm < 2) continue;
           const uint64_t hw = fold(wpm, (uint64_t)ww);
           const uint64_t ha = fold(hw, 0), hb = fold(hw, 1);
           const Radix rr = make_radix((uint32_t)mm);
+          const uint2 sh = day_shifts(wsh, ww, mm);
           tab[2 * ww] = make_uint4((uint32_t)ha, (uint32_t)(ha >> 32), (uint32_t)hb, 0u);
-          tab[2 * ww + 1] = make_uint4(rr.n, rr.a, rr.b, rr.magic);
+          tab[2 * ww + 1] = make_uint4(rr.n | rr.a << 8 | rr.b << 16, rr.magic, sh.x, sh.y);   // (m <= 255)
         }
       }
     } else {
@@ -519,7 +522,14 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
         hs.age = age;
         schedule_pending(A.P, st, A.K, t, A.tau_lut, b, pend, hs);
       }
-      if (works) shp = day_shifts(dk[d3n].wshift, w, m);
+      if (works) {
+        if (d >= 1) {                      // (written during day d - 1 with the keys)
+          const uint4 e1 = LDM(R.wtab + (size_t)(d % 3) * 2 * net.n_workplaces + 2 * w + 1);
+          shp = make_uint2(e1.z, e1.w);
+        } else {
+          shp = day_shifts(dk[d3n].wshift, w, m);
+        }
+      }
       if (valid) hp = load_hot(st, b);
       ++bar;
       if (threadIdx.x == 0) grid_wait(R.barrier, bar * gridDim.x);
@@ -531,7 +541,14 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
         hs.age = age;
         schedule_pending(A.P, st, A.K, t, A.tau_lut, b, pend, hs);
       }
-      if (d + 1 < R.n_days && works) shp = day_shifts(dk[d3n].wshift, w, m);
+      if (d + 1 < R.n_days && works) {
+        if (d >= 1) {
+          const uint4 e1 = LDM(R.wtab + (size_t)(d % 3) * 2 * net.n_workplaces + 2 * w + 1);
+          shp = make_uint2(e1.z, e1.w);
+        } else {
+          shp = day_shifts(dk[d3n].wshift, w, m);
+        }
+      }
       if (d + 1 < R.n_days && valid) hp = load_hot(st, b);
     }
   }
