@@ -177,19 +177,23 @@ __device__ __forceinline__ uint32_t work_shift(uint64_t wshift_prefix, int w, in
 }
 
 // Random-slot count n_{t,a} ~ Poisson(mean) truncated at `slots`.
-__device__ __forceinline__ int random_count(const epi_net& net, uint64_t rcount_prefix, int64_t a) {
+// (cdf: the network's Poisson CDF, from wherever the caller keeps it -- a
+// kernel parameter's array indexed per lane is a serialised constant load)
+__device__ __forceinline__ int random_count_cdf(const double* cdf, int slots, uint64_t rcount_prefix, int64_t a) {
   const double u = keyed_u(rcount_prefix, (uint64_t)a, 0);
   // #{k < slots : u >= cdf[k]} for the non-decreasing cdf: a branch-free
   // binary search (6 compares instead of up to 32)
-  const int slots = net.random_slots;
   int c = 0;
 #pragma unroll
   for (int step = EPI_MAX_SLOTS / 2; step >= 1; step >>= 1) {
     const int k = c + step - 1;
-    c += (k < slots && u >= net.poisson_cdf[k]) ? step : 0;
+    c += (k < slots && u >= cdf[k]) ? step : 0;
   }
-  c += (c < slots && u >= net.poisson_cdf[c < EPI_MAX_SLOTS ? c : EPI_MAX_SLOTS - 1]) ? 1 : 0;
+  c += (c < slots && u >= cdf[c < EPI_MAX_SLOTS ? c : EPI_MAX_SLOTS - 1]) ? 1 : 0;
   return c;
+}
+__device__ __forceinline__ int random_count(const epi_net& net, uint64_t rcount_prefix, int64_t a) {
+  return random_count_cdf(net.poisson_cdf, net.random_slots, rcount_prefix, a);
 }
 
 // Enumerate the in-edges of destination b (alive); visit(src, kind, code_src).

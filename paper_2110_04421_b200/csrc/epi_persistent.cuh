@@ -168,9 +168,11 @@ __global__ void __launch_bounds__(MAXT, 1) k_fused_run(RunArgs R, epi_net net) {
   __shared__ uint8_t own_s[MAXT / 32][32 * RT_SLOTS];
   __shared__ DayKeys dk[2];                // keys by day parity
   __shared__ uint16_t hcode_s[2][MAXT - 32];     // the block's codes by day parity
+  __shared__ double cdf_s[EPI_MAX_SLOTS];         // the random-slot count CDF (per-lane indexed)
   extern __shared__ uint4 run_dyn_s[];
   uint32_t* const out_s = (uint32_t*)run_dyn_s;    // [agent][RUN_OUT_STRIDE]
   load_msg_tables(T, R.mt);
+  if (threadIdx.x < EPI_MAX_SLOTS) cdf_s[threadIdx.x] = net.poisson_cdf[threadIdx.x];
   rec_init(racc[0]);
   rec_init(racc[1]);
   const int warp = threadIdx.x >> 5, lane = lane_id();
@@ -220,7 +222,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_fused_run(RunArgs R, epi_net net) {
   // between each barrier's arrive and wait): today's shifts, the slot count
   // of tomorrow's code and tomorrow's workplace position
   uint2 shp = works ? day_shifts(dk[0].wshift, w, m) : make_uint2(0, 0);
-  int cnt_nx = valid ? random_count(net, dk[0].rcount_next, b) : 0;
+  int cnt_nx = valid ? random_count_cdf(cdf_s, net.random_slots, dk[0].rcount_next, b) : 0;
   uint32_t q_nx = works ? walk_inv((uint32_t)loc, work_keys(dk[0].wperm_next, w), rm) : 0u;
   for (int d = 0; d < R.n_days; ++d) {
     const int t = R.first_step + d;
@@ -416,7 +418,7 @@ __global__ void __launch_bounds__(MAXT, 1) k_fused_run(RunArgs R, epi_net net) {
           q_nx = walk_inv((uint32_t)loc, work_keys(dk[(d + 1) & 1].wperm_next, w), rm);
         }
       }
-      if (valid) cnt_nx = random_count(net, dk[(d + 1) & 1].rcount_next, b);
+      if (valid) cnt_nx = random_count_cdf(cdf_s, net.random_slots, dk[(d + 1) & 1].rcount_next, b);
       if (threadIdx.x == 0) grid_wait(R.barrier, (unsigned)(d + 1) * gridDim.x);
       __syncthreads();
     } else if (pend >= 0) {

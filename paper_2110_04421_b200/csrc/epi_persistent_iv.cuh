@@ -85,6 +85,7 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
   __shared__ uint16_t cn_s[RUN_MAX_THREADS / 32][32];
   __shared__ uint8_t own_s[RUN_MAX_THREADS / 32][32 * RT_SLOTS];
   __shared__ uint16_t hcode_s[2][RUN_MAX_AGENTS];   // the block's codes by day parity
+  __shared__ double cdf_s[EPI_MAX_SLOTS];           // the random-slot count CDF (per-lane indexed)
   extern __shared__ uint4 run_dyn_s[];
   uint32_t* const out_s = (uint32_t*)run_dyn_s;    // out-rows [agent][RUN_OUT_STRIDE] (as k_fused_run)
   // per-warp eligibility histograms by day parity [2][warps][NUM_BUCKETS + 1]:
@@ -92,6 +93,7 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
   // bucket is the sum over the warps before it (no block barrier for either)
   unsigned* const hw_s = (unsigned*)(out_s + (size_t)RUN_MAX_AGENTS * RUN_OUT_STRIDE);
   load_msg_tables(T, R.mt);
+  if (threadIdx.x < EPI_MAX_SLOTS) cdf_s[threadIdx.x] = net.poisson_cdf[threadIdx.x];
   rec_init(racc[0]);
   rec_init(racc[1]);
   rec_init(racc[2]);
@@ -188,7 +190,7 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
         if (R.died_at && stage == S_DEAD && R.died_at[b] == INT32_MAX) R.died_at[b] = t;
         cn = source_code(A.P, stage, st.infected_at[b], st.quarantine_until[b], t + 1);
         if (stage == S_DEAD) cn |= CODE_DEAD;
-        else cn |= (uint16_t)(random_count(net, D.rcount_next, b) << 8);
+        else cn |= (uint16_t)(random_count_cdf(cdf_s, net.random_slots, D.rcount_next, b) << 8);
         codes_next[b] = cn;
         hcode_s[par ^ 1][threadIdx.x] = cn;
       }
