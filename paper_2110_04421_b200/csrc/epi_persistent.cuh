@@ -128,6 +128,49 @@ template <int MAXT> constexpr size_t run_dyn_smem() { return (size_t)(MAXT - 32)
 // grid barrier orders them after the writers' stores
 template <class T> __device__ __forceinline__ T LDM(const T* p) { return *p; }
 
+// The household in-edge sources of an agent in visit order (members
+// ascending, the agent itself skipped).  `hp` points at the first member's
+// code of the day: the block's shared-memory copy when the whole household
+// lies in the block, else the global code vector (a generic pointer either
+// way); bit i of the static `hmask` is set for the members i < HH other than
+// the agent.  Absent slots read as CODE_DEAD (no edge, factor 0).
+template <int HH>
+__device__ __forceinline__ void load_household(uint16_t (&hc)[HH], const uint16_t* hp, unsigned hmask) {
+#pragma unroll
+  for (int i = 0; i < HH; ++i) hc[i] = ((hmask >> i) & 1u) ? LDM(hp + i) : (uint16_t)CODE_DEAD;
+}
+__host__ __device__ __forceinline__ unsigned household_mask(int hh, int sz, int off) {
+  return (sz >= hh ? (1u << hh) - 1u : (1u << sz) - 1u) & (off < hh ? ~(1u << off) : ~0u);
+}
+// The colleague in-edge sources of a worker at position p of its workplace
+// window (m >= 2 members, codes at wc[base .. base + m)): per draw j the
+// partners at p + r_j and p - r_j (mod m), visit order out, in; the day's
+// shifts r_j (1 <= r_j <= m - 1) packed one byte each in `shp`.  Non-workers
+// and draws >= `draws` read as CODE_DEAD.  32-bit table indices, the window
+// wrap as a select between two precomputed bases; the full-draw case (every
+// config network) has no per-draw test.
+template <int DR>
+__device__ __forceinline__ void load_colleagues(uint16_t (&wio)[2 * DR], bool works, const uint16_t* wc, uint32_t base,
+                                                uint32_t p, uint32_t m, uint2 shp, int draws) {
+#pragma unroll
+  for (int j = 0; j < 2 * DR; ++j) wio[j] = (uint16_t)CODE_DEAD;
+  const uint32_t bp = base + p, mp = m - p;          // out: p + r wraps iff r >= m - p
+  const uint32_t bpo = bp - m, bpi = bp + m;         // in: p - r wraps iff r > p
+  auto load = [&](int j) {
+    const uint32_t r = ((j < 4 ? shp.x : shp.y) >> (8 * (j & 3))) & 0xFFu;
+    wio[2 * j] = LDM(wc + ((r >= mp ? bpo : bp) + r));
+    wio[2 * j + 1] = LDM(wc + ((r > p ? bpi : bp) - r));
+  };
+  if (works && draws == DR) {
+#pragma unroll
+    for (int j = 0; j < DR; ++j) load(j);
+  } else if (works) {
+#pragma unroll
+    for (int j = 0; j < DR; ++j)
+      if (j < draws) load(j);
+  }
+}
+
 // The day's 8 colleague shifts r_j of workplace w (work_shift: four 16-bit
 // fields per hash), packed one byte each (r_j <= m - 1 <= 254).
 __device__ __forceinline__ uint2 day_shifts(uint64_t wshift_prefix, int w, int m) {
@@ -216,6 +259,9 @@ __global__ void __launch_bounds__(MAXT, 1) k_fused_run(RunArgs R, epi_net net) {
   const int nloc = (int)(bhi - blo);
   const bool works = w >= 0 && m >= 2;
   const int64_t start = b - off;
+  // the whole household in the block: its codes come from hcode_s
+  const bool hin = hl0 >= 0 && hl0 + sz <= nloc;
+  const unsigned hmask = household_mask(HH, sz, off);
   const Radix rm = make_radix(works ? (uint32_t)m : 1u);
   __syncthreads();
   // state-independent values of the coming day, computed ahead (here, then
@@ -258,7 +304,6 @@ __global__ void __launch_bounds__(MAXT, 1) k_fused_run(RunArgs R, epi_net net) {
     uint16_t* codes_next = R.codes[par ^ 1];
     const WorkTables& W = R.wt[par];
     const WorkTables& Wn = R.wt[par ^ 1];
-    const uint16_t* hcs = hcode_s[par];
     unsigned edges = 0;
     double lam = 0.0;
     if (valid) {
@@ -270,48 +315,21 @@ __global__ void __launch_bounds__(MAXT, 1) k_fused_run(RunArgs R, epi_net net) {
         const int nb = code_count(cb);
         const int nbe = nb < RT_SLOTS ? nb : RT_SLOTS;
         const uint4 o0 = nbe > 0 ? ro[0] : make_uint4(self, self, self, self);
-        auto hh_code = [&](int i) -> uint16_t {
-          return (unsigned)(hl0 + i) < (unsigned)nloc ? hcs[hl0 + i] : LDM(codes + start + i);
-        };
-        uint16_t hc[HH];
-#pragma unroll
-        for (int i = 0; i < HH; ++i)
-          hc[i] = (i < sz && start + i != b) ? hh_code(i) : (uint16_t)CODE_DEAD;
-        // the day's colleague shifts r_j (hashed while the previous barrier waited)
-        uint32_t sh[DR];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          sh[q] = (shp.x >> (8 * q)) & 0xFFu;
-          sh[4 + q] = (shp.y >> (8 * q)) & 0xFFu;
-        }
-        // level 2
+        // level 2: every load of the day's sources before any sum
+        uint16_t hc[HH], wio[2 * DR];
+        load_household<HH>(hc, hin ? hcode_s[par] + hl0 : codes + start, hmask);
+        load_colleagues<DR>(wio, works, W.wcode, (uint32_t)base, p, (uint32_t)m, shp, draws);
         const uint32_t po0[4] = {o0.x, o0.y, o0.z, o0.w};
         uint16_t co0[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q)
           co0[q] = (q < nbe && po0[q] != self) ? LDM(codes + po0[q]) : (uint16_t)CODE_DEAD;
-        uint16_t wo[DR], wi[DR];
-#pragma unroll
-        for (int j = 0; j < DR; ++j) {
-          wo[j] = wi[j] = (uint16_t)CODE_DEAD;
-          if (works && j < draws) {
-            const uint32_t r = sh[j];
-            wo[j] = LDM(W.wcode + base + add_mod(p, r, (uint32_t)m));
-            wi[j] = LDM(W.wcode + base + sub_mod(p, r, (uint32_t)m));
-          }
-        }
         // per-kind sums in the visit order of for_each_in_code
         float acc[3] = {0.f, 0.f, 0.f};
         add_src_group<HH>(acc[0], edges, T.factor, hc);
         for (int i = HH; i < sz; ++i) {
-          if (start + i == b) continue;
-          add_src(acc[0], edges, T.factor, hh_code(i));
-        }
-        uint16_t wio[2 * DR];                 // visit order: out, in per draw
-#pragma unroll
-        for (int j = 0; j < DR; ++j) {
-          wio[2 * j] = wo[j];
-          wio[2 * j + 1] = wi[j];
+          if (i == off) continue;
+          add_src(acc[0], edges, T.factor, LDM((hin ? hcode_s[par] + hl0 : codes + start) + i));
         }
         add_src_group<2 * DR>(acc[1], edges, T.factor, wio);
         if (n >= 2) {
