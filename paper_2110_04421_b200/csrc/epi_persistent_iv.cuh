@@ -407,11 +407,15 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
       // (and the block's active count: one atomic per block)
       const unsigned* hw = hw_s + (size_t)par * (RUN_MAX_THREADS / 32) * IV_HW_ROW;
       unsigned* hw_next = hw_s + (size_t)(par ^ 1) * (RUN_MAX_THREADS / 32) * IV_HW_ROW;
-      for (int i = threadIdx.x; i < IV_HW_ROW; i += blockDim.x) {
+      // (one warp per bucket: lane w holds warp w's row entry, one warp sum)
+      for (int i = warp; i < IV_HW_ROW; i += nwa + 1) {
         unsigned v = 0;
-        for (int ww = 0; ww < nwa; ++ww) v += hw[ww * IV_HW_ROW + i];
-        if (i < NUM_BUCKETS) tile_hist[(size_t)blockIdx.x * NUM_BUCKETS + i] = v;
-        if (v) atomicAdd(&hist[i], (unsigned long long)v);
+        for (int ww = lane; ww < nwa; ww += 32) v += hw[ww * IV_HW_ROW + i];
+        v = __reduce_add_sync(0xFFFFFFFFu, v);
+        if (lane == 0) {
+          if (i < NUM_BUCKETS) tile_hist[(size_t)blockIdx.x * NUM_BUCKETS + i] = v;
+          if (v) atomicAdd(&hist[i], (unsigned long long)v);
+        }
       }
       // tomorrow's rows start empty (yesterday's doses, their last reader, are done)
       for (int i = threadIdx.x; i < (RUN_MAX_THREADS / 32) * IV_HW_ROW; i += blockDim.x) hw_next[i] = 0u;
@@ -488,8 +492,20 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
         const bool in_cut = cut >= 0 && cut < NUM_BUCKETS && bk == (uint8_t)cut;
         if (cut >= 0 && cut < NUM_BUCKETS && !service) {
           const unsigned ball = __ballot_sync(0xFFFFFFFFu, in_cut);
+          // (the blocks' tile rows: every load issued before the first add)
           unsigned part = 0;
-          for (int bb = lane; bb < (int)blockIdx.x; bb += 32) part += LDM(tile_hist + (size_t)bb * NUM_BUCKETS + cut);
+          if (blockIdx.x <= 256) {
+            unsigned v[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              const int bb = lane + 32 * k;
+              v[k] = bb < (int)blockIdx.x ? LDM(tile_hist + (size_t)bb * NUM_BUCKETS + cut) : 0u;
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) part += v[k];
+          } else {
+            for (int bb = lane; bb < (int)blockIdx.x; bb += 32) part += LDM(tile_hist + (size_t)bb * NUM_BUCKETS + cut);
+          }
           if (lane < warp) part += hw_s[((size_t)par * (RUN_MAX_THREADS / 32) + lane) * IV_HW_ROW + cut];
           const long long rank = (long long)__reduce_add_sync(0xFFFFFFFFu, part) + __popc(ball & ((1u << lane) - 1u));
           if (valid && bk != NO_BUCKET && ((long long)bk < cut || (in_cut && rank < rem))) give_dose(A, b, bk);
