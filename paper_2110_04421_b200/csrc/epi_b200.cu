@@ -2153,4 +2153,12 @@ int epi_refnet_run(epi_refnet_t* r, epi_ctx* c, const epi_state* st, uint64_t gr
   return 0;
 }
 
+#ifdef EPI_IV_TRACE
+// k_iv_run's phase timeline of the last launch (a -DEPI_IV_TRACE build only)
+int epi_debug_iv_trace(unsigned long long* out, long long n) {
+  const size_t bytes = sizeof(epi::g_iv_trace);
+  if ((size_t)n * sizeof(unsigned long long) < bytes) return -1;
+  return cudaMemcpyFromSymbol(out, epi::g_iv_trace, bytes) == cudaSuccess ? 0 : -3;
+}
+#endif
 }  // extern "C"

@@ -48,6 +48,22 @@ struct IvRunArgs {
   uint4* wtab;                    // [3][n_workplaces][2]: per-workplace keys, domain, shifts by run day mod 3
 };
 
+// Phase timeline (a build with -DEPI_IV_TRACE only, tools/iv_timeline.py):
+// %globaltimer of thread 0 of every block at the day's phase boundaries.
+#ifdef EPI_IV_TRACE
+constexpr int IV_TRACE_DAYS = 200, IV_TRACE_BLOCKS = 160, IV_TRACE_PTS = 6;
+__device__ unsigned long long g_iv_trace[IV_TRACE_DAYS][IV_TRACE_BLOCKS][IV_TRACE_PTS];
+__device__ __forceinline__ void iv_mark(int d, int k) {
+  if (threadIdx.x == 0 && d < IV_TRACE_DAYS && blockIdx.x < IV_TRACE_BLOCKS) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_iv_trace[d][blockIdx.x][k] = t;
+  }
+}
+#else
+__device__ __forceinline__ void iv_mark(int, int) {}
+#endif
+
 constexpr int IV_HIST = NUM_BUCKETS + 1;
 constexpr int IV_HW_ROW = NUM_BUCKETS + 1;           // + the warp's active count
 constexpr int IV_HW_WORDS = 2 * (RUN_MAX_THREADS / 32) * IV_HW_ROW;
@@ -249,6 +265,7 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
       if (!bar1) __syncthreads();
     }
     // ---- phase A ----------------------------------------------------------
+    iv_mark(d, 0);
     if (service) {
       if (d > 0 && !bar1)
         rec_flush_warp(racc[d3p], R.records + (size_t)(d - 1) * EPI_REC_LEN, t - 1, nwa, lane);
@@ -401,6 +418,7 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
       if (R.post && valid) iv_post_rest_agent(A, b, false);
       next_day();
     }
+    iv_mark(d, 1);
     if (R.vax) {
       // the block's histogram to the day's histogram and to its tile row
       __syncthreads();
@@ -424,6 +442,7 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
     // barrier 1: the notifier list and the eligibility histogram are complete
     if (bar1) {
       grid_barrier(R.barrier, ++bar * gridDim.x);
+      iv_mark(d, 2);
       if (service && d > 0)               // yesterday's record (incl. this morning's follow-ups)
         rec_flush_warp(racc[d3p], R.records + (size_t)(d - 1) * EPI_REC_LEN, t - 1, nwa, lane);
     }
@@ -443,6 +462,7 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
       }
       // no barrier: nothing until tomorrow reads the marks (see den_ok)
     }
+    iv_mark(d, 3);
     // ---- phase C: the vaccination plan (every warp derives it from the
     // complete histogram) and the doses in id order -------------------------
     if (blockIdx.x == 0 && threadIdx.x == 0 && R.den_count) R.den_count[par ^ 1] = 0;   // tomorrow's list
@@ -549,9 +569,11 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
         }
       }
       if (valid) hp = load_hot(st, b);
+      iv_mark(d, 4);
       ++bar;
       if (threadIdx.x == 0) grid_wait(R.barrier, bar * gridDim.x);
       __syncthreads();
+      iv_mark(d, 5);
     } else {
       if (!service) finish_day();
       if (pend >= 0) {
