@@ -544,6 +544,49 @@ __device__ __forceinline__ void add_src_group(float& acc, unsigned& edges, const
     for (int i = 0; i < K; ++i) acc += factor[c[i] & 0xFF];
   }
 }
+// The household in-edge sources of an agent in visit order (members
+// ascending, the agent itself skipped).  `hp` points at the first member's
+// code of the day: the block's shared-memory copy when the whole household
+// lies in the block, else the global code vector (a generic pointer either
+// way); bit i of the static `hmask` is set for the members i < HH other than
+// the agent.  Absent slots read as CODE_DEAD (no edge, factor 0).
+template <int HH>
+__device__ __forceinline__ void load_household(uint16_t (&hc)[HH], const uint16_t* hp, unsigned hmask) {
+#pragma unroll
+  for (int i = 0; i < HH; ++i) hc[i] = ((hmask >> i) & 1u) ? hp[i] : (uint16_t)CODE_DEAD;
+}
+__host__ __device__ __forceinline__ unsigned household_mask(int hh, int sz, int off) {
+  return (sz >= hh ? (1u << hh) - 1u : (1u << sz) - 1u) & (off < hh ? ~(1u << off) : ~0u);
+}
+// The colleague in-edge sources of a worker at position p of its workplace
+// window (m >= 2 members, codes at wc[base .. base + m)): per draw j the
+// partners at p + r_j and p - r_j (mod m), visit order out, in; the day's
+// shifts r_j (1 <= r_j <= m - 1) packed one byte each in `shp`.  Non-workers
+// and draws >= `draws` read as CODE_DEAD.  32-bit table indices, the window
+// wrap as a select between two precomputed bases; the full-draw case (every
+// config network) has no per-draw test.
+template <int DR>
+__device__ __forceinline__ void load_colleagues(uint16_t (&wio)[2 * DR], bool works, const uint16_t* wc, uint32_t base,
+                                                uint32_t p, uint32_t m, uint2 shp, int draws) {
+#pragma unroll
+  for (int j = 0; j < 2 * DR; ++j) wio[j] = (uint16_t)CODE_DEAD;
+  const uint32_t bp = base + p, mp = m - p;          // out: p + r wraps iff r >= m - p
+  const uint32_t bpo = bp - m, bpi = bp + m;         // in: p - r wraps iff r > p
+  auto load = [&](int j) {
+    const uint32_t r = ((j < 4 ? shp.x : shp.y) >> (8 * (j & 3))) & 0xFFu;
+    wio[2 * j] = wc[(r >= mp ? bpo : bp) + r];
+    wio[2 * j + 1] = wc[(r > p ? bpi : bp) - r];
+  };
+  if (works && draws == DR) {
+#pragma unroll
+    for (int j = 0; j < DR; ++j) load(j);
+  } else if (works) {
+#pragma unroll
+    for (int j = 0; j < DR; ++j)
+      if (j < draws) load(j);
+  }
+}
+
 // A push row (RT_SLOTS codes as two uint4, low half of each word first): the
 // same adds in slot order; the present bits (14) of both halves of a word are
 // counted together in 16-bit lanes of one register.
@@ -656,13 +699,12 @@ __device__ __forceinline__ void sparse_kind_sums(const epi_net& net, const PermK
   const uint4* ri = (const uint4*)(wt->rin + (size_t)b * RT_SLOTS);
   const uint4 in0 = __ldcs(ri), in1 = __ldcs(ri + 1);   // issued first: the row's latency under the rest
   {
+    // (the agent itself skipped: its slot would add +0.0f and no edge)
     const int off = net.hh_off[b];
     const int sz = net.hh_size[b];
-    const int64_t start = b - off;
-    for (int i = 0; i < sz; ++i) {
-      const int64_t c = start + i;
-      add_src(acc[0], edges, factor, c == b ? (uint16_t)CODE_DEAD : codes[c]);
-    }
+    const uint16_t* hp = codes + (b - off);
+    for (int i = 0; i < sz; ++i)
+      if (i != off) add_src(acc[0], edges, factor, hp[i]);
   }
   const int w = net.wp_id[b];
   if (w >= 0) {
@@ -671,12 +713,20 @@ __device__ __forceinline__ void sparse_kind_sums(const epi_net& net, const PermK
       const int base = net.wp_base[w];
       const int draws = net.colleague_draws;
       const uint32_t p = wt->pos_of[base + net.wp_local[b]];
-      const uint8_t* sh = wt->shift + (size_t)w * draws;
-      const uint16_t* wc = wt->wcode + base;
-      for (int j = 0; j < draws; ++j) {
-        const uint32_t r = sh[j];
-        add_src(acc[1], edges, factor, wc[add_mod(p, r, (uint32_t)m)]);
-        add_src(acc[1], edges, factor, wc[sub_mod(p, r, (uint32_t)m)]);
+      if (draws == 8) {                    // every config network: the 8 shifts in one load
+        const uint2 shp = *(const uint2*)(wt->shift + (size_t)w * 8);
+        uint16_t wio[16];
+        load_colleagues<8>(wio, true, wt->wcode, (uint32_t)base, p, (uint32_t)m, shp, 8);
+#pragma unroll
+        for (int k = 0; k < 16; ++k) add_src(acc[1], edges, factor, wio[k]);
+      } else {
+        const uint8_t* sh = wt->shift + (size_t)w * draws;
+        const uint16_t* wc = wt->wcode + base;
+        for (int j = 0; j < draws; ++j) {
+          const uint32_t r = sh[j];
+          add_src(acc[1], edges, factor, wc[add_mod(p, r, (uint32_t)m)]);
+          add_src(acc[1], edges, factor, wc[sub_mod(p, r, (uint32_t)m)]);
+        }
       }
     }
   }

@@ -128,49 +128,6 @@ template <int MAXT> constexpr size_t run_dyn_smem() { return (size_t)(MAXT - 32)
 // grid barrier orders them after the writers' stores
 template <class T> __device__ __forceinline__ T LDM(const T* p) { return *p; }
 
-// The household in-edge sources of an agent in visit order (members
-// ascending, the agent itself skipped).  `hp` points at the first member's
-// code of the day: the block's shared-memory copy when the whole household
-// lies in the block, else the global code vector (a generic pointer either
-// way); bit i of the static `hmask` is set for the members i < HH other than
-// the agent.  Absent slots read as CODE_DEAD (no edge, factor 0).
-template <int HH>
-__device__ __forceinline__ void load_household(uint16_t (&hc)[HH], const uint16_t* hp, unsigned hmask) {
-#pragma unroll
-  for (int i = 0; i < HH; ++i) hc[i] = ((hmask >> i) & 1u) ? LDM(hp + i) : (uint16_t)CODE_DEAD;
-}
-__host__ __device__ __forceinline__ unsigned household_mask(int hh, int sz, int off) {
-  return (sz >= hh ? (1u << hh) - 1u : (1u << sz) - 1u) & (off < hh ? ~(1u << off) : ~0u);
-}
-// The colleague in-edge sources of a worker at position p of its workplace
-// window (m >= 2 members, codes at wc[base .. base + m)): per draw j the
-// partners at p + r_j and p - r_j (mod m), visit order out, in; the day's
-// shifts r_j (1 <= r_j <= m - 1) packed one byte each in `shp`.  Non-workers
-// and draws >= `draws` read as CODE_DEAD.  32-bit table indices, the window
-// wrap as a select between two precomputed bases; the full-draw case (every
-// config network) has no per-draw test.
-template <int DR>
-__device__ __forceinline__ void load_colleagues(uint16_t (&wio)[2 * DR], bool works, const uint16_t* wc, uint32_t base,
-                                                uint32_t p, uint32_t m, uint2 shp, int draws) {
-#pragma unroll
-  for (int j = 0; j < 2 * DR; ++j) wio[j] = (uint16_t)CODE_DEAD;
-  const uint32_t bp = base + p, mp = m - p;          // out: p + r wraps iff r >= m - p
-  const uint32_t bpo = bp - m, bpi = bp + m;         // in: p - r wraps iff r > p
-  auto load = [&](int j) {
-    const uint32_t r = ((j < 4 ? shp.x : shp.y) >> (8 * (j & 3))) & 0xFFu;
-    wio[2 * j] = LDM(wc + ((r >= mp ? bpo : bp) + r));
-    wio[2 * j + 1] = LDM(wc + ((r > p ? bpi : bp) - r));
-  };
-  if (works && draws == DR) {
-#pragma unroll
-    for (int j = 0; j < DR; ++j) load(j);
-  } else if (works) {
-#pragma unroll
-    for (int j = 0; j < DR; ++j)
-      if (j < draws) load(j);
-  }
-}
-
 // The day's 8 colleague shifts r_j of workplace w (work_shift: four 16-bit
 // fields per hash), packed one byte each (r_j <= m - 1 <= 254).
 __device__ __forceinline__ uint2 day_shifts(uint64_t wshift_prefix, int w, int m) {
