@@ -274,8 +274,28 @@ __global__ void __launch_bounds__(MAXT, 1) k_fused_run(RunArgs R, epi_net net) {
         const uint4 o0 = nbe > 0 ? ro[0] : make_uint4(self, self, self, self);
         // level 2: every load of the day's sources before any sum
         uint16_t hc[HH], wio[2 * DR];
-        load_household<HH>(hc, hin ? hcode_s[par] + hl0 : codes + start, hmask);
-        load_colleagues<DR>(wio, works, W.wcode, (uint32_t)base, p, (uint32_t)m, shp, draws);
+        if constexpr (MAXT <= RUN_MAX_THREADS) {
+          load_household<HH>(hc, hin ? hcode_s[par] + hl0 : codes + start, hmask);
+          load_colleagues<DR>(wio, works, W.wcode, (uint32_t)base, p, (uint32_t)m, shp, draws);
+        } else {
+          // the 64-register variant: per-member in-block tests and per-draw
+          // modular indices spill less (measured 2.44 vs 2.69 ms at 120 k agents)
+          const uint16_t* hcs = hcode_s[par];
+#pragma unroll
+          for (int i = 0; i < HH; ++i)
+            hc[i] = (i < sz && start + i != b)
+                        ? ((unsigned)(hl0 + i) < (unsigned)nloc ? hcs[hl0 + i] : LDM(codes + start + i))
+                        : (uint16_t)CODE_DEAD;
+#pragma unroll
+          for (int j = 0; j < DR; ++j) {
+            wio[2 * j] = wio[2 * j + 1] = (uint16_t)CODE_DEAD;
+            if (works && j < draws) {
+              const uint32_t r = ((j < 4 ? shp.x : shp.y) >> (8 * (j & 3))) & 0xFFu;
+              wio[2 * j] = LDM(W.wcode + base + add_mod(p, r, (uint32_t)m));
+              wio[2 * j + 1] = LDM(W.wcode + base + sub_mod(p, r, (uint32_t)m));
+            }
+          }
+        }
         const uint32_t po0[4] = {o0.x, o0.y, o0.z, o0.w};
         uint16_t co0[4];
 #pragma unroll
