@@ -315,6 +315,7 @@ struct epi_ctx {
   unsigned* ivr_tile_hist = nullptr;       // k_iv_run: [2][SMs][NUM_BUCKETS]
   unsigned* run_barrier = nullptr;   // arrival counter of k_fused_run's grid barrier
   uint4* run_wtab = nullptr;         // per-workplace window values of the persistent runs [3][W][2]
+  uint16_t* run_crow = nullptr;      // k_fused_run's colleague rows [2][member slots][16] (all zero between launches)
   LamProbe probe{};                  // debug hazard export (epi_set_lambda_probe)
   // days of a fused run without push tables (partitioned ranks, populations
   // above the L2 cut-off): tomorrow's sigma tables are built on a side
@@ -577,6 +578,7 @@ int epi_destroy(epi_ctx* c) {
   dput(c->den_count);
   dput(c->run_barrier);
   dput(c->run_wtab);
+  dput(c->run_crow);
   dput(c->iv_tile_hist);
   dput(c->iv_hist);
   dput(c->ivr_hist);
@@ -1551,6 +1553,13 @@ static int launch_run(epi_ctx* c, const epi_state* st, int32_t first, int32_t n_
     int rc = dalloc(&c->run_wtab, (size_t)6 * (c->net.n_workplaces > 0 ? c->net.n_workplaces : 1));
     if (rc) return rc;
   }
+  const bool big = run_threads(c->n) > RUN_MAX_AGENTS;      // (the 1024-thread variant)
+  const size_t crow_len = (size_t)16 * (size_t)(c->net.n_member_slots > 0 ? c->net.n_member_slots : 1);
+  if (!big && !c->run_crow) {
+    int rc = dalloc(&c->run_crow, 2 * crow_len);
+    if (rc) return rc;
+    CK(cudaMemsetAsync(c->run_crow, 0, 2 * crow_len * sizeof(uint16_t), s));
+  }
   CK(cudaMemsetAsync(c->run_barrier, 0, sizeof(unsigned), s));
   RunArgs R{};
   R.P = c->P;
@@ -1570,9 +1579,10 @@ static int launch_run(epi_ctx* c, const epi_state* st, int32_t first, int32_t n_
   R.barrier = c->run_barrier;
   R.probe = c->probe;
   R.wtab = c->run_wtab;
+  R.crow[0] = c->run_crow;
+  R.crow[1] = c->run_crow ? c->run_crow + crow_len : nullptr;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)sm_count());
-  const bool big = run_threads(c->n) > RUN_MAX_AGENTS;      // (the 1024-thread variant)
   cfg.blockDim = dim3((unsigned)run_threads(c->n) + 32);     // + the service warp
   cfg.dynamicSmemBytes = big ? run_dyn_smem<RUN_BIG_THREADS>() : run_dyn_smem<RUN_MAX_THREADS>();
   cfg.stream = s;

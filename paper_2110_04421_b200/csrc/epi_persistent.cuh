@@ -58,6 +58,13 @@ struct RunArgs {
   unsigned* barrier;              // zeroed arrival counter
   LamProbe probe;
   uint4* wtab;                    // [3][n_workplaces][2]: per-workplace window values by run day mod 3 (a slow block may still read day d's while a fast one writes day d + 1's)
+  // colleague rows (k_fused_run<RUN_MAX_THREADS>), by workplace position:
+  // crow[par][(base_W + q) * 16 + s] = the code of the colleague in slot s
+  // (2j: out-partner of draw j, 2j + 1: in-partner) of the worker at position
+  // q on the days of that parity, written only by infectious or dead
+  // colleagues (0 otherwise) and cleared by its reader; all zero between
+  // launches
+  uint16_t* crow[2];
 };
 
 // Grid barrier between days: one arrival per block (release reduction on one
@@ -127,6 +134,30 @@ template <int MAXT> constexpr size_t run_dyn_smem() { return (size_t)(MAXT - 32)
 // loads of data written during the run: plain (coherent) global loads; the
 // grid barrier orders them after the writers' stores
 template <class T> __device__ __forceinline__ T LDM(const T* p) { return *p; }
+
+// A colleague row (16 slots of codes, two uint4, low half of each word
+// first = the visit order out, in per draw): the slot-ordered factor adds
+// when some slot holds an infectious colleague (the others add +0.0f: bitwise
+// add_src_group over the gathered codes), and `present` minus the dead
+// colleagues as edges.
+__device__ __forceinline__ void add_crow(float& acc, unsigned& edges, const float* __restrict__ factor, uint4 c0,
+                                         uint4 c1, unsigned present) {
+  const uint32_t w[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+  uint32_t any = 0, dead = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    any |= w[i];
+    dead += (w[i] >> 15) & 0x00010001u;
+  }
+  if (any & 0x00FF00FFu) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      acc += factor[w[i] & 0xFF];
+      acc += factor[(w[i] >> 16) & 0xFF];
+    }
+  }
+  edges += present - ((dead & 0xFFFFu) + (dead >> 16));
+}
 
 // The day's 8 colleague shifts r_j of workplace w (work_shift: four 16-bit
 // fields per hash), packed one byte each (r_j <= m - 1 <= 254).
@@ -227,6 +258,34 @@ __global__ void __launch_bounds__(MAXT, 1) k_fused_run(RunArgs R, epi_net net) {
   uint2 shp = works ? day_shifts(dk[0].wshift, w, m) : make_uint2(0, 0);
   int cnt_nx = valid ? random_count_cdf(cdf_s, net.random_slots, dk[0].rcount_next, b) : 0;
   uint32_t q_nx = works ? walk_inv((uint32_t)loc, work_keys(dk[0].wperm_next, w), rm) : 0u;
+  // colleague rows (the 736-thread variant): infectious and dead workers push
+  // their code of day t + 1 into the rows, by position, of their colleagues of
+  // t + 1, so a worker reads one 32-byte row instead of gathering 16 codes;
+  // the launch's first day is pushed before the loop
+  constexpr bool CROW = MAXT <= RUN_MAX_THREADS;
+  unsigned bar0 = 0;                       // grid barriers before the first day's
+  uint2 shq = make_uint2(0, 0);            // the shifts of the rows being pushed (t + 1)
+  // code `c` of the worker at position `q` into the rows of its colleagues
+  // (shifts `sh`, rows by position `crn`): out-partner of draw j of the
+  // worker at q - r_j, in-partner of the one at q + r_j (stores only)
+  auto push_rows = [&](uint16_t c, uint32_t q, uint2 sh, uint16_t* crn) {
+    const uint32_t um = (uint32_t)m;
+#pragma unroll
+    for (int j = 0; j < DR; ++j) {
+      if (j < draws) {
+        const uint32_t r = ((j < 4 ? sh.x : sh.y) >> (8 * (j & 3))) & 0xFFu;
+        crn[(size_t)(base + sub_mod(q, r, um)) * 16 + 2 * j] = c;
+        crn[(size_t)(base + add_mod(q, r, um)) * 16 + 2 * j + 1] = c;
+      }
+    }
+  };
+  if (CROW) {
+    // the rows of the launch's first day from today's codes
+    if (works && (cb & 0x80FFu) != 0u) push_rows(cb, p, shp, R.crow[R.first_step & 1]);
+    if (works && R.n_days > 1) shq = day_shifts(key_prefix(R.seed, R.first_step + 1, P_NET_WSHIFT), w, m);
+    grid_barrier(R.barrier, gridDim.x);
+    bar0 = 1;
+  }
   for (int d = 0; d < R.n_days; ++d) {
     const int t = R.first_step + d;
     const int par = t & 1;
@@ -267,6 +326,8 @@ __global__ void __launch_bounds__(MAXT, 1) k_fused_run(RunArgs R, epi_net net) {
       // rows of the day (level 1)
       const uint4* ri = (const uint4*)(W.rin + (size_t)b * RT_SLOTS);
       const uint4 in0 = LDM(ri), in1 = LDM(ri + 1);
+      const bool rows = CROW && works;
+      bool row_used = false;
       if (!code_dead(cb)) {
         const uint4* ro = (const uint4*)(out_s + threadIdx.x * RUN_OUT_STRIDE);
         const int nb = code_count(cb);
@@ -274,9 +335,9 @@ __global__ void __launch_bounds__(MAXT, 1) k_fused_run(RunArgs R, epi_net net) {
         const uint4 o0 = nbe > 0 ? ro[0] : make_uint4(self, self, self, self);
         // level 2: every load of the day's sources before any sum
         uint16_t hc[HH], wio[2 * DR];
-        if constexpr (MAXT <= RUN_MAX_THREADS) {
+        if constexpr (CROW) {
           load_household<HH>(hc, hin ? hcode_s[par] + hl0 : codes + start, hmask);
-          load_colleagues<DR>(wio, works, W.wcode, (uint32_t)base, p, (uint32_t)m, shp, draws);
+          (void)wio;
         } else {
           // the 64-register variant: per-member in-block tests and per-draw
           // modular indices spill less (measured 2.44 vs 2.69 ms at 120 k agents)
@@ -308,7 +369,16 @@ __global__ void __launch_bounds__(MAXT, 1) k_fused_run(RunArgs R, epi_net net) {
           if (i == off) continue;
           add_src(acc[0], edges, T.factor, LDM((hin ? hcode_s[par] + hl0 : codes + start) + i));
         }
-        add_src_group<2 * DR>(acc[1], edges, T.factor, wio);
+        if (CROW) {
+          if (works) {
+            const uint4* cr = (const uint4*)(R.crow[par] + (size_t)(base + p) * 16);
+            const uint4 cr0 = LDM(cr), cr1 = LDM(cr + 1);
+            row_used = (cr0.x | cr0.y | cr0.z | cr0.w | cr1.x | cr1.y | cr1.z | cr1.w) != 0u;
+            add_crow(acc[1], edges, T.factor, cr0, cr1, 2u * (unsigned)draws);
+          }
+        } else {
+          add_src_group<2 * DR>(acc[1], edges, T.factor, wio);
+        }
         if (n >= 2) {
           unsigned eo = 0;
           add_src_group<4>(acc[2], eo, T.factor, co0);
@@ -337,6 +407,17 @@ __global__ void __launch_bounds__(MAXT, 1) k_fused_run(RunArgs R, epi_net net) {
         rw[0] = make_uint4(0, 0, 0, 0);
         rw[1] = make_uint4(0, 0, 0, 0);
       }
+      // (so is the colleague row, also a dead agent's)
+      if (rows && code_dead(cb)) {         // (a dead agent's row is read only to be cleared)
+        const uint4* cr = (const uint4*)(R.crow[par] + (size_t)(base + p) * 16);
+        const uint4 cr0 = LDM(cr), cr1 = LDM(cr + 1);
+        row_used = (cr0.x | cr0.y | cr0.z | cr0.w | cr1.x | cr1.y | cr1.z | cr1.w) != 0u;
+      }
+      if (row_used) {
+        uint4* cw = (uint4*)(R.crow[par] + (size_t)(base + p) * 16);
+        cw[0] = make_uint4(0, 0, 0, 0);
+        cw[1] = make_uint4(0, 0, 0, 0);
+      }
     }
     unsigned ev = 0;
     if (valid) probe_lambda(R.probe, t, b, lam);
@@ -362,6 +443,8 @@ __global__ void __launch_bounds__(MAXT, 1) k_fused_run(RunArgs R, epi_net net) {
         Wn.pos_of[base + loc] = (uint8_t)q;
         for (int j = loc; j < draws; j += m)
           Wn.shift[(size_t)w * draws + j] = (uint8_t)work_shift(D.wshift_next, w, j, m);
+      } else if (CROW && (cn & 0x80FFu) != 0u) {
+        push_rows(cn, q, shq, R.crow[par ^ 1]);   // tomorrow's colleague rows
       }
     }
     // random: flatten the warp's (agent, slot < n) items, 32 at a time
@@ -405,16 +488,25 @@ __global__ void __launch_bounds__(MAXT, 1) k_fused_run(RunArgs R, epi_net net) {
       if (works) {
         if (d >= 1) {                      // computed by a service warp during day d - 1
           const uint4* e = R.wtab + (size_t)(d % 3) * 2 * net.n_workplaces + 2 * w;
-          const uint4 e0 = LDM(e), e1 = LDM(e + 1);
-          shp = make_uint2(e1.x, e1.y);
+          const uint4 e0 = LDM(e);
+          if (!CROW) {
+            const uint4 e1 = LDM(e + 1);
+            shp = make_uint2(e1.x, e1.y);
+          }
           q_nx = walk_inv((uint32_t)loc, work_keys_from(((uint64_t)e0.y << 32) | e0.x, e0.z), rm);
         } else {
-          shp = day_shifts(dk[(d + 1) & 1].wshift, w, m);
+          if (!CROW) shp = day_shifts(dk[(d + 1) & 1].wshift, w, m);
           q_nx = walk_inv((uint32_t)loc, work_keys(dk[(d + 1) & 1].wperm_next, w), rm);
+        }
+        if (CROW && d + 2 < R.n_days) {
+          // the pushes of day d + 1 (rows of t + 2): the shifts of t + 2 (a
+          // service warp's, written during day d)
+          const uint4 e1 = LDM(R.wtab + (size_t)((d + 1) % 3) * 2 * net.n_workplaces + 2 * w + 1);
+          shq = make_uint2(e1.x, e1.y);
         }
       }
       if (valid) cnt_nx = random_count_cdf(cdf_s, net.random_slots, dk[(d + 1) & 1].rcount_next, b);
-      if (threadIdx.x == 0) grid_wait(R.barrier, (unsigned)(d + 1) * gridDim.x);
+      if (threadIdx.x == 0) grid_wait(R.barrier, (unsigned)(d + 1 + bar0) * gridDim.x);
       __syncthreads();
     } else if (pend >= 0) {
       schedule_pending(R.P, R.st, D.K, t, R.tau_lut, b, pend, h);
