@@ -1546,6 +1546,20 @@ static bool persistent_ok(epi_ctx* c, int32_t mode, int32_t precision) {
   return ps >= 1;
 }
 
+// The persistent kernels' colleague rows, [2][member slots][16] codes, zeroed
+// once (every launch leaves them zero).
+static int run_crow(epi_ctx* c, cudaStream_t s, uint16_t* out[2]) {
+  const size_t len = (size_t)16 * (size_t)(c->net.n_member_slots > 0 ? c->net.n_member_slots : 1);
+  if (!c->run_crow) {
+    int rc = dalloc(&c->run_crow, 2 * len);
+    if (rc) return rc;
+    CK(cudaMemsetAsync(c->run_crow, 0, 2 * len * sizeof(uint16_t), s));
+  }
+  out[0] = c->run_crow;
+  out[1] = c->run_crow + len;
+  return 0;
+}
+
 static int launch_run(epi_ctx* c, const epi_state* st, int32_t first, int32_t n_days, uint64_t seed,
                       uint16_t* codes0, uint16_t* codes1, int64_t* records, cudaStream_t s) {
   if (!c->run_barrier) CK(dmalloc((void**)&c->run_barrier, sizeof(unsigned)));
@@ -1554,11 +1568,10 @@ static int launch_run(epi_ctx* c, const epi_state* st, int32_t first, int32_t n_
     if (rc) return rc;
   }
   const bool big = run_threads(c->n) > RUN_MAX_AGENTS;      // (the 1024-thread variant)
-  const size_t crow_len = (size_t)16 * (size_t)(c->net.n_member_slots > 0 ? c->net.n_member_slots : 1);
-  if (!big && !c->run_crow) {
-    int rc = dalloc(&c->run_crow, 2 * crow_len);
+  uint16_t* crow[2] = {nullptr, nullptr};
+  if (!big) {
+    int rc = run_crow(c, s, crow);
     if (rc) return rc;
-    CK(cudaMemsetAsync(c->run_crow, 0, 2 * crow_len * sizeof(uint16_t), s));
   }
   CK(cudaMemsetAsync(c->run_barrier, 0, sizeof(unsigned), s));
   RunArgs R{};
@@ -1579,8 +1592,8 @@ static int launch_run(epi_ctx* c, const epi_state* st, int32_t first, int32_t n_
   R.barrier = c->run_barrier;
   R.probe = c->probe;
   R.wtab = c->run_wtab;
-  R.crow[0] = c->run_crow;
-  R.crow[1] = c->run_crow ? c->run_crow + crow_len : nullptr;
+  R.crow[0] = crow[0];
+  R.crow[1] = crow[1];
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)sm_count());
   cfg.blockDim = dim3((unsigned)run_threads(c->n) + 32);     // + the service warp

@@ -158,6 +158,22 @@ __device__ __forceinline__ void add_crow(float& acc, unsigned& edges, const floa
   }
   edges += present - ((dead & 0xFFFFu) + (dead >> 16));
 }
+// Code `c` of the worker at position `q` of a workplace window (base, m) into
+// the colleague rows `crn` (by position) of the day the shifts `sh` belong
+// to: it is the out-partner of draw j of the worker at q - r_j and the
+// in-partner of the one at q + r_j (stores only).
+template <int DR>
+__device__ __forceinline__ void push_colleague_rows(uint16_t* crn, int base, uint32_t q, uint32_t m, uint2 sh,
+                                                    int draws, uint16_t c) {
+#pragma unroll
+  for (int j = 0; j < DR; ++j) {
+    if (j < draws) {
+      const uint32_t r = ((j < 4 ? sh.x : sh.y) >> (8 * (j & 3))) & 0xFFu;
+      crn[(size_t)(base + sub_mod(q, r, m)) * 16 + 2 * j] = c;
+      crn[(size_t)(base + add_mod(q, r, m)) * 16 + 2 * j + 1] = c;
+    }
+  }
+}
 
 // The day's 8 colleague shifts r_j of workplace w (work_shift: four 16-bit
 // fields per hash), packed one byte each (r_j <= m - 1 <= 254).
@@ -265,19 +281,8 @@ __global__ void __launch_bounds__(MAXT, 1) k_fused_run(RunArgs R, epi_net net) {
   constexpr bool CROW = MAXT <= RUN_MAX_THREADS;
   unsigned bar0 = 0;                       // grid barriers before the first day's
   uint2 shq = make_uint2(0, 0);            // the shifts of the rows being pushed (t + 1)
-  // code `c` of the worker at position `q` into the rows of its colleagues
-  // (shifts `sh`, rows by position `crn`): out-partner of draw j of the
-  // worker at q - r_j, in-partner of the one at q + r_j (stores only)
   auto push_rows = [&](uint16_t c, uint32_t q, uint2 sh, uint16_t* crn) {
-    const uint32_t um = (uint32_t)m;
-#pragma unroll
-    for (int j = 0; j < DR; ++j) {
-      if (j < draws) {
-        const uint32_t r = ((j < 4 ? sh.x : sh.y) >> (8 * (j & 3))) & 0xFFu;
-        crn[(size_t)(base + sub_mod(q, r, um)) * 16 + 2 * j] = c;
-        crn[(size_t)(base + add_mod(q, r, um)) * 16 + 2 * j + 1] = c;
-      }
-    }
+    push_colleague_rows<DR>(crn, base, q, (uint32_t)m, sh, draws, c);
   };
   if (CROW) {
     // the rows of the launch's first day from today's codes
