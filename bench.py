@@ -573,10 +573,13 @@ def persistent_profile(sim):
     has_iv = iv.testing_enabled or iv.quarantine_enabled or iv.den_enabled or iv.vaccination_enabled
     # per agent-day, state in registers and the out-rows (rout) in shared
     # memory: own code write 2 + in-row read 32 + in-row clear 32 + next-day
-    # scatter ~16 = 82 B; on intervention days + the agent's state reloaded
-    # (16) and the intervention columns read and written (testing, DEN,
-    # dropout, doses, buckets: ~44) = 142 B
-    b_day = (142 if has_iv else 82) * n
+    # scatter ~16 = 82 B; k_fused_run (up to 704 agents per SM) reads each
+    # worker's 32-byte colleague row instead of gathering 16 codes: + 32 B
+    # per worker.  On intervention days + the agent's state reloaded (16) and
+    # the intervention columns read and written (testing, DEN, dropout,
+    # doses, buckets: ~44) = 142 B
+    workers = len(sim.population.wp_members) if sim.n <= 148 * 704 else 0
+    b_day = 142 * n if has_iv else 82 * n + 32 * workers
     b_day0 = (16 + 2 + 32 + 64 + 32 + 16) * n + (32 + 10 + 1) * n      # + day-0 tables
     total = day0 + run
     name = "k_iv_run" if has_iv else "k_fused_run"
@@ -594,7 +597,7 @@ def persistent_profile(sim):
             "alg_bytes_per_sim": float(b_day * days + b_day0),
             "roofline": {"bound": "hbm", "kernel": name, "achieved": achieved, "unit": "GB/s",
                          "traffic": None, "days_per_launch": days,
-                         "bytes_model": f"{b_day // n} B per agent-day (DESIGN.md §4), x 179 days per launch"}}
+                         "bytes_model": f"{b_day / n:.1f} B per agent-day (DESIGN.md §4), x 179 days per launch"}}
 
 
 def end_to_end(sim, a, sim2=None):
