@@ -1202,7 +1202,7 @@ static int iv_fused_day(epi_ctx* c, const StepArgs& A, int32_t step, uint64_t se
   if (ev) CK(cudaEventRecord((cudaEvent_t)ev[1], s));
   const int fgrid = balanced_grid(c->n, 128, c->day_blocks_per_sm);
   DayTests tests{p.testing_enabled ? 1 : 0, listed ? c->den_list : nullptr, listed ? c->den_count : nullptr};
-  CK(launch_pdl_w(&c->hot, k_fused_step, dim3(fgrid), dim3(128), 0, s, A, c->net, nk, codes_cur,
+  CK(launch_pdl_w(&c->hot, k_fused_step<1>, dim3(fgrid), dim3(128), 0, s, A, c->net, nk, codes_cur,
                   c->host.rate_scale, codes_next, (const epi_net*)c->net_dev, rcount_next, 0,
                   (const WorkTables*)c->wt_dev[par][2], (const MsgTables*)c->msg_dev, (const NetTables*)nt_today,
                   NextTables{}, 1, tests));
@@ -1447,10 +1447,11 @@ static int sim_step_impl(epi_ctx* c, const epi_state* st, int32_t step, uint64_t
       nx.keys = nt_next;                  // (written by today's day tables; the day after's too)
       nx.keys_out = nullptr;
     }
-    CK(launch_pdl_w(&c->hot, k_fused_step, dim3(fgrid), dim3(128), 0, s, A, c->net, nk, codes_cur,
-                  c->host.rate_scale, codes_next, (const epi_net*)c->net_dev, rcount_next, iv ? 0 : 1, wt,
-                  (const MsgTables*)c->msg_dev, (const NetTables*)nt_today, nx, push_rand ? 1 : (sparse ? 2 : 0),
-                  DayTests{}));
+    const int push = push_rand ? 1 : (sparse ? 2 : 0);
+    CK(launch_pdl_w(&c->hot, push == 1 ? k_fused_step<1> : push == 2 ? k_fused_step<2> : k_fused_step<0>,
+                    dim3(fgrid), dim3(128), 0, s, A, c->net, nk, codes_cur,
+                    c->host.rate_scale, codes_next, (const epi_net*)c->net_dev, rcount_next, iv ? 0 : 1, wt,
+                    (const MsgTables*)c->msg_dev, (const NetTables*)nt_today, nx, push, DayTests{}));
     c->merged_ready = merged ? step + 1 : -1;
     c->sparse_ready = sparse && whole ? step + 1 : -1;
     c->sparse_clean = sparse ? step + 1 : -1;   // (the day's consumed rows were cleared)
