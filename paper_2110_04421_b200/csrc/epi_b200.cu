@@ -1073,7 +1073,7 @@ int epi_net_attach(epi_ctx* c, const epi_net* net) {
     rc = dalloc(&c->died_at, (size_t)c->n);
     if (!rc) rc = dalloc(&c->den_mark, (size_t)c->n + 4);
     if (!rc) rc = dalloc(&c->den_list, 2 * (size_t)c->n);     // [2][n]: k_iv_run uses both day parities
-    if (!rc) rc = dalloc(&c->den_count, 2);
+    if (!rc) rc = dalloc(&c->den_count, 3);      // k_iv_run: [3] by run day mod 3
     if (rc) return rc;
     k_fill_i32<<<grid_for(c->n, 256), 256>>>(c->died_at, c->n, INT32_MAX);
     CKL();
@@ -1855,7 +1855,7 @@ int epi_sim_run(epi_ctx* c, const epi_state* st, int32_t first_step, int32_t n_d
     }
     if (n_days - d0 >= 1) {
       // the per-day path's notifier list / histogram state is not carried over
-      if (c->den_count) CK(cudaMemsetAsync(c->den_count, 0, 2 * sizeof(int), S(stream)));
+      if (c->den_count) CK(cudaMemsetAsync(c->den_count, 0, 3 * sizeof(int), S(stream)));
       return launch_iv_run(c, st, first_step + d0, n_days - d0, seed, codes0, codes1,
                            records + (size_t)d0 * EPI_REC_LEN, vax_open, S(stream));
     }

@@ -40,7 +40,7 @@ struct IvRunArgs {
   unsigned* tile_hist;            // [2][blocks][NUM_BUCKETS] by run day parity
   int32_t* vax_open;
   int32_t* den_list;              // [2][den_stride] by day parity
-  int* den_count;                 // [2] by day parity
+  int* den_count;                 // [3] by run day mod 3 (day d's list length; zeroed at launch)
   int64_t den_stride;
   int32_t* died_at;
   int den_lookback;
@@ -266,6 +266,10 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
     }
     // ---- phase A ----------------------------------------------------------
     iv_mark(d, 0);
+    // tomorrow's list length starts at 0: its last readers (day d - 2's phase
+    // B) are done since barrier 1 of d - 1, and tomorrow's appends come after
+    // today's barrier 1
+    if (blockIdx.x == 0 && threadIdx.x == 0 && R.den_count) R.den_count[d3n] = 0;
     if (service) {
       if (d > 0 && !bar1)
         rec_flush_warp(racc[d3p], R.records + (size_t)(d - 1) * EPI_REC_LEN, t - 1, nwa, lane);
@@ -388,7 +392,7 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
         if (valid) {
           uint8_t fl = (ev & 8u) ? FL_SYMPTOMATIC : A.flags[b];
           tested = test_agent(A, b, h.stage, fl, R.den ? R.den_list + (size_t)par * R.den_stride : nullptr,
-                              R.den_count ? R.den_count + par : nullptr);
+                              R.den_count ? R.den_count + d3 : nullptr);
           A.flags[b] = fl;
         }
         if (R.den) {
@@ -446,9 +450,12 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
       if (service && d > 0)               // yesterday's record (incl. this morning's follow-ups)
         rec_flush_warp(racc[d3p], R.records + (size_t)(d - 1) * EPI_REC_LEN, t - 1, nwa, lane);
     }
-    if (phase_b) {
+    // the day's notifier count (complete at barrier 1, the same in every block):
+    // a day without notifiers makes no DEN marks and needs no end barrier
+    const int den_items = phase_b ? LDM(R.den_count + d3) : 0;
+    if (den_items > 0) {
       if (!service) {
-        const int64_t items = (int64_t)LDM(R.den_count + par) * n_back;
+        const int64_t items = (int64_t)den_items * n_back;
         const int32_t* list = R.den_list + (size_t)par * R.den_stride;
         // items spread over the blocks first (a few hundred items: one per
         // block and warp, so no block carries more than its share)
@@ -465,7 +472,6 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
     iv_mark(d, 3);
     // ---- phase C: the vaccination plan (every warp derives it from the
     // complete histogram) and the doses in id order -------------------------
-    if (blockIdx.x == 0 && threadIdx.x == 0 && R.den_count) R.den_count[par ^ 1] = 0;   // tomorrow's list
     // the vaccination plan (every warp derives it from the complete
     // histogram, barrier 1) and the doses in id order; the day's record rows.
     // Thread-local writes only: with DEN in the end barrier's window, else
@@ -548,7 +554,7 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
       for (int i = threadIdx.x; i < IV_HIST; i += blockDim.x) R.hist[(size_t)d3p * IV_HIST + i] = 0;
     // end of day: a grid barrier when DEN marks were made today (tomorrow's
     // follow-ups read them) or when there was no barrier 1 (tomorrow's codes)
-    const bool end_bar = d + 1 < R.n_days && (phase_b || !bar1);
+    const bool end_bar = d + 1 < R.n_days && (den_items > 0 || !bar1);
     if (end_bar) {
       // end of day, split: the plan, the doses and tomorrow's shifts between
       // arrive and wait
@@ -597,7 +603,7 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
     grid_barrier(R.barrier, ++bar * gridDim.x);
     if (!service)
       den_follow_up(R, b, valid, den_ok, den_pref, R.first_step + R.n_days, racc[(R.n_days - 1) % 3]);
-    if (blockIdx.x == 0 && threadIdx.x == 0 && R.den_count) R.den_count[0] = R.den_count[1] = 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && R.den_count) R.den_count[0] = R.den_count[1] = R.den_count[2] = 0;
   }
   __syncthreads();
   if (service)
