@@ -477,6 +477,16 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
     // Thread-local writes only: with DEN in the end barrier's window, else
     // right after barrier 1
     auto finish_day = [&]() {
+      // the record's stage and infection day: loaded first, so their latency
+      // overlaps the plan's (reloaded after a dose, whose immunity may be
+      // realised at once with a zero latency)
+      bool dosed = false;
+      int stage = 0;
+      int32_t inf = 0;
+      if (valid) {
+        stage = st.stage[b];
+        inf = st.infected_at[b];
+      }
       if (R.vax) {
         // the plan (k_vax_plan), derived by every warp from the complete
         // histogram (no block barrier): lane l holds buckets 2l, 2l+1; the cut
@@ -534,21 +544,18 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
           }
           if (lane < warp) part += hw_s[((size_t)par * (RUN_MAX_THREADS / 32) + lane) * IV_HW_ROW + cut];
           const long long rank = (long long)__reduce_add_sync(0xFFFFFFFFu, part) + __popc(ball & ((1u << lane) - 1u));
-          if (valid && bk != NO_BUCKET && ((long long)bk < cut || (in_cut && rank < rem))) give_dose(A, b, bk);
+          if (valid && bk != NO_BUCKET && ((long long)bk < cut || (in_cut && rank < rem))) { give_dose(A, b, bk); dosed = true; }
         } else if (valid && cut >= 0 && bk != NO_BUCKET) {
           give_dose(A, b, bk);                // cut == NUM_BUCKETS: every eligible agent
+          dosed = true;
         }
-      }
-      {
-        int stage = 0;
-        int32_t inf = 0;
-        if (valid) {
+        if (dosed) {
           stage = st.stage[b];
           inf = st.infected_at[b];
-          if (!R.den) A.flags[b] = 0;       // (with DEN: cleared by tomorrow's follow-up)
         }
-        rec_agent(rc, valid, stage, inf);
       }
+      if (valid && !R.den) A.flags[b] = 0;   // (with DEN: cleared by tomorrow's follow-up)
+      rec_agent(rc, valid, stage, inf);
     };
     if (R.vax && blockIdx.x == 0)           // the histogram of day d + 2 starts empty
       for (int i = threadIdx.x; i < IV_HIST; i += blockDim.x) R.hist[(size_t)d3p * IV_HIST + i] = 0;
