@@ -1401,22 +1401,70 @@ __global__ void k_died_update(const uint16_t* __restrict__ codes, int64_t n, int
 
 // One (notifier, past day) item of the DEN regeneration, one warp: the
 // notifier's in-edges of that day enumerated again (who was dead that day:
-// died_at) and their sources marked notified.  `rk_w` = the warp's
-// shared-memory slot-key row.
+// died_at) and their sources marked notified.  The in-edges of
+// for_each_in_edge_f, with each lane on ONE kind so that its load and walk
+// chain is one network's, not three in a row: lanes 0-7 household members,
+// 8-15 colleague draws, 16-31 random slots (the marks are an OR: the order of
+// the visits is free).  `rk_w` is unused (each random lane derives its slot's
+// keys).
 __device__ __forceinline__ void den_regen_item(const epi_net& net, const NetKeys& nk, int day, int64_t an,
                                                PermKeys* rk_w, const Radix* wrad,
                                                const int32_t* __restrict__ died_at, uint8_t* mark, int lane) {
-  if (lane < net.random_slots) rk_w[lane] = random_slot_keys(nk.rperm, lane);
-  __syncwarp();
+  (void)rk_w;
   auto code_of = [&](int64_t c) -> uint16_t {
     if (died_at[c] < day) return CODE_DEAD;
     return (uint16_t)(random_count(net, nk.rcount, c) << 8);
   };
-  for_each_in_edge_f(net, nk, rk_w, wrad, code_of, an, code_of(an), lane, 32,
-                     [&](int64_t c, int, uint16_t) {
-                       if (!(mark[c] & FL_NOTIFIED))
-                         atomicOr((unsigned*)(mark + (c & ~3ll)), (unsigned)FL_NOTIFIED << (8 * (c & 3)));
-                     });
+  auto mark_c = [&](int64_t c) {
+    if (!(mark[c] & FL_NOTIFIED)) atomicOr((unsigned*)(mark + (c & ~3ll)), (unsigned)FL_NOTIFIED << (8 * (c & 3)));
+  };
+  if (lane < 8) {
+    // household: contiguous range
+    const int off = net.hh_off[an];
+    const int sz = net.hh_size[an];
+    const int64_t start = an - off;
+    for (int i = lane; i < sz; i += 8) {
+      const int64_t c = start + i;
+      if (c != an && !code_dead(code_of(c))) mark_c(c);
+    }
+  } else if (lane < 16) {
+    const int li = lane - 8;
+    const int w = li < net.colleague_draws ? net.wp_id[an] : -1;
+    if (w >= 0) {
+      const int m = net.wp_size[w];
+      if (m >= 2) {
+        const Radix d = wrad[m];
+        const PermKeys K = work_keys(nk.wperm, w);
+        const int base = net.wp_base[w];
+        const uint32_t p = walk_inv(net.wp_local[an], K, d);
+        const uint64_t hw = fold(nk.wshift, (uint64_t)w);
+        for (int j = li; j < net.colleague_draws; j += 8) {
+          const uint64_t hq = fold(hw, (uint64_t)(j >> 2));
+          const uint32_t v = (uint32_t)((hq >> (16 * (j & 3))) & 0xFFFF);
+          const uint32_t r = 1u + ((v * (uint32_t)(m - 1)) >> 16);
+          const int32_t co = net.wp_members[base + walk_fwd(add_mod(p, r, (uint32_t)m), K, d)];
+          const int32_t ci = net.wp_members[base + walk_fwd(sub_mod(p, r, (uint32_t)m), K, d)];
+          if (!code_dead(code_of(co))) mark_c(co);
+          if (!code_dead(code_of(ci))) mark_c(ci);
+        }
+      }
+    }
+  } else {
+    const uint32_t n = (uint32_t)net.n_agents;
+    if (n >= 2) {
+      const Radix d = make_radix(n);
+      const int nb = code_count(code_of(an));
+      for (int j = lane - 16; j < net.random_slots; j += 16) {
+        const PermKeys K = random_slot_keys(nk.rperm, j);
+        const uint32_t ci = walk_inv((uint32_t)an, K, d);
+        if (j < nb) {
+          const uint32_t c = walk_fwd((uint32_t)an, K, d);
+          if (c != (uint32_t)an && !code_dead(code_of(c))) mark_c(c);
+        }
+        if (ci != (uint32_t)an && j < code_count(code_of(ci))) mark_c(ci);
+      }
+    }
+  }
   __syncwarp();
 }
 

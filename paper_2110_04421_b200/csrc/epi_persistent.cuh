@@ -503,16 +503,18 @@ __global__ void __launch_bounds__(MAXT, 1) k_fused_run(RunArgs R, epi_net net) {
           if (!CROW) shp = day_shifts(dk[(d + 1) & 1].wshift, w, m);
           q_nx = walk_inv((uint32_t)loc, work_keys(dk[(d + 1) & 1].wperm_next, w), rm);
         }
-        if (CROW && d + 2 < R.n_days) {
-          // the pushes of day d + 1 (rows of t + 2): the shifts of t + 2 (a
-          // service warp's, written during day d)
-          const uint4 e1 = LDM(R.wtab + (size_t)((d + 1) % 3) * 2 * net.n_workplaces + 2 * w + 1);
-          shq = make_uint2(e1.x, e1.y);
-        }
       }
       if (valid) cnt_nx = random_count_cdf(cdf_s, net.random_slots, dk[(d + 1) & 1].rcount_next, b);
       if (threadIdx.x == 0) grid_wait(R.barrier, (unsigned)(d + 1 + bar0) * gridDim.x);
       __syncthreads();
+      if (CROW && works && d + 2 < R.n_days) {
+        // the pushes of day d + 1 (rows of t + 2): the shifts of t + 2, written
+        // during day d by the service warp of whichever block owns workplace w,
+        // so read only after the barrier's wait (in the window, before it, a
+        // slow block's entry could still be missing: an intermittent race)
+        const uint4 e1 = LDM(R.wtab + (size_t)((d + 1) % 3) * 2 * net.n_workplaces + 2 * w + 1);
+        shq = make_uint2(e1.x, e1.y);
+      }
     } else if (pend >= 0) {
       schedule_pending(R.P, R.st, D.K, t, R.tau_lut, b, pend, h);
     }

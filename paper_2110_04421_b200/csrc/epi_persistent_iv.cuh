@@ -603,6 +603,7 @@ __global__ void __launch_bounds__(RUN_MAX_THREADS, 1) k_iv_run(IvRunArgs R, epi_
         }
       }
       if (d + 1 < R.n_days && valid) hp = load_hot(st, b);
+      iv_mark(d, 4);
     }
   }
   if (R.den) {

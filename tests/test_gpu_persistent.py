@@ -149,11 +149,16 @@ def test_reset_after_a_partial_run_equals_a_fresh_run(iv_on):
     mk = lambda: ConfigSimulation(synthesize(spec, 5), default_disease(), default_progression(), iv, 9,
                                   mode="fused", horizon=90)
     a, b = mk(), mk()
-    a.run(37)
-    a.reset()
-    a.run()
     b.run()
-    _same(a, b)
+    # repeated: a grid-barrier ordering race (k_fused_run read tomorrow's
+    # colleague shifts between a barrier's arrive and wait) failed this
+    # comparison in about one run in three
+    for _ in range(3):
+        a.run(37)
+        a.reset()
+        a.run()
+        _same(a, b)
+        a.reset()
 
 
 def test_persistent_runs_are_deterministic_under_repetition():

@@ -47,8 +47,15 @@ print(f"days with an end barrier {int(eb.sum())}")
 print("end window per block         ", st(rel[eb][:, :, 4] - rel[eb][:, :, 3]))
 print("end window end (latest)      ", st(rel[eb][:, :, 4].max(axis=1)))
 print("after end barrier (first)    ", st(rel[eb][:, :, 5].min(axis=1)))
+ne = ~eb & np.all(tr[:, :, 4] > 0, axis=1)                                 # days without one
+print(f"days without an end barrier {int(ne.sum())}")
+if ne.any():
+    print("finish per block (no end bar)", st(rel[ne][:, :, 4] - rel[ne][:, :, 3]))
 nxt = np.diff(tr[:, 0, 0])
 print("day length (block 0 starts)  ", st(nxt[nxt < 1e3]))
+ok = nxt < 1e3
+print("  with an end barrier        ", st(nxt[ok & eb[:-1]]))
+print("  without                    ", st(nxt[ok & ne[:-1]]))
 for q in (10, 30, 60, 90, 120, 170):
     i = min(q, len(days) - 1)
     r = rel[i]
