@@ -652,7 +652,7 @@ def end_to_end(sim, a, sim2=None):
             "edges_per_step": edges, "copies": mode}
 
 
-def measure_partition(steps, warmup, rank, local_rank, world, dist):
+def measure_partition(steps, warmup, rank, local_rank, world, dist, e2e_args=None):
     """Config 3 (10M agents, config-1 networks, 180 days): one simulation
     partitioned by agent range over the `world` ranks (strong scaling), the
     per-day code all-gather over native NCCL inside the native day loop, the
@@ -699,7 +699,13 @@ def measure_partition(steps, warmup, rank, local_rank, world, dist):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
     edges = float(rec[:, N.REC["edges"]].sum().item()) * steps
-    return {"workload": "config3 (BASELINE.json configs[3]): 10M agents, config-1 networks, 180 days, "
+    e2e = None
+    if e2e_args is not None and world == 1:
+        # end to end through the public API: the 10M-agent initial state from
+        # pinned host memory in, the time series out, every simulation
+        e2e = end_to_end(sim, e2e_args)
+        e2e.pop("edges_per_step", None)
+    return {"e2e": e2e, "workload": "config3 (BASELINE.json configs[3]): 10M agents, config-1 networks, 180 days, "
                         "fused mode, no interventions",
             "value": edges / (ms / 1e3), "unit": "agent-interactions/s", "n_gpus": world,
             "steps": steps, "warmup": warmup, "ms_per_step": ms / steps, "scaling": "strong",
@@ -729,7 +735,7 @@ def run_config3(a):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl")
-    m = measure_partition(a.steps, a.warmup, rank, local_rank, world, dist)
+    m = measure_partition(a.steps, a.warmup, rank, local_rank, world, dist, e2e_args=a)
     if rank == 0:
         clocks = m.pop("clocks")
         print(json.dumps({
@@ -738,7 +744,7 @@ def run_config3(a):
             "ms_per_step": m["ms_per_step"], "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": m["workload"], "parallelism": m["parallelism"], "l2": m["l2"]},
-            "wall_s_per_sim": m["wall_s_per_sim"], "clocks": clocks}), flush=True)
+            "wall_s_per_sim": m["wall_s_per_sim"], "clocks": clocks, "e2e": m["e2e"]}), flush=True)
 
 
 def run_config4(a):
