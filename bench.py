@@ -817,6 +817,40 @@ def run_config4(a):
         allc = [torch.empty_like(new_inf) for _ in range(world)]
         dist.all_gather(allc, new_inf)
         new_inf = torch.cat(allc)
+    # end to end through the public API: every replica's initial state from
+    # pinned host memory in, its time series out, inside the timed region
+    pinned = [s_.initial.host_arena(s_.initial_host_columns()) for s_ in sims]
+    outs = [torch.empty((HORIZON, 19), dtype=torch.int64).pin_memory() for _ in sims]
+
+    def sweep_e2e():
+        for i, s_ in enumerate(sims):
+            with torch.cuda.stream(streams[i % len(streams)]):
+                s_.initial.arena.copy_(pinned[i], non_blocking=True)
+                s_._graph.replay()
+                outs[i].copy_(s_.rec[:, :19], non_blocking=True)
+        for st_ in streams:
+            torch.cuda.current_stream().wait_stream(st_)
+    e_steps = max(1, min(a.steps, 3))
+    sweep_e2e()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    st.record()
+    for _ in range(e_steps):
+        sweep_e2e()
+    en.record()
+    torch.cuda.synchronize()
+    e_ms = st.elapsed_time(en)
+    e_edges = float(torch.stack([s_.rec for s_ in sims])[:, :, N.REC["edges"]].sum().item()) * e_steps
+    if dist:
+        tt = torch.tensor([e_ms, e_edges], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt[:1], op=dist.ReduceOp.MAX)
+        dist.all_reduce(tt[1:])
+        e_ms, e_edges = float(tt[0]), float(tt[1])
+    e2e = {"value": e_edges / (e_ms / 1e3), "unit": "agent-interactions/s", "ms_per_step": e_ms / e_steps,
+           "steps": e_steps, "h2d_bytes_per_step": int(sum(int(x.numel()) for x in pinned)),
+           "d2h_bytes_per_step": int(sum(o.numel() * o.element_size() for o in outs)),
+           "copies": "serial per replica: its initial state in, its 180 days, its series out"}
     reps = a.replicas * world
     # replication quartiles of the daily infection curve on the device
     # (row f3 output: epi_quartiles, bitwise the reference's summarize)
@@ -841,7 +875,7 @@ def run_config4(a):
             "daily_new_infections_std": [round(float(x), 2) for x in std],
             "daily_new_infections_quartiles": (None if quart is None else
                                                [[round(float(v), 2) for v in row] for row in quart]),
-            "clocks": clocks}), flush=True)
+            "clocks": clocks, "e2e": e2e}), flush=True)
 
 
 REFNET_DESC = ("refnet: the reference's own benchmark scenario (epivec bench --agents 100000 --steps "
