@@ -452,7 +452,7 @@ def run_ours(a):
     if not a.no_cpu_baseline and world == 1:
         line["cpu_baseline"] = cpu_baseline_single(a.workload, a.cpu_seconds)
     if part is not None:
-        line["partition_config3"] = part
+        line["partition_config3"] = {k: v for k, v in part.items() if v is not None or k != "e2e"}
     if not a.no_message_pass and world == 1:
         # north-star part (a) alone at BASELINE config-3 scale (10M agents):
         # the HBM-bound kernel of the decomposition, streamed 16-bit messages
